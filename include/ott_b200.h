@@ -1,0 +1,120 @@
+/*
+ * ott_b200.h — C ABI of the B200-native OTT quantized-KV decode path.
+ *
+ * This is the drop-in boundary for the reference's cache/attention API
+ * (/root/reference/pkg/src/kvtrace). The reference is a Python package whose
+ * only "FFI" is its Python call surface; the Python host layer
+ * (paper_2505_10938_b200/) binds these symbols with ctypes (see
+ * INTEGRATION.md) and keeps the reference's names and error behaviour.
+ *
+ *   ott_ring_write   <- TieredCache.append            cache.py:124-139 (row copy part)
+ *   ott_flush        <- TieredCache.quantize_oldest_group  cache.py:141-186
+ *                       (score_tokens outlier.py:45-49, OutlierPool.update
+ *                       outlier.py:84-117, substitute_means outlier.py:120-142,
+ *                       quantize_keys_channelwise / quantize_values_tokenwise
+ *                       quant.py:201-234, pack_codes quant.py:241-256)
+ *   ott_attend       <- attend_mixed                   attention.py:79-92
+ *                       (reconstructed_kv attention.py:62-76,
+ *                       attend_full_precision attention.py:35-59)
+ *   ott_logits       <- AttentionResult.scores         attention.py:26-32 (debug)
+ *
+ * Conventions: all buffer pointers are DEVICE memory owned by the caller (the
+ * host layer allocates them; this library never allocates or frees). Every
+ * call is asynchronous on the given stream and returns an ott_status. The
+ * cache holds n_units = batch * n_kv_heads independent (layer, head) caches of
+ * the reference, all at the same token count (lock-step decode).
+ */
+#ifndef OTT_B200_H
+#define OTT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  OTT_OK = 0,
+  OTT_ERR_CONTRACT = 1, /* maps to kvtrace.ContractViolation (errors.py:4-5) */
+  OTT_ERR_UNSUPPORTED = 2,
+  OTT_ERR_CUDA = 3,
+} ott_status;
+
+/* Device-side state of one layer's batched tiered cache. Sizes in elements.
+ * Block record (one per (unit, group)), byte layout, all little-endian:
+ *   [0, G*d*bits/8)                 K codes, reference pack_codes order
+ *   [+G*d*bits/8)                   V codes
+ *   float32 k_step[d], k_xmin[d]    per-channel K params  (QuantParams)
+ *   float32 v_step[G], v_xmin[G]    per-token V params
+ * Per-token bitmasks hold one bit per absolute position (32 per word). */
+typedef struct {
+  int32_t n_units;      /* batch * n_kv_heads */
+  int32_t head_dim;     /* d: 64 or 128 */
+  int32_t group_size;   /* G: multiple of 32, <= 128 */
+  int32_t residual;     /* R >= 0 */
+  int32_t capacity;     /* N: pool capacity for this layer (EngineConfig.outlier_capacity) */
+  int32_t aux_capacity; /* A */
+  int32_t bits;         /* 2 */
+  int32_t max_groups;   /* block records allocated per unit */
+  uint8_t* blocks;      /* [n_units][max_groups][record_bytes] */
+  uint16_t* pend_k;     /* fp16 [n_units][G+R][d], slot = position % (G+R) */
+  uint16_t* pend_v;
+  uint32_t* pool_mask;  /* [n_units][max_groups*G/32]: 1 = position currently in pool.entries */
+  uint32_t* subst_mask; /* [n_units][max_groups*G/32]: substituted_positions */
+  int32_t* pool_pos;    /* [n_units][N] slot-stable entries, -1 = empty; reference order =
+                           ascending (score, position), outlier.py:52-54 */
+  double* pool_score;   /* [n_units][N] */
+  uint16_t* pool_k;     /* fp16 [n_units][N][d] */
+  uint16_t* pool_v;
+  int32_t* aux_pos;     /* [n_units][A] in reference order */
+  double* aux_score;    /* [n_units][A] */
+  uint16_t* aux_k;      /* fp16 [n_units][A][d] */
+  uint16_t* aux_v;
+  int32_t* pool_meta;   /* [n_units][4] = {n_entries, n_aux, frozen, 0} */
+  double* params64;     /* optional [n_units][max_groups][2*(d+G)] exact float64 params
+                           (k_xmin[d], k_step[d], v_xmin[G], v_step[G]); NULL = off */
+} ott_cache_t;
+
+/* Bytes of one block record for the given shape. */
+size_t ott_record_bytes(int32_t head_dim, int32_t group_size, int32_t bits);
+
+/* Copy rows into the pending ring. Row r (0 <= r < n_rows) of unit u is read
+ * from k + u*in_unit_stride + (first_pos - in_first_pos + r)*d and lands at
+ * ring slot (first_pos + r) % (G+R). Rows are fp16. */
+int ott_ring_write(const ott_cache_t* c, const uint16_t* k, const uint16_t* v, int64_t in_unit_stride,
+                   int64_t in_first_pos, int64_t first_pos, int64_t n_rows, void* stream);
+
+/* Quantize n_groups consecutive groups per unit, starting at absolute position
+ * quantized_tokens (sequentially: each group's pool competition sees the pool
+ * left by the previous one, cache.py:141-186). A row at position p is read
+ * from the pending ring when p < ring_end, else from
+ * in_k + u*in_unit_stride + (p - in_first_pos)*d (bulk prefill). */
+int ott_flush(const ott_cache_t* c, int64_t quantized_tokens, int32_t n_groups, int64_t ring_end,
+              const uint16_t* in_k, const uint16_t* in_v, int64_t in_unit_stride, int64_t in_first_pos,
+              void* stream);
+
+/* Mixed-tier decode attention (attend_mixed) for n_rep query heads per unit.
+ * q, out: fp16 [n_units][n_rep][d] (= [B][H_q][d] with H_q = H_kv*n_rep).
+ * The sequence axis is split n_splits ways (split-K flash decoding) and the
+ * partials merged in-kernel; ott_pick_splits chooses a count that fills the
+ * GPU, ott_attend_workspace_floats sizes the float32 workspace for it. */
+int ott_pick_splits(const ott_cache_t* c, int32_t n_rep, int64_t total_tokens);
+size_t ott_attend_workspace_floats(const ott_cache_t* c, int32_t n_rep, int32_t n_splits);
+int ott_attend(const ott_cache_t* c, const uint16_t* q, uint16_t* out, int32_t n_rep, int64_t quantized_tokens,
+               int64_t total_tokens, float* workspace, int32_t n_splits, void* stream);
+
+/* Debug: pre-softmax logits (AttentionResult.scores, attention.py:55) for all
+ * total_tokens positions, float32 [n_units][n_rep][total_tokens]. */
+int ott_logits(const ott_cache_t* c, const uint16_t* q, float* logits, int32_t n_rep, int64_t quantized_tokens,
+               int64_t total_tokens, void* stream);
+
+/* Number of SMs of the current device (0 if unknown) and library version. */
+int ott_num_sms(void);
+const char* ott_version(void);
+const char* ott_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

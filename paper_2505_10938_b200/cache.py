@@ -1,0 +1,408 @@
+"""Batched GPU tiered KV cache — the reference's TieredCache (kvtrace/cache.py:90-203)
+for all (batch, kv-head) units of one layer at once, resident in HBM.
+
+State lives in torch CUDA tensors (allocation/streams only); every byte of it is
+produced and consumed by the sm_100a kernels in ``csrc/`` via the C ABI in
+``include/ott_b200.h``. There is no CPU fallback: without a CUDA device and
+``libott_b200.so`` every method raises.
+
+HBM layout per unit (u = b * H_kv + h), see DESIGN.md §3:
+  blocks     uint8 [U, max_groups, record]  K codes | V codes | K step,x_min f32[d] | V step,x_min f32[G]
+  pend_k/v   fp16  [U, G+R, d]              pending ring, slot = position % (G+R)
+  pool_*     slot-stable pool.entries (pos, score f64, K/V rows fp16), aux ledger, meta
+  pool_mask  uint32 [U, max_tokens/32]      1 bit per position currently in pool.entries
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _native
+from .config import EngineConfig, MemoryBreakdown
+from .errors import ContractViolation
+from .views import (FP16_BITS, AttentionResult, GroupAxis, OutlierEntry, OutlierPoolView, QuantizedBlock, QuantParams,
+                    require)
+
+
+def _stream_handle() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+class OTTCache:
+    """One layer's OTT cache for ``batch * n_kv_heads`` independent units.
+
+    All units advance in lock step (one token per unit per ``append``), so the
+    flush trigger ``pending - R >= G`` (cache.py:138) is decided on the host
+    from the shared token count with no device synchronisation.
+
+    Args:
+        config: EngineConfig (same fields as the reference). bits must be 2;
+            head_dim 64 or 128; group_size a multiple of 32 up to 128.
+        batch, n_kv_heads: unit grid.
+        max_tokens: capacity of the quantized store per unit.
+        layer: layer index; pool capacity is ``config.outlier_capacity(layer)``.
+        keep_f64_params: also store the exact float64 (x_min, step) of every
+            parameter line (parity/debug; 2.5x the param bytes).
+        validate: check inputs for NaN/Inf on every call (costs a device sync;
+            the reference raises ContractViolation, cache.py:131-132).
+    """
+
+    def __init__(self, config: EngineConfig, batch: int, n_kv_heads: int, max_tokens: int, layer: int = 0,
+                 device=None, keep_f64_params: bool = False, validate: bool = False):
+        if not torch.cuda.is_available():
+            raise _native.NativeError("OTTCache needs a CUDA device (B200); there is no CPU path")
+        require(config.bits == 2, "the B200 path implements bits=2 only")
+        require(config.head_dim in (64, 128), "head_dim must be 64 or 128")
+        require(config.group_size % 32 == 0 and 32 <= config.group_size <= 128,
+                "group_size must be a multiple of 32 in [32, 128]")
+        require(batch >= 1 and n_kv_heads >= 1 and max_tokens >= 1, "batch, n_kv_heads, max_tokens must be >= 1")
+        self.config = config
+        self.layer = layer
+        self.batch, self.n_kv_heads = batch, n_kv_heads
+        self.n_units = batch * n_kv_heads
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.validate = validate
+        d, G, R = config.head_dim, config.group_size, config.residual
+        self.N = config.outlier_capacity(layer)
+        self.A = config.aux_capacity
+        require(self.N <= 128, "outlier_num must be <= 128 on the GPU path")
+        require(self.A <= 1024, "aux_capacity must be <= 1024 on the GPU path")
+        self.max_groups = (max_tokens + G - 1) // G
+        self.max_tokens = max_tokens
+        L = _native.lib()
+        self.record_bytes = int(L.ott_record_bytes(d, G, 2))
+        U, dev = self.n_units, self.device
+        kw = dict(device=dev)
+        self.blocks = torch.zeros((U, self.max_groups, self.record_bytes), dtype=torch.uint8, **kw)
+        self.pend_k = torch.zeros((U, G + R, d), dtype=torch.float16, **kw)
+        self.pend_v = torch.zeros((U, G + R, d), dtype=torch.float16, **kw)
+        words = self.max_groups * G // 32
+        self.pool_mask = torch.zeros((U, words), dtype=torch.int32, **kw)
+        self.subst_mask = torch.zeros((U, words), dtype=torch.int32, **kw)
+        n, a = max(self.N, 1), max(self.A, 1)
+        self.pool_pos = torch.full((U, n), -1, dtype=torch.int32, **kw)
+        self.pool_score = torch.zeros((U, n), dtype=torch.float64, **kw)
+        self.pool_k = torch.zeros((U, n, d), dtype=torch.float16, **kw)
+        self.pool_v = torch.zeros((U, n, d), dtype=torch.float16, **kw)
+        self.aux_pos = torch.full((U, a), -1, dtype=torch.int32, **kw)
+        self.aux_score = torch.zeros((U, a), dtype=torch.float64, **kw)
+        self.aux_k = torch.zeros((U, a, d), dtype=torch.float16, **kw)
+        self.aux_v = torch.zeros((U, a, d), dtype=torch.float16, **kw)
+        self.pool_meta = torch.zeros((U, 4), dtype=torch.int32, **kw)
+        if self.A == 0:
+            self.pool_meta[:, 2] = 1  # outlier.py:77-78: aux_capacity 0 freezes at construction
+        self.params64 = (torch.zeros((U, self.max_groups, 2 * (d + G)), dtype=torch.float64, **kw)
+                         if keep_f64_params else None)
+        self._c = _native.OttCacheT(
+            n_units=U, head_dim=d, group_size=G, residual=R, capacity=self.N, aux_capacity=self.A, bits=2,
+            max_groups=self.max_groups, blocks=_ptr(self.blocks), pend_k=_ptr(self.pend_k), pend_v=_ptr(self.pend_v),
+            pool_mask=_ptr(self.pool_mask), subst_mask=_ptr(self.subst_mask), pool_pos=_ptr(self.pool_pos),
+            pool_score=_ptr(self.pool_score), pool_k=_ptr(self.pool_k), pool_v=_ptr(self.pool_v),
+            aux_pos=_ptr(self.aux_pos), aux_score=_ptr(self.aux_score), aux_k=_ptr(self.aux_k),
+            aux_v=_ptr(self.aux_v), pool_meta=_ptr(self.pool_meta), params64=_ptr(self.params64))
+        self._cref = ctypes.byref(self._c)
+        self.total_tokens = 0
+        self.quantized_tokens = 0
+        self._ws = None
+        self._ws_key = None
+
+    # ------------------------------------------------------------------ helpers
+    @property
+    def pending_rows(self) -> int:
+        return self.total_tokens - self.quantized_tokens
+
+    def _check_rows(self, x: torch.Tensor, name: str, T: int | None = None) -> torch.Tensor:
+        d = self.config.head_dim
+        shape = (self.batch, self.n_kv_heads, d) if T is None else (self.batch, self.n_kv_heads, T, d)
+        if tuple(x.shape) != shape:
+            if T is None and tuple(x.shape) == (self.n_units, d):
+                pass
+            else:
+                raise ContractViolation(f"{name} must have shape {shape}, got {tuple(x.shape)}")
+        require(x.dtype == torch.float16, f"{name} must be float16")
+        require(x.device == self.device, f"{name} must live on {self.device}")
+        x = x.contiguous()
+        if self.validate and not bool(torch.isfinite(x).all()):
+            raise ContractViolation("rows contain NaN or Inf")  # cache.py:131-132
+        return x
+
+    # --------------------------------------------------------------- write path
+    def append(self, k: torch.Tensor, v: torch.Tensor) -> None:
+        """cache.py:124-139: add one token per unit; quantize a group when due."""
+        k = self._check_rows(k, "k")
+        v = self._check_rows(v, "v")
+        _native.check(_native.lib().ott_ring_write(self._cref, k.data_ptr(), v.data_ptr(), self.config.head_dim,
+                                                   self.total_tokens, self.total_tokens, 1, _stream_handle()))
+        self.total_tokens += 1
+        if self.pending_rows - self.config.residual >= self.config.group_size:  # cache.py:138
+            self.quantize_oldest_group()
+
+    def quantize_oldest_group(self) -> None:
+        """cache.py:141-186 for every unit (one launch of the flush kernel)."""
+        G = self.config.group_size
+        if self.pending_rows < G:
+            raise ContractViolation(f"need {G} pending rows to quantize, have {self.pending_rows}")
+        self._flush(1, ring_end=self.total_tokens)
+
+    def _flush(self, n_groups: int, ring_end: int, in_k=None, in_v=None, in_stride: int = 0,
+               in_first: int = 0) -> None:
+        require(self.quantized_tokens // self.config.group_size + n_groups <= self.max_groups,
+                "cache capacity (max_tokens) exceeded")
+        _native.check(_native.lib().ott_flush(self._cref, self.quantized_tokens, n_groups, ring_end, _ptr(in_k),
+                                              _ptr(in_v), in_stride, in_first, _stream_handle()))
+        self.quantized_tokens += n_groups * self.config.group_size
+
+    def update(self, k: torch.Tensor, v: torch.Tensor) -> None:
+        """Bulk insert of T tokens per unit, numerically identical to T sequential
+        ``append`` calls: full groups are flushed straight from the
+        input (one launch; the pool competition runs group by group inside it),
+        the newest rows land in the pending ring."""
+        require(k.dim() == 4, "k must be [batch, n_kv_heads, T, d]")
+        T = k.shape[2]
+        k = self._check_rows(k, "k", T)
+        v = self._check_rows(v, "v", T)
+        if T == 0:
+            return
+        G, R, d = self.config.group_size, self.config.residual, self.config.head_dim
+        t0 = self.total_tokens
+        n_groups = max(0, (self.pending_rows + T - R) // G)
+        if n_groups:
+            self._flush(n_groups, ring_end=t0, in_k=k, in_v=v, in_stride=T * d, in_first=t0)
+        self.total_tokens = t0 + T
+        first = max(self.quantized_tokens, t0)
+        n_rows = self.total_tokens - first
+        if n_rows:
+            _native.check(_native.lib().ott_ring_write(self._cref, k.data_ptr(), v.data_ptr(), T * d, t0, first,
+                                                       n_rows, _stream_handle()))
+
+    # ---------------------------------------------------------------- read path
+    def splits(self, n_rep: int) -> int:
+        return int(_native.lib().ott_pick_splits(self._cref, n_rep, self.total_tokens))
+
+    def workspace(self, n_rep: int, n_splits: int) -> torch.Tensor:
+        n = int(_native.lib().ott_attend_workspace_floats(self._cref, n_rep, n_splits))
+        if self._ws is None or self._ws.numel() < n:
+            self._ws = torch.empty(n, dtype=torch.float32, device=self.device)
+        return self._ws
+
+    def attend(self, q: torch.Tensor, out: torch.Tensor | None = None, n_splits: int | None = None) -> torch.Tensor:
+        """attend_mixed (attention.py:79-92) for every query head.
+
+        q: fp16 [batch, H_q, d] with H_q = n_kv_heads * n_rep; query head h reads
+        kv head h // n_rep. Returns fp16 [batch, H_q, d]."""
+        require(q.dim() == 3 and q.shape[0] == self.batch and q.shape[2] == self.config.head_dim,
+                f"query must have shape (batch, H_q, {self.config.head_dim})")
+        require(q.shape[1] % self.n_kv_heads == 0, "H_q must be a multiple of n_kv_heads")
+        require(q.dtype == torch.float16 and q.device == self.device, "query must be float16 on the cache device")
+        if self.total_tokens == 0:
+            raise ContractViolation("cannot attend over an empty cache")  # attention.py:89-90
+        n_rep = q.shape[1] // self.n_kv_heads
+        q = q.contiguous()
+        if out is None:
+            out = torch.empty_like(q)
+        s = n_splits or self.splits(n_rep)
+        ws = self.workspace(n_rep, s)
+        _native.check(_native.lib().ott_attend(self._cref, q.data_ptr(), out.data_ptr(), n_rep, self.quantized_tokens,
+                                               self.total_tokens, ws.data_ptr(), s, _stream_handle()))
+        return out
+
+    def logits(self, q: torch.Tensor) -> torch.Tensor:
+        """Debug: AttentionResult.scores for every unit/head, float32 [batch, H_q, T]."""
+        n_rep = q.shape[1] // self.n_kv_heads
+        out = torch.empty((self.batch, q.shape[1], self.total_tokens), dtype=torch.float32, device=self.device)
+        _native.check(_native.lib().ott_logits(self._cref, q.contiguous().data_ptr(), out.data_ptr(), n_rep,
+                                               self.quantized_tokens, self.total_tokens, _stream_handle()))
+        return out
+
+    # ------------------------------------------------------------- accounting
+    def memory_usage(self, b: int = 0, h: int = 0) -> MemoryBreakdown:
+        """cache.py:188-203 for unit (b, h), identical bit counts."""
+        G, d = self.config.group_size, self.config.head_dim
+        nb = self.quantized_tokens // G
+        meta = self.pool_meta[b * self.n_kv_heads + h].tolist() if self.N > 0 else [0, 0, 0, 0]
+        return MemoryBreakdown(
+            quantized_bits=2 * nb * G * d * self.config.bits,
+            param_bits=nb * (d + G) * 2 * FP16_BITS,
+            pending_bits=self.pending_rows * d * FP16_BITS * 2,
+            pool_bits=(meta[0] + meta[1]) * d * FP16_BITS * 2,
+        )
+
+    def hbm_bytes(self) -> int:
+        """Bytes of device state actually allocated for this layer."""
+        ts = [self.blocks, self.pend_k, self.pend_v, self.pool_mask, self.subst_mask, self.pool_pos, self.pool_score,
+              self.pool_k, self.pool_v, self.aux_pos, self.aux_score, self.aux_k, self.aux_v, self.pool_meta]
+        if self.params64 is not None:
+            ts.append(self.params64)
+        return sum(t.numel() * t.element_size() for t in ts)
+
+    # --------------------------------------------------------------- snapshots
+    def unit(self, b: int, h: int) -> "UnitView":
+        """Reference-shaped snapshot of one (batch, kv-head) unit."""
+        return UnitView(self, b * self.n_kv_heads + h)
+
+
+class UnitView:
+    """Read-only host snapshot of one unit with the reference TieredCache's
+    attribute names (quantized_k/v, pool, substituted_positions, pending_k/v)."""
+
+    def __init__(self, cache: OTTCache, u: int):
+        torch.cuda.synchronize(cache.device)
+        cfg = cache.config
+        d, G = cfg.head_dim, cfg.group_size
+        self.config = cfg
+        self.total_tokens = cache.total_tokens
+        self.quantized_tokens = cache.quantized_tokens
+        nb = cache.quantized_tokens // G
+        rec = cache.blocks[u, :nb].cpu().numpy()
+        code_b = G * d // 4
+        kst = rec[:, 2 * code_b: 2 * code_b + 4 * d].copy().view(np.float32)
+        kmn = rec[:, 2 * code_b + 4 * d: 2 * code_b + 8 * d].copy().view(np.float32)
+        vst = rec[:, 2 * code_b + 8 * d: 2 * code_b + 8 * d + 4 * G].copy().view(np.float32)
+        vmn = rec[:, 2 * code_b + 8 * d + 4 * G:].copy().view(np.float32)
+        self.k_step32, self.k_xmin32, self.v_step32, self.v_xmin32 = kst, kmn, vst, vmn
+        if cache.params64 is not None:
+            p = cache.params64[u, :nb].cpu().numpy()
+            kmn64, kst64, vmn64, vst64 = p[:, :d], p[:, d:2 * d], p[:, 2 * d:2 * d + G], p[:, 2 * d + G:]
+        else:
+            kmn64, kst64, vmn64, vst64 = kmn, kst, vmn, vst
+        self.quantized_k, self.quantized_v = [], []
+        for i in range(nb):
+            self.quantized_k.append(QuantizedBlock(rec[i, :code_b].tobytes(), GroupAxis.PER_CHANNEL,
+                                                   [QuantParams(float(kmn64[i, c]), float(kst64[i, c]), 2)
+                                                    for c in range(d)], G, d, 2))
+            self.quantized_v.append(QuantizedBlock(rec[i, code_b:2 * code_b].tobytes(), GroupAxis.PER_TOKEN,
+                                                   [QuantParams(float(vmn64[i, t]), float(vst64[i, t]), 2)
+                                                    for t in range(G)], G, d, 2))
+        cap = G + cfg.residual
+        pos = np.arange(cache.quantized_tokens, cache.total_tokens)
+        pk = cache.pend_k[u].float().cpu().numpy()
+        pv = cache.pend_v[u].float().cpu().numpy()
+        self.pending_k = pk[pos % cap] if len(pos) else np.zeros((0, d), np.float32)
+        self.pending_v = pv[pos % cap] if len(pos) else np.zeros((0, d), np.float32)
+        pool = OutlierPoolView(capacity=cache.N, aux_capacity=cache.A)
+        if cache.N > 0:
+            meta = cache.pool_meta[u].tolist()
+            ppos = cache.pool_pos[u].cpu().numpy()
+            psc = cache.pool_score[u].cpu().numpy()
+            pkr = cache.pool_k[u].float().cpu().numpy()
+            pvr = cache.pool_v[u].float().cpu().numpy()
+            ents = [OutlierEntry(int(ppos[s]), pkr[s], pvr[s], float(psc[s])) for s in range(cache.N) if ppos[s] >= 0]
+            pool.entries = sorted(ents, key=lambda e: (e.score, e.position))  # outlier.py:102-103 order
+            apos = cache.aux_pos[u].cpu().numpy()
+            asc = cache.aux_score[u].cpu().numpy()
+            akr = cache.aux_k[u].float().cpu().numpy()
+            avr = cache.aux_v[u].float().cpu().numpy()
+            pool.aux = [OutlierEntry(int(apos[s]), akr[s], avr[s], float(asc[s])) for s in range(meta[1])]
+            pool.frozen = bool(meta[2])
+        else:
+            pool.frozen = cache.A == 0
+        self.pool = pool
+        sm = cache.subst_mask[u].cpu().numpy().view(np.uint32)
+        bits = np.unpackbits(sm.view(np.uint8), bitorder="little")
+        self.substituted_positions = set(np.nonzero(bits)[0].tolist())
+        pm = cache.pool_mask[u].cpu().numpy().view(np.uint32)
+        self.pool_mask_positions = set(np.nonzero(np.unpackbits(pm.view(np.uint8), bitorder="little"))[0].tolist())
+
+    @property
+    def pending_rows(self) -> int:
+        return self.total_tokens - self.quantized_tokens
+
+
+class TieredCache:
+    """Drop-in for ``kvtrace.TieredCache(config, layer, passthrough)`` (cache.py:90-203):
+    one (layer, head) cache with the reference's numpy row interface, backed by
+    a one-unit OTTCache on the GPU. Rows must be fp16-representable (the GPU
+    stores fp16, exactly as the reference's traces are fp16 in practice)."""
+
+    def __init__(self, config: EngineConfig, layer: int = 0, passthrough: bool = False, max_tokens: int = 65536,
+                 device=None, keep_f64_params: bool = True):
+        if passthrough:
+            raise ContractViolation("passthrough (lossless test fixture, quant.py:166-198) is not a GPU mode")
+        self.config = config
+        self.layer = layer
+        self._c = OTTCache(config, 1, 1, max_tokens, layer=layer, device=device, keep_f64_params=keep_f64_params)
+
+    def _row(self, x, name):
+        a = np.asarray(x, dtype=np.float32)
+        d = self.config.head_dim
+        if a.shape != (d,):
+            raise ContractViolation(f"rows must have shape ({d},)")  # cache.py:129-130
+        if not np.isfinite(a).all():
+            raise ContractViolation("rows contain NaN or Inf")  # cache.py:131-132
+        h = a.astype(np.float16)
+        if not np.array_equal(h.astype(np.float32), a):
+            raise ContractViolation(f"{name} row is not fp16-representable")
+        return torch.from_numpy(h).to(self._c.device).view(1, 1, d)
+
+    def append(self, k_row, v_row) -> None:
+        self._c.append(self._row(k_row, "key"), self._row(v_row, "value"))
+
+    def extend(self, keys, values) -> None:
+        """Bulk append (prefill), identical to appending row by row."""
+        k = np.asarray(keys, dtype=np.float32)
+        v = np.asarray(values, dtype=np.float32)
+        require(k.ndim == 2 and k.shape == v.shape and k.shape[1] == self.config.head_dim, "bad prefill shape")
+        require(np.isfinite(k).all() and np.isfinite(v).all(), "rows contain NaN or Inf")
+        kh, vh = k.astype(np.float16), v.astype(np.float16)
+        require(np.array_equal(kh.astype(np.float32), k) and np.array_equal(vh.astype(np.float32), v),
+                "rows are not fp16-representable")
+        dev = self._c.device
+        self._c.update(torch.from_numpy(kh).to(dev)[None, None], torch.from_numpy(vh).to(dev)[None, None])
+
+    def quantize_oldest_group(self) -> None:
+        self._c.quantize_oldest_group()
+
+    def memory_usage(self) -> MemoryBreakdown:
+        return self._c.memory_usage(0, 0)
+
+    def snapshot(self) -> UnitView:
+        return self._c.unit(0, 0)
+
+    @property
+    def total_tokens(self) -> int:
+        return self._c.total_tokens
+
+    @property
+    def quantized_tokens(self) -> int:
+        return self._c.quantized_tokens
+
+    @property
+    def pending_rows(self) -> int:
+        return self._c.pending_rows
+
+    @property
+    def gpu(self) -> OTTCache:
+        return self._c
+
+
+def attend_mixed(q, cache, with_weights: bool = False):
+    """attention.py:79-92. With a TieredCache (numpy interface) returns an
+    AttentionResult; with an OTTCache, q is fp16 [B, H_q, d] and the fp16
+    output tensor is returned."""
+    if isinstance(cache, OTTCache):
+        return cache.attend(q)
+    require(isinstance(cache, TieredCache), "cache must be a TieredCache or OTTCache")
+    d = cache.config.head_dim
+    qa = np.asarray(q, dtype=np.float32)
+    if qa.shape != (d,):
+        raise ContractViolation(f"query must have shape ({d},)")  # attention.py:87-88
+    if cache.total_tokens == 0:
+        raise ContractViolation("cannot attend over an empty cache")
+    qh = qa.astype(np.float16)
+    require(np.array_equal(qh.astype(np.float32), qa), "query is not fp16-representable")
+    qt = torch.from_numpy(qh).to(cache.gpu.device).view(1, 1, d)
+    out = cache.gpu.attend(qt)
+    res = AttentionResult(output=out.float().cpu().numpy().reshape(d))
+    if with_weights:
+        s = cache.gpu.logits(qt).cpu().numpy().reshape(-1).astype(np.float64)
+        w = np.exp(s - s.max())
+        res.weights = (w / w.sum()).astype(np.float32)  # tensor.py:45-57
+        res.scores = s.astype(np.float32)
+    return res

@@ -1,0 +1,147 @@
+// ott_capi.cu — extern "C" entry points (include/ott_b200.h): argument checks
+// that mirror the reference's ContractViolation preconditions, then launches.
+#include <stdio.h>
+#include <string.h>
+
+#include "ott_common.cuh"
+
+namespace ott {
+cudaError_t launch_flush(const ott_cache_t& c, int64_t q0, int n_groups, int64_t ring_end, const uint16_t* in_k,
+                         const uint16_t* in_v, int64_t in_stride, int64_t in_first, cudaStream_t st);
+cudaError_t launch_ring_write(const ott_cache_t& c, const uint16_t* k, const uint16_t* v, int64_t in_stride,
+                              int64_t in_first, int64_t first_pos, int64_t n_rows, cudaStream_t st);
+cudaError_t launch_attend(const ott_cache_t& c, const uint16_t* q, uint16_t* out, int n_rep, int64_t q_tokens,
+                          int64_t total, float* ws, int n_splits, cudaStream_t st);
+cudaError_t launch_logits(const ott_cache_t& c, const uint16_t* q, float* logits, int n_rep, int64_t q_tokens,
+                          int64_t total, cudaStream_t st);
+}  // namespace ott
+
+static thread_local char g_err[512];
+
+static int fail(int code, const char* msg) {
+  snprintf(g_err, sizeof(g_err), "%s", msg);
+  return code;
+}
+
+static int cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return OTT_OK;
+  snprintf(g_err, sizeof(g_err), "CUDA error: %s", cudaGetErrorString(e));
+  return OTT_ERR_CUDA;
+}
+
+static int check_cache(const ott_cache_t* c) {
+  if (!c) return fail(OTT_ERR_CONTRACT, "null cache");
+  if (c->bits != 2) return fail(OTT_ERR_UNSUPPORTED, "only 2-bit codes are implemented on the GPU path");
+  if (c->head_dim != 64 && c->head_dim != 128) return fail(OTT_ERR_UNSUPPORTED, "head_dim must be 64 or 128");
+  if (c->group_size < 32 || c->group_size > ott::kMaxG || c->group_size % 32)
+    return fail(OTT_ERR_UNSUPPORTED, "group_size must be a multiple of 32 in [32, 128]");
+  if (c->residual < 0 || c->capacity < 0 || c->aux_capacity < 0)
+    return fail(OTT_ERR_CONTRACT, "residual, outlier_num, aux_capacity must be >= 0");
+  if (c->capacity > ott::kMaxN) return fail(OTT_ERR_UNSUPPORTED, "outlier_num must be <= 128");
+  if (c->aux_capacity > ott::kMaxA) return fail(OTT_ERR_UNSUPPORTED, "aux_capacity must be <= 1024");
+  if (c->n_units < 1 || c->max_groups < 0) return fail(OTT_ERR_CONTRACT, "bad unit/group counts");
+  if (!c->blocks || !c->pend_k || !c->pend_v || !c->pool_mask || !c->subst_mask || !c->pool_meta)
+    return fail(OTT_ERR_CONTRACT, "null state buffer");
+  return OTT_OK;
+}
+
+extern "C" {
+
+size_t ott_record_bytes(int32_t head_dim, int32_t group_size, int32_t bits) {
+  if (bits != 2) return 0;
+  return (size_t)ott::RecordLayout(head_dim, group_size).bytes();
+}
+
+int ott_ring_write(const ott_cache_t* c, const uint16_t* k, const uint16_t* v, int64_t in_unit_stride,
+                   int64_t in_first_pos, int64_t first_pos, int64_t n_rows, void* stream) {
+  int s = check_cache(c);
+  if (s) return s;
+  if (n_rows < 0 || first_pos < in_first_pos) return fail(OTT_ERR_CONTRACT, "bad row range");
+  if (n_rows == 0) return OTT_OK;
+  if (n_rows > c->group_size + c->residual) return fail(OTT_ERR_CONTRACT, "more rows than the pending ring holds");
+  if (!k || !v) return fail(OTT_ERR_CONTRACT, "null rows");
+  return cuda_status(ott::launch_ring_write(*c, k, v, in_unit_stride, in_first_pos, first_pos, n_rows,
+                                            (cudaStream_t)stream));
+}
+
+int ott_flush(const ott_cache_t* c, int64_t quantized_tokens, int32_t n_groups, int64_t ring_end,
+              const uint16_t* in_k, const uint16_t* in_v, int64_t in_unit_stride, int64_t in_first_pos,
+              void* stream) {
+  int s = check_cache(c);
+  if (s) return s;
+  if (n_groups <= 0) return n_groups == 0 ? OTT_OK : fail(OTT_ERR_CONTRACT, "negative group count");
+  if (quantized_tokens % c->group_size) return fail(OTT_ERR_CONTRACT, "quantized_tokens not group aligned");
+  if (quantized_tokens / c->group_size + n_groups > c->max_groups)
+    return fail(OTT_ERR_CONTRACT, "cache capacity (max_tokens) exceeded");
+  if (quantized_tokens + (int64_t)n_groups * c->group_size > ring_end && (!in_k || !in_v))
+    return fail(OTT_ERR_CONTRACT, "rows beyond the ring need an input buffer");
+  if (quantized_tokens + (int64_t)n_groups * c->group_size > 0x7fffffffLL)
+    return fail(OTT_ERR_UNSUPPORTED, "positions must fit in int32");
+  if (c->capacity > 0 && (!c->pool_pos || !c->pool_score || !c->pool_k || !c->pool_v))
+    return fail(OTT_ERR_CONTRACT, "null pool buffers");
+  if (c->capacity > 0 && c->aux_capacity > 0 && (!c->aux_pos || !c->aux_score || !c->aux_k || !c->aux_v))
+    return fail(OTT_ERR_CONTRACT, "null aux buffers");
+  return cuda_status(ott::launch_flush(*c, quantized_tokens, n_groups, ring_end, in_k, in_v, in_unit_stride,
+                                       in_first_pos, (cudaStream_t)stream));
+}
+
+int ott_num_sms(void) {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
+  return n;
+}
+
+int ott_pick_splits(const ott_cache_t* c, int32_t n_rep, int64_t total_tokens) {
+  (void)n_rep;
+  if (!c || c->n_units < 1) return 1;
+  const int64_t q_tokens = total_tokens >= c->residual + c->group_size
+                               ? ((total_tokens - c->residual) / c->group_size) * c->group_size
+                               : 0;
+  const int64_t n_tiles = q_tokens / 32 + (c->capacity + 31) / 32 + (total_tokens - q_tokens + 31) / 32 + 1;
+  int sms = ott_num_sms();
+  if (sms <= 0) sms = 148;
+  const int64_t target = (int64_t)sms * 4;
+  int64_t s = (target + c->n_units - 1) / c->n_units;
+  const int64_t max_by_tiles = n_tiles / 8 > 0 ? n_tiles / 8 : 1;  // >= 8 tiles (2 per warp) per split
+  if (s > max_by_tiles) s = max_by_tiles;
+  if (s > 64) s = 64;
+  if (s < 1) s = 1;
+  return (int)s;
+}
+
+size_t ott_attend_workspace_floats(const ott_cache_t* c, int32_t n_rep, int32_t n_splits) {
+  if (!c) return 0;
+  return (size_t)c->n_units * n_rep * (n_splits > 0 ? n_splits : 1) * (c->head_dim + 2);
+}
+
+int ott_attend(const ott_cache_t* c, const uint16_t* q, uint16_t* out, int32_t n_rep, int64_t quantized_tokens,
+               int64_t total_tokens, float* workspace, int32_t n_splits, void* stream) {
+  int s = check_cache(c);
+  if (s) return s;
+  if (total_tokens <= 0) return fail(OTT_ERR_CONTRACT, "cannot attend over an empty cache");
+  if (n_rep != 1 && n_rep != 2 && n_rep != 4 && n_rep != 8)
+    return fail(OTT_ERR_UNSUPPORTED, "n_rep (H_q / H_kv) must be 1, 2, 4 or 8");
+  if (quantized_tokens < 0 || quantized_tokens > total_tokens || quantized_tokens % c->group_size)
+    return fail(OTT_ERR_CONTRACT, "inconsistent token counts");
+  if (total_tokens - quantized_tokens > c->group_size + c->residual)
+    return fail(OTT_ERR_CONTRACT, "more pending rows than the ring holds");
+  if (!q || !out || !workspace || n_splits < 1) return fail(OTT_ERR_CONTRACT, "null buffer or bad split count");
+  return cuda_status(ott::launch_attend(*c, q, out, n_rep, quantized_tokens, total_tokens, workspace, n_splits,
+                                        (cudaStream_t)stream));
+}
+
+int ott_logits(const ott_cache_t* c, const uint16_t* q, float* logits, int32_t n_rep, int64_t quantized_tokens,
+               int64_t total_tokens, void* stream) {
+  int s = check_cache(c);
+  if (s) return s;
+  if (total_tokens <= 0) return fail(OTT_ERR_CONTRACT, "cannot attend over an empty cache");
+  if (!q || !logits) return fail(OTT_ERR_CONTRACT, "null buffer");
+  return cuda_status(
+      ott::launch_logits(*c, q, logits, n_rep, quantized_tokens, total_tokens, (cudaStream_t)stream));
+}
+
+const char* ott_version(void) { return "ott_b200 0.1 (sm_100a)"; }
+const char* ott_last_error(void) { return g_err; }
+
+}  // extern "C"

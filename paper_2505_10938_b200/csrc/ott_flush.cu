@@ -1,0 +1,391 @@
+// ott_flush.cu — K1 (group flush: score -> pool competition -> mean substitution
+// -> 2-bit floor quantization -> bit packing) and K4 (pending-ring write).
+//
+// Bit-exactness contract: every float64 operation below is an explicit
+// round-to-nearest intrinsic (__dadd_rn/__dsub_rn/__dmul_rn/__ddiv_rn), so no
+// fused multiply-add can change a result; this TU is also compiled with
+// -fmad=false. For fp16-valued inputs, L1 scores and group means are exact
+// float64 sums in any summation order, so they match numpy's pairwise sums.
+#include "ott_common.cuh"
+
+namespace ott {
+
+constexpr int kFlushThreads = 256;
+
+// quant.py:59-102 for one line held in registers/smem by ONE thread.
+// Returns step; writes codes (0..3) and x_min.
+__device__ __forceinline__ void line_params(double mn, double mx, double& step_out) {
+  const double levels = 3.0;
+  double step = __ddiv_rn(__dsub_rn(mx, mn), levels);  // quant.py:64
+  // quant.py:68-69: while step > 0 and x_min + levels*step > x_max: nextafter(step, 0)
+  while (step > 0.0 && __dadd_rn(mn, __dmul_rn(levels, step)) > mx)
+    step = __longlong_as_double(__double_as_longlong(step) - 1);
+  step_out = step;
+}
+
+__device__ __forceinline__ int quant_code(double x, double mn, double mx, double step) {
+  if (step == 0.0) return 0;  // quant.py:91-92
+  double f = floor(__ddiv_rn(__dsub_rn(x, mn), step));  // quant.py:93
+  int c = f < 0.0 ? 0 : (f > 3.0 ? 3 : (int)f);           // quant.py:94
+  if (__dadd_rn(__dmul_rn((double)c, step), mn) > x) c -= 1;  // quant.py:97
+  c = c < 0 ? 0 : c;                                          // quant.py:98
+  if (x == mx) c = 3;                                         // quant.py:101
+  return c;
+}
+
+struct FlushShared {
+  int n_entries, n_aux, frozen, any_selected;
+  int n_evicted, n_win_cand;
+};
+
+// Dynamic smem layout (floats/doubles/bytes), sized on the host:
+//   float  sk[G*d], sv[G*d]           group rows (substituted in place)
+//   double score[G]
+//   double it_score[N+G]; int it_pos[N+G]; int it_rank[N+G]
+//   int    free_slot[N]; uint8 kc[G*d], vc[G*d]; uint8 sel[G]
+__host__ __device__ inline size_t flush_smem_bytes(int d, int G, int N) {
+  size_t b = 0;
+  b += (size_t)2 * G * d * sizeof(float);
+  b += (size_t)G * sizeof(double);
+  b += (size_t)(N + G) * (sizeof(double) + 2 * sizeof(int));
+  b += (size_t)(N > 0 ? N : 1) * sizeof(int);
+  b += (size_t)2 * G * d;
+  b += (size_t)G;
+  return (b + 15) & ~(size_t)15;
+}
+
+__global__ void __launch_bounds__(kFlushThreads) flush_kernel(ott_cache_t c, int64_t q0, int n_groups,
+                                                              int64_t ring_end, const uint16_t* __restrict__ in_k,
+                                                              const uint16_t* __restrict__ in_v,
+                                                              int64_t in_stride, int64_t in_first) {
+  const int u = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nwarps = kFlushThreads / 32;
+  const int d = c.head_dim, G = c.group_size, N = c.capacity, A = c.aux_capacity;
+  const int cap = G + c.residual;
+  const RecordLayout L(d, G);
+
+  extern __shared__ __align__(16) unsigned char smem[];
+  float* sk = reinterpret_cast<float*>(smem);
+  float* sv = sk + G * d;
+  double* score = reinterpret_cast<double*>(sv + G * d);
+  double* it_score = score + G;
+  int* it_pos = reinterpret_cast<int*>(it_score + N + G);
+  int* it_rank = it_pos + N + G;
+  int* free_slot = it_rank + N + G;
+  uint8_t* kc = reinterpret_cast<uint8_t*>(free_slot + (N > 0 ? N : 1));
+  uint8_t* vc = kc + G * d;
+  uint8_t* sel = vc + G * d;
+  __shared__ FlushShared sh;
+
+  int32_t* meta = c.pool_meta + (size_t)u * 4;
+  int32_t* ppos = c.pool_pos + (size_t)u * N;
+  double* pscore = c.pool_score + (size_t)u * N;
+  uint16_t* pk = c.pool_k + (size_t)u * N * d;
+  uint16_t* pv = c.pool_v + (size_t)u * N * d;
+  int32_t* apos = c.aux_pos + (size_t)u * A;
+  double* ascore = c.aux_score + (size_t)u * A;
+  uint16_t* ak = c.aux_k + (size_t)u * A * d;
+  uint16_t* av = c.aux_v + (size_t)u * A * d;
+  uint32_t* pmask = c.pool_mask + (size_t)u * mask_words_per_unit(c);
+  uint32_t* smask = c.subst_mask + (size_t)u * mask_words_per_unit(c);
+
+  if (tid == 0) {
+    sh.n_entries = meta[0];
+    sh.n_aux = meta[1];
+    sh.frozen = meta[2];
+  }
+  __syncthreads();
+
+  for (int g = 0; g < n_groups; ++g) {
+    const int64_t base = q0 + (int64_t)g * G;
+    const int64_t gi = base / G;
+    uint8_t* rec = record_ptr(c, u, gi);
+
+    // ---- 1. gather the oldest G pending rows (cache.py:155-156), fp16 -> f32
+    for (int e = tid * 8; e < G * d; e += kFlushThreads * 8) {
+      const int i = e / d, col = e % d;
+      const int64_t p = base + i;
+      const uint16_t *srck, *srcv;
+      if (p < ring_end) {
+        const size_t off = ((size_t)u * cap + (size_t)(p % cap)) * d + col;
+        srck = c.pend_k + off;
+        srcv = c.pend_v + off;
+      } else {
+        const size_t off = (size_t)u * in_stride + (size_t)(p - in_first) * d + col;
+        srck = in_k + off;
+        srcv = in_v + off;
+      }
+      const uint4 k8 = *reinterpret_cast<const uint4*>(srck);
+      const uint4 v8 = *reinterpret_cast<const uint4*>(srcv);
+      const uint16_t* kh = reinterpret_cast<const uint16_t*>(&k8);
+      const uint16_t* vh = reinterpret_cast<const uint16_t*>(&v8);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        sk[e + j] = h2f(kh[j]);
+        sv[e + j] = h2f(vh[j]);
+      }
+    }
+    if (tid < G) sel[tid] = 0;
+    if (tid == 0) sh.any_selected = 0;
+    __syncthreads();
+
+    const bool active = N > 0 && !sh.frozen;  // cache.py:158 (block-uniform)
+    if (active) {
+      // ---- 2a. score_tokens: L1 norm of each key row in float64 (outlier.py:45-49)
+      for (int i = warp; i < G; i += nwarps) {
+        double s = 0.0;
+        for (int col = lane; col < d; col += 32) s = __dadd_rn(s, fabs((double)sk[i * d + col]));
+        s = warp_sum(s);
+        if (lane == 0) score[i] = s;
+      }
+      __syncthreads();
+      // ---- 2b. OutlierPool.update (outlier.py:84-117), rank-by-count.
+      // items [0, N): current slots (pos < 0 = empty); [N, N+G): candidates.
+      const int M = N + G;
+      for (int t = tid; t < M; t += kFlushThreads) {
+        if (t < N) {
+          it_pos[t] = ppos[t];
+          it_score[t] = pscore[t];
+        } else {
+          it_pos[t] = (int)(base + (t - N));
+          it_score[t] = score[t - N];
+        }
+      }
+      __syncthreads();
+      for (int t = tid; t < M; t += kFlushThreads) {
+        int r = -1;
+        if (it_pos[t] >= 0) {
+          const double s = it_score[t];
+          const int p = it_pos[t];
+          r = 0;
+          for (int j = 0; j < M; ++j) {
+            if (it_pos[j] < 0) continue;
+            const double sj = it_score[j];
+            r += (sj < s || (sj == s && it_pos[j] < p)) ? 1 : 0;  // _rank, outlier.py:52-54
+          }
+        }
+        it_rank[t] = r;
+      }
+      __syncthreads();
+      // evicted old entries -> aux in old reference order (= ascending rank),
+      // free slots listed in ascending slot index.
+      if (tid < N) {
+        const int r = it_rank[tid];
+        const bool evicted = r >= N;
+        const bool is_free = r < 0 || evicted;
+        int fidx = 0;
+        for (int s = 0; s < tid; ++s) {
+          const int rs = it_rank[s];
+          fidx += (rs < 0 || rs >= N) ? 1 : 0;
+        }
+        if (is_free) free_slot[fidx] = tid;
+        if (evicted) {
+          int eidx = 0;
+          for (int s = 0; s < N; ++s) eidx += (it_rank[s] >= N && it_rank[s] < r) ? 1 : 0;
+          const int room = A - sh.n_aux;  // outlier.py:113-114
+          if (eidx < room) {
+            const int a = sh.n_aux + eidx;
+            apos[a] = it_pos[tid];
+            ascore[a] = it_score[tid];
+          }
+          const int p = it_pos[tid];
+          atomicAnd(&pmask[p >> 5], ~(1u << (p & 31)));  // back to its shadow row
+        }
+      }
+      __syncthreads();
+      if (tid == 0) {
+        int n_ev = 0, n_old = 0;
+        for (int s = 0; s < N; ++s) {
+          n_ev += it_rank[s] >= N ? 1 : 0;
+          n_old += it_rank[s] >= 0 ? 1 : 0;
+        }
+        int n_wc = 0;
+        for (int i = 0; i < G; ++i) n_wc += it_rank[N + i] < N ? 1 : 0;
+        sh.n_evicted = n_ev;
+        sh.n_win_cand = n_wc;
+        sh.any_selected = n_wc > 0;
+      }
+      __syncthreads();
+      // copy evicted rows into aux before their slots are reused
+      {
+        const int room = A - sh.n_aux;
+        for (int s = warp; s < N; s += nwarps) {
+          const int r = it_rank[s];
+          if (r < N) continue;
+          int eidx = 0;
+          for (int t = 0; t < N; ++t) eidx += (it_rank[t] >= N && it_rank[t] < r) ? 1 : 0;
+          if (eidx >= room) continue;
+          const int a = sh.n_aux + eidx;
+          for (int col = lane; col < d; col += 32) {
+            ak[(size_t)a * d + col] = pk[(size_t)s * d + col];
+            av[(size_t)a * d + col] = pv[(size_t)s * d + col];
+          }
+        }
+      }
+      __syncthreads();
+      // winning candidates take free slots in candidate order
+      for (int i = warp; i < G; i += nwarps) {
+        const int r = it_rank[N + i];
+        if (r >= N) continue;
+        int widx = 0;
+        for (int j = 0; j < i; ++j) widx += it_rank[N + j] < N ? 1 : 0;
+        const int s = free_slot[widx];
+        for (int col = lane; col < d; col += 32) {
+          pk[(size_t)s * d + col] = f2h(sk[i * d + col]);  // original row (fp16-exact)
+          pv[(size_t)s * d + col] = f2h(sv[i * d + col]);
+        }
+        if (lane == 0) {
+          ppos[s] = (int)(base + i);
+          pscore[s] = score[i];
+          sel[i] = 1;
+          const int p = (int)(base + i);
+          atomicOr(&pmask[p >> 5], 1u << (p & 31));
+          atomicOr(&smask[p >> 5], 1u << (p & 31));  // cache.py:173
+        }
+      }
+      __syncthreads();
+      if (tid == 0) {
+        const int room = A - sh.n_aux;
+        sh.n_aux += sh.n_evicted < room ? sh.n_evicted : room;
+        int n_e = 0;
+        for (int t = 0; t < M; ++t) n_e += (it_rank[t] >= 0 && it_rank[t] < N) ? 1 : 0;
+        sh.n_entries = n_e;
+        if (sh.n_aux >= A) sh.frozen = 1;  // outlier.py:115-116
+      }
+      // ---- 2c. substitute_means (outlier.py:120-142): column means over the
+      // ORIGINAL G rows, float64 accumulate, cast to float32, then overwrite.
+      if (sh.any_selected) {
+        for (int col = tid; col < d; col += kFlushThreads) {
+          double mk = 0.0, mv = 0.0;
+          for (int i = 0; i < G; ++i) {
+            mk = __dadd_rn(mk, (double)sk[i * d + col]);
+            mv = __dadd_rn(mv, (double)sv[i * d + col]);
+          }
+          const float fk = __double2float_rn(__ddiv_rn(mk, (double)G));
+          const float fv = __double2float_rn(__ddiv_rn(mv, (double)G));
+          for (int i = 0; i < G; ++i) {
+            if (sel[i]) {
+              sk[i * d + col] = fk;
+              sv[i * d + col] = fv;
+            }
+          }
+        }
+      }
+      __syncthreads();
+    }
+
+    // ---- 3. quantize: K per channel (threads [0,d)), V per token (remaining warps)
+    double* p64 = c.params64 ? c.params64 + ((size_t)u * c.max_groups + (size_t)gi) * 2 * (d + G) : nullptr;
+    float* kstep = reinterpret_cast<float*>(rec + L.k_step());
+    float* kxmin = reinterpret_cast<float*>(rec + L.k_xmin());
+    float* vstep = reinterpret_cast<float*>(rec + L.v_step());
+    float* vxmin = reinterpret_cast<float*>(rec + L.v_xmin());
+    if (tid < d) {
+      const int col = tid;
+      double mn = (double)sk[col], mx = mn;
+      for (int i = 1; i < G; ++i) {
+        const double x = (double)sk[i * d + col];
+        mn = fmin(mn, x);
+        mx = fmax(mx, x);
+      }
+      double step;
+      line_params(mn, mx, step);
+      for (int i = 0; i < G; ++i) kc[i * d + col] = (uint8_t)quant_code((double)sk[i * d + col], mn, mx, step);
+      kstep[col] = __double2float_rn(step);
+      kxmin[col] = __double2float_rn(mn);
+      if (p64) {
+        p64[col] = mn;
+        p64[d + col] = step;
+      }
+    } else {
+      const int vw = warp - d / 32, nvw = nwarps - d / 32;
+      for (int i = vw; i < G; i += nvw) {
+        double mn = 1e308, mx = -1e308;
+        for (int col = lane; col < d; col += 32) {
+          const double x = (double)sv[i * d + col];
+          mn = fmin(mn, x);
+          mx = fmax(mx, x);
+        }
+        mn = warp_min_d(mn);
+        mx = warp_max_d(mx);
+        double step;
+        line_params(mn, mx, step);
+        for (int col = lane; col < d; col += 32)
+          vc[i * d + col] = (uint8_t)quant_code((double)sv[i * d + col], mn, mx, step);
+        if (lane == 0) {
+          vstep[i] = __double2float_rn(step);
+          vxmin[i] = __double2float_rn(mn);
+          if (p64) {
+            p64[2 * d + i] = mn;
+            p64[2 * d + G + i] = step;
+          }
+        }
+      }
+    }
+    __syncthreads();
+
+    // ---- 4. pack_codes (quant.py:241-256): element e=t*d+c at bits [2e, 2e+2)
+    {
+      uint32_t* kw = reinterpret_cast<uint32_t*>(rec + L.k_codes());
+      uint32_t* vw = reinterpret_cast<uint32_t*>(rec + L.v_codes());
+      const int n_words = G * d / 16;
+      for (int w = tid; w < 2 * n_words; w += kFlushThreads) {
+        const bool isv = w >= n_words;
+        const int ww = isv ? w - n_words : w;
+        const uint8_t* src = (isv ? vc : kc) + ww * 16;
+        uint32_t word = 0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) word |= (uint32_t)src[j] << (2 * j);
+        (isv ? vw : kw)[ww] = word;
+      }
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    meta[0] = sh.n_entries;
+    meta[1] = sh.n_aux;
+    meta[2] = sh.frozen;
+  }
+}
+
+// K4: ring write. One thread per 8 halves.
+__global__ void ring_write_kernel(ott_cache_t c, const uint16_t* __restrict__ k, const uint16_t* __restrict__ v,
+                                  int64_t in_stride, int64_t in_first, int64_t first_pos, int64_t n_rows) {
+  const int d = c.head_dim;
+  const int cap = c.group_size + c.residual;
+  const int vec_per_row = d / 8;
+  const int64_t total = (int64_t)c.n_units * n_rows * vec_per_row;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(idx % vec_per_row);
+    const int64_t r = (idx / vec_per_row) % n_rows;
+    const int u = (int)(idx / (vec_per_row * n_rows));
+    const int64_t p = first_pos + r;
+    const size_t src = (size_t)u * in_stride + (size_t)(p - in_first) * d + j * 8;
+    const size_t dst = ((size_t)u * cap + (size_t)(p % cap)) * d + j * 8;
+    *reinterpret_cast<uint4*>(c.pend_k + dst) = *reinterpret_cast<const uint4*>(k + src);
+    *reinterpret_cast<uint4*>(c.pend_v + dst) = *reinterpret_cast<const uint4*>(v + src);
+  }
+}
+
+cudaError_t launch_flush(const ott_cache_t& c, int64_t q0, int n_groups, int64_t ring_end, const uint16_t* in_k,
+                         const uint16_t* in_v, int64_t in_stride, int64_t in_first, cudaStream_t st) {
+  const size_t smem = flush_smem_bytes(c.head_dim, c.group_size, c.capacity);
+  cudaError_t e = cudaFuncSetAttribute(flush_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  flush_kernel<<<c.n_units, kFlushThreads, smem, st>>>(c, q0, n_groups, ring_end, in_k, in_v, in_stride, in_first);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ring_write(const ott_cache_t& c, const uint16_t* k, const uint16_t* v, int64_t in_stride,
+                              int64_t in_first, int64_t first_pos, int64_t n_rows, cudaStream_t st) {
+  const int64_t total = (int64_t)c.n_units * n_rows * (c.head_dim / 8);
+  int blocks = (int)((total + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) blocks = 1;
+  ring_write_kernel<<<blocks, 256, 0, st>>>(c, k, v, in_stride, in_first, first_pos, n_rows);
+  return cudaGetLastError();
+}
+
+}  // namespace ott

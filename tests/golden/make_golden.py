@@ -192,15 +192,15 @@ def gen_caches(kv):
     k, v = fp16(k), fp16(rng.standard_normal((T, d)))
     q = fp16(rng.standard_normal((3, d)))
     np.savez_compressed(os.path.join(HERE, "cache_default.npz"), **run_cache(kv, k, v, q, 2, 128, 32, 3, 32, 64))
-    # fast-freezing pool: small aux so freezing happens mid-stream; G=32, d=32, R=0
+    # fast-freezing pool: small aux so freezing happens mid-stream; G=32, d=64, R=0
     rng = np.random.default_rng(6)
-    T, d = 800, 32
+    T, d = 800, 64
     k = rng.standard_normal((T, d)) * 3
     low = rng.choice(T, 60, replace=False)
     k[low] *= 0.01
     k, v = fp16(k), fp16(rng.standard_normal((T, d)))
     q = fp16(rng.standard_normal((2, d)))
-    np.savez_compressed(os.path.join(HERE, "cache_freeze.npz"), **run_cache(kv, k, v, q, 2, 32, 0, 4, 5, 32))
+    np.savez_compressed(os.path.join(HERE, "cache_freeze.npz"), **run_cache(kv, k, v, q, 2, 32, 0, 4, 5, 64))
 
 
 def main():

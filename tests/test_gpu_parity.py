@@ -1,0 +1,367 @@
+"""GPU parity: the sm_100a path (through the C ABI) vs the CPU oracle and the
+reference's golden fixtures. Quantization state must be bit-exact; attention
+outputs within |gpu - ref| <= 2e-3 + 1e-2*|ref| (north_star: max-abs 2e-3 /
+rtol 1e-2, fp16 output)."""
+
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import GOLDEN
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+ATOL, RTOL = 2e-3, 1e-2
+
+
+def within_tol(out, ref):
+    err = np.abs(np.asarray(out, np.float64) - np.asarray(ref, np.float64))
+    return bool((err <= ATOL + RTOL * np.abs(ref)).all()), float(err.max())
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2505_10938_b200 import _native
+
+    _native.lib()
+    torch.cuda.set_device(0)
+
+
+def cfg_of(bits, G, R, N, A, d):
+    from paper_2505_10938_b200 import EngineConfig
+
+    return EngineConfig(bits=bits, group_size=G, residual=R, outlier_num=N, aux_capacity=A, skip_layers=(), head_dim=d)
+
+
+def assert_unit_matches_oracle(u, ref, exact64=True):
+    """Bit-exact quantization state of one GPU unit vs an oracle cache."""
+    assert u.total_tokens == ref.total_tokens and u.quantized_tokens == ref.quantized_tokens
+    assert len(u.quantized_k) == ref.n_blocks
+    for b in range(ref.n_blocks):
+        blk = ref.block(b)
+        assert u.quantized_k[b].codes == blk["k_codes"], f"K codes block {b}"
+        assert u.quantized_v[b].codes == blk["v_codes"], f"V codes block {b}"
+        if exact64:
+            assert [p.x_min for p in u.quantized_k[b].params] == blk["k_xmin"].tolist()
+            assert [p.step for p in u.quantized_k[b].params] == blk["k_step"].tolist()
+            assert [p.x_min for p in u.quantized_v[b].params] == blk["v_xmin"].tolist()
+            assert [p.step for p in u.quantized_v[b].params] == blk["v_step"].tolist()
+        np.testing.assert_array_equal(u.k_step32[b], blk["k_step"].astype(np.float32))
+        np.testing.assert_array_equal(u.k_xmin32[b], blk["k_xmin"].astype(np.float32))
+        np.testing.assert_array_equal(u.v_step32[b], blk["v_step"].astype(np.float32))
+        np.testing.assert_array_equal(u.v_xmin32[b], blk["v_xmin"].astype(np.float32))
+    pe = ref.pool_entries()
+    assert [e.position for e in u.pool.entries] == pe["position"].tolist()
+    assert [e.score for e in u.pool.entries] == pe["score"].tolist()
+    for e, k, v in zip(u.pool.entries, pe["key"], pe["value"]):
+        np.testing.assert_array_equal(e.key, k)
+        np.testing.assert_array_equal(e.value, v)
+    ae = ref.aux_entries()
+    assert [e.position for e in u.pool.aux] == ae["position"].tolist()
+    assert [e.score for e in u.pool.aux] == ae["score"].tolist()
+    for e, k in zip(u.pool.aux, ae["key"]):
+        np.testing.assert_array_equal(e.key, k)
+    assert u.pool.frozen == ref.frozen
+    assert sorted(u.substituted_positions) == ref.substituted_positions.tolist()
+    assert u.pool_mask_positions == set(pe["position"].tolist())
+    pk, pv = ref.pending()
+    np.testing.assert_array_equal(u.pending_k, pk)
+    np.testing.assert_array_equal(u.pending_v, pv)
+
+
+# --------------------------------------------------------------------------- golden fixtures
+
+
+@pytest.mark.parametrize("name", ["cache_c0_n32.npz", "cache_c0_n3.npz", "cache_default.npz", "cache_freeze.npz"])
+@pytest.mark.parametrize("mode", ["append", "update"])
+def test_golden_stream(name, mode):
+    from paper_2505_10938_b200 import OTTCache
+
+    g = np.load(os.path.join(GOLDEN, name))
+    bits, G, R, N, A, d = (int(x) for x in g["cfg"])
+    T = g["k"].shape[0]
+    cache = OTTCache(cfg_of(bits, G, R, N, A, d), 1, 1, max_tokens=T + G, keep_f64_params=True)
+    kt = torch.from_numpy(g["k"].astype(np.float16)).cuda()
+    vt = torch.from_numpy(g["v"].astype(np.float16)).cuda()
+    hist = []
+    if mode == "append":
+        for t in range(T):
+            nb = cache.quantized_tokens
+            cache.append(kt[t].view(1, 1, d), vt[t].view(1, 1, d))
+            if cache.quantized_tokens != nb:
+                pos = [e.position for e in cache.unit(0, 0).pool.entries]
+                hist.append(pos + [-1] * (max(N, 1) - len(pos)))
+        np.testing.assert_array_equal(np.array(hist).reshape(g["hist_entries"].shape), g["hist_entries"])
+    else:
+        cuts = [0, 1, 77, 300, T // 2, T - 5, T]
+        for a, b in zip(cuts[:-1], cuts[1:]):
+            cache.update(kt[a:b][None, None], vt[a:b][None, None])
+    u = cache.unit(0, 0)
+    nb = g["k_codes"].shape[0]
+    assert len(u.quantized_k) == nb
+    for b in range(nb):
+        assert u.quantized_k[b].codes == g["k_codes"][b].tobytes()
+        assert u.quantized_v[b].codes == g["v_codes"][b].tobytes()
+        assert [p.x_min for p in u.quantized_k[b].params] == g["k_xmin"][b].tolist()
+        assert [p.step for p in u.quantized_k[b].params] == g["k_step"][b].tolist()
+        assert [p.x_min for p in u.quantized_v[b].params] == g["v_xmin"][b].tolist()
+        assert [p.step for p in u.quantized_v[b].params] == g["v_step"][b].tolist()
+    assert [e.position for e in u.pool.entries] == g["pool_pos"].tolist()
+    assert [e.score for e in u.pool.entries] == g["pool_score"].tolist()
+    assert [e.position for e in u.pool.aux] == g["aux_pos"].tolist()
+    assert u.pool.frozen == bool(g["frozen"])
+    assert sorted(u.substituted_positions) == g["substituted"].tolist()
+    mu = cache.memory_usage(0, 0)
+    assert [mu.quantized_bits, mu.param_bits, mu.pending_bits, mu.pool_bits] == g["memory"].tolist()
+    q = torch.from_numpy(g["q"].astype(np.float16)).cuda()
+    for i in range(q.shape[0]):
+        out = cache.attend(q[i].view(1, 1, d)).float().cpu().numpy().reshape(d)
+        ok, err = within_tol(out, g["attn_out"][i])
+        assert ok, err
+
+
+# --------------------------------------------------------------------------- batched vs oracle
+
+
+def config0_batch(seed, H, T, d=128):
+    """BASELINE config 0 generator for H heads: per-head seeded streams."""
+    ks, vs, qs = [], [], []
+    for h in range(H):
+        rng = np.random.default_rng(np.random.SeedSequence(entropy=seed, spawn_key=(0, 0, h)))
+        k = rng.standard_normal((T, d))
+        ch = rng.choice(d, 4, replace=False)
+        k[:, ch] *= 15.0
+        tok = rng.choice(T, 8, replace=False)
+        k[np.ix_(tok, ch)] *= 0.05
+        ks.append(k)
+        vs.append(rng.standard_normal((T, d)))
+        qs.append(rng.standard_normal((8, d)))
+    f = lambda a: np.array(a).astype(np.float16)
+    return f(ks), f(vs), f(qs)
+
+
+@pytest.mark.parametrize("N", [32, 3, 0])
+def test_config0_all_heads_bit_exact(N):
+    from paper_2505_10938_b200 import OTTCache
+
+    H, T, d = 32, 1024, 128
+    k, v, q = config0_batch(0, H, T)
+    cache = OTTCache(cfg_of(2, 32, 128, N, 32, d), 1, H, max_tokens=T, keep_f64_params=True)
+    kt, vt = torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda()
+    cache.update(kt[None, :, : T - 64], vt[None, :, : T - 64])
+    for t in range(T - 64, T):
+        cache.append(kt[None, :, t], vt[None, :, t])
+    out = cache.attend(torch.from_numpy(q[:, 0]).cuda()[None]).float().cpu().numpy()[0]
+    for h in range(H):
+        ref = oracle.OracleCache(2, 32, 128, N, 32, d)
+        ref.extend(k[h].astype(np.float32), v[h].astype(np.float32))
+        assert_unit_matches_oracle(cache.unit(0, h), ref)
+        ok, err = within_tol(out[h], ref.attend(q[h, 0].astype(np.float32)))
+        assert ok, (h, err)
+
+
+@pytest.mark.parametrize("n_rep", [1, 2, 4, 8])
+def test_gqa_attention_vs_oracle(n_rep):
+    from paper_2505_10938_b200 import OTTCache
+
+    B, Hkv, T, d = 2, 4, 2048 + 45, 128
+    k, v, q = config0_batch(3, B * Hkv, T)
+    cache = OTTCache(cfg_of(2, 32, 128, 32, 32, d), B, Hkv, max_tokens=T)
+    cache.update(torch.from_numpy(k.reshape(B, Hkv, T, d)).cuda(), torch.from_numpy(v.reshape(B, Hkv, T, d)).cuda())
+    qh = q[:, :n_rep].reshape(B, Hkv * n_rep, d)
+    out = cache.attend(torch.from_numpy(qh).cuda()).float().cpu().numpy()
+    for u in range(B * Hkv):
+        ref = oracle.OracleCache(2, 32, 128, 32, 32, d)
+        ref.extend(k[u].astype(np.float32), v[u].astype(np.float32))
+        b, h = divmod(u, Hkv)
+        for r in range(n_rep):
+            ok, err = within_tol(out[b, h * n_rep + r], ref.attend(qh[b, h * n_rep + r].astype(np.float32)))
+            assert ok, (u, r, err)
+
+
+def test_explicit_splits_agree():
+    from paper_2505_10938_b200 import OTTCache
+
+    H, T, d = 4, 3000, 128
+    k, v, q = config0_batch(5, H, T)
+    cache = OTTCache(cfg_of(2, 32, 128, 3, 32, d), 1, H, max_tokens=T)
+    cache.update(torch.from_numpy(k[None]).cuda(), torch.from_numpy(v[None]).cuda())
+    qt = torch.from_numpy(q[:, :2].reshape(1, H * 2, d)).cuda()
+    outs = [cache.attend(qt, n_splits=s).float().cpu().numpy() for s in (1, 3, 7, 16)]
+    for o in outs[1:]:
+        np.testing.assert_allclose(o, outs[0], atol=2e-3, rtol=0)
+
+
+# --------------------------------------------------------------------------- semantics / edge cases
+
+
+def test_drop_in_tiered_cache_and_attend_mixed():
+    """Reference-shaped API: TieredCache.append + attend_mixed with weights."""
+    from paper_2505_10938_b200 import ContractViolation, TieredCache, attend_mixed
+
+    g = np.load(os.path.join(GOLDEN, "cache_c0_n32.npz"))
+    bits, G, R, N, A, d = (int(x) for x in g["cfg"])
+    c = TieredCache(cfg_of(bits, G, R, N, A, d), layer=0, max_tokens=2048)
+    for kr, vr in zip(g["k"], g["v"]):
+        c.append(kr, vr)
+    res = attend_mixed(g["q"][0], c, with_weights=True)
+    ok, err = within_tol(res.output, g["attn_out"][0])
+    assert ok, err
+    np.testing.assert_allclose(res.weights, g["attn_w"][0], atol=5e-5, rtol=1e-3)
+    assert abs(float(res.weights.sum(dtype=np.float64)) - 1.0) <= 1e-6
+    with pytest.raises(ContractViolation):
+        c.append(np.zeros(d + 1, np.float32), np.zeros(d, np.float32))
+    with pytest.raises(ContractViolation):
+        c.append(np.full(d, np.nan, np.float32), np.zeros(d, np.float32))
+    with pytest.raises(ContractViolation):
+        attend_mixed(np.zeros(3, np.float32), c)
+    with pytest.raises(ContractViolation):
+        TieredCache(cfg_of(2, 32, 0, 1, 4, 128), passthrough=True)
+
+
+def test_empty_and_single_token():
+    from paper_2505_10938_b200 import ContractViolation, OTTCache
+
+    d = 128
+    cache = OTTCache(cfg_of(2, 32, 128, 32, 32, d), 2, 2, max_tokens=64)
+    with pytest.raises(ContractViolation):
+        cache.attend(torch.zeros((2, 2, d), dtype=torch.float16, device="cuda"))
+    with pytest.raises(ContractViolation):
+        cache.quantize_oldest_group()  # cache.py:150-153
+    kv = torch.randn((2, 2, d), device="cuda").half()
+    vv = torch.randn((2, 2, d), device="cuda").half()
+    cache.append(kv, vv)
+    out = cache.attend(torch.randn((2, 2, d), device="cuda").half())
+    torch.testing.assert_close(out, vv, atol=1e-3, rtol=0)  # test_attention.py:102-110 (softmax of a singleton)
+
+
+def test_residual_zero_and_manual_quantize():
+    """G=32, R=0 triggers at every 32nd append; a manual quantize needs G pending rows."""
+    from paper_2505_10938_b200 import OTTCache
+
+    H, T, d = 2, 96, 128
+    k, v, _ = config0_batch(9, H, T)
+    cache = OTTCache(cfg_of(2, 32, 0, 2, 32, d), 1, H, max_tokens=T, keep_f64_params=True)
+    for t in range(T):
+        cache.append(torch.from_numpy(k[None, :, t]).cuda(), torch.from_numpy(v[None, :, t]).cuda())
+        assert cache.pending_rows == (t + 1) % 32
+    for h in range(H):
+        ref = oracle.OracleCache(2, 32, 0, 2, 32, d)
+        ref.extend(k[h].astype(np.float32), v[h].astype(np.float32))
+        assert_unit_matches_oracle(cache.unit(0, h), ref)
+
+
+def test_manual_quantize_oldest_group_with_residual():
+    from paper_2505_10938_b200 import OTTCache
+
+    H, T, d = 2, 70, 64
+    k, v, _ = config0_batch(11, H, T, d=d)
+    cache = OTTCache(cfg_of(2, 32, 128, 4, 32, d), 1, H, max_tokens=256, keep_f64_params=True)
+    cache.update(torch.from_numpy(k[None]).cuda(), torch.from_numpy(v[None]).cuda())
+    cache.quantize_oldest_group()  # explicit flush with R rows not yet exceeded
+    cache.quantize_oldest_group()
+    for h in range(H):
+        ref = oracle.OracleCache(2, 32, 128, 4, 32, d)
+        ref.extend(k[h].astype(np.float32), v[h].astype(np.float32))
+        ref.quantize_oldest_group()
+        ref.quantize_oldest_group()
+        assert_unit_matches_oracle(cache.unit(0, h), ref)
+
+
+def test_aux_zero_freezes_at_construction_and_n0_is_kivi():
+    """outlier.py:77-78 (A=0 frozen) and cache.py N=0 == direct group quantization."""
+    from paper_2505_10938_b200 import OTTCache
+
+    H, T, d = 2, 300, 128
+    k, v, _ = config0_batch(12, H, T)
+    for N, A in ((4, 0), (0, 32)):
+        cache = OTTCache(cfg_of(2, 32, 128, N, A, d), 1, H, max_tokens=T, keep_f64_params=True)
+        cache.update(torch.from_numpy(k[None]).cuda(), torch.from_numpy(v[None]).cuda())
+        for h in range(H):
+            u = cache.unit(0, h)
+            assert u.pool.entries == [] and u.substituted_positions == set()
+            for b in range(len(u.quantized_k)):
+                kc, _, _ = oracle.quantize_group(k[h, b * 32:(b + 1) * 32].astype(np.float32), 2, True)
+                vc, _, _ = oracle.quantize_group(v[h, b * 32:(b + 1) * 32].astype(np.float32), 2, False)
+                assert u.quantized_k[b].codes == kc and u.quantized_v[b].codes == vc
+
+
+def test_pool_logit_ignores_shadow_row():
+    """test_attention.py:141-166: corrupting the mean-substituted quantized row of
+    a pooled position must not change the output (bitwise)."""
+    from paper_2505_10938_b200 import OTTCache
+
+    H, T, d = 1, 512, 128
+    k, v, q = config0_batch(13, H, T)
+    cache = OTTCache(cfg_of(2, 32, 128, 3, 32, d), 1, H, max_tokens=T)
+    cache.update(torch.from_numpy(k[None]).cuda(), torch.from_numpy(v[None]).cuda())
+    qt = torch.from_numpy(q[:, 0][None]).cuda()
+    before = cache.attend(qt, n_splits=1).clone()
+    u = cache.unit(0, 0)
+    assert len(u.pool.entries) == 3
+    for e in u.pool.entries:
+        gi, row = divmod(e.position, 32)
+        cache.blocks[0, gi, row * 32:(row + 1) * 32] ^= 0xFF  # K codes of that token
+        cache.blocks[0, gi, 1024 + row * 32:1024 + (row + 1) * 32] = 0  # V codes
+    after = cache.attend(qt, n_splits=1)
+    assert torch.equal(before, after)
+
+
+def test_capacity_exceeded_is_contract_violation():
+    from paper_2505_10938_b200 import ContractViolation, OTTCache
+
+    d = 128
+    cache = OTTCache(cfg_of(2, 32, 0, 2, 32, d), 1, 1, max_tokens=64)
+    x = torch.randn((1, 1, 96, d), device="cuda").half()
+    with pytest.raises(ContractViolation):
+        cache.update(x, x)
+
+
+def test_unsupported_shapes_rejected():
+    from paper_2505_10938_b200 import ContractViolation, OTTCache
+
+    with pytest.raises(ContractViolation):
+        OTTCache(cfg_of(4, 32, 0, 2, 32, 128), 1, 1, 64)
+    with pytest.raises(ContractViolation):
+        OTTCache(cfg_of(2, 48, 0, 2, 32, 128), 1, 1, 64)
+    with pytest.raises(ContractViolation):
+        OTTCache(cfg_of(2, 32, 0, 2, 32, 96), 1, 1, 64)
+
+
+# --------------------------------------------------------------------------- full-size properties
+
+
+def test_config3_scale_sampled_units():
+    """Config 3 shape (H_q=32, H_kv=8, d=128) at B=16, T=4096: bulk prefill on the GPU,
+    sampled units checked bit-exact + attention within tolerance against the oracle."""
+    from paper_2505_10938_b200 import OTTCache
+
+    B, Hkv, n_rep, T, d = 16, 8, 4, 4096, 128
+    gen = torch.Generator(device="cuda").manual_seed(0)
+    k = torch.randn((B, Hkv, T, d), device="cuda", generator=gen)
+    k[..., :4] *= 15
+    k = k.half()
+    v = torch.randn((B, Hkv, T, d), device="cuda", generator=gen).half()
+    q = torch.randn((B, Hkv * n_rep, d), device="cuda", generator=gen).half()
+    cache = OTTCache(cfg_of(2, 32, 128, 32, 32, d), B, Hkv, max_tokens=T + 64)
+    cache.update(k, v)
+    out = cache.attend(q).float().cpu().numpy()
+    kh, vh, qh = k.cpu().numpy(), v.cpu().numpy(), q.cpu().numpy()
+    for b, h in ((0, 0), (7, 3), (15, 7)):
+        ref = oracle.OracleCache(2, 32, 128, 32, 32, d)
+        ref.extend(kh[b, h].astype(np.float32), vh[b, h].astype(np.float32))
+        assert_unit_matches_oracle(cache.unit(b, h), ref, exact64=False)
+        for r in range(n_rep):
+            ok, err = within_tol(out[b, h * n_rep + r], ref.attend(qh[b, h * n_rep + r].astype(np.float32)))
+            assert ok, (b, h, r, err)
+
+
+def test_graft_smoke():
+    import __graft_entry__
+
+    __graft_entry__.smoke()
