@@ -1,0 +1,386 @@
+"""bench.py — OTT 2-bit quantized-KV decode on B200 (BASELINE.json metric).
+
+Default workload (N=1): BASELINE configs[4], the Llama-3-70B-shaped KV cache —
+80 layers, B=128, H_q=64, H_kv=8, d=128, 16,384-token context, 2-bit G=32,
+R=128, outlier pool 32 (aux 32, paper skip_layers (0, 1)). A decode step =
+for every layer: append one token per (batch, kv head) unit (flush the
+residual window when due) + mixed-tier attention for all 64 query heads.
+Under torchrun (N>1) the batch is partitioned across ranks (whole sequences,
+all kv heads of a sequence on one rank) and head outputs are all-gathered over
+NCCL every layer.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4|c3|c3s|c2|c0]
+  python bench.py --impl reference ...   # CPU oracle port of the reference path
+
+Prints one JSON line (rank 0).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "quantized-KV decode attention HBM GB/s (% of peak); decode tokens/sec at 1/2/4/8 GPU"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def unit_bytes(wl, Tq, Tp, pool_rows, ref_accounting=False):
+    """Algorithmic HBM bytes one attend launch reads/writes per (batch, kv-head)
+    unit: codes + params + full-precision tiers + q/out."""
+    d, G = wl.head_dim, wl.group_size
+    codes = 2 * Tq * d * 2 // 8
+    if ref_accounting:  # reference cache.py:188-203 accounting: params at 16 bits
+        params = (Tq // G) * d * 2 * 2 + Tq * 2 * 2
+        mask = 0
+    else:  # this build's layout: float32 (step, x_min) per line + 1 mask bit per token
+        params = (Tq // G) * d * 2 * 4 + Tq * 2 * 4
+        mask = Tq // 8
+    fp = (Tp + pool_rows) * d * 2 * 2
+    qo = 2 * wl.n_rep * d * 2
+    return codes + params + mask + fp + qo
+
+
+class Clocks:
+    """Sample nvidia-smi SM clocks and throttle reasons during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            return None
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for n, val in zip(names, f[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- CPU arm
+
+
+def cpu_sample(wl, n_units, steps, threads, seed=0):
+    """Time the reference path restated in C (oracle/, OpenMP over units) on a
+    bounded sample: n_units (layer, b, kv-head) units prefilled to the workload's
+    context, then `steps` decode steps (append + n_rep attend_mixed calls each).
+    Returns seconds per unit-step measured with all `threads` busy."""
+    import numpy as np
+
+    import oracle
+
+    rng = np.random.default_rng(seed)
+    d, T = wl.head_dim, wl.context
+    scale = np.ones((n_units, 1, d), np.float32)
+    for u in range(n_units):
+        scale[u, 0, rng.choice(d, 4, replace=False)] = 15.0
+    k = (rng.standard_normal((n_units, T, d), dtype=np.float32) * scale).astype(np.float16).astype(np.float32)
+    v = rng.standard_normal((n_units, T, d), dtype=np.float32).astype(np.float16).astype(np.float32)
+    N = wl.outlier_num
+    caches = [oracle.OracleCache(2, wl.group_size, wl.residual, N, wl.aux_capacity, d) for _ in range(n_units)]
+    oracle.prefill(caches, k, v, threads)
+    del k, v
+    times = []
+    for _ in range(steps):
+        kr = (rng.standard_normal((n_units, d), dtype=np.float32) * scale[:, 0]).astype(np.float16).astype(np.float32)
+        vr = rng.standard_normal((n_units, d), dtype=np.float32).astype(np.float16).astype(np.float32)
+        q = rng.standard_normal((n_units, wl.n_rep, d), dtype=np.float32).astype(np.float16).astype(np.float32)
+        t0 = time.perf_counter()
+        oracle.decode_step(caches, kr, vr, q, wl.n_rep, threads)
+        times.append(time.perf_counter() - t0)
+    return statistics.median(times) / n_units
+
+
+def run_reference(args, wl, rank, world):
+    if rank != 0:
+        return
+    threads = len(os.sched_getaffinity(0))
+    n_units = max(threads, 1)
+    units_per_step = wl.n_layers * wl.batch * wl.n_kv_heads
+    per_unit = cpu_sample(wl, n_units, args.warmup + args.steps, threads)
+    step_s = per_unit * units_per_step
+    tok_s = wl.batch / step_s
+    sample = (f"{n_units} (layer,b,kv-head) units prefilled to T={wl.context}, {args.warmup + args.steps} decode "
+              f"steps each (append + {wl.n_rep} attend_mixed), extrapolated x{units_per_step / n_units:.0f} to the "
+              f"full step")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": tok_s, "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64 params / f32 attention", "data": "synthetic",
+        "config": {"workload": wl.name, "layers": wl.n_layers, "batch": wl.batch, "context": wl.context},
+        "cpu_baseline": {"value": tok_s, "unit": "tokens/s", "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": tok_s, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU arm
+
+
+def run_ours(args, wl, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2505_10938_b200 import EngineConfig, OTTCache
+    from paper_2505_10938_b200.workloads import decode_rows, fill_prefill
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    if wl.batch % world:
+        raise SystemExit(f"batch {wl.batch} not divisible by world size {world}")
+    B = wl.batch // world  # whole sequences per rank (batch x kv-head partitioning)
+    H, Hq, d, L = wl.n_kv_heads, wl.n_q_heads, wl.head_dim, wl.n_layers
+    cfg = EngineConfig(bits=2, group_size=wl.group_size, residual=wl.residual, outlier_num=wl.outlier_num,
+                       aux_capacity=wl.aux_capacity, skip_layers=wl.skip_layers, n_layers=L, n_heads=H, head_dim=d)
+    total_steps = 2 * (args.warmup + args.steps) + 8
+    max_tokens = wl.context + total_steps
+    caches = [OTTCache(cfg, B, H, max_tokens, layer=l, device=dev) for l in range(L)]
+    gen = torch.Generator(device=dev).manual_seed(1000 + rank)
+    t0 = time.time()
+    kbuf = torch.empty((B, H, wl.context, d), dtype=torch.float16, device=dev)
+    vbuf = torch.empty_like(kbuf)
+    scales = []
+    for l in range(L):
+        scales.append(fill_prefill(gen, kbuf, vbuf))
+        caches[l].update(kbuf, vbuf)
+    torch.cuda.synchronize()
+    del kbuf, vbuf
+    torch.cuda.empty_cache()
+    prefill_s = time.time() - t0
+
+    n_sets = 2
+    kin = torch.empty((n_sets, L, B, H, d), dtype=torch.float16, device=dev)
+    vin = torch.empty_like(kin)
+    for s in range(n_sets):
+        for l in range(L):
+            kin[s, l], vin[s, l] = decode_rows(gen, scales[l], B, H)
+    qin = torch.randn((n_sets, L, B, Hq, d), generator=gen, device=dev).half()
+    outs = torch.empty((L, B, Hq, d), dtype=torch.float16, device=dev)
+    gathered = torch.empty((L, wl.batch, Hq, d), dtype=torch.float16, device=dev) if world > 1 else None
+    splits = [c.splits(wl.n_rep) for c in caches]
+
+    launches = {"n": 0}
+
+    def step(i, ev=None):
+        s = i % n_sets
+        for l in range(L):
+            c = caches[l]
+            before = c.quantized_tokens
+            c.append(kin[s, l], vin[s, l])
+            launches["n"] += 1 + (1 if c.quantized_tokens != before else 0)
+            if ev is not None:
+                ev[l][0].record()
+            c.attend(qin[s, l], out=outs[l], n_splits=splits[l])
+            if ev is not None:
+                ev[l][1].record()
+            launches["n"] += 2
+            if gathered is not None:
+                dist.all_gather_into_tensor(gathered[l], outs[l])
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = Clocks(local_rank)
+    clocks.start()
+    time.sleep(0.3)
+    launches["n"] = 0
+    evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(L)] for _ in range(args.steps)]
+    tok_before = [(c.quantized_tokens, c.total_tokens) for c in caches]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    start.record()
+    for i in range(args.steps):
+        step(args.warmup + i, evs[i])
+    end.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = start.elapsed_time(end)
+    ms_t = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    ms_per_step = ms / args.steps
+    value = wl.batch * args.steps / (ms / 1e3)  # whole-job decode tokens/s (all ranks)
+
+    # roofline of the dominant kernel (attention), algorithmic bytes per launch
+    att_ms, att_bytes, att_bytes_ref = 0.0, 0, 0
+    for i in range(args.steps):
+        for l in range(L):
+            att_ms += evs[i][l][0].elapsed_time(evs[i][l][1])
+    n_att = args.steps * L
+    for l, c in enumerate(caches):
+        q0, t0_ = tok_before[l]
+        for i in range(args.steps):
+            T = t0_ + i + 1
+            Tq = ((T - wl.residual) // wl.group_size) * wl.group_size if T >= wl.residual + wl.group_size else 0
+            Tq = max(Tq, q0)
+            pool_rows = min(c.N, Tq)
+            att_bytes += B * H * unit_bytes(wl, Tq, T - Tq, pool_rows)
+            att_bytes_ref += B * H * unit_bytes(wl, Tq, T - Tq, pool_rows, ref_accounting=True)
+    avg_att_s = att_ms / n_att / 1e3
+    achieved = att_bytes / n_att / avg_att_s / 1e9
+    peak, peak_kind = peaks()
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_attention_summary.json")) as f:
+            prof = json.load(f)
+        if prof.get("workload") == wl.name:
+            traffic = prof.get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    gpu_launches = launches["n"]
+
+    # e2e: through the public API with HOST buffers (pinned), copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        k_h = kin[0].cpu().pin_memory()
+        v_h = vin[0].cpu().pin_memory()
+        q_h = qin[0].cpu().pin_memory()
+        o_h = torch.empty((L, B, Hq, d), dtype=torch.float16).pin_memory()
+        k_d = torch.empty((B, H, d), dtype=torch.float16, device=dev)
+        v_d, q_d = torch.empty_like(k_d), torch.empty((B, Hq, d), dtype=torch.float16, device=dev)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for i in range(args.steps):
+            for l in range(L):
+                k_d.copy_(k_h[l], non_blocking=True)
+                v_d.copy_(v_h[l], non_blocking=True)
+                q_d.copy_(q_h[l], non_blocking=True)
+                caches[l].append(k_d, v_d)
+                caches[l].attend(q_d, out=outs[l], n_splits=splits[l])
+                if gathered is not None:
+                    dist.all_gather_into_tensor(gathered[l], outs[l])
+                    o_h[l].copy_(gathered[l][rank * B:(rank + 1) * B], non_blocking=True)
+                else:
+                    o_h[l].copy_(outs[l], non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        e_ms = torch.tensor([e0.elapsed_time(e1)], device=dev)
+        if world > 1:
+            dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+        h2d = L * (k_h[0].numel() + v_h[0].numel() + q_h[0].numel()) * 2
+        d2h = L * o_h[0].numel() * 2
+        e2e = {"value": wl.batch * args.steps / (float(e_ms.item()) / 1e3), "unit": "tokens/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        threads = len(os.sched_getaffinity(0))
+        n_units = threads
+        per_unit = cpu_sample(wl, n_units, 2, threads)
+        cpu_step = per_unit * L * wl.batch * H
+        cpu = {"value": wl.batch / cpu_step, "unit": "tokens/s", "cores": threads, "kind": "port",
+               "sample": f"{n_units} units prefilled to T={wl.context}, 2 decode steps (append + {wl.n_rep} "
+                         f"attend_mixed each), extrapolated to {L * wl.batch * H} units per step"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u2 codes / f32 params / f16 rows, f32 accumulate", "data": "synthetic",
+            "config": {"workload": wl.name, "layers": L, "batch": wl.batch, "n_q_heads": Hq, "n_kv_heads": H,
+                       "head_dim": d, "context": wl.context, "group_size": wl.group_size, "residual": wl.residual,
+                       "outlier_pool": wl.outlier_num, "aux_capacity": wl.aux_capacity,
+                       "skip_layers": list(wl.skip_layers), "partition": f"batch/{world} x all kv heads per rank",
+                       "l2": "working set > L2 (126 MB): %.1f GB of cache per GPU" % (
+                           sum(c.hbm_bytes() for c in caches) / 1e9),
+                       "prefill_s": round(prefill_s, 2)},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                         "kernel": "ott attend (split-K decode + combine)", "avg_launch_us": avg_att_s * 1e6,
+                         "bytes_per_launch": att_bytes / n_att,
+                         "achieved_ref_accounting_GBs": att_bytes_ref / n_att / avg_att_s / 1e9},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": gpu_launches,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=32)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    from paper_2505_10938_b200.workloads import WORKLOADS
+
+    wl = WORKLOADS[args.config]
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, wl, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    run_ours(args, wl, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -88,6 +88,10 @@ long ottref_pack_codes(const int64_t* codes, size_t count, int bits, uint8_t* ou
 
 /* quant.py:259-273 */
 void ottref_unpack_codes(const uint8_t* data, size_t count, int bits, int64_t* out) {
+  if (bits == 2) { /* fast path: 4 codes per byte, code 4j+i in bits [2i, 2i+2) of byte j */
+    for (size_t e = 0; e < count; ++e) out[e] = (data[e >> 2] >> (2 * (e & 3))) & 3;
+    return;
+  }
   for (size_t e = 0; e < count; ++e) {
     int64_t v = 0;
     for (int b = 0; b < bits; ++b) {
