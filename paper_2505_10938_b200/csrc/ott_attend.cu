@@ -1,16 +1,29 @@
 // ott_attend.cu — K2/K3: split-K flash-decoding attention over the three cache
-// tiers (attend_mixed, attention.py:79-92), CUDA-core (SIMT) variant, plus the
-// split combine and a debug logits kernel.
+// tiers (attend_mixed, attention.py:79-92) and the split combine.
 //
-// Per unit (batch b, kv head h) the token axis is cut into 32-token tiles:
-//   [0, Tq/32)               quantized tiles (codes dequantized in registers;
-//                            positions currently in pool.entries masked, they
-//                            are represented by the pool tile instead —
-//                            attention.py:73-75 overwrite semantics)
-//   next ceil(N/32) tiles    pool.entries rows (fp16, exact)
-//   next ceil(Tp/32) tiles   pending rows (fp16 ring)
-// Splits take contiguous tile ranges; each warp keeps an online softmax state
-// per query head; warps then splits are merged (log-sum-exp).
+// Per unit (batch b, kv head h) the token axis is:
+//   quantized groups  [0, Tq)   2-bit codes, dequantized in registers; positions
+//                               currently in pool.entries are masked (their
+//                               full-precision rows are attended from the pool
+//                               instead — the overwrite semantics of
+//                               attention.py:73-75, never double counted)
+//   pool.entries rows           fp16, <= N slots (empty slots masked)
+//   pending rows      [Tq, T)   fp16 ring
+//
+// Grid = (units, n_qsplits + 1): the first n_qsplits CTAs of a unit stream
+// contiguous ranges of quantized group records; the last CTA attends the
+// full-precision tiers. Each CTA writes an online-softmax partial (m, l, acc)
+// per query head; combine_kernel merges them.
+//
+// Quantized path (d = 128): tensor cores via mma.sync m16n8k16 (f16 in, f32
+// accumulate). Group records (codes + params, contiguous) are staged into
+// shared memory with TMA bulk copies (cp.async.bulk + mbarrier), 2-3 stages per
+// warp. K codes become fp16 (1 + c/4) with one shift + one LOP3 per pair; the
+// per-channel K steps are folded into q (B operand, hi/lo fp16 split so the
+// products keep ~22 bits) and K x_min (minus the exact offset) into a
+// per-(group, head) bias. V codes become exact fp16 subnormals c * 2^-16; the
+// per-token V step is folded into P' = 4 p step (fp16) and V x_min into a
+// per-head fp32 bias. See DESIGN.md §4.
 #include "ott_common.cuh"
 
 namespace ott {
@@ -18,28 +31,31 @@ namespace ott {
 constexpr int kAttnThreads = 128;
 constexpr int kAttnWarps = kAttnThreads / 32;
 constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLazy = 6.f;  // lazy-rescale threshold (log2 units): p <= 64, P' = 4 p step fits fp16
 
 struct AttnArgs {
   ott_cache_t c;
   const uint16_t* q;
   uint16_t* out;
-  float* ws;  // [n_units][NR][S][D+2]
+  float* ws;  // [n_units][NR][n_splits][D+2]
   int64_t q_tokens, total_tokens;
-  int n_splits, n_qtiles, n_ptiles, n_rtiles;
-  float scale_log2;  // log2(e) / float32(sqrt(d))
+  int n_splits;   // total partials per (unit, head) = n_qsplits + 1
+  int n_qsplits;  // splits over the quantized region
+  int n_qtiles, n_ptiles, n_rtiles;  // 32-token tiles: quantized, pool, pending
+  float scale_log2;                  // log2(e) / float32(sqrt(d))
 };
 
-// Per-warp smem scratch for one tile.
+// ============================================================ SIMT (CUDA-core) tiles
 template <int NR, int D>
 struct WarpScratch {
-  float qp[NR][D];     // q * step (quantized tiles) — folded K step
-  float p[NR][32];     // softmax numerators of the tile
+  float qp[NR][D];
+  float p[NR][32];
   uint32_t vw[32][D / 16];
   float vstep[32], vxmin[32];
 };
 
 template <int NR, int D>
-struct AttnSmem {
+struct SimtSmem {
   float qs[NR][D];  // q * scale_log2
   WarpScratch<NR, D> w[kAttnWarps];
   float m[kAttnWarps][NR], l[kAttnWarps][NR];
@@ -47,13 +63,13 @@ struct AttnSmem {
 };
 
 template <int NR, int D>
-__device__ __forceinline__ void online_update(float (&s)[NR], float (&m)[NR], float (&l)[NR], float (&acc)[NR][D / 32],
-                                              WarpScratch<NR, D>& ws, int lane) {
+__device__ __forceinline__ void online_update(float (&s)[NR], float (&m)[NR], float (&l)[NR],
+                                              float (&acc)[NR][D / 32], WarpScratch<NR, D>& ws, int lane) {
 #pragma unroll
   for (int r = 0; r < NR; ++r) {
     const float tmax = warp_max(s[r]);
     const float m_new = fmaxf(m[r], tmax);
-    if (m_new == -INFINITY) {  // whole tile masked and nothing seen yet
+    if (m_new == -INFINITY) {
       ws.p[r][lane] = 0.f;
       continue;
     }
@@ -68,25 +84,19 @@ __device__ __forceinline__ void online_update(float (&s)[NR], float (&m)[NR], fl
   __syncwarp();
 }
 
+// Processes 32-token tiles [t_begin, t_end) of unit u (warp-strided), merges
+// the warps of the CTA and writes partial `split`.
 template <int NR, int D>
-__global__ void __launch_bounds__(kAttnThreads) attend_simt_kernel(AttnArgs a) {
+__device__ void simt_body(const AttnArgs& a, int u, int t_begin, int t_end, int split, SimtSmem<NR, D>& sm) {
   const ott_cache_t& c = a.c;
-  const int u = blockIdx.x, split = blockIdx.y;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int G = c.group_size, N = c.capacity, cap = G + c.residual;
   const RecordLayout L(D, G);
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  AttnSmem<NR, D>& sm = *reinterpret_cast<AttnSmem<NR, D>*>(smem_raw);
   WarpScratch<NR, D>& ws = sm.w[warp];
 
   for (int i = tid; i < NR * D; i += kAttnThreads)
     sm.qs[i / D][i % D] = h2f(a.q[((size_t)u * NR) * D + i]) * a.scale_log2;
   __syncthreads();
-
-  const int n_tiles = a.n_qtiles + a.n_ptiles + a.n_rtiles;
-  const int per = (n_tiles + a.n_splits - 1) / a.n_splits;
-  const int t_begin = split * per;
-  const int t_end = min(n_tiles, t_begin + per);
 
   float m[NR], l[NR], acc[NR][D / 32];
 #pragma unroll
@@ -97,13 +107,10 @@ __global__ void __launch_bounds__(kAttnThreads) attend_simt_kernel(AttnArgs a) {
     for (int k = 0; k < D / 32; ++k) acc[r][k] = 0.f;
   }
   const uint32_t* pmask = c.pool_mask + (size_t)u * mask_words_per_unit(c);
-  const int n_entries = N > 0 ? c.pool_meta[(size_t)u * 4] : 0;
-  (void)n_entries;
 
   for (int t = t_begin + warp; t < t_end; t += kAttnWarps) {
     float s[NR];
     if (t < a.n_qtiles) {
-      // ---------------- quantized tile: 32 tokens of one group
       const int64_t tok0 = (int64_t)t * 32;
       const int64_t gi = tok0 / G;
       const int row0 = (int)(tok0 - gi * G);
@@ -123,7 +130,6 @@ __global__ void __launch_bounds__(kAttnThreads) attend_simt_kernel(AttnArgs a) {
       }
 #pragma unroll
       for (int r = 0; r < NR; ++r) bias[r] = warp_sum(bias[r]);
-      // V codes / params of this tile into warp smem
       const uint32_t* vcw = reinterpret_cast<const uint32_t*>(rec + L.v_codes()) + (size_t)row0 * (D / 16);
 #pragma unroll
       for (int j = 0; j < D / 16; ++j) {
@@ -133,7 +139,6 @@ __global__ void __launch_bounds__(kAttnThreads) attend_simt_kernel(AttnArgs a) {
       ws.vstep[lane] = reinterpret_cast<const float*>(rec + L.v_step())[row0 + lane];
       ws.vxmin[lane] = reinterpret_cast<const float*>(rec + L.v_xmin())[row0 + lane];
       __syncwarp();
-      // logits, lane = token
       const uint32_t* kcw = reinterpret_cast<const uint32_t*>(rec + L.k_codes()) + (size_t)(row0 + lane) * (D / 16);
 #pragma unroll
       for (int r = 0; r < NR; ++r) s[r] = bias[r];
@@ -153,7 +158,6 @@ __global__ void __launch_bounds__(kAttnThreads) attend_simt_kernel(AttnArgs a) {
         for (int r = 0; r < NR; ++r) s[r] = -INFINITY;
       }
       online_update<NR, D>(s, m, l, acc, ws, lane);
-      // P . V with V dequantized per token: v = code*step_t + xmin_t
 #pragma unroll 4
       for (int tt = 0; tt < 32; ++tt) {
         const float st = ws.vstep[tt], mn = ws.vxmin[tt];
@@ -167,7 +171,6 @@ __global__ void __launch_bounds__(kAttnThreads) attend_simt_kernel(AttnArgs a) {
       }
       __syncwarp();
     } else {
-      // ---------------- full-precision tile: pool entries or pending rows
       const bool is_pool = t < a.n_qtiles + a.n_ptiles;
       const uint16_t *krow, *vrow;
       bool valid;
@@ -203,7 +206,6 @@ __global__ void __launch_bounds__(kAttnThreads) attend_simt_kernel(AttnArgs a) {
         for (int r = 0; r < NR; ++r) s[r] = -INFINITY;
       }
       online_update<NR, D>(s, m, l, acc, ws, lane);
-      // P . V: lane owns channels lane + 32k; row pointers broadcast per token
       for (int tt = 0; tt < 32; ++tt) {
         const unsigned long long vp = __shfl_sync(0xffffffffu, (unsigned long long)vrow, tt);
         const int ok = __shfl_sync(0xffffffffu, valid ? 1 : 0, tt);
@@ -220,7 +222,6 @@ __global__ void __launch_bounds__(kAttnThreads) attend_simt_kernel(AttnArgs a) {
     }
   }
 
-  // ---- merge warps of this CTA, write the split partial
   if (lane == 0) {
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
@@ -256,7 +257,358 @@ __global__ void __launch_bounds__(kAttnThreads) attend_simt_kernel(AttnArgs a) {
   }
 }
 
-// K3: merge split partials -> fp16 output. One CTA per (unit, head).
+template <int NR, int D>
+__global__ void __launch_bounds__(kAttnThreads) attend_simt_kernel(AttnArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SimtSmem<NR, D>& sm = *reinterpret_cast<SimtSmem<NR, D>*>(smem_raw);
+  const int n_tiles = a.n_qtiles + a.n_ptiles + a.n_rtiles;
+  const int per = (n_tiles + a.n_splits - 1) / a.n_splits;
+  const int t_begin = blockIdx.y * per;
+  const int t_end = min(n_tiles, t_begin + per);
+  simt_body<NR, D>(a, blockIdx.x, t_begin, t_end, blockIdx.y, sm);
+}
+
+// ============================================================ tensor-core path
+__device__ __forceinline__ void mma16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                         uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};\n"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], uint32_t saddr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(saddr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t (&r)[4], uint32_t saddr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(saddr));
+}
+__device__ __forceinline__ uint32_t movm_t(uint32_t x) {
+  uint32_t y;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;\n" : "=r"(y) : "r"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t pack_h2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;\n" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+// 2-bit code pair at bits (2m, 2m+16) -> half2 (1 + c/4) in each half.
+template <int M>
+__device__ __forceinline__ uint32_t dq(uint32_t w) {
+  uint32_t x;
+  if constexpr (M < 4) x = w << (8 - 2 * M);
+  else if constexpr (M == 4) x = w;
+  else x = w >> (2 * M - 8);
+  return (x & 0x03000300u) | 0x3C003C00u;
+}
+// Same pair as fp16 SUBNORMALS c * 2^-16 (exact, no offset): used for V so the
+// fp16 rounding of P' only scales each token's own contribution.
+template <int M>
+__device__ __forceinline__ uint32_t dqv(uint32_t w) {
+  uint32_t x;
+  if constexpr (M < 4) x = w << (8 - 2 * M);
+  else if constexpr (M == 4) x = w;
+  else x = w >> (2 * M - 8);
+  return x & 0x03000300u;
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(phase)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void tma_bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
+template <int G>
+struct MmaSmem {
+  static constexpr int kRec = G * 128 / 2 + 8 * 128 + 8 * G;  // record bytes at d = 128
+  static constexpr int kStages = G == 32 ? 3 : 2;             // TMA pipeline depth per warp
+  float q4[8][128];                                          // q * 4 * scale_log2, heads padded to 8
+  float esc[kAttnWarps][128];                                // x_min - 4*step per channel (current group)
+  alignas(128) uint8_t stage[kAttnWarps][kStages][kRec];
+  alignas(8) uint64_t bar[kAttnWarps][kStages];
+  float mm[kAttnWarps][8], ll[kAttnWarps][8];
+};
+
+// Quantized-region partial for (unit blockIdx.x, split blockIdx.y < n_qsplits).
+template <int NR, int G>
+__device__ void mma_body(const AttnArgs& a, MmaSmem<G>& sm) {
+  constexpr int D = 128;
+  constexpr int kRec = MmaSmem<G>::kRec;
+  constexpr int kMt = G / 16;  // 16-token m-tiles per group
+  constexpr int kStages = MmaSmem<G>::kStages;
+  const RecordLayout L(D, G);
+  const ott_cache_t& c = a.c;
+  const int u = blockIdx.x, split = blockIdx.y;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, tig = lane & 3;
+
+  const int n_groups = (int)(a.q_tokens / G);
+  const int per = (n_groups + a.n_qsplits - 1) / a.n_qsplits;
+  const int g0 = split * per;
+  const int g1 = min(n_groups, g0 + per);
+  const int my_n = g1 > g0 + warp ? (g1 - g0 - warp + kAttnWarps - 1) / kAttnWarps : 0;
+
+  for (int i = tid; i < 8 * D; i += kAttnThreads) {
+    const int h = i / D;
+    sm.q4[h][i % D] = h < NR ? h2f(a.q[((size_t)u * NR + h) * D + (i % D)]) * (4.f * a.scale_log2) : 0.f;
+  }
+  const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&sm.bar[warp][0]);
+  const uint32_t stage0 = (uint32_t)__cvta_generic_to_shared(&sm.stage[warp][0][0]);
+  const uint8_t* unit_rec = c.blocks + (size_t)u * c.max_groups * kRec;
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < kStages; ++s) mbar_init(bar0 + 8 * s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+#pragma unroll
+    for (int s = 0; s < kStages; ++s)
+      if (s < my_n)
+        tma_bulk_load(stage0 + s * kRec, unit_rec + (size_t)(g0 + warp + s * kAttnWarps) * kRec, kRec, bar0 + 8 * s);
+  }
+  __syncthreads();
+
+  float o[8][4];
+#pragma unroll
+  for (int cm = 0; cm < 8; ++cm) o[cm][0] = o[cm][1] = o[cm][2] = o[cm][3] = 0.f;
+  float mrun[2] = {-INFINITY, -INFINITY}, lsum[2] = {0.f, 0.f}, vb[2] = {0.f, 0.f};
+  const uint32_t* pmask = c.pool_mask + (size_t)u * mask_words_per_unit(c);
+  float* esc = sm.esc[warp];
+
+  // ldmatrix row addresses (bytes, relative to a 16-token tile): matrix i = lane/8,
+  // row r = lane%8: i0 tokens 0-7 bytes 0-15, i1 tokens 8-15 bytes 0-15,
+  // i2 tokens 0-7 bytes 16-31, i3 tokens 8-15 bytes 16-31.
+  const uint32_t lm_off = (uint32_t)(((lane & 7) + ((lane >> 3) & 1) * 8) * 32 + (lane >> 4) * 16);
+
+  for (int k = 0; k < my_n; ++k) {
+    const int s = k % kStages;
+    const int gi = g0 + warp + k * kAttnWarps;
+    mbar_wait(bar0 + 8 * s, (uint32_t)((k / kStages) & 1));
+    const uint8_t* rec = &sm.stage[warp][s][0];
+    const uint32_t rec_s = stage0 + s * kRec;
+    const float* kstep = reinterpret_cast<const float*>(rec + L.k_step());
+    const float* kxmin = reinterpret_cast<const float*>(rec + L.k_xmin());
+    const float* vstep = reinterpret_cast<const float*>(rec + L.v_step());
+    const float* vxmin = reinterpret_cast<const float*>(rec + L.v_xmin());
+
+    // ---- per-channel e = x_min - 4*step (shared by the 8 head-rows of the warp)
+    {
+      const float4 st = *reinterpret_cast<const float4*>(kstep + 4 * lane);
+      const float4 mn = *reinterpret_cast<const float4*>(kxmin + 4 * lane);
+      *reinterpret_cast<float4*>(esc + 4 * lane) =
+          make_float4(fmaf(-4.f, st.x, mn.x), fmaf(-4.f, st.y, mn.y), fmaf(-4.f, st.z, mn.z), fmaf(-4.f, st.w, mn.w));
+    }
+    __syncwarp();
+
+    // ---- B operand (q' = 4*scale*q*step, hi/lo fp16) and K bias for head g
+    uint32_t bh[2][8], bl[2][8];
+    float bias = 0.f;
+#pragma unroll
+    for (int hw = 0; hw < 2; ++hw) {
+      const int ch0 = 16 * (tig + 4 * hw);
+      float qv[16], sv[16], ev[16];
+#pragma unroll
+      for (int v4 = 0; v4 < 4; ++v4) {
+        const float4 q4 = *reinterpret_cast<const float4*>(&sm.q4[g][ch0 + 4 * v4]);
+        const float4 s4 = *reinterpret_cast<const float4*>(kstep + ch0 + 4 * v4);
+        const float4 e4 = *reinterpret_cast<const float4*>(esc + ch0 + 4 * v4);
+        qv[4 * v4] = q4.x; qv[4 * v4 + 1] = q4.y; qv[4 * v4 + 2] = q4.z; qv[4 * v4 + 3] = q4.w;
+        sv[4 * v4] = s4.x; sv[4 * v4 + 1] = s4.y; sv[4 * v4 + 2] = s4.z; sv[4 * v4 + 3] = s4.w;
+        ev[4 * v4] = e4.x; ev[4 * v4 + 1] = e4.y; ev[4 * v4 + 2] = e4.z; ev[4 * v4 + 3] = e4.w;
+      }
+#pragma unroll
+      for (int m = 0; m < 8; ++m) {
+        const float B0 = qv[m] * sv[m], B1 = qv[m + 8] * sv[m + 8];
+        const float h0 = __uint_as_float(__float_as_uint(B0) & 0xFFFFE000u);
+        const float h1 = __uint_as_float(__float_as_uint(B1) & 0xFFFFE000u);
+        bh[hw][m] = pack_h2(h0, h1);
+        bl[hw][m] = pack_h2(B0 - h0, B1 - h1);
+        bias = fmaf(qv[m], ev[m], bias);
+        bias = fmaf(qv[m + 8], ev[m + 8], bias);
+      }
+    }
+    bias += __shfl_xor_sync(0xffffffffu, bias, 1);
+    bias += __shfl_xor_sync(0xffffffffu, bias, 2);
+    bias *= 0.25f;
+    const float bias0 = __shfl_sync(0xffffffffu, bias, 8 * tig);      // head 2*tig
+    const float bias1 = __shfl_sync(0xffffffffu, bias, 8 * tig + 4);  // head 2*tig+1
+
+    // ---- S = Q K^T for the group's m-tiles
+    float sc[kMt][4];
+#pragma unroll
+    for (int mt = 0; mt < kMt; ++mt) {
+      uint32_t kw[4];
+      ldsm_x4(kw, rec_s + L.k_codes() + mt * 16 * 32 + lm_off);
+      float cc[4] = {bias0, bias1, bias0, bias1};
+#define OTT_QK_SLICE(HW, MM)                                                                          \
+  {                                                                                                   \
+    const uint32_t a0 = dq<MM>(kw[2 * HW]), a1 = dq<MM>(kw[2 * HW + 1]);                              \
+    const uint32_t a2 = dq<MM + 1>(kw[2 * HW]), a3 = dq<MM + 1>(kw[2 * HW + 1]);                      \
+    mma16816(cc, a0, a1, a2, a3, bh[HW][MM], bh[HW][MM + 1]);                                         \
+    mma16816(cc, a0, a1, a2, a3, bl[HW][MM], bl[HW][MM + 1]);                                         \
+  }
+      OTT_QK_SLICE(0, 0) OTT_QK_SLICE(0, 2) OTT_QK_SLICE(0, 4) OTT_QK_SLICE(0, 6)
+      OTT_QK_SLICE(1, 0) OTT_QK_SLICE(1, 2) OTT_QK_SLICE(1, 4) OTT_QK_SLICE(1, 6)
+#undef OTT_QK_SLICE
+      sc[mt][0] = cc[0];
+      sc[mt][1] = cc[1];
+      sc[mt][2] = cc[2];
+      sc[mt][3] = cc[3];
+    }
+    // pooled positions: their logits come from the pool tile (overwrite semantics)
+#pragma unroll
+    for (int w = 0; w < G / 32; ++w) {
+      const uint32_t mw = __ldg(&pmask[(size_t)gi * (G / 32) + w]);
+      if (mw) {
+#pragma unroll
+        for (int mt = 2 * w; mt < 2 * w + 2; ++mt) {
+          if ((mw >> ((mt & 1) * 16 + g)) & 1u) sc[mt][0] = sc[mt][1] = -INFINITY;
+          if ((mw >> ((mt & 1) * 16 + g + 8)) & 1u) sc[mt][2] = sc[mt][3] = -INFINITY;
+        }
+      }
+    }
+
+    // ---- online softmax (heads 2*tig, 2*tig+1), lazily rescaled: the running max
+    // only moves when a logit exceeds it by kLazy (log2 units), so p <= 2^kLazy
+    float tmax[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      float t = -INFINITY;
+#pragma unroll
+      for (int mt = 0; mt < kMt; ++mt) t = fmaxf(t, fmaxf(sc[mt][h], sc[mt][h + 2]));
+      t = fmaxf(t, __shfl_xor_sync(0xffffffffu, t, 4));
+      t = fmaxf(t, __shfl_xor_sync(0xffffffffu, t, 8));
+      t = fmaxf(t, __shfl_xor_sync(0xffffffffu, t, 16));
+      tmax[h] = t;
+    }
+    const bool need = tmax[0] > mrun[0] + kLazy || tmax[1] > mrun[1] + kLazy;
+    if (__any_sync(0xffffffffu, need)) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const float mnew = fmaxf(mrun[h], tmax[h]);
+        const float corr = mnew == -INFINITY ? 1.f : exp2f(mrun[h] - mnew);
+        lsum[h] *= corr;
+        vb[h] *= corr;
+#pragma unroll
+        for (int cm = 0; cm < 8; ++cm) {
+          o[cm][h] *= corr;
+          o[cm][h + 2] *= corr;
+        }
+        mrun[h] = mnew;
+      }
+    }
+    const float me0 = mrun[0] == -INFINITY ? 0.f : mrun[0];
+    const float me1 = mrun[1] == -INFINITY ? 0.f : mrun[1];
+
+    // ---- O^T += V^T P'  (V step folded into P' = 4 p step, V x_min into vb;
+    // with codes as c * 2^-16 the accumulator holds sum(p step c) * 2^-14)
+#pragma unroll
+    for (int mt = 0; mt < kMt; ++mt) {
+      const float vs0 = vstep[mt * 16 + g], vs1 = vstep[mt * 16 + g + 8];
+      const float ve0 = vxmin[mt * 16 + g], ve1 = vxmin[mt * 16 + g + 8];
+      const float p00 = exp2f(sc[mt][0] - me0), p01 = exp2f(sc[mt][1] - me1);
+      const float p10 = exp2f(sc[mt][2] - me0), p11 = exp2f(sc[mt][3] - me1);
+      lsum[0] += p00 + p10;
+      lsum[1] += p01 + p11;
+      vb[0] = fmaf(p00, ve0, fmaf(p10, ve1, vb[0]));
+      vb[1] = fmaf(p01, ve0, fmaf(p11, ve1, vb[1]));
+      const float f0 = 4.f * vs0, f1 = 4.f * vs1;
+      const uint32_t b0 = movm_t(pack_h2(p00 * f0, p01 * f0));
+      const uint32_t b1 = movm_t(pack_h2(p10 * f1, p11 * f1));
+      uint32_t vr[4];
+      ldsm_x4_t(vr, rec_s + L.v_codes() + mt * 16 * 32 + lm_off);
+#define OTT_PV(CM) mma16816(o[CM], dqv<CM>(vr[0]), dqv<CM>(vr[2]), dqv<CM>(vr[1]), dqv<CM>(vr[3]), b0, b1);
+      OTT_PV(0) OTT_PV(1) OTT_PV(2) OTT_PV(3) OTT_PV(4) OTT_PV(5) OTT_PV(6) OTT_PV(7)
+#undef OTT_PV
+    }
+
+    __syncwarp();
+    if (lane == 0 && k + kStages < my_n) {
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      tma_bulk_load(rec_s, unit_rec + (size_t)(gi + kStages * kAttnWarps) * kRec, kRec, bar0 + 8 * s);
+    }
+  }
+
+  // ---- reduce l, vb over the token rows (lanes with equal tig), merge warps
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+#pragma unroll
+    for (int off = 4; off < 32; off <<= 1) {
+      lsum[h] += __shfl_xor_sync(0xffffffffu, lsum[h], off);
+      vb[h] += __shfl_xor_sync(0xffffffffu, vb[h], off);
+    }
+  }
+  if (g == 0) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      sm.mm[warp][2 * tig + h] = mrun[h];
+      sm.ll[warp][2 * tig + h] = lsum[h];
+    }
+  }
+  __syncthreads();  // every warp is past its loop: stage memory is free
+  float* accw = reinterpret_cast<float*>(&sm.stage[warp][0][0]);  // [8 heads][128] natural channel order
+#pragma unroll
+  for (int cm = 0; cm < 8; ++cm) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      accw[(2 * tig + h) * D + 8 * g + cm] = fmaf(o[cm][h], 16384.f, vb[h]);
+      accw[(2 * tig + h) * D + 64 + 8 * g + cm] = fmaf(o[cm][h + 2], 16384.f, vb[h]);
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < NR * D; i += kAttnThreads) {
+    const int r = i / D, col = i % D;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < kAttnWarps; ++w) M = fmaxf(M, sm.mm[w][r]);
+    float Lsum = 0.f, A = 0.f;
+    if (M != -INFINITY) {
+#pragma unroll
+      for (int w = 0; w < kAttnWarps; ++w) {
+        if (sm.mm[w][r] == -INFINITY) continue;
+        const float f = exp2f(sm.mm[w][r] - M);
+        Lsum += sm.ll[w][r] * f;
+        A += reinterpret_cast<const float*>(&sm.stage[w][0][0])[r * D + col] * f;
+      }
+    }
+    float* base = a.ws + (((size_t)u * NR + r) * a.n_splits + split) * (D + 2);
+    base[2 + col] = A;
+    if (col == 0) {
+      base[0] = M;
+      base[1] = Lsum;
+    }
+  }
+}
+
+template <int NR, int G>
+__global__ void __launch_bounds__(kAttnThreads) attend_mma_kernel(AttnArgs a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  if ((int)blockIdx.y == a.n_qsplits) {  // full-precision tiers: pool.entries + pending window
+    const int t0 = a.n_qtiles, t1 = a.n_qtiles + a.n_ptiles + a.n_rtiles;
+    simt_body<NR, 128>(a, blockIdx.x, t0, t1, blockIdx.y, *reinterpret_cast<SimtSmem<NR, 128>*>(smem_raw));
+  } else {
+    mma_body<NR, G>(a, *reinterpret_cast<MmaSmem<G>*>(smem_raw));
+  }
+}
+
+// ============================================================ combine + debug logits
 template <int D>
 __global__ void combine_kernel(const float* __restrict__ ws, uint16_t* __restrict__ out, int n_splits) {
   const int ur = blockIdx.x;  // unit*NR + r
@@ -276,7 +628,6 @@ __global__ void combine_kernel(const float* __restrict__ ws, uint16_t* __restric
   }
 }
 
-// Debug K: reference logits (attention.py:55) for every position.
 template <int D>
 __global__ void logits_kernel(ott_cache_t c, const uint16_t* __restrict__ q, float* __restrict__ logits, int NR,
                               int64_t q_tokens, int64_t total, float inv_sqrt_d) {
@@ -316,22 +667,38 @@ __global__ void logits_kernel(ott_cache_t c, const uint16_t* __restrict__ q, flo
   }
 }
 
+// ============================================================ launchers
 template <int NR, int D>
-static cudaError_t launch_attend_t(const AttnArgs& a, cudaStream_t st) {
-  const size_t smem = sizeof(AttnSmem<NR, D>);
+static cudaError_t launch_simt_t(const AttnArgs& a, cudaStream_t st) {
+  const size_t smem = sizeof(SimtSmem<NR, D>);
   cudaError_t e = cudaFuncSetAttribute(attend_simt_kernel<NR, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
-  dim3 grid(a.c.n_units, a.n_splits);
-  attend_simt_kernel<NR, D><<<grid, kAttnThreads, smem, st>>>(a);
+  attend_simt_kernel<NR, D><<<dim3(a.c.n_units, a.n_splits), kAttnThreads, smem, st>>>(a);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   combine_kernel<D><<<a.c.n_units * NR, D, 0, st>>>(a.ws, a.out, a.n_splits);
   return cudaGetLastError();
 }
 
+template <int NR, int G>
+static cudaError_t launch_mma_t(const AttnArgs& a, cudaStream_t st) {
+  const size_t smem = sizeof(MmaSmem<G>) > sizeof(SimtSmem<NR, 128>) ? sizeof(MmaSmem<G>)
+                                                                       : sizeof(SimtSmem<NR, 128>);
+  cudaError_t e =
+      cudaFuncSetAttribute(attend_mma_kernel<NR, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  attend_mma_kernel<NR, G><<<dim3(a.c.n_units, a.n_splits), kAttnThreads, smem, st>>>(a);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  combine_kernel<128><<<a.c.n_units * NR, 128, 0, st>>>(a.ws, a.out, a.n_splits);
+  return cudaGetLastError();
+}
+
+bool mma_eligible(const ott_cache_t& c) { return c.head_dim == 128; }
+
 cudaError_t launch_attend(const ott_cache_t& c, const uint16_t* q, uint16_t* out, int n_rep, int64_t q_tokens,
-                          int64_t total, float* ws, int n_splits, cudaStream_t st) {
+                          int64_t total, float* ws, int n_qsplits, cudaStream_t st) {
   AttnArgs a;
   a.c = c;
   a.q = q;
@@ -339,15 +706,24 @@ cudaError_t launch_attend(const ott_cache_t& c, const uint16_t* q, uint16_t* out
   a.ws = ws;
   a.q_tokens = q_tokens;
   a.total_tokens = total;
-  a.n_splits = n_splits;
+  a.n_qsplits = n_qsplits;
+  a.n_splits = n_qsplits + 1;
   a.n_qtiles = (int)(q_tokens / 32);
   a.n_ptiles = (c.capacity + 31) / 32;
   a.n_rtiles = (int)((total - q_tokens + 31) / 32);
   a.scale_log2 = kLog2e / sqrtf((float)c.head_dim);
-  const int D = c.head_dim;
+  const int D = c.head_dim, G = c.group_size;
+  if (mma_eligible(c)) {
+#define OTT_MCASE(NRv, Gv) \
+  if (n_rep == NRv && G == Gv) return launch_mma_t<NRv, Gv>(a, st);
+    OTT_MCASE(1, 32) OTT_MCASE(2, 32) OTT_MCASE(4, 32) OTT_MCASE(8, 32)
+    OTT_MCASE(1, 64) OTT_MCASE(2, 64) OTT_MCASE(4, 64) OTT_MCASE(8, 64)
+    OTT_MCASE(1, 128) OTT_MCASE(2, 128) OTT_MCASE(4, 128) OTT_MCASE(8, 128)
+#undef OTT_MCASE
+    return cudaErrorInvalidValue;
+  }
 #define OTT_CASE(NRv, Dv) \
-  if (n_rep == NRv && D == Dv) return launch_attend_t<NRv, Dv>(a, st);
-  OTT_CASE(1, 128) OTT_CASE(2, 128) OTT_CASE(4, 128) OTT_CASE(8, 128)
+  if (n_rep == NRv && D == Dv) return launch_simt_t<NRv, Dv>(a, st);
   OTT_CASE(1, 64) OTT_CASE(2, 64) OTT_CASE(4, 64) OTT_CASE(8, 64)
 #undef OTT_CASE
   return cudaErrorInvalidValue;

@@ -92,19 +92,23 @@ int ott_num_sms(void) {
   return n;
 }
 
+// n_splits = number of splits of the quantized region; the kernels add one more
+// partial per (unit, head) for the full-precision tiers (pool + pending).
 int ott_pick_splits(const ott_cache_t* c, int32_t n_rep, int64_t total_tokens) {
   (void)n_rep;
   if (!c || c->n_units < 1) return 1;
   const int64_t q_tokens = total_tokens >= c->residual + c->group_size
                                ? ((total_tokens - c->residual) / c->group_size) * c->group_size
                                : 0;
-  const int64_t n_tiles = q_tokens / 32 + (c->capacity + 31) / 32 + (total_tokens - q_tokens + 31) / 32 + 1;
+  const int64_t n_groups = q_tokens / c->group_size;
   int sms = ott_num_sms();
   if (sms <= 0) sms = 148;
-  const int64_t target = (int64_t)sms * 4;
+  // ~24 CTAs of 4 warps per SM over the launch keeps the tail short (CTAs are
+  // scheduled dynamically) while each split streams >= 8 groups (2 per warp).
+  const int64_t target = (int64_t)sms * 24;
   int64_t s = (target + c->n_units - 1) / c->n_units;
-  const int64_t max_by_tiles = n_tiles / 8 > 0 ? n_tiles / 8 : 1;  // >= 8 tiles (2 per warp) per split
-  if (s > max_by_tiles) s = max_by_tiles;
+  const int64_t max_by_groups = n_groups / 8 > 0 ? n_groups / 8 : 1;
+  if (s > max_by_groups) s = max_by_groups;
   if (s > 64) s = 64;
   if (s < 1) s = 1;
   return (int)s;
@@ -112,7 +116,7 @@ int ott_pick_splits(const ott_cache_t* c, int32_t n_rep, int64_t total_tokens) {
 
 size_t ott_attend_workspace_floats(const ott_cache_t* c, int32_t n_rep, int32_t n_splits) {
   if (!c) return 0;
-  return (size_t)c->n_units * n_rep * (n_splits > 0 ? n_splits : 1) * (c->head_dim + 2);
+  return (size_t)c->n_units * n_rep * ((n_splits > 0 ? n_splits : 1) + 1) * (c->head_dim + 2);
 }
 
 int ott_attend(const ott_cache_t* c, const uint16_t* q, uint16_t* out, int32_t n_rep, int64_t quantized_tokens,
