@@ -13,7 +13,7 @@ import subprocess
 from .errors import ContractViolation, NativeError
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "_lib", "libott_b200.so")
+LIB_PATH = os.environ.get("OTT_LIB_PATH") or os.path.join(_PKG, "_lib", "libott_b200.so")
 CSRC = os.path.join(_PKG, "csrc")
 
 OTT_OK, OTT_ERR_CONTRACT, OTT_ERR_UNSUPPORTED, OTT_ERR_CUDA = 0, 1, 2, 3

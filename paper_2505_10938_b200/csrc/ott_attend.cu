@@ -28,6 +28,9 @@
 
 namespace ott {
 
+#ifndef OTT_MMA_MIN_BLOCKS
+#define OTT_MMA_MIN_BLOCKS 4
+#endif
 constexpr int kAttnThreads = 128;
 constexpr int kAttnWarps = kAttnThreads / 32;
 constexpr float kLog2e = 1.4426950408889634f;
@@ -43,6 +46,8 @@ struct AttnArgs {
   int n_qsplits;  // splits over the quantized region
   int n_qtiles, n_ptiles, n_rtiles;  // 32-token tiles: quantized, pool, pending
   float scale_log2;                  // log2(e) / float32(sqrt(d))
+  uint32_t k_magic;                  // 0x3C003C00 (fp16 1.0 pair), passed at run time so the
+                                     // compiler keeps it in a register: one LOP3 per code pair
 };
 
 // ============================================================ SIMT (CUDA-core) tiles
@@ -259,7 +264,7 @@ __device__ void simt_body(const AttnArgs& a, int u, int t_begin, int t_end, int 
 
 template <int NR, int D>
 __global__ void __launch_bounds__(kAttnThreads) attend_simt_kernel(AttnArgs a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   SimtSmem<NR, D>& sm = *reinterpret_cast<SimtSmem<NR, D>*>(smem_raw);
   const int n_tiles = a.n_qtiles + a.n_ptiles + a.n_rtiles;
   const int per = (n_tiles + a.n_splits - 1) / a.n_splits;
@@ -287,6 +292,11 @@ __device__ __forceinline__ void ldsm_x4_t(uint32_t (&r)[4], uint32_t saddr) {
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
                : "r"(saddr));
 }
+__device__ __forceinline__ float ex2(float x) {  // 2^x, MUFU.EX2 (ftz; -inf -> 0)
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;\n" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ uint32_t movm_t(uint32_t x) {
   uint32_t y;
   asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;\n" : "=r"(y) : "r"(x));
@@ -296,25 +306,6 @@ __device__ __forceinline__ uint32_t pack_h2(float lo, float hi) {
   uint32_t r;
   asm("cvt.rn.f16x2.f32 %0, %1, %2;\n" : "=r"(r) : "f"(hi), "f"(lo));
   return r;
-}
-// 2-bit code pair at bits (2m, 2m+16) -> half2 (1 + c/4) in each half.
-template <int M>
-__device__ __forceinline__ uint32_t dq(uint32_t w) {
-  uint32_t x;
-  if constexpr (M < 4) x = w << (8 - 2 * M);
-  else if constexpr (M == 4) x = w;
-  else x = w >> (2 * M - 8);
-  return (x & 0x03000300u) | 0x3C003C00u;
-}
-// Same pair as fp16 SUBNORMALS c * 2^-16 (exact, no offset): used for V so the
-// fp16 rounding of P' only scales each token's own contribution.
-template <int M>
-__device__ __forceinline__ uint32_t dqv(uint32_t w) {
-  uint32_t x;
-  if constexpr (M < 4) x = w << (8 - 2 * M);
-  else if constexpr (M == 4) x = w;
-  else x = w >> (2 * M - 8);
-  return x & 0x03000300u;
 }
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
@@ -337,12 +328,47 @@ __device__ __forceinline__ void tma_bulk_load(uint32_t dst, const void* src, uin
       : "memory");
 }
 
+// ---- 2-bit pair extraction. A word holds 16 codes (code m at bits 2m, code
+// m+8 at bits 16+2m). Pair m is used in place at fp16 mantissa position P(m)
+// (bits 2P..2P+1 of both halves) taken from one of three copies of the word:
+//   m:    0    1    2   3   4   5    6    7
+//   src:  <<6  <<6  x   x   x   >>6  >>6  >>6      (2 SHF + 8 LOP3 per word)
+//   P:    3    4    2   3   4   2    3    4
+// K codes become fp16 1 + c*2^(2P-10) (one LOP3 with the 1.0 magic); V codes
+// become exact fp16 subnormals c*2^(2P-24). The per-position scale is folded
+// into q' (K) or the final accumulator scale (V).
+struct Shifted {
+  uint32_t x, l6, r6;
+};
+__device__ __forceinline__ Shifted shifted(uint32_t w) { return {w, w << 6, w >> 6}; }
+__host__ __device__ constexpr int pair_pos(int m) { return m == 2 || m == 5 ? 2 : (m == 0 || m == 3 || m == 6 ? 3 : 4); }
+__host__ __device__ constexpr uint32_t pos_mask(int p) { return p == 2 ? 0x00300030u : (p == 3 ? 0x00C000C0u : 0x03000300u); }
+template <int M>
+__device__ __forceinline__ uint32_t pair_src(const Shifted& s) {
+  return M <= 1 ? s.l6 : (M <= 4 ? s.x : s.r6);
+}
+template <int M>
+__device__ __forceinline__ uint32_t kq(const Shifted& s, uint32_t magic) {
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;\n" : "=r"(r) : "r"(pair_src<M>(s)), "n"(pos_mask(pair_pos(M))), "r"(magic));
+  return r;
+}
+template <int M>
+__device__ __forceinline__ uint32_t vq(const Shifted& s) {
+  return pair_src<M>(s) & pos_mask(pair_pos(M));
+}
+
 template <int G>
 struct MmaSmem {
   static constexpr int kRec = G * 128 / 2 + 8 * 128 + 8 * G;  // record bytes at d = 128
   static constexpr int kStages = G == 32 ? 3 : 2;             // TMA pipeline depth per warp
-  float q4[8][128];                                          // q * 4 * scale_log2, heads padded to 8
-  float esc[kAttnWarps][128];                                // x_min - 4*step per channel (current group)
+  // q * 4 * scale_log2 in per-lane order: [hw][v4][lane] = head lane/4, channels
+  // 16*(lane%4 + 4*hw) + 4*v4 .. +3  (conflict-free LDS.128)
+  float4 q4p[2][4][32];
+  // per-group channel scratch in per-tig order [hw][v4][tig]: step * f and
+  // x_min - 4 f step, f = 1 (even pair) or 4 (odd pair)
+  float4 stp[kAttnWarps][2][4][4];
+  float4 esc[kAttnWarps][2][4][4];
   alignas(128) uint8_t stage[kAttnWarps][kStages][kRec];
   alignas(8) uint64_t bar[kAttnWarps][kStages];
   float mm[kAttnWarps][8], ll[kAttnWarps][8];
@@ -361,15 +387,23 @@ __device__ void mma_body(const AttnArgs& a, MmaSmem<G>& sm) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, tig = lane & 3;
 
+  const uint32_t magic = a.k_magic;
   const int n_groups = (int)(a.q_tokens / G);
   const int per = (n_groups + a.n_qsplits - 1) / a.n_qsplits;
   const int g0 = split * per;
   const int g1 = min(n_groups, g0 + per);
   const int my_n = g1 > g0 + warp ? (g1 - g0 - warp + kAttnWarps - 1) / kAttnWarps : 0;
 
-  for (int i = tid; i < 8 * D; i += kAttnThreads) {
-    const int h = i / D;
-    sm.q4[h][i % D] = h < NR ? h2f(a.q[((size_t)u * NR + h) * D + (i % D)]) * (4.f * a.scale_log2) : 0.f;
+  for (int i = tid; i < 2 * 4 * 32; i += kAttnThreads) {
+    const int hw = i >> 7, v4 = (i >> 5) & 3, ln = i & 31;
+    const int h = ln >> 2, ch = 16 * ((ln & 3) + 4 * hw) + 4 * v4;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (h < NR) {
+      const uint16_t* qp = a.q + ((size_t)u * NR + h) * D + ch;
+      const float f = 4.f * a.scale_log2;
+      v = make_float4(h2f(qp[0]) * f, h2f(qp[1]) * f, h2f(qp[2]) * f, h2f(qp[3]) * f);
+    }
+    sm.q4p[hw][v4][ln] = v;
   }
   const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&sm.bar[warp][0]);
   const uint32_t stage0 = (uint32_t)__cvta_generic_to_shared(&sm.stage[warp][0][0]);
@@ -390,92 +424,119 @@ __device__ void mma_body(const AttnArgs& a, MmaSmem<G>& sm) {
   for (int cm = 0; cm < 8; ++cm) o[cm][0] = o[cm][1] = o[cm][2] = o[cm][3] = 0.f;
   float mrun[2] = {-INFINITY, -INFINITY}, lsum[2] = {0.f, 0.f}, vb[2] = {0.f, 0.f};
   const uint32_t* pmask = c.pool_mask + (size_t)u * mask_words_per_unit(c);
-  float* esc = sm.esc[warp];
 
   // ldmatrix row addresses (bytes, relative to a 16-token tile): matrix i = lane/8,
   // row r = lane%8: i0 tokens 0-7 bytes 0-15, i1 tokens 8-15 bytes 0-15,
   // i2 tokens 0-7 bytes 16-31, i3 tokens 8-15 bytes 16-31.
   const uint32_t lm_off = (uint32_t)(((lane & 7) + ((lane >> 3) & 1) * 8) * 32 + (lane >> 4) * 16);
+  // cooperative channel pass: lane owns channels 4*lane..+3 = word lane/4, v4 = lane%4
+  const int cw = lane >> 2;
+  float4* stp_w = &sm.stp[warp][cw >> 2][lane & 3][cw & 3];
+  float4* esc_w = &sm.esc[warp][cw >> 2][lane & 3][cw & 3];
+  // f = 4^(4 - P(m)) for this lane's pairs: m = 0..3 -> {4, 1, 16, 4}; m = 4..7 -> {1, 16, 4, 1}
+  const float4 cf = (lane & 1) ? make_float4(1.f, 16.f, 4.f, 1.f) : make_float4(4.f, 1.f, 16.f, 4.f);
 
   for (int k = 0; k < my_n; ++k) {
     const int s = k % kStages;
     const int gi = g0 + warp + k * kAttnWarps;
+    uint32_t mwords[G / 32];
+#pragma unroll
+    for (int w = 0; w < G / 32; ++w) mwords[w] = __ldg(&pmask[(size_t)gi * (G / 32) + w]);
     mbar_wait(bar0 + 8 * s, (uint32_t)((k / kStages) & 1));
     const uint8_t* rec = &sm.stage[warp][s][0];
     const uint32_t rec_s = stage0 + s * kRec;
-    const float* kstep = reinterpret_cast<const float*>(rec + L.k_step());
-    const float* kxmin = reinterpret_cast<const float*>(rec + L.k_xmin());
     const float* vstep = reinterpret_cast<const float*>(rec + L.v_step());
     const float* vxmin = reinterpret_cast<const float*>(rec + L.v_xmin());
 
-    // ---- per-channel e = x_min - 4*step (shared by the 8 head-rows of the warp)
+    // ---- channel pass: step * f and e = x_min - 4 f step with f = 4^(4 - P(m))
+    // (lane holds channels 4*lane..+3 = pairs m = 4*(lane&1) + 0..3)
     {
-      const float4 st = *reinterpret_cast<const float4*>(kstep + 4 * lane);
-      const float4 mn = *reinterpret_cast<const float4*>(kxmin + 4 * lane);
-      *reinterpret_cast<float4*>(esc + 4 * lane) =
-          make_float4(fmaf(-4.f, st.x, mn.x), fmaf(-4.f, st.y, mn.y), fmaf(-4.f, st.z, mn.z), fmaf(-4.f, st.w, mn.w));
+      const float4 st = *reinterpret_cast<const float4*>(rec + L.k_step() + 16 * lane);
+      const float4 mn = *reinterpret_cast<const float4*>(rec + L.k_xmin() + 16 * lane);
+      *stp_w = make_float4(st.x * cf.x, st.y * cf.y, st.z * cf.z, st.w * cf.w);
+      *esc_w = make_float4(fmaf(-4.f * cf.x, st.x, mn.x), fmaf(-4.f * cf.y, st.y, mn.y), fmaf(-4.f * cf.z, st.z, mn.z),
+                           fmaf(-4.f * cf.w, st.w, mn.w));
     }
+    // K code words of every m-tile (ldmatrix: token g / g+8, words tig and 4+tig)
+    uint32_t kw[kMt][4];
+#pragma unroll
+    for (int mt = 0; mt < kMt; ++mt) ldsm_x4(kw[mt], rec_s + L.k_codes() + mt * 16 * 32 + lm_off);
     __syncwarp();
 
-    // ---- B operand (q' = 4*scale*q*step, hi/lo fp16) and K bias for head g
-    uint32_t bh[2][8], bl[2][8];
-    float bias = 0.f;
+    // ---- S = Q K^T, one 16-channel word half (hw) at a time: B operand q' =
+    // q4 * step * f as hi/lo fp16 pairs (channels m, m+8), two accumulator chains
+    // (hi, lo) per m-tile, K bias (x_min terms) added at the end.
+    float ch[kMt][4], cl[kMt][4];
+#pragma unroll
+    for (int mt = 0; mt < kMt; ++mt)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) ch[mt][j] = cl[mt][j] = 0.f;
+    float2 bias2 = make_float2(0.f, 0.f);
 #pragma unroll
     for (int hw = 0; hw < 2; ++hw) {
-      const int ch0 = 16 * (tig + 4 * hw);
-      float qv[16], sv[16], ev[16];
+      uint32_t bh[8], bl[8];
+      {
+        float2 B[8];
 #pragma unroll
-      for (int v4 = 0; v4 < 4; ++v4) {
-        const float4 q4 = *reinterpret_cast<const float4*>(&sm.q4[g][ch0 + 4 * v4]);
-        const float4 s4 = *reinterpret_cast<const float4*>(kstep + ch0 + 4 * v4);
-        const float4 e4 = *reinterpret_cast<const float4*>(esc + ch0 + 4 * v4);
-        qv[4 * v4] = q4.x; qv[4 * v4 + 1] = q4.y; qv[4 * v4 + 2] = q4.z; qv[4 * v4 + 3] = q4.w;
-        sv[4 * v4] = s4.x; sv[4 * v4 + 1] = s4.y; sv[4 * v4 + 2] = s4.z; sv[4 * v4 + 3] = s4.w;
-        ev[4 * v4] = e4.x; ev[4 * v4 + 1] = e4.y; ev[4 * v4 + 2] = e4.z; ev[4 * v4 + 3] = e4.w;
+        for (int v4 = 0; v4 < 4; ++v4) {
+          const float4 q4 = sm.q4p[hw][v4][lane];
+          const float4 s4 = sm.stp[warp][hw][v4][tig];
+          const float4 e4 = sm.esc[warp][hw][v4][tig];
+          const float2 q0 = make_float2(q4.x, q4.y), q1 = make_float2(q4.z, q4.w);
+          B[2 * v4] = __fmul2_rn(q0, make_float2(s4.x, s4.y));
+          B[2 * v4 + 1] = __fmul2_rn(q1, make_float2(s4.z, s4.w));
+          bias2 = __ffma2_rn(q0, make_float2(e4.x, e4.y), bias2);
+          bias2 = __ffma2_rn(q1, make_float2(e4.z, e4.w), bias2);
+        }
+        float hi[16], lo[16];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float2 h = make_float2(__uint_as_float(__float_as_uint(B[j].x) & 0xFFFFE000u),
+                                       __uint_as_float(__float_as_uint(B[j].y) & 0xFFFFE000u));
+          const float2 l = __fadd2_rn(B[j], make_float2(-h.x, -h.y));
+          hi[2 * j] = h.x;
+          hi[2 * j + 1] = h.y;
+          lo[2 * j] = l.x;
+          lo[2 * j + 1] = l.y;
+        }
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+          bh[m] = pack_h2(hi[m], hi[m + 8]);
+          bl[m] = pack_h2(lo[m], lo[m + 8]);
+        }
       }
 #pragma unroll
-      for (int m = 0; m < 8; ++m) {
-        const float B0 = qv[m] * sv[m], B1 = qv[m + 8] * sv[m + 8];
-        const float h0 = __uint_as_float(__float_as_uint(B0) & 0xFFFFE000u);
-        const float h1 = __uint_as_float(__float_as_uint(B1) & 0xFFFFE000u);
-        bh[hw][m] = pack_h2(h0, h1);
-        bl[hw][m] = pack_h2(B0 - h0, B1 - h1);
-        bias = fmaf(qv[m], ev[m], bias);
-        bias = fmaf(qv[m + 8], ev[m + 8], bias);
+      for (int mt = 0; mt < kMt; ++mt) {
+        const Shifted s0 = shifted(kw[mt][2 * hw]), s1 = shifted(kw[mt][2 * hw + 1]);
+#define OTT_QK(MM)                                                                      \
+  {                                                                                     \
+    const uint32_t a0 = kq<MM>(s0, magic), a1 = kq<MM>(s1, magic);                      \
+    const uint32_t a2 = kq<MM + 1>(s0, magic), a3 = kq<MM + 1>(s1, magic);              \
+    mma16816(ch[mt], a0, a1, a2, a3, bh[MM], bh[MM + 1]);                               \
+    mma16816(cl[mt], a0, a1, a2, a3, bl[MM], bl[MM + 1]);                               \
+  }
+        OTT_QK(0) OTT_QK(2) OTT_QK(4) OTT_QK(6)
+#undef OTT_QK
       }
     }
+    float bias = bias2.x + bias2.y;
     bias += __shfl_xor_sync(0xffffffffu, bias, 1);
     bias += __shfl_xor_sync(0xffffffffu, bias, 2);
     bias *= 0.25f;
     const float bias0 = __shfl_sync(0xffffffffu, bias, 8 * tig);      // head 2*tig
     const float bias1 = __shfl_sync(0xffffffffu, bias, 8 * tig + 4);  // head 2*tig+1
-
-    // ---- S = Q K^T for the group's m-tiles
     float sc[kMt][4];
 #pragma unroll
     for (int mt = 0; mt < kMt; ++mt) {
-      uint32_t kw[4];
-      ldsm_x4(kw, rec_s + L.k_codes() + mt * 16 * 32 + lm_off);
-      float cc[4] = {bias0, bias1, bias0, bias1};
-#define OTT_QK_SLICE(HW, MM)                                                                          \
-  {                                                                                                   \
-    const uint32_t a0 = dq<MM>(kw[2 * HW]), a1 = dq<MM>(kw[2 * HW + 1]);                              \
-    const uint32_t a2 = dq<MM + 1>(kw[2 * HW]), a3 = dq<MM + 1>(kw[2 * HW + 1]);                      \
-    mma16816(cc, a0, a1, a2, a3, bh[HW][MM], bh[HW][MM + 1]);                                         \
-    mma16816(cc, a0, a1, a2, a3, bl[HW][MM], bl[HW][MM + 1]);                                         \
-  }
-      OTT_QK_SLICE(0, 0) OTT_QK_SLICE(0, 2) OTT_QK_SLICE(0, 4) OTT_QK_SLICE(0, 6)
-      OTT_QK_SLICE(1, 0) OTT_QK_SLICE(1, 2) OTT_QK_SLICE(1, 4) OTT_QK_SLICE(1, 6)
-#undef OTT_QK_SLICE
-      sc[mt][0] = cc[0];
-      sc[mt][1] = cc[1];
-      sc[mt][2] = cc[2];
-      sc[mt][3] = cc[3];
+      sc[mt][0] = ch[mt][0] + cl[mt][0] + bias0;
+      sc[mt][1] = ch[mt][1] + cl[mt][1] + bias1;
+      sc[mt][2] = ch[mt][2] + cl[mt][2] + bias0;
+      sc[mt][3] = ch[mt][3] + cl[mt][3] + bias1;
     }
     // pooled positions: their logits come from the pool tile (overwrite semantics)
 #pragma unroll
     for (int w = 0; w < G / 32; ++w) {
-      const uint32_t mw = __ldg(&pmask[(size_t)gi * (G / 32) + w]);
+      const uint32_t mw = mwords[w];
       if (mw) {
 #pragma unroll
         for (int mt = 2 * w; mt < 2 * w + 2; ++mt) {
@@ -493,17 +554,18 @@ __device__ void mma_body(const AttnArgs& a, MmaSmem<G>& sm) {
       float t = -INFINITY;
 #pragma unroll
       for (int mt = 0; mt < kMt; ++mt) t = fmaxf(t, fmaxf(sc[mt][h], sc[mt][h + 2]));
-      t = fmaxf(t, __shfl_xor_sync(0xffffffffu, t, 4));
-      t = fmaxf(t, __shfl_xor_sync(0xffffffffu, t, 8));
-      t = fmaxf(t, __shfl_xor_sync(0xffffffffu, t, 16));
       tmax[h] = t;
     }
     const bool need = tmax[0] > mrun[0] + kLazy || tmax[1] > mrun[1] + kLazy;
-    if (__any_sync(0xffffffffu, need)) {
+    if (__any_sync(0xffffffffu, need)) {  // rare: warp max over the token rows, rescale
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const float mnew = fmaxf(mrun[h], tmax[h]);
-        const float corr = mnew == -INFINITY ? 1.f : exp2f(mrun[h] - mnew);
+        float t = tmax[h];
+        t = fmaxf(t, __shfl_xor_sync(0xffffffffu, t, 4));
+        t = fmaxf(t, __shfl_xor_sync(0xffffffffu, t, 8));
+        t = fmaxf(t, __shfl_xor_sync(0xffffffffu, t, 16));
+        const float mnew = fmaxf(mrun[h], t);
+        const float corr = mnew == -INFINITY ? 1.f : ex2(mrun[h] - mnew);
         lsum[h] *= corr;
         vb[h] *= corr;
 #pragma unroll
@@ -517,14 +579,14 @@ __device__ void mma_body(const AttnArgs& a, MmaSmem<G>& sm) {
     const float me0 = mrun[0] == -INFINITY ? 0.f : mrun[0];
     const float me1 = mrun[1] == -INFINITY ? 0.f : mrun[1];
 
-    // ---- O^T += V^T P'  (V step folded into P' = 4 p step, V x_min into vb;
-    // with codes as c * 2^-16 the accumulator holds sum(p step c) * 2^-14)
+    // ---- O^T += V^T P'  (P' = 4 p step fp16, V x_min into vb; with V codes as
+    // subnormals the accumulator holds sum(p step c) * 2^-14 (even pairs) or 2^-16)
 #pragma unroll
     for (int mt = 0; mt < kMt; ++mt) {
       const float vs0 = vstep[mt * 16 + g], vs1 = vstep[mt * 16 + g + 8];
       const float ve0 = vxmin[mt * 16 + g], ve1 = vxmin[mt * 16 + g + 8];
-      const float p00 = exp2f(sc[mt][0] - me0), p01 = exp2f(sc[mt][1] - me1);
-      const float p10 = exp2f(sc[mt][2] - me0), p11 = exp2f(sc[mt][3] - me1);
+      const float p00 = ex2(sc[mt][0] - me0), p01 = ex2(sc[mt][1] - me1);
+      const float p10 = ex2(sc[mt][2] - me0), p11 = ex2(sc[mt][3] - me1);
       lsum[0] += p00 + p10;
       lsum[1] += p01 + p11;
       vb[0] = fmaf(p00, ve0, fmaf(p10, ve1, vb[0]));
@@ -534,7 +596,8 @@ __device__ void mma_body(const AttnArgs& a, MmaSmem<G>& sm) {
       const uint32_t b1 = movm_t(pack_h2(p10 * f1, p11 * f1));
       uint32_t vr[4];
       ldsm_x4_t(vr, rec_s + L.v_codes() + mt * 16 * 32 + lm_off);
-#define OTT_PV(CM) mma16816(o[CM], dqv<CM>(vr[0]), dqv<CM>(vr[2]), dqv<CM>(vr[1]), dqv<CM>(vr[3]), b0, b1);
+      const Shifted v0 = shifted(vr[0]), v1 = shifted(vr[1]), v2 = shifted(vr[2]), v3 = shifted(vr[3]);
+#define OTT_PV(CM) mma16816(o[CM], vq<CM>(v0), vq<CM>(v2), vq<CM>(v1), vq<CM>(v3), b0, b1);
       OTT_PV(0) OTT_PV(1) OTT_PV(2) OTT_PV(3) OTT_PV(4) OTT_PV(5) OTT_PV(6) OTT_PV(7)
 #undef OTT_PV
     }
@@ -566,10 +629,11 @@ __device__ void mma_body(const AttnArgs& a, MmaSmem<G>& sm) {
   float* accw = reinterpret_cast<float*>(&sm.stage[warp][0][0]);  // [8 heads][128] natural channel order
 #pragma unroll
   for (int cm = 0; cm < 8; ++cm) {
+    const float f = pair_pos(cm) == 2 ? 262144.f : (pair_pos(cm) == 3 ? 65536.f : 16384.f);  // 2^(22-2P)
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      accw[(2 * tig + h) * D + 8 * g + cm] = fmaf(o[cm][h], 16384.f, vb[h]);
-      accw[(2 * tig + h) * D + 64 + 8 * g + cm] = fmaf(o[cm][h + 2], 16384.f, vb[h]);
+      accw[(2 * tig + h) * D + 8 * g + cm] = fmaf(o[cm][h], f, vb[h]);
+      accw[(2 * tig + h) * D + 64 + 8 * g + cm] = fmaf(o[cm][h + 2], f, vb[h]);
     }
   }
   __syncthreads();
@@ -597,12 +661,212 @@ __device__ void mma_body(const AttnArgs& a, MmaSmem<G>& sm) {
   }
 }
 
+// ---- full-precision tiers (pool.entries + pending ring) on tensor cores.
+// 16-row tiles of fp16 K/V rows are staged with per-row TMA bulk copies into a
+// padded layout (272-byte row pitch: conflict-free ldmatrix); q (exact fp16) is
+// the B operand of Q K^T, P the B operand of V^T P. One stage per warp: these
+// tiers hold at most N + G + R - 1 rows per unit.
+struct FpSmem {
+  static constexpr int kRow = 272;
+  alignas(128) uint8_t kr[kAttnWarps][16][kRow];
+  alignas(128) uint8_t vr[kAttnWarps][16][kRow];
+  alignas(8) uint64_t bar[kAttnWarps];
+  float mm[kAttnWarps][8], ll[kAttnWarps][8];
+};
+
+__device__ __forceinline__ void tma_row(uint32_t dst, const void* src, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 256, [%2];\n" ::"r"(dst),
+      "l"(src), "r"(bar)
+      : "memory");
+}
+
+template <int NR>
+__device__ void fp_body(const AttnArgs& a, FpSmem& sm) {
+  constexpr int D = 128, kRow = FpSmem::kRow;
+  const ott_cache_t& c = a.c;
+  const int u = blockIdx.x, split = blockIdx.y;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, tig = lane & 3;
+  const int N = c.capacity, cap = c.group_size + c.residual;
+  const int n_pool_t = (N + 15) / 16;
+  const int Tp = (int)(a.total_tokens - a.q_tokens);
+  const int n_tiles = n_pool_t + (Tp + 15) / 16;
+
+  // q (exact fp16) as the B fragments of Q K^T: head g, channels 16j + 2tig (+1), +8
+  uint32_t qb[8][2];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    if (g < NR) {
+      const uint32_t* qp = reinterpret_cast<const uint32_t*>(a.q + ((size_t)u * NR + g) * D + 16 * j + 2 * tig);
+      qb[j][0] = qp[0];
+      qb[j][1] = qp[4];
+    } else {
+      qb[j][0] = qb[j][1] = 0u;
+    }
+  }
+  // zero the staging rows once: rows a tile does not copy keep finite (stale or zero)
+  // data, so a zero softmax weight never meets a NaN
+  for (int i = lane; i < 16 * kRow / 16; i += 32) {
+    reinterpret_cast<uint4*>(&sm.kr[warp][0][0])[i] = make_uint4(0, 0, 0, 0);
+    reinterpret_cast<uint4*>(&sm.vr[warp][0][0])[i] = make_uint4(0, 0, 0, 0);
+  }
+  const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&sm.bar[warp]);
+  const uint32_t kr_s = (uint32_t)__cvta_generic_to_shared(&sm.kr[warp][0][0]);
+  const uint32_t vr_s = (uint32_t)__cvta_generic_to_shared(&sm.vr[warp][0][0]);
+  if (lane == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  __syncwarp();
+
+  float o[8][4];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
+  float mrun[2] = {-INFINITY, -INFINITY}, lsum[2] = {0.f, 0.f};
+  // ldmatrix lane addressing (row, byte column) for K (non-trans) and V (trans)
+  const int k_row = (lane & 7) + ((lane >> 3) & 1) * 8, k_col = (lane >> 4) * 16;
+  const int v_row = (lane & 7) + ((lane >> 4) & 1) * 8, v_col = ((lane >> 3) & 1) * 16;
+  uint32_t phase = 0;
+
+  for (int t = warp; t < n_tiles; t += kAttnWarps) {
+    const bool is_pool = t < n_pool_t;
+    // row validity of this lane's two rows (g, g+8)
+    bool valid[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = g + 8 * h;
+      if (is_pool) {
+        const int slot = 16 * t + r;
+        valid[h] = slot < N && c.pool_pos[(size_t)u * N + slot] >= 0;
+      } else {
+        valid[h] = 16 * (t - n_pool_t) + r < Tp;
+      }
+    }
+    if (lane == 0) {
+      const int rows = is_pool ? min(16, N - 16 * t) : min(16, Tp - 16 * (t - n_pool_t));
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(rows * 512)
+                   : "memory");
+      for (int r = 0; r < rows; ++r) {
+        size_t off;
+        if (is_pool) {
+          off = ((size_t)u * N + 16 * t + r) * D;
+        } else {
+          const int64_t p = a.q_tokens + 16 * (t - n_pool_t) + r;
+          off = ((size_t)u * cap + (size_t)(p % cap)) * D;
+        }
+        tma_row(kr_s + r * kRow, (is_pool ? c.pool_k : c.pend_k) + off, bar);
+        tma_row(vr_s + r * kRow, (is_pool ? c.pool_v : c.pend_v) + off, bar);
+      }
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      uint32_t ak[4];
+      ldsm_x4(ak, kr_s + k_row * kRow + 32 * j + k_col);
+      mma16816(acc, ak[0], ak[1], ak[2], ak[3], qb[j][0], qb[j][1]);
+    }
+    float sc[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) sc[j] = valid[j >> 1] ? acc[j] * a.scale_log2 : -INFINITY;
+    float tmax[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      float tm = fmaxf(sc[h], sc[h + 2]);
+      tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 4));
+      tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 8));
+      tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 16));
+      tmax[h] = tm;
+    }
+    const bool need = tmax[0] > mrun[0] + kLazy || tmax[1] > mrun[1] + kLazy;
+    if (__any_sync(0xffffffffu, need)) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const float mnew = fmaxf(mrun[h], tmax[h]);
+        const float corr = mnew == -INFINITY ? 1.f : ex2(mrun[h] - mnew);
+        lsum[h] *= corr;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          o[j][h] *= corr;
+          o[j][h + 2] *= corr;
+        }
+        mrun[h] = mnew;
+      }
+    }
+    const float me0 = mrun[0] == -INFINITY ? 0.f : mrun[0];
+    const float me1 = mrun[1] == -INFINITY ? 0.f : mrun[1];
+    const float p00 = ex2(sc[0] - me0), p01 = ex2(sc[1] - me1);
+    const float p10 = ex2(sc[2] - me0), p11 = ex2(sc[3] - me1);
+    lsum[0] += p00 + p10;
+    lsum[1] += p01 + p11;
+    const uint32_t b0 = movm_t(pack_h2(p00, p01));
+    const uint32_t b1 = movm_t(pack_h2(p10, p11));
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      uint32_t av[4];
+      ldsm_x4_t(av, vr_s + v_row * kRow + 32 * j + v_col);
+      mma16816(o[j], av[0], av[1], av[2], av[3], b0, b1);
+    }
+    __syncwarp();
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  }
+
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+#pragma unroll
+    for (int off = 4; off < 32; off <<= 1) lsum[h] += __shfl_xor_sync(0xffffffffu, lsum[h], off);
+  }
+  if (g == 0) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      sm.mm[warp][2 * tig + h] = mrun[h];
+      sm.ll[warp][2 * tig + h] = lsum[h];
+    }
+  }
+  __syncthreads();
+  float* accw = reinterpret_cast<float*>(&sm.kr[warp][0][0]);  // [8 heads][128]
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      accw[(2 * tig + h) * D + 16 * j + g] = o[j][h];
+      accw[(2 * tig + h) * D + 16 * j + 8 + g] = o[j][h + 2];
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < NR * D; i += kAttnThreads) {
+    const int r = i / D, col = i % D;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < kAttnWarps; ++w) M = fmaxf(M, sm.mm[w][r]);
+    float Lsum = 0.f, A = 0.f;
+    if (M != -INFINITY) {
+#pragma unroll
+      for (int w = 0; w < kAttnWarps; ++w) {
+        if (sm.mm[w][r] == -INFINITY) continue;
+        const float f = exp2f(sm.mm[w][r] - M);
+        Lsum += sm.ll[w][r] * f;
+        A += reinterpret_cast<const float*>(&sm.kr[w][0][0])[r * D + col] * f;
+      }
+    }
+    float* base = a.ws + (((size_t)u * NR + r) * a.n_splits + split) * (D + 2);
+    base[2 + col] = A;
+    if (col == 0) {
+      base[0] = M;
+      base[1] = Lsum;
+    }
+  }
+}
+
 template <int NR, int G>
-__global__ void __launch_bounds__(kAttnThreads) attend_mma_kernel(AttnArgs a) {
+__global__ void __launch_bounds__(kAttnThreads, OTT_MMA_MIN_BLOCKS) attend_mma_kernel(AttnArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   if ((int)blockIdx.y == a.n_qsplits) {  // full-precision tiers: pool.entries + pending window
-    const int t0 = a.n_qtiles, t1 = a.n_qtiles + a.n_ptiles + a.n_rtiles;
-    simt_body<NR, 128>(a, blockIdx.x, t0, t1, blockIdx.y, *reinterpret_cast<SimtSmem<NR, 128>*>(smem_raw));
+    fp_body<NR>(a, *reinterpret_cast<FpSmem*>(smem_raw));
   } else {
     mma_body<NR, G>(a, *reinterpret_cast<MmaSmem<G>*>(smem_raw));
   }
@@ -683,8 +947,7 @@ static cudaError_t launch_simt_t(const AttnArgs& a, cudaStream_t st) {
 
 template <int NR, int G>
 static cudaError_t launch_mma_t(const AttnArgs& a, cudaStream_t st) {
-  const size_t smem = sizeof(MmaSmem<G>) > sizeof(SimtSmem<NR, 128>) ? sizeof(MmaSmem<G>)
-                                                                       : sizeof(SimtSmem<NR, 128>);
+  const size_t smem = sizeof(MmaSmem<G>) > sizeof(FpSmem) ? sizeof(MmaSmem<G>) : sizeof(FpSmem);
   cudaError_t e =
       cudaFuncSetAttribute(attend_mma_kernel<NR, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -712,6 +975,7 @@ cudaError_t launch_attend(const ott_cache_t& c, const uint16_t* q, uint16_t* out
   a.n_ptiles = (c.capacity + 31) / 32;
   a.n_rtiles = (int)((total - q_tokens + 31) / 32);
   a.scale_log2 = kLog2e / sqrtf((float)c.head_dim);
+  a.k_magic = 0x3C003C00u;
   const int D = c.head_dim, G = c.group_size;
   if (mma_eligible(c)) {
 #define OTT_MCASE(NRv, Gv) \
