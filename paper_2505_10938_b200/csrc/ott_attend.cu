@@ -24,6 +24,9 @@
 // per-(group, head) bias. V codes become exact fp16 subnormals c * 2^-16; the
 // per-token V step is folded into P' = 4 p step (fp16) and V x_min into a
 // per-head fp32 bias. See DESIGN.md §4.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "ott_common.cuh"
 
 namespace ott {
@@ -358,25 +361,53 @@ __device__ __forceinline__ uint32_t vq(const Shifted& s) {
   return pair_src<M>(s) & pos_mask(pair_pos(M));
 }
 
+__device__ __forceinline__ uint32_t swz(uint32_t o) { return o ^ ((o >> 3) & 16u); }  // Swizzle<1,4,3>
+__host__ __device__ constexpr int tile_slot(int v4, int tig) { return 4 * v4 + (tig ^ ((v4 >> 1) << 1)); }
+__device__ __forceinline__ void tma_tensor_rows(uint32_t dst, const CUtensorMap* map, int row, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          dst),
+      "l"(map), "r"(0), "r"(row), "r"(bar)
+      : "memory");
+}
+template <int G>
+struct RecTma {  // a record is kRows rows of 32 bytes; loaded as kBoxes boxes of kBoxRows rows
+  static constexpr int kRows = (G * 128 / 2 + 8 * 128 + 8 * G) / 32;
+  static constexpr int kBoxes = kRows > 256 ? 2 : 1;
+  static constexpr int kBoxRows = kRows / kBoxes;
+};
+template <int G>
+__device__ __forceinline__ void load_record(uint32_t dst, const CUtensorMap* map, int64_t rec_index, uint32_t bar) {
+  constexpr int kRec = RecTma<G>::kRows * 32;
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(kRec) : "memory");
+#pragma unroll
+  for (int b = 0; b < RecTma<G>::kBoxes; ++b)
+    tma_tensor_rows(dst + b * RecTma<G>::kBoxRows * 32, map,
+                    (int)(rec_index * RecTma<G>::kRows + b * RecTma<G>::kBoxRows), bar);
+}
+
 template <int G>
 struct MmaSmem {
   static constexpr int kRec = G * 128 / 2 + 8 * 128 + 8 * G;  // record bytes at d = 128
-  static constexpr int kStages = G == 32 ? 3 : 2;             // TMA pipeline depth per warp
+  static constexpr int kStages = 2;                           // TMA pipeline depth per warp
   // q * 4 * scale_log2 in per-lane order: [hw][v4][lane] = head lane/4, channels
   // 16*(lane%4 + 4*hw) + 4*v4 .. +3  (conflict-free LDS.128)
   float4 q4p[2][4][32];
-  // per-group channel scratch in per-tig order [hw][v4][tig]: step * f and
-  // x_min - 4 f step, f = 1 (even pair) or 4 (odd pair)
-  float4 stp[kAttnWarps][2][4][4];
-  float4 esc[kAttnWarps][2][4][4];
-  alignas(128) uint8_t stage[kAttnWarps][kStages][kRec];
+  // per-group channel scratch [hw][slot], slot = 4*v4 + (tig ^ 2*(v4>>1)) (bank-conflict
+  // free for the lane-ordered writes and the per-tig broadcast reads): step * f and
+  // x_min - 4 f step with f = 4^(4 - P(m))
+  float4 stp[kAttnWarps][2][16];
+  float4 esc[kAttnWarps][2][16];
+  // group records land here through a SWIZZLE_32B tensor map (16-byte chunk bit 4 ^= bit 7
+  // of the offset): ldmatrix over 32-byte token rows is then bank-conflict free
+  alignas(256) uint8_t stage[kAttnWarps][kStages][kRec];
   alignas(8) uint64_t bar[kAttnWarps][kStages];
   float mm[kAttnWarps][8], ll[kAttnWarps][8];
 };
 
 // Quantized-region partial for (unit blockIdx.x, split blockIdx.y < n_qsplits).
 template <int NR, int G>
-__device__ void mma_body(const AttnArgs& a, MmaSmem<G>& sm) {
+__device__ void mma_body(const AttnArgs& a, const CUtensorMap* tmap, MmaSmem<G>& sm) {
   constexpr int D = 128;
   constexpr int kRec = MmaSmem<G>::kRec;
   constexpr int kMt = G / 16;  // 16-token m-tiles per group
@@ -407,15 +438,14 @@ __device__ void mma_body(const AttnArgs& a, MmaSmem<G>& sm) {
   }
   const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&sm.bar[warp][0]);
   const uint32_t stage0 = (uint32_t)__cvta_generic_to_shared(&sm.stage[warp][0][0]);
-  const uint8_t* unit_rec = c.blocks + (size_t)u * c.max_groups * kRec;
+  const int64_t unit_rec = (int64_t)u * c.max_groups;  // record index of group 0
   if (lane == 0) {
 #pragma unroll
     for (int s = 0; s < kStages; ++s) mbar_init(bar0 + 8 * s, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
 #pragma unroll
     for (int s = 0; s < kStages; ++s)
-      if (s < my_n)
-        tma_bulk_load(stage0 + s * kRec, unit_rec + (size_t)(g0 + warp + s * kAttnWarps) * kRec, kRec, bar0 + 8 * s);
+      if (s < my_n) load_record<G>(stage0 + s * kRec, tmap, unit_rec + g0 + warp + s * kAttnWarps, bar0 + 8 * s);
   }
   __syncthreads();
 
@@ -431,8 +461,8 @@ __device__ void mma_body(const AttnArgs& a, MmaSmem<G>& sm) {
   const uint32_t lm_off = (uint32_t)(((lane & 7) + ((lane >> 3) & 1) * 8) * 32 + (lane >> 4) * 16);
   // cooperative channel pass: lane owns channels 4*lane..+3 = word lane/4, v4 = lane%4
   const int cw = lane >> 2;
-  float4* stp_w = &sm.stp[warp][cw >> 2][lane & 3][cw & 3];
-  float4* esc_w = &sm.esc[warp][cw >> 2][lane & 3][cw & 3];
+  float4* stp_w = &sm.stp[warp][cw >> 2][tile_slot(lane & 3, cw & 3)];
+  float4* esc_w = &sm.esc[warp][cw >> 2][tile_slot(lane & 3, cw & 3)];
   // f = 4^(4 - P(m)) for this lane's pairs: m = 0..3 -> {4, 1, 16, 4}; m = 4..7 -> {1, 16, 4, 1}
   const float4 cf = (lane & 1) ? make_float4(1.f, 16.f, 4.f, 1.f) : make_float4(4.f, 1.f, 16.f, 4.f);
 
@@ -445,14 +475,12 @@ __device__ void mma_body(const AttnArgs& a, MmaSmem<G>& sm) {
     mbar_wait(bar0 + 8 * s, (uint32_t)((k / kStages) & 1));
     const uint8_t* rec = &sm.stage[warp][s][0];
     const uint32_t rec_s = stage0 + s * kRec;
-    const float* vstep = reinterpret_cast<const float*>(rec + L.v_step());
-    const float* vxmin = reinterpret_cast<const float*>(rec + L.v_xmin());
 
     // ---- channel pass: step * f and e = x_min - 4 f step with f = 4^(4 - P(m))
     // (lane holds channels 4*lane..+3 = pairs m = 4*(lane&1) + 0..3)
     {
-      const float4 st = *reinterpret_cast<const float4*>(rec + L.k_step() + 16 * lane);
-      const float4 mn = *reinterpret_cast<const float4*>(rec + L.k_xmin() + 16 * lane);
+      const float4 st = *reinterpret_cast<const float4*>(rec + swz(L.k_step() + 16 * lane));
+      const float4 mn = *reinterpret_cast<const float4*>(rec + swz(L.k_xmin() + 16 * lane));
       *stp_w = make_float4(st.x * cf.x, st.y * cf.y, st.z * cf.z, st.w * cf.w);
       *esc_w = make_float4(fmaf(-4.f * cf.x, st.x, mn.x), fmaf(-4.f * cf.y, st.y, mn.y), fmaf(-4.f * cf.z, st.z, mn.z),
                            fmaf(-4.f * cf.w, st.w, mn.w));
@@ -460,7 +488,7 @@ __device__ void mma_body(const AttnArgs& a, MmaSmem<G>& sm) {
     // K code words of every m-tile (ldmatrix: token g / g+8, words tig and 4+tig)
     uint32_t kw[kMt][4];
 #pragma unroll
-    for (int mt = 0; mt < kMt; ++mt) ldsm_x4(kw[mt], rec_s + L.k_codes() + mt * 16 * 32 + lm_off);
+    for (int mt = 0; mt < kMt; ++mt) ldsm_x4(kw[mt], rec_s + swz(L.k_codes() + mt * 16 * 32 + lm_off));
     __syncwarp();
 
     // ---- S = Q K^T, one 16-channel word half (hw) at a time: B operand q' =
@@ -474,49 +502,55 @@ __device__ void mma_body(const AttnArgs& a, MmaSmem<G>& sm) {
     float2 bias2 = make_float2(0.f, 0.f);
 #pragma unroll
     for (int hw = 0; hw < 2; ++hw) {
-      uint32_t bh[8], bl[8];
-      {
-        float2 B[8];
 #pragma unroll
-        for (int v4 = 0; v4 < 4; ++v4) {
+      for (int half = 0; half < 2; ++half) {  // pairs m = 4*half .. 4*half+3 (channels m, m+8)
+        uint32_t bh[4], bl[4];
+#pragma unroll
+        for (int pp = 0; pp < 2; ++pp) {  // v4 = half (channels 4*half..+3), v4 = 2 + half (+8)
+          const int v4 = half + 2 * pp;
           const float4 q4 = sm.q4p[hw][v4][lane];
-          const float4 s4 = sm.stp[warp][hw][v4][tig];
-          const float4 e4 = sm.esc[warp][hw][v4][tig];
+          const float4 s4 = sm.stp[warp][hw][tile_slot(v4, tig)];
+          const float4 e4 = sm.esc[warp][hw][tile_slot(v4, tig)];
           const float2 q0 = make_float2(q4.x, q4.y), q1 = make_float2(q4.z, q4.w);
-          B[2 * v4] = __fmul2_rn(q0, make_float2(s4.x, s4.y));
-          B[2 * v4 + 1] = __fmul2_rn(q1, make_float2(s4.z, s4.w));
+          const float2 B0 = __fmul2_rn(q0, make_float2(s4.x, s4.y));
+          const float2 B1 = __fmul2_rn(q1, make_float2(s4.z, s4.w));
           bias2 = __ffma2_rn(q0, make_float2(e4.x, e4.y), bias2);
           bias2 = __ffma2_rn(q1, make_float2(e4.z, e4.w), bias2);
+          const float2 h0 = make_float2(__uint_as_float(__float_as_uint(B0.x) & 0xFFFFE000u),
+                                        __uint_as_float(__float_as_uint(B0.y) & 0xFFFFE000u));
+          const float2 h1 = make_float2(__uint_as_float(__float_as_uint(B1.x) & 0xFFFFE000u),
+                                        __uint_as_float(__float_as_uint(B1.y) & 0xFFFFE000u));
+          const float2 l0 = __fadd2_rn(B0, make_float2(-h0.x, -h0.y));
+          const float2 l1 = __fadd2_rn(B1, make_float2(-h1.x, -h1.y));
+          if (pp == 0) {  // low channel of each pair
+            bh[0] = __float_as_uint(h0.x); bh[1] = __float_as_uint(h0.y);
+            bh[2] = __float_as_uint(h1.x); bh[3] = __float_as_uint(h1.y);
+            bl[0] = __float_as_uint(l0.x); bl[1] = __float_as_uint(l0.y);
+            bl[2] = __float_as_uint(l1.x); bl[3] = __float_as_uint(l1.y);
+          } else {  // pack (low, high = channel + 8)
+            bh[0] = pack_h2(__uint_as_float(bh[0]), h0.x); bh[1] = pack_h2(__uint_as_float(bh[1]), h0.y);
+            bh[2] = pack_h2(__uint_as_float(bh[2]), h1.x); bh[3] = pack_h2(__uint_as_float(bh[3]), h1.y);
+            bl[0] = pack_h2(__uint_as_float(bl[0]), l0.x); bl[1] = pack_h2(__uint_as_float(bl[1]), l0.y);
+            bl[2] = pack_h2(__uint_as_float(bl[2]), l1.x); bl[3] = pack_h2(__uint_as_float(bl[3]), l1.y);
+          }
         }
-        float hi[16], lo[16];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const float2 h = make_float2(__uint_as_float(__float_as_uint(B[j].x) & 0xFFFFE000u),
-                                       __uint_as_float(__float_as_uint(B[j].y) & 0xFFFFE000u));
-          const float2 l = __fadd2_rn(B[j], make_float2(-h.x, -h.y));
-          hi[2 * j] = h.x;
-          hi[2 * j + 1] = h.y;
-          lo[2 * j] = l.x;
-          lo[2 * j + 1] = l.y;
-        }
-#pragma unroll
-        for (int m = 0; m < 8; ++m) {
-          bh[m] = pack_h2(hi[m], hi[m + 8]);
-          bl[m] = pack_h2(lo[m], lo[m + 8]);
-        }
-      }
-#pragma unroll
-      for (int mt = 0; mt < kMt; ++mt) {
-        const Shifted s0 = shifted(kw[mt][2 * hw]), s1 = shifted(kw[mt][2 * hw + 1]);
+        for (int mt = 0; mt < kMt; ++mt) {
+          const Shifted s0 = shifted(kw[mt][2 * hw]), s1 = shifted(kw[mt][2 * hw + 1]);
 #define OTT_QK(MM)                                                                      \
   {                                                                                     \
     const uint32_t a0 = kq<MM>(s0, magic), a1 = kq<MM>(s1, magic);                      \
     const uint32_t a2 = kq<MM + 1>(s0, magic), a3 = kq<MM + 1>(s1, magic);              \
-    mma16816(ch[mt], a0, a1, a2, a3, bh[MM], bh[MM + 1]);                               \
-    mma16816(cl[mt], a0, a1, a2, a3, bl[MM], bl[MM + 1]);                               \
+    mma16816(ch[mt], a0, a1, a2, a3, bh[(MM) & 3], bh[((MM) & 3) + 1]);                 \
+    mma16816(cl[mt], a0, a1, a2, a3, bl[(MM) & 3], bl[((MM) & 3) + 1]);                 \
   }
-        OTT_QK(0) OTT_QK(2) OTT_QK(4) OTT_QK(6)
+          if (half == 0) {
+            OTT_QK(0) OTT_QK(2)
+          } else {
+            OTT_QK(4) OTT_QK(6)
+          }
 #undef OTT_QK
+        }
       }
     }
     float bias = bias2.x + bias2.y;
@@ -583,8 +617,10 @@ __device__ void mma_body(const AttnArgs& a, MmaSmem<G>& sm) {
     // subnormals the accumulator holds sum(p step c) * 2^-14 (even pairs) or 2^-16)
 #pragma unroll
     for (int mt = 0; mt < kMt; ++mt) {
-      const float vs0 = vstep[mt * 16 + g], vs1 = vstep[mt * 16 + g + 8];
-      const float ve0 = vxmin[mt * 16 + g], ve1 = vxmin[mt * 16 + g + 8];
+      const float vs0 = *reinterpret_cast<const float*>(rec + swz(L.v_step() + 4 * (mt * 16 + g)));
+      const float vs1 = *reinterpret_cast<const float*>(rec + swz(L.v_step() + 4 * (mt * 16 + g + 8)));
+      const float ve0 = *reinterpret_cast<const float*>(rec + swz(L.v_xmin() + 4 * (mt * 16 + g)));
+      const float ve1 = *reinterpret_cast<const float*>(rec + swz(L.v_xmin() + 4 * (mt * 16 + g + 8)));
       const float p00 = ex2(sc[mt][0] - me0), p01 = ex2(sc[mt][1] - me1);
       const float p10 = ex2(sc[mt][2] - me0), p11 = ex2(sc[mt][3] - me1);
       lsum[0] += p00 + p10;
@@ -595,7 +631,7 @@ __device__ void mma_body(const AttnArgs& a, MmaSmem<G>& sm) {
       const uint32_t b0 = movm_t(pack_h2(p00 * f0, p01 * f0));
       const uint32_t b1 = movm_t(pack_h2(p10 * f1, p11 * f1));
       uint32_t vr[4];
-      ldsm_x4_t(vr, rec_s + L.v_codes() + mt * 16 * 32 + lm_off);
+      ldsm_x4_t(vr, rec_s + swz(L.v_codes() + mt * 16 * 32 + lm_off));
       const Shifted v0 = shifted(vr[0]), v1 = shifted(vr[1]), v2 = shifted(vr[2]), v3 = shifted(vr[3]);
 #define OTT_PV(CM) mma16816(o[CM], vq<CM>(v0), vq<CM>(v2), vq<CM>(v1), vq<CM>(v3), b0, b1);
       OTT_PV(0) OTT_PV(1) OTT_PV(2) OTT_PV(3) OTT_PV(4) OTT_PV(5) OTT_PV(6) OTT_PV(7)
@@ -605,7 +641,7 @@ __device__ void mma_body(const AttnArgs& a, MmaSmem<G>& sm) {
     __syncwarp();
     if (lane == 0 && k + kStages < my_n) {
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      tma_bulk_load(rec_s, unit_rec + (size_t)(gi + kStages * kAttnWarps) * kRec, kRec, bar0 + 8 * s);
+      load_record<G>(rec_s, tmap, unit_rec + gi + kStages * kAttnWarps, bar0 + 8 * s);
     }
   }
 
@@ -863,12 +899,13 @@ __device__ void fp_body(const AttnArgs& a, FpSmem& sm) {
 }
 
 template <int NR, int G>
-__global__ void __launch_bounds__(kAttnThreads, OTT_MMA_MIN_BLOCKS) attend_mma_kernel(AttnArgs a) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
+__global__ void __launch_bounds__(kAttnThreads, OTT_MMA_MIN_BLOCKS)
+    attend_mma_kernel(const __grid_constant__ AttnArgs a, const __grid_constant__ CUtensorMap tmap) {
+  extern __shared__ __align__(256) unsigned char smem_raw[];
   if ((int)blockIdx.y == a.n_qsplits) {  // full-precision tiers: pool.entries + pending window
     fp_body<NR>(a, *reinterpret_cast<FpSmem*>(smem_raw));
   } else {
-    mma_body<NR, G>(a, *reinterpret_cast<MmaSmem<G>*>(smem_raw));
+    mma_body<NR, G>(a, &tmap, *reinterpret_cast<MmaSmem<G>*>(smem_raw));
   }
 }
 
@@ -945,13 +982,37 @@ static cudaError_t launch_simt_t(const AttnArgs& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// Tensor map over all block records of the cache: 2-D uint8 view [rows of 32 B],
+// SWIZZLE_32B, one (or two) boxes per record. Encoded per launch (host only).
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+static cudaError_t record_tensor_map(const ott_cache_t& c, int box_rows, int rec_rows, CUtensorMap* map) {
+  if (!g_encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn) return cudaErrorNotSupported;
+    g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const cuuint64_t dims[2] = {32, (cuuint64_t)c.n_units * (cuuint64_t)c.max_groups * (cuuint64_t)rec_rows};
+  const cuuint64_t strides[1] = {32};
+  const cuuint32_t box[2] = {32, (cuuint32_t)box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, c.blocks, dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 template <int NR, int G>
 static cudaError_t launch_mma_t(const AttnArgs& a, cudaStream_t st) {
+  CUtensorMap tmap;
+  cudaError_t te = record_tensor_map(a.c, RecTma<G>::kBoxRows, RecTma<G>::kRows, &tmap);
+  if (te != cudaSuccess) return te;
   const size_t smem = sizeof(MmaSmem<G>) > sizeof(FpSmem) ? sizeof(MmaSmem<G>) : sizeof(FpSmem);
   cudaError_t e =
       cudaFuncSetAttribute(attend_mma_kernel<NR, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  attend_mma_kernel<NR, G><<<dim3(a.c.n_units, a.n_splits), kAttnThreads, smem, st>>>(a);
+  attend_mma_kernel<NR, G><<<dim3(a.c.n_units, a.n_splits), kAttnThreads, smem, st>>>(a, tmap);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   combine_kernel<128><<<a.c.n_units * NR, 128, 0, st>>>(a.ws, a.out, a.n_splits);
