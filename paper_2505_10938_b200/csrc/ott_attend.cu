@@ -267,7 +267,7 @@ __device__ void simt_body(const AttnArgs& a, int u, int t_begin, int t_end, int 
 
 template <int NR, int D>
 __global__ void __launch_bounds__(kAttnThreads) attend_simt_kernel(AttnArgs a) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
+  extern __shared__ __align__(256) unsigned char smem_raw[];
   SimtSmem<NR, D>& sm = *reinterpret_cast<SimtSmem<NR, D>*>(smem_raw);
   const int n_tiles = a.n_qtiles + a.n_ptiles + a.n_rtiles;
   const int per = (n_tiles + a.n_splits - 1) / a.n_splits;
@@ -389,7 +389,10 @@ __device__ __forceinline__ void load_record(uint32_t dst, const CUtensorMap* map
 template <int G>
 struct MmaSmem {
   static constexpr int kRec = G * 128 / 2 + 8 * 128 + 8 * G;  // record bytes at d = 128
-  static constexpr int kStages = 2;                           // TMA pipeline depth per warp
+#ifndef OTT_STAGES
+#define OTT_STAGES 2
+#endif
+  static constexpr int kStages = G == 32 ? OTT_STAGES : 2;   // TMA pipeline depth per warp
   // q * 4 * scale_log2 in per-lane order: [hw][v4][lane] = head lane/4, channels
   // 16*(lane%4 + 4*hw) + 4*v4 .. +3  (conflict-free LDS.128)
   float4 q4p[2][4][32];
