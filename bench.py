@@ -167,13 +167,13 @@ def run_ours(args, wl, rank, world, local_rank):
     import torch.distributed as dist
 
     from paper_2505_10938_b200 import EngineConfig, OTTCache
+    from paper_2505_10938_b200.parallel import all_gather_heads, shard_bounds
     from paper_2505_10938_b200.workloads import decode_rows, fill_prefill
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
-    if wl.batch % world:
-        raise SystemExit(f"batch {wl.batch} not divisible by world size {world}")
-    B = wl.batch // world  # whole sequences per rank (batch x kv-head partitioning)
+    b_lo, b_hi = shard_bounds(wl.batch, world, rank)
+    B = b_hi - b_lo  # whole sequences per rank (batch x kv-head partitioning)
     H, Hq, d, L = wl.n_kv_heads, wl.n_q_heads, wl.head_dim, wl.n_layers
     cfg = EngineConfig(bits=2, group_size=wl.group_size, residual=wl.residual, outlier_num=wl.outlier_num,
                        aux_capacity=wl.aux_capacity, skip_layers=wl.skip_layers, n_layers=L, n_heads=H, head_dim=d)
@@ -220,7 +220,7 @@ def run_ours(args, wl, rank, world, local_rank):
                 ev[l][1].record()
             launches["n"] += 2
             if gathered is not None:
-                dist.all_gather_into_tensor(gathered[l], outs[l])
+                all_gather_heads(outs[l], out=gathered[l])
 
     for i in range(args.warmup):
         step(i)
@@ -301,8 +301,8 @@ def run_ours(args, wl, rank, world, local_rank):
                 caches[l].append(k_d, v_d)
                 caches[l].attend(q_d, out=outs[l], n_splits=splits[l])
                 if gathered is not None:
-                    dist.all_gather_into_tensor(gathered[l], outs[l])
-                    o_h[l].copy_(gathered[l][rank * B:(rank + 1) * B], non_blocking=True)
+                    all_gather_heads(outs[l], out=gathered[l])
+                    o_h[l].copy_(gathered[l][b_lo:b_hi], non_blocking=True)
                 else:
                     o_h[l].copy_(outs[l], non_blocking=True)
         e1.record()
