@@ -31,6 +31,16 @@
 
 namespace ott {
 
+// hi and lo products of Q K^T accumulate into one chain (1) or two (0); one
+// chain measured ~1% faster (fewer registers, 8 fewer FADD per group)
+#ifndef OTT_SINGLE_CHAIN
+#define OTT_SINGLE_CHAIN 1
+#endif
+#if OTT_SINGLE_CHAIN
+#define OTT_LO_ACC ch
+#else
+#define OTT_LO_ACC cl
+#endif
 #ifndef OTT_MMA_MIN_BLOCKS
 #define OTT_MMA_MIN_BLOCKS 4
 #endif
@@ -545,7 +555,7 @@ __device__ void mma_body(const AttnArgs& a, const CUtensorMap* tmap, MmaSmem<G>&
     const uint32_t a0 = kq<MM>(s0, magic), a1 = kq<MM>(s1, magic);                      \
     const uint32_t a2 = kq<MM + 1>(s0, magic), a3 = kq<MM + 1>(s1, magic);              \
     mma16816(ch[mt], a0, a1, a2, a3, bh[(MM) & 3], bh[((MM) & 3) + 1]);                 \
-    mma16816(cl[mt], a0, a1, a2, a3, bl[(MM) & 3], bl[((MM) & 3) + 1]);                 \
+    mma16816(OTT_LO_ACC[mt], a0, a1, a2, a3, bl[(MM) & 3], bl[((MM) & 3) + 1]);         \
   }
           if (half == 0) {
             OTT_QK(0) OTT_QK(2)

@@ -103,9 +103,10 @@ int ott_pick_splits(const ott_cache_t* c, int32_t n_rep, int64_t total_tokens) {
   const int64_t n_groups = q_tokens / c->group_size;
   int sms = ott_num_sms();
   if (sms <= 0) sms = 148;
-  // ~24 CTAs of 4 warps per SM over the launch keeps the tail short (CTAs are
-  // scheduled dynamically) while each split streams >= 8 groups (2 per warp).
-  const int64_t target = (int64_t)sms * 24;
+  // ~8 quantized-range CTAs per SM over the launch: longer CTAs amortise their
+  // start-up (first TMA round trip, q staging, merge) — measured best on config 3/4 —
+  // while each split still streams >= 8 groups (2 per warp).
+  const int64_t target = (int64_t)sms * 8;
   int64_t s = (target + c->n_units - 1) / c->n_units;
   const int64_t max_by_groups = n_groups / 8 > 0 ? n_groups / 8 : 1;
   if (s > max_by_groups) s = max_by_groups;
