@@ -289,7 +289,8 @@ __global__ void __launch_bounds__(kAttnThreads) attend_simt_kernel(AttnArgs a) {
 // ============================================================ tensor-core path
 __device__ __forceinline__ void mma16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
                                          uint32_t b0, uint32_t b1) {
-  asm volatile(
+  // not volatile: a pure register op, so the scheduler may interleave independent chains
+  asm(
       "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
       "{%0,%1,%2,%3};\n"
       : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
@@ -312,7 +313,7 @@ __device__ __forceinline__ float ex2(float x) {  // 2^x, MUFU.EX2 (ftz; -inf -> 
 }
 __device__ __forceinline__ uint32_t movm_t(uint32_t x) {
   uint32_t y;
-  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;\n" : "=r"(y) : "r"(x));
+  asm("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;\n" : "=r"(y) : "r"(x));
   return y;
 }
 __device__ __forceinline__ uint32_t pack_h2(float lo, float hi) {
@@ -399,18 +400,28 @@ __device__ __forceinline__ void load_record(uint32_t dst, const CUtensorMap* map
 template <int G>
 struct MmaSmem {
   static constexpr int kRec = G * 128 / 2 + 8 * 128 + 8 * G;  // record bytes at d = 128
+#ifndef OTT_NO_TMA
+#define OTT_NO_TMA 0  // timing experiment only: compute on stale shared memory
+#endif
+#ifndef OTT_Q_IN_REGS
+#define OTT_Q_IN_REGS 0
+#endif
+#ifndef OTT_NG
+#define OTT_NG 1  // groups per loop iteration per warp (2 measured slower: register spills)
+#endif
 #ifndef OTT_STAGES
 #define OTT_STAGES 2
 #endif
-  static constexpr int kStages = G == 32 ? OTT_STAGES : 2;   // TMA pipeline depth per warp
+  static constexpr int kNG = G == 32 ? OTT_NG : 1;               // groups per loop iteration
+  static constexpr int kStages = G == 32 ? OTT_STAGES : 2;          // TMA pipeline depth per warp
   // q * 4 * scale_log2 in per-lane order: [hw][v4][lane] = head lane/4, channels
   // 16*(lane%4 + 4*hw) + 4*v4 .. +3  (conflict-free LDS.128)
   float4 q4p[2][4][32];
   // per-group channel scratch [hw][slot], slot = 4*v4 + (tig ^ 2*(v4>>1)) (bank-conflict
   // free for the lane-ordered writes and the per-tig broadcast reads): step * f and
   // x_min - 4 f step with f = 4^(4 - P(m))
-  float4 stp[kAttnWarps][2][16];
-  float4 esc[kAttnWarps][2][16];
+  float4 stp[kAttnWarps][kNG][2][16];
+  float4 esc[kAttnWarps][kNG][2][16];
   // group records land here through a SWIZZLE_32B tensor map (16-byte chunk bit 4 ^= bit 7
   // of the offset): ldmatrix over 32-byte token rows is then bank-conflict free
   alignas(256) uint8_t stage[kAttnWarps][kStages][kRec];
@@ -458,7 +469,8 @@ __device__ void mma_body(const AttnArgs& a, const CUtensorMap* tmap, MmaSmem<G>&
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
 #pragma unroll
     for (int s = 0; s < kStages; ++s)
-      if (s < my_n) load_record<G>(stage0 + s * kRec, tmap, unit_rec + g0 + warp + s * kAttnWarps, bar0 + 8 * s);
+      if (s < my_n && !OTT_NO_TMA)
+        load_record<G>(stage0 + s * kRec, tmap, unit_rec + g0 + warp + s * kAttnWarps, bar0 + 8 * s);
   }
   __syncthreads();
 
@@ -474,121 +486,152 @@ __device__ void mma_body(const AttnArgs& a, const CUtensorMap* tmap, MmaSmem<G>&
   const uint32_t lm_off = (uint32_t)(((lane & 7) + ((lane >> 3) & 1) * 8) * 32 + (lane >> 4) * 16);
   // cooperative channel pass: lane owns channels 4*lane..+3 = word lane/4, v4 = lane%4
   const int cw = lane >> 2;
-  float4* stp_w = &sm.stp[warp][cw >> 2][tile_slot(lane & 3, cw & 3)];
-  float4* esc_w = &sm.esc[warp][cw >> 2][tile_slot(lane & 3, cw & 3)];
+  float4* stp_w = &sm.stp[warp][0][cw >> 2][tile_slot(lane & 3, cw & 3)];  // + j*32 for group j
+  float4* esc_w = &sm.esc[warp][0][cw >> 2][tile_slot(lane & 3, cw & 3)];
   // f = 4^(4 - P(m)) for this lane's pairs: m = 0..3 -> {4, 1, 16, 4}; m = 4..7 -> {1, 16, 4, 1}
   const float4 cf = (lane & 1) ? make_float4(1.f, 16.f, 4.f, 1.f) : make_float4(4.f, 1.f, 16.f, 4.f);
 
-  for (int k = 0; k < my_n; ++k) {
-    const int s = k % kStages;
-    const int gi = g0 + warp + k * kAttnWarps;
-    uint32_t mwords[G / 32];
+#if OTT_Q_IN_REGS
+  float4 qreg[2][4];
 #pragma unroll
-    for (int w = 0; w < G / 32; ++w) mwords[w] = __ldg(&pmask[(size_t)gi * (G / 32) + w]);
-    mbar_wait(bar0 + 8 * s, (uint32_t)((k / kStages) & 1));
-    const uint8_t* rec = &sm.stage[warp][s][0];
-    const uint32_t rec_s = stage0 + s * kRec;
-
-    // ---- channel pass: step * f and e = x_min - 4 f step with f = 4^(4 - P(m))
-    // (lane holds channels 4*lane..+3 = pairs m = 4*(lane&1) + 0..3)
-    {
-      const float4 st = *reinterpret_cast<const float4*>(rec + swz(L.k_step() + 16 * lane));
-      const float4 mn = *reinterpret_cast<const float4*>(rec + swz(L.k_xmin() + 16 * lane));
-      *stp_w = make_float4(st.x * cf.x, st.y * cf.y, st.z * cf.z, st.w * cf.w);
-      *esc_w = make_float4(fmaf(-4.f * cf.x, st.x, mn.x), fmaf(-4.f * cf.y, st.y, mn.y), fmaf(-4.f * cf.z, st.z, mn.z),
-                           fmaf(-4.f * cf.w, st.w, mn.w));
+  for (int hw = 0; hw < 2; ++hw)
+#pragma unroll
+    for (int v4 = 0; v4 < 4; ++v4) qreg[hw][v4] = sm.q4p[hw][v4][lane];
+#endif
+  // Groups are processed NG at a time (two independent instruction streams per
+  // warp for the scheduler); a lone tail group is paired with a masked dummy.
+  constexpr int NG = MmaSmem<G>::kNG;
+  for (int k = 0; k < my_n; k += NG) {
+    const int ng = min(NG, my_n - k);
+    const uint8_t* rec[NG];
+    uint32_t rec_s[NG];
+    uint32_t mwords[NG][G / 32];
+#pragma unroll
+    for (int j = 0; j < NG; ++j) {
+      const int kk = k + (j < ng ? j : 0);
+      const int gi = g0 + warp + kk * kAttnWarps;
+#pragma unroll
+      for (int w = 0; w < G / 32; ++w) mwords[j][w] = __ldg(&pmask[(size_t)gi * (G / 32) + w]);
+      const int s = kk % kStages;
+      if (j < ng && !OTT_NO_TMA) mbar_wait(bar0 + 8 * s, (uint32_t)((kk / kStages) & 1));
+      rec[j] = &sm.stage[warp][s][0];
+      rec_s[j] = stage0 + s * kRec;
     }
-    // K code words of every m-tile (ldmatrix: token g / g+8, words tig and 4+tig)
-    uint32_t kw[kMt][4];
+    uint32_t kw[NG][kMt][4];
 #pragma unroll
-    for (int mt = 0; mt < kMt; ++mt) ldsm_x4(kw[mt], rec_s + swz(L.k_codes() + mt * 16 * 32 + lm_off));
+    for (int j = 0; j < NG; ++j) {
+      // channel pass: step * f and e = x_min - 4 f step with f = 4^(4 - P(m))
+      const float4 st = *reinterpret_cast<const float4*>(rec[j] + swz(L.k_step() + 16 * lane));
+      const float4 mn = *reinterpret_cast<const float4*>(rec[j] + swz(L.k_xmin() + 16 * lane));
+      stp_w[j * 32] = make_float4(st.x * cf.x, st.y * cf.y, st.z * cf.z, st.w * cf.w);
+      esc_w[j * 32] = make_float4(fmaf(-4.f * cf.x, st.x, mn.x), fmaf(-4.f * cf.y, st.y, mn.y),
+                                  fmaf(-4.f * cf.z, st.z, mn.z), fmaf(-4.f * cf.w, st.w, mn.w));
+      // K code words (ldmatrix: token g / g+8, words tig and 4+tig)
+#pragma unroll
+      for (int mt = 0; mt < kMt; ++mt) ldsm_x4(kw[j][mt], rec_s[j] + swz(L.k_codes() + mt * 16 * 32 + lm_off));
+    }
     __syncwarp();
 
-    // ---- S = Q K^T, one 16-channel word half (hw) at a time: B operand q' =
-    // q4 * step * f as hi/lo fp16 pairs (channels m, m+8), two accumulator chains
-    // (hi, lo) per m-tile, K bias (x_min terms) added at the end.
-    float ch[kMt][4], cl[kMt][4];
+    // ---- S = Q K^T: B operand q' = q4 * step * f as hi/lo fp16 pairs (channels m,
+    // m+8) built one (hw, half) slice at a time; hi and lo accumulate into one chain
+    float ch[NG][kMt][4];
+    float2 bias2[NG];
+#if OTT_Q_IN_REGS
+    // (q4 lives in registers, loaded once per CTA: qreg[hw][v4])
+#endif
 #pragma unroll
-    for (int mt = 0; mt < kMt; ++mt)
+    for (int j = 0; j < NG; ++j) {
+      bias2[j] = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) ch[mt][j] = cl[mt][j] = 0.f;
-    float2 bias2 = make_float2(0.f, 0.f);
+      for (int mt = 0; mt < kMt; ++mt) ch[j][mt][0] = ch[j][mt][1] = ch[j][mt][2] = ch[j][mt][3] = 0.f;
+    }
 #pragma unroll
     for (int hw = 0; hw < 2; ++hw) {
 #pragma unroll
       for (int half = 0; half < 2; ++half) {  // pairs m = 4*half .. 4*half+3 (channels m, m+8)
-        uint32_t bh[4], bl[4];
 #pragma unroll
-        for (int pp = 0; pp < 2; ++pp) {  // v4 = half (channels 4*half..+3), v4 = 2 + half (+8)
-          const int v4 = half + 2 * pp;
-          const float4 q4 = sm.q4p[hw][v4][lane];
-          const float4 s4 = sm.stp[warp][hw][tile_slot(v4, tig)];
-          const float4 e4 = sm.esc[warp][hw][tile_slot(v4, tig)];
-          const float2 q0 = make_float2(q4.x, q4.y), q1 = make_float2(q4.z, q4.w);
-          const float2 B0 = __fmul2_rn(q0, make_float2(s4.x, s4.y));
-          const float2 B1 = __fmul2_rn(q1, make_float2(s4.z, s4.w));
-          bias2 = __ffma2_rn(q0, make_float2(e4.x, e4.y), bias2);
-          bias2 = __ffma2_rn(q1, make_float2(e4.z, e4.w), bias2);
-          const float2 h0 = make_float2(__uint_as_float(__float_as_uint(B0.x) & 0xFFFFE000u),
-                                        __uint_as_float(__float_as_uint(B0.y) & 0xFFFFE000u));
-          const float2 h1 = make_float2(__uint_as_float(__float_as_uint(B1.x) & 0xFFFFE000u),
-                                        __uint_as_float(__float_as_uint(B1.y) & 0xFFFFE000u));
-          const float2 l0 = __fadd2_rn(B0, make_float2(-h0.x, -h0.y));
-          const float2 l1 = __fadd2_rn(B1, make_float2(-h1.x, -h1.y));
-          if (pp == 0) {  // low channel of each pair
-            bh[0] = __float_as_uint(h0.x); bh[1] = __float_as_uint(h0.y);
-            bh[2] = __float_as_uint(h1.x); bh[3] = __float_as_uint(h1.y);
-            bl[0] = __float_as_uint(l0.x); bl[1] = __float_as_uint(l0.y);
-            bl[2] = __float_as_uint(l1.x); bl[3] = __float_as_uint(l1.y);
-          } else {  // pack (low, high = channel + 8)
-            bh[0] = pack_h2(__uint_as_float(bh[0]), h0.x); bh[1] = pack_h2(__uint_as_float(bh[1]), h0.y);
-            bh[2] = pack_h2(__uint_as_float(bh[2]), h1.x); bh[3] = pack_h2(__uint_as_float(bh[3]), h1.y);
-            bl[0] = pack_h2(__uint_as_float(bl[0]), l0.x); bl[1] = pack_h2(__uint_as_float(bl[1]), l0.y);
-            bl[2] = pack_h2(__uint_as_float(bl[2]), l1.x); bl[3] = pack_h2(__uint_as_float(bl[3]), l1.y);
+        for (int j = 0; j < NG; ++j) {
+          uint32_t bh[4], bl[4];
+#pragma unroll
+          for (int pp = 0; pp < 2; ++pp) {  // v4 = half (channels 4*half..+3), v4 = 2 + half (+8)
+            const int v4 = half + 2 * pp;
+#if OTT_Q_IN_REGS
+            const float4 q4 = qreg[hw][v4];
+#else
+            const float4 q4 = sm.q4p[hw][v4][lane];
+#endif
+            const float4 s4 = sm.stp[warp][j][hw][tile_slot(v4, tig)];
+            const float4 e4 = sm.esc[warp][j][hw][tile_slot(v4, tig)];
+            const float2 q0 = make_float2(q4.x, q4.y), q1 = make_float2(q4.z, q4.w);
+            const float2 B0 = __fmul2_rn(q0, make_float2(s4.x, s4.y));
+            const float2 B1 = __fmul2_rn(q1, make_float2(s4.z, s4.w));
+            bias2[j] = __ffma2_rn(q0, make_float2(e4.x, e4.y), bias2[j]);
+            bias2[j] = __ffma2_rn(q1, make_float2(e4.z, e4.w), bias2[j]);
+            const float2 h0 = make_float2(__uint_as_float(__float_as_uint(B0.x) & 0xFFFFE000u),
+                                          __uint_as_float(__float_as_uint(B0.y) & 0xFFFFE000u));
+            const float2 h1 = make_float2(__uint_as_float(__float_as_uint(B1.x) & 0xFFFFE000u),
+                                          __uint_as_float(__float_as_uint(B1.y) & 0xFFFFE000u));
+            const float2 l0 = __fadd2_rn(B0, make_float2(-h0.x, -h0.y));
+            const float2 l1 = __fadd2_rn(B1, make_float2(-h1.x, -h1.y));
+            if (pp == 0) {  // low channel of each pair
+              bh[0] = __float_as_uint(h0.x); bh[1] = __float_as_uint(h0.y);
+              bh[2] = __float_as_uint(h1.x); bh[3] = __float_as_uint(h1.y);
+              bl[0] = __float_as_uint(l0.x); bl[1] = __float_as_uint(l0.y);
+              bl[2] = __float_as_uint(l1.x); bl[3] = __float_as_uint(l1.y);
+            } else {  // pack (low, high = channel + 8)
+              bh[0] = pack_h2(__uint_as_float(bh[0]), h0.x); bh[1] = pack_h2(__uint_as_float(bh[1]), h0.y);
+              bh[2] = pack_h2(__uint_as_float(bh[2]), h1.x); bh[3] = pack_h2(__uint_as_float(bh[3]), h1.y);
+              bl[0] = pack_h2(__uint_as_float(bl[0]), l0.x); bl[1] = pack_h2(__uint_as_float(bl[1]), l0.y);
+              bl[2] = pack_h2(__uint_as_float(bl[2]), l1.x); bl[3] = pack_h2(__uint_as_float(bl[3]), l1.y);
+            }
           }
-        }
 #pragma unroll
-        for (int mt = 0; mt < kMt; ++mt) {
-          const Shifted s0 = shifted(kw[mt][2 * hw]), s1 = shifted(kw[mt][2 * hw + 1]);
+          for (int mt = 0; mt < kMt; ++mt) {
+            const Shifted s0 = shifted(kw[j][mt][2 * hw]), s1 = shifted(kw[j][mt][2 * hw + 1]);
 #define OTT_QK(MM)                                                                      \
   {                                                                                     \
     const uint32_t a0 = kq<MM>(s0, magic), a1 = kq<MM>(s1, magic);                      \
     const uint32_t a2 = kq<MM + 1>(s0, magic), a3 = kq<MM + 1>(s1, magic);              \
-    mma16816(ch[mt], a0, a1, a2, a3, bh[(MM) & 3], bh[((MM) & 3) + 1]);                 \
-    mma16816(OTT_LO_ACC[mt], a0, a1, a2, a3, bl[(MM) & 3], bl[((MM) & 3) + 1]);         \
+    mma16816(ch[j][mt], a0, a1, a2, a3, bh[(MM) & 3], bh[((MM) & 3) + 1]);              \
+    mma16816(ch[j][mt], a0, a1, a2, a3, bl[(MM) & 3], bl[((MM) & 3) + 1]);              \
   }
-          if (half == 0) {
-            OTT_QK(0) OTT_QK(2)
-          } else {
-            OTT_QK(4) OTT_QK(6)
-          }
+            if (half == 0) {
+              OTT_QK(0) OTT_QK(2)
+            } else {
+              OTT_QK(4) OTT_QK(6)
+            }
 #undef OTT_QK
+          }
         }
       }
     }
-    float bias = bias2.x + bias2.y;
-    bias += __shfl_xor_sync(0xffffffffu, bias, 1);
-    bias += __shfl_xor_sync(0xffffffffu, bias, 2);
-    bias *= 0.25f;
-    const float bias0 = __shfl_sync(0xffffffffu, bias, 8 * tig);      // head 2*tig
-    const float bias1 = __shfl_sync(0xffffffffu, bias, 8 * tig + 4);  // head 2*tig+1
-    float sc[kMt][4];
+    float sc[NG][kMt][4];
 #pragma unroll
-    for (int mt = 0; mt < kMt; ++mt) {
-      sc[mt][0] = ch[mt][0] + cl[mt][0] + bias0;
-      sc[mt][1] = ch[mt][1] + cl[mt][1] + bias1;
-      sc[mt][2] = ch[mt][2] + cl[mt][2] + bias0;
-      sc[mt][3] = ch[mt][3] + cl[mt][3] + bias1;
-    }
-    // pooled positions: their logits come from the pool tile (overwrite semantics)
+    for (int j = 0; j < NG; ++j) {
+      float bias = bias2[j].x + bias2[j].y;
+      bias += __shfl_xor_sync(0xffffffffu, bias, 1);
+      bias += __shfl_xor_sync(0xffffffffu, bias, 2);
+      bias *= 0.25f;
+      const float bias0 = __shfl_sync(0xffffffffu, bias, 8 * tig);      // head 2*tig
+      const float bias1 = __shfl_sync(0xffffffffu, bias, 8 * tig + 4);  // head 2*tig+1
+      const bool dummy = j >= ng;
 #pragma unroll
-    for (int w = 0; w < G / 32; ++w) {
-      const uint32_t mw = mwords[w];
-      if (mw) {
+      for (int mt = 0; mt < kMt; ++mt) {
+        sc[j][mt][0] = dummy ? -INFINITY : ch[j][mt][0] + bias0;
+        sc[j][mt][1] = dummy ? -INFINITY : ch[j][mt][1] + bias1;
+        sc[j][mt][2] = dummy ? -INFINITY : ch[j][mt][2] + bias0;
+        sc[j][mt][3] = dummy ? -INFINITY : ch[j][mt][3] + bias1;
+      }
+      // pooled positions: their logits come from the pool tile (overwrite semantics)
 #pragma unroll
-        for (int mt = 2 * w; mt < 2 * w + 2; ++mt) {
-          if ((mw >> ((mt & 1) * 16 + g)) & 1u) sc[mt][0] = sc[mt][1] = -INFINITY;
-          if ((mw >> ((mt & 1) * 16 + g + 8)) & 1u) sc[mt][2] = sc[mt][3] = -INFINITY;
+      for (int w = 0; w < G / 32; ++w) {
+        const uint32_t mw = mwords[j][w];
+        if (mw) {
+#pragma unroll
+          for (int mt = 2 * w; mt < 2 * w + 2; ++mt) {
+            if ((mw >> ((mt & 1) * 16 + g)) & 1u) sc[j][mt][0] = sc[j][mt][1] = -INFINITY;
+            if ((mw >> ((mt & 1) * 16 + g + 8)) & 1u) sc[j][mt][2] = sc[j][mt][3] = -INFINITY;
+          }
         }
       }
     }
@@ -600,7 +643,9 @@ __device__ void mma_body(const AttnArgs& a, const CUtensorMap* tmap, MmaSmem<G>&
     for (int h = 0; h < 2; ++h) {
       float t = -INFINITY;
 #pragma unroll
-      for (int mt = 0; mt < kMt; ++mt) t = fmaxf(t, fmaxf(sc[mt][h], sc[mt][h + 2]));
+      for (int j = 0; j < NG; ++j)
+#pragma unroll
+        for (int mt = 0; mt < kMt; ++mt) t = fmaxf(t, fmaxf(sc[j][mt][h], sc[j][mt][h + 2]));
       tmax[h] = t;
     }
     const bool need = tmax[0] > mrun[0] + kLazy || tmax[1] > mrun[1] + kLazy;
@@ -627,34 +672,44 @@ __device__ void mma_body(const AttnArgs& a, const CUtensorMap* tmap, MmaSmem<G>&
     const float me1 = mrun[1] == -INFINITY ? 0.f : mrun[1];
 
     // ---- O^T += V^T P'  (P' = 4 p step fp16, V x_min into vb; with V codes as
-    // subnormals the accumulator holds sum(p step c) * 2^-14 (even pairs) or 2^-16)
+    // subnormals the accumulator holds sum(p step c) * 2^(2P-22))
 #pragma unroll
-    for (int mt = 0; mt < kMt; ++mt) {
-      const float vs0 = *reinterpret_cast<const float*>(rec + swz(L.v_step() + 4 * (mt * 16 + g)));
-      const float vs1 = *reinterpret_cast<const float*>(rec + swz(L.v_step() + 4 * (mt * 16 + g + 8)));
-      const float ve0 = *reinterpret_cast<const float*>(rec + swz(L.v_xmin() + 4 * (mt * 16 + g)));
-      const float ve1 = *reinterpret_cast<const float*>(rec + swz(L.v_xmin() + 4 * (mt * 16 + g + 8)));
-      const float p00 = ex2(sc[mt][0] - me0), p01 = ex2(sc[mt][1] - me1);
-      const float p10 = ex2(sc[mt][2] - me0), p11 = ex2(sc[mt][3] - me1);
-      lsum[0] += p00 + p10;
-      lsum[1] += p01 + p11;
-      vb[0] = fmaf(p00, ve0, fmaf(p10, ve1, vb[0]));
-      vb[1] = fmaf(p01, ve0, fmaf(p11, ve1, vb[1]));
-      const float f0 = 4.f * vs0, f1 = 4.f * vs1;
-      const uint32_t b0 = movm_t(pack_h2(p00 * f0, p01 * f0));
-      const uint32_t b1 = movm_t(pack_h2(p10 * f1, p11 * f1));
-      uint32_t vr[4];
-      ldsm_x4_t(vr, rec_s + swz(L.v_codes() + mt * 16 * 32 + lm_off));
-      const Shifted v0 = shifted(vr[0]), v1 = shifted(vr[1]), v2 = shifted(vr[2]), v3 = shifted(vr[3]);
+    for (int j = 0; j < NG; ++j) {
+#pragma unroll
+      for (int mt = 0; mt < kMt; ++mt) {
+        const float vs0 = *reinterpret_cast<const float*>(rec[j] + swz(L.v_step() + 4 * (mt * 16 + g)));
+        const float vs1 = *reinterpret_cast<const float*>(rec[j] + swz(L.v_step() + 4 * (mt * 16 + g + 8)));
+        const float ve0 = *reinterpret_cast<const float*>(rec[j] + swz(L.v_xmin() + 4 * (mt * 16 + g)));
+        const float ve1 = *reinterpret_cast<const float*>(rec[j] + swz(L.v_xmin() + 4 * (mt * 16 + g + 8)));
+        const float p00 = ex2(sc[j][mt][0] - me0), p01 = ex2(sc[j][mt][1] - me1);
+        const float p10 = ex2(sc[j][mt][2] - me0), p11 = ex2(sc[j][mt][3] - me1);
+        lsum[0] += p00 + p10;
+        lsum[1] += p01 + p11;
+        vb[0] = fmaf(p00, ve0, fmaf(p10, ve1, vb[0]));
+        vb[1] = fmaf(p01, ve0, fmaf(p11, ve1, vb[1]));
+        const float f0 = 4.f * vs0, f1 = 4.f * vs1;
+        const uint32_t b0 = movm_t(pack_h2(p00 * f0, p01 * f0));
+        const uint32_t b1 = movm_t(pack_h2(p10 * f1, p11 * f1));
+        uint32_t vr[4];
+        ldsm_x4_t(vr, rec_s[j] + swz(L.v_codes() + mt * 16 * 32 + lm_off));
+        const Shifted v0 = shifted(vr[0]), v1 = shifted(vr[1]), v2 = shifted(vr[2]), v3 = shifted(vr[3]);
 #define OTT_PV(CM) mma16816(o[CM], vq<CM>(v0), vq<CM>(v2), vq<CM>(v1), vq<CM>(v3), b0, b1);
-      OTT_PV(0) OTT_PV(1) OTT_PV(2) OTT_PV(3) OTT_PV(4) OTT_PV(5) OTT_PV(6) OTT_PV(7)
+        OTT_PV(0) OTT_PV(1) OTT_PV(2) OTT_PV(3) OTT_PV(4) OTT_PV(5) OTT_PV(6) OTT_PV(7)
 #undef OTT_PV
+      }
     }
 
     __syncwarp();
-    if (lane == 0 && k + kStages < my_n) {
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      load_record<G>(rec_s, tmap, unit_rec + gi + kStages * kAttnWarps, bar0 + 8 * s);
+    if (lane == 0) {
+#pragma unroll
+      for (int j = 0; j < NG; ++j) {
+        const int kk = k + j, ka = kk + kStages;
+        if (j < ng && ka < my_n && !OTT_NO_TMA) {
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+          load_record<G>(stage0 + (kk % kStages) * kRec, tmap, unit_rec + g0 + warp + ka * kAttnWarps,
+                         bar0 + 8 * (kk % kStages));
+        }
+      }
     }
   }
 
