@@ -365,3 +365,41 @@ def test_graft_smoke():
     import __graft_entry__
 
     __graft_entry__.smoke()
+
+
+@pytest.mark.parametrize("N", [32, 3])
+def test_config2_streaming_stress_sampled(N):
+    """BASELINE config 2: B=4, H=32, d=128, prefill 32,768 tokens then 1,024 decode appends with
+    fresh outlier tokens injected at 1 %; flushes and pool eviction fire repeatedly. Sampled units
+    are checked bit-exact (codes, params, pool/aux order, frozen, substitutions) and attention within
+    tolerance against the oracle replaying the same fp16 stream."""
+    from paper_2505_10938_b200 import OTTCache
+    from paper_2505_10938_b200.workloads import decode_rows, fill_prefill
+
+    B, H, T0, steps, d = 4, 32, 32768, 1024, 128
+    gen = torch.Generator(device="cuda").manual_seed(7)
+    k = torch.empty((B, H, T0, d), dtype=torch.float16, device="cuda")
+    v = torch.empty_like(k)
+    scale = fill_prefill(gen, k, v, n_out_tok=int(0.01 * T0))
+    cache = OTTCache(cfg_of(2, 32, 128, N, 32, d), B, H, max_tokens=T0 + steps)
+    cache.update(k, v)
+    rows_k, rows_v = [], []
+    for _ in range(steps):
+        kr, vr = decode_rows(gen, scale, B, H, outlier_rate=0.01)
+        cache.append(kr, vr)
+        rows_k.append(kr)
+        rows_v.append(vr)
+    q = torch.randn((B, H, d), generator=gen, device="cuda").half()
+    out = cache.attend(q).float().cpu().numpy()
+    kk = torch.cat([k, torch.stack(rows_k, dim=2)], dim=2).cpu().numpy()
+    vv = torch.cat([v, torch.stack(rows_v, dim=2)], dim=2).cpu().numpy()
+    qh = q.cpu().numpy()
+    for b, h in ((0, 0), (1, 17), (3, 31)):
+        ref = oracle.OracleCache(2, 32, 128, N, 32, d)
+        ref.extend(kk[b, h].astype(np.float32), vv[b, h].astype(np.float32))
+        u = cache.unit(b, h)
+        assert_unit_matches_oracle(u, ref, exact64=False)
+        if N == 3:
+            assert not u.pool.frozen and len(u.pool.aux) > 0  # eviction fired, pool still live
+        ok, err = within_tol(out[b, h], ref.attend(qh[b, h].astype(np.float32)))
+        assert ok, (b, h, err)
