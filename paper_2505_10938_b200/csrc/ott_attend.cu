@@ -535,6 +535,9 @@ __device__ void mma_body(const AttnArgs& a, const CUtensorMap* tmap, MmaSmem<G>&
     // ---- S = Q K^T: B operand q' = q4 * step * f as hi/lo fp16 pairs (channels m,
     // m+8) built one (hw, half) slice at a time; hi and lo accumulate into one chain
     float ch[NG][kMt][4];
+#if !OTT_SINGLE_CHAIN
+    float cl[NG][kMt][4];
+#endif
     float2 bias2[NG];
 #if OTT_Q_IN_REGS
     // (q4 lives in registers, loaded once per CTA: qreg[hw][v4])
@@ -543,7 +546,12 @@ __device__ void mma_body(const AttnArgs& a, const CUtensorMap* tmap, MmaSmem<G>&
     for (int j = 0; j < NG; ++j) {
       bias2[j] = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int mt = 0; mt < kMt; ++mt) ch[j][mt][0] = ch[j][mt][1] = ch[j][mt][2] = ch[j][mt][3] = 0.f;
+      for (int mt = 0; mt < kMt; ++mt) {
+        ch[j][mt][0] = ch[j][mt][1] = ch[j][mt][2] = ch[j][mt][3] = 0.f;
+#if !OTT_SINGLE_CHAIN
+        cl[j][mt][0] = cl[j][mt][1] = cl[j][mt][2] = cl[j][mt][3] = 0.f;
+#endif
+      }
     }
 #pragma unroll
     for (int hw = 0; hw < 2; ++hw) {
@@ -585,23 +593,29 @@ __device__ void mma_body(const AttnArgs& a, const CUtensorMap* tmap, MmaSmem<G>&
               bl[2] = pack_h2(__uint_as_float(bl[2]), l1.x); bl[3] = pack_h2(__uint_as_float(bl[3]), l1.y);
             }
           }
+          // slice-major over the m-tiles so consecutive HMMAs feed different
+          // accumulators (hi -> ch, lo -> cl per m-tile: 2*kMt independent chains)
+          Shifted s0[kMt], s1[kMt];
 #pragma unroll
           for (int mt = 0; mt < kMt; ++mt) {
-            const Shifted s0 = shifted(kw[j][mt][2 * hw]), s1 = shifted(kw[j][mt][2 * hw + 1]);
-#define OTT_QK(MM)                                                                      \
-  {                                                                                     \
-    const uint32_t a0 = kq<MM>(s0, magic), a1 = kq<MM>(s1, magic);                      \
-    const uint32_t a2 = kq<MM + 1>(s0, magic), a3 = kq<MM + 1>(s1, magic);              \
-    mma16816(ch[j][mt], a0, a1, a2, a3, bh[(MM) & 3], bh[((MM) & 3) + 1]);              \
-    mma16816(ch[j][mt], a0, a1, a2, a3, bl[(MM) & 3], bl[((MM) & 3) + 1]);              \
-  }
-            if (half == 0) {
-              OTT_QK(0) OTT_QK(2)
-            } else {
-              OTT_QK(4) OTT_QK(6)
-            }
-#undef OTT_QK
+            s0[mt] = shifted(kw[j][mt][2 * hw]);
+            s1[mt] = shifted(kw[j][mt][2 * hw + 1]);
           }
+#define OTT_QK(MM)                                                                        \
+  {                                                                                       \
+    _Pragma("unroll") for (int mt = 0; mt < kMt; ++mt) {                                  \
+      const uint32_t a0 = kq<MM>(s0[mt], magic), a1 = kq<MM>(s1[mt], magic);             \
+      const uint32_t a2 = kq<MM + 1>(s0[mt], magic), a3 = kq<MM + 1>(s1[mt], magic);     \
+      mma16816(ch[j][mt], a0, a1, a2, a3, bh[(MM) & 3], bh[((MM) & 3) + 1]);              \
+      mma16816(OTT_LO_ACC[j][mt], a0, a1, a2, a3, bl[(MM) & 3], bl[((MM) & 3) + 1]);      \
+    }                                                                                     \
+  }
+          if (half == 0) {
+            OTT_QK(0) OTT_QK(2)
+          } else {
+            OTT_QK(4) OTT_QK(6)
+          }
+#undef OTT_QK
         }
       }
     }
@@ -617,6 +631,10 @@ __device__ void mma_body(const AttnArgs& a, const CUtensorMap* tmap, MmaSmem<G>&
       const bool dummy = j >= ng;
 #pragma unroll
       for (int mt = 0; mt < kMt; ++mt) {
+#if !OTT_SINGLE_CHAIN
+#pragma unroll
+        for (int q = 0; q < 4; ++q) ch[j][mt][q] += cl[j][mt][q];
+#endif
         sc[j][mt][0] = dummy ? -INFINITY : ch[j][mt][0] + bias0;
         sc[j][mt][1] = dummy ? -INFINITY : ch[j][mt][1] + bias1;
         sc[j][mt][2] = dummy ? -INFINITY : ch[j][mt][2] + bias0;
