@@ -45,8 +45,13 @@ typedef enum {
  * Block record (one per (unit, group)), byte layout, all little-endian:
  *   [0, G*d*bits/8)                 K codes, reference pack_codes order
  *   [+G*d*bits/8)                   V codes
- *   float32 k_step[d], k_xmin[d]    per-channel K params  (QuantParams)
+ *   fp16 k_sh[d], k_sl[d]           per-channel K step = sh + sl, in pair order
+ *                                   (index 16*(c/16) + 2*(c%8) + (c%16)/8)
+ *   float32 k_e[d]                  per-channel K x_min - 4*u(c)*step, u(c) = 4^(4-P(c%8)),
+ *                                   P = {3,4,2,3,4,2,3,4} (fp16 mantissa position of the
+ *                                   code pair in the decode kernels)
  *   float32 v_step[G], v_xmin[G]    per-token V params
+ * The exact float64 QuantParams are kept in params64 when it is allocated. 
  * Per-token bitmasks hold one bit per absolute position (32 per word). */
 typedef struct {
   int32_t n_units;      /* batch * n_kv_heads */

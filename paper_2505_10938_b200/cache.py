@@ -35,6 +35,19 @@ def _ptr(t) -> int | None:
     return None if t is None else t.data_ptr()
 
 
+
+def kpair_index(c):
+    """Pair-order index of channel c in the record's fp16 K step halves (ott_b200.h)."""
+    c = np.asarray(c)
+    return 16 * (c // 16) + 2 * (c % 8) + (c % 16) // 8
+
+
+def kpair_u(c):
+    """Position scale u(c) = 4^(4 - P(c % 8)) of the decode kernels' code-pair unpack."""
+    P = np.array([3, 4, 2, 3, 4, 2, 3, 4])[np.asarray(c) % 8]
+    return (4.0 ** (4 - P)).astype(np.float32)
+
+
 class OTTCache:
     """One layer's OTT cache for ``batch * n_kv_heads`` independent units.
 
@@ -262,10 +275,17 @@ class UnitView:
         nb = cache.quantized_tokens // G
         rec = cache.blocks[u, :nb].cpu().numpy()
         code_b = G * d // 4
-        kst = rec[:, 2 * code_b: 2 * code_b + 4 * d].copy().view(np.float32)
-        kmn = rec[:, 2 * code_b + 4 * d: 2 * code_b + 8 * d].copy().view(np.float32)
+        # K params are stored in the decode kernels' encoding (ott_b200.h): fp16 halves
+        # sh + sl of the step in pair order and e = x_min - 4 u step; the float32 views
+        # below are reconstructions, the exact values come from params64
+        self.k_sh16 = rec[:, 2 * code_b: 2 * code_b + 2 * d].copy().view(np.float16)
+        self.k_sl16 = rec[:, 2 * code_b + 2 * d: 2 * code_b + 4 * d].copy().view(np.float16)
+        self.k_e32 = rec[:, 2 * code_b + 4 * d: 2 * code_b + 8 * d].copy().view(np.float32)
         vst = rec[:, 2 * code_b + 8 * d: 2 * code_b + 8 * d + 4 * G].copy().view(np.float32)
         vmn = rec[:, 2 * code_b + 8 * d + 4 * G:].copy().view(np.float32)
+        pidx = kpair_index(np.arange(d))
+        kst = self.k_sh16[:, pidx].astype(np.float32) + self.k_sl16[:, pidx].astype(np.float32)
+        kmn = (self.k_e32 + np.float32(4) * kpair_u(np.arange(d)) * kst).astype(np.float32)
         self.k_step32, self.k_xmin32, self.v_step32, self.v_xmin32 = kst, kmn, vst, vmn
         if cache.params64 is not None:
             p = cache.params64[u, :nb].cpu().numpy()

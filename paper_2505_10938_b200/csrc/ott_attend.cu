@@ -24,6 +24,9 @@
 // per-(group, head) bias. V codes become exact fp16 subnormals c * 2^-16; the
 // per-token V step is folded into P' = 4 p step (fp16) and V x_min into a
 // per-head fp32 bias. See DESIGN.md §4.
+#include <cstdlib>
+#include <cstring>
+
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -31,16 +34,6 @@
 
 namespace ott {
 
-// hi and lo products of Q K^T accumulate into one chain (1) or two (0); one
-// chain measured ~1% faster (fewer registers, 8 fewer FADD per group)
-#ifndef OTT_SINGLE_CHAIN
-#define OTT_SINGLE_CHAIN 1
-#endif
-#if OTT_SINGLE_CHAIN
-#define OTT_LO_ACC ch
-#else
-#define OTT_LO_ACC cl
-#endif
 #ifndef OTT_MMA_MIN_BLOCKS
 #define OTT_MMA_MIN_BLOCKS 4
 #endif
@@ -133,13 +126,11 @@ __device__ void simt_body(const AttnArgs& a, int u, int t_begin, int t_end, int 
       const int64_t gi = tok0 / G;
       const int row0 = (int)(tok0 - gi * G);
       const uint8_t* rec = record_ptr(c, u, gi);
-      const float* kstep = reinterpret_cast<const float*>(rec + L.k_step());
-      const float* kxmin = reinterpret_cast<const float*>(rec + L.k_xmin());
       float bias[NR];
 #pragma unroll
       for (int r = 0; r < NR; ++r) bias[r] = 0.f;
       for (int col = lane; col < D; col += 32) {
-        const float st = kstep[col], mn = kxmin[col];
+        const float st = k_step_of(rec, L, col), mn = k_xmin_of(rec, L, col, st);
 #pragma unroll
         for (int r = 0; r < NR; ++r) {
           ws.qp[r][col] = sm.qs[r][col] * st;
@@ -321,6 +312,7 @@ __device__ __forceinline__ uint32_t pack_h2(float lo, float hi) {
   asm("cvt.rn.f16x2.f32 %0, %1, %2;\n" : "=r"(r) : "f"(hi), "f"(lo));
   return r;
 }
+__device__ __forceinline__ uint32_t h2_as_u32(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
 }
@@ -403,9 +395,6 @@ struct MmaSmem {
 #ifndef OTT_NO_TMA
 #define OTT_NO_TMA 0  // timing experiment only: compute on stale shared memory
 #endif
-#ifndef OTT_Q_IN_REGS
-#define OTT_Q_IN_REGS 0
-#endif
 #ifndef OTT_NG
 #define OTT_NG 1  // groups per loop iteration per warp (2 measured slower: register spills)
 #endif
@@ -414,14 +403,7 @@ struct MmaSmem {
 #endif
   static constexpr int kNG = G == 32 ? OTT_NG : 1;               // groups per loop iteration
   static constexpr int kStages = G == 32 ? OTT_STAGES : 2;          // TMA pipeline depth per warp
-  // q * 4 * scale_log2 in per-lane order: [hw][v4][lane] = head lane/4, channels
-  // 16*(lane%4 + 4*hw) + 4*v4 .. +3  (conflict-free LDS.128)
-  float4 q4p[2][4][32];
-  // per-group channel scratch [hw][slot], slot = 4*v4 + (tig ^ 2*(v4>>1)) (bank-conflict
-  // free for the lane-ordered writes and the per-tig broadcast reads): step * f and
-  // x_min - 4 f step with f = 4^(4 - P(m))
-  float4 stp[kAttnWarps][kNG][2][16];
-  float4 esc[kAttnWarps][kNG][2][16];
+  float4 qt[8][32];  // q (fp32) per lane for the x_min bias, see mma_body
   // group records land here through a SWIZZLE_32B tensor map (16-byte chunk bit 4 ^= bit 7
   // of the offset): ldmatrix over 32-byte token rows is then bank-conflict free
   alignas(256) uint8_t stage[kAttnWarps][kStages][kRec];
@@ -449,16 +431,19 @@ __device__ void mma_body(const AttnArgs& a, const CUtensorMap* tmap, MmaSmem<G>&
   const int g1 = min(n_groups, g0 + per);
   const int my_n = g1 > g0 + warp ? (g1 - g0 - warp + kAttnWarps - 1) / kAttnWarps : 0;
 
-  for (int i = tid; i < 2 * 4 * 32; i += kAttnThreads) {
-    const int hw = i >> 7, v4 = (i >> 5) & 3, ln = i & 31;
-    const int h = ln >> 2, ch = 16 * ((ln & 3) + 4 * hw) + 4 * v4;
+  // q (fp32) table for the x_min bias: [k][lane] = q[head lane/4][channels of words tig, 4+tig]:
+  // k < 4: 16 tig + 4k .. +3; k >= 4: 64 + 16 tig + 4(k-4) .. +3  (conflict-free LDS.128)
+  for (int i = tid; i < 8 * 32; i += kAttnThreads) {
+    const int k = i >> 5, ln = i & 31, h = ln >> 2, t4 = ln & 3;
+    const int ch = (k < 4 ? 16 * t4 : 64 + 16 * t4) + 4 * (k & 3);
     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
     if (h < NR) {
-      const uint16_t* qp = a.q + ((size_t)u * NR + h) * D + ch;
-      const float f = 4.f * a.scale_log2;
-      v = make_float4(h2f(qp[0]) * f, h2f(qp[1]) * f, h2f(qp[2]) * f, h2f(qp[3]) * f);
+      const uint2 raw = __ldg(reinterpret_cast<const uint2*>(a.q + ((size_t)u * NR + h) * D + ch));
+      const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&raw.x));
+      const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&raw.y));
+      v = make_float4(f0.x, f0.y, f1.x, f1.y);
     }
-    sm.q4p[hw][v4][ln] = v;
+    sm.qt[k][ln] = v;
   }
   const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&sm.bar[warp][0]);
   const uint32_t stage0 = (uint32_t)__cvta_generic_to_shared(&sm.stage[warp][0][0]);
@@ -484,20 +469,21 @@ __device__ void mma_body(const AttnArgs& a, const CUtensorMap* tmap, MmaSmem<G>&
   // row r = lane%8: i0 tokens 0-7 bytes 0-15, i1 tokens 8-15 bytes 0-15,
   // i2 tokens 0-7 bytes 16-31, i3 tokens 8-15 bytes 16-31.
   const uint32_t lm_off = (uint32_t)(((lane & 7) + ((lane >> 3) & 1) * 8) * 32 + (lane >> 4) * 16);
-  // cooperative channel pass: lane owns channels 4*lane..+3 = word lane/4, v4 = lane%4
-  const int cw = lane >> 2;
-  float4* stp_w = &sm.stp[warp][0][cw >> 2][tile_slot(lane & 3, cw & 3)];  // + j*32 for group j
-  float4* esc_w = &sm.esc[warp][0][cw >> 2][tile_slot(lane & 3, cw & 3)];
-  // f = 4^(4 - P(m)) for this lane's pairs: m = 0..3 -> {4, 1, 16, 4}; m = 4..7 -> {1, 16, 4, 1}
-  const float4 cf = (lane & 1) ? make_float4(1.f, 16.f, 4.f, 1.f) : make_float4(4.f, 1.f, 16.f, 4.f);
-
-#if OTT_Q_IN_REGS
-  float4 qreg[2][4];
+  __syncthreads();
+  // q * u(m) as exact fp16 pairs (channels 16w+m, 16w+m+8) of head g, words w = tig + 4 hw:
+  // the B operand q' = q u step is formed per group from the record's fp16 step halves
+  __half2 q16[2][8];
 #pragma unroll
   for (int hw = 0; hw < 2; ++hw)
 #pragma unroll
-    for (int v4 = 0; v4 < 4; ++v4) qreg[hw][v4] = sm.q4p[hw][v4][lane];
-#endif
+    for (int m = 0; m < 8; ++m) {
+      const float4 qa = sm.qt[4 * hw + m / 4][lane];
+      const float4 qb = sm.qt[4 * hw + 2 + m / 4][lane];
+      const float lo = (m % 4 == 0 ? qa.x : m % 4 == 1 ? qa.y : m % 4 == 2 ? qa.z : qa.w) * kpair_u(m);
+      const float hi = (m % 4 == 0 ? qb.x : m % 4 == 1 ? qb.y : m % 4 == 2 ? qb.z : qb.w) * kpair_u(m);
+      q16[hw][m] = __floats2half2_rn(lo, hi);
+    }
+  const float scale4 = 4.f * a.scale_log2;
   // Groups are processed NG at a time (two independent instruction streams per
   // warp for the scheduler); a lone tail group is paired with a masked dummy.
   constexpr int NG = MmaSmem<G>::kNG;
@@ -520,125 +506,89 @@ __device__ void mma_body(const AttnArgs& a, const CUtensorMap* tmap, MmaSmem<G>&
     uint32_t kw[NG][kMt][4];
 #pragma unroll
     for (int j = 0; j < NG; ++j) {
-      // channel pass: step * f and e = x_min - 4 f step with f = 4^(4 - P(m))
-      const float4 st = *reinterpret_cast<const float4*>(rec[j] + swz(L.k_step() + 16 * lane));
-      const float4 mn = *reinterpret_cast<const float4*>(rec[j] + swz(L.k_xmin() + 16 * lane));
-      stp_w[j * 32] = make_float4(st.x * cf.x, st.y * cf.y, st.z * cf.z, st.w * cf.w);
-      esc_w[j * 32] = make_float4(fmaf(-4.f * cf.x, st.x, mn.x), fmaf(-4.f * cf.y, st.y, mn.y),
-                                  fmaf(-4.f * cf.z, st.z, mn.z), fmaf(-4.f * cf.w, st.w, mn.w));
       // K code words (ldmatrix: token g / g+8, words tig and 4+tig)
 #pragma unroll
       for (int mt = 0; mt < kMt; ++mt) ldsm_x4(kw[j][mt], rec_s[j] + swz(L.k_codes() + mt * 16 * 32 + lm_off));
     }
     __syncwarp();
 
-    // ---- S = Q K^T: B operand q' = q4 * step * f as hi/lo fp16 pairs (channels m,
-    // m+8) built one (hw, half) slice at a time; hi and lo accumulate into one chain
+    // ---- S = Q K^T on tensor cores. B operand q' = q u step as an exact fp16 hi/lo split
+    // from the record's fp16 step halves (sh + sl): hi = q sh, err = fma(q, sh, -hi) (exact),
+    // lo = fma(q, sl, err); hi and lo accumulate into one chain.
+    // x_min bias (scale * sum_c q e, e = x_min - 4 u step from the record) per head g.
     float ch[NG][kMt][4];
-#if !OTT_SINGLE_CHAIN
-    float cl[NG][kMt][4];
-#endif
-    float2 bias2[NG];
-#if OTT_Q_IN_REGS
-    // (q4 lives in registers, loaded once per CTA: qreg[hw][v4])
-#endif
+    float bias_g[NG];
 #pragma unroll
     for (int j = 0; j < NG; ++j) {
-      bias2[j] = make_float2(0.f, 0.f);
+      float2 acc2 = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int mt = 0; mt < kMt; ++mt) {
-        ch[j][mt][0] = ch[j][mt][1] = ch[j][mt][2] = ch[j][mt][3] = 0.f;
-#if !OTT_SINGLE_CHAIN
-        cl[j][mt][0] = cl[j][mt][1] = cl[j][mt][2] = cl[j][mt][3] = 0.f;
-#endif
+      for (int k = 0; k < 8; ++k) {
+        const int wd = k < 4 ? tig : 4 + tig;
+        const float4 ev = *reinterpret_cast<const float4*>(rec[j] + swz(L.k_e() + 64 * wd + 16 * (k & 3)));
+        const float4 qv = sm.qt[k][lane];
+        acc2 = __ffma2_rn(make_float2(qv.x, qv.y), make_float2(ev.x, ev.y), acc2);
+        acc2 = __ffma2_rn(make_float2(qv.z, qv.w), make_float2(ev.z, ev.w), acc2);
       }
+      bias_g[j] = acc2.x + acc2.y;
+#pragma unroll
+      for (int mt = 0; mt < kMt; ++mt) ch[j][mt][0] = ch[j][mt][1] = ch[j][mt][2] = ch[j][mt][3] = 0.f;
     }
 #pragma unroll
     for (int hw = 0; hw < 2; ++hw) {
 #pragma unroll
-      for (int half = 0; half < 2; ++half) {  // pairs m = 4*half .. 4*half+3 (channels m, m+8)
+      for (int j = 0; j < NG; ++j) {
+        const int wd = tig + 4 * hw;
+        const uint4 h0 = *reinterpret_cast<const uint4*>(rec[j] + swz(L.k_sh() + 32 * wd));
+        const uint4 h1 = *reinterpret_cast<const uint4*>(rec[j] + swz(L.k_sh() + 32 * wd + 16));
+        const uint4 l0 = *reinterpret_cast<const uint4*>(rec[j] + swz(L.k_sl() + 32 * wd));
+        const uint4 l1 = *reinterpret_cast<const uint4*>(rec[j] + swz(L.k_sl() + 32 * wd + 16));
+        const uint32_t shw[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+        const uint32_t slw[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
+        uint32_t bh[8], bl[8];
 #pragma unroll
-        for (int j = 0; j < NG; ++j) {
-          uint32_t bh[4], bl[4];
-#pragma unroll
-          for (int pp = 0; pp < 2; ++pp) {  // v4 = half (channels 4*half..+3), v4 = 2 + half (+8)
-            const int v4 = half + 2 * pp;
-#if OTT_Q_IN_REGS
-            const float4 q4 = qreg[hw][v4];
-#else
-            const float4 q4 = sm.q4p[hw][v4][lane];
-#endif
-            const float4 s4 = sm.stp[warp][j][hw][tile_slot(v4, tig)];
-            const float4 e4 = sm.esc[warp][j][hw][tile_slot(v4, tig)];
-            const float2 q0 = make_float2(q4.x, q4.y), q1 = make_float2(q4.z, q4.w);
-            const float2 B0 = __fmul2_rn(q0, make_float2(s4.x, s4.y));
-            const float2 B1 = __fmul2_rn(q1, make_float2(s4.z, s4.w));
-            bias2[j] = __ffma2_rn(q0, make_float2(e4.x, e4.y), bias2[j]);
-            bias2[j] = __ffma2_rn(q1, make_float2(e4.z, e4.w), bias2[j]);
-            const float2 h0 = make_float2(__uint_as_float(__float_as_uint(B0.x) & 0xFFFFE000u),
-                                          __uint_as_float(__float_as_uint(B0.y) & 0xFFFFE000u));
-            const float2 h1 = make_float2(__uint_as_float(__float_as_uint(B1.x) & 0xFFFFE000u),
-                                          __uint_as_float(__float_as_uint(B1.y) & 0xFFFFE000u));
-            const float2 l0 = __fadd2_rn(B0, make_float2(-h0.x, -h0.y));
-            const float2 l1 = __fadd2_rn(B1, make_float2(-h1.x, -h1.y));
-            if (pp == 0) {  // low channel of each pair
-              bh[0] = __float_as_uint(h0.x); bh[1] = __float_as_uint(h0.y);
-              bh[2] = __float_as_uint(h1.x); bh[3] = __float_as_uint(h1.y);
-              bl[0] = __float_as_uint(l0.x); bl[1] = __float_as_uint(l0.y);
-              bl[2] = __float_as_uint(l1.x); bl[3] = __float_as_uint(l1.y);
-            } else {  // pack (low, high = channel + 8)
-              bh[0] = pack_h2(__uint_as_float(bh[0]), h0.x); bh[1] = pack_h2(__uint_as_float(bh[1]), h0.y);
-              bh[2] = pack_h2(__uint_as_float(bh[2]), h1.x); bh[3] = pack_h2(__uint_as_float(bh[3]), h1.y);
-              bl[0] = pack_h2(__uint_as_float(bl[0]), l0.x); bl[1] = pack_h2(__uint_as_float(bl[1]), l0.y);
-              bl[2] = pack_h2(__uint_as_float(bl[2]), l1.x); bl[3] = pack_h2(__uint_as_float(bl[3]), l1.y);
-            }
-          }
-          // slice-major over the m-tiles so consecutive HMMAs feed different
-          // accumulators (hi -> ch, lo -> cl per m-tile: 2*kMt independent chains)
-          Shifted s0[kMt], s1[kMt];
-#pragma unroll
-          for (int mt = 0; mt < kMt; ++mt) {
-            s0[mt] = shifted(kw[j][mt][2 * hw]);
-            s1[mt] = shifted(kw[j][mt][2 * hw + 1]);
-          }
-#define OTT_QK(MM)                                                                        \
-  {                                                                                       \
-    _Pragma("unroll") for (int mt = 0; mt < kMt; ++mt) {                                  \
-      const uint32_t a0 = kq<MM>(s0[mt], magic), a1 = kq<MM>(s1[mt], magic);             \
-      const uint32_t a2 = kq<MM + 1>(s0[mt], magic), a3 = kq<MM + 1>(s1[mt], magic);     \
-      mma16816(ch[j][mt], a0, a1, a2, a3, bh[(MM) & 3], bh[((MM) & 3) + 1]);              \
-      mma16816(OTT_LO_ACC[j][mt], a0, a1, a2, a3, bl[(MM) & 3], bl[((MM) & 3) + 1]);      \
-    }                                                                                     \
-  }
-          if (half == 0) {
-            OTT_QK(0) OTT_QK(2)
-          } else {
-            OTT_QK(4) OTT_QK(6)
-          }
-#undef OTT_QK
+        for (int m = 0; m < 8; ++m) {
+          const __half2 sh = *reinterpret_cast<const __half2*>(&shw[m]);
+          const __half2 sl = *reinterpret_cast<const __half2*>(&slw[m]);
+          const __half2 H = __hmul2(q16[hw][m], sh);
+          const __half2 E = __hfma2(q16[hw][m], sh, __hneg2(H));
+          bh[m] = h2_as_u32(H);
+          bl[m] = h2_as_u32(__hfma2(q16[hw][m], sl, E));
         }
+        Shifted s0[kMt], s1[kMt];
+#pragma unroll
+        for (int mt = 0; mt < kMt; ++mt) {
+          s0[mt] = shifted(kw[j][mt][2 * hw]);
+          s1[mt] = shifted(kw[j][mt][2 * hw + 1]);
+        }
+#define OTT_QK(MM)                                                                    \
+  {                                                                                   \
+    _Pragma("unroll") for (int mt = 0; mt < kMt; ++mt) {                              \
+      const uint32_t a0 = kq<MM>(s0[mt], magic), a1 = kq<MM>(s1[mt], magic);         \
+      const uint32_t a2 = kq<MM + 1>(s0[mt], magic), a3 = kq<MM + 1>(s1[mt], magic); \
+      mma16816(ch[j][mt], a0, a1, a2, a3, bh[MM], bh[MM + 1]);                        \
+      mma16816(ch[j][mt], a0, a1, a2, a3, bl[MM], bl[MM + 1]);                        \
+    }                                                                                 \
+  }
+        OTT_QK(0) OTT_QK(2) OTT_QK(4) OTT_QK(6)
+#undef OTT_QK
       }
     }
     float sc[NG][kMt][4];
 #pragma unroll
     for (int j = 0; j < NG; ++j) {
-      float bias = bias2[j].x + bias2[j].y;
+      float bias = bias_g[j];
       bias += __shfl_xor_sync(0xffffffffu, bias, 1);
       bias += __shfl_xor_sync(0xffffffffu, bias, 2);
-      bias *= 0.25f;
+      bias *= a.scale_log2;
       const float bias0 = __shfl_sync(0xffffffffu, bias, 8 * tig);      // head 2*tig
       const float bias1 = __shfl_sync(0xffffffffu, bias, 8 * tig + 4);  // head 2*tig+1
       const bool dummy = j >= ng;
 #pragma unroll
       for (int mt = 0; mt < kMt; ++mt) {
-#if !OTT_SINGLE_CHAIN
-#pragma unroll
-        for (int q = 0; q < 4; ++q) ch[j][mt][q] += cl[j][mt][q];
-#endif
-        sc[j][mt][0] = dummy ? -INFINITY : ch[j][mt][0] + bias0;
-        sc[j][mt][1] = dummy ? -INFINITY : ch[j][mt][1] + bias1;
-        sc[j][mt][2] = dummy ? -INFINITY : ch[j][mt][2] + bias0;
-        sc[j][mt][3] = dummy ? -INFINITY : ch[j][mt][3] + bias1;
+        sc[j][mt][0] = dummy ? -INFINITY : fmaf(ch[j][mt][0], scale4, bias0);
+        sc[j][mt][1] = dummy ? -INFINITY : fmaf(ch[j][mt][1], scale4, bias1);
+        sc[j][mt][2] = dummy ? -INFINITY : fmaf(ch[j][mt][2], scale4, bias0);
+        sc[j][mt][3] = dummy ? -INFINITY : fmaf(ch[j][mt][3], scale4, bias1);
       }
       // pooled positions: their logits come from the pool tile (overwrite semantics)
 #pragma unroll
@@ -796,6 +746,9 @@ struct FpSmem {
   float mm[kAttnWarps][8], ll[kAttnWarps][8];
 };
 
+// barrier over warps 0-3 only (the tcgen05 kernel's fifth warp does not take part)
+__device__ __forceinline__ void sync4() { asm volatile("bar.sync 1, 128;\n" ::: "memory"); }
+
 __device__ __forceinline__ void tma_row(uint32_t dst, const void* src, uint32_t bar) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 256, [%2];\n" ::"r"(dst),
@@ -949,7 +902,7 @@ __device__ void fp_body(const AttnArgs& a, FpSmem& sm) {
       sm.ll[warp][2 * tig + h] = lsum[h];
     }
   }
-  __syncthreads();
+  sync4();
   float* accw = reinterpret_cast<float*>(&sm.kr[warp][0][0]);  // [8 heads][128]
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
@@ -959,7 +912,7 @@ __device__ void fp_body(const AttnArgs& a, FpSmem& sm) {
       accw[(2 * tig + h) * D + 16 * j + 8 + g] = o[j][h + 2];
     }
   }
-  __syncthreads();
+  sync4();
   for (int i = tid; i < NR * D; i += kAttnThreads) {
     const int r = i / D, col = i % D;
     float M = -INFINITY;
@@ -992,6 +945,458 @@ __global__ void __launch_bounds__(kAttnThreads, OTT_MMA_MIN_BLOCKS)
     fp_body<NR>(a, *reinterpret_cast<FpSmem*>(smem_raw));
   } else {
     mma_body<NR, G>(a, &tmap, *reinterpret_cast<MmaSmem<G>*>(smem_raw));
+  }
+}
+
+// ============================================================ tcgen05 path (d = 128, G = 32)
+// Q K^T on the 5th-generation tensor cores, P V on the warp-level path.
+//
+// CTA = 4 compute warps + 1 MMA-issuer warp. A 128-token chunk is 4 consecutive
+// groups, one per compute warp. Per chunk:
+//   * each compute warp (thread = token) unpacks its group's K codes into fp16
+//     (1 + c 2^(2P-10), one LOP3 per pair) and stores the 32 x 128 tile into its
+//     32 TMEM lanes (tcgen05.st, A operand of the MMA);
+//   * lane (head pair, code word) forms q' = q u step as an exact fp16 hi/lo split
+//     from the record's pair-ordered fp16 step halves: hi = q*sh, err = fma(q, sh,
+//     -hi) (exact), lo = fma(q, sl, err); rows 16w+h (hi) and 16w+8+h (lo) of the
+//     shared-memory B operand (K-major, canonical no-swizzle layout);
+//   * the issuer runs 8 tcgen05.mma kind::f16 (M=128 tokens, N=64, K=16) into a
+//     TMEM accumulator; only the diagonal 32x16 blocks are used;
+//   * while that runs the warps finish the previous chunk: tcgen05.ld of their
+//     logits (thread = token, 8 heads), lazily rescaled online softmax, P' = 4 p
+//     step to shared memory, and V^T P' with mma.sync m16n8k16 on the V codes
+//     (exact fp16 subnormals), accumulating in registers per warp.
+// logit = scale * (4 S + sum_c q_c e_c), e = x_min - 4 u step (record encoding).
+namespace tc5 {
+constexpr int kCW = 4;                       // compute warps
+constexpr int kThreads = 32 * (kCW + 1);     // + MMA issuer
+constexpr int kStages = 6;                   // record stages per compute warp (2 in use, 4 in flight)
+constexpr int kRec = 3328;                   // record bytes at d = 128, G = 32
+constexpr uint32_t kLBO = 128, kSBO = 16 * 128;  // B operand core-matrix strides (bytes)
+constexpr uint32_t kCols = 128;              // TMEM: A at 0 (f16 pairs), D at 64 (f32)
+constexpr uint32_t kIdesc = (1u << 4)        // D f32, A/B f16, both K-major
+                            | ((uint32_t)(64 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}  // namespace tc5
+
+#ifndef OTT_TC5_MIN_BLOCKS
+#define OTT_TC5_MIN_BLOCKS 2
+#endif
+#ifndef OTT_TC5_ABL  // timing ablations only (results wrong): 1 no softmax/PV, 2 no q'/bias, 4 no K unpack
+#define OTT_TC5_ABL 0
+#endif
+
+struct Tc5Smem {
+  alignas(256) uint8_t stage[tc5::kCW][tc5::kStages][tc5::kRec];
+  alignas(128) uint8_t b1[64 * 128 * 2];       // q' hi/lo rows, K-major canonical
+  alignas(16) uint16_t pp[tc5::kCW][32][8];    // P' [token][head] per warp
+  alignas(16) float4 qt[8][32];                // q (fp32) per lane (head lane%8, channels 32(lane/8) + 4k..)
+  alignas(16) float bias[tc5::kCW][2][8];      // scale * sum_c q e per (warp, chunk parity, head)
+  float mm[tc5::kCW][8], ll[tc5::kCW][8];
+  alignas(8) uint64_t rbar[tc5::kCW][tc5::kStages];
+  alignas(8) uint64_t qk_ready, qk_done;
+  uint32_t tmem_base;
+};
+
+__device__ __forceinline__ uint64_t tc5_bdesc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)(tc5::kLBO >> 4) << 16) |
+         ((uint64_t)(tc5::kSBO >> 4) << 32) | (1ull << 46);
+}
+__device__ __forceinline__ void tmem_st64(uint32_t taddr, const uint32_t (&r)[64]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x64.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,"
+      "%43,%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63,%64};\n" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]), "r"(r[32]), "r"(r[33]), "r"(r[34]), "r"(r[35]), "r"(r[36]),
+      "r"(r[37]), "r"(r[38]), "r"(r[39]), "r"(r[40]), "r"(r[41]), "r"(r[42]), "r"(r[43]), "r"(r[44]), "r"(r[45]),
+      "r"(r[46]), "r"(r[47]), "r"(r[48]), "r"(r[49]), "r"(r[50]), "r"(r[51]), "r"(r[52]), "r"(r[53]), "r"(r[54]),
+      "r"(r[55]), "r"(r[56]), "r"(r[57]), "r"(r[58]), "r"(r[59]), "r"(r[60]), "r"(r[61]), "r"(r[62]), "r"(r[63])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+template <int I>
+__device__ __forceinline__ float pick4(const float (&v)[8], int tig) {  // v[2 tig + I]
+  return tig == 0 ? v[I] : (tig == 1 ? v[2 + I] : (tig == 2 ? v[4 + I] : v[6 + I]));
+}
+
+// K side of chunk j for compute warp w: A tile into TMEM, q' rows into B, bias.
+template <int NR>
+__device__ __forceinline__ void tc5_kstage(Tc5Smem& sm, int w, int lane, const uint8_t* rec, uint32_t a_lane,
+                                           uint8_t* b1, const __half2 (&q16)[2][8], uint32_t magic, float scale,
+                                           int slot) {
+  const RecordLayout L(128, 32);
+  if (!(OTT_TC5_ABL & 4)) {  // A row = token `lane`: 8 code words -> 64 fp16 pairs
+    const uint4 c0 = *reinterpret_cast<const uint4*>(rec + swz(L.k_codes() + lane * 32));
+    const uint4 c1 = *reinterpret_cast<const uint4*>(rec + swz(L.k_codes() + lane * 32 + 16));
+    const uint32_t wd[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+    uint32_t r[64];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const Shifted sft = shifted(wd[j]);
+      r[8 * j + 0] = kq<0>(sft, magic);
+      r[8 * j + 1] = kq<1>(sft, magic);
+      r[8 * j + 2] = kq<2>(sft, magic);
+      r[8 * j + 3] = kq<3>(sft, magic);
+      r[8 * j + 4] = kq<4>(sft, magic);
+      r[8 * j + 5] = kq<5>(sft, magic);
+      r[8 * j + 6] = kq<6>(sft, magic);
+      r[8 * j + 7] = kq<7>(sft, magic);
+    }
+    tmem_st64(a_lane, r);
+  }
+  // q' rows: lane = (head h = lane % 8, word pair e4 = lane / 8: code words 2e4, 2e4+1 =
+  // channels 32e4 .. 32e4+31). Lanes 8k..8k+7 write rows 0..7 of one core matrix:
+  // 128 contiguous bytes per store phase, bank-conflict free.
+  const int h = lane & 7, e4 = lane >> 3;
+  float part = 0.f;
+  if (h < NR && !(OTT_TC5_ABL & 2)) {
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};  // sum_c q_c e_c, 4 independent chains
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float4 ev = *reinterpret_cast<const float4*>(rec + swz(L.k_e() + 128 * e4 + 16 * k));
+      const float4 qv = sm.qt[k][lane];
+      acc[0] = fmaf(qv.x, ev.x, acc[0]);
+      acc[1] = fmaf(qv.y, ev.y, acc[1]);
+      acc[2] = fmaf(qv.z, ev.z, acc[2]);
+      acc[3] = fmaf(qv.w, ev.w, acc[3]);
+    }
+    part = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+#pragma unroll
+    for (int w2 = 0; w2 < 2; ++w2) {
+      const int wd = 2 * e4 + w2;  // code word: channels 16 wd .. 16 wd + 15
+      const uint4 h0 = *reinterpret_cast<const uint4*>(rec + swz(L.k_sh() + 32 * wd));
+      const uint4 h1 = *reinterpret_cast<const uint4*>(rec + swz(L.k_sh() + 32 * wd + 16));
+      const uint4 l0 = *reinterpret_cast<const uint4*>(rec + swz(L.k_sl() + 32 * wd));
+      const uint4 l1 = *reinterpret_cast<const uint4*>(rec + swz(L.k_sl() + 32 * wd + 16));
+      const uint32_t shw[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+      const uint32_t slw[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
+      uint32_t hi[8], lo[8];
+#pragma unroll
+      for (int m = 0; m < 8; ++m) {
+        const __half2 sh = *reinterpret_cast<const __half2*>(&shw[m]);
+        const __half2 sl = *reinterpret_cast<const __half2*>(&slw[m]);
+        const __half2 H = __hmul2(q16[w2][m], sh);
+        const __half2 E = __hfma2(q16[w2][m], sh, __hneg2(H));  // exact rounding error of H
+        hi[m] = h2_as_u32(H);
+        lo[m] = h2_as_u32(__hfma2(q16[w2][m], sl, E));
+      }
+      uint8_t* bh = b1 + (2 * w) * tc5::kSBO + (2 * wd) * tc5::kLBO + h * 16;
+      uint8_t* bl = bh + tc5::kSBO;
+      *reinterpret_cast<uint4*>(bh) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+      *reinterpret_cast<uint4*>(bh + tc5::kLBO) = make_uint4(hi[4], hi[5], hi[6], hi[7]);
+      *reinterpret_cast<uint4*>(bl) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+      *reinterpret_cast<uint4*>(bl + tc5::kLBO) = make_uint4(lo[4], lo[5], lo[6], lo[7]);
+    }
+  }
+  // reduce over the 4 word pairs (all lanes take part; idle heads carry 0)
+  part += __shfl_xor_sync(0xffffffffu, part, 8);
+  part += __shfl_xor_sync(0xffffffffu, part, 16);
+  if (e4 == 0 && h < NR) sm.bias[w][slot][h] = part * scale;
+}
+
+template <int NR>
+__device__ void tc5_body(const AttnArgs& a, const CUtensorMap* tmap, Tc5Smem& sm) {
+  constexpr int D = 128, G = 32, kS = tc5::kStages;
+  const RecordLayout L(D, G);
+  const ott_cache_t& c = a.c;
+  const int u = blockIdx.x, split = blockIdx.y;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, tig = lane & 3;
+  const int n_groups = (int)(a.q_tokens / G);
+  const int per = (((n_groups + a.n_qsplits - 1) / a.n_qsplits) + 3) & ~3;  // whole chunks per split
+  const int g0 = min(n_groups, split * per);
+  const int g1 = min(n_groups, g0 + per);
+  const int n_chunks = (g1 - g0 + 3) / 4;
+  const int64_t unit_rec = (int64_t)u * c.max_groups;
+
+  const uint32_t qk_ready = (uint32_t)__cvta_generic_to_shared(&sm.qk_ready);
+  const uint32_t qk_done = (uint32_t)__cvta_generic_to_shared(&sm.qk_done);
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(&sm.tmem_base)),
+                 "n"(tc5::kCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (tid == 0) {
+    for (int w = 0; w < tc5::kCW; ++w)
+      for (int s = 0; s < kS; ++s) mbar_init((uint32_t)__cvta_generic_to_shared(&sm.rbar[w][s]), 1);
+    mbar_init(qk_ready, tc5::kCW);
+    mbar_init(qk_done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  for (int i = tid; i < 8 * 32; i += tc5::kThreads) {  // q table: [k][lane] = q[lane % 8][32 (lane / 8) + 4k ..]
+    const int k = i >> 5, ln = i & 31, h = ln & 7;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (h < NR) {
+      const uint2 raw = __ldg(reinterpret_cast<const uint2*>(a.q + ((size_t)u * NR + h) * D + 32 * (ln >> 3) + 4 * k));
+      const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&raw.x));
+      const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&raw.y));
+      v = make_float4(f0.x, f0.y, f1.x, f1.y);
+    }
+    sm.qt[k][ln] = v;
+  }
+  for (int i = tid; i < 64 * 128 * 2 / 16; i += tc5::kThreads)
+    reinterpret_cast<uint4*>(sm.b1)[i] = make_uint4(0u, 0u, 0u, 0u);
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = sm.tmem_base;
+  const uint32_t a_tm = tmem, d_tm = tmem + 64;
+
+  float o[8][4];
+#pragma unroll
+  for (int cm = 0; cm < 8; ++cm) o[cm][0] = o[cm][1] = o[cm][2] = o[cm][3] = 0.f;
+  float m[8], l[8], vb[8];
+#pragma unroll
+  for (int h = 0; h < 8; ++h) {
+    m[h] = -INFINITY;
+    l[h] = 0.f;
+    vb[h] = 0.f;
+  }
+
+  if (warp == tc5::kCW) {
+    // ---------------- MMA issuer
+    const uint32_t b_s = (uint32_t)__cvta_generic_to_shared(sm.b1);
+    const uint32_t a_b = a_tm, d_b = d_tm;
+    for (int i = 0; i < n_chunks; ++i) {
+      mbar_wait(qk_ready, (uint32_t)(i & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      if (lane == 0) {
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+          const uint64_t bd = tc5_bdesc(b_s + s * 2 * tc5::kLBO);
+          asm volatile(
+              "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+              "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_b),
+              "r"(a_b + 8 * s), "l"(bd), "r"(tc5::kIdesc), "r"(s)
+              : "memory");
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(qk_done)
+                     : "memory");
+      }
+      __syncwarp();
+    }
+  } else {
+    // ---------------- compute warps
+    const int w = warp;
+    const uint32_t rbar0 = (uint32_t)__cvta_generic_to_shared(&sm.rbar[w][0]);
+    const uint32_t stage0 = (uint32_t)__cvta_generic_to_shared(&sm.stage[w][0][0]);
+    auto group_of = [&](int j) { return g0 + 4 * j + w; };
+    if (lane == 0) {
+#pragma unroll
+      for (int s = 0; s < kS; ++s)
+        if (s < n_chunks && group_of(s) < g1)
+          load_record<G>(stage0 + s * tc5::kRec, tmap, unit_rec + group_of(s), rbar0 + 8 * s);
+    }
+    const uint32_t magic = a.k_magic;
+    const float scale = a.scale_log2, scale4 = 4.f * a.scale_log2;
+    // q * u(m) as fp16 pairs (channels 16e+m, 16e+m+8) for heads 2hp, 2hp+1
+    // q * u(m) as fp16 pairs (channels 16wd+m, 16wd+m+8) of head lane % 8, words wd = 2e4 + w2
+    __half2 q16[2][8];
+#pragma unroll
+    for (int w2 = 0; w2 < 2; ++w2)
+#pragma unroll
+      for (int m = 0; m < 8; ++m) {
+        // channel 32e4 + 16w2 + m lives in table entry k = 4w2 + m/4, component m%4
+        const float4 qa = sm.qt[4 * w2 + m / 4][lane];
+        const float4 qb = sm.qt[4 * w2 + 2 + m / 4][lane];
+        const float lo = (m % 4 == 0 ? qa.x : m % 4 == 1 ? qa.y : m % 4 == 2 ? qa.z : qa.w) * kpair_u(m);
+        const float hi = (m % 4 == 0 ? qb.x : m % 4 == 1 ? qb.y : m % 4 == 2 ? qb.z : qb.w) * kpair_u(m);
+        q16[w2][m] = __floats2half2_rn(lo, hi);
+      }
+    const uint32_t a_lane = a_tm + ((uint32_t)(32 * w) << 16);
+    const uint32_t d_lane = d_tm + ((uint32_t)(32 * w) << 16) + 16 * w;
+    const uint32_t pp_s = (uint32_t)__cvta_generic_to_shared(&sm.pp[w][0][0]);
+    const uint32_t lm_off = (uint32_t)(((lane & 7) + ((lane >> 3) & 1) * 8) * 32 + (lane >> 4) * 16);
+    const uint32_t* pmask = c.pool_mask + (size_t)u * mask_words_per_unit(c);
+
+    auto kstage = [&](int j) {
+      const int gj = group_of(j);
+      if (gj < g1) {
+        mbar_wait(rbar0 + 8 * (j % kS), (uint32_t)((j / kS) & 1));
+        tc5_kstage<NR>(sm, w, lane, &sm.stage[w][j % kS][0], a_lane, sm.b1, q16, magic, scale, j & 1);
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(qk_ready);
+    };
+    if (n_chunks > 0) kstage(0);
+
+    for (int i = 0; i < n_chunks; ++i) {
+      // ---- logits of chunk i (this warp's 32 tokens x 16 columns: hi heads, lo heads)
+      mbar_wait(qk_done, (uint32_t)(i & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      uint32_t sv[16];
+      tmem_ld16(d_lane, sv);
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      // ---- K side of chunk i + 1 (the MMA of chunk i is complete and its logits are
+      // read); the MMA of chunk i + 1 then runs under this chunk's softmax and P V
+      if (i + 1 < n_chunks) kstage(i + 1);
+
+      const int gi = group_of(i);
+      if (gi < g1 && !(OTT_TC5_ABL & 1)) {
+        const int st = i % kS;
+        const uint8_t* rec = &sm.stage[w][st][0];
+        const uint32_t rec_s = stage0 + st * tc5::kRec;
+        const float4 b0 = *reinterpret_cast<const float4*>(&sm.bias[w][i & 1][0]);
+        const float4 b1 = *reinterpret_cast<const float4*>(&sm.bias[w][i & 1][4]);
+        const float bias[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+        const bool pooled = (__ldg(&pmask[gi]) >> lane) & 1u;
+        float s[8];
+#pragma unroll
+        for (int h = 0; h < 8; ++h)
+          s[h] = (h < NR && !pooled)
+                     ? fmaf(__uint_as_float(sv[h]), scale4, fmaf(__uint_as_float(sv[8 + h]), scale4, bias[h]))
+                     : -INFINITY;
+        // lazily rescaled online softmax: the warp's running max moves only when a
+        // logit exceeds it by kLazy (p <= 2^kLazy keeps P' = 4 p step in fp16 range)
+        float dmax = -INFINITY;
+#pragma unroll
+        for (int h = 0; h < NR; ++h) dmax = fmaxf(dmax, s[h] - m[h]);
+        if (__any_sync(0xffffffffu, dmax > kLazy || m[0] == -INFINITY)) {
+          float corr[8];
+#pragma unroll
+          for (int h = 0; h < 8; ++h) {
+            corr[h] = 1.f;
+            if (h < NR) {
+              const float t = warp_max(s[h]);
+              const float mnew = fmaxf(m[h], t);
+              corr[h] = mnew == -INFINITY ? 1.f : ex2(m[h] - mnew);
+              m[h] = mnew;
+              l[h] *= corr[h];
+              vb[h] *= corr[h];
+            }
+          }
+          const float c0 = pick4<0>(corr, tig), c1 = pick4<1>(corr, tig);
+#pragma unroll
+          for (int cm = 0; cm < 8; ++cm) {
+            o[cm][0] *= c0;
+            o[cm][1] *= c1;
+            o[cm][2] *= c0;
+            o[cm][3] *= c1;
+          }
+        }
+        float me[8];
+#pragma unroll
+        for (int h = 0; h < 8; ++h) me[h] = m[h] == -INFINITY ? 0.f : m[h];
+        const float vs = *reinterpret_cast<const float*>(rec + swz(L.v_step() + 4 * lane));
+        const float vx = *reinterpret_cast<const float*>(rec + swz(L.v_xmin() + 4 * lane));
+        const float f = 4.f * vs;
+        float pq[8];
+#pragma unroll
+        for (int h = 0; h < 8; ++h) {
+          pq[h] = 0.f;
+          if (h < NR) {
+            const float p = ex2(s[h] - me[h]);
+            l[h] += p;
+            vb[h] = fmaf(p, vx, vb[h]);
+            pq[h] = p * f;
+          }
+        }
+        *reinterpret_cast<uint4*>(&sm.pp[w][lane][0]) =
+            make_uint4(pack_h2(pq[0], pq[1]), pack_h2(pq[2], pq[3]), pack_h2(pq[4], pq[5]), pack_h2(pq[6], pq[7]));
+        __syncwarp();
+        uint32_t bq[4];
+        ldsm_x4_t(bq, pp_s + lane * 16);
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          const uint32_t bb0 = bq[2 * mt], bb1 = bq[2 * mt + 1];
+          uint32_t vr[4];
+          ldsm_x4_t(vr, rec_s + swz(L.v_codes() + mt * 16 * 32 + lm_off));
+          const Shifted v0 = shifted(vr[0]), v1 = shifted(vr[1]), v2 = shifted(vr[2]), v3 = shifted(vr[3]);
+#define OTT_PV5(CM) mma16816(o[CM], vq<CM>(v0), vq<CM>(v2), vq<CM>(v1), vq<CM>(v3), bb0, bb1);
+          OTT_PV5(0) OTT_PV5(1) OTT_PV5(2) OTT_PV5(3) OTT_PV5(4) OTT_PV5(5) OTT_PV5(6) OTT_PV5(7)
+#undef OTT_PV5
+        }
+      }
+      // ---- release this stage: prefetch the record of chunk i + kStages
+      __syncwarp();
+      if (lane == 0 && i + kS < n_chunks && group_of(i + kS) < g1) {
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        load_record<G>(stage0 + (i % kS) * tc5::kRec, tmap, unit_rec + group_of(i + kS), rbar0 + 8 * (i % kS));
+      }
+    }
+
+    // ---- per-warp totals (thread = token: sum l, vb over the lanes)
+#pragma unroll
+    for (int h = 0; h < 8; ++h) {
+      l[h] = warp_sum(l[h]);
+      vb[h] = warp_sum(vb[h]);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int h = 0; h < 8; ++h) {
+        sm.mm[w][h] = m[h];
+        sm.ll[w][h] = l[h];
+      }
+    }
+  }
+  __syncthreads();  // every warp is past its loop: stage memory is free
+  if (warp < tc5::kCW) {
+    float* accw = reinterpret_cast<float*>(&sm.stage[warp][0][0]);  // [8 heads][128] natural channel order
+    const float vb0 = pick4<0>(vb, tig), vb1 = pick4<1>(vb, tig);
+#pragma unroll
+    for (int cm = 0; cm < 8; ++cm) {
+      const float f = pair_pos(cm) == 2 ? 262144.f : (pair_pos(cm) == 3 ? 65536.f : 16384.f);  // 2^(22-2P)
+      accw[(2 * tig) * D + 8 * g + cm] = fmaf(o[cm][0], f, vb0);
+      accw[(2 * tig + 1) * D + 8 * g + cm] = fmaf(o[cm][1], f, vb1);
+      accw[(2 * tig) * D + 64 + 8 * g + cm] = fmaf(o[cm][2], f, vb0);
+      accw[(2 * tig + 1) * D + 64 + 8 * g + cm] = fmaf(o[cm][3], f, vb1);
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < NR * D; i += tc5::kThreads) {
+    const int r = i / D, col = i % D;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < tc5::kCW; ++w) M = fmaxf(M, sm.mm[w][r]);
+    float Lsum = 0.f, A = 0.f;
+    if (M != -INFINITY) {
+#pragma unroll
+      for (int w = 0; w < tc5::kCW; ++w) {
+        if (sm.mm[w][r] == -INFINITY) continue;
+        const float f = exp2f(sm.mm[w][r] - M);
+        Lsum += sm.ll[w][r] * f;
+        A += reinterpret_cast<const float*>(&sm.stage[w][0][0])[r * D + col] * f;
+      }
+    }
+    float* base = a.ws + (((size_t)u * NR + r) * a.n_splits + split) * (D + 2);
+    base[2 + col] = A;
+    if (col == 0) {
+      base[0] = M;
+      base[1] = Lsum;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(tc5::kCols));
+}
+
+template <int NR>
+__global__ void __launch_bounds__(tc5::kThreads, OTT_TC5_MIN_BLOCKS)
+    attend_tc5_kernel(const __grid_constant__ AttnArgs a, const __grid_constant__ CUtensorMap tmap) {
+  extern __shared__ __align__(256) unsigned char smem_raw[];
+  if ((int)blockIdx.y == a.n_qsplits) {  // full-precision tiers on warps 0-3
+    if (threadIdx.x >= 128) return;
+    fp_body<NR>(a, *reinterpret_cast<FpSmem*>(smem_raw));
+  } else {
+    tc5_body<NR>(a, &tmap, *reinterpret_cast<Tc5Smem*>(smem_raw));
   }
 }
 
@@ -1039,9 +1444,10 @@ __global__ void logits_kernel(ott_cache_t c, const uint16_t* __restrict__ q, flo
       const int row = (int)(p - gi * G);
       const uint8_t* rec = record_ptr(c, u, gi);
       const uint32_t* kcw = reinterpret_cast<const uint32_t*>(rec + L.k_codes()) + (size_t)row * (D / 16);
-      const float* kstep = reinterpret_cast<const float*>(rec + L.k_step());
-      const float* kxmin = reinterpret_cast<const float*>(rec + L.k_xmin());
-      for (int j = 0; j < D; ++j) k[j] = fmaf((float)((kcw[j / 16] >> (2 * (j % 16))) & 3u), kstep[j], kxmin[j]);
+      for (int j = 0; j < D; ++j) {
+        const float st = k_step_of(rec, L, j);
+        k[j] = fmaf((float)((kcw[j / 16] >> (2 * (j % 16))) & 3u), st, k_xmin_of(rec, L, j, st));
+      }
     }
   } else {
     const size_t off = ((size_t)u * cap + (size_t)(p % cap)) * D;
@@ -1105,6 +1511,33 @@ static cudaError_t launch_mma_t(const AttnArgs& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+template <int NR>
+static cudaError_t launch_tc5_t(const AttnArgs& a, cudaStream_t st) {
+  CUtensorMap tmap;
+  cudaError_t te = record_tensor_map(a.c, RecTma<32>::kBoxRows, RecTma<32>::kRows, &tmap);
+  if (te != cudaSuccess) return te;
+  const size_t smem = sizeof(Tc5Smem) > sizeof(FpSmem) ? sizeof(Tc5Smem) : sizeof(FpSmem);
+  cudaError_t e = cudaFuncSetAttribute(attend_tc5_kernel<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  attend_tc5_kernel<NR><<<dim3(a.c.n_units, a.n_splits), tc5::kThreads, smem, st>>>(a, tmap);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  combine_kernel<128><<<a.c.n_units * NR, 128, 0, st>>>(a.ws, a.out, a.n_splits);
+  return cudaGetLastError();
+}
+
+// Attention kernel for (d = 128, G = 32): the mma.sync kernel (default, faster as
+// measured) or the tcgen05 Q K^T kernel (OTT_ATTN_KERNEL=tc5); read
+// once per process.
+static bool use_tc5() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("OTT_ATTN_KERNEL");
+    v = (e && strcmp(e, "tc5") == 0) ? 1 : 0;
+  }
+  return v == 1;
+}
+
 bool mma_eligible(const ott_cache_t& c) { return c.head_dim == 128; }
 
 cudaError_t launch_attend(const ott_cache_t& c, const uint16_t* q, uint16_t* out, int n_rep, int64_t q_tokens,
@@ -1124,6 +1557,13 @@ cudaError_t launch_attend(const ott_cache_t& c, const uint16_t* q, uint16_t* out
   a.scale_log2 = kLog2e / sqrtf((float)c.head_dim);
   a.k_magic = 0x3C003C00u;
   const int D = c.head_dim, G = c.group_size;
+  if (mma_eligible(c) && G == 32 && use_tc5()) {
+    if (n_rep == 1) return launch_tc5_t<1>(a, st);
+    if (n_rep == 2) return launch_tc5_t<2>(a, st);
+    if (n_rep == 4) return launch_tc5_t<4>(a, st);
+    if (n_rep == 8) return launch_tc5_t<8>(a, st);
+    return cudaErrorInvalidValue;
+  }
   if (mma_eligible(c)) {
 #define OTT_MCASE(NRv, Gv) \
   if (n_rep == NRv && G == Gv) return launch_mma_t<NRv, Gv>(a, st);

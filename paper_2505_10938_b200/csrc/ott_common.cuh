@@ -21,12 +21,25 @@ struct RecordLayout {
   __host__ __device__ int code_bytes() const { return G * d / 4; }  // 2-bit codes
   __host__ __device__ int k_codes() const { return 0; }
   __host__ __device__ int v_codes() const { return code_bytes(); }
-  __host__ __device__ int k_step() const { return 2 * code_bytes(); }
-  __host__ __device__ int k_xmin() const { return k_step() + 4 * d; }
-  __host__ __device__ int v_step() const { return k_xmin() + 4 * d; }
+  __host__ __device__ int k_sh() const { return 2 * code_bytes(); }  // fp16 [d], pair order
+  __host__ __device__ int k_sl() const { return k_sh() + 2 * d; }     // fp16 [d], pair order
+  __host__ __device__ int k_e() const { return k_sl() + 2 * d; }      // f32 [d], channel order
+  __host__ __device__ int v_step() const { return k_e() + 4 * d; }
   __host__ __device__ int v_xmin() const { return v_step() + 4 * G; }
   __host__ __device__ int bytes() const { return v_xmin() + 4 * G; }
 };
+
+// ---- K parameter encoding (tensor-core friendly; exact values live in params64).
+// A 32-bit code word holds 16 channels of one token; the decode kernels extract
+// code pairs (channel m, m+8) of a word in place at fp16 mantissa position P(m)
+// (see ott_attend.cu), so the per-channel K step is stored split into two fp16
+// values sh + sl (sh = fp16_rn(step64), sl = fp16_rn(step64 - sh)) in "pair
+// order" (index 16*(c/16) + 2*(c%8) + (c%16)/8), and x_min is stored folded with
+// that position scale: e = f32_rn(x_min64 - 4 * u(c) * step64), u(c) = 4^(4-P(c%8)).
+// Dequantisation of channel c: k = code * step + x_min = code * step + e + 4 u step.
+__host__ __device__ constexpr int kpair_pos(int m) { return m == 2 || m == 5 ? 2 : (m == 0 || m == 3 || m == 6 ? 3 : 4); }
+__host__ __device__ constexpr float kpair_u(int m) { return kpair_pos(m) == 2 ? 16.f : (kpair_pos(m) == 3 ? 4.f : 1.f); }
+__host__ __device__ constexpr int kpair_index(int c) { return 16 * (c / 16) + 2 * (c % 8) + (c % 16) / 8; }
 
 __host__ __device__ inline size_t mask_words_per_unit(const ott_cache_t& c) {
   return (size_t)c.max_groups * c.group_size / 32;
@@ -38,6 +51,14 @@ __host__ __device__ inline uint8_t* record_ptr(const ott_cache_t& c, int unit, i
 }
 
 __device__ __forceinline__ float h2f(uint16_t h) { return __half2float(__ushort_as_half(h)); }
+// float32 K step / x_min of channel c reconstructed from the record encoding
+__device__ __forceinline__ float k_step_of(const uint8_t* rec, const RecordLayout& L, int c) {
+  const int j = kpair_index(c);
+  return h2f(reinterpret_cast<const uint16_t*>(rec + L.k_sh())[j]) + h2f(reinterpret_cast<const uint16_t*>(rec + L.k_sl())[j]);
+}
+__device__ __forceinline__ float k_xmin_of(const uint8_t* rec, const RecordLayout& L, int c, float step) {
+  return fmaf(4.f * kpair_u(c % 8), step, reinterpret_cast<const float*>(rec + L.k_e())[c]);
+}
 __device__ __forceinline__ uint16_t f2h(float f) { return __half_as_ushort(__float2half_rn(f)); }
 
 template <typename T>

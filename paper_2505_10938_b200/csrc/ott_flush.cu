@@ -277,8 +277,9 @@ __global__ void __launch_bounds__(kFlushThreads) flush_kernel(ott_cache_t c, int
 
     // ---- 3. quantize: K per channel (threads [0,d)), V per token (remaining warps)
     double* p64 = c.params64 ? c.params64 + ((size_t)u * c.max_groups + (size_t)gi) * 2 * (d + G) : nullptr;
-    float* kstep = reinterpret_cast<float*>(rec + L.k_step());
-    float* kxmin = reinterpret_cast<float*>(rec + L.k_xmin());
+    __half* ksh = reinterpret_cast<__half*>(rec + L.k_sh());
+    __half* ksl = reinterpret_cast<__half*>(rec + L.k_sl());
+    float* ke = reinterpret_cast<float*>(rec + L.k_e());
     float* vstep = reinterpret_cast<float*>(rec + L.v_step());
     float* vxmin = reinterpret_cast<float*>(rec + L.v_xmin());
     if (tid < d) {
@@ -292,8 +293,12 @@ __global__ void __launch_bounds__(kFlushThreads) flush_kernel(ott_cache_t c, int
       double step;
       line_params(mn, mx, step);
       for (int i = 0; i < G; ++i) kc[i * d + col] = (uint8_t)quant_code((double)sk[i * d + col], mn, mx, step);
-      kstep[col] = __double2float_rn(step);
-      kxmin[col] = __double2float_rn(mn);
+      // decode-side encoding (ott_common.cuh): step = sh + sl, e = x_min - 4 u step
+      const __half sh = __double2half(step);
+      const __half sl = __double2half(__dsub_rn(step, (double)__half2float(sh)));
+      ksh[kpair_index(col)] = sh;
+      ksl[kpair_index(col)] = sl;
+      ke[col] = __double2float_rn(__dsub_rn(mn, __dmul_rn(4.0 * (double)kpair_u(col % 8), step)));
       if (p64) {
         p64[col] = mn;
         p64[d + col] = step;

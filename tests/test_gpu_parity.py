@@ -38,6 +38,24 @@ def cfg_of(bits, G, R, N, A, d):
     return EngineConfig(bits=bits, group_size=G, residual=R, outlier_num=N, aux_capacity=A, skip_layers=(), head_dim=d)
 
 
+def expected_k_encoding(step64, xmin64):
+    """The record's K parameter encoding (ott_b200.h) computed from the exact
+    float64 params: sh = fp16(step), sl = fp16(step - sh) in pair order, and
+    e = f32(x_min - 4 u(c) step)."""
+    from paper_2505_10938_b200.cache import kpair_index, kpair_u
+    step64 = np.asarray(step64, np.float64)
+    xmin64 = np.asarray(xmin64, np.float64)
+    d = len(step64)
+    sh = step64.astype(np.float16)
+    sl = (step64 - sh.astype(np.float64)).astype(np.float16)
+    e = (xmin64 - 4.0 * kpair_u(np.arange(d)).astype(np.float64) * step64).astype(np.float32)
+    sh_p = np.empty(d, np.float16)
+    sl_p = np.empty(d, np.float16)
+    sh_p[kpair_index(np.arange(d))] = sh
+    sl_p[kpair_index(np.arange(d))] = sl
+    return sh_p, sl_p, e
+
+
 def assert_unit_matches_oracle(u, ref, exact64=True):
     """Bit-exact quantization state of one GPU unit vs an oracle cache."""
     assert u.total_tokens == ref.total_tokens and u.quantized_tokens == ref.quantized_tokens
@@ -51,8 +69,10 @@ def assert_unit_matches_oracle(u, ref, exact64=True):
             assert [p.step for p in u.quantized_k[b].params] == blk["k_step"].tolist()
             assert [p.x_min for p in u.quantized_v[b].params] == blk["v_xmin"].tolist()
             assert [p.step for p in u.quantized_v[b].params] == blk["v_step"].tolist()
-        np.testing.assert_array_equal(u.k_step32[b], blk["k_step"].astype(np.float32))
-        np.testing.assert_array_equal(u.k_xmin32[b], blk["k_xmin"].astype(np.float32))
+        sh, sl, e = expected_k_encoding(blk["k_step"], blk["k_xmin"])
+        np.testing.assert_array_equal(u.k_sh16[b].view(np.uint16), sh.view(np.uint16))
+        np.testing.assert_array_equal(u.k_sl16[b].view(np.uint16), sl.view(np.uint16))
+        np.testing.assert_array_equal(u.k_e32[b], e)
         np.testing.assert_array_equal(u.v_step32[b], blk["v_step"].astype(np.float32))
         np.testing.assert_array_equal(u.v_xmin32[b], blk["v_xmin"].astype(np.float32))
     pe = ref.pool_entries()

@@ -1,0 +1,5 @@
+for v in "$@"; do
+  echo "== $v"
+  if [ "$v" = base ]; then L=""; else L="OTT_LIB_PATH=tools/variants/$v.so"; fi
+  env $L timeout 120 python tools/prof_attend.py --batch 128 --rep 8 --ctx 16384 --iters 10 2>&1 | tail -1
+done
