@@ -282,29 +282,26 @@ def run_ours(args, wl, rank, world, local_rank):
     # e2e: through the public API with HOST buffers (pinned), copies inside the timed region
     e2e = None
     if not args.no_e2e:
+        from paper_2505_10938_b200.pipeline import HostDecodePipeline
+
         k_h = kin[0].cpu().pin_memory()
         v_h = vin[0].cpu().pin_memory()
         q_h = qin[0].cpu().pin_memory()
         o_h = torch.empty((L, B, Hq, d), dtype=torch.float16).pin_memory()
-        k_d = torch.empty((B, H, d), dtype=torch.float16, device=dev)
-        v_d, q_d = torch.empty_like(k_d), torch.empty((B, Hq, d), dtype=torch.float16, device=dev)
+        gather = None
+        if gathered is not None:
+            def gather(o_local, l):
+                all_gather_heads(o_local, out=gathered[l])
+                return gathered[l][b_lo:b_hi]
+        pipe = HostDecodePipeline(caches, Hq, gather=gather)
+        pipe.step(k_h, v_h, q_h, o_h)  # warm-up (streams, events)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for i in range(args.steps):
-            for l in range(L):
-                k_d.copy_(k_h[l], non_blocking=True)
-                v_d.copy_(v_h[l], non_blocking=True)
-                q_d.copy_(q_h[l], non_blocking=True)
-                caches[l].append(k_d, v_d)
-                caches[l].attend(q_d, out=outs[l], n_splits=splits[l])
-                if gathered is not None:
-                    all_gather_heads(outs[l], out=gathered[l])
-                    o_h[l].copy_(gathered[l][b_lo:b_hi], non_blocking=True)
-                else:
-                    o_h[l].copy_(outs[l], non_blocking=True)
+            pipe.step(k_h, v_h, q_h, o_h)
         e1.record()
         torch.cuda.synchronize()
         e_ms = torch.tensor([e0.elapsed_time(e1)], device=dev)

@@ -423,3 +423,43 @@ def test_config2_streaming_stress_sampled(N):
             assert not u.pool.frozen and len(u.pool.aux) > 0  # eviction fired, pool still live
         ok, err = within_tol(out[b, h], ref.attend(qh[b, h].astype(np.float32)))
         assert ok, (b, h, err)
+
+
+# --------------------------------------------------------------------------- host-buffer pipeline
+
+
+def test_host_pipeline_matches_direct_calls():
+    """HostDecodePipeline (overlapped H2D / kernels / D2H over a layer stack) gives
+    bit-identical outputs and cache state to plain per-layer append + attend."""
+    from paper_2505_10938_b200 import OTTCache
+    from paper_2505_10938_b200.pipeline import HostDecodePipeline
+
+    L, B, H, n_rep, d, T, steps = 3, 2, 2, 4, 128, 700, 40
+    rng = np.random.default_rng(11)
+    mk = lambda *s: rng.standard_normal(s).astype(np.float16)  # noqa: E731
+    pre_k, pre_v = mk(L, B, H, T, d), mk(L, B, H, T, d)
+    ks, vs, qs = mk(steps, L, B, H, d), mk(steps, L, B, H, d), mk(steps, L, B, H * n_rep, d)
+
+    def stack():
+        cs = [OTTCache(cfg_of(2, 32, 128, 4, 32, d), B, H, max_tokens=T + steps + 8, layer=l) for l in range(L)]
+        for l, c in enumerate(cs):
+            c.update(torch.from_numpy(pre_k[l]).cuda(), torch.from_numpy(pre_v[l]).cuda())
+        return cs
+
+    direct, piped = stack(), stack()
+    pipe = HostDecodePipeline(piped, H * n_rep)
+    out_h = torch.empty((L, B, H * n_rep, d), dtype=torch.float16).pin_memory()
+    for i in range(steps):
+        ref = []
+        for l, c in enumerate(direct):
+            c.append(torch.from_numpy(ks[i, l]).cuda(), torch.from_numpy(vs[i, l]).cuda())
+            ref.append(c.attend(torch.from_numpy(qs[i, l]).cuda()).cpu())
+        k_h = torch.from_numpy(ks[i]).pin_memory()
+        v_h = torch.from_numpy(vs[i]).pin_memory()
+        q_h = torch.from_numpy(qs[i]).pin_memory()
+        pipe.step(k_h, v_h, q_h, out_h).synchronize()
+        for l in range(L):
+            assert torch.equal(out_h[l], ref[l]), (i, l)
+    for a, b in zip(direct, piped):
+        assert a.total_tokens == b.total_tokens and a.quantized_tokens == b.quantized_tokens
+        assert torch.equal(a.blocks, b.blocks)
