@@ -9,7 +9,7 @@ Under torchrun (N>1) the batch is partitioned across ranks (whole sequences,
 all kv heads of a sequence on one rank) and head outputs are all-gathered over
 NCCL every layer.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4|c3|c3s|c2|c0]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4|c3|c3s|c2|c0|c1]
   python bench.py --impl reference ...   # CPU oracle port of the reference path
 
 Prints one JSON line (rank 0).
@@ -347,6 +347,61 @@ def run_ours(args, wl, rank, world, local_rank):
         print(json.dumps(line), flush=True)
 
 
+
+# ----------------------------------------------------------------------------- config 1 (model decode)
+
+
+def run_c1(args, rank, world, local_rank):
+    """BASELINE configs[1]: Llama-2-7B-shaped random-init decoder, B=8, 2048-token
+    random prompt, 256 greedy decode steps with the OTT cache (2-bit, G=32, R=128,
+    pool 32, paper skip_layers (0, 1)); the fp16-KV-cache decoder with the same
+    weights is timed beside it. Replicas only under torchrun (each rank its own batch)."""
+    import torch
+
+    from paper_2505_10938_b200.model import LLAMA2_7B, Decoder
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    B, T, steps = 8, 2048, args.steps if args.steps != 32 else 256
+    prompt = torch.randint(0, LLAMA2_7B.vocab, (B, T), generator=torch.Generator().manual_seed(rank)).to(dev)
+    res = {}
+    for kv in ("ott", "fp16"):
+        m = Decoder(LLAMA2_7B, B, T + steps + 8, kv=kv, device=dev, seed=0)
+        torch.cuda.synchronize()
+        t0 = time.time()
+        tok = m.prefill(prompt)
+        torch.cuda.synchronize()
+        prefill_s = time.time() - t0
+        for _ in range(args.warmup):  # warm-up decode steps (allocator, cuBLAS heuristics)
+            tok = m.decode(tok)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        gen = []
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(steps):
+            tok = m.decode(tok)
+            gen.append(tok)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        res[kv] = {"tok_s": B * steps / (ms / 1e3), "ms_per_step": ms / steps, "prefill_s": prefill_s,
+                   "tokens": torch.stack(gen, 1).cpu()}
+        del m
+        torch.cuda.empty_cache()
+    agree = float((res["ott"]["tokens"] == res["fp16"]["tokens"]).float().mean())
+    if rank == 0:
+        print(json.dumps({
+            "metric": "decode tokens/s (config 1: Llama-2-7B-shaped decoder, OTT cache)", "value": res["ott"]["tok_s"] * world,
+            "unit": "tokens/s", "n_gpus": world, "steps": steps, "warmup": args.warmup,
+            "ms_per_step": res["ott"]["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f16 weights/activations, u2 KV codes", "data": "synthetic (random ids, random-init weights)",
+            "config": {"workload": "config1-llama2-7b-B8-prompt2048-decode%d" % steps, "batch": B, "prompt": T,
+                       "layers": LLAMA2_7B.n_layers, "parallelism": f"replicas x{world}"},
+            "fp16_kv_baseline": {"value": res["fp16"]["tok_s"] * world, "ms_per_step": res["fp16"]["ms_per_step"]},
+            "prefill_s": {"ott": round(res["ott"]["prefill_s"], 3), "fp16": round(res["fp16"]["prefill_s"], 3)},
+            "greedy_token_agreement_vs_fp16": agree,
+        }), flush=True)
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -359,10 +414,18 @@ def main():
     args = ap.parse_args()
     from paper_2505_10938_b200.workloads import WORKLOADS
 
-    wl = WORKLOADS[args.config]
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.config == "c1":
+        if args.impl == "reference":
+            if rank == 0:
+                print(json.dumps({"impl": "reference", "unavailable": "config 1 is a model decode; the reference "
+                                  "has no model (bench.py --impl reference times the default config-4 path)"}))
+            return
+        run_c1(args, rank, world, local_rank)
+        return
+    wl = WORKLOADS[args.config]
     if args.impl == "reference":
         run_reference(args, wl, rank, world)
         return

@@ -463,3 +463,39 @@ def test_host_pipeline_matches_direct_calls():
     for a, b in zip(direct, piped):
         assert a.total_tokens == b.total_tokens and a.quantized_tokens == b.quantized_tokens
         assert torch.equal(a.blocks, b.blocks)
+
+
+# --------------------------------------------------------------------------- config-1 decoder
+
+
+def test_decoder_ott_plumbing_matches_fp16_cache():
+    """Llama-shaped decoder (BASELINE configs[1], scaled down). With a residual window
+    longer than the whole run the OTT cache keeps every row in full precision, so the
+    OTT decoder must reproduce the fp16-KV-cache decoder (RoPE positions, append, attend
+    and layer plumbing); with the config-1 cache (G=32, R=128) the cache quantizes
+    during prefill and decode and stays finite."""
+    from paper_2505_10938_b200 import EngineConfig
+    from paper_2505_10938_b200.model import Decoder, DecoderConfig
+
+    cfg = DecoderConfig(n_layers=3, hidden=512, n_heads=4, n_kv_heads=4, head_dim=128, mlp=1024, vocab=1000)
+    B, T, steps = 2, 400, 48
+    prompt = torch.randint(0, cfg.vocab, (B, T), generator=torch.Generator().manual_seed(3)).cuda()
+    lossless = EngineConfig(bits=2, group_size=32, residual=512, outlier_num=32, aux_capacity=32, head_dim=128)
+    ott = Decoder(cfg, B, T + steps + 8, kv="ott", ott=lossless, seed=7)
+    ref = Decoder(cfg, B, T + steps + 8, kv="fp16", seed=7)
+    tok = ref.prefill(prompt)
+    assert torch.equal(ott.prefill(prompt), tok)
+    for _ in range(steps):
+        t_ott = ott.decode(tok)
+        tok = ref.decode(tok)
+        a, b = ott.last_logits.float(), ref.last_logits.float()
+        assert torch.equal(t_ott, tok)
+        assert (a - b).abs().max().item() <= 2e-2 * b.abs().max().item()
+    assert ott.caches[0].quantized_tokens == 0 and ott.caches[-1].total_tokens == T + steps
+
+    q = Decoder(cfg, B, T + steps + 8, kv="ott", seed=7)  # config-1 cache: 2-bit G=32 R=128 N=32
+    tok = q.prefill(prompt)
+    for _ in range(steps):
+        tok = q.decode(tok)
+        assert torch.isfinite(q.last_logits).all()
+    assert q.caches[0].quantized_tokens == ((T + steps - 128) // 32) * 32
