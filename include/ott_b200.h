@@ -17,6 +17,8 @@
  *                       (reconstructed_kv attention.py:62-76,
  *                       attend_full_precision attention.py:35-59)
  *   ott_logits       <- AttentionResult.scores         attention.py:26-32 (debug)
+ *   ott_decode_step  <- append + attend_mixed of one decode step, token counts in device
+ *                       memory (CUDA-graph capturable)    cache.py:124-139, attention.py:79-92
  *
  * Conventions: all buffer pointers are DEVICE memory owned by the caller (the
  * host layer allocates them; this library never allocates or frees). Every
@@ -111,6 +113,17 @@ int ott_attend(const ott_cache_t* c, const uint16_t* q, uint16_t* out, int32_t n
 
 /* Debug: pre-softmax logits (AttentionResult.scores, attention.py:55) for all
  * total_tokens positions, float32 [n_units][n_rep][total_tokens]. */
+/* One decode step with the token counts in device memory, so a whole model step can be
+ * captured in a CUDA graph and replayed: counters = int64[2] {quantized_tokens,
+ * total_tokens} on the device, read by the kernels and advanced by the last one.
+ * Launches: ring write of (k, v) [n_units][head_dim] at position total, flush of one
+ * group per unit iff it became due (cache.py:138; the kernel returns early otherwise),
+ * split-K attention of q [n_units*n_rep][head_dim] -> out, and the combine. n_splits
+ * is fixed by the caller (size it for the largest context of the run). The caller
+ * guarantees capacity (max_groups) for the steps it replays. */
+int ott_decode_step(const ott_cache_t* c, const uint16_t* k, const uint16_t* v, const uint16_t* q, uint16_t* out,
+                    int32_t n_rep, int64_t* counters, float* workspace, int32_t n_splits, void* stream);
+
 int ott_logits(const ott_cache_t* c, const uint16_t* q, float* logits, int32_t n_rep, int64_t quantized_tokens,
                int64_t total_tokens, void* stream);
 

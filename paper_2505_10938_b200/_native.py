@@ -63,6 +63,7 @@ def lib() -> ctypes.CDLL:
         L.ott_attend_workspace_floats.restype = ctypes.c_size_t
         L.ott_attend.argtypes = [P, _vp, _vp, _i32, _i64, _i64, _vp, _i32, _vp]
         L.ott_logits.argtypes = [P, _vp, _vp, _i32, _i64, _i64, _vp]
+        L.ott_decode_step.argtypes = [P, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _i32, _vp]
         L.ott_num_sms.argtypes = []
         L.ott_version.restype = ctypes.c_char_p
         L.ott_last_error.restype = ctypes.c_char_p
@@ -71,7 +72,7 @@ def lib() -> ctypes.CDLL:
 
 
 EXPORTED = ("ott_record_bytes", "ott_ring_write", "ott_flush", "ott_pick_splits", "ott_attend_workspace_floats",
-            "ott_attend", "ott_logits", "ott_num_sms", "ott_version", "ott_last_error")
+            "ott_attend", "ott_logits", "ott_decode_step", "ott_num_sms", "ott_version", "ott_last_error")
 
 
 def check(status: int) -> None:

@@ -123,6 +123,8 @@ class OTTCache:
         self._cref = ctypes.byref(self._c)
         self.total_tokens = 0
         self.quantized_tokens = 0
+        # device copy of (quantized_tokens, total_tokens) for graph-capturable decode steps
+        self.counters = torch.zeros(2, dtype=torch.int64, device=dev)
         self._ws = None
         self._ws_key = None
 
@@ -204,6 +206,42 @@ class OTTCache:
         if self._ws is None or self._ws.numel() < n:
             self._ws = torch.empty(n, dtype=torch.float32, device=self.device)
         return self._ws
+
+    def sync_counters(self) -> None:
+        """Copy the host token counts into `counters` (before capturing `decode_step`)."""
+        self.counters.copy_(torch.tensor([self.quantized_tokens, self.total_tokens], dtype=torch.int64))
+
+    def decode_step(self, k: torch.Tensor, v: torch.Tensor, q: torch.Tensor, out: torch.Tensor,
+                    n_splits: int) -> torch.Tensor:
+        """append(k, v) + attend(q) -> out with the token counts read from and advanced
+        in device memory (`counters`), so the launches can be captured in a CUDA graph
+        and replayed once per step (ott_decode_step). The host counts advance too; call
+        `sync_counters()` once before the first device-counter step."""
+        k = self._check_rows(k, "k")
+        v = self._check_rows(v, "v")
+        require(q.dim() == 3 and q.shape[0] == self.batch and q.shape[2] == self.config.head_dim
+                and q.shape[1] % self.n_kv_heads == 0 and q.dtype == torch.float16 and q.is_contiguous(),
+                "query must be contiguous float16 (batch, H_q, head_dim)")
+        require(out.shape == q.shape and out.dtype == torch.float16 and out.is_contiguous(), "bad output buffer")
+        G, R = self.config.group_size, self.config.residual
+        due = self.total_tokens + 1 - self.quantized_tokens - R >= G
+        require(not due or self.quantized_tokens // G + 1 <= self.max_groups, "cache capacity (max_tokens) exceeded")
+        n_rep = q.shape[1] // self.n_kv_heads
+        ws = self.workspace(n_rep, n_splits)
+        _native.check(_native.lib().ott_decode_step(self._cref, k.data_ptr(), v.data_ptr(), q.data_ptr(),
+                                                    out.data_ptr(), n_rep, self.counters.data_ptr(), ws.data_ptr(),
+                                                    n_splits, _stream_handle()))
+        self.advance_host_counts()
+        return out
+
+    def advance_host_counts(self) -> None:
+        """Host mirror of one device-counter step (what the combine kernel does to
+        `counters`); used by callers that replay a captured `decode_step`."""
+        G, R = self.config.group_size, self.config.residual
+        self.total_tokens += 1
+        if self.total_tokens - self.quantized_tokens - R >= G:
+            require(self.quantized_tokens // G + 1 <= self.max_groups, "cache capacity (max_tokens) exceeded")
+            self.quantized_tokens += G
 
     def attend(self, q: torch.Tensor, out: torch.Tensor | None = None, n_splits: int | None = None) -> torch.Tensor:
         """attend_mixed (attention.py:79-92) for every query head.

@@ -54,7 +54,34 @@ struct AttnArgs {
   float scale_log2;                  // log2(e) / float32(sqrt(d))
   uint32_t k_magic;                  // 0x3C003C00 (fp16 1.0 pair), passed at run time so the
                                      // compiler keeps it in a register: one LOP3 per code pair
+  const int64_t* dev_counts;         // non-null: device-counter decode step (token counts below are
+                                     // taken from [quantized, total] before this step's append)
 };
+
+// Token counts of one launch. Host mode: the launch arguments. Device-counter mode
+// (CUDA-graph decode step: ring write, flush-if-due, attend, combine): the counters
+// hold the state before the step's append, which has already been written, and the
+// flush kernel has quantized one group iff it was due (cache.py:138).
+struct Counts {
+  int64_t q_tokens, total_tokens;
+  int n_qtiles, n_ptiles, n_rtiles;
+};
+__device__ __forceinline__ Counts counts_of(const AttnArgs& a) {
+  Counts k;
+  if (a.dev_counts) {
+    const int64_t qt = a.dev_counts[0], tot = a.dev_counts[1] + 1;
+    const bool due = tot - qt - a.c.residual >= a.c.group_size && qt / a.c.group_size + 1 <= a.c.max_groups;
+    k.q_tokens = qt + (due ? a.c.group_size : 0);
+    k.total_tokens = tot;
+  } else {
+    k.q_tokens = a.q_tokens;
+    k.total_tokens = a.total_tokens;
+  }
+  k.n_qtiles = (int)(k.q_tokens / 32);
+  k.n_ptiles = (a.c.capacity + 31) / 32;
+  k.n_rtiles = (int)((k.total_tokens - k.q_tokens + 31) / 32);
+  return k;
+}
 
 // ============================================================ SIMT (CUDA-core) tiles
 template <int NR, int D>
@@ -98,7 +125,8 @@ __device__ __forceinline__ void online_update(float (&s)[NR], float (&m)[NR], fl
 // Processes 32-token tiles [t_begin, t_end) of unit u (warp-strided), merges
 // the warps of the CTA and writes partial `split`.
 template <int NR, int D>
-__device__ void simt_body(const AttnArgs& a, int u, int t_begin, int t_end, int split, SimtSmem<NR, D>& sm) {
+__device__ void simt_body(const AttnArgs& a, const Counts& n, int u, int t_begin, int t_end, int split,
+                          SimtSmem<NR, D>& sm) {
   const ott_cache_t& c = a.c;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int G = c.group_size, N = c.capacity, cap = G + c.residual;
@@ -121,7 +149,7 @@ __device__ void simt_body(const AttnArgs& a, int u, int t_begin, int t_end, int 
 
   for (int t = t_begin + warp; t < t_end; t += kAttnWarps) {
     float s[NR];
-    if (t < a.n_qtiles) {
+    if (t < n.n_qtiles) {
       const int64_t tok0 = (int64_t)t * 32;
       const int64_t gi = tok0 / G;
       const int row0 = (int)(tok0 - gi * G);
@@ -180,19 +208,19 @@ __device__ void simt_body(const AttnArgs& a, int u, int t_begin, int t_end, int 
       }
       __syncwarp();
     } else {
-      const bool is_pool = t < a.n_qtiles + a.n_ptiles;
+      const bool is_pool = t < n.n_qtiles + n.n_ptiles;
       const uint16_t *krow, *vrow;
       bool valid;
       if (is_pool) {
-        const int slot = (t - a.n_qtiles) * 32 + lane;
+        const int slot = (t - n.n_qtiles) * 32 + lane;
         valid = slot < N && c.pool_pos[(size_t)u * N + slot] >= 0;
         const size_t off = ((size_t)u * N + (valid ? slot : 0)) * D;
         krow = c.pool_k + off;
         vrow = c.pool_v + off;
       } else {
-        const int64_t p = a.q_tokens + (int64_t)(t - a.n_qtiles - a.n_ptiles) * 32 + lane;
-        valid = p < a.total_tokens;
-        const size_t off = ((size_t)u * cap + (size_t)((valid ? p : a.q_tokens) % cap)) * D;
+        const int64_t p = n.q_tokens + (int64_t)(t - n.n_qtiles - n.n_ptiles) * 32 + lane;
+        valid = p < n.total_tokens;
+        const size_t off = ((size_t)u * cap + (size_t)((valid ? p : n.q_tokens) % cap)) * D;
         krow = c.pend_k + off;
         vrow = c.pend_v + off;
       }
@@ -270,11 +298,12 @@ template <int NR, int D>
 __global__ void __launch_bounds__(kAttnThreads) attend_simt_kernel(AttnArgs a) {
   extern __shared__ __align__(256) unsigned char smem_raw[];
   SimtSmem<NR, D>& sm = *reinterpret_cast<SimtSmem<NR, D>*>(smem_raw);
-  const int n_tiles = a.n_qtiles + a.n_ptiles + a.n_rtiles;
+  const Counts n = counts_of(a);
+  const int n_tiles = n.n_qtiles + n.n_ptiles + n.n_rtiles;
   const int per = (n_tiles + a.n_splits - 1) / a.n_splits;
   const int t_begin = blockIdx.y * per;
   const int t_end = min(n_tiles, t_begin + per);
-  simt_body<NR, D>(a, blockIdx.x, t_begin, t_end, blockIdx.y, sm);
+  simt_body<NR, D>(a, n, blockIdx.x, t_begin, t_end, blockIdx.y, sm);
 }
 
 // ============================================================ tensor-core path
@@ -413,7 +442,7 @@ struct MmaSmem {
 
 // Quantized-region partial for (unit blockIdx.x, split blockIdx.y < n_qsplits).
 template <int NR, int G>
-__device__ void mma_body(const AttnArgs& a, const CUtensorMap* tmap, MmaSmem<G>& sm) {
+__device__ void mma_body(const AttnArgs& a, const Counts& n, const CUtensorMap* tmap, MmaSmem<G>& sm) {
   constexpr int D = 128;
   constexpr int kRec = MmaSmem<G>::kRec;
   constexpr int kMt = G / 16;  // 16-token m-tiles per group
@@ -425,7 +454,7 @@ __device__ void mma_body(const AttnArgs& a, const CUtensorMap* tmap, MmaSmem<G>&
   const int g = lane >> 2, tig = lane & 3;
 
   const uint32_t magic = a.k_magic;
-  const int n_groups = (int)(a.q_tokens / G);
+  const int n_groups = (int)(n.q_tokens / G);
   const int per = (n_groups + a.n_qsplits - 1) / a.n_qsplits;
   const int g0 = split * per;
   const int g1 = min(n_groups, g0 + per);
@@ -757,7 +786,7 @@ __device__ __forceinline__ void tma_row(uint32_t dst, const void* src, uint32_t 
 }
 
 template <int NR>
-__device__ void fp_body(const AttnArgs& a, FpSmem& sm) {
+__device__ void fp_body(const AttnArgs& a, const Counts& n, FpSmem& sm) {
   constexpr int D = 128, kRow = FpSmem::kRow;
   const ott_cache_t& c = a.c;
   const int u = blockIdx.x, split = blockIdx.y;
@@ -765,7 +794,7 @@ __device__ void fp_body(const AttnArgs& a, FpSmem& sm) {
   const int g = lane >> 2, tig = lane & 3;
   const int N = c.capacity, cap = c.group_size + c.residual;
   const int n_pool_t = (N + 15) / 16;
-  const int Tp = (int)(a.total_tokens - a.q_tokens);
+  const int Tp = (int)(n.total_tokens - n.q_tokens);
   const int n_tiles = n_pool_t + (Tp + 15) / 16;
 
   // q (exact fp16) as the B fragments of Q K^T: head g, channels 16j + 2tig (+1), +8
@@ -828,7 +857,7 @@ __device__ void fp_body(const AttnArgs& a, FpSmem& sm) {
         if (is_pool) {
           off = ((size_t)u * N + 16 * t + r) * D;
         } else {
-          const int64_t p = a.q_tokens + 16 * (t - n_pool_t) + r;
+          const int64_t p = n.q_tokens + 16 * (t - n_pool_t) + r;
           off = ((size_t)u * cap + (size_t)(p % cap)) * D;
         }
         tma_row(kr_s + r * kRow, (is_pool ? c.pool_k : c.pend_k) + off, bar);
@@ -942,9 +971,9 @@ __global__ void __launch_bounds__(kAttnThreads, OTT_MMA_MIN_BLOCKS)
     attend_mma_kernel(const __grid_constant__ AttnArgs a, const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(256) unsigned char smem_raw[];
   if ((int)blockIdx.y == a.n_qsplits) {  // full-precision tiers: pool.entries + pending window
-    fp_body<NR>(a, *reinterpret_cast<FpSmem*>(smem_raw));
+    fp_body<NR>(a, counts_of(a), *reinterpret_cast<FpSmem*>(smem_raw));
   } else {
-    mma_body<NR, G>(a, &tmap, *reinterpret_cast<MmaSmem<G>*>(smem_raw));
+    mma_body<NR, G>(a, counts_of(a), &tmap, *reinterpret_cast<MmaSmem<G>*>(smem_raw));
   }
 }
 
@@ -1108,14 +1137,14 @@ __device__ __forceinline__ void tc5_kstage(Tc5Smem& sm, int w, int lane, const u
 }
 
 template <int NR>
-__device__ void tc5_body(const AttnArgs& a, const CUtensorMap* tmap, Tc5Smem& sm) {
+__device__ void tc5_body(const AttnArgs& a, const Counts& n, const CUtensorMap* tmap, Tc5Smem& sm) {
   constexpr int D = 128, G = 32, kS = tc5::kStages;
   const RecordLayout L(D, G);
   const ott_cache_t& c = a.c;
   const int u = blockIdx.x, split = blockIdx.y;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, tig = lane & 3;
-  const int n_groups = (int)(a.q_tokens / G);
+  const int n_groups = (int)(n.q_tokens / G);
   const int per = (((n_groups + a.n_qsplits - 1) / a.n_qsplits) + 3) & ~3;  // whole chunks per split
   const int g0 = min(n_groups, split * per);
   const int g1 = min(n_groups, g0 + per);
@@ -1394,16 +1423,22 @@ __global__ void __launch_bounds__(tc5::kThreads, OTT_TC5_MIN_BLOCKS)
   extern __shared__ __align__(256) unsigned char smem_raw[];
   if ((int)blockIdx.y == a.n_qsplits) {  // full-precision tiers on warps 0-3
     if (threadIdx.x >= 128) return;
-    fp_body<NR>(a, *reinterpret_cast<FpSmem*>(smem_raw));
+    fp_body<NR>(a, counts_of(a), *reinterpret_cast<FpSmem*>(smem_raw));
   } else {
-    tc5_body<NR>(a, &tmap, *reinterpret_cast<Tc5Smem*>(smem_raw));
+    tc5_body<NR>(a, counts_of(a), &tmap, *reinterpret_cast<Tc5Smem*>(smem_raw));
   }
 }
 
 // ============================================================ combine + debug logits
 template <int D>
-__global__ void combine_kernel(const float* __restrict__ ws, uint16_t* __restrict__ out, int n_splits) {
+__global__ void combine_kernel(const float* __restrict__ ws, uint16_t* __restrict__ out, int n_splits,
+                               int64_t* __restrict__ dev_counts, int G, int R, int max_groups) {
   const int ur = blockIdx.x;  // unit*NR + r
+  if (dev_counts && ur == 0 && threadIdx.x == 0) {  // last kernel of a device-counter step: advance
+    const int64_t qt = dev_counts[0], tot = dev_counts[1] + 1;
+    if (tot - qt - R >= G && qt / G + 1 <= max_groups) dev_counts[0] = qt + G;
+    dev_counts[1] = tot;
+  }
   const float* base = ws + (size_t)ur * n_splits * (D + 2);
   float M = -INFINITY;
   for (int s = 0; s < n_splits; ++s) M = fmaxf(M, base[(size_t)s * (D + 2)]);
@@ -1470,7 +1505,8 @@ static cudaError_t launch_simt_t(const AttnArgs& a, cudaStream_t st) {
   attend_simt_kernel<NR, D><<<dim3(a.c.n_units, a.n_splits), kAttnThreads, smem, st>>>(a);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  combine_kernel<D><<<a.c.n_units * NR, D, 0, st>>>(a.ws, a.out, a.n_splits);
+  combine_kernel<D><<<a.c.n_units * NR, D, 0, st>>>(a.ws, a.out, a.n_splits, const_cast<int64_t*>(a.dev_counts),
+                                                   a.c.group_size, a.c.residual, a.c.max_groups);
   return cudaGetLastError();
 }
 
@@ -1507,7 +1543,8 @@ static cudaError_t launch_mma_t(const AttnArgs& a, cudaStream_t st) {
   attend_mma_kernel<NR, G><<<dim3(a.c.n_units, a.n_splits), kAttnThreads, smem, st>>>(a, tmap);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  combine_kernel<128><<<a.c.n_units * NR, 128, 0, st>>>(a.ws, a.out, a.n_splits);
+  combine_kernel<128><<<a.c.n_units * NR, 128, 0, st>>>(a.ws, a.out, a.n_splits, const_cast<int64_t*>(a.dev_counts),
+                                                     a.c.group_size, a.c.residual, a.c.max_groups);
   return cudaGetLastError();
 }
 
@@ -1522,7 +1559,8 @@ static cudaError_t launch_tc5_t(const AttnArgs& a, cudaStream_t st) {
   attend_tc5_kernel<NR><<<dim3(a.c.n_units, a.n_splits), tc5::kThreads, smem, st>>>(a, tmap);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  combine_kernel<128><<<a.c.n_units * NR, 128, 0, st>>>(a.ws, a.out, a.n_splits);
+  combine_kernel<128><<<a.c.n_units * NR, 128, 0, st>>>(a.ws, a.out, a.n_splits, const_cast<int64_t*>(a.dev_counts),
+                                                     a.c.group_size, a.c.residual, a.c.max_groups);
   return cudaGetLastError();
 }
 
@@ -1541,8 +1579,9 @@ static bool use_tc5() {
 bool mma_eligible(const ott_cache_t& c) { return c.head_dim == 128; }
 
 cudaError_t launch_attend(const ott_cache_t& c, const uint16_t* q, uint16_t* out, int n_rep, int64_t q_tokens,
-                          int64_t total, float* ws, int n_qsplits, cudaStream_t st) {
+                          int64_t total, float* ws, int n_qsplits, cudaStream_t st, int64_t* dev_counts) {
   AttnArgs a;
+  a.dev_counts = dev_counts;
   a.c = c;
   a.q = q;
   a.out = out;

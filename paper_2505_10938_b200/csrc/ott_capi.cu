@@ -7,11 +7,13 @@
 
 namespace ott {
 cudaError_t launch_flush(const ott_cache_t& c, int64_t q0, int n_groups, int64_t ring_end, const uint16_t* in_k,
-                         const uint16_t* in_v, int64_t in_stride, int64_t in_first, cudaStream_t st);
+                         const uint16_t* in_v, int64_t in_stride, int64_t in_first, cudaStream_t st,
+                         const int64_t* dev_counts = nullptr);
 cudaError_t launch_ring_write(const ott_cache_t& c, const uint16_t* k, const uint16_t* v, int64_t in_stride,
-                              int64_t in_first, int64_t first_pos, int64_t n_rows, cudaStream_t st);
+                              int64_t in_first, int64_t first_pos, int64_t n_rows, cudaStream_t st,
+                              const int64_t* dev_counts = nullptr);
 cudaError_t launch_attend(const ott_cache_t& c, const uint16_t* q, uint16_t* out, int n_rep, int64_t q_tokens,
-                          int64_t total, float* ws, int n_splits, cudaStream_t st);
+                          int64_t total, float* ws, int n_splits, cudaStream_t st, int64_t* dev_counts = nullptr);
 cudaError_t launch_logits(const ott_cache_t& c, const uint16_t* q, float* logits, int n_rep, int64_t q_tokens,
                           int64_t total, cudaStream_t st);
 }  // namespace ott
@@ -134,6 +136,22 @@ int ott_attend(const ott_cache_t* c, const uint16_t* q, uint16_t* out, int32_t n
   if (!q || !out || !workspace || n_splits < 1) return fail(OTT_ERR_CONTRACT, "null buffer or bad split count");
   return cuda_status(ott::launch_attend(*c, q, out, n_rep, quantized_tokens, total_tokens, workspace, n_splits,
                                         (cudaStream_t)stream));
+}
+
+int ott_decode_step(const ott_cache_t* c, const uint16_t* k, const uint16_t* v, const uint16_t* q, uint16_t* out,
+                    int32_t n_rep, int64_t* counters, float* workspace, int32_t n_splits, void* stream) {
+  int s = check_cache(c);
+  if (s) return s;
+  if (n_rep != 1 && n_rep != 2 && n_rep != 4 && n_rep != 8) return fail(OTT_ERR_UNSUPPORTED, "n_rep must be 1, 2, 4 or 8");
+  if (!k || !v || !q || !out || !counters || !workspace || n_splits < 1)
+    return fail(OTT_ERR_CONTRACT, "null buffer or bad split count");
+  if (c->capacity > 0 && (!c->pool_pos || !c->pool_score || !c->pool_k || !c->pool_v))
+    return fail(OTT_ERR_CONTRACT, "null pool buffers");
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = ott::launch_ring_write(*c, k, v, c->head_dim, 0, 0, 1, st, counters);
+  if (e == cudaSuccess) e = ott::launch_flush(*c, 0, 1, 0, nullptr, nullptr, 0, 0, st, counters);
+  if (e == cudaSuccess) e = ott::launch_attend(*c, q, out, n_rep, 0, 1, workspace, n_splits, st, counters);
+  return cuda_status(e);
 }
 
 int ott_logits(const ott_cache_t* c, const uint16_t* q, float* logits, int32_t n_rep, int64_t quantized_tokens,

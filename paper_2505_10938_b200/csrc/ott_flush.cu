@@ -57,7 +57,15 @@ __host__ __device__ inline size_t flush_smem_bytes(int d, int G, int N) {
 __global__ void __launch_bounds__(kFlushThreads) flush_kernel(ott_cache_t c, int64_t q0, int n_groups,
                                                               int64_t ring_end, const uint16_t* __restrict__ in_k,
                                                               const uint16_t* __restrict__ in_v,
-                                                              int64_t in_stride, int64_t in_first) {
+                                                              int64_t in_stride, int64_t in_first,
+                                                              const int64_t* __restrict__ dev_counts) {
+  if (dev_counts) {  // device-counter decode step: flush one group iff the append just made it due
+    const int64_t qt = dev_counts[0], tot = dev_counts[1] + 1;
+    if (tot - qt - c.residual < c.group_size || qt / c.group_size + 1 > c.max_groups) return;
+    q0 = qt;
+    n_groups = 1;
+    ring_end = tot;
+  }
   const int u = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nwarps = kFlushThreads / 32;
@@ -356,7 +364,12 @@ __global__ void __launch_bounds__(kFlushThreads) flush_kernel(ott_cache_t c, int
 
 // K4: ring write. One thread per 8 halves.
 __global__ void ring_write_kernel(ott_cache_t c, const uint16_t* __restrict__ k, const uint16_t* __restrict__ v,
-                                  int64_t in_stride, int64_t in_first, int64_t first_pos, int64_t n_rows) {
+                                  int64_t in_stride, int64_t in_first, int64_t first_pos, int64_t n_rows,
+                                  const int64_t* __restrict__ dev_counts) {
+  if (dev_counts) {  // device-counter decode step: one row at position total_tokens
+    first_pos = dev_counts[1];
+    in_first = first_pos;
+  }
   const int d = c.head_dim;
   const int cap = c.group_size + c.residual;
   const int vec_per_row = d / 8;
@@ -375,21 +388,24 @@ __global__ void ring_write_kernel(ott_cache_t c, const uint16_t* __restrict__ k,
 }
 
 cudaError_t launch_flush(const ott_cache_t& c, int64_t q0, int n_groups, int64_t ring_end, const uint16_t* in_k,
-                         const uint16_t* in_v, int64_t in_stride, int64_t in_first, cudaStream_t st) {
+                         const uint16_t* in_v, int64_t in_stride, int64_t in_first, cudaStream_t st,
+                         const int64_t* dev_counts) {
   const size_t smem = flush_smem_bytes(c.head_dim, c.group_size, c.capacity);
   cudaError_t e = cudaFuncSetAttribute(flush_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  flush_kernel<<<c.n_units, kFlushThreads, smem, st>>>(c, q0, n_groups, ring_end, in_k, in_v, in_stride, in_first);
+  flush_kernel<<<c.n_units, kFlushThreads, smem, st>>>(c, q0, n_groups, ring_end, in_k, in_v, in_stride, in_first,
+                                                         dev_counts);
   return cudaGetLastError();
 }
 
 cudaError_t launch_ring_write(const ott_cache_t& c, const uint16_t* k, const uint16_t* v, int64_t in_stride,
-                              int64_t in_first, int64_t first_pos, int64_t n_rows, cudaStream_t st) {
+                              int64_t in_first, int64_t first_pos, int64_t n_rows, cudaStream_t st,
+                              const int64_t* dev_counts) {
   const int64_t total = (int64_t)c.n_units * n_rows * (c.head_dim / 8);
   int blocks = (int)((total + 255) / 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (blocks < 1) blocks = 1;
-  ring_write_kernel<<<blocks, 256, 0, st>>>(c, k, v, in_stride, in_first, first_pos, n_rows);
+  ring_write_kernel<<<blocks, 256, 0, st>>>(c, k, v, in_stride, in_first, first_pos, n_rows, dev_counts);
   return cudaGetLastError();
 }
 

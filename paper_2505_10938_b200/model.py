@@ -99,9 +99,10 @@ class Decoder:
             self.k_cache = torch.zeros((cfg.n_layers, batch, Hkv, max_tokens, d), dtype=torch.float16, device=dev)
             self.v_cache = torch.zeros_like(self.k_cache)
         self.pos = 0
+        self.graph = None
 
     # ------------------------------------------------------------------ blocks
-    def _qkv(self, x, lw, pos0):
+    def _qkv(self, x, lw, pos0, cos=None, sin=None):
         cfg, B = self.cfg, x.shape[0]
         H, Hkv, d = cfg.n_heads, cfg.n_kv_heads, cfg.head_dim
         T = x.shape[1]
@@ -110,7 +111,8 @@ class Decoder:
         q = q.view(B, T, H, d).transpose(1, 2)
         k = k.view(B, T, Hkv, d).transpose(1, 2)
         v = v.view(B, T, Hkv, d).transpose(1, 2)
-        cos, sin = self.cos[pos0:pos0 + T], self.sin[pos0:pos0 + T]
+        if cos is None:
+            cos, sin = self.cos[pos0:pos0 + T], self.sin[pos0:pos0 + T]
         return apply_rope(q, cos, sin), apply_rope(k, cos, sin), v.contiguous()
 
     def _mlp(self, x, lw):
@@ -174,6 +176,67 @@ class Decoder:
         self.pos = p + 1
         self.last_logits = self._logits(x[:, 0])
         return self.last_logits.argmax(-1)
+
+    # ------------------------------------------------------------------ CUDA graph decode
+    def _graph_body(self):
+        """One decode step on static buffers: token ids g_tok, position g_pos (device),
+        OTT decode steps with device token counters; writes g_next, advances g_pos."""
+        cfg, B = self.cfg, self.batch
+        x = self.embed.index_select(0, self.g_tok)[:, None]
+        cos, sin = self.cos.index_select(0, self.g_pos), self.sin.index_select(0, self.g_pos)
+        for l, lw in enumerate(self.layers):
+            q, k, v = self._qkv(x, lw, 0, cos, sin)
+            c = self.caches[l]
+            self.g_q[l].copy_(q[:, :, 0])
+            c.decode_step(k[:, :, 0], v[:, :, 0], self.g_q[l], self.g_o[l], self.g_splits[l])
+            x = x + self.g_o[l].view(B, 1, -1) @ lw["wo"]
+            x = x + self._mlp(x, lw)
+        self.g_logits.copy_(self._logits(x[:, 0]))
+        self.g_next.copy_(self.g_logits.argmax(-1))
+        self.g_pos.add_(1)
+
+    @torch.no_grad()
+    def capture_decode_graph(self) -> None:
+        """Capture one OTT decode step (all layers: GEMMs, RoPE, ring write, flush-if-due,
+        attention, combine) in a CUDA graph; `decode_graph` then replays it per step."""
+        if self.kv != "ott":
+            raise ContractViolation("graph decode needs the OTT cache (device token counters)")
+        cfg, B, dev = self.cfg, self.batch, self.device
+        self.g_tok = torch.zeros(B, dtype=torch.int64, device=dev)
+        self.g_next = torch.zeros(B, dtype=torch.int64, device=dev)
+        self.g_pos = torch.full((1,), self.pos, dtype=torch.int64, device=dev)
+        self.g_q = torch.zeros((cfg.n_layers, B, cfg.n_heads, cfg.head_dim), dtype=torch.float16, device=dev)
+        self.g_o = torch.zeros_like(self.g_q)
+        self.g_logits = torch.zeros((B, cfg.vocab), dtype=torch.float16, device=dev)
+        n_rep = cfg.n_heads // cfg.n_kv_heads
+        # splits sized for the longest context of the run; workspaces allocated before capture
+        self.g_splits = [c.splits(n_rep) for c in self.caches]
+        saved = []
+        for c, s in zip(self.caches, self.g_splits):
+            c.workspace(n_rep, s)
+            c.sync_counters()
+            saved.append((c.total_tokens, c.quantized_tokens))
+        torch.cuda.synchronize(dev)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self._graph_body()
+        for c, (t, q) in zip(self.caches, saved):  # capture ran the host side once, not the kernels
+            c.total_tokens, c.quantized_tokens = t, q
+
+    @torch.no_grad()
+    def decode_graph(self, tokens: torch.Tensor) -> torch.Tensor:
+        """`decode` through the captured graph (captured on first use)."""
+        if self.graph is None:
+            self.capture_decode_graph()
+        if self.pos + 1 > self.max_tokens:
+            raise ContractViolation("decoder is full")
+        for c in self.caches:
+            c.advance_host_counts()  # checks capacity before the replay writes
+        self.g_tok.copy_(tokens)
+        self.graph.replay()
+        self.pos += 1
+        self.last_logits = self.g_logits
+        return self.g_next.clone()
 
     @torch.no_grad()
     def generate(self, prompt: torch.Tensor, steps: int) -> torch.Tensor:

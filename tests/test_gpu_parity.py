@@ -499,3 +499,42 @@ def test_decoder_ott_plumbing_matches_fp16_cache():
         tok = q.decode(tok)
         assert torch.isfinite(q.last_logits).all()
     assert q.caches[0].quantized_tokens == ((T + steps - 128) // 32) * 32
+
+
+def test_device_counter_decode_step_and_graph():
+    """ott_decode_step (token counts in device memory) equals append + attend, across
+    flushes; the decoder's CUDA-graph decode equals its eager decode token for token."""
+    from paper_2505_10938_b200 import OTTCache
+    from paper_2505_10938_b200.model import Decoder, DecoderConfig
+
+    B, H, n_rep, d, T, steps = 2, 2, 4, 128, 300, 70
+    rng = np.random.default_rng(5)
+    pre_k, pre_v = (rng.standard_normal((B, H, T, d)).astype(np.float16) for _ in range(2))
+    cs = []
+    for _ in range(2):
+        c = OTTCache(cfg_of(2, 32, 128, 4, 32, d), B, H, max_tokens=T + steps + 8)
+        c.update(torch.from_numpy(pre_k).cuda(), torch.from_numpy(pre_v).cuda())
+        cs.append(c)
+    host, dev = cs
+    dev.sync_counters()
+    out = torch.empty((B, H * n_rep, d), dtype=torch.float16, device="cuda")
+    for i in range(steps):
+        k, v = (torch.from_numpy(rng.standard_normal((B, H, d)).astype(np.float16)).cuda() for _ in range(2))
+        q = torch.from_numpy(rng.standard_normal((B, H * n_rep, d)).astype(np.float16)).cuda()
+        host.append(k, v)
+        ref = host.attend(q, n_splits=3)
+        dev.decode_step(k, v, q, out, n_splits=3)
+        assert torch.equal(out, ref), i
+        assert dev.counters.tolist() == [host.quantized_tokens, host.total_tokens]
+    assert torch.equal(dev.blocks, host.blocks) and torch.equal(dev.pool_pos, host.pool_pos)
+
+    cfg = DecoderConfig(n_layers=3, hidden=512, n_heads=4, n_kv_heads=4, head_dim=128, mlp=1024, vocab=1000)
+    prompt = torch.randint(0, cfg.vocab, (2, 300), generator=torch.Generator().manual_seed(4)).cuda()
+    eager = Decoder(cfg, 2, 400, kv="ott", seed=9)
+    graph = Decoder(cfg, 2, 400, kv="ott", seed=9)
+    te, tg = eager.prefill(prompt), graph.prefill(prompt)
+    for _ in range(60):
+        te, tg = eager.decode(te), graph.decode_graph(tg)
+        assert torch.equal(te, tg)
+        assert torch.equal(eager.last_logits, graph.last_logits)
+    assert graph.caches[-1].total_tokens == eager.caches[-1].total_tokens == 360
