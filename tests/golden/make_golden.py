@@ -203,12 +203,55 @@ def gen_caches(kv):
     np.savez_compressed(os.path.join(HERE, "cache_freeze.npz"), **run_cache(kv, k, v, q, 2, 32, 0, 4, 5, 64))
 
 
+def gen_trace(kv):
+    """KVTRACE1 fixtures: (1) a tiny file written by the reference's write_trace (bytes +
+    arrays) for the reader/writer round trip; (2) the reference's `simulate` replay
+    (cli.py:189-236 restated: TieredCache.append + attend_mixed vs attend_full_precision,
+    l1_error, memory_usage) on an fp16-valued synthetic trace from its own generator."""
+    import io
+    import tempfile
+
+    from kvtrace.trace import SyntheticSpec, Trace, TraceHeader, generate_synthetic, write_trace
+    from kvtrace.attention import attend_full_precision, l1_error
+
+    rng = np.random.default_rng(77)
+    tiny = Trace(TraceHeader(1, 2, 4, 3), *(fp16(rng.standard_normal((1, 2, 3, 4))) for _ in range(3)))
+    with tempfile.NamedTemporaryFile(suffix=".kvt") as f:
+        write_trace(f.name, tiny)
+        raw = open(f.name, "rb").read()
+
+    L, H, d, T = 2, 2, 128, 256
+    tr = generate_synthetic(SyntheticSpec(seed=5), L, H, d, T)
+    q, k, v = fp16(tr.q), fp16(tr.k), fp16(tr.v)
+    G, R, N, A = 32, 64, 3, 32
+    cfg = kv.EngineConfig(bits=2, group_size=G, residual=R, outlier_num=N, skip_layers=(), aux_capacity=A,
+                          n_layers=L, n_heads=H, head_dim=d)
+    caches = {(l, h): kv.TieredCache(cfg, layer=l) for l in range(L) for h in range(H)}
+    errs = np.zeros(T)
+    for t in range(T):
+        tot = 0.0
+        for (l, h), c in caches.items():
+            c.append(k[l, h, t], v[l, h, t])
+            mixed = kv.attend_mixed(q[l, h, t], c)
+            ref = attend_full_precision(q[l, h, t], k[l, h, : t + 1], v[l, h, : t + 1])
+            tot += l1_error(mixed.output, ref.output)
+        errs[t] = tot / len(caches)
+    mus = [c.memory_usage() for c in caches.values()]
+    usage = np.array([sum(m.quantized_bits for m in mus), sum(m.param_bits for m in mus),
+                      sum(m.pending_bits for m in mus), sum(m.pool_bits for m in mus)], dtype=np.int64)
+    np.savez_compressed(os.path.join(HERE, "trace.npz"), tiny_bytes=np.frombuffer(raw, np.uint8),
+                        tiny_q=tiny.q, tiny_k=tiny.k, tiny_v=tiny.v,
+                        q=q.astype(np.float16), k=k.astype(np.float16), v=v.astype(np.float16),
+                        cfg=np.array([G, R, N, A]), step_errors=errs, usage=usage)
+
+
 def main():
     kv = _kv()
     gen_quant_lines(kv)
     gen_pack(kv)
     gen_pool_streams(kv)
     gen_caches(kv)
+    gen_trace(kv)
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))

@@ -1,1 +1,1 @@
-timeout 300 python tools/prof_c1.py --steps 8 > gpurun_out/c1.log 2>&1 && timeout 900 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/c1_launches.csv python tools/prof_c1.py --steps 1 > gpurun_out/c1_ncu.log 2>&1
+timeout 600 python -m pytest tests -m gpu -x -q -k "trace" > gpurun_out/pytest_gpu.log 2>&1; echo pytest_exit=$? >> gpurun_out/pytest_gpu.log
