@@ -245,6 +245,33 @@ def gen_trace(kv):
                         cfg=np.array([G, R, N, A]), step_errors=errs, usage=usage)
 
 
+def gen_ratio(kv):
+    """report.ratio_curve (report.py:159-216) restated with fp16-valued rows (the
+    reference draws float32 N(0,1) rows; the product consumes fp16): memory bits and
+    ratio vs fp16 at ascending lengths, for the paper setting and the config-1 cache."""
+    from kvtrace.cache import TieredCache
+
+    out = {}
+    for name, cfg in (("paper", kv.EngineConfig(bits=2, group_size=128, residual=32, outlier_num=3, head_dim=64)),
+                      ("c1", kv.EngineConfig(bits=2, group_size=32, residual=128, outlier_num=32, head_dim=128))):
+        layer = 0
+        while layer in cfg.skip_layers:
+            layer += 1
+        cache = TieredCache(cfg, layer=layer)
+        rng = np.random.default_rng(0)
+        d = cfg.head_dim
+        seq = [128, 1024, 4096]
+        rows, tok = [], 0
+        for target in seq:
+            while tok < target:
+                cache.append(fp16(rng.standard_normal(d)), fp16(rng.standard_normal(d)))
+                tok += 1
+            u = cache.memory_usage()
+            rows.append([target, u.quantized_bits, u.param_bits, u.pending_bits, u.pool_bits, u.total_bits])
+        out[name] = np.array(rows, dtype=np.int64)
+    np.savez_compressed(os.path.join(HERE, "ratio.npz"), **out)
+
+
 def main():
     kv = _kv()
     gen_quant_lines(kv)
@@ -252,6 +279,7 @@ def main():
     gen_pool_streams(kv)
     gen_caches(kv)
     gen_trace(kv)
+    gen_ratio(kv)
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))
