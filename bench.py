@@ -364,18 +364,23 @@ def run_c1(args, rank, world, local_rank):
     torch.cuda.set_device(dev)
     B, T, steps = 8, 2048, args.steps if args.steps != 32 else 256
     prompt = torch.randint(0, LLAMA2_7B.vocab, (B, T), generator=torch.Generator().manual_seed(rank)).to(dev)
+    from paper_2505_10938_b200 import EngineConfig
+
     res = {}
     for kv in ("ott", "fp16"):
-        m = Decoder(LLAMA2_7B, B, T + steps + 8, kv=kv, device=dev, seed=0)
+        # fp16 baseline: the same engine and CUDA graph with a residual window longer than
+        # the run, so every K/V row stays in the fp16 tier (a plain fp16 KV cache)
+        lossless = EngineConfig(bits=2, group_size=32, residual=T + steps + 64, outlier_num=0,
+                                n_layers=LLAMA2_7B.n_layers, n_heads=LLAMA2_7B.n_kv_heads, head_dim=LLAMA2_7B.head_dim)
+        m = Decoder(LLAMA2_7B, B, T + steps + 8, kv="ott", ott=None if kv == "ott" else lossless, device=dev, seed=0)
         torch.cuda.synchronize()
         t0 = time.time()
         tok = m.prefill(prompt)
         torch.cuda.synchronize()
         prefill_s = time.time() - t0
-        # OTT decoder: the whole decode step (32 layers) is one captured CUDA graph with the
-        # cache's token counts in device memory; the fp16-KV baseline runs eagerly (SDPA
-        # over a growing cache cannot be captured with static shapes)
-        dec = m.decode_graph if kv == "ott" else m.decode
+        # the whole decode step (32 layers) is one captured CUDA graph with the cache's
+        # token counts in device memory
+        dec = m.decode_graph
         for _ in range(args.warmup):  # warm-up decode steps (graph capture, cuBLAS heuristics)
             tok = dec(tok)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -401,7 +406,8 @@ def run_c1(args, rank, world, local_rank):
             "vs_baseline": None, "dtype": "f16 weights/activations, u2 KV codes", "data": "synthetic (random ids, random-init weights)",
             "config": {"workload": "config1-llama2-7b-B8-prompt2048-decode%d" % steps, "batch": B, "prompt": T,
                        "layers": LLAMA2_7B.n_layers, "parallelism": f"replicas x{world}", "decode": "CUDA graph per step"},
-            "fp16_kv_baseline": {"value": res["fp16"]["tok_s"] * world, "ms_per_step": res["fp16"]["ms_per_step"]},
+            "fp16_kv_baseline": {"value": res["fp16"]["tok_s"] * world, "ms_per_step": res["fp16"]["ms_per_step"],
+                                 "how": "same engine + CUDA graph, residual window > run: all K/V rows fp16"},
             "prefill_s": {"ott": round(res["ott"]["prefill_s"], 3), "fp16": round(res["fp16"]["prefill_s"], 3)},
             "greedy_token_agreement_vs_fp16": agree,
         }), flush=True)

@@ -970,9 +970,14 @@ template <int NR, int G>
 __global__ void __launch_bounds__(kAttnThreads, OTT_MMA_MIN_BLOCKS)
     attend_mma_kernel(const __grid_constant__ AttnArgs a, const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(256) unsigned char smem_raw[];
+#ifndef OTT_ABL_TIER  // timing ablation only (results wrong): 1 skip the fp-tier CTAs, 2 skip quantized CTAs
+#define OTT_ABL_TIER 0
+#endif
   if ((int)blockIdx.y == a.n_qsplits) {  // full-precision tiers: pool.entries + pending window
+    if (OTT_ABL_TIER & 1) return;
     fp_body<NR>(a, counts_of(a), *reinterpret_cast<FpSmem*>(smem_raw));
   } else {
+    if (OTT_ABL_TIER & 2) return;
     mma_body<NR, G>(a, counts_of(a), &tmap, *reinterpret_cast<MmaSmem<G>*>(smem_raw));
   }
 }

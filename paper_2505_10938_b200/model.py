@@ -25,7 +25,8 @@ from dataclasses import dataclass
 import torch
 import torch.nn.functional as F
 
-from .cache import OTTCache
+from . import _native
+from .cache import OTTCache, _stream_handle
 from .config import EngineConfig
 from .errors import ContractViolation
 
@@ -149,50 +150,80 @@ class Decoder:
         self.last_logits = self._logits(x[:, -1])
         return self.last_logits.argmax(-1)
 
-    @torch.no_grad()
-    def decode(self, tokens: torch.Tensor) -> torch.Tensor:
-        """One greedy step: tokens int64 [B] at position self.pos -> next tokens [B]."""
-        cfg, B = self.cfg, self.batch
-        if self.pos + 1 > self.max_tokens:
-            raise ContractViolation("decoder is full")
-        x = self.embed[tokens][:, None]  # [B, 1, D]
-        p = self.pos
+    # ------------------------------------------------------------------ decode step
+    def _decode_buffers(self):
+        if getattr(self, "_dbuf", None) is None:
+            cfg, B, dev = self.cfg, self.batch, self.device
+            H, Hkv, d = cfg.n_heads, cfg.n_kv_heads, cfg.head_dim
+            kw = dict(dtype=torch.float16, device=dev)
+            self._dbuf = {
+                "h": torch.empty((B, cfg.hidden), **kw), "qkv": torch.empty((B, (H + 2 * Hkv) * d), **kw),
+                "q": torch.empty((B, H, d), **kw), "k": torch.empty((B, Hkv, d), **kw),
+                "v": torch.empty((B, Hkv, d), **kw), "o": torch.empty((B, H, d), **kw),
+                "gu": torch.empty((B, 2 * cfg.mlp), **kw), "act": torch.empty((B, cfg.mlp), **kw),
+                "logits": torch.empty((B, cfg.vocab), **kw),
+            }
+        return self._dbuf
+
+    def _layers_step(self, x, pos_host: int, pos_dev=None, graph: bool = False):
+        """One decode step over all layers on the residual stream x [B, D] (updated in
+        place): fused RMSNorm / RoPE+split / SiLU-gate kernels (ott_model.h), cuBLAS
+        GEMMs with the residual adds in their epilogues (addmm_), and the OTT cache
+        (device-counter `decode_step` when graph=True, host-count append+attend otherwise)."""
+        cfg, B, lib, st = self.cfg, self.batch, _native.lib(), _stream_handle()
+        H, Hkv, d, D = cfg.n_heads, cfg.n_kv_heads, cfg.head_dim, cfg.hidden
+        bf = self._decode_buffers()
+        h, qkv, q, k, v, o, gu, act = (bf[n] for n in ("h", "qkv", "q", "k", "v", "o", "gu", "act"))
+        pos_ptr = pos_dev.data_ptr() if pos_dev is not None else None
         for l, lw in enumerate(self.layers):
-            q, k, v = self._qkv(x, lw, p)  # [B, h, 1, d]
+            _native.check(lib.ott_model_rmsnorm(x.data_ptr(), lw["n1"].data_ptr(), h.data_ptr(), B, D, cfg.eps, st))
+            torch.mm(h, lw["wqkv"], out=qkv)
+            _native.check(lib.ott_model_rope_qkv(qkv.data_ptr(), self.cos.data_ptr(), self.sin.data_ptr(), pos_ptr,
+                                                 pos_host, q.data_ptr(), k.data_ptr(), v.data_ptr(), B, H, Hkv, d, st))
             if self.kv == "ott":
                 c = self.caches[l]
-                c.append(k[:, :, 0].contiguous(), v[:, :, 0].contiguous())
-                o = c.attend(q[:, :, 0].contiguous())  # [B, H, d]
+                if graph:
+                    c.decode_step(k, v, q, o, self.g_splits[l])
+                else:
+                    c.append(k, v)
+                    c.attend(q, out=o)
             else:
-                self.k_cache[l, :, :, p] = k[:, :, 0]
-                self.v_cache[l, :, :, p] = v[:, :, 0]
-                rep = cfg.n_heads // cfg.n_kv_heads
+                p = pos_host
+                self.k_cache[l, :, :, p] = k
+                self.v_cache[l, :, :, p] = v
+                rep = H // Hkv
                 kk, vv = self.k_cache[l, :, :, : p + 1], self.v_cache[l, :, :, : p + 1]
                 if rep > 1:
                     kk, vv = kk.repeat_interleave(rep, dim=1), vv.repeat_interleave(rep, dim=1)
-                o = F.scaled_dot_product_attention(q, kk, vv)[:, :, 0]
-            x = x + o.reshape(B, 1, -1) @ lw["wo"]
-            x = x + self._mlp(x, lw)
-        self.pos = p + 1
-        self.last_logits = self._logits(x[:, 0])
-        return self.last_logits.argmax(-1)
+                o.copy_(F.scaled_dot_product_attention(q[:, :, None], kk, vv)[:, :, 0])
+            x.addmm_(o.view(B, H * d), lw["wo"])
+            _native.check(lib.ott_model_rmsnorm(x.data_ptr(), lw["n2"].data_ptr(), h.data_ptr(), B, D, cfg.eps, st))
+            torch.mm(h, lw["wgu"], out=gu)
+            _native.check(lib.ott_model_silu_mul(gu.data_ptr(), act.data_ptr(), B, cfg.mlp, st))
+            x.addmm_(act, lw["wd"])
+        _native.check(lib.ott_model_rmsnorm(x.data_ptr(), self.norm.data_ptr(), h.data_ptr(), B, D, cfg.eps, st))
+        torch.mm(h, self.lm_head, out=bf["logits"])
+        return bf["logits"]
+
+    @torch.no_grad()
+    def decode(self, tokens: torch.Tensor) -> torch.Tensor:
+        """One greedy step: tokens int64 [B] at position self.pos -> next tokens [B]."""
+        if self.pos + 1 > self.max_tokens:
+            raise ContractViolation("decoder is full")
+        x = self.embed.index_select(0, tokens)
+        logits = self._layers_step(x, self.pos)
+        self.pos += 1
+        self.last_logits = logits.clone()
+        return logits.argmax(-1)
 
     # ------------------------------------------------------------------ CUDA graph decode
     def _graph_body(self):
         """One decode step on static buffers: token ids g_tok, position g_pos (device),
         OTT decode steps with device token counters; writes g_next, advances g_pos."""
-        cfg, B = self.cfg, self.batch
-        x = self.embed.index_select(0, self.g_tok)[:, None]
-        cos, sin = self.cos.index_select(0, self.g_pos), self.sin.index_select(0, self.g_pos)
-        for l, lw in enumerate(self.layers):
-            q, k, v = self._qkv(x, lw, 0, cos, sin)
-            c = self.caches[l]
-            self.g_q[l].copy_(q[:, :, 0])
-            c.decode_step(k[:, :, 0], v[:, :, 0], self.g_q[l], self.g_o[l], self.g_splits[l])
-            x = x + self.g_o[l].view(B, 1, -1) @ lw["wo"]
-            x = x + self._mlp(x, lw)
-        self.g_logits.copy_(self._logits(x[:, 0]))
-        self.g_next.copy_(self.g_logits.argmax(-1))
+        self.g_x.copy_(self.embed.index_select(0, self.g_tok))
+        logits = self._layers_step(self.g_x, 0, pos_dev=self.g_pos, graph=True)
+        self.g_logits.copy_(logits)
+        self.g_next.copy_(logits.argmax(-1))
         self.g_pos.add_(1)
 
     @torch.no_grad()
@@ -205,8 +236,8 @@ class Decoder:
         self.g_tok = torch.zeros(B, dtype=torch.int64, device=dev)
         self.g_next = torch.zeros(B, dtype=torch.int64, device=dev)
         self.g_pos = torch.full((1,), self.pos, dtype=torch.int64, device=dev)
-        self.g_q = torch.zeros((cfg.n_layers, B, cfg.n_heads, cfg.head_dim), dtype=torch.float16, device=dev)
-        self.g_o = torch.zeros_like(self.g_q)
+        self.g_x = torch.zeros((B, cfg.hidden), dtype=torch.float16, device=dev)
+        self._decode_buffers()
         self.g_logits = torch.zeros((B, cfg.vocab), dtype=torch.float16, device=dev)
         n_rep = cfg.n_heads // cfg.n_kv_heads
         # splits sized for the longest context of the run; workspaces allocated before capture

@@ -12,7 +12,7 @@ from conftest import ROOT
 
 
 def header_symbols():
-    src = open(os.path.join(ROOT, "include", "ott_b200.h")).read()
+    src = "".join(open(os.path.join(ROOT, "include", f)).read() for f in ("ott_b200.h", "ott_model.h"))
     return sorted(set(re.findall(r"\b(ott_[a-z0-9_]+)\s*\(", src)))
 
 
