@@ -549,16 +549,17 @@ __device__ void mma_body(const AttnArgs& a, const Counts& n, const CUtensorMap* 
     float bias_g[NG];
 #pragma unroll
     for (int j = 0; j < NG; ++j) {
-      float2 acc2 = make_float2(0.f, 0.f);
+      float2 acc2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                        make_float2(0.f, 0.f)};  // 4 independent chains
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const int wd = k < 4 ? tig : 4 + tig;
         const float4 ev = *reinterpret_cast<const float4*>(rec[j] + swz(L.k_e() + 64 * wd + 16 * (k & 3)));
         const float4 qv = sm.qt[k][lane];
-        acc2 = __ffma2_rn(make_float2(qv.x, qv.y), make_float2(ev.x, ev.y), acc2);
-        acc2 = __ffma2_rn(make_float2(qv.z, qv.w), make_float2(ev.z, ev.w), acc2);
+        acc2[(2 * k) & 3] = __ffma2_rn(make_float2(qv.x, qv.y), make_float2(ev.x, ev.y), acc2[(2 * k) & 3]);
+        acc2[(2 * k + 1) & 3] = __ffma2_rn(make_float2(qv.z, qv.w), make_float2(ev.z, ev.w), acc2[(2 * k + 1) & 3]);
       }
-      bias_g[j] = acc2.x + acc2.y;
+      bias_g[j] = ((acc2[0].x + acc2[0].y) + (acc2[1].x + acc2[1].y)) + ((acc2[2].x + acc2[2].y) + (acc2[3].x + acc2[3].y));
 #pragma unroll
       for (int mt = 0; mt < kMt; ++mt) ch[j][mt][0] = ch[j][mt][1] = ch[j][mt][2] = ch[j][mt][3] = 0.f;
     }
