@@ -240,6 +240,65 @@ __global__ void timing3(long long* cycles, uint32_t id, int reps, int mode) {
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(128));
 }
 
+// issue-cost test: descriptors precomputed outside the loop (uniform), 8 MMAs per iteration
+template <int MODE>
+__global__ void timing4(long long* cycles, uint32_t id, int reps) {
+  __shared__ alignas(128) uint8_t bs[16 * K * 2];
+  __shared__ alignas(8) uint64_t bar;
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < 16 * K * 2 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(bs)[i] = 0x3C003C00u;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tbase)), "n"(128));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(&bar)), "r"(1));
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  const uint32_t tmem = tbase;
+  long long t0 = clock64();
+  if (tid == 0) {
+    const uint32_t b0 = smem_u32(bs);
+    const uint64_t d0 = sdesc(b0);
+    for (int rep = 0; rep < reps; ++rep) {
+      if (MODE == 0) {
+        asm volatile(
+            "{\n .reg .pred p, q;\n .reg .b64 d1, d2, d3, d4, d5, d6, d7;\n setp.ne.b32 p, %3, 0;\n setp.ne.b32 q, 1, 0;\n"
+            "add.s64 d1, %2, 16;\n add.s64 d2, %2, 32;\n add.s64 d3, %2, 48;\n add.s64 d4, %2, 64;\n"
+            "add.s64 d5, %2, 80;\n add.s64 d6, %2, 96;\n add.s64 d7, %2, 112;\n"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %4, p;\n"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], [%5], d1, %4, q;\n"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], [%6], d2, %4, q;\n"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], [%7], d3, %4, q;\n"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], [%8], d4, %4, q;\n"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], [%9], d5, %4, q;\n"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], [%10], d6, %4, q;\n"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], [%11], d7, %4, q;\n}\n" ::"r"(tmem + 64),
+            "r"(tmem), "l"(d0), "r"(rep), "r"(id), "r"(tmem + 8), "r"(tmem + 16), "r"(tmem + 24), "r"(tmem + 32),
+            "r"(tmem + 40), "r"(tmem + 48), "r"(tmem + 56));
+      }
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(&bar)));
+  }
+  __syncwarp();
+  {
+    uint32_t done = 0;
+    while (!done)
+      asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                   : "=r"(done) : "r"(smem_u32(&bar)), "r"(0) : "memory");
+  }
+  long long t1 = clock64();
+  if (tid == 0) cycles[blockIdx.x] = t1 - t0;
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(128));
+}
+
 static uint16_t h(float x) { __half v = __float2half_rn(x); uint16_t u; memcpy(&u, &v, 2); return u; }
 static double hf(uint16_t u) { __half v; memcpy(&v, &u, 2); return (double)__half2float(v); }
 
@@ -308,6 +367,20 @@ int main() {
         CK(cudaMemcpy(hc, dcy, 8 * grid, cudaMemcpyDeviceToHost));
         double avg = 0; for (int i = 0; i < grid; ++i) avg += hc[i]; avg /= grid;
         printf("timing3 %d CTA/SM M128 N%d: %.2f cycles per MMA per CTA\n", per, n, avg / (512 * 8));
+      }
+  }
+  {
+    long long* dcy; CK(cudaMalloc(&dcy, 8 * 148 * 8));
+    long long hc[148 * 8];
+    for (int per : {1, 4})
+      for (int n : {16, 64}) {
+        const int grid = 148 * per;
+        timing4<0><<<grid, 128>>>(dcy, idesc(128, n), 512);
+        CK(cudaGetLastError());
+        CK(cudaDeviceSynchronize());
+        CK(cudaMemcpy(hc, dcy, 8 * grid, cudaMemcpyDeviceToHost));
+        double avg = 0; for (int i = 0; i < grid; ++i) avg += hc[i]; avg /= grid;
+        printf("timing4 (8 MMAs per asm block) %d CTA/SM M128 N%d: %.2f cycles per MMA per CTA\n", per, n, avg / (512 * 8));
       }
   }
   printf(bad_total ? "PROBE FAILED\n" : "PROBE OK\n");
