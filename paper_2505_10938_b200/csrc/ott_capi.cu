@@ -105,12 +105,14 @@ int ott_pick_splits(const ott_cache_t* c, int32_t n_rep, int64_t total_tokens) {
   const int64_t n_groups = q_tokens / c->group_size;
   int sms = ott_num_sms();
   if (sms <= 0) sms = 148;
-  // ~8 quantized-range CTAs per SM over the launch: longer CTAs amortise their
-  // start-up (first TMA round trip, q staging, merge) — measured best on config 3/4 —
-  // while each split still streams >= 8 groups (2 per warp).
-  const int64_t target = (int64_t)sms * 8;
-  int64_t s = (target + c->n_units - 1) / c->n_units;
-  const int64_t max_by_groups = n_groups / 8 > 0 ? n_groups / 8 : 1;
+  // ~3 quantized-range CTAs per SM over the launch (round to nearest): long CTAs
+  // amortise their start-up (first TMA round trip, q staging, merge) and the fp-tier
+  // CTAs fill the tail. Measured (v7 sweep over config-3/4 shapes): best or within 3 %
+  // of the best split count on B=16/64/128 x T=4K-16K; the previous 8/SM rule was up to
+  // 29 % slower on small batches. Each split still streams >= 16 groups (4 per warp).
+  const int64_t target = (int64_t)sms * 3;
+  int64_t s = (target + c->n_units / 2) / c->n_units;
+  const int64_t max_by_groups = n_groups / 16 > 0 ? n_groups / 16 : 1;
   if (s > max_by_groups) s = max_by_groups;
   if (s > 64) s = 64;
   if (s < 1) s = 1;
