@@ -62,7 +62,7 @@ typedef struct {
   int32_t residual;     /* R >= 0 */
   int32_t capacity;     /* N: pool capacity for this layer (EngineConfig.outlier_capacity) */
   int32_t aux_capacity; /* A */
-  int32_t bits;         /* 2 */
+  int32_t bits;         /* 1..8 (2: tensor-core attention; others: CUDA-core kernel) */
   int32_t max_groups;   /* block records allocated per unit */
   uint8_t* blocks;      /* [n_units][max_groups][record_bytes] */
   uint16_t* pend_k;     /* fp16 [n_units][G+R][d], slot = position % (G+R) */

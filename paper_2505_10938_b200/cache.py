@@ -56,7 +56,8 @@ class OTTCache:
     from the shared token count with no device synchronisation.
 
     Args:
-        config: EngineConfig (same fields as the reference). bits must be 2;
+        config: EngineConfig (same fields as the reference). bits in [1, 8]
+            (2-bit uses the tensor-core kernels, other widths the CUDA-core kernel);
             head_dim 64 or 128; group_size a multiple of 32 up to 128.
         batch, n_kv_heads: unit grid.
         max_tokens: capacity of the quantized store per unit.
@@ -71,7 +72,7 @@ class OTTCache:
                  device=None, keep_f64_params: bool = False, validate: bool = False):
         if not torch.cuda.is_available():
             raise _native.NativeError("OTTCache needs a CUDA device (B200); there is no CPU path")
-        require(config.bits == 2, "the B200 path implements bits=2 only")
+        require(1 <= config.bits <= 8, "bits must be in [1, 8]")
         require(config.head_dim in (64, 128), "head_dim must be 64 or 128")
         require(config.group_size % 32 == 0 and 32 <= config.group_size <= 128,
                 "group_size must be a multiple of 32 in [32, 128]")
@@ -90,7 +91,7 @@ class OTTCache:
         self.max_groups = (max_tokens + G - 1) // G
         self.max_tokens = max_tokens
         L = _native.lib()
-        self.record_bytes = int(L.ott_record_bytes(d, G, 2))
+        self.record_bytes = int(L.ott_record_bytes(d, G, config.bits))
         U, dev = self.n_units, self.device
         kw = dict(device=dev)
         self.blocks = torch.zeros((U, self.max_groups, self.record_bytes), dtype=torch.uint8, **kw)
@@ -114,7 +115,7 @@ class OTTCache:
         self.params64 = (torch.zeros((U, self.max_groups, 2 * (d + G)), dtype=torch.float64, **kw)
                          if keep_f64_params else None)
         self._c = _native.OttCacheT(
-            n_units=U, head_dim=d, group_size=G, residual=R, capacity=self.N, aux_capacity=self.A, bits=2,
+            n_units=U, head_dim=d, group_size=G, residual=R, capacity=self.N, aux_capacity=self.A, bits=config.bits,
             max_groups=self.max_groups, blocks=_ptr(self.blocks), pend_k=_ptr(self.pend_k), pend_v=_ptr(self.pend_v),
             pool_mask=_ptr(self.pool_mask), subst_mask=_ptr(self.subst_mask), pool_pos=_ptr(self.pool_pos),
             pool_score=_ptr(self.pool_score), pool_k=_ptr(self.pool_k), pool_v=_ptr(self.pool_v),
@@ -312,7 +313,7 @@ class UnitView:
         self.quantized_tokens = cache.quantized_tokens
         nb = cache.quantized_tokens // G
         rec = cache.blocks[u, :nb].cpu().numpy()
-        code_b = G * d // 4
+        code_b = G * d * cfg.bits // 8
         # K params are stored in the decode kernels' encoding (ott_b200.h): fp16 halves
         # sh + sl of the step in pair order and e = x_min - 4 u step; the float32 views
         # below are reconstructions, the exact values come from params64
@@ -332,12 +333,13 @@ class UnitView:
             kmn64, kst64, vmn64, vst64 = kmn, kst, vmn, vst
         self.quantized_k, self.quantized_v = [], []
         for i in range(nb):
+            b = cfg.bits
             self.quantized_k.append(QuantizedBlock(rec[i, :code_b].tobytes(), GroupAxis.PER_CHANNEL,
-                                                   [QuantParams(float(kmn64[i, c]), float(kst64[i, c]), 2)
-                                                    for c in range(d)], G, d, 2))
+                                                   [QuantParams(float(kmn64[i, c]), float(kst64[i, c]), b)
+                                                    for c in range(d)], G, d, b))
             self.quantized_v.append(QuantizedBlock(rec[i, code_b:2 * code_b].tobytes(), GroupAxis.PER_TOKEN,
-                                                   [QuantParams(float(vmn64[i, t]), float(vst64[i, t]), 2)
-                                                    for t in range(G)], G, d, 2))
+                                                   [QuantParams(float(vmn64[i, t]), float(vst64[i, t]), b)
+                                                    for t in range(G)], G, d, b))
         cap = G + cfg.residual
         pos = np.arange(cache.quantized_tokens, cache.total_tokens)
         pk = cache.pend_k[u].float().cpu().numpy()

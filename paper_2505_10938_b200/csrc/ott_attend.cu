@@ -88,7 +88,7 @@ template <int NR, int D>
 struct WarpScratch {
   float qp[NR][D];
   float p[NR][32];
-  uint32_t vw[32][D / 16];
+  uint32_t vw[32][D / 4];  // V codes of 32 tokens, packed (any width up to 8 bits)
   float vstep[32], vxmin[32];
 };
 
@@ -130,7 +130,8 @@ __device__ void simt_body(const AttnArgs& a, const Counts& n, int u, int t_begin
   const ott_cache_t& c = a.c;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int G = c.group_size, N = c.capacity, cap = G + c.residual;
-  const RecordLayout L(D, G);
+  const int bits = c.bits;
+  const RecordLayout L(D, G, bits);
   WarpScratch<NR, D>& ws = sm.w[warp];
 
   for (int i = tid; i < NR * D; i += kAttnThreads)
@@ -167,26 +168,33 @@ __device__ void simt_body(const AttnArgs& a, const Counts& n, int u, int t_begin
       }
 #pragma unroll
       for (int r = 0; r < NR; ++r) bias[r] = warp_sum(bias[r]);
-      const uint32_t* vcw = reinterpret_cast<const uint32_t*>(rec + L.v_codes()) + (size_t)row0 * (D / 16);
-#pragma unroll
-      for (int j = 0; j < D / 16; ++j) {
-        const int idx = j * 32 + lane;
-        ws.vw[idx / (D / 16)][idx % (D / 16)] = vcw[idx];
-      }
+      // V code rows of the tile (32 * D * bits / 32 words, contiguous in pack order)
+      const uint32_t* vcw = reinterpret_cast<const uint32_t*>(rec + L.v_codes()) + (size_t)row0 * D * bits / 32;
+      for (int idx = lane; idx < D * bits; idx += 32) (&ws.vw[0][0])[idx] = vcw[idx];
       ws.vstep[lane] = reinterpret_cast<const float*>(rec + L.v_step())[row0 + lane];
       ws.vxmin[lane] = reinterpret_cast<const float*>(rec + L.v_xmin())[row0 + lane];
       __syncwarp();
-      const uint32_t* kcw = reinterpret_cast<const uint32_t*>(rec + L.k_codes()) + (size_t)(row0 + lane) * (D / 16);
 #pragma unroll
       for (int r = 0; r < NR; ++r) s[r] = bias[r];
+      if (bits == 2) {
+        const uint32_t* kcw = reinterpret_cast<const uint32_t*>(rec + L.k_codes()) + (size_t)(row0 + lane) * (D / 16);
 #pragma unroll
-      for (int j = 0; j < D / 16; ++j) {
-        const uint32_t w = kcw[j];
+        for (int j = 0; j < D / 16; ++j) {
+          const uint32_t w = kcw[j];
 #pragma unroll
-        for (int b = 0; b < 16; ++b) {
-          const float code = (float)((w >> (2 * b)) & 3u);
+          for (int b = 0; b < 16; ++b) {
+            const float code = (float)((w >> (2 * b)) & 3u);
 #pragma unroll
-          for (int r = 0; r < NR; ++r) s[r] = fmaf(code, ws.qp[r][j * 16 + b], s[r]);
+            for (int r = 0; r < NR; ++r) s[r] = fmaf(code, ws.qp[r][j * 16 + b], s[r]);
+          }
+        }
+      } else {  // other widths (quant.py supports 1..8): generic stream extraction
+        const uint8_t* kc = rec + L.k_codes();
+        const int64_t e0 = (int64_t)(row0 + lane) * D;
+        for (int col = 0; col < D; ++col) {
+          const float code = (float)code_at(kc, e0 + col, bits);
+#pragma unroll
+          for (int r = 0; r < NR; ++r) s[r] = fmaf(code, ws.qp[r][col], s[r]);
         }
       }
       const bool pooled = (pmask[tok0 >> 5] >> lane) & 1u;
@@ -195,13 +203,16 @@ __device__ void simt_body(const AttnArgs& a, const Counts& n, int u, int t_begin
         for (int r = 0; r < NR; ++r) s[r] = -INFINITY;
       }
       online_update<NR, D>(s, m, l, acc, ws, lane);
+      const uint8_t* vcodes = reinterpret_cast<const uint8_t*>(&ws.vw[0][0]);
 #pragma unroll 4
       for (int tt = 0; tt < 32; ++tt) {
         const float st = ws.vstep[tt], mn = ws.vxmin[tt];
 #pragma unroll
         for (int k = 0; k < D / 32; ++k) {
           const int col = lane + 32 * k;
-          const float v = fmaf((float)((ws.vw[tt][col >> 4] >> (2 * (col & 15))) & 3u), st, mn);
+          const uint32_t code = bits == 2 ? (uint32_t)((vcodes[(tt * D + col) >> 2] >> (2 * (col & 3))) & 3u)
+                                          : code_at(vcodes, (int64_t)tt * D + col, bits);
+          const float v = fmaf((float)code, st, mn);
 #pragma unroll
           for (int r = 0; r < NR; ++r) acc[r][k] = fmaf(ws.p[r][tt], v, acc[r][k]);
         }
@@ -1468,7 +1479,7 @@ __global__ void logits_kernel(ott_cache_t c, const uint16_t* __restrict__ q, flo
   const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= total) return;
   const int G = c.group_size, N = c.capacity, cap = G + c.residual;
-  const RecordLayout L(D, G);
+  const RecordLayout L(D, G, c.bits);
   float k[D];
   bool done = false;
   if (p < q_tokens) {
@@ -1484,10 +1495,9 @@ __global__ void logits_kernel(ott_cache_t c, const uint16_t* __restrict__ q, flo
       const int64_t gi = p / G;
       const int row = (int)(p - gi * G);
       const uint8_t* rec = record_ptr(c, u, gi);
-      const uint32_t* kcw = reinterpret_cast<const uint32_t*>(rec + L.k_codes()) + (size_t)row * (D / 16);
       for (int j = 0; j < D; ++j) {
         const float st = k_step_of(rec, L, j);
-        k[j] = fmaf((float)((kcw[j / 16] >> (2 * (j % 16))) & 3u), st, k_xmin_of(rec, L, j, st));
+        k[j] = fmaf((float)code_at(rec + L.k_codes(), (int64_t)row * D + j, c.bits), st, k_xmin_of(rec, L, j, st));
       }
     }
   } else {
@@ -1582,7 +1592,7 @@ static bool use_tc5() {
   return v == 1;
 }
 
-bool mma_eligible(const ott_cache_t& c) { return c.head_dim == 128; }
+bool mma_eligible(const ott_cache_t& c) { return c.head_dim == 128 && c.bits == 2; }
 
 cudaError_t launch_attend(const ott_cache_t& c, const uint16_t* q, uint16_t* out, int n_rep, int64_t q_tokens,
                           int64_t total, float* ws, int n_qsplits, cudaStream_t st, int64_t* dev_counts) {
@@ -1602,6 +1612,14 @@ cudaError_t launch_attend(const ott_cache_t& c, const uint16_t* q, uint16_t* out
   a.scale_log2 = kLog2e / sqrtf((float)c.head_dim);
   a.k_magic = 0x3C003C00u;
   const int D = c.head_dim, G = c.group_size;
+  if (c.bits != 2) {  // other widths: CUDA-core kernel with generic code extraction
+#define OTT_BCASE(NRv, Dv) \
+  if (n_rep == NRv && D == Dv) return launch_simt_t<NRv, Dv>(a, st);
+    OTT_BCASE(1, 64) OTT_BCASE(2, 64) OTT_BCASE(4, 64) OTT_BCASE(8, 64)
+    OTT_BCASE(1, 128) OTT_BCASE(2, 128) OTT_BCASE(4, 128) OTT_BCASE(8, 128)
+#undef OTT_BCASE
+    return cudaErrorInvalidValue;
+  }
   if (mma_eligible(c) && G == 32 && use_tc5()) {
     if (n_rep == 1) return launch_tc5_t<1>(a, st);
     if (n_rep == 2) return launch_tc5_t<2>(a, st);

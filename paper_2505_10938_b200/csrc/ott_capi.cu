@@ -33,7 +33,7 @@ static int cuda_status(cudaError_t e) {
 
 static int check_cache(const ott_cache_t* c) {
   if (!c) return fail(OTT_ERR_CONTRACT, "null cache");
-  if (c->bits != 2) return fail(OTT_ERR_UNSUPPORTED, "only 2-bit codes are implemented on the GPU path");
+  if (c->bits < 1 || c->bits > 8) return fail(OTT_ERR_CONTRACT, "bits must be in [1, 8]");
   if (c->head_dim != 64 && c->head_dim != 128) return fail(OTT_ERR_UNSUPPORTED, "head_dim must be 64 or 128");
   if (c->group_size < 32 || c->group_size > ott::kMaxG || c->group_size % 32)
     return fail(OTT_ERR_UNSUPPORTED, "group_size must be a multiple of 32 in [32, 128]");
@@ -50,8 +50,8 @@ static int check_cache(const ott_cache_t* c) {
 extern "C" {
 
 size_t ott_record_bytes(int32_t head_dim, int32_t group_size, int32_t bits) {
-  if (bits != 2) return 0;
-  return (size_t)ott::RecordLayout(head_dim, group_size).bytes();
+  if (bits < 1 || bits > 8) return 0;
+  return (size_t)ott::RecordLayout(head_dim, group_size, bits).bytes();
 }
 
 int ott_ring_write(const ott_cache_t* c, const uint16_t* k, const uint16_t* v, int64_t in_unit_stride,

@@ -16,9 +16,9 @@ constexpr int kMaxA = 1024;
 
 // Block record layout (see ott_b200.h). All offsets in bytes.
 struct RecordLayout {
-  int d, G;
-  __host__ __device__ RecordLayout(int d_, int G_) : d(d_), G(G_) {}
-  __host__ __device__ int code_bytes() const { return G * d / 4; }  // 2-bit codes
+  int d, G, bits;
+  __host__ __device__ RecordLayout(int d_, int G_, int bits_ = 2) : d(d_), G(G_), bits(bits_) {}
+  __host__ __device__ int code_bytes() const { return G * d * bits / 8; }  // packed codes (G*d % 8 == 0)
   __host__ __device__ int k_codes() const { return 0; }
   __host__ __device__ int v_codes() const { return code_bytes(); }
   __host__ __device__ int k_sh() const { return 2 * code_bytes(); }  // fp16 [d], pair order
@@ -46,11 +46,19 @@ __host__ __device__ inline size_t mask_words_per_unit(const ott_cache_t& c) {
 }
 
 __host__ __device__ inline uint8_t* record_ptr(const ott_cache_t& c, int unit, int64_t group) {
-  const RecordLayout L(c.head_dim, c.group_size);
+  const RecordLayout L(c.head_dim, c.group_size, c.bits);
   return c.blocks + ((size_t)unit * c.max_groups + (size_t)group) * L.bytes();
 }
 
 __device__ __forceinline__ float h2f(uint16_t h) { return __half2float(__ushort_as_half(h)); }
+// code of element e of a pack_codes stream (quant.py:241-256: element e at bits
+// [e*bits, e*bits + bits), LSB first); a code spans at most two bytes for bits <= 8
+__device__ __forceinline__ uint32_t code_at(const uint8_t* codes, int64_t e, int bits) {
+  const int64_t b0 = e * bits;
+  const uint32_t lo = codes[b0 >> 3];
+  const uint32_t hi = ((b0 & 7) + bits > 8) ? codes[(b0 >> 3) + 1] : 0u;
+  return ((lo | (hi << 8)) >> (b0 & 7)) & ((1u << bits) - 1u);
+}
 // float32 K step / x_min of channel c reconstructed from the record encoding
 __device__ __forceinline__ float k_step_of(const uint8_t* rec, const RecordLayout& L, int c) {
   const int j = kpair_index(c);

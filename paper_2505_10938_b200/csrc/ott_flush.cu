@@ -13,9 +13,8 @@ namespace ott {
 constexpr int kFlushThreads = 256;
 
 // quant.py:59-102 for one line held in registers/smem by ONE thread.
-// Returns step; writes codes (0..3) and x_min.
-__device__ __forceinline__ void line_params(double mn, double mx, double& step_out) {
-  const double levels = 3.0;
+// levels = 2^bits - 1. Returns step.
+__device__ __forceinline__ void line_params(double mn, double mx, double levels, double& step_out) {
   double step = __ddiv_rn(__dsub_rn(mx, mn), levels);  // quant.py:64
   // quant.py:68-69: while step > 0 and x_min + levels*step > x_max: nextafter(step, 0)
   while (step > 0.0 && __dadd_rn(mn, __dmul_rn(levels, step)) > mx)
@@ -23,13 +22,13 @@ __device__ __forceinline__ void line_params(double mn, double mx, double& step_o
   step_out = step;
 }
 
-__device__ __forceinline__ int quant_code(double x, double mn, double mx, double step) {
+__device__ __forceinline__ int quant_code(double x, double mn, double mx, double step, int levels) {
   if (step == 0.0) return 0;  // quant.py:91-92
   double f = floor(__ddiv_rn(__dsub_rn(x, mn), step));  // quant.py:93
-  int c = f < 0.0 ? 0 : (f > 3.0 ? 3 : (int)f);           // quant.py:94
+  int c = f < 0.0 ? 0 : (f > (double)levels ? levels : (int)f);  // quant.py:94
   if (__dadd_rn(__dmul_rn((double)c, step), mn) > x) c -= 1;  // quant.py:97
   c = c < 0 ? 0 : c;                                          // quant.py:98
-  if (x == mx) c = 3;                                         // quant.py:101
+  if (x == mx) c = levels;                                    // quant.py:101
   return c;
 }
 
@@ -71,7 +70,8 @@ __global__ void __launch_bounds__(kFlushThreads) flush_kernel(ott_cache_t c, int
   const int nwarps = kFlushThreads / 32;
   const int d = c.head_dim, G = c.group_size, N = c.capacity, A = c.aux_capacity;
   const int cap = G + c.residual;
-  const RecordLayout L(d, G);
+  const RecordLayout L(d, G, c.bits);
+  const int levels = (1 << c.bits) - 1;
 
   extern __shared__ __align__(16) unsigned char smem[];
   float* sk = reinterpret_cast<float*>(smem);
@@ -299,8 +299,9 @@ __global__ void __launch_bounds__(kFlushThreads) flush_kernel(ott_cache_t c, int
         mx = fmax(mx, x);
       }
       double step;
-      line_params(mn, mx, step);
-      for (int i = 0; i < G; ++i) kc[i * d + col] = (uint8_t)quant_code((double)sk[i * d + col], mn, mx, step);
+      line_params(mn, mx, (double)levels, step);
+      for (int i = 0; i < G; ++i)
+        kc[i * d + col] = (uint8_t)quant_code((double)sk[i * d + col], mn, mx, step, levels);
       // decode-side encoding (ott_common.cuh): step = sh + sl, e = x_min - 4 u step
       const __half sh = __double2half(step);
       const __half sl = __double2half(__dsub_rn(step, (double)__half2float(sh)));
@@ -323,9 +324,9 @@ __global__ void __launch_bounds__(kFlushThreads) flush_kernel(ott_cache_t c, int
         mn = warp_min_d(mn);
         mx = warp_max_d(mx);
         double step;
-        line_params(mn, mx, step);
+        line_params(mn, mx, (double)levels, step);
         for (int col = lane; col < d; col += 32)
-          vc[i * d + col] = (uint8_t)quant_code((double)sv[i * d + col], mn, mx, step);
+          vc[i * d + col] = (uint8_t)quant_code((double)sv[i * d + col], mn, mx, step, levels);
         if (lane == 0) {
           vstep[i] = __double2float_rn(step);
           vxmin[i] = __double2float_rn(mn);
@@ -338,18 +339,28 @@ __global__ void __launch_bounds__(kFlushThreads) flush_kernel(ott_cache_t c, int
     }
     __syncthreads();
 
-    // ---- 4. pack_codes (quant.py:241-256): element e=t*d+c at bits [2e, 2e+2)
+    // ---- 4. pack_codes (quant.py:241-256): element e=t*d+c at bits [b*e, b*e+b)
     {
       uint32_t* kw = reinterpret_cast<uint32_t*>(rec + L.k_codes());
       uint32_t* vw = reinterpret_cast<uint32_t*>(rec + L.v_codes());
-      const int n_words = G * d / 16;
+      const int bits = c.bits;
+      const int n_words = G * d * bits / 32;
       for (int w = tid; w < 2 * n_words; w += kFlushThreads) {
         const bool isv = w >= n_words;
         const int ww = isv ? w - n_words : w;
-        const uint8_t* src = (isv ? vc : kc) + ww * 16;
+        const uint8_t* src = isv ? vc : kc;
         uint32_t word = 0;
+        if (bits == 2) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) word |= (uint32_t)src[j] << (2 * j);
+          for (int j = 0; j < 16; ++j) word |= (uint32_t)src[ww * 16 + j] << (2 * j);
+        } else {  // codes overlapping stream bits [32 ww, 32 ww + 32); some straddle words
+          const int e0 = (32 * ww) / bits, e1 = (32 * ww + 31) / bits;
+          for (int e = e0; e <= e1; ++e) {
+            const int sh = e * bits - 32 * ww;  // may be negative for the first code
+            const uint64_t v = (uint64_t)src[e];
+            word |= (uint32_t)(sh >= 0 ? (v << sh) : (v >> -sh));
+          }
+        }
         (isv ? vw : kw)[ww] = word;
       }
     }

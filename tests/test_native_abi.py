@@ -41,8 +41,8 @@ def test_record_bytes_and_version_without_gpu():
 def test_contract_errors_map_to_contract_violation():
     from paper_2505_10938_b200 import ContractViolation, _native
 
-    c = _native.OttCacheT(n_units=1, head_dim=128, group_size=32, residual=0, capacity=0, aux_capacity=0, bits=4)
-    with pytest.raises(ContractViolation):
+    c = _native.OttCacheT(n_units=1, head_dim=128, group_size=32, residual=0, capacity=0, aux_capacity=0, bits=9)
+    with pytest.raises(ContractViolation):  # bits outside [1, 8] (quant.py:53-54)
         _native.check(_native.lib().ott_flush(ctypes.byref(c), 0, 1, 0, None, None, 0, 0, None))
     c.bits = 2
     with pytest.raises(ContractViolation):  # null state buffers
