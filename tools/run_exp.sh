@@ -1,2 +1,2 @@
-timeout 300 python tools/prof_c1.py --steps 16 > gpurun_out/c1.log 2>&1
-timeout 300 python -m pytest tests -m gpu -x -q -k "decoder or device_counter" > gpurun_out/pytest_gpu.log 2>&1; echo pytest_exit=$? >> gpurun_out/pytest_gpu.log
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest_exit=$? >> gpurun_out/pytest_gpu.log
+bash tools/run_var.sh base prev base prev > gpurun_out/var.log 2>&1
