@@ -11,6 +11,9 @@
 namespace ott {
 
 constexpr int kFlushThreads = 256;
+#ifndef OTT_FLUSH_MIN_BLOCKS
+#define OTT_FLUSH_MIN_BLOCKS 3  // <= 85 registers: 3 CTAs per SM for large unit counts
+#endif
 
 // quant.py:59-102 for one line held in registers/smem by ONE thread.
 // levels = 2^bits - 1. Returns step.
@@ -22,9 +25,23 @@ __device__ __forceinline__ void line_params(double mn, double mx, double levels,
   step_out = step;
 }
 
-__device__ __forceinline__ int quant_code(double x, double mn, double mx, double step, int levels) {
+// inv = __drcp_rn(step). floor((x - mn) / step) of quant.py:93 is taken from the product
+// (x - mn) * inv when that lies more than 1e-9 (relative) from an integer: the product
+// and the correctly rounded quotient differ by < 4e-16 relative, so both floor to the
+// same integer; otherwise (exact lattice points, ties) the IEEE division decides.
+// x >= x_min for every element of the line, so the product is non-negative.
+__device__ __forceinline__ int quant_code(double x, double mn, double mx, double step, double inv, int levels) {
   if (step == 0.0) return 0;  // quant.py:91-92
-  double f = floor(__ddiv_rn(__dsub_rn(x, mn), step));  // quant.py:93
+  const double dd = __dsub_rn(x, mn);
+  double f;
+  if (dd == 0.0) {
+    f = 0.0;
+  } else {
+    const double qa = __dmul_rn(dd, inv);
+    f = floor(qa);
+    const double t = __dsub_rn(qa, f);  // fractional part; qa >= 0 here (x >= x_min)
+    if (!(t > 1e-9 * fmax(1.0, qa) && t < 1.0 - 1e-9 * fmax(1.0, qa))) f = floor(__ddiv_rn(dd, step));
+  }
   int c = f < 0.0 ? 0 : (f > (double)levels ? levels : (int)f);  // quant.py:94
   if (__dadd_rn(__dmul_rn((double)c, step), mn) > x) c -= 1;  // quant.py:97
   c = c < 0 ? 0 : c;                                          // quant.py:98
@@ -53,7 +70,7 @@ __host__ __device__ inline size_t flush_smem_bytes(int d, int G, int N) {
   return (b + 15) & ~(size_t)15;
 }
 
-__global__ void __launch_bounds__(kFlushThreads) flush_kernel(ott_cache_t c, int64_t q0, int n_groups,
+__global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_kernel(ott_cache_t c, int64_t q0, int n_groups,
                                                               int64_t ring_end, const uint16_t* __restrict__ in_k,
                                                               const uint16_t* __restrict__ in_v,
                                                               int64_t in_stride, int64_t in_first,
@@ -105,27 +122,65 @@ __global__ void __launch_bounds__(kFlushThreads) flush_kernel(ott_cache_t c, int
   }
   __syncthreads();
 
+  // the first kPre row loads of the next group are issued into registers before the
+  // current group is processed, so their global latency overlaps its compute
+  constexpr int kPre = 2;
+  uint4 pk8[kPre], pv8[kPre];
+#define OTT_ROW_SRC(BASE, E, SK, SV)                                               \
+  {                                                                                \
+    const int i_ = (E) / d, col_ = (E) % d;                                        \
+    const int64_t p_ = (BASE) + i_;                                                \
+    if (p_ < ring_end) {                                                           \
+      const size_t off_ = ((size_t)u * cap + (size_t)(p_ % cap)) * d + col_;        \
+      SK = c.pend_k + off_;                                                        \
+      SV = c.pend_v + off_;                                                        \
+    } else {                                                                       \
+      const size_t off_ = (size_t)u * in_stride + (size_t)(p_ - in_first) * d + col_; \
+      SK = in_k + off_;                                                            \
+      SV = in_v + off_;                                                            \
+    }                                                                              \
+  }
+#define OTT_PREFETCH(BASE)                                              \
+  {                                                                     \
+    _Pragma("unroll") for (int it = 0; it < kPre; ++it) {               \
+      const int e_ = tid * 8 + it * kFlushThreads * 8;                  \
+      if (e_ < G * d) {                                                 \
+        const uint16_t *sk_, *sv_;                                      \
+        OTT_ROW_SRC(BASE, e_, sk_, sv_)                                 \
+        pk8[it] = *reinterpret_cast<const uint4*>(sk_);                 \
+        pv8[it] = *reinterpret_cast<const uint4*>(sv_);                 \
+      }                                                                 \
+    }                                                                   \
+  }
+  if (n_groups > 0) OTT_PREFETCH(q0)
+
   for (int g = 0; g < n_groups; ++g) {
     const int64_t base = q0 + (int64_t)g * G;
     const int64_t gi = base / G;
     uint8_t* rec = record_ptr(c, u, gi);
 
     // ---- 1. gather the oldest G pending rows (cache.py:155-156), fp16 -> f32
-    for (int e = tid * 8; e < G * d; e += kFlushThreads * 8) {
-      const int i = e / d, col = e % d;
-      const int64_t p = base + i;
-      const uint16_t *srck, *srcv;
-      if (p < ring_end) {
-        const size_t off = ((size_t)u * cap + (size_t)(p % cap)) * d + col;
-        srck = c.pend_k + off;
-        srcv = c.pend_v + off;
-      } else {
-        const size_t off = (size_t)u * in_stride + (size_t)(p - in_first) * d + col;
-        srck = in_k + off;
-        srcv = in_v + off;
+#pragma unroll
+    for (int it = 0; it < kPre; ++it) {
+      const int e = tid * 8 + it * kFlushThreads * 8;
+      if (e < G * d) {
+        const uint16_t* kh = reinterpret_cast<const uint16_t*>(&pk8[it]);
+        const uint16_t* vh = reinterpret_cast<const uint16_t*>(&pv8[it]);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          sk[e + j] = h2f(kh[j]);
+          sv[e + j] = h2f(vh[j]);
+        }
       }
-      const uint4 k8 = *reinterpret_cast<const uint4*>(srck);
-      const uint4 v8 = *reinterpret_cast<const uint4*>(srcv);
+    }
+    for (int e = tid * 8 + kPre * kFlushThreads * 8; e < G * d; e += kFlushThreads * 8) {
+      uint4 k8, v8;
+      {
+        const uint16_t *srck, *srcv;
+        OTT_ROW_SRC(base, e, srck, srcv)
+        k8 = *reinterpret_cast<const uint4*>(srck);
+        v8 = *reinterpret_cast<const uint4*>(srcv);
+      }
       const uint16_t* kh = reinterpret_cast<const uint16_t*>(&k8);
       const uint16_t* vh = reinterpret_cast<const uint16_t*>(&v8);
 #pragma unroll
@@ -134,6 +189,7 @@ __global__ void __launch_bounds__(kFlushThreads) flush_kernel(ott_cache_t c, int
         sv[e + j] = h2f(vh[j]);
       }
     }
+    if (g + 1 < n_groups) OTT_PREFETCH(base + G)
     if (tid < G) sel[tid] = 0;
     if (tid == 0) sh.any_selected = 0;
     __syncthreads();
@@ -292,16 +348,18 @@ __global__ void __launch_bounds__(kFlushThreads) flush_kernel(ott_cache_t c, int
     float* vxmin = reinterpret_cast<float*>(rec + L.v_xmin());
     if (tid < d) {
       const int col = tid;
-      double mn = (double)sk[col], mx = mn;
+      float fmn = sk[col], fmx = fmn;
       for (int i = 1; i < G; ++i) {
-        const double x = (double)sk[i * d + col];
-        mn = fmin(mn, x);
-        mx = fmax(mx, x);
+        const float x = sk[i * d + col];
+        fmn = fminf(fmn, x);
+        fmx = fmaxf(fmx, x);
       }
+      const double mn = (double)fmn, mx = (double)fmx;
       double step;
       line_params(mn, mx, (double)levels, step);
+      const double inv = step > 0.0 ? __drcp_rn(step) : 0.0;
       for (int i = 0; i < G; ++i)
-        kc[i * d + col] = (uint8_t)quant_code((double)sk[i * d + col], mn, mx, step, levels);
+        kc[i * d + col] = (uint8_t)quant_code((double)sk[i * d + col], mn, mx, step, inv, levels);
       // decode-side encoding (ott_common.cuh): step = sh + sl, e = x_min - 4 u step
       const __half sh = __double2half(step);
       const __half sl = __double2half(__dsub_rn(step, (double)__half2float(sh)));
@@ -315,18 +373,24 @@ __global__ void __launch_bounds__(kFlushThreads) flush_kernel(ott_cache_t c, int
     } else {
       const int vw = warp - d / 32, nvw = nwarps - d / 32;
       for (int i = vw; i < G; i += nvw) {
-        double mn = 1e308, mx = -1e308;
+        // min/max of fp16-valued floats are exact in float32: reduce in float (1 shuffle per level)
+        float fmn = 3.4e38f, fmx = -3.4e38f;
         for (int col = lane; col < d; col += 32) {
-          const double x = (double)sv[i * d + col];
-          mn = fmin(mn, x);
-          mx = fmax(mx, x);
+          const float x = sv[i * d + col];
+          fmn = fminf(fmn, x);
+          fmx = fmaxf(fmx, x);
         }
-        mn = warp_min_d(mn);
-        mx = warp_max_d(mx);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          fmn = fminf(fmn, __shfl_xor_sync(0xffffffffu, fmn, o));
+          fmx = fmaxf(fmx, __shfl_xor_sync(0xffffffffu, fmx, o));
+        }
+        const double mn = (double)fmn, mx = (double)fmx;
         double step;
         line_params(mn, mx, (double)levels, step);
+        const double inv = step > 0.0 ? __drcp_rn(step) : 0.0;
         for (int col = lane; col < d; col += 32)
-          vc[i * d + col] = (uint8_t)quant_code((double)sv[i * d + col], mn, mx, step, levels);
+          vc[i * d + col] = (uint8_t)quant_code((double)sv[i * d + col], mn, mx, step, inv, levels);
         if (lane == 0) {
           vstep[i] = __double2float_rn(step);
           vxmin[i] = __double2float_rn(mn);
@@ -366,6 +430,8 @@ __global__ void __launch_bounds__(kFlushThreads) flush_kernel(ott_cache_t c, int
     }
     __syncthreads();
   }
+#undef OTT_PREFETCH
+#undef OTT_ROW_SRC
   if (tid == 0) {
     meta[0] = sh.n_entries;
     meta[1] = sh.n_aux;
