@@ -1447,29 +1447,47 @@ __global__ void __launch_bounds__(tc5::kThreads, OTT_TC5_MIN_BLOCKS)
 }
 
 // ============================================================ combine + debug logits
+// Split combine: one warp per (unit, head) row, 8 rows per 256-thread block; lane
+// handles columns 2*lane, 2*lane+1 (+64, +65 at D = 128) with float2 loads.
+constexpr int kCombineRows = 8;
 template <int D>
-__global__ void combine_kernel(const float* __restrict__ ws, uint16_t* __restrict__ out, int n_splits,
-                               int64_t* __restrict__ dev_counts, int G, int R, int max_groups) {
-  const int ur = blockIdx.x;  // unit*NR + r
-  if (dev_counts && ur == 0 && threadIdx.x == 0) {  // last kernel of a device-counter step: advance
+__global__ void __launch_bounds__(32 * kCombineRows) combine_kernel(const float* __restrict__ ws,
+                                                                   uint16_t* __restrict__ out, int n_rows,
+                                                                   int n_splits, int64_t* __restrict__ dev_counts,
+                                                                   int G, int R, int max_groups) {
+  const int lane = threadIdx.x & 31;
+  const int ur = blockIdx.x * kCombineRows + (threadIdx.x >> 5);  // unit*NR + r
+  if (dev_counts && blockIdx.x == 0 && threadIdx.x == 0) {  // last kernel of a device-counter step: advance
     const int64_t qt = dev_counts[0], tot = dev_counts[1] + 1;
     if (tot - qt - R >= G && qt / G + 1 <= max_groups) dev_counts[0] = qt + G;
     dev_counts[1] = tot;
   }
+  if (ur >= n_rows) return;
   const float* base = ws + (size_t)ur * n_splits * (D + 2);
   float M = -INFINITY;
   for (int s = 0; s < n_splits; ++s) M = fmaxf(M, base[(size_t)s * (D + 2)]);
-  for (int col = threadIdx.x; col < D; col += blockDim.x) {
-    float Lsum = 0.f, A = 0.f;
-    for (int s = 0; s < n_splits; ++s) {
-      const float* p = base + (size_t)s * (D + 2);
-      if (p[0] == -INFINITY) continue;
-      const float f = exp2f(p[0] - M);
-      Lsum += p[1] * f;
-      A += p[2 + col] * f;
+  float Lsum = 0.f;
+  float2 acc[D / 64];
+#pragma unroll
+  for (int k = 0; k < D / 64; ++k) acc[k] = make_float2(0.f, 0.f);
+  for (int s = 0; s < n_splits; ++s) {
+    const float* p = base + (size_t)s * (D + 2);
+    const float m = p[0];
+    if (m == -INFINITY) continue;
+    const float f = exp2f(m - M);
+    Lsum += p[1] * f;
+#pragma unroll
+    for (int k = 0; k < D / 64; ++k) {
+      const float2 v = *reinterpret_cast<const float2*>(p + 2 + 64 * k + 2 * lane);
+      acc[k].x = fmaf(v.x, f, acc[k].x);
+      acc[k].y = fmaf(v.y, f, acc[k].y);
     }
-    out[(size_t)ur * D + col] = f2h(A / Lsum);
   }
+  const float inv = 1.f / Lsum;
+#pragma unroll
+  for (int k = 0; k < D / 64; ++k)
+    *reinterpret_cast<__half2*>(out + (size_t)ur * D + 64 * k + 2 * lane) =
+        __floats2half2_rn(acc[k].x * inv, acc[k].y * inv);
 }
 
 template <int D>
@@ -1521,7 +1539,8 @@ static cudaError_t launch_simt_t(const AttnArgs& a, cudaStream_t st) {
   attend_simt_kernel<NR, D><<<dim3(a.c.n_units, a.n_splits), kAttnThreads, smem, st>>>(a);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  combine_kernel<D><<<a.c.n_units * NR, D, 0, st>>>(a.ws, a.out, a.n_splits, const_cast<int64_t*>(a.dev_counts),
+  combine_kernel<D><<<(a.c.n_units * NR + kCombineRows - 1) / kCombineRows, 32 * kCombineRows, 0, st>>>(
+      a.ws, a.out, a.c.n_units * NR, a.n_splits, const_cast<int64_t*>(a.dev_counts),
                                                    a.c.group_size, a.c.residual, a.c.max_groups);
   return cudaGetLastError();
 }
@@ -1559,7 +1578,8 @@ static cudaError_t launch_mma_t(const AttnArgs& a, cudaStream_t st) {
   attend_mma_kernel<NR, G><<<dim3(a.c.n_units, a.n_splits), kAttnThreads, smem, st>>>(a, tmap);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  combine_kernel<128><<<a.c.n_units * NR, 128, 0, st>>>(a.ws, a.out, a.n_splits, const_cast<int64_t*>(a.dev_counts),
+  combine_kernel<128><<<(a.c.n_units * NR + kCombineRows - 1) / kCombineRows, 32 * kCombineRows, 0, st>>>(
+      a.ws, a.out, a.c.n_units * NR, a.n_splits, const_cast<int64_t*>(a.dev_counts),
                                                      a.c.group_size, a.c.residual, a.c.max_groups);
   return cudaGetLastError();
 }
@@ -1575,7 +1595,8 @@ static cudaError_t launch_tc5_t(const AttnArgs& a, cudaStream_t st) {
   attend_tc5_kernel<NR><<<dim3(a.c.n_units, a.n_splits), tc5::kThreads, smem, st>>>(a, tmap);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  combine_kernel<128><<<a.c.n_units * NR, 128, 0, st>>>(a.ws, a.out, a.n_splits, const_cast<int64_t*>(a.dev_counts),
+  combine_kernel<128><<<(a.c.n_units * NR + kCombineRows - 1) / kCombineRows, 32 * kCombineRows, 0, st>>>(
+      a.ws, a.out, a.c.n_units * NR, a.n_splits, const_cast<int64_t*>(a.dev_counts),
                                                      a.c.group_size, a.c.residual, a.c.max_groups);
   return cudaGetLastError();
 }
