@@ -17,6 +17,7 @@
  *                       (reconstructed_kv attention.py:62-76,
  *                       attend_full_precision attention.py:35-59)
  *   ott_logits       <- AttentionResult.scores         attention.py:26-32 (debug)
+ *   ott_append_attend <- append + attend_mixed of one decode step (ring write fused)
  *   ott_decode_step  <- append + attend_mixed of one decode step, token counts in device
  *                       memory (CUDA-graph capturable)    cache.py:124-139, attention.py:79-92
  *
@@ -113,6 +114,15 @@ int ott_attend(const ott_cache_t* c, const uint16_t* q, uint16_t* out, int32_t n
 
 /* Debug: pre-softmax logits (AttentionResult.scores, attention.py:55) for all
  * total_tokens positions, float32 [n_units][n_rep][total_tokens]. */
+/* append + attend of one decode step with host token counts: (k, v) [n_units][head_dim] is
+ * the row at position total_tokens - 1 (total_tokens counts it). A flush that became due
+ * with this row must have been launched before (ott_flush; with residual >= 1 it never
+ * needs the new row). On the tensor-core path the attention kernel writes the row into
+ * the pending ring itself (no separate ring-write launch). */
+int ott_append_attend(const ott_cache_t* c, const uint16_t* k, const uint16_t* v, const uint16_t* q, uint16_t* out,
+                      int32_t n_rep, int64_t quantized_tokens, int64_t total_tokens, float* workspace,
+                      int32_t n_splits, void* stream);
+
 /* One decode step with the token counts in device memory, so a whole model step can be
  * captured in a CUDA graph and replayed: counters = int64[2] {quantized_tokens,
  * total_tokens} on the device, read by the kernels and advanced by the last one.

@@ -64,6 +64,7 @@ def lib() -> ctypes.CDLL:
         L.ott_attend.argtypes = [P, _vp, _vp, _i32, _i64, _i64, _vp, _i32, _vp]
         L.ott_logits.argtypes = [P, _vp, _vp, _i32, _i64, _i64, _vp]
         L.ott_decode_step.argtypes = [P, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _i32, _vp]
+        L.ott_append_attend.argtypes = [P, _vp, _vp, _vp, _vp, _i32, _i64, _i64, _vp, _i32, _vp]
         L.ott_model_rmsnorm.argtypes = [_vp, _vp, _vp, _i32, _i32, ctypes.c_float, _vp]
         L.ott_model_rope_qkv.argtypes = [_vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp]
         L.ott_model_silu_mul.argtypes = [_vp, _vp, _i32, _i32, _vp]
@@ -75,7 +76,7 @@ def lib() -> ctypes.CDLL:
 
 
 EXPORTED = ("ott_record_bytes", "ott_ring_write", "ott_flush", "ott_pick_splits", "ott_attend_workspace_floats",
-            "ott_attend", "ott_logits", "ott_decode_step", "ott_num_sms", "ott_version", "ott_last_error",
+            "ott_attend", "ott_logits", "ott_append_attend", "ott_decode_step", "ott_num_sms", "ott_version", "ott_last_error",
             "ott_model_rmsnorm", "ott_model_rope_qkv", "ott_model_silu_mul")
 
 

@@ -208,6 +208,38 @@ class OTTCache:
             self._ws = torch.empty(n, dtype=torch.float32, device=self.device)
         return self._ws
 
+    def append_attend(self, k: torch.Tensor, v: torch.Tensor, q: torch.Tensor, out: torch.Tensor | None = None,
+                      n_splits: int | None = None) -> torch.Tensor:
+        """``append(k, v)`` then ``attend(q)`` in one call (the decode step of cli.py:211-213):
+        a due flush is launched first (it never needs the new row when R >= 1), and on the
+        tensor-core path the attention kernel writes the new row into the pending ring
+        itself, saving the ring-write launch. Same results as the two calls."""
+        k = self._check_rows(k, "k")
+        v = self._check_rows(v, "v")
+        require(q.dim() == 3 and q.shape[0] == self.batch and q.shape[2] == self.config.head_dim,
+                f"query must have shape (batch, H_q, {self.config.head_dim})")
+        require(q.shape[1] % self.n_kv_heads == 0, "H_q must be a multiple of n_kv_heads")
+        require(q.dtype == torch.float16 and q.device == self.device, "query must be float16 on the cache device")
+        if self.config.residual == 0:  # the new row may belong to the flushed group
+            self.append(k, v)
+            return self.attend(q, out=out, n_splits=n_splits)
+        n_rep = q.shape[1] // self.n_kv_heads
+        q = q.contiguous()
+        if out is None:
+            out = torch.empty_like(q)
+        G, R = self.config.group_size, self.config.residual
+        due = self.total_tokens + 1 - self.quantized_tokens - R >= G  # cache.py:138
+        require(not due or self.quantized_tokens // G + 1 <= self.max_groups, "cache capacity (max_tokens) exceeded")
+        self.total_tokens += 1
+        if due:
+            self._flush(1, ring_end=self.total_tokens)
+        s = n_splits or self.splits(n_rep)
+        ws = self.workspace(n_rep, s)
+        _native.check(_native.lib().ott_append_attend(self._cref, k.data_ptr(), v.data_ptr(), q.data_ptr(),
+                                                      out.data_ptr(), n_rep, self.quantized_tokens,
+                                                      self.total_tokens, ws.data_ptr(), s, _stream_handle()))
+        return out
+
     def sync_counters(self) -> None:
         """Copy the host token counts into `counters` (before capturing `decode_step`)."""
         self.counters.copy_(torch.tensor([self.quantized_tokens, self.total_tokens], dtype=torch.int64))

@@ -40,7 +40,10 @@ namespace ott {
 constexpr int kAttnThreads = 128;
 constexpr int kAttnWarps = kAttnThreads / 32;
 constexpr float kLog2e = 1.4426950408889634f;
-constexpr float kLazy = 6.f;  // lazy-rescale threshold (log2 units): p <= 64, P' = 4 p step fits fp16
+constexpr float kLazy = 6.f;
+#ifndef OTT_FP_FIRST  // 1: the full-precision-tier CTA of a unit is blockIdx.y == 0 (scheduled first)
+#define OTT_FP_FIRST 0
+#endif  // lazy-rescale threshold (log2 units): p <= 64, P' = 4 p step fits fp16
 
 struct AttnArgs {
   ott_cache_t c;
@@ -56,6 +59,8 @@ struct AttnArgs {
                                      // compiler keeps it in a register: one LOP3 per code pair
   const int64_t* dev_counts;         // non-null: device-counter decode step (token counts below are
                                      // taken from [quantized, total] before this step's append)
+  const uint16_t *new_k, *new_v;     // non-null: this step's appended rows [n_units][d], written to
+                                     // the pending ring (slot (total-1) % (G+R)) by the fp-tier CTA
 };
 
 // Token counts of one launch. Host mode: the launch arguments. Device-counter mode
@@ -467,7 +472,7 @@ __device__ void mma_body(const AttnArgs& a, const Counts& n, const CUtensorMap* 
   const uint32_t magic = a.k_magic;
   const int n_groups = (int)(n.q_tokens / G);
   const int per = (n_groups + a.n_qsplits - 1) / a.n_qsplits;
-  const int g0 = split * per;
+  const int g0 = (split - OTT_FP_FIRST) * per;
   const int g1 = min(n_groups, g0 + per);
   const int my_n = g1 > g0 + warp ? (g1 - g0 - warp + kAttnWarps - 1) / kAttnWarps : 0;
 
@@ -835,6 +840,15 @@ __device__ void fp_body(const AttnArgs& a, const Counts& n, FpSmem& sm) {
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  if (a.new_k) {  // fused ring write (cache.py:134-135): this CTA alone reads the pending tier
+    if (tid < 2 * D / 8) {
+      const size_t dst = ((size_t)u * cap + (size_t)((n.total_tokens - 1) % cap)) * D + (tid % (D / 8)) * 8;
+      const uint16_t* src = (tid < D / 8 ? a.new_k : a.new_v) + (size_t)u * D + (tid % (D / 8)) * 8;
+      *reinterpret_cast<uint4*>((tid < D / 8 ? c.pend_k : c.pend_v) + dst) = *reinterpret_cast<const uint4*>(src);
+      asm volatile("fence.proxy.async.global;\n" ::: "memory");  // visible to this CTA's TMA reads
+    }
+    sync4();
+  }
   __syncwarp();
 
   float o[8][4];
@@ -985,7 +999,7 @@ __global__ void __launch_bounds__(kAttnThreads, OTT_MMA_MIN_BLOCKS)
 #ifndef OTT_ABL_TIER  // timing ablation only (results wrong): 1 skip the fp-tier CTAs, 2 skip quantized CTAs
 #define OTT_ABL_TIER 0
 #endif
-  if ((int)blockIdx.y == a.n_qsplits) {  // full-precision tiers: pool.entries + pending window
+  if ((int)blockIdx.y == (OTT_FP_FIRST ? 0 : a.n_qsplits)) {  // full-precision tiers: pool + pending
     if (OTT_ABL_TIER & 1) return;
     fp_body<NR>(a, counts_of(a), *reinterpret_cast<FpSmem*>(smem_raw));
   } else {
@@ -1163,7 +1177,7 @@ __device__ void tc5_body(const AttnArgs& a, const Counts& n, const CUtensorMap* 
   const int g = lane >> 2, tig = lane & 3;
   const int n_groups = (int)(n.q_tokens / G);
   const int per = (((n_groups + a.n_qsplits - 1) / a.n_qsplits) + 3) & ~3;  // whole chunks per split
-  const int g0 = min(n_groups, split * per);
+  const int g0 = min(n_groups, (split - OTT_FP_FIRST) * per);
   const int g1 = min(n_groups, g0 + per);
   const int n_chunks = (g1 - g0 + 3) / 4;
   const int64_t unit_rec = (int64_t)u * c.max_groups;
@@ -1438,7 +1452,7 @@ template <int NR>
 __global__ void __launch_bounds__(tc5::kThreads, OTT_TC5_MIN_BLOCKS)
     attend_tc5_kernel(const __grid_constant__ AttnArgs a, const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(256) unsigned char smem_raw[];
-  if ((int)blockIdx.y == a.n_qsplits) {  // full-precision tiers on warps 0-3
+  if ((int)blockIdx.y == (OTT_FP_FIRST ? 0 : a.n_qsplits)) {  // full-precision tiers on warps 0-3
     if (threadIdx.x >= 128) return;
     fp_body<NR>(a, counts_of(a), *reinterpret_cast<FpSmem*>(smem_raw));
   } else {
@@ -1615,10 +1629,22 @@ static bool use_tc5() {
 
 bool mma_eligible(const ott_cache_t& c) { return c.head_dim == 128 && c.bits == 2; }
 
+// True when the attention kernel can write the step's new rows itself (fp-tier CTA of the
+// tensor-core kernels); otherwise the caller launches the ring write first.
+#ifndef OTT_FUSE_RING
+#define OTT_FUSE_RING 1
+#endif
+bool attend_fuses_ring_write(const ott_cache_t& c) {
+  return OTT_FUSE_RING && c.head_dim == 128 && c.bits == 2 && c.residual >= 1;
+}
+
 cudaError_t launch_attend(const ott_cache_t& c, const uint16_t* q, uint16_t* out, int n_rep, int64_t q_tokens,
-                          int64_t total, float* ws, int n_qsplits, cudaStream_t st, int64_t* dev_counts) {
+                          int64_t total, float* ws, int n_qsplits, cudaStream_t st, int64_t* dev_counts,
+                          const uint16_t* new_k, const uint16_t* new_v) {
   AttnArgs a;
   a.dev_counts = dev_counts;
+  a.new_k = new_k;
+  a.new_v = new_v;
   a.c = c;
   a.q = q;
   a.out = out;

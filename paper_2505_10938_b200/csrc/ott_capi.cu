@@ -13,7 +13,9 @@ cudaError_t launch_ring_write(const ott_cache_t& c, const uint16_t* k, const uin
                               int64_t in_first, int64_t first_pos, int64_t n_rows, cudaStream_t st,
                               const int64_t* dev_counts = nullptr);
 cudaError_t launch_attend(const ott_cache_t& c, const uint16_t* q, uint16_t* out, int n_rep, int64_t q_tokens,
-                          int64_t total, float* ws, int n_splits, cudaStream_t st, int64_t* dev_counts = nullptr);
+                          int64_t total, float* ws, int n_splits, cudaStream_t st, int64_t* dev_counts = nullptr,
+                          const uint16_t* new_k = nullptr, const uint16_t* new_v = nullptr);
+bool attend_fuses_ring_write(const ott_cache_t& c);
 cudaError_t launch_logits(const ott_cache_t& c, const uint16_t* q, float* logits, int n_rep, int64_t q_tokens,
                           int64_t total, cudaStream_t st);
 }  // namespace ott
@@ -140,6 +142,30 @@ int ott_attend(const ott_cache_t* c, const uint16_t* q, uint16_t* out, int32_t n
                                         (cudaStream_t)stream));
 }
 
+int ott_append_attend(const ott_cache_t* c, const uint16_t* k, const uint16_t* v, const uint16_t* q, uint16_t* out,
+                      int32_t n_rep, int64_t quantized_tokens, int64_t total_tokens, float* workspace,
+                      int32_t n_splits, void* stream) {
+  int s = check_cache(c);
+  if (s) return s;
+  if (!k || !v) return fail(OTT_ERR_CONTRACT, "null rows");
+  if (total_tokens <= 0) return fail(OTT_ERR_CONTRACT, "cannot attend over an empty cache");
+  if (n_rep != 1 && n_rep != 2 && n_rep != 4 && n_rep != 8)
+    return fail(OTT_ERR_UNSUPPORTED, "n_rep (H_q / H_kv) must be 1, 2, 4 or 8");
+  if (quantized_tokens < 0 || quantized_tokens > total_tokens - 1 || quantized_tokens % c->group_size)
+    return fail(OTT_ERR_CONTRACT, "inconsistent token counts");
+  if (total_tokens - quantized_tokens > c->group_size + c->residual)
+    return fail(OTT_ERR_CONTRACT, "more pending rows than the ring holds");
+  if (!q || !out || !workspace || n_splits < 1) return fail(OTT_ERR_CONTRACT, "null buffer or bad split count");
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool fuse = ott::attend_fuses_ring_write(*c);
+  cudaError_t e = fuse ? cudaSuccess
+                       : ott::launch_ring_write(*c, k, v, c->head_dim, total_tokens - 1, total_tokens - 1, 1, st);
+  if (e == cudaSuccess)
+    e = ott::launch_attend(*c, q, out, n_rep, quantized_tokens, total_tokens, workspace, n_splits, st, nullptr,
+                           fuse ? k : nullptr, fuse ? v : nullptr);
+  return cuda_status(e);
+}
+
 int ott_decode_step(const ott_cache_t* c, const uint16_t* k, const uint16_t* v, const uint16_t* q, uint16_t* out,
                     int32_t n_rep, int64_t* counters, float* workspace, int32_t n_splits, void* stream) {
   int s = check_cache(c);
@@ -150,9 +176,12 @@ int ott_decode_step(const ott_cache_t* c, const uint16_t* k, const uint16_t* v, 
   if (c->capacity > 0 && (!c->pool_pos || !c->pool_score || !c->pool_k || !c->pool_v))
     return fail(OTT_ERR_CONTRACT, "null pool buffers");
   cudaStream_t st = (cudaStream_t)stream;
-  cudaError_t e = ott::launch_ring_write(*c, k, v, c->head_dim, 0, 0, 1, st, counters);
+  const bool fuse = ott::attend_fuses_ring_write(*c);  // the new row is written by the attention kernel
+  cudaError_t e = fuse ? cudaSuccess : ott::launch_ring_write(*c, k, v, c->head_dim, 0, 0, 1, st, counters);
   if (e == cudaSuccess) e = ott::launch_flush(*c, 0, 1, 0, nullptr, nullptr, 0, 0, st, counters);
-  if (e == cudaSuccess) e = ott::launch_attend(*c, q, out, n_rep, 0, 1, workspace, n_splits, st, counters);
+  if (e == cudaSuccess)
+    e = ott::launch_attend(*c, q, out, n_rep, 0, 1, workspace, n_splits, st, counters, fuse ? k : nullptr,
+                           fuse ? v : nullptr);
   return cuda_status(e);
 }
 

@@ -85,9 +85,8 @@ class HostDecodePipeline:
             if l >= 2:
                 main.wait_event(read[l - 2])  # o_d[b] drained
             before = c.quantized_tokens
-            c.append(self.k_d[b], self.v_d[b])
-            c.attend(self.q_d[b], out=self.o_d[b], n_splits=self.splits[l])
-            self.launches += 3 + (1 if c.quantized_tokens != before else 0)
+            c.append_attend(self.k_d[b], self.v_d[b], self.q_d[b], out=self.o_d[b], n_splits=self.splits[l])
+            self.launches += 2 + (1 if c.quantized_tokens != before else 0)
             src = self.o_d[b] if self.gather is None else self.gather(self.o_d[b], l)
             computed[l].record(main)
             with torch.cuda.stream(self.d2h):

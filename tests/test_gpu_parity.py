@@ -563,3 +563,26 @@ def test_device_counter_decode_step_and_graph():
         assert torch.equal(te, tg)
         assert torch.equal(eager.last_logits, graph.last_logits)
     assert graph.caches[-1].total_tokens == eager.caches[-1].total_tokens == 360
+
+
+@pytest.mark.parametrize("d,R", [(128, 128), (64, 64), (128, 0)])
+def test_append_attend_equals_append_then_attend(d, R):
+    """OTTCache.append_attend (ring write fused into the attention kernel on the tensor-core
+    path; fallback otherwise) gives bit-identical outputs and state to append + attend."""
+    from paper_2505_10938_b200 import OTTCache
+
+    B, H, n_rep, T, steps = 2, 2, 4, 300, 70
+    rng = np.random.default_rng(8)
+    pre_k, pre_v = (rng.standard_normal((B, H, T, d)).astype(np.float16) for _ in range(2))
+    a, b = (OTTCache(cfg_of(2, 32, R, 4, 32, d), B, H, max_tokens=T + steps + 8) for _ in range(2))
+    for c in (a, b):
+        c.update(torch.from_numpy(pre_k).cuda(), torch.from_numpy(pre_v).cuda())
+    for i in range(steps):
+        k, v = (torch.from_numpy(rng.standard_normal((B, H, d)).astype(np.float16)).cuda() for _ in range(2))
+        q = torch.from_numpy(rng.standard_normal((B, H * n_rep, d)).astype(np.float16)).cuda()
+        a.append(k, v)
+        ref = a.attend(q, n_splits=2)
+        out = b.append_attend(k, v, q, n_splits=2)
+        assert torch.equal(out, ref), i
+    assert (a.total_tokens, a.quantized_tokens) == (b.total_tokens, b.quantized_tokens)
+    assert torch.equal(a.blocks, b.blocks) and torch.equal(a.pend_k, b.pend_k) and torch.equal(a.pend_v, b.pend_v)

@@ -22,12 +22,13 @@ ap.add_argument("--ctx", type=int, default=8192)
 ap.add_argument("--iters", type=int, default=20)
 ap.add_argument("--pool", type=int, default=32)
 ap.add_argument("--splits", type=int, default=0)
+ap.add_argument("--append", action="store_true", help="time append_attend (fused ring write) steps")
 args = ap.parse_args()
 
 torch.cuda.set_device(0)
 cfg = EngineConfig(bits=2, group_size=32, residual=128, outlier_num=args.pool, aux_capacity=32, skip_layers=(),
                    head_dim=128)
-cache = OTTCache(cfg, args.batch, args.kv, args.ctx + 64)
+cache = OTTCache(cfg, args.batch, args.kv, args.ctx + 64 + args.iters)
 gen = torch.Generator(device="cuda").manual_seed(0)
 k = torch.empty((args.batch, args.kv, args.ctx, 128), dtype=torch.float16, device="cuda")
 v = torch.empty_like(k)
@@ -41,9 +42,14 @@ for _ in range(3):
     cache.attend(q, out=out, n_splits=splits)
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+kn = torch.randn((args.batch, args.kv, 128), generator=gen, device="cuda").half()
+vn = torch.randn((args.batch, args.kv, 128), generator=gen, device="cuda").half()
 e0.record()
 for _ in range(args.iters):
-    cache.attend(q, out=out, n_splits=splits)
+    if args.append:
+        cache.append_attend(kn, vn, q, out=out, n_splits=splits)
+    else:
+        cache.attend(q, out=out, n_splits=splits)
 e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / args.iters

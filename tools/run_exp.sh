@@ -1,6 +1,4 @@
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest_exit=$? >> gpurun_out/pytest_gpu.log
-bash tools/run_var.sh base prev base prev > gpurun_out/var.log 2>&1
-for v in base prev; do
+for v in base nofuse base nofuse; do
   if [ $v = base ]; then L=""; else L="OTT_LIB_PATH=tools/variants/$v.so"; fi
-  echo "== $v c3"; env $L timeout 120 python tools/prof_attend.py --batch 16 --rep 4 --ctx 4096 --iters 50 2>&1 | tail -1
-done >> gpurun_out/var.log 2>&1
+  echo "== $v"; env $L timeout 900 python bench.py --no-cpu --no-e2e --steps 16 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['ms_per_step'], d['roofline']['avg_launch_us'], d['clocks']['sm_mhz'])"
+done > gpurun_out/var.log 2>&1
