@@ -23,6 +23,7 @@ ap.add_argument("--iters", type=int, default=20)
 ap.add_argument("--pool", type=int, default=32)
 ap.add_argument("--splits", type=int, default=0)
 ap.add_argument("--append", action="store_true", help="time append_attend (fused ring write) steps")
+ap.add_argument("--graph", action="store_true", help="capture the iters attend launches in one CUDA graph (no host gaps)")
 args = ap.parse_args()
 
 torch.cuda.set_device(0)
@@ -44,12 +45,22 @@ torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 kn = torch.randn((args.batch, args.kv, 128), generator=gen, device="cuda").half()
 vn = torch.randn((args.batch, args.kv, 128), generator=gen, device="cuda").half()
+if args.graph:  # same launches, replayed from one graph so small shapes are not host bound
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(args.iters):
+            cache.attend(q, out=out, n_splits=splits)
+    g.replay()
+    torch.cuda.synchronize()
 e0.record()
-for _ in range(args.iters):
-    if args.append:
-        cache.append_attend(kn, vn, q, out=out, n_splits=splits)
-    else:
-        cache.attend(q, out=out, n_splits=splits)
+if args.graph:
+    g.replay()
+else:
+    for _ in range(args.iters):
+        if args.append:
+            cache.append_attend(kn, vn, q, out=out, n_splits=splits)
+        else:
+            cache.attend(q, out=out, n_splits=splits)
 e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / args.iters
