@@ -586,3 +586,27 @@ def test_append_attend_equals_append_then_attend(d, R):
         assert torch.equal(out, ref), i
     assert (a.total_tokens, a.quantized_tokens) == (b.total_tokens, b.quantized_tokens)
     assert torch.equal(a.blocks, b.blocks) and torch.equal(a.pend_k, b.pend_k) and torch.equal(a.pend_v, b.pend_v)
+
+
+def test_long_context_64k_vs_oracle():
+    """Maximum-size edge: a 64K-token context (2,044 quantized groups per unit, many
+    splits) stays bit-exact in its quantization state and within tolerance in attention."""
+    from paper_2505_10938_b200 import OTTCache
+
+    B, Hkv, n_rep, T, d = 1, 2, 8, 65536 + 77, 128
+    k, v, q = config0_batch(21, B * Hkv, T, d)
+    cache = OTTCache(cfg_of(2, 32, 128, 32, 32, d), B, Hkv, max_tokens=T, keep_f64_params=True)
+    kt, vt = torch.from_numpy(k.reshape(B, Hkv, T, d)).cuda(), torch.from_numpy(v.reshape(B, Hkv, T, d)).cuda()
+    cache.update(kt[:, :, : T - 5], vt[:, :, : T - 5])
+    for t in range(T - 5, T):
+        cache.append(kt[:, :, t], vt[:, :, t])
+    assert cache.splits(n_rep) > 1
+    qh = q[:, :n_rep].reshape(B, Hkv * n_rep, d)
+    out = cache.attend(torch.from_numpy(qh).cuda()).float().cpu().numpy()
+    for u in range(B * Hkv):
+        ref = oracle.OracleCache(2, 32, 128, 32, 32, d)
+        ref.extend(k[u].astype(np.float32), v[u].astype(np.float32))
+        assert_unit_matches_oracle(cache.unit(0, u), ref)
+        for r in range(n_rep):
+            ok, err = within_tol(out[0, u * n_rep + r], ref.attend(qh[0, u * n_rep + r].astype(np.float32)))
+            assert ok, (u, r, err)
