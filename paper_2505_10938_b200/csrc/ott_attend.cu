@@ -41,6 +41,14 @@ constexpr int kAttnThreads = 128;
 constexpr int kAttnWarps = kAttnThreads / 32;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLazy = 6.f;
+#ifndef OTT_PDL  // launch the split combine as a programmatic dependent of the attention grid
+#define OTT_PDL 1
+#endif
+__device__ __forceinline__ void allow_dependents() {
+#if OTT_PDL
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+#endif
+}
 #ifndef OTT_FP_FIRST  // 1: the full-precision-tier CTA of a unit is blockIdx.y == 0 (scheduled first)
 #define OTT_FP_FIRST 0
 #endif  // lazy-rescale threshold (log2 units): p <= 64, P' = 4 p step fits fp16
@@ -313,6 +321,7 @@ __device__ void simt_body(const AttnArgs& a, const Counts& n, int u, int t_begin
 template <int NR, int D>
 __global__ void __launch_bounds__(kAttnThreads) attend_simt_kernel(AttnArgs a) {
   extern __shared__ __align__(256) unsigned char smem_raw[];
+  allow_dependents();
   SimtSmem<NR, D>& sm = *reinterpret_cast<SimtSmem<NR, D>*>(smem_raw);
   const Counts n = counts_of(a);
   const int n_tiles = n.n_qtiles + n.n_ptiles + n.n_rtiles;
@@ -996,6 +1005,7 @@ template <int NR, int G>
 __global__ void __launch_bounds__(kAttnThreads, OTT_MMA_MIN_BLOCKS)
     attend_mma_kernel(const __grid_constant__ AttnArgs a, const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(256) unsigned char smem_raw[];
+  allow_dependents();
 #ifndef OTT_ABL_TIER  // timing ablation only (results wrong): 1 skip the fp-tier CTAs, 2 skip quantized CTAs
 #define OTT_ABL_TIER 0
 #endif
@@ -1452,6 +1462,7 @@ template <int NR>
 __global__ void __launch_bounds__(tc5::kThreads, OTT_TC5_MIN_BLOCKS)
     attend_tc5_kernel(const __grid_constant__ AttnArgs a, const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(256) unsigned char smem_raw[];
+  allow_dependents();
   if ((int)blockIdx.y == (OTT_FP_FIRST ? 0 : a.n_qsplits)) {  // full-precision tiers on warps 0-3
     if (threadIdx.x >= 128) return;
     fp_body<NR>(a, counts_of(a), *reinterpret_cast<FpSmem*>(smem_raw));
@@ -1465,10 +1476,15 @@ __global__ void __launch_bounds__(tc5::kThreads, OTT_TC5_MIN_BLOCKS)
 // handles columns 2*lane, 2*lane+1 (+64, +65 at D = 128) with float2 loads.
 constexpr int kCombineRows = 8;
 template <int D>
+static cudaError_t launch_combine(const AttnArgs& a, int NR, cudaStream_t st);
+template <int D>
 __global__ void __launch_bounds__(32 * kCombineRows) combine_kernel(const float* __restrict__ ws,
                                                                    uint16_t* __restrict__ out, int n_rows,
                                                                    int n_splits, int64_t* __restrict__ dev_counts,
                                                                    int G, int R, int max_groups) {
+#if OTT_PDL
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");  // the attention grid's partials are complete
+#endif
   const int lane = threadIdx.x & 31;
   const int ur = blockIdx.x * kCombineRows + (threadIdx.x >> 5);  // unit*NR + r
   if (dev_counts && blockIdx.x == 0 && threadIdx.x == 0) {  // last kernel of a device-counter step: advance
@@ -1502,6 +1518,22 @@ __global__ void __launch_bounds__(32 * kCombineRows) combine_kernel(const float*
   for (int k = 0; k < D / 64; ++k)
     *reinterpret_cast<__half2*>(out + (size_t)ur * D + 64 * k + 2 * lane) =
         __floats2half2_rn(acc[k].x * inv, acc[k].y * inv);
+}
+
+template <int D>
+static cudaError_t launch_combine(const AttnArgs& a, int NR, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((a.c.n_units * NR + kCombineRows - 1) / kCombineRows);
+  cfg.blockDim = dim3(32 * kCombineRows);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = OTT_PDL;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, combine_kernel<D>, (const float*)a.ws, a.out, a.c.n_units * NR, a.n_splits,
+                            const_cast<int64_t*>(a.dev_counts), a.c.group_size, a.c.residual, a.c.max_groups);
 }
 
 template <int D>
@@ -1553,10 +1585,7 @@ static cudaError_t launch_simt_t(const AttnArgs& a, cudaStream_t st) {
   attend_simt_kernel<NR, D><<<dim3(a.c.n_units, a.n_splits), kAttnThreads, smem, st>>>(a);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  combine_kernel<D><<<(a.c.n_units * NR + kCombineRows - 1) / kCombineRows, 32 * kCombineRows, 0, st>>>(
-      a.ws, a.out, a.c.n_units * NR, a.n_splits, const_cast<int64_t*>(a.dev_counts),
-                                                   a.c.group_size, a.c.residual, a.c.max_groups);
-  return cudaGetLastError();
+  return launch_combine<D>(a, NR, st);
 }
 
 // Tensor map over all block records of the cache: 2-D uint8 view [rows of 32 B],
@@ -1592,10 +1621,7 @@ static cudaError_t launch_mma_t(const AttnArgs& a, cudaStream_t st) {
   attend_mma_kernel<NR, G><<<dim3(a.c.n_units, a.n_splits), kAttnThreads, smem, st>>>(a, tmap);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  combine_kernel<128><<<(a.c.n_units * NR + kCombineRows - 1) / kCombineRows, 32 * kCombineRows, 0, st>>>(
-      a.ws, a.out, a.c.n_units * NR, a.n_splits, const_cast<int64_t*>(a.dev_counts),
-                                                     a.c.group_size, a.c.residual, a.c.max_groups);
-  return cudaGetLastError();
+  return launch_combine<128>(a, NR, st);
 }
 
 template <int NR>
@@ -1609,10 +1635,7 @@ static cudaError_t launch_tc5_t(const AttnArgs& a, cudaStream_t st) {
   attend_tc5_kernel<NR><<<dim3(a.c.n_units, a.n_splits), tc5::kThreads, smem, st>>>(a, tmap);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  combine_kernel<128><<<(a.c.n_units * NR + kCombineRows - 1) / kCombineRows, 32 * kCombineRows, 0, st>>>(
-      a.ws, a.out, a.c.n_units * NR, a.n_splits, const_cast<int64_t*>(a.dev_counts),
-                                                     a.c.group_size, a.c.residual, a.c.max_groups);
-  return cudaGetLastError();
+  return launch_combine<128>(a, NR, st);
 }
 
 // Attention kernel for (d = 128, G = 32): the mma.sync kernel (default, faster as
