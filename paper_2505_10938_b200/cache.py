@@ -31,6 +31,19 @@ def _stream_handle() -> int:
     return torch.cuda.current_stream().cuda_stream
 
 
+def _on_device(fn):
+    """Run a cache method with the cache's GPU as the current device, so the C ABI
+    launches on that device's current stream (multi-GPU processes)."""
+    import functools
+
+    @functools.wraps(fn)
+    def wrapper(self, *args, **kwargs):
+        with torch.cuda.device(self.device):
+            return fn(self, *args, **kwargs)
+
+    return wrapper
+
+
 def _ptr(t) -> int | None:
     return None if t is None else t.data_ptr()
 
@@ -150,6 +163,7 @@ class OTTCache:
         return x
 
     # --------------------------------------------------------------- write path
+    @_on_device
     def append(self, k: torch.Tensor, v: torch.Tensor) -> None:
         """cache.py:124-139: add one token per unit; quantize a group when due."""
         k = self._check_rows(k, "k")
@@ -160,6 +174,7 @@ class OTTCache:
         if self.pending_rows - self.config.residual >= self.config.group_size:  # cache.py:138
             self.quantize_oldest_group()
 
+    @_on_device
     def quantize_oldest_group(self) -> None:
         """cache.py:141-186 for every unit (one launch of the flush kernel)."""
         G = self.config.group_size
@@ -175,6 +190,7 @@ class OTTCache:
                                               _ptr(in_v), in_stride, in_first, _stream_handle()))
         self.quantized_tokens += n_groups * self.config.group_size
 
+    @_on_device
     def update(self, k: torch.Tensor, v: torch.Tensor) -> None:
         """Bulk insert of T tokens per unit, numerically identical to T sequential
         ``append`` calls: full groups are flushed straight from the
@@ -208,6 +224,7 @@ class OTTCache:
             self._ws = torch.empty(n, dtype=torch.float32, device=self.device)
         return self._ws
 
+    @_on_device
     def append_attend(self, k: torch.Tensor, v: torch.Tensor, q: torch.Tensor, out: torch.Tensor | None = None,
                       n_splits: int | None = None) -> torch.Tensor:
         """``append(k, v)`` then ``attend(q)`` in one call (the decode step of cli.py:211-213):
@@ -240,10 +257,12 @@ class OTTCache:
                                                       self.total_tokens, ws.data_ptr(), s, _stream_handle()))
         return out
 
+    @_on_device
     def sync_counters(self) -> None:
         """Copy the host token counts into `counters` (before capturing `decode_step`)."""
         self.counters.copy_(torch.tensor([self.quantized_tokens, self.total_tokens], dtype=torch.int64))
 
+    @_on_device
     def decode_step(self, k: torch.Tensor, v: torch.Tensor, q: torch.Tensor, out: torch.Tensor,
                     n_splits: int) -> torch.Tensor:
         """append(k, v) + attend(q) -> out with the token counts read from and advanced
@@ -276,6 +295,7 @@ class OTTCache:
             require(self.quantized_tokens // G + 1 <= self.max_groups, "cache capacity (max_tokens) exceeded")
             self.quantized_tokens += G
 
+    @_on_device
     def attend(self, q: torch.Tensor, out: torch.Tensor | None = None, n_splits: int | None = None) -> torch.Tensor:
         """attend_mixed (attention.py:79-92) for every query head.
 

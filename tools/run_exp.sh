@@ -1,1 +1,2 @@
-bash tools/run_var.sh base q16smb5 q16s mb5 base q16smb5 > gpurun_out/var.log 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest_exit=$? >> gpurun_out/pytest_gpu.log
+timeout 300 python tools/prof_c1.py --steps 16 > gpurun_out/c1.log 2>&1
