@@ -46,20 +46,24 @@ typedef enum {
 
 /* Device-side state of one layer's batched tiered cache. Sizes in elements.
  * Block record (one per (unit, group)), byte layout, all little-endian:
- *   [0, G*d*bits/8)                 K codes, reference pack_codes order
- *   [+G*d*bits/8)                   V codes
+ *   [0, CB)                         K codes, reference pack_codes order; CB =
+ *                                   ceil(G*d*bits/8) rounded up to 16 (= G*d*bits/8
+ *                                   when d in {64, 128} and G % 32 == 0)
+ *   [CB, 2 CB)                      V codes
  *   fp16 k_sh[d], k_sl[d]           per-channel K step = sh + sl, in pair order
- *                                   (index 16*(c/16) + 2*(c%8) + (c%16)/8)
+ *                                   (index 16*(c/16) + 2*(c%8) + (c%16)/8 when
+ *                                   d % 16 == 0, else c)
  *   float32 k_e[d]                  per-channel K x_min - 4*u(c)*step, u(c) = 4^(4-P(c%8)),
  *                                   P = {3,4,2,3,4,2,3,4} (fp16 mantissa position of the
  *                                   code pair in the decode kernels)
  *   float32 v_step[G], v_xmin[G]    per-token V params
+ *   (record size rounded up to 16 bytes)
  * The exact float64 QuantParams are kept in params64 when it is allocated. 
  * Per-token bitmasks hold one bit per absolute position (32 per word). */
 typedef struct {
   int32_t n_units;      /* batch * n_kv_heads */
-  int32_t head_dim;     /* d: 64 or 128 */
-  int32_t group_size;   /* G: multiple of 32, <= 128 */
+  int32_t head_dim;     /* d in [1, 128] (tensor-core kernels: 128; tile kernel: 64, 128) */
+  int32_t group_size;   /* G in [1, 128] (tensor-core / tile kernels: multiple of 32) */
   int32_t residual;     /* R >= 0 */
   int32_t capacity;     /* N: pool capacity for this layer (EngineConfig.outlier_capacity) */
   int32_t aux_capacity; /* A */
@@ -68,8 +72,8 @@ typedef struct {
   uint8_t* blocks;      /* [n_units][max_groups][record_bytes] */
   uint16_t* pend_k;     /* fp16 [n_units][G+R][d], slot = position % (G+R) */
   uint16_t* pend_v;
-  uint32_t* pool_mask;  /* [n_units][max_groups*G/32]: 1 = position currently in pool.entries */
-  uint32_t* subst_mask; /* [n_units][max_groups*G/32]: substituted_positions */
+  uint32_t* pool_mask;  /* [n_units][ceil(max_groups*G/32)]: 1 = position in pool.entries */
+  uint32_t* subst_mask; /* [n_units][ceil(max_groups*G/32)]: substituted_positions */
   int32_t* pool_pos;    /* [n_units][N] slot-stable entries, -1 = empty; reference order =
                            ascending (score, position), outlier.py:52-54 */
   double* pool_score;   /* [n_units][N] */

@@ -49,10 +49,17 @@ def _ptr(t) -> int | None:
 
 
 
-def kpair_index(c):
-    """Pair-order index of channel c in the record's fp16 K step halves (ott_b200.h)."""
+def kpair_index(c, d=128):
+    """Index of channel c in the record's fp16 K step halves (ott_b200.h): pair order
+    when d % 16 == 0, channel order otherwise."""
     c = np.asarray(c)
-    return 16 * (c // 16) + 2 * (c % 8) + (c % 16) // 8
+    c = np.asarray(c)
+    return c if d % 16 else 16 * (c // 16) + 2 * (c % 8) + (c % 16) // 8
+
+
+def record_code_bytes(d, G, bits):
+    """Bytes of one code field of a block record: ceil(G d bits / 8) padded to 16."""
+    return ((G * d * bits + 7) // 8 + 15) & ~15
 
 
 def kpair_u(c):
@@ -71,7 +78,9 @@ class OTTCache:
     Args:
         config: EngineConfig (same fields as the reference). bits in [1, 8]
             (2-bit uses the tensor-core kernels, other widths the CUDA-core kernel);
-            head_dim 64 or 128; group_size a multiple of 32 up to 128.
+            head_dim and group_size in [1, 128] (d = 128 with G % 32 == 0 runs the
+            tensor-core kernels; other shapes, e.g. the reference tests' d = 2..16,
+            G = 4..16, run a generic CUDA-core kernel).
         batch, n_kv_heads: unit grid.
         max_tokens: capacity of the quantized store per unit.
         layer: layer index; pool capacity is ``config.outlier_capacity(layer)``.
@@ -86,9 +95,8 @@ class OTTCache:
         if not torch.cuda.is_available():
             raise _native.NativeError("OTTCache needs a CUDA device (B200); there is no CPU path")
         require(1 <= config.bits <= 8, "bits must be in [1, 8]")
-        require(config.head_dim in (64, 128), "head_dim must be 64 or 128")
-        require(config.group_size % 32 == 0 and 32 <= config.group_size <= 128,
-                "group_size must be a multiple of 32 in [32, 128]")
+        require(1 <= config.head_dim <= 128, "head_dim must be in [1, 128] on the GPU path")
+        require(1 <= config.group_size <= 128, "group_size must be in [1, 128] on the GPU path")
         require(batch >= 1 and n_kv_heads >= 1 and max_tokens >= 1, "batch, n_kv_heads, max_tokens must be >= 1")
         self.config = config
         self.layer = layer
@@ -110,7 +118,7 @@ class OTTCache:
         self.blocks = torch.zeros((U, self.max_groups, self.record_bytes), dtype=torch.uint8, **kw)
         self.pend_k = torch.zeros((U, G + R, d), dtype=torch.float16, **kw)
         self.pend_v = torch.zeros((U, G + R, d), dtype=torch.float16, **kw)
-        words = self.max_groups * G // 32
+        words = (self.max_groups * G + 31) // 32
         self.pool_mask = torch.zeros((U, words), dtype=torch.int32, **kw)
         self.subst_mask = torch.zeros((U, words), dtype=torch.int32, **kw)
         n, a = max(self.N, 1), max(self.A, 1)
@@ -365,7 +373,8 @@ class UnitView:
         self.quantized_tokens = cache.quantized_tokens
         nb = cache.quantized_tokens // G
         rec = cache.blocks[u, :nb].cpu().numpy()
-        code_b = G * d * cfg.bits // 8
+        code_b = record_code_bytes(d, G, cfg.bits)  # padded field (ott_b200.h)
+        code_n = (G * d * cfg.bits + 7) // 8  # the reference's packed size (quant.py:237-238)
         # K params are stored in the decode kernels' encoding (ott_b200.h): fp16 halves
         # sh + sl of the step in pair order and e = x_min - 4 u step; the float32 views
         # below are reconstructions, the exact values come from params64
@@ -373,8 +382,8 @@ class UnitView:
         self.k_sl16 = rec[:, 2 * code_b + 2 * d: 2 * code_b + 4 * d].copy().view(np.float16)
         self.k_e32 = rec[:, 2 * code_b + 4 * d: 2 * code_b + 8 * d].copy().view(np.float32)
         vst = rec[:, 2 * code_b + 8 * d: 2 * code_b + 8 * d + 4 * G].copy().view(np.float32)
-        vmn = rec[:, 2 * code_b + 8 * d + 4 * G:].copy().view(np.float32)
-        pidx = kpair_index(np.arange(d))
+        vmn = rec[:, 2 * code_b + 8 * d + 4 * G: 2 * code_b + 8 * d + 8 * G].copy().view(np.float32)
+        pidx = kpair_index(np.arange(d), d)
         kst = self.k_sh16[:, pidx].astype(np.float32) + self.k_sl16[:, pidx].astype(np.float32)
         kmn = (self.k_e32 + np.float32(4) * kpair_u(np.arange(d)) * kst).astype(np.float32)
         self.k_step32, self.k_xmin32, self.v_step32, self.v_xmin32 = kst, kmn, vst, vmn
@@ -386,10 +395,10 @@ class UnitView:
         self.quantized_k, self.quantized_v = [], []
         for i in range(nb):
             b = cfg.bits
-            self.quantized_k.append(QuantizedBlock(rec[i, :code_b].tobytes(), GroupAxis.PER_CHANNEL,
+            self.quantized_k.append(QuantizedBlock(rec[i, :code_n].tobytes(), GroupAxis.PER_CHANNEL,
                                                    [QuantParams(float(kmn64[i, c]), float(kst64[i, c]), b)
                                                     for c in range(d)], G, d, b))
-            self.quantized_v.append(QuantizedBlock(rec[i, code_b:2 * code_b].tobytes(), GroupAxis.PER_TOKEN,
+            self.quantized_v.append(QuantizedBlock(rec[i, code_b:code_b + code_n].tobytes(), GroupAxis.PER_TOKEN,
                                                    [QuantParams(float(vmn64[i, t]), float(vst64[i, t]), b)
                                                     for t in range(G)], G, d, b))
         cap = G + cfg.residual

@@ -331,6 +331,186 @@ __global__ void __launch_bounds__(kAttnThreads) attend_simt_kernel(AttnArgs a) {
   simt_body<NR, D>(a, n, blockIdx.x, t_begin, t_end, blockIdx.y, sm);
 }
 
+// ============================================================ generic shapes
+// Any head_dim in [1, 128] and group size in [1, 128] (the reference's own tests use
+// d in {2..16} and G in {4, 8, 16}): a 32-token tile may span several groups, so every
+// token looks up its own group record. Same tile order and split/combine structure as
+// the SIMT kernel; this path is for shape coverage, not speed.
+template <int NR>
+struct GenericSmem {
+  float qs[NR][kMaxD];  // q * scale_log2
+  float p[kAttnWarps][NR][32];
+  float m[kAttnWarps][NR], l[kAttnWarps][NR];
+  float acc[kAttnWarps][NR][kMaxD];
+};
+
+template <int NR>
+__global__ void __launch_bounds__(kAttnThreads) attend_generic_kernel(AttnArgs a) {
+  extern __shared__ __align__(256) unsigned char smem_raw[];
+  allow_dependents();
+  GenericSmem<NR>& sm = *reinterpret_cast<GenericSmem<NR>*>(smem_raw);
+  const Counts n = counts_of(a);
+  const ott_cache_t& c = a.c;
+  const int D = c.head_dim, G = c.group_size, N = c.capacity, cap = G + c.residual, bits = c.bits;
+  const RecordLayout L(D, G, bits);
+  const int u = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nq = (int)((n.q_tokens + 31) / 32), np = (N + 31) / 32;
+  const int nr = (int)((n.total_tokens - n.q_tokens + 31) / 32);
+  const int n_tiles = nq + np + nr;
+  const int per = (n_tiles + a.n_splits - 1) / a.n_splits;
+  const int t_begin = blockIdx.y * per, t_end = min(n_tiles, t_begin + per);
+  const uint32_t* pmask = c.pool_mask + (size_t)u * mask_words_per_unit(c);
+
+  for (int i = tid; i < NR * D; i += kAttnThreads)
+    sm.qs[i / D][i % D] = h2f(a.q[((size_t)u * NR) * D + i]) * a.scale_log2;
+  __syncthreads();
+
+  float m[NR], l[NR], acc[NR][kMaxD / 32];
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    m[r] = -INFINITY;
+    l[r] = 0.f;
+#pragma unroll
+    for (int k = 0; k < kMaxD / 32; ++k) acc[r][k] = 0.f;
+  }
+  for (int t = t_begin + warp; t < t_end; t += kAttnWarps) {
+    // logits of this lane's token
+    float s[NR];
+    const uint16_t* vrow = nullptr;  // fp tiers: the token's V row
+    bool valid;
+    if (t < nq) {
+      const int64_t p = (int64_t)t * 32 + lane;
+      valid = p < n.q_tokens && !((pmask[p >> 5] >> (p & 31)) & 1u);  // pooled: attended from the pool
+      if (valid) {
+        const int64_t gi = p / G;
+        const int row = (int)(p - gi * G);
+        const uint8_t* rec = record_ptr(c, u, gi);
+#pragma unroll
+        for (int r = 0; r < NR; ++r) s[r] = 0.f;
+        for (int col = 0; col < D; ++col) {
+          const float st = k_step_of(rec, L, col);
+          const float kv = fmaf((float)code_at(rec + L.k_codes(), (int64_t)row * D + col, bits), st,
+                                k_xmin_of(rec, L, col, st));
+#pragma unroll
+          for (int r = 0; r < NR; ++r) s[r] = fmaf(kv, sm.qs[r][col], s[r]);
+        }
+      }
+    } else {
+      const uint16_t* krow;
+      if (t < nq + np) {
+        const int slot = (t - nq) * 32 + lane;
+        valid = slot < N && c.pool_pos[(size_t)u * N + slot] >= 0;
+        const size_t off = ((size_t)u * N + (valid ? slot : 0)) * D;
+        krow = c.pool_k + off;
+        vrow = c.pool_v + off;
+      } else {
+        const int64_t p = n.q_tokens + (int64_t)(t - nq - np) * 32 + lane;
+        valid = p < n.total_tokens;
+        const size_t off = ((size_t)u * cap + (size_t)((valid ? p : n.q_tokens) % cap)) * D;
+        krow = c.pend_k + off;
+        vrow = c.pend_v + off;
+      }
+      if (valid) {
+#pragma unroll
+        for (int r = 0; r < NR; ++r) s[r] = 0.f;
+        for (int col = 0; col < D; ++col) {
+          const float kv = h2f(krow[col]);
+#pragma unroll
+          for (int r = 0; r < NR; ++r) s[r] = fmaf(kv, sm.qs[r][col], s[r]);
+        }
+      }
+    }
+    if (!valid) {
+#pragma unroll
+      for (int r = 0; r < NR; ++r) s[r] = -INFINITY;
+    }
+    // online softmax over the tile
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const float m_new = fmaxf(m[r], warp_max(s[r]));
+      float pr = 0.f;
+      if (m_new != -INFINITY) {
+        const float corr = exp2f(m[r] - m_new);
+        pr = exp2f(s[r] - m_new);
+        l[r] = l[r] * corr + warp_sum(pr);
+        m[r] = m_new;
+#pragma unroll
+        for (int k = 0; k < kMaxD / 32; ++k) acc[r][k] *= corr;
+      }
+      sm.p[warp][r][lane] = pr;
+    }
+    __syncwarp();
+    // O += p V, lanes over channels
+    for (int tt = 0; tt < 32; ++tt) {
+      if (!__shfl_sync(0xffffffffu, valid ? 1 : 0, tt)) continue;
+      if (t < nq) {
+        const int64_t p = (int64_t)t * 32 + tt;
+        const int64_t gi = p / G;
+        const int row = (int)(p - gi * G);
+        const uint8_t* rec = record_ptr(c, u, gi);
+        const float st = reinterpret_cast<const float*>(rec + L.v_step())[row];
+        const float mn = reinterpret_cast<const float*>(rec + L.v_xmin())[row];
+#pragma unroll
+        for (int k = 0; k < kMaxD / 32; ++k) {
+          const int col = lane + 32 * k;
+          if (col < D) {
+            const float v = fmaf((float)code_at(rec + L.v_codes(), (int64_t)row * D + col, bits), st, mn);
+#pragma unroll
+            for (int r = 0; r < NR; ++r) acc[r][k] = fmaf(sm.p[warp][r][tt], v, acc[r][k]);
+          }
+        }
+      } else {
+        const uint16_t* vr =
+            reinterpret_cast<const uint16_t*>(__shfl_sync(0xffffffffu, (unsigned long long)vrow, tt));
+#pragma unroll
+        for (int k = 0; k < kMaxD / 32; ++k) {
+          const int col = lane + 32 * k;
+          if (col < D) {
+            const float v = h2f(vr[col]);
+#pragma unroll
+            for (int r = 0; r < NR; ++r) acc[r][k] = fmaf(sm.p[warp][r][tt], v, acc[r][k]);
+          }
+        }
+      }
+    }
+    __syncwarp();
+  }
+  // merge the warps, write partial blockIdx.y ([D + 2] floats per (unit, head, split))
+  if (lane == 0) {
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      sm.m[warp][r] = m[r];
+      sm.l[warp][r] = l[r];
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < NR; ++r)
+#pragma unroll
+    for (int k = 0; k < kMaxD / 32; ++k) sm.acc[warp][r][lane + 32 * k] = acc[r][k];
+  __syncthreads();
+  for (int i = tid; i < NR * D; i += kAttnThreads) {
+    const int r = i / D, col = i % D;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < kAttnWarps; ++w) M = fmaxf(M, sm.m[w][r]);
+    float Lsum = 0.f, A = 0.f;
+    if (M != -INFINITY) {
+#pragma unroll
+      for (int w = 0; w < kAttnWarps; ++w) {
+        const float f = exp2f(sm.m[w][r] - M);
+        Lsum += sm.l[w][r] * f;
+        A += sm.acc[w][r][col] * f;
+      }
+    }
+    float* base = a.ws + (((size_t)u * NR + r) * a.n_splits + blockIdx.y) * (D + 2);
+    base[2 + col] = A;
+    if (col == 0) {
+      base[0] = M;
+      base[1] = Lsum;
+    }
+  }
+}
+
 // ============================================================ tensor-core path
 __device__ __forceinline__ void mma16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
                                          uint32_t b0, uint32_t b1) {
@@ -451,6 +631,9 @@ struct MmaSmem {
 #endif
 #ifndef OTT_NG
 #define OTT_NG 1  // groups per loop iteration per warp (2 measured slower: register spills)
+#endif
+#ifndef OTT_QK_LO  // 1: Q.K^T also multiplies the lo halves of q' (2 HMMA per k-step)
+#define OTT_QK_LO 1
 #endif
 #ifndef OTT_STAGES
 #define OTT_STAGES 3  // 3 measured 2 % faster than 2 on config 4 (v7)
@@ -588,6 +771,11 @@ __device__ void mma_body(const AttnArgs& a, const Counts& n, const CUtensorMap* 
 #pragma unroll
       for (int mt = 0; mt < kMt; ++mt) ch[j][mt][0] = ch[j][mt][1] = ch[j][mt][2] = ch[j][mt][3] = 0.f;
     }
+#if !OTT_QK_LO
+    __half2 lo_acc[NG][2];
+#pragma unroll
+    for (int j = 0; j < NG; ++j) lo_acc[j][0] = lo_acc[j][1] = __float2half2_rn(0.f);
+#endif
 #pragma unroll
     for (int hw = 0; hw < 2; ++hw) {
 #pragma unroll
@@ -607,7 +795,11 @@ __device__ void mma_body(const AttnArgs& a, const Counts& n, const CUtensorMap* 
           const __half2 H = __hmul2(q16[hw][m], sh);
           const __half2 E = __hfma2(q16[hw][m], sh, __hneg2(H));
           bh[m] = h2_as_u32(H);
+#if OTT_QK_LO
           bl[m] = h2_as_u32(__hfma2(q16[hw][m], sl, E));
+#else
+          lo_acc[j][m & 1] = __hadd2(lo_acc[j][m & 1], __hfma2(q16[hw][m], sl, E));
+#endif
         }
         Shifted s0[kMt], s1[kMt];
 #pragma unroll
@@ -621,13 +813,23 @@ __device__ void mma_body(const AttnArgs& a, const Counts& n, const CUtensorMap* 
       const uint32_t a0 = kq<MM>(s0[mt], magic), a1 = kq<MM>(s1[mt], magic);         \
       const uint32_t a2 = kq<MM + 1>(s0[mt], magic), a3 = kq<MM + 1>(s1[mt], magic); \
       mma16816(ch[j][mt], a0, a1, a2, a3, bh[MM], bh[MM + 1]);                        \
-      mma16816(ch[j][mt], a0, a1, a2, a3, bl[MM], bl[MM + 1]);                        \
+      if (OTT_QK_LO) mma16816(ch[j][mt], a0, a1, a2, a3, bl[MM], bl[MM + 1]);         \
     }                                                                                 \
   }
         OTT_QK(0) OTT_QK(2) OTT_QK(4) OTT_QK(6)
 #undef OTT_QK
       }
     }
+#if !OTT_QK_LO
+    // Q.K^T used only the hi halves: ch = sum (q' - lo) (1 + c 2^(2P-10)). The bias takes
+    // back sum lo (the offset part, 4u/c times larger than the code part), leaving
+    // -sum lo c 2^(2P-10): the rounding error of q' step c in fp16, 2^-12 relative per term.
+#pragma unroll
+    for (int j = 0; j < NG; ++j) {
+      const float2 lf = __half22float2(__hadd2(lo_acc[j][0], lo_acc[j][1]));
+      bias_g[j] = fmaf(4.f, lf.x + lf.y, bias_g[j]);
+    }
+#endif
     float sc[NG][kMt][4];
 #pragma unroll
     for (int j = 0; j < NG; ++j) {
@@ -1481,7 +1683,7 @@ template <int D>
 __global__ void __launch_bounds__(32 * kCombineRows) combine_kernel(const float* __restrict__ ws,
                                                                    uint16_t* __restrict__ out, int n_rows,
                                                                    int n_splits, int64_t* __restrict__ dev_counts,
-                                                                   int G, int R, int max_groups) {
+                                                                   int G, int R, int max_groups, int d) {
 #if OTT_PDL
   asm volatile("griddepcontrol.wait;\n" ::: "memory");  // the attention grid's partials are complete
 #endif
@@ -1493,11 +1695,30 @@ __global__ void __launch_bounds__(32 * kCombineRows) combine_kernel(const float*
     dev_counts[1] = tot;
   }
   if (ur >= n_rows) return;
+  if constexpr (D == 0) {  // generic head_dim: lane-strided columns
+    const float* base = ws + (size_t)ur * n_splits * (d + 2);
+    float M = -INFINITY;
+    for (int s = 0; s < n_splits; ++s) M = fmaxf(M, base[(size_t)s * (d + 2)]);
+    float Lsum = 0.f, acc[kMaxD / 32] = {0.f, 0.f, 0.f, 0.f};
+    for (int s = 0; s < n_splits; ++s) {
+      const float* p = base + (size_t)s * (d + 2);
+      if (p[0] == -INFINITY) continue;
+      const float f = exp2f(p[0] - M);
+      Lsum += p[1] * f;
+#pragma unroll
+      for (int k = 0; k < kMaxD / 32; ++k)
+        if (lane + 32 * k < d) acc[k] = fmaf(p[2 + lane + 32 * k], f, acc[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < kMaxD / 32; ++k)
+      if (lane + 32 * k < d) out[(size_t)ur * d + lane + 32 * k] = f2h(acc[k] / Lsum);
+    return;
+  }
   const float* base = ws + (size_t)ur * n_splits * (D + 2);
   float M = -INFINITY;
   for (int s = 0; s < n_splits; ++s) M = fmaxf(M, base[(size_t)s * (D + 2)]);
   float Lsum = 0.f;
-  float2 acc[D / 64];
+  float2 acc[D > 0 ? D / 64 : 1];
 #pragma unroll
   for (int k = 0; k < D / 64; ++k) acc[k] = make_float2(0.f, 0.f);
   for (int s = 0; s < n_splits; ++s) {
@@ -1533,18 +1754,20 @@ static cudaError_t launch_combine(const AttnArgs& a, int NR, cudaStream_t st) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, combine_kernel<D>, (const float*)a.ws, a.out, a.c.n_units * NR, a.n_splits,
-                            const_cast<int64_t*>(a.dev_counts), a.c.group_size, a.c.residual, a.c.max_groups);
+                            const_cast<int64_t*>(a.dev_counts), a.c.group_size, a.c.residual, a.c.max_groups,
+                            a.c.head_dim);
 }
 
-template <int D>
+template <int DT>  // 0: runtime head_dim (debug path; k lives in local memory then)
 __global__ void logits_kernel(ott_cache_t c, const uint16_t* __restrict__ q, float* __restrict__ logits, int NR,
                               int64_t q_tokens, int64_t total, float inv_sqrt_d) {
+  const int D = DT ? DT : c.head_dim;
   const int u = blockIdx.y;
   const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= total) return;
   const int G = c.group_size, N = c.capacity, cap = G + c.residual;
   const RecordLayout L(D, G, c.bits);
-  float k[D];
+  float k[DT ? DT : kMaxD];
   bool done = false;
   if (p < q_tokens) {
     const uint32_t* pmask = c.pool_mask + (size_t)u * mask_words_per_unit(c);
@@ -1586,6 +1809,18 @@ static cudaError_t launch_simt_t(const AttnArgs& a, cudaStream_t st) {
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   return launch_combine<D>(a, NR, st);
+}
+
+template <int NR>
+static cudaError_t launch_generic_t(const AttnArgs& a, cudaStream_t st) {
+  const size_t smem = sizeof(GenericSmem<NR>);
+  cudaError_t e = cudaFuncSetAttribute(attend_generic_kernel<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  attend_generic_kernel<NR><<<dim3(a.c.n_units, a.n_splits), kAttnThreads, smem, st>>>(a);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  return launch_combine<0>(a, NR, st);
 }
 
 // Tensor map over all block records of the cache: 2-D uint8 view [rows of 32 B],
@@ -1682,6 +1917,13 @@ cudaError_t launch_attend(const ott_cache_t& c, const uint16_t* q, uint16_t* out
   a.scale_log2 = kLog2e / sqrtf((float)c.head_dim);
   a.k_magic = 0x3C003C00u;
   const int D = c.head_dim, G = c.group_size;
+  if ((D != 64 && D != 128) || G % 32) {  // shapes outside the fast kernels' tiling
+    if (n_rep == 1) return launch_generic_t<1>(a, st);
+    if (n_rep == 2) return launch_generic_t<2>(a, st);
+    if (n_rep == 4) return launch_generic_t<4>(a, st);
+    if (n_rep == 8) return launch_generic_t<8>(a, st);
+    return cudaErrorInvalidValue;
+  }
   if (c.bits != 2) {  // other widths: CUDA-core kernel with generic code extraction
 #define OTT_BCASE(NRv, Dv) \
   if (n_rep == NRv && D == Dv) return launch_simt_t<NRv, Dv>(a, st);
@@ -1719,7 +1961,7 @@ cudaError_t launch_logits(const ott_cache_t& c, const uint16_t* q, float* logits
   const float inv = 1.0f / sqrtf((float)c.head_dim);
   if (c.head_dim == 128) logits_kernel<128><<<grid, 128, 0, st>>>(c, q, logits, n_rep, q_tokens, total, inv);
   else if (c.head_dim == 64) logits_kernel<64><<<grid, 128, 0, st>>>(c, q, logits, n_rep, q_tokens, total, inv);
-  else return cudaErrorInvalidValue;
+  else logits_kernel<0><<<grid, 128, 0, st>>>(c, q, logits, n_rep, q_tokens, total, inv);
   return cudaGetLastError();
 }
 

@@ -36,9 +36,11 @@ static int cuda_status(cudaError_t e) {
 static int check_cache(const ott_cache_t* c) {
   if (!c) return fail(OTT_ERR_CONTRACT, "null cache");
   if (c->bits < 1 || c->bits > 8) return fail(OTT_ERR_CONTRACT, "bits must be in [1, 8]");
-  if (c->head_dim != 64 && c->head_dim != 128) return fail(OTT_ERR_UNSUPPORTED, "head_dim must be 64 or 128");
-  if (c->group_size < 32 || c->group_size > ott::kMaxG || c->group_size % 32)
-    return fail(OTT_ERR_UNSUPPORTED, "group_size must be a multiple of 32 in [32, 128]");
+  // any shape in range runs; d = 128 / 2-bit / G % 32 == 0 takes the tensor-core kernels,
+  // d in {64, 128} with G % 32 == 0 the CUDA-core tile kernel, the rest the generic kernel
+  if (c->head_dim < 1 || c->head_dim > ott::kMaxD) return fail(OTT_ERR_UNSUPPORTED, "head_dim must be in [1, 128]");
+  if (c->group_size < 1 || c->group_size > ott::kMaxG)
+    return fail(OTT_ERR_UNSUPPORTED, "group_size must be in [1, 128]");
   if (c->residual < 0 || c->capacity < 0 || c->aux_capacity < 0)
     return fail(OTT_ERR_CONTRACT, "residual, outlier_num, aux_capacity must be >= 0");
   if (c->capacity > ott::kMaxN) return fail(OTT_ERR_UNSUPPORTED, "outlier_num must be <= 128");

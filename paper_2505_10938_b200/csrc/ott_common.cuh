@@ -18,7 +18,9 @@ constexpr int kMaxA = 1024;
 struct RecordLayout {
   int d, G, bits;
   __host__ __device__ RecordLayout(int d_, int G_, int bits_ = 2) : d(d_), G(G_), bits(bits_) {}
-  __host__ __device__ int code_bytes() const { return G * d * bits / 8; }  // packed codes (G*d % 8 == 0)
+  // packed codes: ceil(G d bits / 8) bytes (quant.py:237-238), padded to 16 so every
+  // field stays aligned (no padding at the tensor-core shapes d in {64, 128}, G % 32 == 0)
+  __host__ __device__ int code_bytes() const { return ((G * d * bits + 7) / 8 + 15) & ~15; }
   __host__ __device__ int k_codes() const { return 0; }
   __host__ __device__ int v_codes() const { return code_bytes(); }
   __host__ __device__ int k_sh() const { return 2 * code_bytes(); }  // fp16 [d], pair order
@@ -26,7 +28,7 @@ struct RecordLayout {
   __host__ __device__ int k_e() const { return k_sl() + 2 * d; }      // f32 [d], channel order
   __host__ __device__ int v_step() const { return k_e() + 4 * d; }
   __host__ __device__ int v_xmin() const { return v_step() + 4 * G; }
-  __host__ __device__ int bytes() const { return v_xmin() + 4 * G; }
+  __host__ __device__ int bytes() const { return (v_xmin() + 4 * G + 15) & ~15; }
 };
 
 // ---- K parameter encoding (tensor-core friendly; exact values live in params64).
@@ -39,10 +41,13 @@ struct RecordLayout {
 // Dequantisation of channel c: k = code * step + x_min = code * step + e + 4 u step.
 __host__ __device__ constexpr int kpair_pos(int m) { return m == 2 || m == 5 ? 2 : (m == 0 || m == 3 || m == 6 ? 3 : 4); }
 __host__ __device__ constexpr float kpair_u(int m) { return kpair_pos(m) == 2 ? 16.f : (kpair_pos(m) == 3 ? 4.f : 1.f); }
-__host__ __device__ constexpr int kpair_index(int c) { return 16 * (c / 16) + 2 * (c % 8) + (c % 16) / 8; }
+// (pair order only when d % 16 == 0, where the tensor-core kernels read it; identity otherwise)
+__host__ __device__ constexpr int kpair_index(int c, int d) {
+  return d % 16 ? c : 16 * (c / 16) + 2 * (c % 8) + (c % 16) / 8;
+}
 
 __host__ __device__ inline size_t mask_words_per_unit(const ott_cache_t& c) {
-  return (size_t)c.max_groups * c.group_size / 32;
+  return ((size_t)c.max_groups * c.group_size + 31) / 32;  // one bit per quantized position
 }
 
 __host__ __device__ inline uint8_t* record_ptr(const ott_cache_t& c, int unit, int64_t group) {
@@ -61,7 +66,7 @@ __device__ __forceinline__ uint32_t code_at(const uint8_t* codes, int64_t e, int
 }
 // float32 K step / x_min of channel c reconstructed from the record encoding
 __device__ __forceinline__ float k_step_of(const uint8_t* rec, const RecordLayout& L, int c) {
-  const int j = kpair_index(c);
+  const int j = kpair_index(c, L.d);
   return h2f(reinterpret_cast<const uint16_t*>(rec + L.k_sh())[j]) + h2f(reinterpret_cast<const uint16_t*>(rec + L.k_sl())[j]);
 }
 __device__ __forceinline__ float k_xmin_of(const uint8_t* rec, const RecordLayout& L, int c, float step) {

@@ -152,7 +152,9 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
       }                                                                 \
     }                                                                   \
   }
-  if (n_groups > 0) OTT_PREFETCH(q0)
+  // 8-half vector loads need rows of whole 16-byte chunks; other head dims gather per element
+  const bool vec = d % 8 == 0;
+  if (n_groups > 0 && vec) OTT_PREFETCH(q0)
 
   for (int g = 0; g < n_groups; ++g) {
     const int64_t base = q0 + (int64_t)g * G;
@@ -160,10 +162,18 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
     uint8_t* rec = record_ptr(c, u, gi);
 
     // ---- 1. gather the oldest G pending rows (cache.py:155-156), fp16 -> f32
+    if (!vec) {
+      for (int e = tid; e < G * d; e += kFlushThreads) {
+        const uint16_t *srck, *srcv;
+        OTT_ROW_SRC(base, e, srck, srcv)
+        sk[e] = h2f(*srck);
+        sv[e] = h2f(*srcv);
+      }
+    }
 #pragma unroll
     for (int it = 0; it < kPre; ++it) {
       const int e = tid * 8 + it * kFlushThreads * 8;
-      if (e < G * d) {
+      if (vec && e < G * d) {
         const uint16_t* kh = reinterpret_cast<const uint16_t*>(&pk8[it]);
         const uint16_t* vh = reinterpret_cast<const uint16_t*>(&pv8[it]);
 #pragma unroll
@@ -173,7 +183,7 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
         }
       }
     }
-    for (int e = tid * 8 + kPre * kFlushThreads * 8; e < G * d; e += kFlushThreads * 8) {
+    for (int e = tid * 8 + kPre * kFlushThreads * 8; vec && e < G * d; e += kFlushThreads * 8) {
       uint4 k8, v8;
       {
         const uint16_t *srck, *srcv;
@@ -189,7 +199,7 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
         sv[e + j] = h2f(vh[j]);
       }
     }
-    if (g + 1 < n_groups) OTT_PREFETCH(base + G)
+    if (g + 1 < n_groups && vec) OTT_PREFETCH(base + G)
     if (tid < G) sel[tid] = 0;
     if (tid == 0) sh.any_selected = 0;
     __syncthreads();
@@ -339,39 +349,43 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
       __syncthreads();
     }
 
-    // ---- 3. quantize: K per channel (threads [0,d)), V per token (remaining warps)
+    // ---- 3. quantize: K per channel (threads [0,d) of the first ceil(d/32) warps), V per
+    // token (the remaining warps; d <= 128 leaves at least 4)
+    const int kwarps = (d + 31) / 32;
     double* p64 = c.params64 ? c.params64 + ((size_t)u * c.max_groups + (size_t)gi) * 2 * (d + G) : nullptr;
     __half* ksh = reinterpret_cast<__half*>(rec + L.k_sh());
     __half* ksl = reinterpret_cast<__half*>(rec + L.k_sl());
     float* ke = reinterpret_cast<float*>(rec + L.k_e());
     float* vstep = reinterpret_cast<float*>(rec + L.v_step());
     float* vxmin = reinterpret_cast<float*>(rec + L.v_xmin());
-    if (tid < d) {
+    if (warp < kwarps) {
       const int col = tid;
-      float fmn = sk[col], fmx = fmn;
-      for (int i = 1; i < G; ++i) {
-        const float x = sk[i * d + col];
-        fmn = fminf(fmn, x);
-        fmx = fmaxf(fmx, x);
-      }
-      const double mn = (double)fmn, mx = (double)fmx;
-      double step;
-      line_params(mn, mx, (double)levels, step);
-      const double inv = step > 0.0 ? __drcp_rn(step) : 0.0;
-      for (int i = 0; i < G; ++i)
-        kc[i * d + col] = (uint8_t)quant_code((double)sk[i * d + col], mn, mx, step, inv, levels);
-      // decode-side encoding (ott_common.cuh): step = sh + sl, e = x_min - 4 u step
-      const __half sh = __double2half(step);
-      const __half sl = __double2half(__dsub_rn(step, (double)__half2float(sh)));
-      ksh[kpair_index(col)] = sh;
-      ksl[kpair_index(col)] = sl;
-      ke[col] = __double2float_rn(__dsub_rn(mn, __dmul_rn(4.0 * (double)kpair_u(col % 8), step)));
-      if (p64) {
-        p64[col] = mn;
-        p64[d + col] = step;
+      if (col < d) {
+        float fmn = sk[col], fmx = fmn;
+        for (int i = 1; i < G; ++i) {
+          const float x = sk[i * d + col];
+          fmn = fminf(fmn, x);
+          fmx = fmaxf(fmx, x);
+        }
+        const double mn = (double)fmn, mx = (double)fmx;
+        double step;
+        line_params(mn, mx, (double)levels, step);
+        const double inv = step > 0.0 ? __drcp_rn(step) : 0.0;
+        for (int i = 0; i < G; ++i)
+          kc[i * d + col] = (uint8_t)quant_code((double)sk[i * d + col], mn, mx, step, inv, levels);
+        // decode-side encoding (ott_common.cuh): step = sh + sl, e = x_min - 4 u step
+        const __half sh = __double2half(step);
+        const __half sl = __double2half(__dsub_rn(step, (double)__half2float(sh)));
+        ksh[kpair_index(col, d)] = sh;
+        ksl[kpair_index(col, d)] = sl;
+        ke[col] = __double2float_rn(__dsub_rn(mn, __dmul_rn(4.0 * (double)kpair_u(col % 8), step)));
+        if (p64) {
+          p64[col] = mn;
+          p64[d + col] = step;
+        }
       }
     } else {
-      const int vw = warp - d / 32, nvw = nwarps - d / 32;
+      const int vw = warp - kwarps, nvw = nwarps - kwarps;
       for (int i = vw; i < G; i += nvw) {
         // min/max of fp16-valued floats are exact in float32: reduce in float (1 shuffle per level)
         float fmn = 3.4e38f, fmx = -3.4e38f;
@@ -408,18 +422,19 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
       uint32_t* kw = reinterpret_cast<uint32_t*>(rec + L.k_codes());
       uint32_t* vw = reinterpret_cast<uint32_t*>(rec + L.v_codes());
       const int bits = c.bits;
-      const int n_words = G * d * bits / 32;
+      const int n_codes = G * d;
+      const int n_words = (n_codes * bits + 31) / 32;  // the tail of the last word stays 0
       for (int w = tid; w < 2 * n_words; w += kFlushThreads) {
         const bool isv = w >= n_words;
         const int ww = isv ? w - n_words : w;
         const uint8_t* src = isv ? vc : kc;
         uint32_t word = 0;
-        if (bits == 2) {
+        if (bits == 2 && ww * 16 + 16 <= n_codes) {
 #pragma unroll
           for (int j = 0; j < 16; ++j) word |= (uint32_t)src[ww * 16 + j] << (2 * j);
         } else {  // codes overlapping stream bits [32 ww, 32 ww + 32); some straddle words
           const int e0 = (32 * ww) / bits, e1 = (32 * ww + 31) / bits;
-          for (int e = e0; e <= e1; ++e) {
+          for (int e = e0; e <= e1 && e < n_codes; ++e) {
             const int sh = e * bits - 32 * ww;  // may be negative for the first code
             const uint64_t v = (uint64_t)src[e];
             word |= (uint32_t)(sh >= 0 ? (v << sh) : (v >> -sh));
@@ -449,6 +464,21 @@ __global__ void ring_write_kernel(ott_cache_t c, const uint16_t* __restrict__ k,
   }
   const int d = c.head_dim;
   const int cap = c.group_size + c.residual;
+  if (d % 8) {  // head dims that are not whole 16-byte chunks: one thread per element
+    const int64_t total = (int64_t)c.n_units * n_rows * d;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+      const int j = (int)(idx % d);
+      const int64_t r = (idx / d) % n_rows;
+      const int u = (int)(idx / ((int64_t)d * n_rows));
+      const int64_t p = first_pos + r;
+      const size_t src = (size_t)u * in_stride + (size_t)(p - in_first) * d + j;
+      const size_t dst = ((size_t)u * cap + (size_t)(p % cap)) * d + j;
+      c.pend_k[dst] = k[src];
+      c.pend_v[dst] = v[src];
+    }
+    return;
+  }
   const int vec_per_row = d / 8;
   const int64_t total = (int64_t)c.n_units * n_rows * vec_per_row;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
@@ -478,7 +508,7 @@ cudaError_t launch_flush(const ott_cache_t& c, int64_t q0, int n_groups, int64_t
 cudaError_t launch_ring_write(const ott_cache_t& c, const uint16_t* k, const uint16_t* v, int64_t in_stride,
                               int64_t in_first, int64_t first_pos, int64_t n_rows, cudaStream_t st,
                               const int64_t* dev_counts) {
-  const int64_t total = (int64_t)c.n_units * n_rows * (c.head_dim / 8);
+  const int64_t total = (int64_t)c.n_units * n_rows * (c.head_dim % 8 ? c.head_dim : c.head_dim / 8);
   int blocks = (int)((total + 255) / 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (blocks < 1) blocks = 1;
