@@ -438,17 +438,21 @@ class UnitView:
 
 class TieredCache:
     """Drop-in for ``kvtrace.TieredCache(config, layer, passthrough)`` (cache.py:90-203):
-    one (layer, head) cache with the reference's numpy row interface, backed by
-    a one-unit OTTCache on the GPU. Rows must be fp16-representable (the GPU
-    stores fp16, exactly as the reference's traces are fp16 in practice)."""
+    one (layer, head) cache with the reference's numpy row interface and attribute
+    names (quantized_k/v, pool, substituted_positions, pending_k/v, memory_usage),
+    backed by a one-unit OTTCache on the GPU. Rows must be fp16-representable (the
+    GPU stores fp16, as the reference's traces are fp16 in practice) unless
+    ``round_rows_to_fp16`` is set, which rounds them instead of raising."""
 
     def __init__(self, config: EngineConfig, layer: int = 0, passthrough: bool = False, max_tokens: int = 65536,
-                 device=None, keep_f64_params: bool = True):
+                 device=None, keep_f64_params: bool = True, round_rows_to_fp16: bool = False):
         if passthrough:
             raise ContractViolation("passthrough (lossless test fixture, quant.py:166-198) is not a GPU mode")
         self.config = config
         self.layer = layer
+        self.round_rows_to_fp16 = round_rows_to_fp16
         self._c = OTTCache(config, 1, 1, max_tokens, layer=layer, device=device, keep_f64_params=keep_f64_params)
+        self._snap = None
 
     def _row(self, x, name):
         a = np.asarray(x, dtype=np.float32)
@@ -458,12 +462,14 @@ class TieredCache:
         if not np.isfinite(a).all():
             raise ContractViolation("rows contain NaN or Inf")  # cache.py:131-132
         h = a.astype(np.float16)
-        if not np.array_equal(h.astype(np.float32), a):
+        if not self.round_rows_to_fp16 and not np.array_equal(h.astype(np.float32), a):
             raise ContractViolation(f"{name} row is not fp16-representable")
         return torch.from_numpy(h).to(self._c.device).view(1, 1, d)
 
     def append(self, k_row, v_row) -> None:
-        self._c.append(self._row(k_row, "key"), self._row(v_row, "value"))
+        k, v = self._row(k_row, "key"), self._row(v_row, "value")
+        self._snap = None
+        self._c.append(k, v)
 
     def extend(self, keys, values) -> None:
         """Bulk append (prefill), identical to appending row by row."""
@@ -475,16 +481,46 @@ class TieredCache:
         require(np.array_equal(kh.astype(np.float32), k) and np.array_equal(vh.astype(np.float32), v),
                 "rows are not fp16-representable")
         dev = self._c.device
+        self._snap = None
         self._c.update(torch.from_numpy(kh).to(dev)[None, None], torch.from_numpy(vh).to(dev)[None, None])
 
     def quantize_oldest_group(self) -> None:
+        self._snap = None
         self._c.quantize_oldest_group()
 
     def memory_usage(self) -> MemoryBreakdown:
         return self._c.memory_usage(0, 0)
 
     def snapshot(self) -> UnitView:
-        return self._c.unit(0, 0)
+        """Host copy of the unit's state (taken once per mutation, then reused)."""
+        if self._snap is None:
+            self._snap = self._c.unit(0, 0)
+        return self._snap
+
+    # the reference's state attributes (cache.py:93-122), read from the snapshot
+    @property
+    def quantized_k(self) -> list:
+        return self.snapshot().quantized_k
+
+    @property
+    def quantized_v(self) -> list:
+        return self.snapshot().quantized_v
+
+    @property
+    def pool(self) -> OutlierPoolView:
+        return self.snapshot().pool
+
+    @property
+    def substituted_positions(self) -> set:
+        return self.snapshot().substituted_positions
+
+    @property
+    def pending_k(self) -> np.ndarray:
+        return self.snapshot().pending_k
+
+    @property
+    def pending_v(self) -> np.ndarray:
+        return self.snapshot().pending_v
 
     @property
     def total_tokens(self) -> int:
@@ -503,9 +539,10 @@ class TieredCache:
         return self._c
 
 
-def attend_mixed(q, cache, with_weights: bool = False):
+def attend_mixed(q, cache, with_weights: bool = True):
     """attention.py:79-92. With a TieredCache (numpy interface) returns an
-    AttentionResult; with an OTTCache, q is fp16 [B, H_q, d] and the fp16
+    AttentionResult (weights and scores too, as the reference does, unless
+    with_weights=False); with an OTTCache, q is fp16 [B, H_q, d] and the fp16
     output tensor is returned."""
     if isinstance(cache, OTTCache):
         return cache.attend(q)
@@ -517,7 +554,7 @@ def attend_mixed(q, cache, with_weights: bool = False):
     if cache.total_tokens == 0:
         raise ContractViolation("cannot attend over an empty cache")
     qh = qa.astype(np.float16)
-    require(np.array_equal(qh.astype(np.float32), qa), "query is not fp16-representable")
+    require(cache.round_rows_to_fp16 or np.array_equal(qh.astype(np.float32), qa), "query is not fp16-representable")
     qt = torch.from_numpy(qh).to(cache.gpu.device).view(1, 1, d)
     out = cache.gpu.attend(qt)
     res = AttentionResult(output=out.float().cpu().numpy().reshape(d))
