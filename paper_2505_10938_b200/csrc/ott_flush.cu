@@ -25,28 +25,72 @@ __device__ __forceinline__ void line_params(double mn, double mx, double levels,
   step_out = step;
 }
 
-// inv = __drcp_rn(step). floor((x - mn) / step) of quant.py:93 is taken from the product
-// (x - mn) * inv when that lies more than 1e-9 (relative) from an integer: the product
-// and the correctly rounded quotient differ by < 4e-16 relative, so both floor to the
-// same integer; otherwise (exact lattice points, ties) the IEEE division decides.
-// x >= x_min for every element of the line, so the product is non-negative.
-__device__ __forceinline__ int quant_code(double x, double mn, double mx, double step, double inv, int levels) {
-  if (step == 0.0) return 0;  // quant.py:91-92
+// quant.py:91-102 for one element x (float32) of a line with x_min mn = (double)mnf,
+// x_max mxf, step and inv = __drcp_rn(step). The line-wide rules come first, so the
+// element equal to the max (quant.py:101) and the one equal to the min (code 0) never
+// reach the division. floor((x - mn) / step) of quant.py:93 is taken from the product
+// (x - mn) * inv when its fractional part lies more than eps = 1e-9 (levels + 1) from an
+// integer: the product and the correctly rounded quotient differ by < 4e-16 relative,
+// so both floor to the same integer; otherwise (exact lattice points, ties) the IEEE
+// division decides. x > mn here, so the product is positive.
+__device__ __forceinline__ int quant_code(float xf, float mnf, float mxf, double mn, double step, double inv,
+                                          int levels, double eps) {
+  if (step == 0.0) return 0;     // quant.py:91-92
+  if (xf == mxf) return levels;  // quant.py:101
+  if (xf == mnf) return 0;       // (x - mn) / step == 0; the check below keeps 0
+  const double x = (double)xf;
   const double dd = __dsub_rn(x, mn);
-  double f;
-  if (dd == 0.0) {
-    f = 0.0;
-  } else {
-    const double qa = __dmul_rn(dd, inv);
-    f = floor(qa);
-    const double t = __dsub_rn(qa, f);  // fractional part; qa >= 0 here (x >= x_min)
-    if (!(t > 1e-9 * fmax(1.0, qa) && t < 1.0 - 1e-9 * fmax(1.0, qa))) f = floor(__ddiv_rn(dd, step));
-  }
-  int c = f < 0.0 ? 0 : (f > (double)levels ? levels : (int)f);  // quant.py:94
+  const double qa = __dmul_rn(dd, inv);
+  double f = floor(qa);
+  const double t = __dsub_rn(qa, f);
+  if (!(t > eps && t < 1.0 - eps)) f = floor(__ddiv_rn(dd, step));
+  int c = min(__double2int_rz(f), levels);                     // quant.py:94 (f >= 0)
   if (__dadd_rn(__dmul_rn((double)c, step), mn) > x) c -= 1;  // quant.py:97
-  c = c < 0 ? 0 : c;                                          // quant.py:98
-  if (x == mx) c = levels;                                    // quant.py:101
-  return c;
+  return max(c, 0);                                            // quant.py:98
+}
+
+// Per-line constants of the float32 fast path. For x in (x_min, x_max) the quotient
+// q = (x - x_min) / step lies in (0, levels + 1); q32 = f32(f32(x - x_min) * f32(1/step)) is
+// within 3 * 2^-24 * q (< del / 2) of it. When frac(q32) lies in (del, 1 - del),
+// floor(q32) is the reference's floor of the float64 quotient, and when also
+// max(|x_min|, |x_max|) <= 1e8 * step the float64 check c * step + x_min > x
+// (quant.py:97) cannot fire (its rounding error is < 2^-51 * 1e8 * step < del / 2 * step),
+// so the element needs no float64 work. Other elements and lines take quant_code.
+struct FastLine {
+  float inv32, del;
+  bool ok;
+};
+__device__ __forceinline__ FastLine fast_line(float mnf, float mxf, double step, double inv, int levels) {
+  FastLine f;
+  f.ok = step >= 1e-30 && step <= 1e30 && fmaxf(fabsf(mnf), fabsf(mxf)) <= (float)(1e8 * step);
+  f.inv32 = (float)inv;
+  f.del = 4e-7f * (float)(levels + 1);
+  return f;
+}
+__device__ __forceinline__ int quant_code_fast(float xf, float mnf, float mxf, double mn, double step, double inv,
+                                               int levels, double eps, const FastLine& fl) {
+  if (fl.ok && xf != mxf && xf != mnf) {
+    const float q = __fmul_rn(__fsub_rn(xf, mnf), fl.inv32);
+    const float f = floorf(q), t = __fsub_rn(q, f);
+    if (t > fl.del && t < 1.f - fl.del) return min((int)f, levels);
+  }
+  return quant_code(xf, mnf, mxf, mn, step, inv, levels, eps);
+}
+
+// 8 fp16 -> 8 float32 in shared memory with two 16-byte stores (8 scalar stores at a
+// 32-byte lane stride would be 8-way bank conflicts)
+__device__ __forceinline__ void store8(float* dst, const uint4& h) {
+  const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&h.x));
+  const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&h.y));
+  const float2 c = __half22float2(*reinterpret_cast<const __half2*>(&h.z));
+  const float2 d = __half22float2(*reinterpret_cast<const __half2*>(&h.w));
+  reinterpret_cast<float4*>(dst)[0] = make_float4(a.x, a.y, b.x, b.y);
+  reinterpret_cast<float4*>(dst)[1] = make_float4(c.x, c.y, d.x, d.y);
+}
+// 4 two-bit codes held one per byte (values <= 3) -> one byte, code j at bits 2j
+__device__ __forceinline__ uint32_t pack4x2(uint32_t w) {
+  w = (w | (w >> 6)) & 0x000F000Fu;
+  return (w | (w >> 12)) & 0xFFu;
 }
 
 struct FlushShared {
@@ -54,18 +98,18 @@ struct FlushShared {
   int n_evicted, n_win_cand;
 };
 
-// Dynamic smem layout (floats/doubles/bytes), sized on the host:
+// Dynamic smem layout, sized on the host (flush_smem_bytes):
 //   float  sk[G*d], sv[G*d]           group rows (substituted in place)
-//   double score[G]
+//   uint8  kc[G*d], vc[G*d]           codes (16-byte aligned when G*d % 16 == 0)
+//   double score[G]                   (8-byte aligned)
 //   double it_score[N+G]; int it_pos[N+G]; int it_rank[N+G]
-//   int    free_slot[N]; uint8 kc[G*d], vc[G*d]; uint8 sel[G]
+//   int    free_slot[N]; uint8 sel[G]
+__host__ __device__ inline size_t flush_score_offset(int d, int G) { return ((size_t)10 * G * d + 7) & ~(size_t)7; }
 __host__ __device__ inline size_t flush_smem_bytes(int d, int G, int N) {
-  size_t b = 0;
-  b += (size_t)2 * G * d * sizeof(float);
+  size_t b = flush_score_offset(d, G);
   b += (size_t)G * sizeof(double);
   b += (size_t)(N + G) * (sizeof(double) + 2 * sizeof(int));
   b += (size_t)(N > 0 ? N : 1) * sizeof(int);
-  b += (size_t)2 * G * d;
   b += (size_t)G;
   return (b + 15) & ~(size_t)15;
 }
@@ -89,18 +133,19 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
   const int cap = G + c.residual;
   const RecordLayout L(d, G, c.bits);
   const int levels = (1 << c.bits) - 1;
+  const double eps = 1e-9 * (double)(levels + 1);  // guard band of quant_code (qa <= levels + 1)
 
   extern __shared__ __align__(16) unsigned char smem[];
   float* sk = reinterpret_cast<float*>(smem);
   float* sv = sk + G * d;
-  double* score = reinterpret_cast<double*>(sv + G * d);
+  uint8_t* kc = reinterpret_cast<uint8_t*>(sv + G * d);
+  uint8_t* vc = kc + G * d;
+  double* score = reinterpret_cast<double*>(smem + flush_score_offset(d, G));
   double* it_score = score + G;
   int* it_pos = reinterpret_cast<int*>(it_score + N + G);
   int* it_rank = it_pos + N + G;
   int* free_slot = it_rank + N + G;
-  uint8_t* kc = reinterpret_cast<uint8_t*>(free_slot + (N > 0 ? N : 1));
-  uint8_t* vc = kc + G * d;
-  uint8_t* sel = vc + G * d;
+  uint8_t* sel = reinterpret_cast<uint8_t*>(free_slot + (N > 0 ? N : 1));
   __shared__ FlushShared sh;
 
   int32_t* meta = c.pool_meta + (size_t)u * 4;
@@ -174,13 +219,8 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
     for (int it = 0; it < kPre; ++it) {
       const int e = tid * 8 + it * kFlushThreads * 8;
       if (vec && e < G * d) {
-        const uint16_t* kh = reinterpret_cast<const uint16_t*>(&pk8[it]);
-        const uint16_t* vh = reinterpret_cast<const uint16_t*>(&pv8[it]);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          sk[e + j] = h2f(kh[j]);
-          sv[e + j] = h2f(vh[j]);
-        }
+        store8(sk + e, pk8[it]);
+        store8(sv + e, pv8[it]);
       }
     }
     for (int e = tid * 8 + kPre * kFlushThreads * 8; vec && e < G * d; e += kFlushThreads * 8) {
@@ -191,13 +231,8 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
         k8 = *reinterpret_cast<const uint4*>(srck);
         v8 = *reinterpret_cast<const uint4*>(srcv);
       }
-      const uint16_t* kh = reinterpret_cast<const uint16_t*>(&k8);
-      const uint16_t* vh = reinterpret_cast<const uint16_t*>(&v8);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        sk[e + j] = h2f(kh[j]);
-        sv[e + j] = h2f(vh[j]);
-      }
+      store8(sk + e, k8);
+      store8(sv + e, v8);
     }
     if (g + 1 < n_groups && vec) OTT_PREFETCH(base + G)
     if (tid < G) sel[tid] = 0;
@@ -371,8 +406,10 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
         double step;
         line_params(mn, mx, (double)levels, step);
         const double inv = step > 0.0 ? __drcp_rn(step) : 0.0;
+        const FastLine fl = fast_line(fmn, fmx, step, inv, levels);
+#pragma unroll 4
         for (int i = 0; i < G; ++i)
-          kc[i * d + col] = (uint8_t)quant_code((double)sk[i * d + col], mn, mx, step, inv, levels);
+          kc[i * d + col] = (uint8_t)quant_code_fast(sk[i * d + col], fmn, fmx, mn, step, inv, levels, eps, fl);
         // decode-side encoding (ott_common.cuh): step = sh + sl, e = x_min - 4 u step
         const __half sh = __double2half(step);
         const __half sl = __double2half(__dsub_rn(step, (double)__half2float(sh)));
@@ -403,8 +440,10 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
         double step;
         line_params(mn, mx, (double)levels, step);
         const double inv = step > 0.0 ? __drcp_rn(step) : 0.0;
+        const FastLine fl = fast_line(fmn, fmx, step, inv, levels);
+#pragma unroll 4
         for (int col = lane; col < d; col += 32)
-          vc[i * d + col] = (uint8_t)quant_code((double)sv[i * d + col], mn, mx, step, inv, levels);
+          vc[i * d + col] = (uint8_t)quant_code_fast(sv[i * d + col], fmn, fmx, mn, step, inv, levels, eps, fl);
         if (lane == 0) {
           vstep[i] = __double2float_rn(step);
           vxmin[i] = __double2float_rn(mn);
@@ -429,9 +468,9 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
         const int ww = isv ? w - n_words : w;
         const uint8_t* src = isv ? vc : kc;
         uint32_t word = 0;
-        if (bits == 2 && ww * 16 + 16 <= n_codes) {
-#pragma unroll
-          for (int j = 0; j < 16; ++j) word |= (uint32_t)src[ww * 16 + j] << (2 * j);
+        if (bits == 2 && ww * 16 + 16 <= n_codes && (n_codes & 15) == 0) {  // 16 codes from one 16-byte load
+          const uint4 b = *reinterpret_cast<const uint4*>(src + ww * 16);
+          word = pack4x2(b.x) | (pack4x2(b.y) << 8) | (pack4x2(b.z) << 16) | (pack4x2(b.w) << 24);
         } else {  // codes overlapping stream bits [32 ww, 32 ww + 32); some straddle words
           const int e0 = (32 * ww) / bits, e1 = (32 * ww + 31) / bits;
           for (int e = e0; e <= e1 && e < n_codes; ++e) {

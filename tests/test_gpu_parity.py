@@ -384,6 +384,46 @@ def test_unsupported_shapes_rejected():
         OTTCache(cfg_of(2, 32, 0, 200, 32, 128), 1, 1, 64)  # pool capacity > 128
 
 
+@pytest.mark.parametrize("bits", [2, 3, 1, 8])
+def test_flush_adversarial_lines_vs_oracle(bits):
+    """Quantization lines built to stress K1's float32 fast path and float64 fallback:
+    exact lattice points, ties with the max, fp16 subnormals, large offsets with small
+    ranges, constant and two-valued lines, mean-substituted rows. Bit-exact vs the oracle."""
+    from paper_2505_10938_b200 import OTTCache
+
+    d, G, T = 128, 32, 32 * 12 + 5
+    rng = np.random.default_rng(bits)
+    cols = []
+    for c in range(d):
+        kind = c % 8
+        if kind == 0:    # lattice: x_min + k * step exactly, step a power of two
+            col = rng.integers(-2, 2) + rng.integers(0, (1 << bits), size=T) * 0.25
+        elif kind == 1:  # fp16 subnormals
+            col = rng.integers(0, 40, size=T) * 2.0 ** -24
+        elif kind == 2:  # large offset, small range
+            col = 60000.0 + rng.integers(0, 7, size=T) * 32.0
+        elif kind == 3:  # constant
+            col = np.full(T, rng.standard_normal())
+        elif kind == 4:  # two values
+            col = rng.choice([-3.0, 5.5], size=T)
+        elif kind == 5:  # many ties at the max
+            col = np.minimum(rng.standard_normal(T), 0.5)
+        elif kind == 6:  # integers in a range that divides by levels
+            col = rng.integers(0, 3 * ((1 << bits) - 1) + 1, size=T).astype(np.float64)
+        else:            # plain normal
+            col = rng.standard_normal(T) * 15
+        cols.append(col)
+    k = np.stack(cols, 1).astype(np.float16)
+    v = np.stack(cols[::-1], 1).astype(np.float16)  # V lines = tokens, mixed kinds per row
+    v[:, ::3] = rng.integers(0, 4, size=(T, len(range(0, d, 3)))) * 0.5
+    k[::7, :8] = 0.0  # low-L1 tokens: pooled and mean-substituted (f32 means)
+    cache = OTTCache(cfg_of(bits, G, 64, 4, 6, d), 1, 1, max_tokens=T, keep_f64_params=True)
+    cache.update(torch.from_numpy(k[None, None]).cuda(), torch.from_numpy(v[None, None]).cuda())
+    ref = oracle.OracleCache(bits, G, 64, 4, 6, d)
+    ref.extend(k.astype(np.float32), v.astype(np.float32))
+    assert_unit_matches_oracle(cache.unit(0, 0), ref)
+
+
 # --------------------------------------------------------------------------- generic shapes
 
 
