@@ -67,14 +67,16 @@ __device__ __forceinline__ FastLine fast_line(float mnf, float mxf, double step,
   f.del = 4e-7f * (float)(levels + 1);
   return f;
 }
-__device__ __forceinline__ int quant_code_fast(float xf, float mnf, float mxf, double mn, double step, double inv,
-                                               int levels, double eps, const FastLine& fl) {
-  if (fl.ok && xf != mxf && xf != mnf) {
-    const float q = __fmul_rn(__fsub_rn(xf, mnf), fl.inv32);
-    const float f = floorf(q), t = __fsub_rn(q, f);
-    if (t > fl.del && t < 1.f - fl.del) return min((int)f, levels);
-  }
-  return quant_code(xf, mnf, mxf, mn, step, inv, levels, eps);
+// Branch-free float32 code of x; `slow` marks elements that need quant_code (line not
+// eligible, or frac(q32) inside the guard band). x == x_min gives q32 = 0 and code 0
+// exactly (f32 x - x_min is 0 only for equal values); x == x_max is the max rule.
+__device__ __forceinline__ int quant_code_f32(float xf, float mnf, float mxf, int levels, const FastLine& fl,
+                                              bool& slow) {
+  const float q = __fmul_rn(__fsub_rn(xf, mnf), fl.inv32);
+  const float f = floorf(q), t = __fsub_rn(q, f);
+  const bool is_max = xf == mxf;
+  slow = !fl.ok || (!(t > fl.del && t < 1.f - fl.del) && q != 0.f && !is_max);
+  return is_max ? levels : min(__float2int_rz(f), levels);
 }
 
 // 8 fp16 -> 8 float32 in shared memory with two 16-byte stores (8 scalar stores at a
@@ -408,8 +410,13 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
         const double inv = step > 0.0 ? __drcp_rn(step) : 0.0;
         const FastLine fl = fast_line(fmn, fmx, step, inv, levels);
 #pragma unroll 4
-        for (int i = 0; i < G; ++i)
-          kc[i * d + col] = (uint8_t)quant_code_fast(sk[i * d + col], fmn, fmx, mn, step, inv, levels, eps, fl);
+        for (int i = 0; i < G; ++i) {
+          const float x = sk[i * d + col];
+          bool slow;
+          int code = quant_code_f32(x, fmn, fmx, levels, fl, slow);
+          if (slow) code = quant_code(x, fmn, fmx, mn, step, inv, levels, eps);
+          kc[i * d + col] = (uint8_t)code;
+        }
         // decode-side encoding (ott_common.cuh): step = sh + sl, e = x_min - 4 u step
         const __half sh = __double2half(step);
         const __half sl = __double2half(__dsub_rn(step, (double)__half2float(sh)));
@@ -442,8 +449,13 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
         const double inv = step > 0.0 ? __drcp_rn(step) : 0.0;
         const FastLine fl = fast_line(fmn, fmx, step, inv, levels);
 #pragma unroll 4
-        for (int col = lane; col < d; col += 32)
-          vc[i * d + col] = (uint8_t)quant_code_fast(sv[i * d + col], fmn, fmx, mn, step, inv, levels, eps, fl);
+        for (int col = lane; col < d; col += 32) {
+          const float x = sv[i * d + col];
+          bool slow;
+          int code = quant_code_f32(x, fmn, fmx, levels, fl, slow);
+          if (slow) code = quant_code(x, fmn, fmx, mn, step, inv, levels, eps);
+          vc[i * d + col] = (uint8_t)code;
+        }
         if (lane == 0) {
           vstep[i] = __double2float_rn(step);
           vxmin[i] = __double2float_rn(mn);
