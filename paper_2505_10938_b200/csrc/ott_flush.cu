@@ -170,30 +170,41 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
   __syncthreads();
 
   // the first kPre row loads of the next group are issued into registers before the
-  // current group is processed, so their global latency overlaps its compute
+  // current group is processed, so their global latency overlaps its compute. Positions
+  // fit in int32 (checked by ott_flush); a row's ring slot is (base % cap + row) with one
+  // conditional subtraction, since row < G <= cap.
   constexpr int kPre = 2;
   uint4 pk8[kPre], pv8[kPre];
-#define OTT_ROW_SRC(BASE, E, SK, SV)                                               \
-  {                                                                                \
-    const int i_ = (E) / d, col_ = (E) % d;                                        \
-    const int64_t p_ = (BASE) + i_;                                                \
-    if (p_ < ring_end) {                                                           \
-      const size_t off_ = ((size_t)u * cap + (size_t)(p_ % cap)) * d + col_;        \
-      SK = c.pend_k + off_;                                                        \
-      SV = c.pend_v + off_;                                                        \
-    } else {                                                                       \
-      const size_t off_ = (size_t)u * in_stride + (size_t)(p_ - in_first) * d + col_; \
-      SK = in_k + off_;                                                            \
-      SV = in_v + off_;                                                            \
-    }                                                                              \
+  const int ring_end32 = (int)ring_end, in_first32 = (int)in_first;
+#define OTT_ROW_SRC(BASE, BSLOT, ROW, COL, SK, SV)                                     \
+  {                                                                                    \
+    const int p_ = (BASE) + (ROW);                                                     \
+    if (p_ < ring_end32) {                                                             \
+      int s_ = (BSLOT) + (ROW);                                                        \
+      s_ = s_ >= cap ? s_ - cap : s_;                                                  \
+      const size_t off_ = ((size_t)u * cap + (size_t)s_) * d + (COL);                  \
+      SK = c.pend_k + off_;                                                            \
+      SV = c.pend_v + off_;                                                            \
+    } else {                                                                           \
+      const size_t off_ = (size_t)u * in_stride + (size_t)(p_ - in_first32) * d + (COL); \
+      SK = in_k + off_;                                                                \
+      SV = in_v + off_;                                                                \
+    }                                                                                  \
+  }
+  int prow[kPre], pcol[kPre];  // this thread's (row, column) of prefetch slot it
+#pragma unroll
+  for (int it = 0; it < kPre; ++it) {
+    const int e = tid * 8 + it * kFlushThreads * 8;
+    prow[it] = e / d;
+    pcol[it] = e % d;
   }
 #define OTT_PREFETCH(BASE)                                              \
   {                                                                     \
+    const int b_ = (int)(BASE), bs_ = b_ % cap;                         \
     _Pragma("unroll") for (int it = 0; it < kPre; ++it) {               \
-      const int e_ = tid * 8 + it * kFlushThreads * 8;                  \
-      if (e_ < G * d) {                                                 \
+      if (tid * 8 + it * kFlushThreads * 8 < G * d) {                   \
         const uint16_t *sk_, *sv_;                                      \
-        OTT_ROW_SRC(BASE, e_, sk_, sv_)                                 \
+        OTT_ROW_SRC(b_, bs_, prow[it], pcol[it], sk_, sv_)              \
         pk8[it] = *reinterpret_cast<const uint4*>(sk_);                 \
         pv8[it] = *reinterpret_cast<const uint4*>(sv_);                 \
       }                                                                 \
@@ -207,12 +218,13 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
     const int64_t base = q0 + (int64_t)g * G;
     const int64_t gi = base / G;
     uint8_t* rec = record_ptr(c, u, gi);
+    const int base32 = (int)base, bslot = base32 % cap;
 
     // ---- 1. gather the oldest G pending rows (cache.py:155-156), fp16 -> f32
     if (!vec) {
       for (int e = tid; e < G * d; e += kFlushThreads) {
         const uint16_t *srck, *srcv;
-        OTT_ROW_SRC(base, e, srck, srcv)
+        OTT_ROW_SRC(base32, bslot, e / d, e % d, srck, srcv)
         sk[e] = h2f(*srck);
         sv[e] = h2f(*srcv);
       }
@@ -229,7 +241,7 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
       uint4 k8, v8;
       {
         const uint16_t *srck, *srcv;
-        OTT_ROW_SRC(base, e, srck, srcv)
+        OTT_ROW_SRC(base32, bslot, e / d, e % d, srck, srcv)
         k8 = *reinterpret_cast<const uint4*>(srck);
         v8 = *reinterpret_cast<const uint4*>(srcv);
       }
@@ -429,8 +441,13 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
         }
       }
     } else {
+      // warp vw owns tokens vw + j nvw (j < 32 since G <= 128 and nvw >= 4): the warp reduces
+      // each token's min/max, lane j keeps token j's and derives its line parameters (one
+      // float64 division per lane instead of one per token), then the warp quantizes
       const int vw = warp - kwarps, nvw = nwarps - kwarps;
-      for (int i = vw; i < G; i += nvw) {
+      float my_mn = 0.f, my_mx = 0.f;
+      int n_my = 0;
+      for (int i = vw; i < G; i += nvw, ++n_my) {
         // min/max of fp16-valued floats are exact in float32: reduce in float (1 shuffle per level)
         float fmn = 3.4e38f, fmx = -3.4e38f;
         for (int col = lane; col < d; col += 32) {
@@ -443,26 +460,44 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
           fmn = fminf(fmn, __shfl_xor_sync(0xffffffffu, fmn, o));
           fmx = fmaxf(fmx, __shfl_xor_sync(0xffffffffu, fmx, o));
         }
-        const double mn = (double)fmn, mx = (double)fmx;
-        double step;
-        line_params(mn, mx, (double)levels, step);
-        const double inv = step > 0.0 ? __drcp_rn(step) : 0.0;
-        const FastLine fl = fast_line(fmn, fmx, step, inv, levels);
+        if (lane == n_my) {
+          my_mn = fmn;
+          my_mx = fmx;
+        }
+      }
+      double my_step = 0.0, my_inv = 0.0;
+      FastLine my_fl;
+      my_fl.ok = false;
+      my_fl.inv32 = 0.f;
+      my_fl.del = 0.f;
+      if (lane < n_my) {
+        const int i = vw + lane * nvw;
+        const double mn = (double)my_mn;
+        line_params(mn, (double)my_mx, (double)levels, my_step);
+        my_inv = my_step > 0.0 ? __drcp_rn(my_step) : 0.0;
+        my_fl = fast_line(my_mn, my_mx, my_step, my_inv, levels);
+        vstep[i] = __double2float_rn(my_step);
+        vxmin[i] = __double2float_rn(mn);
+        if (p64) {
+          p64[2 * d + i] = mn;
+          p64[2 * d + G + i] = my_step;
+        }
+      }
+      for (int j = 0; j < n_my; ++j) {
+        const int i = vw + j * nvw;
+        const float fmn = __shfl_sync(0xffffffffu, my_mn, j), fmx = __shfl_sync(0xffffffffu, my_mx, j);
+        const double step = __shfl_sync(0xffffffffu, my_step, j), inv = __shfl_sync(0xffffffffu, my_inv, j);
+        FastLine fl;
+        fl.inv32 = __shfl_sync(0xffffffffu, my_fl.inv32, j);
+        fl.ok = __shfl_sync(0xffffffffu, (int)my_fl.ok, j) != 0;
+        fl.del = 4e-7f * (float)(levels + 1);
 #pragma unroll 4
         for (int col = lane; col < d; col += 32) {
           const float x = sv[i * d + col];
           bool slow;
           int code = quant_code_f32(x, fmn, fmx, levels, fl, slow);
-          if (slow) code = quant_code(x, fmn, fmx, mn, step, inv, levels, eps);
+          if (slow) code = quant_code(x, fmn, fmx, (double)fmn, step, inv, levels, eps);
           vc[i * d + col] = (uint8_t)code;
-        }
-        if (lane == 0) {
-          vstep[i] = __double2float_rn(step);
-          vxmin[i] = __double2float_rn(mn);
-          if (p64) {
-            p64[2 * d + i] = mn;
-            p64[2 * d + G + i] = step;
-          }
         }
       }
     }
