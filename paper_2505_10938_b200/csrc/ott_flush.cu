@@ -76,7 +76,9 @@ __device__ __forceinline__ int quant_code_f32(float xf, float mnf, float mxf, in
   const float f = floorf(q), t = __fsub_rn(q, f);
   const bool is_max = xf == mxf;
   slow = !fl.ok || (!(t > fl.del && t < 1.f - fl.del) && q != 0.f && !is_max);
-  return is_max ? levels : min(__float2int_rz(f), levels);
+  // f is an integer in [0, levels] when !slow (q < levels + 1 - del for x < x_max):
+  // f + 2^23 holds it in the low mantissa bits
+  return is_max ? levels : __float_as_int(__fadd_rn(f, 8388608.f)) - 0x4B000000;
 }
 
 // 8 fp16 -> 8 float32 in shared memory with two 16-byte stores (8 scalar stores at a
