@@ -11,6 +11,9 @@
 namespace ott {
 
 constexpr int kFlushThreads = 256;
+#ifndef OTT_FLUSH_SPLIT  // bulk flush = sequential kernel until the pool freezes + parallel frozen-pool kernel
+#define OTT_FLUSH_SPLIT 1
+#endif
 #ifndef OTT_FLUSH_MIN_BLOCKS
 #define OTT_FLUSH_MIN_BLOCKS 3  // <= 85 registers: 3 CTAs per SM for large unit counts
 #endif
@@ -67,6 +70,13 @@ __device__ __forceinline__ FastLine fast_line(float mnf, float mxf, double step,
   f.del = 4e-7f * (float)(levels + 1);
   return f;
 }
+// The rare float64 fallback as a call: inlined at every element of the unrolled loops it
+// would multiply the code size (instruction-cache misses)
+__device__ __noinline__ int quant_code_slow(float xf, float mnf, float mxf, double mn, double step, double inv,
+                                            int levels, double eps) {
+  return quant_code(xf, mnf, mxf, mn, step, inv, levels, eps);
+}
+
 // Branch-free float32 code of x; `slow` marks elements that need quant_code (line not
 // eligible, or frac(q32) inside the guard band). x == x_min gives q32 = 0 and code 0
 // exactly (f32 x - x_min is 0 only for equal values); x == x_max is the max rule.
@@ -122,7 +132,8 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
                                                               int64_t ring_end, const uint16_t* __restrict__ in_k,
                                                               const uint16_t* __restrict__ in_v,
                                                               int64_t in_stride, int64_t in_first,
-                                                              const int64_t* __restrict__ dev_counts) {
+                                                              const int64_t* __restrict__ dev_counts,
+                                                              bool stop_frozen) {
   if (dev_counts) {  // device-counter decode step: flush one group iff the append just made it due
     const int64_t qt = dev_counts[0], tot = dev_counts[1] + 1;
     if (tot - qt - c.residual < c.group_size || qt / c.group_size + 1 > c.max_groups) return;
@@ -216,7 +227,15 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
   const bool vec = d % 8 == 0;
   if (n_groups > 0 && vec) OTT_PREFETCH(q0)
 
+  int g_done = n_groups;
   for (int g = 0; g < n_groups; ++g) {
+    // stop_frozen: once the pool is frozen (or N = 0) the remaining groups are independent
+    // (cache.py:158 skips scoring, competition and substitution) and flush_frozen_kernel
+    // quantizes them in parallel
+    if (stop_frozen && !(N > 0 && !sh.frozen)) {
+      g_done = g;
+      break;
+    }
     const int64_t base = q0 + (int64_t)g * G;
     const int64_t gi = base / G;
     uint8_t* rec = record_ptr(c, u, gi);
@@ -428,7 +447,7 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
           const float x = sk[i * d + col];
           bool slow;
           int code = quant_code_f32(x, fmn, fmx, levels, fl, slow);
-          if (slow) code = quant_code(x, fmn, fmx, mn, step, inv, levels, eps);
+          if (slow) code = quant_code_slow(x, fmn, fmx, mn, step, inv, levels, eps);
           kc[i * d + col] = (uint8_t)code;
         }
         // decode-side encoding (ott_common.cuh): step = sh + sl, e = x_min - 4 u step
@@ -498,7 +517,7 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
           const float x = sv[i * d + col];
           bool slow;
           int code = quant_code_f32(x, fmn, fmx, levels, fl, slow);
-          if (slow) code = quant_code(x, fmn, fmx, (double)fmn, step, inv, levels, eps);
+          if (slow) code = quant_code_slow(x, fmn, fmx, (double)fmn, step, inv, levels, eps);
           vc[i * d + col] = (uint8_t)code;
         }
       }
@@ -539,6 +558,190 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
     meta[0] = sh.n_entries;
     meta[1] = sh.n_aux;
     meta[2] = sh.frozen;
+    meta[3] = g_done;  // groups of this launch done here (the rest by flush_frozen_kernel)
+  }
+}
+
+// K1b: groups flushed after the unit's pool froze (or N = 0): no scoring, competition or
+// substitution (cache.py:158), so every group is independent. One warp per group, no
+// block barriers; 2-bit, d = 128, G = 32 (the tensor-core decode shapes).
+//   * rows are staged in shared memory as fp16 with cp.async (V rows with their 16-byte
+//     chunks XOR-swizzled by the row, so a lane-per-token read is bank-conflict free);
+//   * K: lane l owns channels 4l..4l+3 (one code byte per token in pack_codes order),
+//   * V: lane t owns token t (its eight 16-code words are built in registers);
+//   * codes come from the same float32 fast path / float64 fallback as flush_kernel, so the
+//     results are bit-identical.
+constexpr int kFrozenWarps = 4;
+struct FrozenSmem {
+  uint16_t k[kFrozenWarps][32 * 128];
+  uint16_t v[kFrozenWarps][32 * 128];
+};
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gsrc) : "memory");
+}
+
+__global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen_kernel(ott_cache_t c, int64_t q0, int n_groups,
+                                                                         int64_t ring_end,
+                                                                         const uint16_t* __restrict__ in_k,
+                                                                         const uint16_t* __restrict__ in_v,
+                                                                         int64_t in_stride, int64_t in_first) {
+  constexpr int D = 128, G = 32, kLevels = 3;
+  extern __shared__ __align__(16) unsigned char smem[];
+  FrozenSmem& sm = *reinterpret_cast<FrozenSmem*>(smem);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t item = (int64_t)blockIdx.x * kFrozenWarps + warp;
+  if (item >= (int64_t)c.n_units * n_groups) return;
+  const int u = (int)(item / n_groups), g = (int)(item % n_groups);
+  if (g < c.pool_meta[(size_t)u * 4 + 3]) return;  // done by flush_kernel (pool still active)
+  const int cap = G + c.residual;
+  const int base = (int)(q0 + (int64_t)g * G);
+  const int64_t gi = base / G;
+  uint8_t* rec = record_ptr(c, u, gi);
+  const RecordLayout L(D, G, 2);
+  uint16_t* sk = sm.k[warp];
+  uint16_t* sv = sm.v[warp];
+
+  // ---- stage the G rows (cache.py:155-156): lane = 16-byte chunk (lane & 15) of row pairs
+  {
+    const int bslot = base % cap, ring_end32 = (int)ring_end, in_first32 = (int)in_first;
+    const int ch = lane & 15;
+#pragma unroll 4
+    for (int it = 0; it < G / 2; ++it) {
+      const int row = 2 * it + (lane >> 4);
+      const int p = base + row;
+      const uint16_t *pk, *pv;
+      if (p < ring_end32) {
+        int sl = bslot + row;
+        sl = sl >= cap ? sl - cap : sl;
+        const size_t off = ((size_t)u * cap + (size_t)sl) * D + ch * 8;
+        pk = c.pend_k + off;
+        pv = c.pend_v + off;
+      } else {
+        const size_t off = (size_t)u * in_stride + (size_t)(p - in_first32) * D + ch * 8;
+        pk = in_k + off;
+        pv = in_v + off;
+      }
+      cp_async16(sk + row * D + ch * 8, pk);
+      cp_async16(sv + row * D + ((ch ^ (row & 15)) * 8), pv);
+    }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    __syncwarp();
+  }
+  double* p64 = c.params64 ? c.params64 + ((size_t)u * c.max_groups + (size_t)gi) * 2 * (D + G) : nullptr;
+  const double eps = 1e-9 * (double)(kLevels + 1);
+
+  // ---- K: channels 4 lane .. 4 lane + 3, lines over the G tokens
+  {
+    __half2 mn01 = __float2half2_rn(65504.f), mn23 = mn01, mx01 = __float2half2_rn(-65504.f), mx23 = mx01;
+    const uint2* kr = reinterpret_cast<const uint2*>(sk) + lane;  // row stride D / 4 uint2
+#pragma unroll 8
+    for (int t = 0; t < G; ++t) {
+      const uint2 r = kr[t * (D / 4)];
+      const __half2 a = *reinterpret_cast<const __half2*>(&r.x), b = *reinterpret_cast<const __half2*>(&r.y);
+      mn01 = __hmin2(mn01, a);
+      mx01 = __hmax2(mx01, a);
+      mn23 = __hmin2(mn23, b);
+      mx23 = __hmax2(mx23, b);
+    }
+    float fmn[4], fmx[4];
+    {
+      const float2 a = __half22float2(mn01), b = __half22float2(mn23), x = __half22float2(mx01),
+                   y = __half22float2(mx23);
+      fmn[0] = a.x; fmn[1] = a.y; fmn[2] = b.x; fmn[3] = b.y;
+      fmx[0] = x.x; fmx[1] = x.y; fmx[2] = y.x; fmx[3] = y.y;
+    }
+    double step[4], inv[4];
+    FastLine fl[4];
+    __half* ksh = reinterpret_cast<__half*>(rec + L.k_sh());
+    __half* ksl = reinterpret_cast<__half*>(rec + L.k_sl());
+    float ke[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int col = 4 * lane + j;
+      const double mn = (double)fmn[j];
+      line_params(mn, (double)fmx[j], (double)kLevels, step[j]);
+      inv[j] = step[j] > 0.0 ? __drcp_rn(step[j]) : 0.0;
+      fl[j] = fast_line(fmn[j], fmx[j], step[j], inv[j], kLevels);
+      const __half sh = __double2half(step[j]);
+      const __half sl = __double2half(__dsub_rn(step[j], (double)__half2float(sh)));
+      ksh[kpair_index(col, D)] = sh;
+      ksl[kpair_index(col, D)] = sl;
+      ke[j] = __double2float_rn(__dsub_rn(mn, __dmul_rn(4.0 * (double)kpair_u(col % 8), step[j])));
+      if (p64) {
+        p64[col] = mn;
+        p64[D + col] = step[j];
+      }
+    }
+    *reinterpret_cast<float4*>(rec + L.k_e() + 16 * lane) = make_float4(ke[0], ke[1], ke[2], ke[3]);
+    uint8_t* kcodes = rec + L.k_codes() + lane;  // byte (t d + 4 lane) / 4 holds channels 4 lane..+3 of token t
+#pragma unroll 4
+    for (int t = 0; t < G; ++t) {
+      const uint2 r = kr[t * (D / 4)];
+      const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&r.x));
+      const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&r.y));
+      const float x[4] = {a.x, a.y, b.x, b.y};
+      uint32_t byte = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        bool slow;
+        int code = quant_code_f32(x[j], fmn[j], fmx[j], kLevels, fl[j], slow);
+        if (slow) code = quant_code_slow(x[j], fmn[j], fmx[j], (double)fmn[j], step[j], inv[j], kLevels, eps);
+        byte |= (uint32_t)code << (2 * j);
+      }
+      kcodes[t * (D / 4)] = (uint8_t)byte;
+    }
+  }
+
+  // ---- V: token `lane`, line over the D channels (chunk j of the row at (j ^ (lane & 15)))
+  {
+    const int t = lane;
+    const uint4* vr = reinterpret_cast<const uint4*>(sv + t * D);
+    const int sw = t & 15;
+    __half2 mn2 = __float2half2_rn(65504.f), mx2 = __float2half2_rn(-65504.f);
+#pragma unroll 4
+    for (int j = 0; j < D / 8; ++j) {
+      const uint4 r = vr[j ^ sw];
+      const __half2* h = reinterpret_cast<const __half2*>(&r);
+      mn2 = __hmin2(__hmin2(mn2, h[0]), __hmin2(h[1], __hmin2(h[2], h[3])));
+      mx2 = __hmax2(__hmax2(mx2, h[0]), __hmax2(h[1], __hmax2(h[2], h[3])));
+    }
+    const float fmn = fminf(__low2float(mn2), __high2float(mn2));
+    const float fmx = fmaxf(__low2float(mx2), __high2float(mx2));
+    const double mn = (double)fmn;
+    double step;
+    line_params(mn, (double)fmx, (double)kLevels, step);
+    const double inv = step > 0.0 ? __drcp_rn(step) : 0.0;
+    const FastLine fl = fast_line(fmn, fmx, step, inv, kLevels);
+    reinterpret_cast<float*>(rec + L.v_step())[t] = __double2float_rn(step);
+    reinterpret_cast<float*>(rec + L.v_xmin())[t] = __double2float_rn(mn);
+    if (p64) {
+      p64[2 * D + t] = mn;
+      p64[2 * D + G + t] = step;
+    }
+    uint32_t w[D / 16];
+#pragma unroll
+    for (int j = 0; j < D / 8; ++j) {  // chunk j = channels 8j..8j+7 -> half of word j / 2
+      const uint4 r = vr[j ^ sw];
+      const __half2* h = reinterpret_cast<const __half2*>(&r);
+      uint32_t bits = 0;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = __half22float2(h[e]);
+        bool s0, s1;
+        int c0 = quant_code_f32(f.x, fmn, fmx, kLevels, fl, s0);
+        int c1 = quant_code_f32(f.y, fmn, fmx, kLevels, fl, s1);
+        if (s0) c0 = quant_code_slow(f.x, fmn, fmx, mn, step, inv, kLevels, eps);
+        if (s1) c1 = quant_code_slow(f.y, fmn, fmx, mn, step, inv, kLevels, eps);
+        bits |= ((uint32_t)c0 << (4 * e)) | ((uint32_t)c1 << (4 * e + 2));
+      }
+      if (j & 1) w[j / 2] |= bits << 16;
+      else w[j / 2] = bits;
+    }
+    uint4* vcodes = reinterpret_cast<uint4*>(rec + L.v_codes() + t * (D / 4));
+    vcodes[0] = make_uint4(w[0], w[1], w[2], w[3]);
+    vcodes[1] = make_uint4(w[4], w[5], w[6], w[7]);
   }
 }
 
@@ -588,8 +791,19 @@ cudaError_t launch_flush(const ott_cache_t& c, int64_t q0, int n_groups, int64_t
   const size_t smem = flush_smem_bytes(c.head_dim, c.group_size, c.capacity);
   cudaError_t e = cudaFuncSetAttribute(flush_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
+  // bulk flushes at the tensor-core shapes: the sequential kernel stops where the pool froze
+  // and the frozen-pool kernel takes the rest of the groups in parallel
+  const bool split = OTT_FLUSH_SPLIT && !dev_counts && n_groups > 1 && c.bits == 2 && c.head_dim == 128 &&
+                     c.group_size == 32;
   flush_kernel<<<c.n_units, kFlushThreads, smem, st>>>(c, q0, n_groups, ring_end, in_k, in_v, in_stride, in_first,
-                                                         dev_counts);
+                                                         dev_counts, split);
+  e = cudaGetLastError();
+  if (e != cudaSuccess || !split) return e;
+  e = cudaFuncSetAttribute(flush_frozen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FrozenSmem));
+  if (e != cudaSuccess) return e;
+  const int64_t items = (int64_t)c.n_units * n_groups;
+  flush_frozen_kernel<<<(unsigned)((items + kFrozenWarps - 1) / kFrozenWarps), 32 * kFrozenWarps, sizeof(FrozenSmem),
+                        st>>>(c, q0, n_groups, ring_end, in_k, in_v, in_stride, in_first);
   return cudaGetLastError();
 }
 
