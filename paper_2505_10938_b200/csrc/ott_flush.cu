@@ -571,6 +571,60 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
 //   * V: lane t owns token t (its eight 16-code words are built in registers);
 //   * codes come from the same float32 fast path / float64 fallback as flush_kernel, so the
 //     results are bit-identical.
+// fp16 neighbours (finite values; -0 and +0 are one value)
+__device__ __forceinline__ uint16_t h_next(uint16_t b) {
+  return b == 0x8000u || b == 0x0000u ? (uint16_t)0x0001u : ((b & 0x8000u) ? (uint16_t)(b - 1) : (uint16_t)(b + 1));
+}
+__device__ __forceinline__ uint16_t h_prev(uint16_t b) {
+  return b == 0x8000u || b == 0x0000u ? (uint16_t)0x8001u : ((b & 0x8000u) ? (uint16_t)(b + 1) : (uint16_t)(b - 1));
+}
+__device__ __forceinline__ double h_val(uint16_t b) { return (double)__half2float(__ushort_as_half(b)); }
+
+// Code thresholds of one line over fp16 inputs: t[k-1] = the smallest fp16 value x of the
+// line's range with code(x) >= k (quant.py:91-102 incl. the max rule), so that
+// code(x) = #{k : x >= t[k-1]} for every fp16 x in [x_min, x_max]. The code is monotone in x.
+// Away from T_k = x_min + k step (real), code(x) >= k <=> x >= T_k: the float64 rounding of
+// the quotient, the floor and the c step + x_min > x check can only flip within
+// 2^-50 (|x_min| + levels step) of some T_c, inside `margin`. So t = the fp16 ceiling of T_k,
+// except when an fp16 value lies within `margin` of T_k: that value is decided by the exact
+// recipe. Returns false (use quant_code per element) if fp16 values there are closer together
+// than 4 margin (a line spanning ~10^12 fp16 spacings).
+__device__ __forceinline__ bool code_thresholds(uint16_t* t, float mnf, float mxf, double mn, double step, double inv,
+                                                int levels, double eps) {
+  const uint16_t mxb = __half_as_ushort(__float2half_rn(mxf));  // x_max is an fp16 value
+  if (step == 0.0) {  // quant.py:91-92: every code 0 (no max rule)
+    for (int k = 0; k < levels; ++k) t[k] = 0x7C00u;  // +inf
+    return true;
+  }
+  const double margin = 1e-12 * (fabs(mn) + (double)levels * step);
+  bool ok = true;
+  for (int k = 1; k <= levels; ++k) {
+    const double T = __dadd_rn(mn, __dmul_rn((double)k, step));
+    uint16_t vb = __half_as_ushort(__float2half_ru(__double2float_ru(T)));  // smallest fp16 >= T (or +inf)
+    if ((vb & 0x7C00u) != 0x7C00u) {
+      const uint16_t ub = h_prev(vb), nb = h_next(vb);
+      const double dv = h_val(vb), du = h_val(ub);
+      if (h_val(nb) - dv <= 4.0 * margin || dv - du <= 4.0 * margin) ok = false;
+      if (dv - T <= margin && quant_code(__half2float(__ushort_as_half(vb)), mnf, mxf, mn, step, inv, levels, eps) < k)
+        vb = nb;
+      else if (T - du <= margin &&
+               quant_code(__half2float(__ushort_as_half(ub)), mnf, mxf, mn, step, inv, levels, eps) >= k)
+        vb = ub;
+    }
+    // x_max has code levels (quant.py:101): no threshold lies above it
+    if (h_val(vb) > (double)mxf || (vb & 0x7C00u) == 0x7C00u) vb = mxb;
+    t[k - 1] = vb;
+  }
+  return ok;
+}
+
+// codes of two fp16 inputs against per-lane thresholds th[0..2]: code at bits 0-1 (low half)
+// and 16-17 (high half). Each compare gives 1.0 or 0.0; 1024 + code is exact in fp16.
+__device__ __forceinline__ uint32_t codes_h2(__half2 x, const __half2* th) {
+  const __half2 c = __hadd2(__hadd2(__hge2(x, th[0]), __hge2(x, th[1])), __hadd2(__hge2(x, th[2]), __float2half2_rn(1024.f)));
+  return *reinterpret_cast<const uint32_t*>(&c) & 0x00030003u;
+}
+
 constexpr int kFrozenWarps = 4;
 struct FrozenSmem {
   uint16_t k[kFrozenWarps][32 * 128];
@@ -653,7 +707,8 @@ __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen_kernel(ott_cac
       fmx[0] = x.x; fmx[1] = x.y; fmx[2] = y.x; fmx[3] = y.y;
     }
     double step[4], inv[4];
-    FastLine fl[4];
+    uint16_t thr[4][kLevels];
+    bool exact = true;  // all four lines have exact fp16 thresholds
     __half* ksh = reinterpret_cast<__half*>(rec + L.k_sh());
     __half* ksl = reinterpret_cast<__half*>(rec + L.k_sl());
     float ke[4];
@@ -663,7 +718,7 @@ __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen_kernel(ott_cac
       const double mn = (double)fmn[j];
       line_params(mn, (double)fmx[j], (double)kLevels, step[j]);
       inv[j] = step[j] > 0.0 ? __drcp_rn(step[j]) : 0.0;
-      fl[j] = fast_line(fmn[j], fmx[j], step[j], inv[j], kLevels);
+      exact &= code_thresholds(thr[j], fmn[j], fmx[j], mn, step[j], inv[j], kLevels, eps);
       const __half sh = __double2half(step[j]);
       const __half sl = __double2half(__dsub_rn(step[j], (double)__half2float(sh)));
       ksh[kpair_index(col, D)] = sh;
@@ -676,21 +731,33 @@ __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen_kernel(ott_cac
     }
     *reinterpret_cast<float4*>(rec + L.k_e() + 16 * lane) = make_float4(ke[0], ke[1], ke[2], ke[3]);
     uint8_t* kcodes = rec + L.k_codes() + lane;  // byte (t d + 4 lane) / 4 holds channels 4 lane..+3 of token t
-#pragma unroll 4
-    for (int t = 0; t < G; ++t) {
-      const uint2 r = kr[t * (D / 4)];
-      const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&r.x));
-      const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&r.y));
-      const float x[4] = {a.x, a.y, b.x, b.y};
-      uint32_t byte = 0;
+    if (exact) {
+      __half2 t01[kLevels], t23[kLevels];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        bool slow;
-        int code = quant_code_f32(x[j], fmn[j], fmx[j], kLevels, fl[j], slow);
-        if (slow) code = quant_code_slow(x[j], fmn[j], fmx[j], (double)fmn[j], step[j], inv[j], kLevels, eps);
-        byte |= (uint32_t)code << (2 * j);
+      for (int k = 0; k < kLevels; ++k) {
+        t01[k] = __halves2half2(__ushort_as_half(thr[0][k]), __ushort_as_half(thr[1][k]));
+        t23[k] = __halves2half2(__ushort_as_half(thr[2][k]), __ushort_as_half(thr[3][k]));
       }
-      kcodes[t * (D / 4)] = (uint8_t)byte;
+#pragma unroll 4
+      for (int t = 0; t < G; ++t) {
+        const uint2 r = kr[t * (D / 4)];
+        const uint32_t c01 = codes_h2(*reinterpret_cast<const __half2*>(&r.x), t01);
+        const uint32_t c23 = codes_h2(*reinterpret_cast<const __half2*>(&r.y), t23);
+        kcodes[t * (D / 4)] = (uint8_t)(((c01 | (c01 >> 14)) & 0xFu) | (((c23 | (c23 >> 14)) & 0xFu) << 4));
+      }
+    } else {  // a line without exact thresholds (extreme range): the float64 recipe per element
+      for (int t = 0; t < G; ++t) {
+        const uint2 r = kr[t * (D / 4)];
+        const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&r.x));
+        const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&r.y));
+        const float x[4] = {a.x, a.y, b.x, b.y};
+        uint32_t byte = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          byte |= (uint32_t)quant_code_slow(x[j], fmn[j], fmx[j], (double)fmn[j], step[j], inv[j], kLevels, eps)
+                  << (2 * j);
+        kcodes[t * (D / 4)] = (uint8_t)byte;
+      }
     }
   }
 
@@ -713,28 +780,36 @@ __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen_kernel(ott_cac
     double step;
     line_params(mn, (double)fmx, (double)kLevels, step);
     const double inv = step > 0.0 ? __drcp_rn(step) : 0.0;
-    const FastLine fl = fast_line(fmn, fmx, step, inv, kLevels);
+    uint16_t thr[kLevels];
+    const bool exact = code_thresholds(thr, fmn, fmx, mn, step, inv, kLevels, eps);
     reinterpret_cast<float*>(rec + L.v_step())[t] = __double2float_rn(step);
     reinterpret_cast<float*>(rec + L.v_xmin())[t] = __double2float_rn(mn);
     if (p64) {
       p64[2 * D + t] = mn;
       p64[2 * D + G + t] = step;
     }
+    __half2 th[kLevels];
+#pragma unroll
+    for (int k = 0; k < kLevels; ++k) th[k] = __half2half2(__ushort_as_half(thr[k]));
     uint32_t w[D / 16];
 #pragma unroll
     for (int j = 0; j < D / 8; ++j) {  // chunk j = channels 8j..8j+7 -> half of word j / 2
       const uint4 r = vr[j ^ sw];
       const __half2* h = reinterpret_cast<const __half2*>(&r);
       uint32_t bits = 0;
+      if (exact) {
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float2 f = __half22float2(h[e]);
-        bool s0, s1;
-        int c0 = quant_code_f32(f.x, fmn, fmx, kLevels, fl, s0);
-        int c1 = quant_code_f32(f.y, fmn, fmx, kLevels, fl, s1);
-        if (s0) c0 = quant_code_slow(f.x, fmn, fmx, mn, step, inv, kLevels, eps);
-        if (s1) c1 = quant_code_slow(f.y, fmn, fmx, mn, step, inv, kLevels, eps);
-        bits |= ((uint32_t)c0 << (4 * e)) | ((uint32_t)c1 << (4 * e + 2));
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t cc = codes_h2(h[e], th);
+          bits |= ((cc | (cc >> 14)) & 0xFu) << (4 * e);
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __half22float2(h[e]);
+          bits |= ((uint32_t)quant_code_slow(f.x, fmn, fmx, mn, step, inv, kLevels, eps) << (4 * e)) |
+                  ((uint32_t)quant_code_slow(f.y, fmn, fmx, mn, step, inv, kLevels, eps) << (4 * e + 2));
+        }
       }
       if (j & 1) w[j / 2] |= bits << 16;
       else w[j / 2] = bits;

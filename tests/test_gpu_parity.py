@@ -384,15 +384,17 @@ def test_unsupported_shapes_rejected():
         OTTCache(cfg_of(2, 32, 0, 200, 32, 128), 1, 1, 64)  # pool capacity > 128
 
 
-@pytest.mark.parametrize("bits", [2, 3, 1, 8])
-def test_flush_adversarial_lines_vs_oracle(bits):
-    """Quantization lines built to stress K1's float32 fast path and float64 fallback:
-    exact lattice points, ties with the max, fp16 subnormals, large offsets with small
-    ranges, constant and two-valued lines, mean-substituted rows. Bit-exact vs the oracle."""
+@pytest.mark.parametrize("bits,N", [(2, 4), (3, 4), (1, 4), (8, 4), (2, 0)])
+def test_flush_adversarial_lines_vs_oracle(bits, N):
+    """Quantization lines built to stress K1's float32 fast path and float64 fallback and the
+    frozen-pool kernel's fp16 code thresholds (N = 0: every group takes flush_frozen_kernel):
+    exact lattice points, ties with the max, fp16 subnormals, large offsets with small ranges,
+    lines spanning -60000..subnormals, signed zeros, constant and two-valued lines,
+    mean-substituted rows. Bit-exact vs the oracle."""
     from paper_2505_10938_b200 import OTTCache
 
     d, G, T = 128, 32, 32 * 12 + 5
-    rng = np.random.default_rng(bits)
+    rng = np.random.default_rng(bits + 10 * N)
     cols = []
     for c in range(d):
         kind = c % 8
@@ -410,6 +412,10 @@ def test_flush_adversarial_lines_vs_oracle(bits):
             col = np.minimum(rng.standard_normal(T), 0.5)
         elif kind == 6:  # integers in a range that divides by levels
             col = rng.integers(0, 3 * ((1 << bits) - 1) + 1, size=T).astype(np.float64)
+        elif c % 16 == 15:  # a code threshold at 0: fp16 subnormals closer than the margin
+            col = rng.choice([-60000.0, 30000.0, 0.0, -0.0, 2.0 ** -24, -2.0 ** -24, 5 * 2.0 ** -24], size=T)
+        elif c % 16 == 7:  # huge range with values near zero (threshold next to subnormals)
+            col = rng.choice([-60000.0, 0.0, -0.0, 2.0 ** -24, 3 * 2.0 ** -24, -2.0 ** -20, 1.0], size=T)
         else:            # plain normal
             col = rng.standard_normal(T) * 15
         cols.append(col)
@@ -417,9 +423,9 @@ def test_flush_adversarial_lines_vs_oracle(bits):
     v = np.stack(cols[::-1], 1).astype(np.float16)  # V lines = tokens, mixed kinds per row
     v[:, ::3] = rng.integers(0, 4, size=(T, len(range(0, d, 3)))) * 0.5
     k[::7, :8] = 0.0  # low-L1 tokens: pooled and mean-substituted (f32 means)
-    cache = OTTCache(cfg_of(bits, G, 64, 4, 6, d), 1, 1, max_tokens=T, keep_f64_params=True)
+    cache = OTTCache(cfg_of(bits, G, 64, N, 6, d), 1, 1, max_tokens=T, keep_f64_params=True)
     cache.update(torch.from_numpy(k[None, None]).cuda(), torch.from_numpy(v[None, None]).cuda())
-    ref = oracle.OracleCache(bits, G, 64, 4, 6, d)
+    ref = oracle.OracleCache(bits, G, 64, N, 6, d)
     ref.extend(k.astype(np.float32), v.astype(np.float32))
     assert_unit_matches_oracle(cache.unit(0, 0), ref)
 
