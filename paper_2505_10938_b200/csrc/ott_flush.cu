@@ -11,6 +11,9 @@
 namespace ott {
 
 constexpr int kFlushThreads = 256;
+#ifndef OTT_FROZEN_SEL  // timing experiment only when 0 (substituted groups quantized wrongly)
+#define OTT_FROZEN_SEL 1
+#endif
 #ifndef OTT_FLUSH_SPLIT  // bulk flush = sequential kernel until the pool freezes + parallel frozen-pool kernel
 #define OTT_FLUSH_SPLIT 1
 #endif
@@ -132,8 +135,7 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
                                                               int64_t ring_end, const uint16_t* __restrict__ in_k,
                                                               const uint16_t* __restrict__ in_v,
                                                               int64_t in_stride, int64_t in_first,
-                                                              const int64_t* __restrict__ dev_counts,
-                                                              bool stop_frozen) {
+                                                              const int64_t* __restrict__ dev_counts) {
   if (dev_counts) {  // device-counter decode step: flush one group iff the append just made it due
     const int64_t qt = dev_counts[0], tot = dev_counts[1] + 1;
     if (tot - qt - c.residual < c.group_size || qt / c.group_size + 1 > c.max_groups) return;
@@ -227,15 +229,7 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
   const bool vec = d % 8 == 0;
   if (n_groups > 0 && vec) OTT_PREFETCH(q0)
 
-  int g_done = n_groups;
   for (int g = 0; g < n_groups; ++g) {
-    // stop_frozen: once the pool is frozen (or N = 0) the remaining groups are independent
-    // (cache.py:158 skips scoring, competition and substitution) and flush_frozen_kernel
-    // quantizes them in parallel
-    if (stop_frozen && !(N > 0 && !sh.frozen)) {
-      g_done = g;
-      break;
-    }
     const int64_t base = q0 + (int64_t)g * G;
     const int64_t gi = base / G;
     uint8_t* rec = record_ptr(c, u, gi);
@@ -558,7 +552,6 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
     meta[0] = sh.n_entries;
     meta[1] = sh.n_aux;
     meta[2] = sh.frozen;
-    meta[3] = g_done;  // groups of this launch done here (the rest by flush_frozen_kernel)
   }
 }
 
@@ -571,6 +564,216 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
 //   * V: lane t owns token t (its eight 16-code words are built in registers);
 //   * codes come from the same float32 fast path / float64 fallback as flush_kernel, so the
 //     results are bit-identical.
+// 16-byte global -> shared copy without a register round trip
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gsrc) : "memory");
+}
+
+// K1a: the sequential part of a bulk flush (cache.py:158-173 for every group in order):
+// score_tokens, OutlierPool.update, the pool/aux rows and the pool/substitution bitmasks.
+// One warp per unit; lane t scores token t of each group; the competition is the same
+// rank-by-count as flush_kernel (outlier.py:84-117). Substitution and quantization are left
+// to flush_frozen_kernel (all groups in parallel). Stops when the pool freezes. d = 128,
+// G = 32, N <= 128.
+constexpr int kScanWarps = 2;
+constexpr int kScanStages = 4;  // K-row groups in flight per warp (cp.async ring)
+struct ScanSmem {
+  uint16_t rows[kScanWarps][kScanStages][32 * 128];  // chunk j of row t at (j ^ (t & 15))
+  int slot_pos[kScanWarps][kMaxN];
+  double slot_score[kScanWarps][kMaxN];
+  int it_pos[kScanWarps][kMaxN + 32];
+  double it_score[kScanWarps][kMaxN + 32];
+  int it_rank[kScanWarps][kMaxN + 32];
+  int free_slot[kScanWarps][kMaxN];
+};
+
+__global__ void __launch_bounds__(32 * kScanWarps) flush_scan_kernel(ott_cache_t c, int64_t q0, int n_groups,
+                                                                     int64_t ring_end, const uint16_t* __restrict__ in_k,
+                                                                     const uint16_t* __restrict__ in_v,
+                                                                     int64_t in_stride, int64_t in_first) {
+  constexpr int D = 128, G = 32;
+  extern __shared__ __align__(16) unsigned char smem[];
+  ScanSmem& sm = *reinterpret_cast<ScanSmem*>(smem);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int u = blockIdx.x * kScanWarps + warp;
+  if (u >= c.n_units) return;
+  const int N = c.capacity, A = c.aux_capacity, M = N + G;
+  const int cap = G + c.residual, ring_end32 = (int)ring_end, in_first32 = (int)in_first;
+  int32_t* meta = c.pool_meta + (size_t)u * 4;
+  int n_entries = meta[0], n_aux = meta[1], frozen = meta[2];
+  if (N == 0 || frozen) return;
+  int32_t* ppos = c.pool_pos + (size_t)u * N;
+  double* pscore = c.pool_score + (size_t)u * N;
+  uint16_t* pk = c.pool_k + (size_t)u * N * D;
+  uint16_t* pv = c.pool_v + (size_t)u * N * D;
+  int32_t* apos = c.aux_pos + (size_t)u * A;
+  double* ascore = c.aux_score + (size_t)u * A;
+  uint16_t* ak = c.aux_k + (size_t)u * A * D;
+  uint16_t* av = c.aux_v + (size_t)u * A * D;
+  uint32_t* pmask = c.pool_mask + (size_t)u * mask_words_per_unit(c);
+  uint32_t* smask = c.subst_mask + (size_t)u * mask_words_per_unit(c);
+  int* spos = sm.slot_pos[warp];
+  double* sscore = sm.slot_score[warp];
+  int* it_pos = sm.it_pos[warp];
+  double* it_score = sm.it_score[warp];
+  int* it_rank = sm.it_rank[warp];
+  int* free_slot = sm.free_slot[warp];
+  for (int s = lane; s < N; s += 32) {
+    spos[s] = ppos[s];
+    sscore[s] = pscore[s];
+  }
+  const int q0i = (int)q0;
+  const int bslot0 = q0i % cap;
+  auto row_of = [&](int p, const uint16_t* ring, const uint16_t* in) -> const uint16_t* {
+    if (p < ring_end32) {
+      int sl = bslot0 + (p - q0i) % cap;
+      sl = sl >= cap ? sl - cap : sl;
+      return ring + ((size_t)u * cap + (size_t)sl) * D;
+    }
+    return in + (size_t)u * in_stride + (size_t)(p - in_first32) * D;
+  };
+  // K rows of group g -> stage g % kScanStages (one cp.async group per load)
+  auto load_group = [&](int g) {
+    if (g < n_groups) {
+      uint16_t* dst = sm.rows[warp][g % kScanStages];
+      const int base = q0i + g * G, ch = lane & 15;
+#pragma unroll 4
+      for (int it = 0; it < G / 2; ++it) {
+        const int row = 2 * it + (lane >> 4);
+        cp_async16(dst + row * D + ((ch ^ (row & 15)) * 8), row_of(base + row, c.pend_k, in_k) + ch * 8);
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+#pragma unroll
+  for (int st = 0; st < kScanStages - 1; ++st) load_group(st);
+  __syncwarp();
+  for (int g = 0; g < n_groups && !frozen; ++g) {
+    const int base = q0i + g * G;
+    load_group(g + kScanStages - 1);
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(kScanStages - 1) : "memory");
+    __syncwarp();
+    const uint16_t* srow = sm.rows[warp][g % kScanStages];
+    // ---- score_tokens (outlier.py:45-49): L1 norm of key row `lane` in float64 (exact)
+    double sc;
+    {
+      const uint4* kr = reinterpret_cast<const uint4*>(srow + lane * D);
+      const int sw = lane & 15;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll 4
+      for (int j = 0; j < D / 8; ++j) {
+        const uint4 r = kr[j ^ sw];
+        const __half2* h = reinterpret_cast<const __half2*>(&r);
+        const float2 f0 = __half22float2(h[0]), f1 = __half22float2(h[1]), f2 = __half22float2(h[2]),
+                     f3 = __half22float2(h[3]);
+        a0 = __dadd_rn(a0, __dadd_rn(fabs((double)f0.x), fabs((double)f0.y)));
+        a1 = __dadd_rn(a1, __dadd_rn(fabs((double)f1.x), fabs((double)f1.y)));
+        a2 = __dadd_rn(a2, __dadd_rn(fabs((double)f2.x), fabs((double)f2.y)));
+        a3 = __dadd_rn(a3, __dadd_rn(fabs((double)f3.x), fabs((double)f3.y)));
+      }
+      sc = __dadd_rn(__dadd_rn(a0, a1), __dadd_rn(a2, a3));  // exact: fp16 magnitudes fit 2^-24..2^16
+    }
+    // ---- OutlierPool.update (outlier.py:84-117): items [0, N) slots, [N, N+G) candidates
+    for (int t = lane; t < N; t += 32) {
+      it_pos[t] = spos[t];
+      it_score[t] = sscore[t];
+    }
+    it_pos[N + lane] = base + lane;
+    it_score[N + lane] = sc;
+    __syncwarp();
+    for (int t = lane; t < M; t += 32) {
+      int r = -1;
+      if (it_pos[t] >= 0) {
+        const double s0 = it_score[t];
+        const int p0 = it_pos[t];
+        r = 0;
+        for (int j = 0; j < M; ++j) {
+          const int pj = it_pos[j];
+          if (pj < 0) continue;
+          const double sj = it_score[j];
+          r += (sj < s0 || (sj == s0 && pj < p0)) ? 1 : 0;  // _rank, outlier.py:52-54
+        }
+      }
+      it_rank[t] = r;
+    }
+    __syncwarp();
+    // evicted old entries -> aux in old-entry order (ascending rank); free slots ascending
+    const int room = A - n_aux;  // outlier.py:113-114
+    int n_ev = 0;
+    for (int s0 = 0; s0 < N; s0 += 32) {
+      const int s = s0 + lane;
+      const int r = s < N ? it_rank[s] : 0;
+      const bool evicted = s < N && r >= N;
+      const bool is_free = s < N && (r < 0 || r >= N);
+      n_ev += __popc(__ballot_sync(0xffffffffu, evicted));
+      if (is_free) {
+        int fidx = 0;
+        for (int q = 0; q < s; ++q) fidx += (it_rank[q] < 0 || it_rank[q] >= N) ? 1 : 0;
+        free_slot[fidx] = s;
+      }
+      if (evicted) {
+        int eidx = 0;
+        for (int q = 0; q < N; ++q) eidx += (it_rank[q] >= N && it_rank[q] < r) ? 1 : 0;
+        if (eidx < room) {
+          apos[n_aux + eidx] = it_pos[s];
+          ascore[n_aux + eidx] = it_score[s];
+        }
+        const int p = it_pos[s];
+        atomicAnd(&pmask[p >> 5], ~(1u << (p & 31)));  // back to its shadow row
+      }
+    }
+    __syncwarp();
+    // copy evicted rows into aux before their slots are reused (lanes 0-15 K, 16-31 V)
+    for (int s = 0; s < N; ++s) {
+      const int r = it_rank[s];
+      if (r < N) continue;
+      int eidx = 0;
+      for (int q = 0; q < N; ++q) eidx += (it_rank[q] >= N && it_rank[q] < r) ? 1 : 0;
+      if (eidx >= room) continue;
+      const int a = n_aux + eidx, j = lane & 15;
+      if (lane < 16) reinterpret_cast<uint4*>(ak + (size_t)a * D)[j] = reinterpret_cast<const uint4*>(pk + (size_t)s * D)[j];
+      else reinterpret_cast<uint4*>(av + (size_t)a * D)[j] = reinterpret_cast<const uint4*>(pv + (size_t)s * D)[j];
+    }
+    __syncwarp();
+    // winning candidates take the free slots in candidate order
+    const bool win = it_rank[N + lane] < N;
+    const uint32_t wins = __ballot_sync(0xffffffffu, win);
+    for (uint32_t wm = wins; wm; wm &= wm - 1) {
+      const int i = __ffs(wm) - 1;
+      const int widx = __popc(wins & ((1u << i) - 1u));
+      const int s = free_slot[widx];
+      const int p = base + i, j = lane & 15;
+      if (lane < 16) reinterpret_cast<uint4*>(pk + (size_t)s * D)[j] = reinterpret_cast<const uint4*>(srow + i * D)[j ^ (i & 15)];
+      else reinterpret_cast<uint4*>(pv + (size_t)s * D)[j] = reinterpret_cast<const uint4*>(row_of(p, c.pend_v, in_v))[j];
+      if (lane == 0) {
+        spos[s] = p;
+        sscore[s] = it_score[N + i];
+        atomicOr(&pmask[p >> 5], 1u << (p & 31));
+        atomicOr(&smask[p >> 5], 1u << (p & 31));  // cache.py:173
+      }
+    }
+    __syncwarp();
+    n_aux += n_ev < room ? n_ev : room;
+    int n_e = 0;
+    for (int t = lane; t < M; t += 32) n_e += (it_rank[t] >= 0 && it_rank[t] < N) ? 1 : 0;
+    n_entries = warp_sum(n_e);
+    if (n_aux >= A) frozen = 1;  // outlier.py:115-116
+    __syncwarp();  // stage g % kScanStages is reloaded next iteration
+  }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  __syncwarp();
+  for (int s = lane; s < N; s += 32) {
+    ppos[s] = spos[s];
+    pscore[s] = sscore[s];
+  }
+  if (lane == 0) {
+    meta[0] = n_entries;
+    meta[1] = n_aux;
+    meta[2] = frozen;
+  }
+}
+
 // fp16 neighbours (finite values; -0 and +0 are one value)
 __device__ __forceinline__ uint16_t h_next(uint16_t b) {
   return b == 0x8000u || b == 0x0000u ? (uint16_t)0x0001u : ((b & 0x8000u) ? (uint16_t)(b - 1) : (uint16_t)(b + 1));
@@ -582,15 +785,19 @@ __device__ __forceinline__ double h_val(uint16_t b) { return (double)__half2floa
 
 // Code thresholds of one line over fp16 inputs: t[k-1] = the smallest fp16 value x of the
 // line's range with code(x) >= k (quant.py:91-102 incl. the max rule), so that
-// code(x) = #{k : x >= t[k-1]} for every fp16 x in [x_min, x_max]. The code is monotone in x.
-// Away from T_k = x_min + k step (real), code(x) >= k <=> x >= T_k: the float64 rounding of
-// the quotient, the floor and the c step + x_min > x check can only flip within
-// 2^-50 (|x_min| + levels step) of some T_c, inside `margin`. So t = the fp16 ceiling of T_k,
-// except when an fp16 value lies within `margin` of T_k: that value is decided by the exact
-// recipe. Returns false (use quant_code per element) if fp16 values there are closer together
-// than 4 margin (a line spanning ~10^12 fp16 spacings).
+// code(x) = #{k : x >= t[k-1]} for every fp16 x in [x_min, x_max] (the code is monotone in x).
+// With T = fl(x_min + fl(k step)) -- exactly the left side of the quant.py:97 check for c = k:
+//   * x < T: code(x) < k (a code of k needs the check fl(k step + x_min) <= x to pass);
+//   * x >= T: code(x) >= k iff fl((x - x_min) / step) >= k, which holds whenever x - T exceeds
+//     margin = 1e-12 (|x_min| + levels step) (all float64 roundings involved are < 2^-50 of it).
+// So t = the fp16 ceiling v of T, except when v - T <= margin: then the float64 quotient at v
+// decides between v and the next fp16 value (false is returned, and quant_code is used per
+// element, if fp16 values there are closer than 4 margin). t[levels-1] = x_max: T_levels lies
+// within float64 rounding below x_max (line_params) and x_max has code levels (quant.py:101).
 __device__ __forceinline__ bool code_thresholds(uint16_t* t, float mnf, float mxf, double mn, double step, double inv,
                                                 int levels, double eps) {
+  (void)inv;
+  (void)eps;
   const uint16_t mxb = __half_as_ushort(__float2half_rn(mxf));  // x_max is an fp16 value
   if (step == 0.0) {  // quant.py:91-92: every code 0 (no max rule)
     for (int k = 0; k < levels; ++k) t[k] = 0x7C00u;  // +inf
@@ -598,23 +805,21 @@ __device__ __forceinline__ bool code_thresholds(uint16_t* t, float mnf, float mx
   }
   const double margin = 1e-12 * (fabs(mn) + (double)levels * step);
   bool ok = true;
-  for (int k = 1; k <= levels; ++k) {
+  for (int k = 1; k < levels; ++k) {
     const double T = __dadd_rn(mn, __dmul_rn((double)k, step));
     uint16_t vb = __half_as_ushort(__float2half_ru(__double2float_ru(T)));  // smallest fp16 >= T (or +inf)
     if ((vb & 0x7C00u) != 0x7C00u) {
-      const uint16_t ub = h_prev(vb), nb = h_next(vb);
-      const double dv = h_val(vb), du = h_val(ub);
-      if (h_val(nb) - dv <= 4.0 * margin || dv - du <= 4.0 * margin) ok = false;
-      if (dv - T <= margin && quant_code(__half2float(__ushort_as_half(vb)), mnf, mxf, mn, step, inv, levels, eps) < k)
-        vb = nb;
-      else if (T - du <= margin &&
-               quant_code(__half2float(__ushort_as_half(ub)), mnf, mxf, mn, step, inv, levels, eps) >= k)
-        vb = ub;
+      const double dv = h_val(vb);
+      if (dv - T <= margin) {
+        const uint16_t nb = h_next(vb);
+        if (h_val(nb) - dv <= 4.0 * margin) ok = false;
+        if (!(floor(__ddiv_rn(__dsub_rn(dv, mn), step)) >= (double)k)) vb = nb;
+      }
     }
-    // x_max has code levels (quant.py:101): no threshold lies above it
-    if (h_val(vb) > (double)mxf || (vb & 0x7C00u) == 0x7C00u) vb = mxb;
+    if ((vb & 0x7C00u) == 0x7C00u || h_val(vb) > (double)mxf) vb = mxb;
     t[k - 1] = vb;
   }
+  t[levels - 1] = mxb;
   return ok;
 }
 
@@ -629,12 +834,176 @@ constexpr int kFrozenWarps = 4;
 struct FrozenSmem {
   uint16_t k[kFrozenWarps][32 * 128];
   uint16_t v[kFrozenWarps][32 * 128];
+  float vmean[kFrozenWarps][128];  // V column means of a group with substituted rows
 };
 
-__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
-  const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gsrc) : "memory");
+// Groups in which the pool competition selected tokens (cache.py:169-173): their rows are
+// replaced by the column means of the ORIGINAL rows (outlier.py:120-142: float64 sums, which
+// are exact for fp16 inputs, / G, rounded to float32) before quantization. The substituted
+// values are float32, so these lines use the float32 fast path / float64 fallback per element
+// instead of fp16 thresholds. `sel` bit t = token t substituted.
+__device__ __forceinline__ void frozen_group_subst(uint8_t* rec, double* p64, const uint16_t* sk, const uint16_t* sv,
+                                                float* vmean, uint32_t sel, int lane) {
+  constexpr int D = 128, G = 32, kLevels = 3;
+  const RecordLayout L(D, G, 2);
+  const double eps = 1e-9 * (double)(kLevels + 1);
+  const uint2* kr = reinterpret_cast<const uint2*>(sk) + lane;
+  // ---- K: channels 4 lane .. +3
+  {
+    double sum[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int t = 0; t < G; ++t) {
+      const uint2 r = kr[t * (D / 4)];
+      const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&r.x));
+      const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&r.y));
+      sum[0] = __dadd_rn(sum[0], (double)a.x);
+      sum[1] = __dadd_rn(sum[1], (double)a.y);
+      sum[2] = __dadd_rn(sum[2], (double)b.x);
+      sum[3] = __dadd_rn(sum[3], (double)b.y);
+    }
+    float mean[4], fmn[4], fmx[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      mean[j] = __double2float_rn(__ddiv_rn(sum[j], (double)G));
+      fmn[j] = 3.4e38f;
+      fmx[j] = -3.4e38f;
+    }
+    auto kval = [&](int t, float (&x)[4]) {
+      if ((sel >> t) & 1u) {
+        x[0] = mean[0]; x[1] = mean[1]; x[2] = mean[2]; x[3] = mean[3];
+      } else {
+        const uint2 r = kr[t * (D / 4)];
+        const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&r.x));
+        const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&r.y));
+        x[0] = a.x; x[1] = a.y; x[2] = b.x; x[3] = b.y;
+      }
+    };
+    for (int t = 0; t < G; ++t) {
+      float x[4];
+      kval(t, x);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        fmn[j] = fminf(fmn[j], x[j]);
+        fmx[j] = fmaxf(fmx[j], x[j]);
+      }
+    }
+    double step[4], inv[4];
+    FastLine fl[4];
+    __half* ksh = reinterpret_cast<__half*>(rec + L.k_sh());
+    __half* ksl = reinterpret_cast<__half*>(rec + L.k_sl());
+    float ke[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int col = 4 * lane + j;
+      const double mn = (double)fmn[j];
+      line_params(mn, (double)fmx[j], (double)kLevels, step[j]);
+      inv[j] = step[j] > 0.0 ? __drcp_rn(step[j]) : 0.0;
+      fl[j] = fast_line(fmn[j], fmx[j], step[j], inv[j], kLevels);
+      const __half sh = __double2half(step[j]);
+      const __half sl = __double2half(__dsub_rn(step[j], (double)__half2float(sh)));
+      ksh[kpair_index(col, D)] = sh;
+      ksl[kpair_index(col, D)] = sl;
+      ke[j] = __double2float_rn(__dsub_rn(mn, __dmul_rn(4.0 * (double)kpair_u(col % 8), step[j])));
+      if (p64) {
+        p64[col] = mn;
+        p64[D + col] = step[j];
+      }
+    }
+    *reinterpret_cast<float4*>(rec + L.k_e() + 16 * lane) = make_float4(ke[0], ke[1], ke[2], ke[3]);
+    uint8_t* kcodes = rec + L.k_codes() + lane;
+    for (int t = 0; t < G; ++t) {
+      float x[4];
+      kval(t, x);
+      uint32_t byte = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        bool slow;
+        int code = quant_code_f32(x[j], fmn[j], fmx[j], kLevels, fl[j], slow);
+        if (slow) code = quant_code_slow(x[j], fmn[j], fmx[j], (double)fmn[j], step[j], inv[j], kLevels, eps);
+        byte |= (uint32_t)code << (2 * j);
+      }
+      kcodes[t * (D / 4)] = (uint8_t)byte;
+    }
+  }
+  // ---- V column means: lane l sums channels 4l..4l+3 (chunk l/2, half l&1 of each swizzled row)
+  {
+    double sum[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int t = 0; t < G; ++t) {
+      const uint2 r = *reinterpret_cast<const uint2*>(sv + t * D + (((lane >> 1) ^ (t & 15)) * 8) + (lane & 1) * 4);
+      const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&r.x));
+      const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&r.y));
+      sum[0] = __dadd_rn(sum[0], (double)a.x);
+      sum[1] = __dadd_rn(sum[1], (double)a.y);
+      sum[2] = __dadd_rn(sum[2], (double)b.x);
+      sum[3] = __dadd_rn(sum[3], (double)b.y);
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) vmean[4 * lane + j] = __double2float_rn(__ddiv_rn(sum[j], (double)G));
+    __syncwarp();
+  }
+  // ---- V: token `lane`
+  {
+    const int t = lane;
+    const bool subst = (sel >> t) & 1u;
+    const uint4* vr = reinterpret_cast<const uint4*>(sv + t * D);
+    const int sw = t & 15;
+    auto vval = [&](int j, float (&x)[8]) {  // channels 8j..8j+7
+      if (subst) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) x[e] = vmean[8 * j + e];
+      } else {
+        const uint4 r = vr[j ^ sw];
+        const __half2* h = reinterpret_cast<const __half2*>(&r);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __half22float2(h[e]);
+          x[2 * e] = f.x;
+          x[2 * e + 1] = f.y;
+        }
+      }
+    };
+    float fmn = 3.4e38f, fmx = -3.4e38f;
+    for (int j = 0; j < D / 8; ++j) {
+      float x[8];
+      vval(j, x);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        fmn = fminf(fmn, x[e]);
+        fmx = fmaxf(fmx, x[e]);
+      }
+    }
+    const double mn = (double)fmn;
+    double step;
+    line_params(mn, (double)fmx, (double)kLevels, step);
+    const double inv = step > 0.0 ? __drcp_rn(step) : 0.0;
+    const FastLine fl = fast_line(fmn, fmx, step, inv, kLevels);
+    reinterpret_cast<float*>(rec + L.v_step())[t] = __double2float_rn(step);
+    reinterpret_cast<float*>(rec + L.v_xmin())[t] = __double2float_rn(mn);
+    if (p64) {
+      p64[2 * D + t] = mn;
+      p64[2 * D + G + t] = step;
+    }
+    uint32_t w[D / 16];
+#pragma unroll
+    for (int j = 0; j < D / 8; ++j) {
+      float x[8];
+      vval(j, x);
+      uint32_t bits = 0;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        bool slow;
+        int code = quant_code_f32(x[e], fmn, fmx, kLevels, fl, slow);
+        if (slow) code = quant_code_slow(x[e], fmn, fmx, mn, step, inv, kLevels, eps);
+        bits |= (uint32_t)code << (2 * e);
+      }
+      if (j & 1) w[j / 2] |= bits << 16;
+      else w[j / 2] = bits;
+    }
+    uint4* vcodes = reinterpret_cast<uint4*>(rec + L.v_codes() + t * (D / 4));
+    vcodes[0] = make_uint4(w[0], w[1], w[2], w[3]);
+    vcodes[1] = make_uint4(w[4], w[5], w[6], w[7]);
+  }
 }
+
 
 __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen_kernel(ott_cache_t c, int64_t q0, int n_groups,
                                                                          int64_t ring_end,
@@ -648,7 +1017,6 @@ __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen_kernel(ott_cac
   const int64_t item = (int64_t)blockIdx.x * kFrozenWarps + warp;
   if (item >= (int64_t)c.n_units * n_groups) return;
   const int u = (int)(item / n_groups), g = (int)(item % n_groups);
-  if (g < c.pool_meta[(size_t)u * 4 + 3]) return;  // done by flush_kernel (pool still active)
   const int cap = G + c.residual;
   const int base = (int)(q0 + (int64_t)g * G);
   const int64_t gi = base / G;
@@ -656,6 +1024,9 @@ __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen_kernel(ott_cac
   const RecordLayout L(D, G, 2);
   uint16_t* sk = sm.k[warp];
   uint16_t* sv = sm.v[warp];
+  // tokens of this group substituted by the pool competition (base is 32-aligned); loaded
+  // before the rows so its latency overlaps theirs
+  const uint32_t sel = c.subst_mask[(size_t)u * mask_words_per_unit(c) + (base >> 5)];
 
   // ---- stage the G rows (cache.py:155-156): lane = 16-byte chunk (lane & 15) of row pairs
   {
@@ -685,6 +1056,10 @@ __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen_kernel(ott_cac
   }
   double* p64 = c.params64 ? c.params64 + ((size_t)u * c.max_groups + (size_t)gi) * 2 * (D + G) : nullptr;
   const double eps = 1e-9 * (double)(kLevels + 1);
+  if (OTT_FROZEN_SEL && sel) {
+    if (OTT_FROZEN_SEL == 1) frozen_group_subst(rec, p64, sk, sv, sm.vmean[warp], sel, lane);
+    return;
+  }
 
   // ---- K: channels 4 lane .. 4 lane + 3, lines over the G tokens
   {
@@ -866,14 +1241,22 @@ cudaError_t launch_flush(const ott_cache_t& c, int64_t q0, int n_groups, int64_t
   const size_t smem = flush_smem_bytes(c.head_dim, c.group_size, c.capacity);
   cudaError_t e = cudaFuncSetAttribute(flush_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  // bulk flushes at the tensor-core shapes: the sequential kernel stops where the pool froze
-  // and the frozen-pool kernel takes the rest of the groups in parallel
+  // bulk flushes at the tensor-core shapes: the sequential kernel runs only the pool
+  // competition (scoring, OutlierPool.update, masks, pool/aux rows) group by group, then
+  // flush_frozen_kernel substitutes and quantizes all groups in parallel
   const bool split = OTT_FLUSH_SPLIT && !dev_counts && n_groups > 1 && c.bits == 2 && c.head_dim == 128 &&
                      c.group_size == 32;
-  flush_kernel<<<c.n_units, kFlushThreads, smem, st>>>(c, q0, n_groups, ring_end, in_k, in_v, in_stride, in_first,
-                                                         dev_counts, split);
+  if (!split) {
+    flush_kernel<<<c.n_units, kFlushThreads, smem, st>>>(c, q0, n_groups, ring_end, in_k, in_v, in_stride, in_first,
+                                                           dev_counts);
+    return cudaGetLastError();
+  }
+  e = cudaFuncSetAttribute(flush_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(ScanSmem));
+  if (e != cudaSuccess) return e;
+  flush_scan_kernel<<<(c.n_units + kScanWarps - 1) / kScanWarps, 32 * kScanWarps, sizeof(ScanSmem), st>>>(
+      c, q0, n_groups, ring_end, in_k, in_v, in_stride, in_first);
   e = cudaGetLastError();
-  if (e != cudaSuccess || !split) return e;
+  if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(flush_frozen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FrozenSmem));
   if (e != cudaSuccess) return e;
   const int64_t items = (int64_t)c.n_units * n_groups;
