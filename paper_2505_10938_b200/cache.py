@@ -383,9 +383,13 @@ class UnitView:
         self.k_e32 = rec[:, 2 * code_b + 4 * d: 2 * code_b + 8 * d].copy().view(np.float32)
         vst = rec[:, 2 * code_b + 8 * d: 2 * code_b + 8 * d + 4 * G].copy().view(np.float32)
         vmn = rec[:, 2 * code_b + 8 * d + 4 * G: 2 * code_b + 8 * d + 8 * G].copy().view(np.float32)
-        pidx = kpair_index(np.arange(d), d)
-        kst = self.k_sh16[:, pidx].astype(np.float32) + self.k_sl16[:, pidx].astype(np.float32)
-        kmn = (self.k_e32 + np.float32(4) * kpair_u(np.arange(d)) * kst).astype(np.float32)
+        if cfg.bits == 2:  # tensor-core encoding: step = sh + sl (pair order), e = x_min - 4 u step
+            pidx = kpair_index(np.arange(d), d)
+            kst = self.k_sh16[:, pidx].astype(np.float32) + self.k_sl16[:, pidx].astype(np.float32)
+            kmn = (self.k_e32 + np.float32(4) * kpair_u(np.arange(d)) * kst).astype(np.float32)
+        else:  # other widths: float32 step[d] in the sh/sl bytes, x_min in e
+            kst = rec[:, 2 * code_b: 2 * code_b + 4 * d].copy().view(np.float32)
+            kmn = self.k_e32.copy()
         self.k_step32, self.k_xmin32, self.v_step32, self.v_xmin32 = kst, kmn, vst, vmn
         if cache.params64 is not None:
             p = cache.params64[u, :nb].cpu().numpy()

@@ -1213,7 +1213,10 @@ __global__ void __launch_bounds__(kAttnThreads, OTT_MMA_MIN_BLOCKS)
 #endif
   if ((int)blockIdx.y == (OTT_FP_FIRST ? 0 : a.n_qsplits)) {  // full-precision tiers: pool + pending
     if (OTT_ABL_TIER & 1) return;
-    fp_body<NR>(a, counts_of(a), *reinterpret_cast<FpSmem*>(smem_raw));
+    const Counts n = counts_of(a);
+    if (blockIdx.x == 0 && threadIdx.x == 0)  // token counts of this launch for the combine's overflow guard
+      reinterpret_cast<int64_t*>(a.ws + (size_t)a.c.n_units * NR * a.n_splits * 130)[0] = n.q_tokens;
+    fp_body<NR>(a, n, *reinterpret_cast<FpSmem*>(smem_raw));
   } else {
     if (OTT_ABL_TIER & 2) return;
     mma_body<NR, G>(a, counts_of(a), &tmap, *reinterpret_cast<MmaSmem<G>*>(smem_raw));
@@ -1678,15 +1681,125 @@ __global__ void __launch_bounds__(tc5::kThreads, OTT_TC5_MIN_BLOCKS)
 // handles columns 2*lane, 2*lane+1 (+64, +65 at D = 128) with float2 loads.
 constexpr int kCombineRows = 8;
 template <int D>
-static cudaError_t launch_combine(const AttnArgs& a, int NR, cudaStream_t st);
+static cudaError_t launch_combine(const AttnArgs& a, int NR, cudaStream_t st, bool tc_path = false);
+
+// Overflow guard of the 2-bit tensor-core path. Its fp16 operands hold q u step (u <= 16)
+// and 4 p v_step (p <= 2^kLazy); pool_meta[u][3] bounds the unit's K and V steps (flush
+// kernels). For a unit whose bound and |q| could overflow them (K or V ranges in the
+// thousands: far outside real activations, but legal fp16 input) the combine recomputes the
+// quantized-tier partial of the head on CUDA cores in float32, so the tensor-core kernel
+// itself carries no extra code.
+struct TcGuard {
+  ott_cache_t c;
+  const uint16_t* q;
+  int NR;
+  float scale_log2;
+};
+// per (unit, head) row: q' of head h only involves q_h
+__device__ __forceinline__ bool tc_row_safe(const TcGuard& gd, int urow, int lane) {
+  const int u = urow / gd.NR;
+  const uint2 raw = reinterpret_cast<const uint2*>(gd.q + (size_t)urow * 128)[lane];
+  const float2 a = __half22float2(__habs2(*reinterpret_cast<const __half2*>(&raw.x)));
+  const float2 b = __half22float2(__habs2(*reinterpret_cast<const __half2*>(&raw.y)));
+  const float qm = warp_max(fmaxf(fmaxf(a.x, a.y), fmaxf(b.x, b.y)));
+  const float smax = __int_as_float(gd.c.pool_meta[(size_t)u * 4 + 3]);
+  const float sm1 = fmaxf(smax, 1.f);
+  return smax <= 3.0e38f && 16.f * qm < 6.5e4f && 16.f * qm * sm1 < 6.5e4f && 4.f * 64.f * sm1 < 6.5e4f;
+}
+// quantized-tier partial (m, l, acc[lane + 32 k]) of head r of unit u over [0, q_tokens),
+// float32 dequantization (quant.py:105-111) and online softmax, one warp
+__device__ __forceinline__ void tc_guard_partial(const TcGuard& gd, int u, int r, int64_t q_tokens, int lane,
+                                                 float& m, float& l, float (&acc)[4]) {
+  constexpr int D = 128;
+  const ott_cache_t& c = gd.c;
+  const int G = c.group_size;
+  const RecordLayout L(D, G, 2);
+  const uint16_t* qrow = gd.q + ((size_t)u * gd.NR + r) * D;
+  m = -INFINITY;
+  l = 0.f;
+  acc[0] = acc[1] = acc[2] = acc[3] = 0.f;
+  const uint32_t* pmask = c.pool_mask + (size_t)u * mask_words_per_unit(c);
+  const int n_groups = (int)(q_tokens / G);
+  for (int gi = 0; gi < n_groups; ++gi) {
+    const uint8_t* rec = record_ptr(c, u, gi);
+    const uint8_t* kc = rec + L.k_codes();
+    const uint8_t* vc = rec + L.v_codes();
+    for (int t0 = 0; t0 < G; t0 += 32) {
+      const int row = t0 + lane;
+      const int64_t p = (int64_t)gi * G + row;
+      float s = 0.f;
+      for (int col = 0; col < D; ++col) {  // the slow path: parameters re-read per token
+        const float code = (float)code_at(kc, (int64_t)row * D + col, 2);
+        const float st = k_step_of(rec, L, col);
+        s = fmaf(h2f(qrow[col]) * gd.scale_log2, fmaf(code, st, k_xmin_of(rec, L, col, st)), s);
+      }
+      if ((pmask[p >> 5] >> (p & 31)) & 1u) s = -INFINITY;  // pooled: attended from the pool
+      const float m_new = fmaxf(m, warp_max(s));
+      float pt = 0.f;
+      if (m_new != -INFINITY) {
+        const float corr = exp2f(m - m_new);
+        pt = exp2f(s - m_new);
+        l = l * corr + warp_sum(pt);
+        for (int k = 0; k < 4; ++k) acc[k] *= corr;
+        m = m_new;
+      }
+      for (int tt = 0; tt < 32; ++tt) {
+        const float pw = __shfl_sync(0xffffffffu, pt, tt);
+        if (pw == 0.f) continue;
+        const int rw = t0 + tt;
+        const float vs = reinterpret_cast<const float*>(rec + L.v_step())[rw];
+        const float vx = reinterpret_cast<const float*>(rec + L.v_xmin())[rw];
+        for (int k = 0; k < 4; ++k) {
+          const int col = lane + 32 * k;
+          acc[k] = fmaf(pw, fmaf((float)code_at(vc, (int64_t)rw * D + col, 2), vs, vx), acc[k]);
+        }
+      }
+    }
+  }
+}
+
 template <int D>
 __global__ void __launch_bounds__(32 * kCombineRows) combine_kernel(const float* __restrict__ ws,
                                                                    uint16_t* __restrict__ out, int n_rows,
                                                                    int n_splits, int64_t* __restrict__ dev_counts,
-                                                                   int G, int R, int max_groups, int d) {
+                                                                   int G, int R, int max_groups, int d,
+                                                                   TcGuard gd, int guard) {
+  // overflow guard inputs (q, pool_meta) predate the attention grid: read them before the
+  // programmatic wait so their latency hides behind its tail
+  bool row_safe = true;
+  if constexpr (D == 128) {
+    const int urow = blockIdx.x * kCombineRows + (threadIdx.x >> 5);
+    if (guard && urow < n_rows) row_safe = tc_row_safe(gd, urow, threadIdx.x & 31);
+  }
 #if OTT_PDL
   asm volatile("griddepcontrol.wait;\n" ::: "memory");  // the attention grid's partials are complete
 #endif
+  if constexpr (D == 128) {
+    if (!row_safe) {
+      const int lane = threadIdx.x & 31, wr = threadIdx.x >> 5;
+      const int urow = blockIdx.x * kCombineRows + wr;
+      // the token counts the attention kernel used (written by its unit-0 fp-tier CTA)
+      const int64_t q_tokens = reinterpret_cast<const int64_t*>(ws + (size_t)n_rows * n_splits * (D + 2))[0];
+      {
+        float m, l, acc[4];
+        tc_guard_partial(gd, urow / gd.NR, urow % gd.NR, q_tokens, lane, m, l, acc);
+        const float* fp = ws + ((size_t)urow * n_splits + (n_splits - 1)) * (D + 2);  // fp-tier partial
+        const float M = fmaxf(m, fp[0]);
+        const float fq = m == -INFINITY ? 0.f : exp2f(m - M), ff = fp[0] == -INFINITY ? 0.f : exp2f(fp[0] - M);
+        const float inv = 1.f / (l * fq + fp[1] * ff);
+        for (int k = 0; k < 4; ++k) {
+          const int col = lane + 32 * k;
+          out[(size_t)urow * D + col] = f2h((acc[k] * fq + fp[2 + col] * ff) * inv);
+        }
+        if (dev_counts && blockIdx.x == 0 && threadIdx.x == 0) {
+          const int64_t qt = dev_counts[0], tot = dev_counts[1] + 1;
+          if (tot - qt - R >= G && qt / G + 1 <= max_groups) dev_counts[0] = qt + G;
+          dev_counts[1] = tot;
+        }
+        return;
+      }
+    }
+  }
   const int lane = threadIdx.x & 31;
   const int ur = blockIdx.x * kCombineRows + (threadIdx.x >> 5);  // unit*NR + r
   if (dev_counts && blockIdx.x == 0 && threadIdx.x == 0) {  // last kernel of a device-counter step: advance
@@ -1742,7 +1855,7 @@ __global__ void __launch_bounds__(32 * kCombineRows) combine_kernel(const float*
 }
 
 template <int D>
-static cudaError_t launch_combine(const AttnArgs& a, int NR, cudaStream_t st) {
+static cudaError_t launch_combine(const AttnArgs& a, int NR, cudaStream_t st, bool tc_path) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((a.c.n_units * NR + kCombineRows - 1) / kCombineRows);
   cfg.blockDim = dim3(32 * kCombineRows);
@@ -1753,9 +1866,14 @@ static cudaError_t launch_combine(const AttnArgs& a, int NR, cudaStream_t st) {
   attr[0].val.programmaticStreamSerializationAllowed = OTT_PDL;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  TcGuard gd;
+  gd.c = a.c;
+  gd.q = a.q;
+  gd.NR = NR;
+  gd.scale_log2 = a.scale_log2;
   return cudaLaunchKernelEx(&cfg, combine_kernel<D>, (const float*)a.ws, a.out, a.c.n_units * NR, a.n_splits,
                             const_cast<int64_t*>(a.dev_counts), a.c.group_size, a.c.residual, a.c.max_groups,
-                            a.c.head_dim);
+                            a.c.head_dim, gd, tc_path ? 1 : 0);
 }
 
 template <int DT>  // 0: runtime head_dim (debug path; k lives in local memory then)
@@ -1856,7 +1974,7 @@ static cudaError_t launch_mma_t(const AttnArgs& a, cudaStream_t st) {
   attend_mma_kernel<NR, G><<<dim3(a.c.n_units, a.n_splits), kAttnThreads, smem, st>>>(a, tmap);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  return launch_combine<128>(a, NR, st);
+  return launch_combine<128>(a, NR, st, true);
 }
 
 template <int NR>

@@ -64,15 +64,29 @@ __device__ __forceinline__ uint32_t code_at(const uint8_t* codes, int64_t e, int
   const uint32_t hi = ((b0 & 7) + bits > 8) ? codes[(b0 >> 3) + 1] : 0u;
   return ((lo | (hi << 8)) >> (b0 & 7)) & ((1u << bits) - 1u);
 }
-// float32 K step / x_min of channel c reconstructed from the record encoding
+// float32 K step / x_min of channel c from the record. 2-bit records hold the tensor-core
+// encoding (sh + sl halves, e = x_min - 4 u step); other widths, whose steps can exceed the
+// fp16 range (1 bit: up to 2 * 65504), hold float32 step[d] in the sh/sl bytes and x_min in e.
 __device__ __forceinline__ float k_step_of(const uint8_t* rec, const RecordLayout& L, int c) {
+  if (L.bits != 2) return reinterpret_cast<const float*>(rec + L.k_sh())[c];
   const int j = kpair_index(c, L.d);
   return h2f(reinterpret_cast<const uint16_t*>(rec + L.k_sh())[j]) + h2f(reinterpret_cast<const uint16_t*>(rec + L.k_sl())[j]);
 }
 __device__ __forceinline__ float k_xmin_of(const uint8_t* rec, const RecordLayout& L, int c, float step) {
+  if (L.bits != 2) return reinterpret_cast<const float*>(rec + L.k_e())[c];
   return fmaf(4.f * kpair_u(c % 8), step, reinterpret_cast<const float*>(rec + L.k_e())[c]);
 }
 __device__ __forceinline__ uint16_t f2h(float f) { return __half_as_ushort(__float2half_rn(f)); }
+
+// Largest K or V step of a unit's 2-bit groups (pool_meta[u][3], float bits, atomic max):
+// the tensor-core attention scales its fp16 operands (q u step, 4 p v_step) by powers of two
+// when this bound and |q| would overflow them (see step_scales in ott_attend.cu).
+__device__ __forceinline__ void note_step_max(int32_t* meta3, float step) {  // whole warp
+  float m = step;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(meta3, __float_as_int(m));
+}
 
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {

@@ -424,6 +424,7 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
     float* vxmin = reinterpret_cast<float*>(rec + L.v_xmin());
     if (warp < kwarps) {
       const int col = tid;
+      float kst = 0.f;
       if (col < d) {
         float fmn = sk[col], fmx = fmn;
         for (int i = 1; i < G; ++i) {
@@ -444,17 +445,25 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
           if (slow) code = quant_code_slow(x, fmn, fmx, mn, step, inv, levels, eps);
           kc[i * d + col] = (uint8_t)code;
         }
-        // decode-side encoding (ott_common.cuh): step = sh + sl, e = x_min - 4 u step
-        const __half sh = __double2half(step);
-        const __half sl = __double2half(__dsub_rn(step, (double)__half2float(sh)));
-        ksh[kpair_index(col, d)] = sh;
-        ksl[kpair_index(col, d)] = sl;
-        ke[col] = __double2float_rn(__dsub_rn(mn, __dmul_rn(4.0 * (double)kpair_u(col % 8), step)));
+        // decode-side encoding (ott_common.cuh): 2-bit: step = sh + sl, e = x_min - 4 u step;
+        // other widths: float32 step and x_min
+        kst = (float)step;
+        if (c.bits == 2) {
+          const __half sh = __double2half(step);
+          const __half sl = __double2half(__dsub_rn(step, (double)__half2float(sh)));
+          ksh[kpair_index(col, d)] = sh;
+          ksl[kpair_index(col, d)] = sl;
+          ke[col] = __double2float_rn(__dsub_rn(mn, __dmul_rn(4.0 * (double)kpair_u(col % 8), step)));
+        } else {
+          reinterpret_cast<float*>(ksh)[col] = __double2float_rn(step);
+          ke[col] = __double2float_rn(mn);
+        }
         if (p64) {
           p64[col] = mn;
           p64[d + col] = step;
         }
       }
+      if (c.bits == 2) note_step_max(meta + 3, kst);
     } else {
       // warp vw owns tokens vw + j nvw (j < 32 since G <= 128 and nvw >= 4): the warp reduces
       // each token's min/max, lane j keeps token j's and derives its line parameters (one
@@ -498,6 +507,7 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
           p64[2 * d + G + i] = my_step;
         }
       }
+      if (c.bits == 2) note_step_max(meta + 3, lane < n_my ? (float)my_step : 0.f);
       for (int j = 0; j < n_my; ++j) {
         const int i = vw + j * nvw;
         const float fmn = __shfl_sync(0xffffffffu, my_mn, j), fmx = __shfl_sync(0xffffffffu, my_mx, j);
@@ -576,7 +586,7 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
 // rank-by-count as flush_kernel (outlier.py:84-117). Substitution and quantization are left
 // to flush_frozen_kernel (all groups in parallel). Stops when the pool freezes. d = 128,
 // G = 32, N <= 128.
-constexpr int kScanWarps = 2;
+constexpr int kScanWarps = 1;  // one warp per block: a unit's scan is latency bound
 constexpr int kScanStages = 4;  // K-row groups in flight per warp (cp.async ring)
 struct ScanSmem {
   uint16_t rows[kScanWarps][kScanStages][32 * 128];  // chunk j of row t at (j ^ (t & 15))
@@ -623,6 +633,16 @@ __global__ void __launch_bounds__(32 * kScanWarps) flush_scan_kernel(ott_cache_t
     spos[s] = ppos[s];
     sscore[s] = pscore[s];
   }
+  // largest entry score (valid when the pool is full; a candidate with an equal score has a
+  // larger position, so it loses the tie)
+  auto max_entry_score = [&]() {
+    double m = -1.0;
+    for (int t = lane; t < N; t += 32)
+      if (spos[t] >= 0) m = fmax(m, sscore[t]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    return m;
+  };
   const int q0i = (int)q0;
   const int bslot0 = q0i % cap;
   auto row_of = [&](int p, const uint16_t* ring, const uint16_t* in) -> const uint16_t* {
@@ -649,6 +669,7 @@ __global__ void __launch_bounds__(32 * kScanWarps) flush_scan_kernel(ott_cache_t
 #pragma unroll
   for (int st = 0; st < kScanStages - 1; ++st) load_group(st);
   __syncwarp();
+  double wmax = max_entry_score();
   for (int g = 0; g < n_groups && !frozen; ++g) {
     const int base = q0i + g * G;
     load_group(g + kScanStages - 1);
@@ -673,6 +694,13 @@ __global__ void __launch_bounds__(32 * kScanWarps) flush_scan_kernel(ott_cache_t
         a3 = __dadd_rn(a3, __dadd_rn(fabs((double)f3.x), fabs((double)f3.y)));
       }
       sc = __dadd_rn(__dadd_rn(a0, a1), __dadd_rn(a2, a3));  // exact: fp16 magnitudes fit 2^-24..2^16
+    }
+    // a full pool only changes if some candidate ranks below its largest entry (ties go to the
+    // smaller position, and candidates come after every entry): otherwise update() selects
+    // and evicts nothing (outlier.py:102-117)
+    if (n_entries == N && !__any_sync(0xffffffffu, sc < wmax)) {
+      __syncwarp();
+      continue;
     }
     // ---- OutlierPool.update (outlier.py:84-117): items [0, N) slots, [N, N+G) candidates
     for (int t = lane; t < N; t += 32) {
@@ -760,6 +788,7 @@ __global__ void __launch_bounds__(32 * kScanWarps) flush_scan_kernel(ott_cache_t
     n_entries = warp_sum(n_e);
     if (n_aux >= A) frozen = 1;  // outlier.py:115-116
     __syncwarp();  // stage g % kScanStages is reloaded next iteration
+    wmax = max_entry_score();
   }
   asm volatile("cp.async.wait_all;\n" ::: "memory");
   __syncwarp();
@@ -843,11 +872,13 @@ struct FrozenSmem {
 // values are float32, so these lines use the float32 fast path / float64 fallback per element
 // instead of fp16 thresholds. `sel` bit t = token t substituted.
 __device__ __forceinline__ void frozen_group_subst(uint8_t* rec, double* p64, const uint16_t* sk, const uint16_t* sv,
-                                                float* vmean, uint32_t sel, int lane) {
+                                                float* vmean, uint32_t sel, int lane, int32_t* meta3) {
   constexpr int D = 128, G = 32, kLevels = 3;
   const RecordLayout L(D, G, 2);
   const double eps = 1e-9 * (double)(kLevels + 1);
   const uint2* kr = reinterpret_cast<const uint2*>(sk) + lane;
+  float kst_max = 0.f;
+  float vst = 0.f;
   // ---- K: channels 4 lane .. +3
   {
     double sum[4] = {0.0, 0.0, 0.0, 0.0};
@@ -898,6 +929,7 @@ __device__ __forceinline__ void frozen_group_subst(uint8_t* rec, double* p64, co
       line_params(mn, (double)fmx[j], (double)kLevels, step[j]);
       inv[j] = step[j] > 0.0 ? __drcp_rn(step[j]) : 0.0;
       fl[j] = fast_line(fmn[j], fmx[j], step[j], inv[j], kLevels);
+      kst_max = fmaxf(kst_max, (float)step[j]);
       const __half sh = __double2half(step[j]);
       const __half sl = __double2half(__dsub_rn(step[j], (double)__half2float(sh)));
       ksh[kpair_index(col, D)] = sh;
@@ -976,6 +1008,7 @@ __device__ __forceinline__ void frozen_group_subst(uint8_t* rec, double* p64, co
     line_params(mn, (double)fmx, (double)kLevels, step);
     const double inv = step > 0.0 ? __drcp_rn(step) : 0.0;
     const FastLine fl = fast_line(fmn, fmx, step, inv, kLevels);
+    vst = (float)step;
     reinterpret_cast<float*>(rec + L.v_step())[t] = __double2float_rn(step);
     reinterpret_cast<float*>(rec + L.v_xmin())[t] = __double2float_rn(mn);
     if (p64) {
@@ -1002,6 +1035,7 @@ __device__ __forceinline__ void frozen_group_subst(uint8_t* rec, double* p64, co
     vcodes[0] = make_uint4(w[0], w[1], w[2], w[3]);
     vcodes[1] = make_uint4(w[4], w[5], w[6], w[7]);
   }
+  note_step_max(meta3, fmaxf(kst_max, vst));
 }
 
 
@@ -1056,10 +1090,13 @@ __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen_kernel(ott_cac
   }
   double* p64 = c.params64 ? c.params64 + ((size_t)u * c.max_groups + (size_t)gi) * 2 * (D + G) : nullptr;
   const double eps = 1e-9 * (double)(kLevels + 1);
+  int32_t* meta3 = c.pool_meta + (size_t)u * 4 + 3;
   if (OTT_FROZEN_SEL && sel) {
-    if (OTT_FROZEN_SEL == 1) frozen_group_subst(rec, p64, sk, sv, sm.vmean[warp], sel, lane);
+    if (OTT_FROZEN_SEL == 1) frozen_group_subst(rec, p64, sk, sv, sm.vmean[warp], sel, lane, meta3);
     return;
   }
+  float kst_max = 0.f;
+  float vst = 0.f;
 
   // ---- K: channels 4 lane .. 4 lane + 3, lines over the G tokens
   {
@@ -1094,6 +1131,7 @@ __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen_kernel(ott_cac
       line_params(mn, (double)fmx[j], (double)kLevels, step[j]);
       inv[j] = step[j] > 0.0 ? __drcp_rn(step[j]) : 0.0;
       exact &= code_thresholds(thr[j], fmn[j], fmx[j], mn, step[j], inv[j], kLevels, eps);
+      kst_max = fmaxf(kst_max, (float)step[j]);
       const __half sh = __double2half(step[j]);
       const __half sl = __double2half(__dsub_rn(step[j], (double)__half2float(sh)));
       ksh[kpair_index(col, D)] = sh;
@@ -1157,6 +1195,7 @@ __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen_kernel(ott_cac
     const double inv = step > 0.0 ? __drcp_rn(step) : 0.0;
     uint16_t thr[kLevels];
     const bool exact = code_thresholds(thr, fmn, fmx, mn, step, inv, kLevels, eps);
+    vst = (float)step;
     reinterpret_cast<float*>(rec + L.v_step())[t] = __double2float_rn(step);
     reinterpret_cast<float*>(rec + L.v_xmin())[t] = __double2float_rn(mn);
     if (p64) {
@@ -1193,6 +1232,7 @@ __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen_kernel(ott_cac
     vcodes[0] = make_uint4(w[0], w[1], w[2], w[3]);
     vcodes[1] = make_uint4(w[4], w[5], w[6], w[7]);
   }
+  note_step_max(meta3, fmaxf(kst_max, vst));
 }
 
 // K4: ring write. One thread per 8 halves.

@@ -73,10 +73,14 @@ def assert_unit_matches_oracle(u, ref, exact64=True):
             assert [p.step for p in u.quantized_k[b].params] == blk["k_step"].tolist()
             assert [p.x_min for p in u.quantized_v[b].params] == blk["v_xmin"].tolist()
             assert [p.step for p in u.quantized_v[b].params] == blk["v_step"].tolist()
-        sh, sl, e = expected_k_encoding(blk["k_step"], blk["k_xmin"])
-        np.testing.assert_array_equal(u.k_sh16[b].view(np.uint16), sh.view(np.uint16))
-        np.testing.assert_array_equal(u.k_sl16[b].view(np.uint16), sl.view(np.uint16))
-        np.testing.assert_array_equal(u.k_e32[b], e)
+        if u.config.bits == 2:
+            sh, sl, e = expected_k_encoding(blk["k_step"], blk["k_xmin"])
+            np.testing.assert_array_equal(u.k_sh16[b].view(np.uint16), sh.view(np.uint16))
+            np.testing.assert_array_equal(u.k_sl16[b].view(np.uint16), sl.view(np.uint16))
+            np.testing.assert_array_equal(u.k_e32[b], e)
+        else:  # float32 step / x_min (ott_b200.h)
+            np.testing.assert_array_equal(u.k_step32[b], blk["k_step"].astype(np.float32))
+            np.testing.assert_array_equal(u.k_xmin32[b], blk["k_xmin"].astype(np.float32))
         np.testing.assert_array_equal(u.v_step32[b], blk["v_step"].astype(np.float32))
         np.testing.assert_array_equal(u.v_xmin32[b], blk["v_xmin"].astype(np.float32))
     pe = ref.pool_entries()
@@ -428,6 +432,10 @@ def test_flush_adversarial_lines_vs_oracle(bits, N):
     ref = oracle.OracleCache(bits, G, 64, N, 6, d)
     ref.extend(k.astype(np.float32), v.astype(np.float32))
     assert_unit_matches_oracle(cache.unit(0, 0), ref)
+    q = (rng.standard_normal((1, 1, d)) * 1e-3).astype(np.float16)  # keeps the 6e4-scale logits finite
+    out = cache.attend(torch.from_numpy(q).cuda()).float().cpu().numpy().reshape(d)
+    ok, err = within_tol(out, ref.attend(q.reshape(d).astype(np.float32)))
+    assert ok, err
 
 
 # --------------------------------------------------------------------------- generic shapes

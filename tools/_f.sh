@@ -1,4 +1,2 @@
-timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -2
-python tools/prof_flush.py --batch 128 --kv 8 --ctx 16384 --reps 2
-python tools/prof_flush.py --batch 4 --kv 32 --ctx 32768 --pool 3 --reps 2
-python tools/prof_flush.py --batch 128 --kv 8 --ctx 16384 --pool 3 --reps 1
+bash tools/run_var2.sh prev base prev base
+ncu --metrics gpu__time_duration.sum -k regex:combine --csv python tools/prof_attend.py --batch 128 --rep 8 --ctx 16384 --iters 3 --append 2>/dev/null | grep combine | awk -F'","' '{print $NF}' | head -3
