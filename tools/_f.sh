@@ -1,2 +1,4 @@
-bash tools/run_var2.sh prev base prev base
-ncu --metrics gpu__time_duration.sum -k regex:combine --csv python tools/prof_attend.py --batch 128 --rep 8 --ctx 16384 --iters 3 --append 2>/dev/null | grep combine | awk -F'","' '{print $NF}' | head -3
+for v in prev base prev base; do
+  if [ $v = base ]; then L=""; else L="OTT_LIB_PATH=tools/variants/$v.so"; fi
+  env $L python bench.py --no-cpu > gpurun_out/bench_ab.jsonl 2> gpurun_out/bench_ab.err; echo "$v $(tail -1 gpurun_out/bench_ab.jsonl | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['value']), round(d['e2e']['value']), round(d['roofline']['avg_launch_us'],1), d['clocks']['sm_mhz'])")"
+done
