@@ -1,4 +1,2 @@
-for v in prev base prev base; do
-  if [ $v = base ]; then L=""; else L="OTT_LIB_PATH=tools/variants/$v.so"; fi
-  env $L python bench.py --no-cpu > gpurun_out/bench_ab.jsonl 2> gpurun_out/bench_ab.err; echo "$v $(tail -1 gpurun_out/bench_ab.jsonl | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['value']), round(d['e2e']['value']), round(d['roofline']['avg_launch_us'],1), d['clocks']['sm_mhz'])")"
-done
+for b in 2 4 3 8; do python tools/prof_attend.py --batch 128 --rep 8 --ctx 16384 --iters 10 --bits $b 2>&1 | tail -1; done
+python tools/prof_attend.py --batch 64 --rep 4 --ctx 8192 --iters 10 --bits 4 2>&1 | tail -1

@@ -21,13 +21,14 @@ ap.add_argument("--rep", type=int, default=4)
 ap.add_argument("--ctx", type=int, default=8192)
 ap.add_argument("--iters", type=int, default=20)
 ap.add_argument("--pool", type=int, default=32)
+ap.add_argument("--bits", type=int, default=2)
 ap.add_argument("--splits", type=int, default=0)
 ap.add_argument("--append", action="store_true", help="time append_attend (fused ring write) steps")
 ap.add_argument("--graph", action="store_true", help="capture the iters attend launches in one CUDA graph (no host gaps)")
 args = ap.parse_args()
 
 torch.cuda.set_device(0)
-cfg = EngineConfig(bits=2, group_size=32, residual=128, outlier_num=args.pool, aux_capacity=32, skip_layers=(),
+cfg = EngineConfig(bits=args.bits, group_size=32, residual=128, outlier_num=args.pool, aux_capacity=32, skip_layers=(),
                    head_dim=128)
 cache = OTTCache(cfg, args.batch, args.kv, args.ctx + 64 + args.iters)
 gen = torch.Generator(device="cuda").manual_seed(0)
@@ -67,7 +68,7 @@ ms = e0.elapsed_time(e1) / args.iters
 Tq = cache.quantized_tokens
 Tp = cache.total_tokens - Tq
 U = args.batch * args.kv
-per_unit = Tq * 64 + (Tq // 32) * 1024 + Tq * 8 + Tq // 8 + (Tp + min(args.pool, Tq)) * 512 + 2 * args.rep * 256
+per_unit = Tq * 64 * args.bits // 2 + (Tq // 32) * 1024 + Tq * 8 + Tq // 8 + (Tp + min(args.pool, Tq)) * 512 + 2 * args.rep * 256
 gbs = U * per_unit / (ms * 1e-3) / 1e9
 print(f"attend B={args.batch} Hkv={args.kv} rep={args.rep} T={args.ctx} splits={splits}: {ms * 1e3:.1f} us, "
       f"{gbs:.0f} GB/s algorithmic ({U * per_unit / 1e6:.1f} MB)")
