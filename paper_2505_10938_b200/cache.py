@@ -62,6 +62,12 @@ def record_code_bytes(d, G, bits):
     return ((G * d * bits + 7) // 8 + 15) & ~15
 
 
+def kpair4_index(c):
+    """4-bit pair order: half2 pairs (8w+k, 8w+k+4) of the nibble unpack (ott_common.cuh)."""
+    c = np.asarray(c)
+    return 8 * (c // 8) + 2 * (c % 4) + (c % 8) // 4
+
+
 def kpair_u(c):
     """Position scale u(c) = 4^(4 - P(c % 8)) of the decode kernels' code-pair unpack."""
     P = np.array([3, 4, 2, 3, 4, 2, 3, 4])[np.asarray(c) % 8]
@@ -387,6 +393,10 @@ class UnitView:
             pidx = kpair_index(np.arange(d), d)
             kst = self.k_sh16[:, pidx].astype(np.float32) + self.k_sl16[:, pidx].astype(np.float32)
             kmn = (self.k_e32 + np.float32(4) * kpair_u(np.arange(d)) * kst).astype(np.float32)
+        elif cfg.bits == 4 and d % 8 == 0:  # 4-bit tensor-core encoding: pair4 order, e = x_min - 64 step
+            pidx = kpair4_index(np.arange(d))
+            kst = self.k_sh16[:, pidx].astype(np.float32) + self.k_sl16[:, pidx].astype(np.float32)
+            kmn = (self.k_e32 + np.float32(64) * kst).astype(np.float32)
         else:  # other widths: float32 step[d] in the sh/sl bytes, x_min in e
             kst = rec[:, 2 * code_b: 2 * code_b + 4 * d].copy().view(np.float32)
             kmn = self.k_e32.copy()

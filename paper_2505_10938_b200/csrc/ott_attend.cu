@@ -1223,6 +1223,344 @@ __global__ void __launch_bounds__(kAttnThreads, OTT_MMA_MIN_BLOCKS)
   }
 }
 
+// ============================================================ 4-bit tensor-core path (d = 128, G = 32)
+// Same structure as mma_body with 4-bit codes (a record is 5,376 B: 64-byte token rows).
+//   * Records arrive through a 128-byte-row tensor map with SWIZZLE_128B (16-byte chunk bits
+//     4-6 ^= offset bits 7-9), so ldmatrix over 64-byte token rows is bank-conflict free; the
+//     stage slots are 1 KB aligned (6 KB each).
+//   * A code word holds channels 8w..8w+7 (nibble i at bits 4i). Nibble k of both halves is
+//     moved to mantissa bits 4-7 (k=0: <<4, k=1: in place, k=2: >>4, k=3: >>8; one LOP3 each):
+//     K codes become fp16 1 + c/64 (1.0 magic), V codes exact subnormals c * 2^-20. The pair is
+//     (channel 8w+k, 8w+k+4); the record's K steps are stored in that order (kpair4_index).
+//   * Q.K^T k-step (h, k): logical columns (2t, 2t+1) = channels 64h + 8t + k (+4), columns
+//     (2t+8, 2t+9) = 64h + 32 + 8t + k (+4). P.V m-tile (h, k): rows g / g+8 = channels
+//     64h + 4g + k / 64h + 32 + 4g + k.
+namespace q4 {
+constexpr int kRec = 32 * 64 + 32 * 64 + 2 * 2 * 128 + 4 * 128 + 8 * 32;  // 5,376 B
+constexpr int kSlot = 6144;                                               // 1 KB aligned slots
+constexpr int kStages = 2;
+constexpr int kRows = kRec / 128;  // tensor-map rows of 128 B
+}  // namespace q4
+struct Mma4Smem {
+  float4 qt[8][32];  // q (fp32) per lane for the x_min bias: [word slot][lane]
+  alignas(1024) uint8_t stage[kAttnWarps][q4::kStages][q4::kSlot];
+  alignas(8) uint64_t bar[kAttnWarps][q4::kStages];
+  float mm[kAttnWarps][8], ll[kAttnWarps][8];
+};
+__device__ __forceinline__ uint32_t swz128(uint32_t o) { return o ^ (((o >> 7) & 7u) << 4); }
+__device__ __forceinline__ void load_record4(uint32_t dst, const CUtensorMap* map, int64_t rec_index, uint32_t bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(q4::kRec) : "memory");
+  tma_tensor_rows(dst, map, (int)(rec_index * q4::kRows), bar);
+}
+struct Nib {
+  uint32_t l4, x, r4, r8;
+};
+__device__ __forceinline__ Nib nibs(uint32_t w) { return {w << 4, w, w >> 4, w >> 8}; }
+template <int K>
+__device__ __forceinline__ uint32_t nib_src(const Nib& n) {
+  return K == 0 ? n.l4 : (K == 1 ? n.x : (K == 2 ? n.r4 : n.r8));
+}
+template <int K>
+__device__ __forceinline__ uint32_t kq4(const Nib& n, uint32_t magic) {
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;\n" : "=r"(r) : "r"(nib_src<K>(n)), "n"(0x00F000F0u), "r"(magic));
+  return r;
+}
+template <int K>
+__device__ __forceinline__ uint32_t vq4(const Nib& n) {
+  return nib_src<K>(n) & 0x00F000F0u;
+}
+
+template <int NR>
+__device__ void mma4_body(const AttnArgs& a, const Counts& n, const CUtensorMap* tmap, Mma4Smem& sm) {
+  constexpr int D = 128, G = 32, kMt = 2, kStages = q4::kStages;
+  const RecordLayout L(D, G, 4);
+  const ott_cache_t& c = a.c;
+  const int u = blockIdx.x, split = blockIdx.y;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, tig = lane & 3;
+  const uint32_t magic = a.k_magic;
+  const int n_groups = (int)(n.q_tokens / G);
+  const int per = (n_groups + a.n_qsplits - 1) / a.n_qsplits;
+  const int g0 = split * per;
+  const int g1 = min(n_groups, g0 + per);
+  const int my_n = g1 > g0 + warp ? (g1 - g0 - warp + kAttnWarps - 1) / kAttnWarps : 0;
+
+  // q (fp32) for the bias: slot 2 s + j of lane (head h, t) = channels 8 w + 4 j .. +3 of word
+  // w = 32 (s >> 1) + 8 (s & 1)... i.e. words W(s) = {t, 4+t, 8+t, 12+t}[s]
+  for (int i = tid; i < 8 * 32; i += kAttnThreads) {
+    const int k = i >> 5, ln = i & 31, h = ln >> 2, t4 = ln & 3;
+    const int w = 4 * (k >> 1) + t4;  // words t, 4+t, 8+t, 12+t
+    const int ch = 8 * w + 4 * (k & 1);
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (h < NR) {
+      const uint2 raw = __ldg(reinterpret_cast<const uint2*>(a.q + ((size_t)u * NR + h) * D + ch));
+      const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&raw.x));
+      const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&raw.y));
+      v = make_float4(f0.x, f0.y, f1.x, f1.y);
+    }
+    sm.qt[k][ln] = v;
+  }
+  const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&sm.bar[warp][0]);
+  const uint32_t stage0 = (uint32_t)__cvta_generic_to_shared(&sm.stage[warp][0][0]);
+  if (stage0 & 1023u) __trap();  // SWIZZLE_128B needs 1 KB-aligned stage slots (see swz128)
+  const int64_t unit_rec = (int64_t)u * c.max_groups;
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < kStages; ++s) mbar_init(bar0 + 8 * s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+#pragma unroll
+    for (int s = 0; s < kStages; ++s)
+      if (s < my_n) load_record4(stage0 + s * q4::kSlot, tmap, unit_rec + g0 + warp + s * kAttnWarps, bar0 + 8 * s);
+  }
+  __syncthreads();
+
+  float o[8][4];
+#pragma unroll
+  for (int cm = 0; cm < 8; ++cm) o[cm][0] = o[cm][1] = o[cm][2] = o[cm][3] = 0.f;
+  float mrun[2] = {-INFINITY, -INFINITY}, lsum[2] = {0.f, 0.f}, vb[2] = {0.f, 0.f};
+  const uint32_t* pmask = c.pool_mask + (size_t)u * mask_words_per_unit(c);
+  // ldmatrix rows (64-byte token rows): matrix i = lane / 8, row r = lane % 8:
+  // i0 tokens 0-7 bytes 0-15, i1 tokens 8-15 bytes 0-15, i2 tokens 0-7 bytes 16-31, i3 tokens 8-15
+  // bytes 16-31 (+32 for the second half of the row)
+  const uint32_t lm_off = (uint32_t)(((lane & 7) + ((lane >> 3) & 1) * 8) * 64 + (lane >> 4) * 16);
+  // q * 64 as fp16 pairs (channels 8w+k, 8w+k+4), words w = {t, 4+t, 8+t, 12+t}[s]
+  __half2 q16[4][4];
+#pragma unroll
+  for (int sw = 0; sw < 4; ++sw)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float4 qa = sm.qt[2 * sw][lane], qb = sm.qt[2 * sw + 1][lane];  // channels 8w..8w+3, 8w+4..8w+7
+      const float lo = (k == 0 ? qa.x : k == 1 ? qa.y : k == 2 ? qa.z : qa.w) * 64.f;
+      const float hi = (k == 0 ? qb.x : k == 1 ? qb.y : k == 2 ? qb.z : qb.w) * 64.f;
+      q16[sw][k] = __floats2half2_rn(lo, hi);
+    }
+  const float scale4 = a.scale_log2;  // ch = sum q 64 step (1 + c/64) = 64 sum q step + sum q step c
+  for (int k = 0; k < my_n; ++k) {
+    const int gi = g0 + warp + k * kAttnWarps;
+    const uint32_t mword = __ldg(&pmask[gi]);
+    const int s = k % kStages;
+    mbar_wait(bar0 + 8 * s, (uint32_t)((k / kStages) & 1));
+    const uint8_t* rec = &sm.stage[warp][s][0];
+    const uint32_t rec_s = stage0 + s * q4::kSlot;
+    // K code words: [mt][half h][4] = token g / g+8, words 8h + t and 8h + 4 + t
+    uint32_t kw[kMt][2][4];
+#pragma unroll
+    for (int mt = 0; mt < kMt; ++mt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) ldsm_x4(kw[mt][h], rec_s + swz128(L.k_codes() + mt * 16 * 64 + 32 * h + lm_off));
+    __syncwarp();
+    // bias: sum_c q e over this lane's 32 channels (words t, 4+t, 8+t, 12+t)
+    float bias;
+    {
+      float2 acc2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        const int w = 4 * (kk >> 1) + tig;
+        const float4 ev = *reinterpret_cast<const float4*>(rec + swz128(L.k_e() + 32 * w + 16 * (kk & 1)));
+        const float4 qv = sm.qt[kk][lane];
+        acc2[(2 * kk) & 3] = __ffma2_rn(make_float2(qv.x, qv.y), make_float2(ev.x, ev.y), acc2[(2 * kk) & 3]);
+        acc2[(2 * kk + 1) & 3] = __ffma2_rn(make_float2(qv.z, qv.w), make_float2(ev.z, ev.w), acc2[(2 * kk + 1) & 3]);
+      }
+      bias = ((acc2[0].x + acc2[0].y) + (acc2[1].x + acc2[1].y)) + ((acc2[2].x + acc2[2].y) + (acc2[3].x + acc2[3].y));
+    }
+    float ch[kMt][4];
+#pragma unroll
+    for (int mt = 0; mt < kMt; ++mt) ch[mt][0] = ch[mt][1] = ch[mt][2] = ch[mt][3] = 0.f;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      // q' = q 64 step as exact fp16 hi/lo from the step halves: words 8h + t (b0) and 8h + 4 + t (b1)
+      uint32_t bh[2][4], bl[2][4];
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        const int w = 8 * h + 4 * b + tig;
+        const uint4 sh4 = *reinterpret_cast<const uint4*>(rec + swz128(L.k_sh() + 16 * w));
+        const uint4 sl4 = *reinterpret_cast<const uint4*>(rec + swz128(L.k_sl() + 16 * w));
+        const uint32_t shw[4] = {sh4.x, sh4.y, sh4.z, sh4.w}, slw[4] = {sl4.x, sl4.y, sl4.z, sl4.w};
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const __half2 sh = *reinterpret_cast<const __half2*>(&shw[kk]);
+          const __half2 sl = *reinterpret_cast<const __half2*>(&slw[kk]);
+          const __half2 qq = q16[2 * h + b][kk];
+          const __half2 H = __hmul2(qq, sh);
+          const __half2 E = __hfma2(qq, sh, __hneg2(H));
+          bh[b][kk] = h2_as_u32(H);
+          bl[b][kk] = h2_as_u32(__hfma2(qq, sl, E));
+        }
+      }
+      Nib n0[kMt], n1[kMt], n2[kMt], n3[kMt];
+#pragma unroll
+      for (int mt = 0; mt < kMt; ++mt) {
+        n0[mt] = nibs(kw[mt][h][0]);  // token g, word 8h + t
+        n1[mt] = nibs(kw[mt][h][1]);  // token g + 8, word 8h + t
+        n2[mt] = nibs(kw[mt][h][2]);  // token g, word 8h + 4 + t
+        n3[mt] = nibs(kw[mt][h][3]);  // token g + 8, word 8h + 4 + t
+      }
+#define OTT_QK4(K)                                                                            \
+  {                                                                                           \
+    _Pragma("unroll") for (int mt = 0; mt < kMt; ++mt) {                                      \
+      const uint32_t a0 = kq4<K>(n0[mt], magic), a1 = kq4<K>(n1[mt], magic);                 \
+      const uint32_t a2 = kq4<K>(n2[mt], magic), a3 = kq4<K>(n3[mt], magic);                 \
+      mma16816(ch[mt], a0, a1, a2, a3, bh[0][K], bh[1][K]);                                   \
+      mma16816(ch[mt], a0, a1, a2, a3, bl[0][K], bl[1][K]);                                   \
+    }                                                                                         \
+  }
+      OTT_QK4(0) OTT_QK4(1) OTT_QK4(2) OTT_QK4(3)
+#undef OTT_QK4
+    }
+    float sc[kMt][4];
+    {
+      bias += __shfl_xor_sync(0xffffffffu, bias, 1);
+      bias += __shfl_xor_sync(0xffffffffu, bias, 2);
+      bias *= a.scale_log2;
+      const float bias0 = __shfl_sync(0xffffffffu, bias, 8 * tig);      // head 2*tig
+      const float bias1 = __shfl_sync(0xffffffffu, bias, 8 * tig + 4);  // head 2*tig+1
+#pragma unroll
+      for (int mt = 0; mt < kMt; ++mt) {
+        sc[mt][0] = fmaf(ch[mt][0], scale4, bias0);
+        sc[mt][1] = fmaf(ch[mt][1], scale4, bias1);
+        sc[mt][2] = fmaf(ch[mt][2], scale4, bias0);
+        sc[mt][3] = fmaf(ch[mt][3], scale4, bias1);
+      }
+      if (mword) {
+#pragma unroll
+        for (int mt = 0; mt < kMt; ++mt) {
+          if ((mword >> (mt * 16 + g)) & 1u) sc[mt][0] = sc[mt][1] = -INFINITY;
+          if ((mword >> (mt * 16 + g + 8)) & 1u) sc[mt][2] = sc[mt][3] = -INFINITY;
+        }
+      }
+    }
+    float tmax[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      float t = -INFINITY;
+#pragma unroll
+      for (int mt = 0; mt < kMt; ++mt) t = fmaxf(t, fmaxf(sc[mt][h], sc[mt][h + 2]));
+      tmax[h] = t;
+    }
+    const bool need = tmax[0] > mrun[0] + kLazy || tmax[1] > mrun[1] + kLazy;
+    if (__any_sync(0xffffffffu, need)) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float t = tmax[h];
+        t = fmaxf(t, __shfl_xor_sync(0xffffffffu, t, 4));
+        t = fmaxf(t, __shfl_xor_sync(0xffffffffu, t, 8));
+        t = fmaxf(t, __shfl_xor_sync(0xffffffffu, t, 16));
+        const float mnew = fmaxf(mrun[h], t);
+        const float corr = mnew == -INFINITY ? 1.f : ex2(mrun[h] - mnew);
+        lsum[h] *= corr;
+        vb[h] *= corr;
+#pragma unroll
+        for (int cm = 0; cm < 8; ++cm) {
+          o[cm][h] *= corr;
+          o[cm][h + 2] *= corr;
+        }
+        mrun[h] = mnew;
+      }
+    }
+    const float me0 = mrun[0] == -INFINITY ? 0.f : mrun[0];
+    const float me1 = mrun[1] == -INFINITY ? 0.f : mrun[1];
+    // ---- O^T += V^T P' (P' = p step fp16; V codes as subnormals c 2^-20)
+#pragma unroll
+    for (int mt = 0; mt < kMt; ++mt) {
+      const float vs0 = *reinterpret_cast<const float*>(rec + swz128(L.v_step() + 4 * (mt * 16 + g)));
+      const float vs1 = *reinterpret_cast<const float*>(rec + swz128(L.v_step() + 4 * (mt * 16 + g + 8)));
+      const float ve0 = *reinterpret_cast<const float*>(rec + swz128(L.v_xmin() + 4 * (mt * 16 + g)));
+      const float ve1 = *reinterpret_cast<const float*>(rec + swz128(L.v_xmin() + 4 * (mt * 16 + g + 8)));
+      const float p00 = ex2(sc[mt][0] - me0), p01 = ex2(sc[mt][1] - me1);
+      const float p10 = ex2(sc[mt][2] - me0), p11 = ex2(sc[mt][3] - me1);
+      lsum[0] += p00 + p10;
+      lsum[1] += p01 + p11;
+      vb[0] = fmaf(p00, ve0, fmaf(p10, ve1, vb[0]));
+      vb[1] = fmaf(p01, ve0, fmaf(p11, ve1, vb[1]));
+      const uint32_t b0 = movm_t(pack_h2(p00 * vs0, p01 * vs0));
+      const uint32_t b1 = movm_t(pack_h2(p10 * vs1, p11 * vs1));
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        uint32_t vr[4];
+        ldsm_x4_t(vr, rec_s + swz128(L.v_codes() + mt * 16 * 64 + 32 * h + lm_off));
+        const Nib v0 = nibs(vr[0]), v1 = nibs(vr[1]), v2 = nibs(vr[2]), v3 = nibs(vr[3]);
+#define OTT_PV4(K) mma16816(o[4 * h + K], vq4<K>(v0), vq4<K>(v2), vq4<K>(v1), vq4<K>(v3), b0, b1);
+        OTT_PV4(0) OTT_PV4(1) OTT_PV4(2) OTT_PV4(3)
+#undef OTT_PV4
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      const int ka = k + kStages;
+      if (ka < my_n) {
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        load_record4(stage0 + s * q4::kSlot, tmap, unit_rec + g0 + warp + ka * kAttnWarps, bar0 + 8 * s);
+      }
+    }
+  }
+  // ---- reduce l, vb over the token rows, merge warps, write the partial
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+#pragma unroll
+    for (int off = 4; off < 32; off <<= 1) {
+      lsum[h] += __shfl_xor_sync(0xffffffffu, lsum[h], off);
+      vb[h] += __shfl_xor_sync(0xffffffffu, vb[h], off);
+    }
+  }
+  if (g == 0) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      sm.mm[warp][2 * tig + h] = mrun[h];
+      sm.ll[warp][2 * tig + h] = lsum[h];
+    }
+  }
+  __syncthreads();  // every warp is past its loop: stage memory is free
+  float* accw = reinterpret_cast<float*>(&sm.stage[warp][0][0]);  // [8 heads][128] natural channel order
+#pragma unroll
+  for (int cm = 0; cm < 8; ++cm) {
+    const int chan = 64 * (cm >> 2) + 4 * g + (cm & 3);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      accw[(2 * tig + h) * D + chan] = fmaf(o[cm][h], 1048576.f, vb[h]);  // 2^20
+      accw[(2 * tig + h) * D + chan + 32] = fmaf(o[cm][h + 2], 1048576.f, vb[h]);
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < NR * D; i += kAttnThreads) {
+    const int r = i / D, col = i % D;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < kAttnWarps; ++w) M = fmaxf(M, sm.mm[w][r]);
+    float Lsum = 0.f, A = 0.f;
+    if (M != -INFINITY) {
+#pragma unroll
+      for (int w = 0; w < kAttnWarps; ++w) {
+        if (sm.mm[w][r] == -INFINITY) continue;
+        const float f = exp2f(sm.mm[w][r] - M);
+        Lsum += sm.ll[w][r] * f;
+        A += reinterpret_cast<const float*>(&sm.stage[w][0][0])[r * D + col] * f;
+      }
+    }
+    float* base = a.ws + (((size_t)u * NR + r) * a.n_splits + split) * (D + 2);
+    base[2 + col] = A;
+    if (col == 0) {
+      base[0] = M;
+      base[1] = Lsum;
+    }
+  }
+}
+
+template <int NR>
+__global__ void __launch_bounds__(kAttnThreads, 4)
+    attend_mma4_kernel(const __grid_constant__ AttnArgs a, const __grid_constant__ CUtensorMap tmap) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  allow_dependents();
+  if ((int)blockIdx.y == a.n_qsplits) {  // full-precision tiers: pool + pending
+    const Counts n = counts_of(a);
+    if (blockIdx.x == 0 && threadIdx.x == 0)  // token counts of this launch for the combine's overflow guard
+      reinterpret_cast<int64_t*>(a.ws + (size_t)a.c.n_units * NR * a.n_splits * 130)[0] = n.q_tokens;
+    fp_body<NR>(a, n, *reinterpret_cast<FpSmem*>(smem_raw));
+  } else {
+    mma4_body<NR>(a, counts_of(a), &tmap, *reinterpret_cast<Mma4Smem*>(smem_raw));
+  }
+}
+
 // ============================================================ tcgen05 path (d = 128, G = 32)
 // Q K^T on the 5th-generation tensor cores, P V on the warp-level path.
 //
@@ -1681,7 +2019,8 @@ __global__ void __launch_bounds__(tc5::kThreads, OTT_TC5_MIN_BLOCKS)
 // handles columns 2*lane, 2*lane+1 (+64, +65 at D = 128) with float2 loads.
 constexpr int kCombineRows = 8;
 template <int D>
-static cudaError_t launch_combine(const AttnArgs& a, int NR, cudaStream_t st, bool tc_path = false);
+static cudaError_t launch_combine(const AttnArgs& a, int NR, cudaStream_t st, bool tc_path = false,
+                                  float umax = 16.f);
 
 // Overflow guard of the 2-bit tensor-core path. Its fp16 operands hold q u step (u <= 16)
 // and 4 p v_step (p <= 2^kLazy); pool_meta[u][3] bounds the unit's K and V steps (flush
@@ -1694,6 +2033,8 @@ struct TcGuard {
   const uint16_t* q;
   int NR;
   float scale_log2;
+  float umax;  // largest position factor u of the K unpack (16 at 2 bits, 64 at 4 bits)
+  int bits;
 };
 // per (unit, head) row: q' of head h only involves q_h
 __device__ __forceinline__ bool tc_row_safe(const TcGuard& gd, int urow, int lane) {
@@ -1704,7 +2045,7 @@ __device__ __forceinline__ bool tc_row_safe(const TcGuard& gd, int urow, int lan
   const float qm = warp_max(fmaxf(fmaxf(a.x, a.y), fmaxf(b.x, b.y)));
   const float smax = __int_as_float(gd.c.pool_meta[(size_t)u * 4 + 3]);
   const float sm1 = fmaxf(smax, 1.f);
-  return smax <= 3.0e38f && 16.f * qm < 6.5e4f && 16.f * qm * sm1 < 6.5e4f && 4.f * 64.f * sm1 < 6.5e4f;
+  return smax <= 3.0e38f && gd.umax * qm < 6.5e4f && gd.umax * qm * sm1 < 6.5e4f && 4.f * 64.f * sm1 < 6.5e4f;
 }
 // quantized-tier partial (m, l, acc[lane + 32 k]) of head r of unit u over [0, q_tokens),
 // float32 dequantization (quant.py:105-111) and online softmax, one warp
@@ -1713,7 +2054,7 @@ __device__ __forceinline__ void tc_guard_partial(const TcGuard& gd, int u, int r
   constexpr int D = 128;
   const ott_cache_t& c = gd.c;
   const int G = c.group_size;
-  const RecordLayout L(D, G, 2);
+  const RecordLayout L(D, G, gd.bits);
   const uint16_t* qrow = gd.q + ((size_t)u * gd.NR + r) * D;
   m = -INFINITY;
   l = 0.f;
@@ -1729,7 +2070,7 @@ __device__ __forceinline__ void tc_guard_partial(const TcGuard& gd, int u, int r
       const int64_t p = (int64_t)gi * G + row;
       float s = 0.f;
       for (int col = 0; col < D; ++col) {  // the slow path: parameters re-read per token
-        const float code = (float)code_at(kc, (int64_t)row * D + col, 2);
+        const float code = (float)code_at(kc, (int64_t)row * D + col, gd.bits);
         const float st = k_step_of(rec, L, col);
         s = fmaf(h2f(qrow[col]) * gd.scale_log2, fmaf(code, st, k_xmin_of(rec, L, col, st)), s);
       }
@@ -1751,7 +2092,7 @@ __device__ __forceinline__ void tc_guard_partial(const TcGuard& gd, int u, int r
         const float vx = reinterpret_cast<const float*>(rec + L.v_xmin())[rw];
         for (int k = 0; k < 4; ++k) {
           const int col = lane + 32 * k;
-          acc[k] = fmaf(pw, fmaf((float)code_at(vc, (int64_t)rw * D + col, 2), vs, vx), acc[k]);
+          acc[k] = fmaf(pw, fmaf((float)code_at(vc, (int64_t)rw * D + col, gd.bits), vs, vx), acc[k]);
         }
       }
     }
@@ -1855,7 +2196,7 @@ __global__ void __launch_bounds__(32 * kCombineRows) combine_kernel(const float*
 }
 
 template <int D>
-static cudaError_t launch_combine(const AttnArgs& a, int NR, cudaStream_t st, bool tc_path) {
+static cudaError_t launch_combine(const AttnArgs& a, int NR, cudaStream_t st, bool tc_path, float umax) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((a.c.n_units * NR + kCombineRows - 1) / kCombineRows);
   cfg.blockDim = dim3(32 * kCombineRows);
@@ -1871,6 +2212,8 @@ static cudaError_t launch_combine(const AttnArgs& a, int NR, cudaStream_t st, bo
   gd.q = a.q;
   gd.NR = NR;
   gd.scale_log2 = a.scale_log2;
+  gd.umax = umax;
+  gd.bits = a.c.bits;
   return cudaLaunchKernelEx(&cfg, combine_kernel<D>, (const float*)a.ws, a.out, a.c.n_units * NR, a.n_splits,
                             const_cast<int64_t*>(a.dev_counts), a.c.group_size, a.c.residual, a.c.max_groups,
                             a.c.head_dim, gd, tc_path ? 1 : 0);
@@ -1962,6 +2305,35 @@ static cudaError_t record_tensor_map(const ott_cache_t& c, int box_rows, int rec
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+// 4-bit records: 2-D uint8 view [rows of 128 B], SWIZZLE_128B, one 42-row box per record
+static cudaError_t record_tensor_map4(const ott_cache_t& c, CUtensorMap* map) {
+  CUtensorMap dummy;
+  cudaError_t e0 = record_tensor_map(c, 1, 1, &dummy);  // resolves the driver entry point
+  if (e0 != cudaSuccess) return e0;
+  const cuuint64_t dims[2] = {128, (cuuint64_t)c.n_units * (cuuint64_t)c.max_groups * (cuuint64_t)q4::kRows};
+  const cuuint64_t strides[1] = {128};
+  const cuuint32_t box[2] = {128, (cuuint32_t)q4::kRows};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, c.blocks, dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+template <int NR>
+static cudaError_t launch_mma4_t(const AttnArgs& a, cudaStream_t st) {
+  CUtensorMap tmap;
+  cudaError_t te = record_tensor_map4(a.c, &tmap);
+  if (te != cudaSuccess) return te;
+  const size_t smem = sizeof(Mma4Smem) > sizeof(FpSmem) ? sizeof(Mma4Smem) : sizeof(FpSmem);
+  cudaError_t e = cudaFuncSetAttribute(attend_mma4_kernel<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  attend_mma4_kernel<NR><<<dim3(a.c.n_units, a.n_splits), kAttnThreads, smem, st>>>(a, tmap);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  return launch_combine<128>(a, NR, st, true, 64.f);
+}
+
 template <int NR, int G>
 static cudaError_t launch_mma_t(const AttnArgs& a, cudaStream_t st) {
   CUtensorMap tmap;
@@ -2004,6 +2376,9 @@ static bool use_tc5() {
 }
 
 bool mma_eligible(const ott_cache_t& c) { return c.head_dim == 128 && c.bits == 2; }
+#ifndef OTT_MMA4  // 4-bit caches at d = 128, G = 32 use the tensor-core kernel (0: CUDA-core kernel)
+#define OTT_MMA4 1
+#endif
 
 // True when the attention kernel can write the step's new rows itself (fp-tier CTA of the
 // tensor-core kernels); otherwise the caller launches the ring write first.
@@ -2040,6 +2415,13 @@ cudaError_t launch_attend(const ott_cache_t& c, const uint16_t* q, uint16_t* out
     if (n_rep == 2) return launch_generic_t<2>(a, st);
     if (n_rep == 4) return launch_generic_t<4>(a, st);
     if (n_rep == 8) return launch_generic_t<8>(a, st);
+    return cudaErrorInvalidValue;
+  }
+  if (OTT_MMA4 && c.bits == 4 && D == 128 && G == 32) {  // 4-bit tensor-core kernel
+    if (n_rep == 1) return launch_mma4_t<1>(a, st);
+    if (n_rep == 2) return launch_mma4_t<2>(a, st);
+    if (n_rep == 4) return launch_mma4_t<4>(a, st);
+    if (n_rep == 8) return launch_mma4_t<8>(a, st);
     return cudaErrorInvalidValue;
   }
   if (c.bits != 2) {  // other widths: CUDA-core kernel with generic code extraction

@@ -42,21 +42,26 @@ def cfg_of(bits, G, R, N, A, d):
     return EngineConfig(bits=bits, group_size=G, residual=R, outlier_num=N, aux_capacity=A, skip_layers=(), head_dim=d)
 
 
-def expected_k_encoding(step64, xmin64):
+def expected_k_encoding(step64, xmin64, bits=2):
     """The record's K parameter encoding (ott_b200.h) computed from the exact
     float64 params: sh = fp16(step), sl = fp16(step - sh) in pair order, and
-    e = f32(x_min - 4 u(c) step)."""
-    from paper_2505_10938_b200.cache import kpair_index, kpair_u
+    e = f32(x_min - 4 u(c) step) (2-bit) or f32(x_min - 64 step) (4-bit)."""
+    from paper_2505_10938_b200.cache import kpair4_index, kpair_index, kpair_u
     step64 = np.asarray(step64, np.float64)
     xmin64 = np.asarray(xmin64, np.float64)
     d = len(step64)
     sh = step64.astype(np.float16)
     sl = (step64 - sh.astype(np.float64)).astype(np.float16)
-    e = (xmin64 - 4.0 * kpair_u(np.arange(d)).astype(np.float64) * step64).astype(np.float32)
+    if bits == 2:
+        e = (xmin64 - 4.0 * kpair_u(np.arange(d)).astype(np.float64) * step64).astype(np.float32)
+        idx = kpair_index(np.arange(d), d)
+    else:
+        e = (xmin64 - 64.0 * step64).astype(np.float32)
+        idx = kpair4_index(np.arange(d))
     sh_p = np.empty(d, np.float16)
     sl_p = np.empty(d, np.float16)
-    sh_p[kpair_index(np.arange(d), d)] = sh
-    sl_p[kpair_index(np.arange(d), d)] = sl
+    sh_p[idx] = sh
+    sl_p[idx] = sl
     return sh_p, sl_p, e
 
 
@@ -73,8 +78,8 @@ def assert_unit_matches_oracle(u, ref, exact64=True):
             assert [p.step for p in u.quantized_k[b].params] == blk["k_step"].tolist()
             assert [p.x_min for p in u.quantized_v[b].params] == blk["v_xmin"].tolist()
             assert [p.step for p in u.quantized_v[b].params] == blk["v_step"].tolist()
-        if u.config.bits == 2:
-            sh, sl, e = expected_k_encoding(blk["k_step"], blk["k_xmin"])
+        if u.config.bits == 2 or (u.config.bits == 4 and u.config.head_dim % 8 == 0):
+            sh, sl, e = expected_k_encoding(blk["k_step"], blk["k_xmin"], u.config.bits)
             np.testing.assert_array_equal(u.k_sh16[b].view(np.uint16), sh.view(np.uint16))
             np.testing.assert_array_equal(u.k_sl16[b].view(np.uint16), sl.view(np.uint16))
             np.testing.assert_array_equal(u.k_e32[b], e)
@@ -193,7 +198,8 @@ def test_config0_all_heads_bit_exact(N):
         assert ok, (h, err)
 
 
-@pytest.mark.parametrize("bits,d,n_rep", [(1, 128, 1), (3, 64, 4), (4, 128, 8), (8, 64, 2), (5, 128, 4)])
+@pytest.mark.parametrize("bits,d,n_rep", [(1, 128, 1), (3, 64, 4), (4, 128, 8), (4, 128, 1), (4, 128, 4), (8, 64, 2),
+                                          (5, 128, 4)])
 def test_other_bit_widths_vs_oracle(bits, d, n_rep):
     """Bit widths other than 2 (quant.py supports 1..8): flush codes,
     params, pool and packing bit-exact vs the oracle; attention through the CUDA-core
@@ -388,7 +394,7 @@ def test_unsupported_shapes_rejected():
         OTTCache(cfg_of(2, 32, 0, 200, 32, 128), 1, 1, 64)  # pool capacity > 128
 
 
-@pytest.mark.parametrize("bits,N", [(2, 4), (3, 4), (1, 4), (8, 4), (2, 0)])
+@pytest.mark.parametrize("bits,N", [(2, 4), (3, 4), (1, 4), (8, 4), (2, 0), (4, 4), (4, 0)])
 def test_flush_adversarial_lines_vs_oracle(bits, N):
     """Quantization lines built to stress K1's float32 fast path and float64 fallback and the
     frozen-pool kernel's fp16 code thresholds (N = 0: every group takes flush_frozen_kernel):
