@@ -2008,7 +2008,10 @@ __global__ void __launch_bounds__(tc5::kThreads, OTT_TC5_MIN_BLOCKS)
   allow_dependents();
   if ((int)blockIdx.y == (OTT_FP_FIRST ? 0 : a.n_qsplits)) {  // full-precision tiers on warps 0-3
     if (threadIdx.x >= 128) return;
-    fp_body<NR>(a, counts_of(a), *reinterpret_cast<FpSmem*>(smem_raw));
+    const Counts n = counts_of(a);
+    if (blockIdx.x == 0 && threadIdx.x == 0)  // token counts of this launch for the combine's overflow guard
+      reinterpret_cast<int64_t*>(a.ws + (size_t)a.c.n_units * NR * a.n_splits * 130)[0] = n.q_tokens;
+    fp_body<NR>(a, n, *reinterpret_cast<FpSmem*>(smem_raw));
   } else {
     tc5_body<NR>(a, counts_of(a), &tmap, *reinterpret_cast<Tc5Smem*>(smem_raw));
   }
@@ -2360,7 +2363,7 @@ static cudaError_t launch_tc5_t(const AttnArgs& a, cudaStream_t st) {
   attend_tc5_kernel<NR><<<dim3(a.c.n_units, a.n_splits), tc5::kThreads, smem, st>>>(a, tmap);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  return launch_combine<128>(a, NR, st);
+  return launch_combine<128>(a, NR, st, true);
 }
 
 // Attention kernel for (d = 128, G = 32): the mma.sync kernel (default, faster as
