@@ -1237,6 +1237,219 @@ __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen_kernel(ott_cac
   note_step_max(meta3, fmaxf(kst_max, vst));
 }
 
+// K1b for 4-bit codes (d = 128, G = 32): one warp per group after flush_scan_kernel, the same
+// staging as flush_frozen_kernel; substituted groups (sel != 0) are handled inline (float64
+// column sums of the original rows, float32 means, outlier.py:120-142). Codes take the float32
+// fast path with the float64 recipe as fallback (levels = 15 would need 15 thresholds).
+__global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen4_kernel(ott_cache_t c, int64_t q0, int n_groups,
+                                                                          int64_t ring_end,
+                                                                          const uint16_t* __restrict__ in_k,
+                                                                          const uint16_t* __restrict__ in_v,
+                                                                          int64_t in_stride, int64_t in_first) {
+  constexpr int D = 128, G = 32, kLevels = 15;
+  extern __shared__ __align__(16) unsigned char smem[];
+  FrozenSmem& sm = *reinterpret_cast<FrozenSmem*>(smem);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t item = (int64_t)blockIdx.x * kFrozenWarps + warp;
+  if (item >= (int64_t)c.n_units * n_groups) return;
+  const int u = (int)(item / n_groups), g = (int)(item % n_groups);
+  const int cap = G + c.residual;
+  const int base = (int)(q0 + (int64_t)g * G);
+  const int64_t gi = base / G;
+  uint8_t* rec = record_ptr(c, u, gi);
+  const RecordLayout L(D, G, 4);
+  uint16_t* sk = sm.k[warp];
+  uint16_t* sv = sm.v[warp];
+  const uint32_t sel = c.subst_mask[(size_t)u * mask_words_per_unit(c) + (base >> 5)];
+  {
+    const int bslot = base % cap, ring_end32 = (int)ring_end, in_first32 = (int)in_first;
+    const int ch = lane & 15;
+#pragma unroll 4
+    for (int it = 0; it < G / 2; ++it) {
+      const int row = 2 * it + (lane >> 4);
+      const int p = base + row;
+      const uint16_t *pk, *pv;
+      if (p < ring_end32) {
+        int sl = bslot + row;
+        sl = sl >= cap ? sl - cap : sl;
+        const size_t off = ((size_t)u * cap + (size_t)sl) * D + ch * 8;
+        pk = c.pend_k + off;
+        pv = c.pend_v + off;
+      } else {
+        const size_t off = (size_t)u * in_stride + (size_t)(p - in_first32) * D + ch * 8;
+        pk = in_k + off;
+        pv = in_v + off;
+      }
+      cp_async16(sk + row * D + ch * 8, pk);
+      cp_async16(sv + row * D + ((ch ^ (row & 15)) * 8), pv);
+    }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    __syncwarp();
+  }
+  double* p64 = c.params64 ? c.params64 + ((size_t)u * c.max_groups + (size_t)gi) * 2 * (D + G) : nullptr;
+  const double eps = 1e-9 * (double)(kLevels + 1);
+  int32_t* meta3 = c.pool_meta + (size_t)u * 4 + 3;
+  float kst_max = 0.f, vst = 0.f;
+  const uint2* kr = reinterpret_cast<const uint2*>(sk) + lane;
+  // ---- K: channels 4 lane .. +3
+  {
+    float mean[4] = {0.f, 0.f, 0.f, 0.f};
+    if (sel) {
+      double sum[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int t = 0; t < G; ++t) {
+        const uint2 r = kr[t * (D / 4)];
+        const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&r.x));
+        const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&r.y));
+        sum[0] = __dadd_rn(sum[0], (double)a.x);
+        sum[1] = __dadd_rn(sum[1], (double)a.y);
+        sum[2] = __dadd_rn(sum[2], (double)b.x);
+        sum[3] = __dadd_rn(sum[3], (double)b.y);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) mean[j] = __double2float_rn(__ddiv_rn(sum[j], (double)G));
+    }
+    auto kval = [&](int t, float (&x)[4]) {
+      if ((sel >> t) & 1u) {
+        x[0] = mean[0]; x[1] = mean[1]; x[2] = mean[2]; x[3] = mean[3];
+      } else {
+        const uint2 r = kr[t * (D / 4)];
+        const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&r.x));
+        const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&r.y));
+        x[0] = a.x; x[1] = a.y; x[2] = b.x; x[3] = b.y;
+      }
+    };
+    float fmn[4] = {3.4e38f, 3.4e38f, 3.4e38f, 3.4e38f}, fmx[4] = {-3.4e38f, -3.4e38f, -3.4e38f, -3.4e38f};
+    for (int t = 0; t < G; ++t) {
+      float x[4];
+      kval(t, x);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        fmn[j] = fminf(fmn[j], x[j]);
+        fmx[j] = fmaxf(fmx[j], x[j]);
+      }
+    }
+    double step[4], inv[4];
+    FastLine fl[4];
+    __half* ksh = reinterpret_cast<__half*>(rec + L.k_sh());
+    __half* ksl = reinterpret_cast<__half*>(rec + L.k_sl());
+    float ke[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int col = 4 * lane + j;
+      const double mn = (double)fmn[j];
+      line_params(mn, (double)fmx[j], (double)kLevels, step[j]);
+      inv[j] = step[j] > 0.0 ? __drcp_rn(step[j]) : 0.0;
+      fl[j] = fast_line(fmn[j], fmx[j], step[j], inv[j], kLevels);
+      kst_max = fmaxf(kst_max, (float)step[j]);
+      const __half sh = __double2half(step[j]);
+      const __half sl = __double2half(__dsub_rn(step[j], (double)__half2float(sh)));
+      ksh[kpair4_index(col)] = sh;
+      ksl[kpair4_index(col)] = sl;
+      ke[j] = __double2float_rn(__dsub_rn(mn, __dmul_rn(64.0, step[j])));
+      if (p64) {
+        p64[col] = mn;
+        p64[D + col] = step[j];
+      }
+    }
+    *reinterpret_cast<float4*>(rec + L.k_e() + 16 * lane) = make_float4(ke[0], ke[1], ke[2], ke[3]);
+    uint16_t* kcodes = reinterpret_cast<uint16_t*>(rec + L.k_codes()) + lane;  // channels 4 lane..+3 of token t
+#pragma unroll 4
+    for (int t = 0; t < G; ++t) {
+      float x[4];
+      kval(t, x);
+      uint32_t h = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        bool slow;
+        int code = quant_code_f32(x[j], fmn[j], fmx[j], kLevels, fl[j], slow);
+        if (slow) code = quant_code_slow(x[j], fmn[j], fmx[j], (double)fmn[j], step[j], inv[j], kLevels, eps);
+        h |= (uint32_t)code << (4 * j);
+      }
+      kcodes[t * (D / 4)] = (uint16_t)h;
+    }
+  }
+  // ---- V column means (substituted groups only): lane l sums channels 4l..4l+3
+  if (sel) {
+    double sum[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int t = 0; t < G; ++t) {
+      const uint2 r = *reinterpret_cast<const uint2*>(sv + t * D + (((lane >> 1) ^ (t & 15)) * 8) + (lane & 1) * 4);
+      const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&r.x));
+      const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&r.y));
+      sum[0] = __dadd_rn(sum[0], (double)a.x);
+      sum[1] = __dadd_rn(sum[1], (double)a.y);
+      sum[2] = __dadd_rn(sum[2], (double)b.x);
+      sum[3] = __dadd_rn(sum[3], (double)b.y);
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) sm.vmean[warp][4 * lane + j] = __double2float_rn(__ddiv_rn(sum[j], (double)G));
+    __syncwarp();
+  }
+  // ---- V: token `lane`
+  {
+    const int t = lane;
+    const bool subst = (sel >> t) & 1u;
+    const uint4* vr = reinterpret_cast<const uint4*>(sv + t * D);
+    const int sw = t & 15;
+    const float* vm = sm.vmean[warp];
+    auto vval = [&](int j, float (&x)[8]) {  // channels 8j..8j+7
+      if (subst) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) x[e] = vm[8 * j + e];
+      } else {
+        const uint4 r = vr[j ^ sw];
+        const __half2* h = reinterpret_cast<const __half2*>(&r);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __half22float2(h[e]);
+          x[2 * e] = f.x;
+          x[2 * e + 1] = f.y;
+        }
+      }
+    };
+    float fmn = 3.4e38f, fmx = -3.4e38f;
+    for (int j = 0; j < D / 8; ++j) {
+      float x[8];
+      vval(j, x);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        fmn = fminf(fmn, x[e]);
+        fmx = fmaxf(fmx, x[e]);
+      }
+    }
+    const double mn = (double)fmn;
+    double step;
+    line_params(mn, (double)fmx, (double)kLevels, step);
+    const double inv = step > 0.0 ? __drcp_rn(step) : 0.0;
+    const FastLine fl = fast_line(fmn, fmx, step, inv, kLevels);
+    vst = (float)step;
+    reinterpret_cast<float*>(rec + L.v_step())[t] = __double2float_rn(step);
+    reinterpret_cast<float*>(rec + L.v_xmin())[t] = __double2float_rn(mn);
+    if (p64) {
+      p64[2 * D + t] = mn;
+      p64[2 * D + G + t] = step;
+    }
+    uint32_t w[D / 8];
+#pragma unroll
+    for (int j = 0; j < D / 8; ++j) {  // chunk j = channels 8j..8j+7 = word j (nibbles)
+      float x[8];
+      vval(j, x);
+      uint32_t bits = 0;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        bool slow;
+        int code = quant_code_f32(x[e], fmn, fmx, kLevels, fl, slow);
+        if (slow) code = quant_code_slow(x[e], fmn, fmx, mn, step, inv, kLevels, eps);
+        bits |= (uint32_t)code << (4 * e);
+      }
+      w[j] = bits;
+    }
+    uint4* vcodes = reinterpret_cast<uint4*>(rec + L.v_codes() + t * (D / 2));
+#pragma unroll
+    for (int q = 0; q < 4; ++q) vcodes[q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+  }
+  note_step_max(meta3, fmaxf(kst_max, vst));
+}
+
 // K4: ring write. One thread per 8 halves.
 __global__ void ring_write_kernel(ott_cache_t c, const uint16_t* __restrict__ k, const uint16_t* __restrict__ v,
                                   int64_t in_stride, int64_t in_first, int64_t first_pos, int64_t n_rows,
@@ -1286,8 +1499,8 @@ cudaError_t launch_flush(const ott_cache_t& c, int64_t q0, int n_groups, int64_t
   // bulk flushes at the tensor-core shapes: the sequential kernel runs only the pool
   // competition (scoring, OutlierPool.update, masks, pool/aux rows) group by group, then
   // flush_frozen_kernel substitutes and quantizes all groups in parallel
-  const bool split = OTT_FLUSH_SPLIT && !dev_counts && n_groups > 1 && c.bits == 2 && c.head_dim == 128 &&
-                     c.group_size == 32;
+  const bool split = OTT_FLUSH_SPLIT && !dev_counts && n_groups > 1 && (c.bits == 2 || c.bits == 4) &&
+                     c.head_dim == 128 && c.group_size == 32;
   if (!split) {
     flush_kernel<<<c.n_units, kFlushThreads, smem, st>>>(c, q0, n_groups, ring_end, in_k, in_v, in_stride, in_first,
                                                            dev_counts);
@@ -1299,9 +1512,16 @@ cudaError_t launch_flush(const ott_cache_t& c, int64_t q0, int n_groups, int64_t
       c, q0, n_groups, ring_end, in_k, in_v, in_stride, in_first);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
+  const int64_t items = (int64_t)c.n_units * n_groups;
+  if (c.bits == 4) {
+    e = cudaFuncSetAttribute(flush_frozen4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FrozenSmem));
+    if (e != cudaSuccess) return e;
+    flush_frozen4_kernel<<<(unsigned)((items + kFrozenWarps - 1) / kFrozenWarps), 32 * kFrozenWarps,
+                           sizeof(FrozenSmem), st>>>(c, q0, n_groups, ring_end, in_k, in_v, in_stride, in_first);
+    return cudaGetLastError();
+  }
   e = cudaFuncSetAttribute(flush_frozen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FrozenSmem));
   if (e != cudaSuccess) return e;
-  const int64_t items = (int64_t)c.n_units * n_groups;
   flush_frozen_kernel<<<(unsigned)((items + kFrozenWarps - 1) / kFrozenWarps), 32 * kFrozenWarps, sizeof(FrozenSmem),
                         st>>>(c, q0, n_groups, ring_end, in_k, in_v, in_stride, in_first);
   return cudaGetLastError();

@@ -1,2 +1,4 @@
-ncu --set full --clock-control none --import-source on -k regex:attend_mma4 -s 1 -c 1 -o gpurun_out/mma4_v1 python tools/prof_attend.py --batch 128 --rep 8 --ctx 16384 --iters 2 --bits 4 > gpurun_out/ncu_mma4.log 2>&1
-tail -1 gpurun_out/ncu_mma4.log
+timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -2
+python tools/prof_flush.py --batch 128 --kv 8 --ctx 16384 --reps 2 --bits 4
+python tools/prof_flush.py --batch 4 --kv 32 --ctx 32768 --pool 3 --reps 2 --bits 4
+python tools/prof_flush.py --batch 128 --kv 8 --ctx 16384 --reps 2
