@@ -44,7 +44,7 @@ def unit_bytes(wl, Tq, Tp, pool_rows, ref_accounting=False):
     """Algorithmic HBM bytes one attend launch reads/writes per (batch, kv-head)
     unit: codes + params + full-precision tiers + q/out."""
     d, G = wl.head_dim, wl.group_size
-    codes = 2 * Tq * d * 2 // 8
+    codes = 2 * Tq * d * wl.bits // 8
     if ref_accounting:  # reference cache.py:188-203 accounting: params at 16 bits
         params = (Tq // G) * d * 2 * 2 + Tq * 2 * 2
         mask = 0
@@ -175,7 +175,7 @@ def run_ours(args, wl, rank, world, local_rank):
     b_lo, b_hi = shard_bounds(wl.batch, world, rank)
     B = b_hi - b_lo  # whole sequences per rank (batch x kv-head partitioning)
     H, Hq, d, L = wl.n_kv_heads, wl.n_q_heads, wl.head_dim, wl.n_layers
-    cfg = EngineConfig(bits=2, group_size=wl.group_size, residual=wl.residual, outlier_num=wl.outlier_num,
+    cfg = EngineConfig(bits=wl.bits, group_size=wl.group_size, residual=wl.residual, outlier_num=wl.outlier_num,
                        aux_capacity=wl.aux_capacity, skip_layers=wl.skip_layers, n_layers=L, n_heads=H, head_dim=d)
     total_steps = 2 * (args.warmup + args.steps) + 8
     max_tokens = wl.context + total_steps
@@ -339,8 +339,8 @@ def run_ours(args, wl, rank, world, local_rank):
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "u2 codes / f32 params / f16 rows, f32 accumulate", "data": "synthetic",
-            "config": {"workload": wl.name, "layers": L, "batch": wl.batch, "n_q_heads": Hq, "n_kv_heads": H,
+            "vs_baseline": None, "dtype": f"u{wl.bits} codes / f32 params / f16 rows, f32 accumulate", "data": "synthetic",
+            "config": {"workload": wl.name, "bits": wl.bits, "layers": L, "batch": wl.batch, "n_q_heads": Hq, "n_kv_heads": H,
                        "head_dim": d, "context": wl.context, "group_size": wl.group_size, "residual": wl.residual,
                        "outlier_pool": wl.outlier_num, "aux_capacity": wl.aux_capacity,
                        "skip_layers": list(wl.skip_layers), "partition": f"batch/{world} x all kv heads per rank",
@@ -439,6 +439,8 @@ def main():
     ap.add_argument("--config", default="c4")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--bits", type=int, default=2, help="code width of the cache (BASELINE: 2)")
+    ap.add_argument("--layers", type=int, default=0, help="override the workload's layer count (variants)")
     args = ap.parse_args()
     from paper_2505_10938_b200.workloads import WORKLOADS
 
@@ -454,6 +456,14 @@ def main():
         run_c1(args, rank, world, local_rank)
         return
     wl = WORKLOADS[args.config]
+    if args.bits != 2:  # a non-BASELINE variant, named as such
+        import dataclasses
+
+        wl = dataclasses.replace(wl, bits=args.bits, name=f"{wl.name}-{args.bits}bit")
+    if args.layers:
+        import dataclasses
+
+        wl = dataclasses.replace(wl, n_layers=args.layers, name=f"{wl.name}-{args.layers}L")
     if args.impl == "reference":
         run_reference(args, wl, rank, world)
         return

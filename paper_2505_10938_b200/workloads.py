@@ -27,6 +27,7 @@ class Workload:
     outlier_num: int = 32
     aux_capacity: int = 32
     skip_layers: tuple = ()
+    bits: int = 2
 
     @property
     def n_rep(self) -> int:
