@@ -85,7 +85,9 @@ typedef struct {
   double* aux_score;    /* [n_units][A] */
   uint16_t* aux_k;      /* fp16 [n_units][A][d] */
   uint16_t* aux_v;
-  int32_t* pool_meta;   /* [n_units][4] = {n_entries, n_aux, frozen, 0} */
+  int32_t* pool_meta;   /* [n_units][4] = {n_entries, n_aux, frozen, float bits of the largest
+                           2/4-bit K or V step flushed (overflow guard of the tensor-core
+                           attention; start at 0)} */
   double* params64;     /* optional [n_units][max_groups][2*(d+G)] exact float64 params
                            (k_xmin[d], k_step[d], v_xmin[G], v_step[G]); NULL = off */
 } ott_cache_t;
