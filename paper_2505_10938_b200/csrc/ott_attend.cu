@@ -1089,13 +1089,15 @@ __device__ void fp_body(const AttnArgs& a, const Counts& n, FpSmem& sm) {
       const int rows = is_pool ? min(16, N - 16 * t) : min(16, Tp - 16 * (t - n_pool_t));
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(rows * 512)
                    : "memory");
+      // ring slot of the tile's first pending row, then consecutive slots (one modulo per tile)
+      int slot = is_pool ? 0 : (int)((n.q_tokens + 16 * (t - n_pool_t)) % cap);
       for (int r = 0; r < rows; ++r) {
         size_t off;
         if (is_pool) {
           off = ((size_t)u * N + 16 * t + r) * D;
         } else {
-          const int64_t p = n.q_tokens + 16 * (t - n_pool_t) + r;
-          off = ((size_t)u * cap + (size_t)(p % cap)) * D;
+          off = ((size_t)u * cap + (size_t)slot) * D;
+          slot = slot + 1 == cap ? 0 : slot + 1;
         }
         tma_row(kr_s + r * kRow, (is_pool ? c.pool_k : c.pend_k) + off, bar);
         tma_row(vr_s + r * kRow, (is_pool ? c.pool_v : c.pend_v) + off, bar);

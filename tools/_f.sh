@@ -1,1 +1,2 @@
-python bench.py --bits 4 --layers 48 --no-cpu > gpurun_out/bench_4bit.jsonl 2> gpurun_out/bench_4bit.err; tail -1 gpurun_out/bench_4bit.jsonl | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['e2e']['value'], d['roofline'], d['prefill']['ms_per_layer'], d['clocks'])"; tail -2 gpurun_out/bench_4bit.err
+timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -1
+bash tools/run_var2.sh prev base prev base
