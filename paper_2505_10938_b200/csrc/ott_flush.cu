@@ -14,6 +14,9 @@ constexpr int kFlushThreads = 256;
 #ifndef OTT_FROZEN_SEL  // timing experiment only when 0 (substituted groups quantized wrongly)
 #define OTT_FROZEN_SEL 1
 #endif
+#ifndef OTT_FLUSH_PRESCORE  // parallel token scoring ahead of the pool scan when N < A
+#define OTT_FLUSH_PRESCORE 1
+#endif
 #ifndef OTT_FLUSH_SPLIT  // bulk flush = sequential kernel until the pool freezes + parallel frozen-pool kernel
 #define OTT_FLUSH_SPLIT 1
 #endif
@@ -582,6 +585,43 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gsrc) : "memory");
 }
 
+// K1a': score_tokens (outlier.py:45-49) for every token of a bulk flush in parallel, ahead of
+// flush_scan_kernel (used when the pool is expected to stay active for many groups, N < A):
+// one warp per group, lane t sums |k| of token t in float64 (exact) and leaves the 32 scores
+// in the first 256 bytes of the group's record, which flush_frozen_kernel overwrites later.
+__global__ void __launch_bounds__(128) flush_score_kernel(ott_cache_t c, int64_t q0, int n_groups, int64_t ring_end,
+                                                          const uint16_t* __restrict__ in_k, int64_t in_stride,
+                                                          int64_t in_first) {
+  constexpr int D = 128, G = 32;
+  const int lane = threadIdx.x & 31;
+  const int64_t item = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (item >= (int64_t)c.n_units * n_groups) return;
+  const int u = (int)(item / n_groups), g = (int)(item % n_groups);
+  if (c.pool_meta[(size_t)u * 4 + 2]) return;  // frozen: nothing will read the scores
+  const int cap = G + c.residual;
+  const int base = (int)(q0 + (int64_t)g * G), p = base + lane;
+  const uint16_t* row;
+  if (p < (int)ring_end) {
+    row = c.pend_k + ((size_t)u * cap + (size_t)(p % cap)) * D;
+  } else {
+    row = in_k + (size_t)u * in_stride + (size_t)(p - (int)in_first) * D;
+  }
+  const uint4* kr = reinterpret_cast<const uint4*>(row);
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll 4
+  for (int j = 0; j < D / 8; ++j) {
+    const uint4 r = kr[j];
+    const __half2* h = reinterpret_cast<const __half2*>(&r);
+    const float2 f0 = __half22float2(h[0]), f1 = __half22float2(h[1]), f2 = __half22float2(h[2]),
+                 f3 = __half22float2(h[3]);
+    a0 = __dadd_rn(a0, __dadd_rn(fabs((double)f0.x), fabs((double)f0.y)));
+    a1 = __dadd_rn(a1, __dadd_rn(fabs((double)f1.x), fabs((double)f1.y)));
+    a2 = __dadd_rn(a2, __dadd_rn(fabs((double)f2.x), fabs((double)f2.y)));
+    a3 = __dadd_rn(a3, __dadd_rn(fabs((double)f3.x), fabs((double)f3.y)));
+  }
+  reinterpret_cast<double*>(record_ptr(c, u, base / G))[lane] = __dadd_rn(__dadd_rn(a0, a1), __dadd_rn(a2, a3));
+}
+
 // K1a: the sequential part of a bulk flush (cache.py:158-173 for every group in order):
 // score_tokens, OutlierPool.update, the pool/aux rows and the pool/substitution bitmasks.
 // One warp per unit; lane t scores token t of each group; the competition is the same
@@ -603,7 +643,8 @@ struct ScanSmem {
 __global__ void __launch_bounds__(32 * kScanWarps) flush_scan_kernel(ott_cache_t c, int64_t q0, int n_groups,
                                                                      int64_t ring_end, const uint16_t* __restrict__ in_k,
                                                                      const uint16_t* __restrict__ in_v,
-                                                                     int64_t in_stride, int64_t in_first) {
+                                                                     int64_t in_stride, int64_t in_first,
+                                                                     bool prescored) {
   constexpr int D = 128, G = 32;
   extern __shared__ __align__(16) unsigned char smem[];
   ScanSmem& sm = *reinterpret_cast<ScanSmem*>(smem);
@@ -655,15 +696,20 @@ __global__ void __launch_bounds__(32 * kScanWarps) flush_scan_kernel(ott_cache_t
     }
     return in + (size_t)u * in_stride + (size_t)(p - in_first32) * D;
   };
-  // K rows of group g -> stage g % kScanStages (one cp.async group per load)
+  // K rows of group g -> stage g % kScanStages (one cp.async group per load); pre-scored:
+  // the group's 32 float64 scores (flush_score_kernel left them in its record)
   auto load_group = [&](int g) {
     if (g < n_groups) {
       uint16_t* dst = sm.rows[warp][g % kScanStages];
       const int base = q0i + g * G, ch = lane & 15;
+      if (prescored) {
+        if (lane < 16) cp_async16(dst + 8 * lane, record_ptr(c, u, base / G) + 16 * lane);
+      } else {
 #pragma unroll 4
-      for (int it = 0; it < G / 2; ++it) {
-        const int row = 2 * it + (lane >> 4);
-        cp_async16(dst + row * D + ((ch ^ (row & 15)) * 8), row_of(base + row, c.pend_k, in_k) + ch * 8);
+        for (int it = 0; it < G / 2; ++it) {
+          const int row = 2 * it + (lane >> 4);
+          cp_async16(dst + row * D + ((ch ^ (row & 15)) * 8), row_of(base + row, c.pend_k, in_k) + ch * 8);
+        }
       }
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
@@ -680,7 +726,9 @@ __global__ void __launch_bounds__(32 * kScanWarps) flush_scan_kernel(ott_cache_t
     const uint16_t* srow = sm.rows[warp][g % kScanStages];
     // ---- score_tokens (outlier.py:45-49): L1 norm of key row `lane` in float64 (exact)
     double sc;
-    {
+    if (prescored) {
+      sc = reinterpret_cast<const double*>(srow)[lane];
+    } else {
       const uint4* kr = reinterpret_cast<const uint4*>(srow + lane * D);
       const int sw = lane & 15;
       double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
@@ -774,7 +822,10 @@ __global__ void __launch_bounds__(32 * kScanWarps) flush_scan_kernel(ott_cache_t
       const int widx = __popc(wins & ((1u << i) - 1u));
       const int s = free_slot[widx];
       const int p = base + i, j = lane & 15;
-      if (lane < 16) reinterpret_cast<uint4*>(pk + (size_t)s * D)[j] = reinterpret_cast<const uint4*>(srow + i * D)[j ^ (i & 15)];
+      if (lane < 16)
+        reinterpret_cast<uint4*>(pk + (size_t)s * D)[j] =
+            prescored ? reinterpret_cast<const uint4*>(row_of(p, c.pend_k, in_k))[j]
+                      : reinterpret_cast<const uint4*>(srow + i * D)[j ^ (i & 15)];
       else reinterpret_cast<uint4*>(pv + (size_t)s * D)[j] = reinterpret_cast<const uint4*>(row_of(p, c.pend_v, in_v))[j];
       if (lane == 0) {
         spos[s] = p;
@@ -1506,10 +1557,20 @@ cudaError_t launch_flush(const ott_cache_t& c, int64_t q0, int n_groups, int64_t
                                                            dev_counts);
     return cudaGetLastError();
   }
+  // a pool that can absorb many evictions before freezing (N < A) stays active for long: score
+  // all tokens in parallel first, so the sequential scan reads 256 B of scores per group
+  const bool prescore = OTT_FLUSH_PRESCORE && c.capacity > 0 && c.capacity < c.aux_capacity;
+  const int64_t n_items = (int64_t)c.n_units * n_groups;
+  if (prescore) {
+    flush_score_kernel<<<(unsigned)((n_items + 3) / 4), 128, 0, st>>>(c, q0, n_groups, ring_end, in_k, in_stride,
+                                                                     in_first);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
   e = cudaFuncSetAttribute(flush_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(ScanSmem));
   if (e != cudaSuccess) return e;
   flush_scan_kernel<<<(c.n_units + kScanWarps - 1) / kScanWarps, 32 * kScanWarps, sizeof(ScanSmem), st>>>(
-      c, q0, n_groups, ring_end, in_k, in_v, in_stride, in_first);
+      c, q0, n_groups, ring_end, in_k, in_v, in_stride, in_first, prescore);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const int64_t items = (int64_t)c.n_units * n_groups;
