@@ -444,6 +444,48 @@ def test_flush_adversarial_lines_vs_oracle(bits, N):
     assert ok, err
 
 
+def test_batch_shards_match_whole_batch():
+    """a rank owns a contiguous batch slice with all its kv heads and needs no
+    exchange but the output all-gather. Two half-batch caches (what two ranks hold) give the
+    same quantization state bit for bit and the same outputs as one whole-batch cache, for
+    bulk prefill, decode appends with flushes, and attention with the same split count."""
+    from paper_2505_10938_b200 import OTTCache
+    from paper_2505_10938_b200.parallel import shard_bounds
+
+    B, Hkv, n_rep, T0, steps, d = 4, 4, 4, 1000, 40, 128
+    k, v, q = config0_batch(21, B * Hkv, T0 + steps)
+    kt = torch.from_numpy(k.reshape(B, Hkv, T0 + steps, d)).cuda()
+    vt = torch.from_numpy(v.reshape(B, Hkv, T0 + steps, d)).cuda()
+    qt = torch.from_numpy(q[:, :n_rep].reshape(B, Hkv * n_rep, d)).cuda()
+    cfg = cfg_of(2, 32, 128, 3, 32, d)
+    whole = OTTCache(cfg, B, Hkv, max_tokens=T0 + steps, keep_f64_params=True)
+    parts = []
+    for r in range(2):
+        lo, hi = shard_bounds(B, 2, r)
+        parts.append((lo, hi, OTTCache(cfg, hi - lo, Hkv, max_tokens=T0 + steps, keep_f64_params=True)))
+    whole.update(kt[:, :, :T0], vt[:, :, :T0])
+    for lo, hi, c in parts:
+        c.update(kt[lo:hi, :, :T0], vt[lo:hi, :, :T0])
+    for t in range(T0, T0 + steps):
+        whole.append(kt[:, :, t].contiguous(), vt[:, :, t].contiguous())
+        for lo, hi, c in parts:
+            c.append(kt[lo:hi, :, t].contiguous(), vt[lo:hi, :, t].contiguous())
+    s = 3
+    out_w = whole.attend(qt, n_splits=s)
+    out_p = torch.cat([c.attend(qt[lo:hi].contiguous(), n_splits=s) for lo, hi, c in parts], 0)
+    torch.testing.assert_close(out_p, out_w, atol=0, rtol=0)  # same kernels, same split: identical
+    for lo, hi, c in parts:
+        for b in range(hi - lo):
+            for h in range(Hkv):
+                x, y = c.unit(b, h), whole.unit(lo + b, h)
+                assert [blk.codes for blk in x.quantized_k] == [blk.codes for blk in y.quantized_k]
+                assert [blk.codes for blk in x.quantized_v] == [blk.codes for blk in y.quantized_v]
+                assert [p.step for blk in x.quantized_k for p in blk.params] == [
+                    p.step for blk in y.quantized_k for p in blk.params]
+                assert [e.position for e in x.pool.entries] == [e.position for e in y.pool.entries]
+                assert x.substituted_positions == y.substituted_positions
+
+
 # --------------------------------------------------------------------------- generic shapes
 
 
