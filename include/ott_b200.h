@@ -56,8 +56,10 @@ typedef enum {
  *   float32 k_e[d]                  per-channel K x_min - 4*u(c)*step, u(c) = 4^(4-P(c%8)),
  *                                   P = {3,4,2,3,4,2,3,4} (fp16 mantissa position of the
  *                                   code pair in the decode kernels)
- *   (bits != 2: the k_sh/k_sl bytes hold float32 step[d] and k_e float32 x_min[d], channel
- *   order: 1-bit steps can exceed the fp16 range)
+ *   (4-bit, d % 8 == 0: sh/sl in 4-bit pair order (8w+k, 8w+k+4), e = x_min - 64 step;
+ *   8-bit, d % 8 == 0: sh/sl in channel order, e = x_min - 1024 step; other widths: the
+ *   k_sh/k_sl bytes hold float32 step[d] and k_e float32 x_min[d], channel order: 1-bit steps
+ *   can exceed the fp16 range)
  *   float32 v_step[G], v_xmin[G]    per-token V params
  *   (record size rounded up to 16 bytes)
  * The exact float64 QuantParams are kept in params64 when it is allocated. 

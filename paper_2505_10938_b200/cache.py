@@ -397,6 +397,9 @@ class UnitView:
             pidx = kpair4_index(np.arange(d))
             kst = self.k_sh16[:, pidx].astype(np.float32) + self.k_sl16[:, pidx].astype(np.float32)
             kmn = (self.k_e32 + np.float32(64) * kst).astype(np.float32)
+        elif cfg.bits == 8 and d % 8 == 0:  # 8-bit tensor-core encoding: channel order, e = x_min - 1024 step
+            kst = self.k_sh16.astype(np.float32) + self.k_sl16.astype(np.float32)
+            kmn = (self.k_e32 + np.float32(1024) * kst).astype(np.float32)
         else:  # other widths: float32 step[d] in the sh/sl bytes, x_min in e
             kst = rec[:, 2 * code_b: 2 * code_b + 4 * d].copy().view(np.float32)
             kmn = self.k_e32.copy()

@@ -1563,6 +1563,311 @@ __global__ void __launch_bounds__(kAttnThreads, 4)
   }
 }
 
+// ============================================================ 8-bit tensor-core path (d = 128, G = 32)
+// As the 4-bit path with byte codes (a record is 9,472 B: 128-byte token rows, SWIZZLE_128B,
+// 10 KB stage slots, 2 stages per warp, 2 CTAs per SM). One PRMT builds an fp16 pair from two
+// code bytes: K as 1024 + c (with exponent byte 0x64, so u = 1 and e = x_min - 1024 step),
+// V as exact subnormals c * 2^-24. K pairs are consecutive channels (c, c+1).
+//   * Q.K^T k-step (h, p): logical columns (2t, 2t+1) = channels 32h + 4t + 2p (+1), columns
+//     (2t+8, 2t+9) = 32h + 16 + 4t + 2p (+1).
+//   * P.V m-tile (h, e): rows g / g+8 = channels 32h + 2g + e / 32h + 16 + 2g + e.
+namespace q8 {
+constexpr int kRec = 32 * 128 * 2 + 2 * 2 * 128 + 4 * 128 + 8 * 32;  // 9,472 B
+constexpr int kSlot = 10240;
+constexpr int kStages = 2;
+constexpr int kRows = kRec / 128;  // 74
+}  // namespace q8
+struct Mma8Smem {
+  float4 qt[8][32];
+  alignas(1024) uint8_t stage[kAttnWarps][q8::kStages][q8::kSlot];
+  alignas(8) uint64_t bar[kAttnWarps][q8::kStages];
+  float mm[kAttnWarps][8], ll[kAttnWarps][8];
+};
+__device__ __forceinline__ void load_record8(uint32_t dst, const CUtensorMap* map, int64_t rec_index, uint32_t bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(q8::kRec) : "memory");
+  tma_tensor_rows(dst, map, (int)(rec_index * q8::kRows), bar);
+}
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;\n" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+  return r;
+}
+
+template <int NR>
+__device__ void mma8_body(const AttnArgs& a, const Counts& n, const CUtensorMap* tmap, Mma8Smem& sm) {
+  constexpr int D = 128, G = 32, kMt = 2, kStages = q8::kStages;
+  const RecordLayout L(D, G, 8);
+  const ott_cache_t& c = a.c;
+  const int u = blockIdx.x, split = blockIdx.y;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, tig = lane & 3;
+  const uint32_t kmagic = 0x64646464u;  // fp16 exponent byte of 1024
+  const int n_groups = (int)(n.q_tokens / G);
+  const int per = (n_groups + a.n_qsplits - 1) / a.n_qsplits;
+  const int g0 = split * per;
+  const int g1 = min(n_groups, g0 + per);
+  const int my_n = g1 > g0 + warp ? (g1 - g0 - warp + kAttnWarps - 1) / kAttnWarps : 0;
+
+  // q (fp32) for the bias: slot s of lane (head h, t) = channels 32 (s >> 1) + 16 (s & 1) + 4t .. +3
+  for (int i = tid; i < 8 * 32; i += kAttnThreads) {
+    const int k = i >> 5, ln = i & 31, h = ln >> 2, t4 = ln & 3;
+    const int ch = 32 * (k >> 1) + 16 * (k & 1) + 4 * t4;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (h < NR) {
+      const uint2 raw = __ldg(reinterpret_cast<const uint2*>(a.q + ((size_t)u * NR + h) * D + ch));
+      const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&raw.x));
+      const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&raw.y));
+      v = make_float4(f0.x, f0.y, f1.x, f1.y);
+    }
+    sm.qt[k][ln] = v;
+  }
+  const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&sm.bar[warp][0]);
+  const uint32_t stage0 = (uint32_t)__cvta_generic_to_shared(&sm.stage[warp][0][0]);
+  if (stage0 & 1023u) __trap();  // SWIZZLE_128B needs 1 KB-aligned stage slots
+  const int64_t unit_rec = (int64_t)u * c.max_groups;
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < kStages; ++s) mbar_init(bar0 + 8 * s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+#pragma unroll
+    for (int s = 0; s < kStages; ++s)
+      if (s < my_n) load_record8(stage0 + s * q8::kSlot, tmap, unit_rec + g0 + warp + s * kAttnWarps, bar0 + 8 * s);
+  }
+  __syncthreads();
+
+  float o[8][4];
+#pragma unroll
+  for (int cm = 0; cm < 8; ++cm) o[cm][0] = o[cm][1] = o[cm][2] = o[cm][3] = 0.f;
+  float mrun[2] = {-INFINITY, -INFINITY}, lsum[2] = {0.f, 0.f}, vb[2] = {0.f, 0.f};
+  const uint32_t* pmask = c.pool_mask + (size_t)u * mask_words_per_unit(c);
+  // ldmatrix rows over 128-byte token rows (+32 h for row quarter h)
+  const uint32_t lm_off = (uint32_t)(((lane & 7) + ((lane >> 3) & 1) * 8) * 128 + (lane >> 4) * 16);
+  // q as fp16 pairs (c, c+1): [h][b][p] = channels 32h + 16b + 4t + 2p (+1)
+  __half2 q16[4][2][2];
+#pragma unroll
+  for (int h = 0; h < 4; ++h)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      const float4 qv = sm.qt[2 * h + b][lane];
+      q16[h][b][0] = __floats2half2_rn(qv.x, qv.y);
+      q16[h][b][1] = __floats2half2_rn(qv.z, qv.w);
+    }
+  const float scale4 = a.scale_log2;
+  for (int k = 0; k < my_n; ++k) {
+    const int gi = g0 + warp + k * kAttnWarps;
+    const uint32_t mword = __ldg(&pmask[gi]);
+    const int s = k % kStages;
+    mbar_wait(bar0 + 8 * s, (uint32_t)((k / kStages) & 1));
+    const uint8_t* rec = &sm.stage[warp][s][0];
+    const uint32_t rec_s = stage0 + s * q8::kSlot;
+    float bias;
+    {
+      float2 acc2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        const int ch = 32 * (kk >> 1) + 16 * (kk & 1) + 4 * tig;
+        const float4 ev = *reinterpret_cast<const float4*>(rec + swz128(L.k_e() + 4 * ch));
+        const float4 qv = sm.qt[kk][lane];
+        acc2[(2 * kk) & 3] = __ffma2_rn(make_float2(qv.x, qv.y), make_float2(ev.x, ev.y), acc2[(2 * kk) & 3]);
+        acc2[(2 * kk + 1) & 3] = __ffma2_rn(make_float2(qv.z, qv.w), make_float2(ev.z, ev.w), acc2[(2 * kk + 1) & 3]);
+      }
+      bias = ((acc2[0].x + acc2[0].y) + (acc2[1].x + acc2[1].y)) + ((acc2[2].x + acc2[2].y) + (acc2[3].x + acc2[3].y));
+    }
+    float ch[kMt][4];
+#pragma unroll
+    for (int mt = 0; mt < kMt; ++mt) ch[mt][0] = ch[mt][1] = ch[mt][2] = ch[mt][3] = 0.f;
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      // K code words: token g / g+8, channels 32h + 4t.. (r0, r1) and 32h + 16 + 4t.. (r2, r3)
+      uint32_t kw[kMt][4];
+#pragma unroll
+      for (int mt = 0; mt < kMt; ++mt) ldsm_x4(kw[mt], rec_s + swz128(L.k_codes() + mt * 16 * 128 + 32 * h + lm_off));
+      // q' = q step (exact fp16 hi/lo): pairs (c, c+1) for c = 32h + 16b + 4t + 2p
+      uint32_t bh[2][2], bl[2][2];
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        const int c0 = 32 * h + 16 * b + 4 * tig;
+        const uint2 sh2 = *reinterpret_cast<const uint2*>(rec + swz128(L.k_sh() + 2 * c0));
+        const uint2 sl2 = *reinterpret_cast<const uint2*>(rec + swz128(L.k_sl() + 2 * c0));
+        const uint32_t shw[2] = {sh2.x, sh2.y}, slw[2] = {sl2.x, sl2.y};
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+          const __half2 sh = *reinterpret_cast<const __half2*>(&shw[p]);
+          const __half2 sl = *reinterpret_cast<const __half2*>(&slw[p]);
+          const __half2 qq = q16[h][b][p];
+          const __half2 H = __hmul2(qq, sh);
+          const __half2 E = __hfma2(qq, sh, __hneg2(H));
+          bh[b][p] = h2_as_u32(H);
+          bl[b][p] = h2_as_u32(__hfma2(qq, sl, E));
+        }
+      }
+#pragma unroll
+      for (int p = 0; p < 2; ++p) {
+        const uint32_t sel = p == 0 ? 0x5140u : 0x5342u;  // bytes (2p, magic, 2p+1, magic)
+#pragma unroll
+        for (int mt = 0; mt < kMt; ++mt) {
+          const uint32_t a0 = prmt(kw[mt][0], kmagic, sel), a1 = prmt(kw[mt][1], kmagic, sel);
+          const uint32_t a2 = prmt(kw[mt][2], kmagic, sel), a3 = prmt(kw[mt][3], kmagic, sel);
+          mma16816(ch[mt], a0, a1, a2, a3, bh[0][p], bh[1][p]);
+          mma16816(ch[mt], a0, a1, a2, a3, bl[0][p], bl[1][p]);
+        }
+      }
+    }
+    float sc[kMt][4];
+    {
+      bias += __shfl_xor_sync(0xffffffffu, bias, 1);
+      bias += __shfl_xor_sync(0xffffffffu, bias, 2);
+      bias *= a.scale_log2;
+      const float bias0 = __shfl_sync(0xffffffffu, bias, 8 * tig);
+      const float bias1 = __shfl_sync(0xffffffffu, bias, 8 * tig + 4);
+#pragma unroll
+      for (int mt = 0; mt < kMt; ++mt) {
+        sc[mt][0] = fmaf(ch[mt][0], scale4, bias0);
+        sc[mt][1] = fmaf(ch[mt][1], scale4, bias1);
+        sc[mt][2] = fmaf(ch[mt][2], scale4, bias0);
+        sc[mt][3] = fmaf(ch[mt][3], scale4, bias1);
+      }
+      if (mword) {
+#pragma unroll
+        for (int mt = 0; mt < kMt; ++mt) {
+          if ((mword >> (mt * 16 + g)) & 1u) sc[mt][0] = sc[mt][1] = -INFINITY;
+          if ((mword >> (mt * 16 + g + 8)) & 1u) sc[mt][2] = sc[mt][3] = -INFINITY;
+        }
+      }
+    }
+    float tmax[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      float t = -INFINITY;
+#pragma unroll
+      for (int mt = 0; mt < kMt; ++mt) t = fmaxf(t, fmaxf(sc[mt][h], sc[mt][h + 2]));
+      tmax[h] = t;
+    }
+    const bool need = tmax[0] > mrun[0] + kLazy || tmax[1] > mrun[1] + kLazy;
+    if (__any_sync(0xffffffffu, need)) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float t = tmax[h];
+        t = fmaxf(t, __shfl_xor_sync(0xffffffffu, t, 4));
+        t = fmaxf(t, __shfl_xor_sync(0xffffffffu, t, 8));
+        t = fmaxf(t, __shfl_xor_sync(0xffffffffu, t, 16));
+        const float mnew = fmaxf(mrun[h], t);
+        const float corr = mnew == -INFINITY ? 1.f : ex2(mrun[h] - mnew);
+        lsum[h] *= corr;
+        vb[h] *= corr;
+#pragma unroll
+        for (int cm = 0; cm < 8; ++cm) {
+          o[cm][h] *= corr;
+          o[cm][h + 2] *= corr;
+        }
+        mrun[h] = mnew;
+      }
+    }
+    const float me0 = mrun[0] == -INFINITY ? 0.f : mrun[0];
+    const float me1 = mrun[1] == -INFINITY ? 0.f : mrun[1];
+    // ---- O^T += V^T P' (P' = p step fp16; V codes as subnormals c 2^-24)
+#pragma unroll
+    for (int mt = 0; mt < kMt; ++mt) {
+      const float vs0 = *reinterpret_cast<const float*>(rec + swz128(L.v_step() + 4 * (mt * 16 + g)));
+      const float vs1 = *reinterpret_cast<const float*>(rec + swz128(L.v_step() + 4 * (mt * 16 + g + 8)));
+      const float ve0 = *reinterpret_cast<const float*>(rec + swz128(L.v_xmin() + 4 * (mt * 16 + g)));
+      const float ve1 = *reinterpret_cast<const float*>(rec + swz128(L.v_xmin() + 4 * (mt * 16 + g + 8)));
+      const float p00 = ex2(sc[mt][0] - me0), p01 = ex2(sc[mt][1] - me1);
+      const float p10 = ex2(sc[mt][2] - me0), p11 = ex2(sc[mt][3] - me1);
+      lsum[0] += p00 + p10;
+      lsum[1] += p01 + p11;
+      vb[0] = fmaf(p00, ve0, fmaf(p10, ve1, vb[0]));
+      vb[1] = fmaf(p01, ve0, fmaf(p11, ve1, vb[1]));
+      const uint32_t b0 = movm_t(pack_h2(p00 * vs0, p01 * vs0));
+      const uint32_t b1 = movm_t(pack_h2(p10 * vs1, p11 * vs1));
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        uint32_t vr[4];
+        ldsm_x4_t(vr, rec_s + swz128(L.v_codes() + mt * 16 * 128 + 32 * h + lm_off));
+        // vr: (token 2t, 2t+1) x 16-bit unit = channels (c, c+1); e picks the channel
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const uint32_t sel = e == 0 ? 0x4240u : 0x4341u;  // bytes (e, zero, 2+e, zero)
+          mma16816(o[2 * h + e], prmt(vr[0], 0u, sel), prmt(vr[2], 0u, sel), prmt(vr[1], 0u, sel),
+                   prmt(vr[3], 0u, sel), b0, b1);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      const int ka = k + kStages;
+      if (ka < my_n) {
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        load_record8(stage0 + s * q8::kSlot, tmap, unit_rec + g0 + warp + ka * kAttnWarps, bar0 + 8 * s);
+      }
+    }
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+#pragma unroll
+    for (int off = 4; off < 32; off <<= 1) {
+      lsum[h] += __shfl_xor_sync(0xffffffffu, lsum[h], off);
+      vb[h] += __shfl_xor_sync(0xffffffffu, vb[h], off);
+    }
+  }
+  if (g == 0) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      sm.mm[warp][2 * tig + h] = mrun[h];
+      sm.ll[warp][2 * tig + h] = lsum[h];
+    }
+  }
+  __syncthreads();
+  float* accw = reinterpret_cast<float*>(&sm.stage[warp][0][0]);
+#pragma unroll
+  for (int cm = 0; cm < 8; ++cm) {
+    const int chan = 32 * (cm >> 1) + 2 * g + (cm & 1);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      accw[(2 * tig + h) * D + chan] = fmaf(o[cm][h], 16777216.f, vb[h]);  // 2^24
+      accw[(2 * tig + h) * D + chan + 16] = fmaf(o[cm][h + 2], 16777216.f, vb[h]);
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < NR * D; i += kAttnThreads) {
+    const int r = i / D, col = i % D;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < kAttnWarps; ++w) M = fmaxf(M, sm.mm[w][r]);
+    float Lsum = 0.f, A = 0.f;
+    if (M != -INFINITY) {
+#pragma unroll
+      for (int w = 0; w < kAttnWarps; ++w) {
+        if (sm.mm[w][r] == -INFINITY) continue;
+        const float f = exp2f(sm.mm[w][r] - M);
+        Lsum += sm.ll[w][r] * f;
+        A += reinterpret_cast<const float*>(&sm.stage[w][0][0])[r * D + col] * f;
+      }
+    }
+    float* base = a.ws + (((size_t)u * NR + r) * a.n_splits + split) * (D + 2);
+    base[2 + col] = A;
+    if (col == 0) {
+      base[0] = M;
+      base[1] = Lsum;
+    }
+  }
+}
+
+template <int NR>
+__global__ void __launch_bounds__(kAttnThreads, 2)
+    attend_mma8_kernel(const __grid_constant__ AttnArgs a, const __grid_constant__ CUtensorMap tmap) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  allow_dependents();
+  if ((int)blockIdx.y == a.n_qsplits) {  // full-precision tiers: pool + pending
+    const Counts n = counts_of(a);
+    if (blockIdx.x == 0 && threadIdx.x == 0)  // token counts of this launch for the combine's overflow guard
+      reinterpret_cast<int64_t*>(a.ws + (size_t)a.c.n_units * NR * a.n_splits * 130)[0] = n.q_tokens;
+    fp_body<NR>(a, n, *reinterpret_cast<FpSmem*>(smem_raw));
+  } else {
+    mma8_body<NR>(a, counts_of(a), &tmap, *reinterpret_cast<Mma8Smem*>(smem_raw));
+  }
+}
+
 // ============================================================ tcgen05 path (d = 128, G = 32)
 // Q K^T on the 5th-generation tensor cores, P V on the warp-level path.
 //
@@ -2325,6 +2630,34 @@ static cudaError_t record_tensor_map4(const ott_cache_t& c, CUtensorMap* map) {
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+static cudaError_t record_tensor_map8(const ott_cache_t& c, CUtensorMap* map) {
+  CUtensorMap dummy;
+  cudaError_t e0 = record_tensor_map(c, 1, 1, &dummy);  // resolves the driver entry point
+  if (e0 != cudaSuccess) return e0;
+  const cuuint64_t dims[2] = {128, (cuuint64_t)c.n_units * (cuuint64_t)c.max_groups * (cuuint64_t)q8::kRows};
+  const cuuint64_t strides[1] = {128};
+  const cuuint32_t box[2] = {128, (cuuint32_t)q8::kRows};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, c.blocks, dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+template <int NR>
+static cudaError_t launch_mma8_t(const AttnArgs& a, cudaStream_t st) {
+  CUtensorMap tmap;
+  cudaError_t te = record_tensor_map8(a.c, &tmap);
+  if (te != cudaSuccess) return te;
+  const size_t smem = sizeof(Mma8Smem) > sizeof(FpSmem) ? sizeof(Mma8Smem) : sizeof(FpSmem);
+  cudaError_t e = cudaFuncSetAttribute(attend_mma8_kernel<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  attend_mma8_kernel<NR><<<dim3(a.c.n_units, a.n_splits), kAttnThreads, smem, st>>>(a, tmap);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  return launch_combine<128>(a, NR, st, true, 1.f);
+}
+
 template <int NR>
 static cudaError_t launch_mma4_t(const AttnArgs& a, cudaStream_t st) {
   CUtensorMap tmap;
@@ -2427,6 +2760,13 @@ cudaError_t launch_attend(const ott_cache_t& c, const uint16_t* q, uint16_t* out
     if (n_rep == 2) return launch_mma4_t<2>(a, st);
     if (n_rep == 4) return launch_mma4_t<4>(a, st);
     if (n_rep == 8) return launch_mma4_t<8>(a, st);
+    return cudaErrorInvalidValue;
+  }
+  if (OTT_MMA4 && c.bits == 8 && D == 128 && G == 32) {  // 8-bit tensor-core kernel
+    if (n_rep == 1) return launch_mma8_t<1>(a, st);
+    if (n_rep == 2) return launch_mma8_t<2>(a, st);
+    if (n_rep == 4) return launch_mma8_t<4>(a, st);
+    if (n_rep == 8) return launch_mma8_t<8>(a, st);
     return cudaErrorInvalidValue;
   }
   if (c.bits != 2) {  // other widths: CUDA-core kernel with generic code extraction

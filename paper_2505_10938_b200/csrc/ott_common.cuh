@@ -69,20 +69,24 @@ __device__ __forceinline__ uint32_t code_at(const uint8_t* codes, int64_t e, int
 // (value 1 + c/64, u = 64). K steps are stored in that pair order, e = x_min - 64 step.
 __host__ __device__ constexpr int kpair4_index(int c) { return 8 * (c / 8) + 2 * (c % 4) + (c % 8) / 4; }
 __host__ __device__ constexpr bool k_tc4(int bits, int d) { return bits == 4 && d % 8 == 0; }
+// 8-bit tensor-core encoding: a byte per code; the unpack pairs consecutive channels
+// (c, c+1) as fp16 1024 + code, so steps are stored in channel order and e = x_min - 1024 step.
+__host__ __device__ constexpr bool k_tc8(int bits, int d) { return bits == 8 && d % 8 == 0; }
 
 // float32 K step / x_min of channel c from the record. 2-bit and 4-bit records hold the
 // tensor-core encodings (sh + sl halves in pair order, e = x_min - 4 u step resp. x_min - 64 step);
 // other widths, whose steps can exceed the fp16 range (1 bit: up to 2 * 65504), hold float32
 // step[d] in the sh/sl bytes and x_min in e.
 __device__ __forceinline__ float k_step_of(const uint8_t* rec, const RecordLayout& L, int c) {
-  if (L.bits != 2 && !k_tc4(L.bits, L.d)) return reinterpret_cast<const float*>(rec + L.k_sh())[c];
-  const int j = L.bits == 2 ? kpair_index(c, L.d) : kpair4_index(c);
+  if (L.bits != 2 && !k_tc4(L.bits, L.d) && !k_tc8(L.bits, L.d)) return reinterpret_cast<const float*>(rec + L.k_sh())[c];
+  const int j = L.bits == 2 ? kpair_index(c, L.d) : (L.bits == 4 ? kpair4_index(c) : c);
   return h2f(reinterpret_cast<const uint16_t*>(rec + L.k_sh())[j]) + h2f(reinterpret_cast<const uint16_t*>(rec + L.k_sl())[j]);
 }
 __device__ __forceinline__ float k_xmin_of(const uint8_t* rec, const RecordLayout& L, int c, float step) {
   const float e = reinterpret_cast<const float*>(rec + L.k_e())[c];
   if (L.bits == 2) return fmaf(4.f * kpair_u(c % 8), step, e);
   if (k_tc4(L.bits, L.d)) return fmaf(64.f, step, e);
+  if (k_tc8(L.bits, L.d)) return fmaf(1024.f, step, e);
   return e;
 }
 __device__ __forceinline__ uint16_t f2h(float f) { return __half_as_ushort(__float2half_rn(f)); }

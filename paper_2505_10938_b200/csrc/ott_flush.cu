@@ -451,13 +451,13 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
         // decode-side encoding (ott_common.cuh): 2-bit: step = sh + sl, e = x_min - 4 u step;
         // other widths: float32 step and x_min
         kst = (float)step;
-        if (c.bits == 2 || k_tc4(c.bits, d)) {
+        if (c.bits == 2 || k_tc4(c.bits, d) || k_tc8(c.bits, d)) {
           const __half sh = __double2half(step);
           const __half sl = __double2half(__dsub_rn(step, (double)__half2float(sh)));
-          const int j = c.bits == 2 ? kpair_index(col, d) : kpair4_index(col);
+          const int j = c.bits == 2 ? kpair_index(col, d) : (c.bits == 4 ? kpair4_index(col) : col);
           ksh[j] = sh;
           ksl[j] = sl;
-          const double off = c.bits == 2 ? 4.0 * (double)kpair_u(col % 8) : 64.0;
+          const double off = c.bits == 2 ? 4.0 * (double)kpair_u(col % 8) : (c.bits == 4 ? 64.0 : 1024.0);
           ke[col] = __double2float_rn(__dsub_rn(mn, __dmul_rn(off, step)));
         } else {
           reinterpret_cast<float*>(ksh)[col] = __double2float_rn(step);
@@ -468,7 +468,7 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
           p64[d + col] = step;
         }
       }
-      if (c.bits == 2 || c.bits == 4) note_step_max(meta + 3, kst);
+      if (c.bits == 2 || c.bits == 4 || c.bits == 8) note_step_max(meta + 3, kst);
     } else {
       // warp vw owns tokens vw + j nvw (j < 32 since G <= 128 and nvw >= 4): the warp reduces
       // each token's min/max, lane j keeps token j's and derives its line parameters (one
@@ -512,7 +512,7 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
           p64[2 * d + G + i] = my_step;
         }
       }
-      if (c.bits == 2 || c.bits == 4) note_step_max(meta + 3, lane < n_my ? (float)my_step : 0.f);
+      if (c.bits == 2 || c.bits == 4 || c.bits == 8) note_step_max(meta + 3, lane < n_my ? (float)my_step : 0.f);
       for (int j = 0; j < n_my; ++j) {
         const int i = vw + j * nvw;
         const float fmn = __shfl_sync(0xffffffffu, my_mn, j), fmx = __shfl_sync(0xffffffffu, my_mx, j);

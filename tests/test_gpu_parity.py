@@ -55,9 +55,12 @@ def expected_k_encoding(step64, xmin64, bits=2):
     if bits == 2:
         e = (xmin64 - 4.0 * kpair_u(np.arange(d)).astype(np.float64) * step64).astype(np.float32)
         idx = kpair_index(np.arange(d), d)
-    else:
+    elif bits == 4:
         e = (xmin64 - 64.0 * step64).astype(np.float32)
         idx = kpair4_index(np.arange(d))
+    else:
+        e = (xmin64 - 1024.0 * step64).astype(np.float32)
+        idx = np.arange(d)
     sh_p = np.empty(d, np.float16)
     sl_p = np.empty(d, np.float16)
     sh_p[idx] = sh
@@ -78,7 +81,7 @@ def assert_unit_matches_oracle(u, ref, exact64=True):
             assert [p.step for p in u.quantized_k[b].params] == blk["k_step"].tolist()
             assert [p.x_min for p in u.quantized_v[b].params] == blk["v_xmin"].tolist()
             assert [p.step for p in u.quantized_v[b].params] == blk["v_step"].tolist()
-        if u.config.bits == 2 or (u.config.bits == 4 and u.config.head_dim % 8 == 0):
+        if u.config.bits == 2 or (u.config.bits in (4, 8) and u.config.head_dim % 8 == 0):
             sh, sl, e = expected_k_encoding(blk["k_step"], blk["k_xmin"], u.config.bits)
             np.testing.assert_array_equal(u.k_sh16[b].view(np.uint16), sh.view(np.uint16))
             np.testing.assert_array_equal(u.k_sl16[b].view(np.uint16), sl.view(np.uint16))
@@ -199,7 +202,7 @@ def test_config0_all_heads_bit_exact(N):
 
 
 @pytest.mark.parametrize("bits,d,n_rep", [(1, 128, 1), (3, 64, 4), (4, 128, 8), (4, 128, 1), (4, 128, 4), (8, 64, 2),
-                                          (5, 128, 4)])
+                                          (8, 128, 8), (8, 128, 1), (5, 128, 4)])
 def test_other_bit_widths_vs_oracle(bits, d, n_rep):
     """Bit widths other than 2 (quant.py supports 1..8): flush codes,
     params, pool and packing bit-exact vs the oracle; attention through the CUDA-core

@@ -1,5 +1,2 @@
-timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -1
-python tools/prof_flush.py --batch 128 --kv 8 --ctx 16384 --reps 2
-python tools/prof_flush.py --batch 128 --kv 8 --ctx 16384 --pool 3 --reps 2
-python tools/prof_flush.py --batch 4 --kv 32 --ctx 32768 --pool 3 --reps 2
-python tools/prof_flush.py --batch 4 --kv 32 --ctx 32768 --pool 3 --reps 2 --bits 4
+OTT_ERRLOG=gpurun_out/err8.log timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -3
+for b in 8 4 2; do python tools/prof_attend.py --batch 128 --rep 8 --ctx 16384 --iters 10 --bits $b 2>&1 | tail -1; done
