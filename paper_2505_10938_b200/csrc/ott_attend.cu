@@ -10,9 +10,9 @@
 //   pool.entries rows           fp16, <= N slots (empty slots masked)
 //   pending rows      [Tq, T)   fp16 ring
 //
-// Grid = (units, n_qsplits + 1): the first n_qsplits CTAs of a unit stream
-// contiguous ranges of quantized group records; the last CTA attends the
-// full-precision tiers. Each CTA writes an online-softmax partial (m, l, acc)
+// Grid = (units, n_qsplits + n_fsplits): the first n_qsplits CTAs of a unit stream
+// contiguous ranges of quantized group records; the last n_fsplits CTAs (1 or 2)
+// attend the full-precision tiers. Each CTA writes an online-softmax partial (m, l, acc)
 // per query head; combine_kernel merges them.
 //
 // Quantized path (d = 128): tensor cores via mma.sync m16n8k16 (f16 in, f32
@@ -49,9 +49,7 @@ __device__ __forceinline__ void allow_dependents() {
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 #endif
 }
-#ifndef OTT_FP_FIRST  // 1: the full-precision-tier CTA of a unit is blockIdx.y == 0 (scheduled first)
-#define OTT_FP_FIRST 0
-#endif  // lazy-rescale threshold (log2 units): p <= 64, P' = 4 p step fits fp16
+// lazy-rescale threshold (log2 units, kLazy above): p <= 64, P' = 4 p step fits fp16
 
 struct AttnArgs {
   ott_cache_t c;
@@ -59,8 +57,9 @@ struct AttnArgs {
   uint16_t* out;
   float* ws;  // [n_units][NR][n_splits][D+2]
   int64_t q_tokens, total_tokens;
-  int n_splits;   // total partials per (unit, head) = n_qsplits + 1
+  int n_splits;   // total partials per (unit, head) = n_qsplits + n_fsplits
   int n_qsplits;  // splits over the quantized region
+  int n_fsplits;  // CTAs sharing the full-precision tiers (1, or 2 for small quantized regions)
   int n_qtiles, n_ptiles, n_rtiles;  // 32-token tiles: quantized, pool, pending
   float scale_log2;                  // log2(e) / float32(sqrt(d))
   uint32_t k_magic;                  // 0x3C003C00 (fp16 1.0 pair), passed at run time so the
@@ -664,7 +663,7 @@ __device__ void mma_body(const AttnArgs& a, const Counts& n, const CUtensorMap* 
   const uint32_t magic = a.k_magic;
   const int n_groups = (int)(n.q_tokens / G);
   const int per = (n_groups + a.n_qsplits - 1) / a.n_qsplits;
-  const int g0 = (split - OTT_FP_FIRST) * per;
+  const int g0 = split * per;
   const int g1 = min(n_groups, g0 + per);
   const int my_n = g1 > g0 + warp ? (g1 - g0 - warp + kAttnWarps - 1) / kAttnWarps : 0;
 
@@ -1071,7 +1070,9 @@ __device__ void fp_body(const AttnArgs& a, const Counts& n, FpSmem& sm) {
   const int v_row = (lane & 7) + ((lane >> 4) & 1) * 8, v_col = ((lane >> 3) & 1) * 16;
   uint32_t phase = 0;
 
-  for (int t = warp; t < n_tiles; t += kAttnWarps) {
+  // the fp-tier CTAs of a unit (n_fsplits of them) interleave the 16-row tiles warp by warp
+  const int f = (int)blockIdx.y - a.n_qsplits;
+  for (int t = warp + kAttnWarps * f; t < n_tiles; t += kAttnWarps * a.n_fsplits) {
     const bool is_pool = t < n_pool_t;
     // row validity of this lane's two rows (g, g+8)
     bool valid[2];
@@ -1213,10 +1214,10 @@ __global__ void __launch_bounds__(kAttnThreads, OTT_MMA_MIN_BLOCKS)
 #ifndef OTT_ABL_TIER  // timing ablation only (results wrong): 1 skip the fp-tier CTAs, 2 skip quantized CTAs
 #define OTT_ABL_TIER 0
 #endif
-  if ((int)blockIdx.y == (OTT_FP_FIRST ? 0 : a.n_qsplits)) {  // full-precision tiers: pool + pending
+  if ((int)blockIdx.y >= a.n_qsplits) {  // full-precision tiers: pool + pending
     if (OTT_ABL_TIER & 1) return;
     const Counts n = counts_of(a);
-    if (blockIdx.x == 0 && threadIdx.x == 0)  // token counts of this launch for the combine's overflow guard
+    if (blockIdx.x == 0 && blockIdx.y == a.n_qsplits && threadIdx.x == 0)  // token counts for the combine's guard
       reinterpret_cast<int64_t*>(a.ws + (size_t)a.c.n_units * NR * a.n_splits * 130)[0] = n.q_tokens;
     fp_body<NR>(a, n, *reinterpret_cast<FpSmem*>(smem_raw));
   } else {
@@ -1553,9 +1554,9 @@ __global__ void __launch_bounds__(kAttnThreads, 4)
     attend_mma4_kernel(const __grid_constant__ AttnArgs a, const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   allow_dependents();
-  if ((int)blockIdx.y == a.n_qsplits) {  // full-precision tiers: pool + pending
+  if ((int)blockIdx.y >= a.n_qsplits) {  // full-precision tiers: pool + pending
     const Counts n = counts_of(a);
-    if (blockIdx.x == 0 && threadIdx.x == 0)  // token counts of this launch for the combine's overflow guard
+    if (blockIdx.x == 0 && blockIdx.y == a.n_qsplits && threadIdx.x == 0)  // token counts for the combine's guard
       reinterpret_cast<int64_t*>(a.ws + (size_t)a.c.n_units * NR * a.n_splits * 130)[0] = n.q_tokens;
     fp_body<NR>(a, n, *reinterpret_cast<FpSmem*>(smem_raw));
   } else {
@@ -1858,9 +1859,9 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
     attend_mma8_kernel(const __grid_constant__ AttnArgs a, const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   allow_dependents();
-  if ((int)blockIdx.y == a.n_qsplits) {  // full-precision tiers: pool + pending
+  if ((int)blockIdx.y >= a.n_qsplits) {  // full-precision tiers: pool + pending
     const Counts n = counts_of(a);
-    if (blockIdx.x == 0 && threadIdx.x == 0)  // token counts of this launch for the combine's overflow guard
+    if (blockIdx.x == 0 && blockIdx.y == a.n_qsplits && threadIdx.x == 0)  // token counts for the combine's guard
       reinterpret_cast<int64_t*>(a.ws + (size_t)a.c.n_units * NR * a.n_splits * 130)[0] = n.q_tokens;
     fp_body<NR>(a, n, *reinterpret_cast<FpSmem*>(smem_raw));
   } else {
@@ -2037,7 +2038,7 @@ __device__ void tc5_body(const AttnArgs& a, const Counts& n, const CUtensorMap* 
   const int g = lane >> 2, tig = lane & 3;
   const int n_groups = (int)(n.q_tokens / G);
   const int per = (((n_groups + a.n_qsplits - 1) / a.n_qsplits) + 3) & ~3;  // whole chunks per split
-  const int g0 = min(n_groups, (split - OTT_FP_FIRST) * per);
+  const int g0 = min(n_groups, split * per);
   const int g1 = min(n_groups, g0 + per);
   const int n_chunks = (g1 - g0 + 3) / 4;
   const int64_t unit_rec = (int64_t)u * c.max_groups;
@@ -2313,10 +2314,10 @@ __global__ void __launch_bounds__(tc5::kThreads, OTT_TC5_MIN_BLOCKS)
     attend_tc5_kernel(const __grid_constant__ AttnArgs a, const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(256) unsigned char smem_raw[];
   allow_dependents();
-  if ((int)blockIdx.y == (OTT_FP_FIRST ? 0 : a.n_qsplits)) {  // full-precision tiers on warps 0-3
+  if ((int)blockIdx.y >= a.n_qsplits) {  // full-precision tiers on warps 0-3
     if (threadIdx.x >= 128) return;
     const Counts n = counts_of(a);
-    if (blockIdx.x == 0 && threadIdx.x == 0)  // token counts of this launch for the combine's overflow guard
+    if (blockIdx.x == 0 && blockIdx.y == a.n_qsplits && threadIdx.x == 0)  // token counts for the combine's guard
       reinterpret_cast<int64_t*>(a.ws + (size_t)a.c.n_units * NR * a.n_splits * 130)[0] = n.q_tokens;
     fp_body<NR>(a, n, *reinterpret_cast<FpSmem*>(smem_raw));
   } else {
@@ -2345,6 +2346,7 @@ struct TcGuard {
   float scale_log2;
   float umax;  // largest position factor u of the K unpack (16 at 2 bits, 64 at 4 bits)
   int bits;
+  int n_qsplits;  // partials [n_qsplits, n_splits) are the full-precision tiers'
 };
 // per (unit, head) row: q' of head h only involves q_h
 __device__ __forceinline__ bool tc_row_safe(const TcGuard& gd, int urow, int lane) {
@@ -2434,14 +2436,22 @@ __global__ void __launch_bounds__(32 * kCombineRows) combine_kernel(const float*
       {
         float m, l, acc[4];
         tc_guard_partial(gd, urow / gd.NR, urow % gd.NR, q_tokens, lane, m, l, acc);
-        const float* fp = ws + ((size_t)urow * n_splits + (n_splits - 1)) * (D + 2);  // fp-tier partial
-        const float M = fmaxf(m, fp[0]);
-        const float fq = m == -INFINITY ? 0.f : exp2f(m - M), ff = fp[0] == -INFINITY ? 0.f : exp2f(fp[0] - M);
-        const float inv = 1.f / (l * fq + fp[1] * ff);
-        for (int k = 0; k < 4; ++k) {
-          const int col = lane + 32 * k;
-          out[(size_t)urow * D + col] = f2h((acc[k] * fq + fp[2 + col] * ff) * inv);
+        // merge with the full-precision-tier partials
+        const float* fp0 = ws + (size_t)urow * n_splits * (D + 2);
+        float M = m;
+        for (int sp = gd.n_qsplits; sp < n_splits; ++sp) M = fmaxf(M, fp0[(size_t)sp * (D + 2)]);
+        const float fq = m == -INFINITY ? 0.f : exp2f(m - M);
+        float Lt = l * fq, At[4];
+        for (int k = 0; k < 4; ++k) At[k] = acc[k] * fq;
+        for (int sp = gd.n_qsplits; sp < n_splits; ++sp) {
+          const float* fp = fp0 + (size_t)sp * (D + 2);
+          if (fp[0] == -INFINITY) continue;
+          const float ff = exp2f(fp[0] - M);
+          Lt += fp[1] * ff;
+          for (int k = 0; k < 4; ++k) At[k] = fmaf(fp[2 + lane + 32 * k], ff, At[k]);
         }
+        const float inv = 1.f / Lt;
+        for (int k = 0; k < 4; ++k) out[(size_t)urow * D + lane + 32 * k] = f2h(At[k] * inv);
         if (dev_counts && blockIdx.x == 0 && threadIdx.x == 0) {
           const int64_t qt = dev_counts[0], tot = dev_counts[1] + 1;
           if (tot - qt - R >= G && qt / G + 1 <= max_groups) dev_counts[0] = qt + G;
@@ -2524,6 +2534,7 @@ static cudaError_t launch_combine(const AttnArgs& a, int NR, cudaStream_t st, bo
   gd.scale_log2 = a.scale_log2;
   gd.umax = umax;
   gd.bits = a.c.bits;
+  gd.n_qsplits = a.n_qsplits;
   return cudaLaunchKernelEx(&cfg, combine_kernel<D>, (const float*)a.ws, a.out, a.c.n_units * NR, a.n_splits,
                             const_cast<int64_t*>(a.dev_counts), a.c.group_size, a.c.residual, a.c.max_groups,
                             a.c.head_dim, gd, tc_path ? 1 : 0);
@@ -2714,6 +2725,9 @@ static bool use_tc5() {
 }
 
 bool mma_eligible(const ott_cache_t& c) { return c.head_dim == 128 && c.bits == 2; }
+#ifndef OTT_FP_SPLIT  // allow two full-precision-tier CTAs per unit (tensor-core kernels)
+#define OTT_FP_SPLIT 1
+#endif
 #ifndef OTT_MMA4  // 4-bit caches at d = 128, G = 32 use the tensor-core kernel (0: CUDA-core kernel)
 #define OTT_MMA4 1
 #endif
@@ -2741,6 +2755,7 @@ cudaError_t launch_attend(const ott_cache_t& c, const uint16_t* q, uint16_t* out
   a.q_tokens = q_tokens;
   a.total_tokens = total;
   a.n_qsplits = n_qsplits;
+  a.n_fsplits = 1;
   a.n_splits = n_qsplits + 1;
   a.n_qtiles = (int)(q_tokens / 32);
   a.n_ptiles = (c.capacity + 31) / 32;
@@ -2754,6 +2769,27 @@ cudaError_t launch_attend(const ott_cache_t& c, const uint16_t* q, uint16_t* out
     if (n_rep == 4) return launch_generic_t<4>(a, st);
     if (n_rep == 8) return launch_generic_t<8>(a, st);
     return cudaErrorInvalidValue;
+  }
+  // tensor-core kernels: two CTAs share a unit's full-precision tiers when the quantized
+  // splits are short (small MHA shapes such as config 1), so the fp tier is not the tail
+  const bool tc_path = (c.bits == 2 && mma_eligible(c)) || (OTT_MMA4 && (c.bits == 4 || c.bits == 8) && D == 128 && G == 32);
+  if (tc_path) {
+    const int64_t ng = dev_counts ? (int64_t)c.max_groups : q_tokens / G;
+    const int64_t per = (ng + n_qsplits - 1) / n_qsplits;
+    const int fp_tiles = (c.capacity + 15) / 16 + (c.group_size + c.residual + 15) / 16;
+    // only if the extra CTAs do not add a wave (4 resident CTAs per SM; 2 for the 8-bit kernel)
+    static int sms = 0;
+    if (!sms) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      if (sms <= 0) sms = 148;
+    }
+    const int64_t slots = (int64_t)sms * (c.bits == 8 ? 2 : 4);
+    const int64_t w1 = ((int64_t)c.n_units * (n_qsplits + 1) + slots - 1) / slots;
+    const int64_t w2 = ((int64_t)c.n_units * (n_qsplits + 2) + slots - 1) / slots;
+    a.n_fsplits = (OTT_FP_SPLIT && per < 96 && fp_tiles >= 6 && w2 == w1) ? 2 : 1;
+    a.n_splits = n_qsplits + a.n_fsplits;
   }
   if (OTT_MMA4 && c.bits == 4 && D == 128 && G == 32) {  // 4-bit tensor-core kernel
     if (n_rep == 1) return launch_mma4_t<1>(a, st);

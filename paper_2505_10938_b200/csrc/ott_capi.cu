@@ -125,8 +125,9 @@ int ott_pick_splits(const ott_cache_t* c, int32_t n_rep, int64_t total_tokens) {
 
 size_t ott_attend_workspace_floats(const ott_cache_t* c, int32_t n_rep, int32_t n_splits) {
   if (!c) return 0;
-  // partials [units][n_rep][splits + 1][d + 2] + 2 floats (the launch's quantized-token count)
-  return (size_t)c->n_units * n_rep * ((n_splits > 0 ? n_splits : 1) + 1) * (c->head_dim + 2) + 2;
+  // partials [units][n_rep][splits + 2][d + 2] (up to two full-precision-tier partials) + 2 floats
+  // (the launch's quantized-token count)
+  return (size_t)c->n_units * n_rep * ((n_splits > 0 ? n_splits : 1) + 2) * (c->head_dim + 2) + 2;
 }
 
 int ott_attend(const ott_cache_t* c, const uint16_t* q, uint16_t* out, int32_t n_rep, int64_t quantized_tokens,
