@@ -907,6 +907,13 @@ __device__ __forceinline__ bool code_thresholds(uint16_t* t, float mnf, float mx
 
 // codes of two fp16 inputs against per-lane thresholds th[0..2]: code at bits 0-1 (low half)
 // and 16-17 (high half). Each compare gives 1.0 or 0.0; 1024 + code is exact in fp16.
+// the same as fp16 bits 1024 + code (bytes: code, 0x64, code', 0x64), unmasked
+__device__ __forceinline__ uint32_t codes_h2_raw(__half2 x, const __half2* th) {
+  const __half2 c = __hadd2(__hadd2(__hge2(x, th[0]), __hge2(x, th[1])), __hadd2(__hge2(x, th[2]), __float2half2_rn(1024.f)));
+  return *reinterpret_cast<const uint32_t*>(&c);
+}
+// four codes from two raw pairs: one PRMT gathers the code bytes, pack4x2 squeezes them
+__device__ __forceinline__ uint32_t codes4(uint32_t raw01, uint32_t raw23) { return pack4x2(__byte_perm(raw01, raw23, 0x6420)); }
 __device__ __forceinline__ uint32_t codes_h2(__half2 x, const __half2* th) {
   const __half2 c = __hadd2(__hadd2(__hge2(x, th[0]), __hge2(x, th[1])), __hadd2(__hge2(x, th[2]), __float2half2_rn(1024.f)));
   return *reinterpret_cast<const uint32_t*>(&c) & 0x00030003u;
@@ -1207,9 +1214,8 @@ __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen_kernel(ott_cac
 #pragma unroll 4
       for (int t = 0; t < G; ++t) {
         const uint2 r = kr[t * (D / 4)];
-        const uint32_t c01 = codes_h2(*reinterpret_cast<const __half2*>(&r.x), t01);
-        const uint32_t c23 = codes_h2(*reinterpret_cast<const __half2*>(&r.y), t23);
-        kcodes[t * (D / 4)] = (uint8_t)(((c01 | (c01 >> 14)) & 0xFu) | (((c23 | (c23 >> 14)) & 0xFu) << 4));
+        kcodes[t * (D / 4)] = (uint8_t)codes4(codes_h2_raw(*reinterpret_cast<const __half2*>(&r.x), t01),
+                                              codes_h2_raw(*reinterpret_cast<const __half2*>(&r.y), t23));
       }
     } else {  // a line without exact thresholds (extreme range): the float64 recipe per element
       for (int t = 0; t < G; ++t) {
@@ -1265,11 +1271,8 @@ __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen_kernel(ott_cac
       const __half2* h = reinterpret_cast<const __half2*>(&r);
       uint32_t bits = 0;
       if (exact) {
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const uint32_t cc = codes_h2(h[e], th);
-          bits |= ((cc | (cc >> 14)) & 0xFu) << (4 * e);
-        }
+        bits = codes4(codes_h2_raw(h[0], th), codes_h2_raw(h[1], th)) |
+               (codes4(codes_h2_raw(h[2], th), codes_h2_raw(h[3], th)) << 8);
       } else {
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
