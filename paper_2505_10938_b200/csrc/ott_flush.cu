@@ -920,10 +920,17 @@ __device__ __forceinline__ uint32_t codes_h2(__half2 x, const __half2* th) {
 }
 
 constexpr int kFrozenWarps = 4;
+#ifndef OTT_FROZEN_PAIR  // 1: two warps per group in the 2-bit kernel (K rows / V rows), 8 KB of rows each
+#define OTT_FROZEN_PAIR 1
+#endif
 struct FrozenSmem {
   uint16_t k[kFrozenWarps][32 * 128];
   uint16_t v[kFrozenWarps][32 * 128];
   float vmean[kFrozenWarps][128];  // V column means of a group with substituted rows
+};
+struct FrozenPairSmem {  // per warp: the K or the V rows of its group
+  uint16_t rows[kFrozenWarps][32 * 128];
+  float vmean[kFrozenWarps][128];
 };
 
 // Groups in which the pool competition selected tokens (cache.py:169-173): their rows are
@@ -932,7 +939,7 @@ struct FrozenSmem {
 // values are float32, so these lines use the float32 fast path / float64 fallback per element
 // instead of fp16 thresholds. `sel` bit t = token t substituted.
 __device__ __forceinline__ void frozen_group_subst(uint8_t* rec, double* p64, const uint16_t* sk, const uint16_t* sv,
-                                                float* vmean, uint32_t sel, int lane, int32_t* meta3) {
+                                                float* vmean, uint32_t sel, int lane, int32_t* meta3, int part) {
   constexpr int D = 128, G = 32, kLevels = 3;
   const RecordLayout L(D, G, 2);
   const double eps = 1e-9 * (double)(kLevels + 1);
@@ -940,7 +947,7 @@ __device__ __forceinline__ void frozen_group_subst(uint8_t* rec, double* p64, co
   float kst_max = 0.f;
   float vst = 0.f;
   // ---- K: channels 4 lane .. +3
-  {
+  if (part != 1) {
     double sum[4] = {0.0, 0.0, 0.0, 0.0};
     for (int t = 0; t < G; ++t) {
       const uint2 r = kr[t * (D / 4)];
@@ -1017,7 +1024,7 @@ __device__ __forceinline__ void frozen_group_subst(uint8_t* rec, double* p64, co
     }
   }
   // ---- V column means: lane l sums channels 4l..4l+3 (chunk l/2, half l&1 of each swizzled row)
-  {
+  if (part != 0) {
     double sum[4] = {0.0, 0.0, 0.0, 0.0};
     for (int t = 0; t < G; ++t) {
       const uint2 r = *reinterpret_cast<const uint2*>(sv + t * D + (((lane >> 1) ^ (t & 15)) * 8) + (lane & 1) * 4);
@@ -1033,7 +1040,7 @@ __device__ __forceinline__ void frozen_group_subst(uint8_t* rec, double* p64, co
     __syncwarp();
   }
   // ---- V: token `lane`
-  {
+  if (part != 0) {
     const int t = lane;
     const bool subst = (sel >> t) & 1u;
     const uint4* vr = reinterpret_cast<const uint4*>(sv + t * D);
@@ -1106,9 +1113,11 @@ __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen_kernel(ott_cac
                                                                          int64_t in_stride, int64_t in_first) {
   constexpr int D = 128, G = 32, kLevels = 3;
   extern __shared__ __align__(16) unsigned char smem[];
-  FrozenSmem& sm = *reinterpret_cast<FrozenSmem*>(smem);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t item = (int64_t)blockIdx.x * kFrozenWarps + warp;
+  // OTT_FROZEN_PAIR: warp pairs share a group, the even warp quantizes K, the odd one V
+  const int part = OTT_FROZEN_PAIR ? (warp & 1) : 2;  // 0 K, 1 V, 2 both
+  const int64_t item = OTT_FROZEN_PAIR ? ((int64_t)blockIdx.x * kFrozenWarps + warp) >> 1
+                                       : (int64_t)blockIdx.x * kFrozenWarps + warp;
   if (item >= (int64_t)c.n_units * n_groups) return;
   const int u = (int)(item / n_groups), g = (int)(item % n_groups);
   const int cap = G + c.residual;
@@ -1116,8 +1125,15 @@ __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen_kernel(ott_cac
   const int64_t gi = base / G;
   uint8_t* rec = record_ptr(c, u, gi);
   const RecordLayout L(D, G, 2);
+#if OTT_FROZEN_PAIR
+  FrozenPairSmem& sm = *reinterpret_cast<FrozenPairSmem*>(smem);
+  uint16_t* sk = sm.rows[warp];
+  uint16_t* sv = sm.rows[warp];
+#else
+  FrozenSmem& sm = *reinterpret_cast<FrozenSmem*>(smem);
   uint16_t* sk = sm.k[warp];
   uint16_t* sv = sm.v[warp];
+#endif
   // tokens of this group substituted by the pool competition (base is 32-aligned); loaded
   // before the rows so its latency overlaps theirs
   const uint32_t sel = c.subst_mask[(size_t)u * mask_words_per_unit(c) + (base >> 5)];
@@ -1142,8 +1158,8 @@ __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen_kernel(ott_cac
         pk = in_k + off;
         pv = in_v + off;
       }
-      cp_async16(sk + row * D + ch * 8, pk);
-      cp_async16(sv + row * D + ((ch ^ (row & 15)) * 8), pv);
+      if (part != 1) cp_async16(sk + row * D + ch * 8, pk);
+      if (part != 0) cp_async16(sv + row * D + ((ch ^ (row & 15)) * 8), pv);
     }
     asm volatile("cp.async.wait_all;\n" ::: "memory");
     __syncwarp();
@@ -1152,14 +1168,14 @@ __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen_kernel(ott_cac
   const double eps = 1e-9 * (double)(kLevels + 1);
   int32_t* meta3 = c.pool_meta + (size_t)u * 4 + 3;
   if (OTT_FROZEN_SEL && sel) {
-    if (OTT_FROZEN_SEL == 1) frozen_group_subst(rec, p64, sk, sv, sm.vmean[warp], sel, lane, meta3);
+    if (OTT_FROZEN_SEL == 1) frozen_group_subst(rec, p64, sk, sv, sm.vmean[warp], sel, lane, meta3, part);
     return;
   }
   float kst_max = 0.f;
   float vst = 0.f;
 
   // ---- K: channels 4 lane .. 4 lane + 3, lines over the G tokens
-  {
+  if (part != 1) {
     __half2 mn01 = __float2half2_rn(65504.f), mn23 = mn01, mx01 = __float2half2_rn(-65504.f), mx23 = mx01;
     const uint2* kr = reinterpret_cast<const uint2*>(sk) + lane;  // row stride D / 4 uint2
 #pragma unroll 8
@@ -1234,7 +1250,7 @@ __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen_kernel(ott_cac
   }
 
   // ---- V: token `lane`, line over the D channels (chunk j of the row at (j ^ (lane & 15)))
-  {
+  if (part != 0) {
     const int t = lane;
     const uint4* vr = reinterpret_cast<const uint4*>(sv + t * D);
     const int sw = t & 15;
@@ -1584,10 +1600,12 @@ cudaError_t launch_flush(const ott_cache_t& c, int64_t q0, int n_groups, int64_t
                            sizeof(FrozenSmem), st>>>(c, q0, n_groups, ring_end, in_k, in_v, in_stride, in_first);
     return cudaGetLastError();
   }
-  e = cudaFuncSetAttribute(flush_frozen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FrozenSmem));
+  const size_t fsm = OTT_FROZEN_PAIR ? sizeof(FrozenPairSmem) : sizeof(FrozenSmem);
+  const int64_t warps = OTT_FROZEN_PAIR ? 2 * items : items;
+  e = cudaFuncSetAttribute(flush_frozen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm);
   if (e != cudaSuccess) return e;
-  flush_frozen_kernel<<<(unsigned)((items + kFrozenWarps - 1) / kFrozenWarps), 32 * kFrozenWarps, sizeof(FrozenSmem),
-                        st>>>(c, q0, n_groups, ring_end, in_k, in_v, in_stride, in_first);
+  flush_frozen_kernel<<<(unsigned)((warps + kFrozenWarps - 1) / kFrozenWarps), 32 * kFrozenWarps, fsm, st>>>(
+      c, q0, n_groups, ring_end, in_k, in_v, in_stride, in_first);
   return cudaGetLastError();
 }
 
