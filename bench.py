@@ -167,7 +167,7 @@ def run_ours(args, wl, rank, world, local_rank):
     import torch.distributed as dist
 
     from paper_2505_10938_b200 import EngineConfig, OTTCache
-    from paper_2505_10938_b200.parallel import all_gather_heads, shard_bounds
+    from paper_2505_10938_b200.parallel import PeerGather, all_gather_heads, shard_bounds
     from paper_2505_10938_b200.workloads import decode_rows, fill_prefill
 
     dev = torch.device("cuda", local_rank)
@@ -211,7 +211,12 @@ def run_ours(args, wl, rank, world, local_rank):
             kin[s, l], vin[s, l] = decode_rows(gen, scales[l], B, H)
     qin = torch.randn((n_sets, L, B, Hq, d), generator=gen, device=dev).half()
     outs = torch.empty((L, B, Hq, d), dtype=torch.float16, device=dev)
-    gathered = torch.empty((L, wl.batch, Hq, d), dtype=torch.float16, device=dev) if world > 1 else None
+    # multi-GPU head-output all-gather: P2P stores fused into the attention's combine kernel
+    # (parallel.PeerGather, default) or a separate NCCL all_gather per layer (OTT_GATHER=nccl)
+    gather_mode = (os.environ.get("OTT_GATHER", "p2p") if world > 1 else "none")
+    pg = PeerGather(caches, Hq) if gather_mode == "p2p" else None
+    gathered = (torch.empty((L, wl.batch, Hq, d), dtype=torch.float16, device=dev)
+                if gather_mode == "nccl" else None)
     splits = [c.splits(wl.n_rep) for c in caches]
 
     launches = {"n": 0}
@@ -228,11 +233,14 @@ def run_ours(args, wl, rank, world, local_rank):
             if ev is not None:
                 ev[l][0].record()
             # append + attend: the attention kernel writes the new K/V row into the ring
-            c.append_attend(kin[s, l], vin[s, l], qin[s, l], out=outs[l], n_splits=splits[l])
+            c.append_attend(kin[s, l], vin[s, l], qin[s, l], out=outs[l] if pg is None else pg.out(l),
+                            n_splits=splits[l])
             if ev is not None:
                 ev[l][1].record()
             launches["n"] += 2
-            if gathered is not None:
+            if pg is not None:
+                pg.wait(l)
+            elif gathered is not None:
                 all_gather_heads(outs[l], out=gathered[l])
 
     for i in range(args.warmup):
@@ -306,7 +314,7 @@ def run_ours(args, wl, rank, world, local_rank):
             def gather(o_local, l):
                 all_gather_heads(o_local, out=gathered[l])
                 return gathered[l][b_lo:b_hi]
-        pipe = HostDecodePipeline(caches, Hq, gather=gather)
+        pipe = HostDecodePipeline(caches, Hq, gather=gather, peer_gather=pg)
         pipe.step(k_h, v_h, q_h, o_h)  # warm-up (streams, events)
         torch.cuda.synchronize()
         if world > 1:
@@ -344,6 +352,9 @@ def run_ours(args, wl, rank, world, local_rank):
                        "head_dim": d, "context": wl.context, "group_size": wl.group_size, "residual": wl.residual,
                        "outlier_pool": wl.outlier_num, "aux_capacity": wl.aux_capacity,
                        "skip_layers": list(wl.skip_layers), "partition": f"batch/{world} x all kv heads per rank",
+                       "gather": {"none": "none (1 GPU)", "nccl": "NCCL all_gather_into_tensor per layer",
+                                  "p2p": "P2P stores fused into the combine kernel + signal-pad barrier per layer"}[
+                           gather_mode],
                        "l2": "working set > L2 (126 MB): %.1f GB of cache per GPU" % (
                            sum(c.hbm_bytes() for c in caches) / 1e9),
                        "prefill_s": round(prefill_s, 2)},

@@ -64,6 +64,8 @@ typedef enum {
  *   (record size rounded up to 16 bytes)
  * The exact float64 QuantParams are kept in params64 when it is allocated. 
  * Per-token bitmasks hold one bit per absolute position (32 per word). */
+#define OTT_MAX_OUT_PEERS 7 /* peer GPUs of an 8-GPU NVSwitch node */
+
 typedef struct {
   int32_t n_units;      /* batch * n_kv_heads */
   int32_t head_dim;     /* d in [1, 128] (tensor-core kernels: 128; tile kernel: 64, 128) */
@@ -92,7 +94,15 @@ typedef struct {
                            attention; start at 0)} */
   double* params64;     /* optional [n_units][max_groups][2*(d+G)] exact float64 params
                            (k_xmin[d], k_step[d], v_xmin[G], v_step[G]); NULL = off */
+  int32_t n_out_peers;  /* fused output all-gather, 0 = off: the attention epilogue
+                           stores every output row into `out` and into each out_peer[i] (same
+                           [n_units][n_rep][d] layout) -- typically this rank's rows of a peer
+                           GPU's gather buffer, written over NVLink (parallel.PeerGather) */
+  uint16_t* out_peer[OTT_MAX_OUT_PEERS];
 } ott_cache_t;
+
+/* sizeof(ott_cache_t), for binding-side layout checks. */
+size_t ott_cache_struct_bytes(void);
 
 /* Bytes of one block record for the given shape. */
 size_t ott_record_bytes(int32_t head_dim, int32_t group_size, int32_t bits);

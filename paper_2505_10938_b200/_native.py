@@ -23,6 +23,9 @@ _i32 = ctypes.c_int32
 _i64 = ctypes.c_int64
 
 
+MAX_OUT_PEERS = 7  # OTT_MAX_OUT_PEERS
+
+
 class OttCacheT(ctypes.Structure):
     """Mirror of ott_cache_t (include/ott_b200.h)."""
 
@@ -33,6 +36,7 @@ class OttCacheT(ctypes.Structure):
         ("pool_pos", _vp), ("pool_score", _vp), ("pool_k", _vp), ("pool_v", _vp),
         ("aux_pos", _vp), ("aux_score", _vp), ("aux_k", _vp), ("aux_v", _vp),
         ("pool_meta", _vp), ("params64", _vp),
+        ("n_out_peers", _i32), ("out_peer", _vp * MAX_OUT_PEERS),
     ]
 
 
@@ -71,13 +75,17 @@ def lib() -> ctypes.CDLL:
         L.ott_num_sms.argtypes = []
         L.ott_version.restype = ctypes.c_char_p
         L.ott_last_error.restype = ctypes.c_char_p
+        L.ott_cache_struct_bytes.restype = ctypes.c_size_t
+        if L.ott_cache_struct_bytes() != ctypes.sizeof(OttCacheT):
+            raise NativeError(f"ott_cache_t layout mismatch: library {L.ott_cache_struct_bytes()} bytes, "
+                              f"binding {ctypes.sizeof(OttCacheT)}")
         _lib = L
     return _lib
 
 
 EXPORTED = ("ott_record_bytes", "ott_ring_write", "ott_flush", "ott_pick_splits", "ott_attend_workspace_floats",
             "ott_attend", "ott_logits", "ott_append_attend", "ott_decode_step", "ott_num_sms", "ott_version", "ott_last_error",
-            "ott_model_rmsnorm", "ott_model_rope_qkv", "ott_model_silu_mul")
+            "ott_cache_struct_bytes", "ott_model_rmsnorm", "ott_model_rope_qkv", "ott_model_silu_mul")
 
 
 def check(status: int) -> None:

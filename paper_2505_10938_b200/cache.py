@@ -271,6 +271,18 @@ class OTTCache:
                                                       self.total_tokens, ws.data_ptr(), s, _stream_handle()))
         return out
 
+    def set_output_peers(self, ptrs) -> None:
+        """Fuse the head-output all-gather into the attention epilogue: every
+        output row this cache's attention writes to `out` is also stored at the same offset
+        from each address in `ptrs` (device pointers, e.g. this rank's rows of the peer GPUs'
+        symmetric gather buffers; at most OTT_MAX_OUT_PEERS). Empty = off."""
+        ptrs = [int(p) for p in ptrs]
+        require(len(ptrs) <= _native.MAX_OUT_PEERS, f"at most {_native.MAX_OUT_PEERS} output peers")
+        require(all(p != 0 for p in ptrs), "null output peer pointer")
+        for i in range(_native.MAX_OUT_PEERS):
+            self._c.out_peer[i] = ptrs[i] if i < len(ptrs) else None
+        self._c.n_out_peers = len(ptrs)
+
     @_on_device
     def sync_counters(self) -> None:
         """Copy the host token counts into `counters` (before capturing `decode_step`)."""

@@ -2411,6 +2411,17 @@ __device__ __forceinline__ void tc_guard_partial(const TcGuard& gd, int u, int r
   }
 }
 
+// Output stores of the combine: `out` plus the fused all-gather copies (ott_cache_t.out_peer,
+// this rank's rows of each peer GPU's gather buffer; plain st.global over NVLink P2P).
+__device__ __forceinline__ void store_out(const ott_cache_t& c, uint16_t* out, size_t off, uint16_t v) {
+  out[off] = v;
+  for (int i = 0; i < c.n_out_peers; ++i) c.out_peer[i][off] = v;
+}
+__device__ __forceinline__ void store_out2(const ott_cache_t& c, uint16_t* out, size_t off, __half2 v) {
+  *reinterpret_cast<__half2*>(out + off) = v;
+  for (int i = 0; i < c.n_out_peers; ++i) *reinterpret_cast<__half2*>(c.out_peer[i] + off) = v;
+}
+
 template <int D>
 __global__ void __launch_bounds__(32 * kCombineRows) combine_kernel(const float* __restrict__ ws,
                                                                    uint16_t* __restrict__ out, int n_rows,
@@ -2451,7 +2462,7 @@ __global__ void __launch_bounds__(32 * kCombineRows) combine_kernel(const float*
           for (int k = 0; k < 4; ++k) At[k] = fmaf(fp[2 + lane + 32 * k], ff, At[k]);
         }
         const float inv = 1.f / Lt;
-        for (int k = 0; k < 4; ++k) out[(size_t)urow * D + lane + 32 * k] = f2h(At[k] * inv);
+        for (int k = 0; k < 4; ++k) store_out(gd.c, out, (size_t)urow * D + lane + 32 * k, f2h(At[k] * inv));
         if (dev_counts && blockIdx.x == 0 && threadIdx.x == 0) {
           const int64_t qt = dev_counts[0], tot = dev_counts[1] + 1;
           if (tot - qt - R >= G && qt / G + 1 <= max_groups) dev_counts[0] = qt + G;
@@ -2485,7 +2496,7 @@ __global__ void __launch_bounds__(32 * kCombineRows) combine_kernel(const float*
     }
 #pragma unroll
     for (int k = 0; k < kMaxD / 32; ++k)
-      if (lane + 32 * k < d) out[(size_t)ur * d + lane + 32 * k] = f2h(acc[k] / Lsum);
+      if (lane + 32 * k < d) store_out(gd.c, out, (size_t)ur * d + lane + 32 * k, f2h(acc[k] / Lsum));
     return;
   }
   const float* base = ws + (size_t)ur * n_splits * (D + 2);
@@ -2511,8 +2522,7 @@ __global__ void __launch_bounds__(32 * kCombineRows) combine_kernel(const float*
   const float inv = 1.f / Lsum;
 #pragma unroll
   for (int k = 0; k < D / 64; ++k)
-    *reinterpret_cast<__half2*>(out + (size_t)ur * D + 64 * k + 2 * lane) =
-        __floats2half2_rn(acc[k].x * inv, acc[k].y * inv);
+    store_out2(gd.c, out, (size_t)ur * D + 64 * k + 2 * lane, __floats2half2_rn(acc[k].x * inv, acc[k].y * inv));
 }
 
 template <int D>

@@ -48,10 +48,16 @@ static int check_cache(const ott_cache_t* c) {
   if (c->n_units < 1 || c->max_groups < 0) return fail(OTT_ERR_CONTRACT, "bad unit/group counts");
   if (!c->blocks || !c->pend_k || !c->pend_v || !c->pool_mask || !c->subst_mask || !c->pool_meta)
     return fail(OTT_ERR_CONTRACT, "null state buffer");
+  if (c->n_out_peers < 0 || c->n_out_peers > OTT_MAX_OUT_PEERS)
+    return fail(OTT_ERR_CONTRACT, "n_out_peers must be in [0, OTT_MAX_OUT_PEERS]");
+  for (int i = 0; i < c->n_out_peers; ++i)
+    if (!c->out_peer[i]) return fail(OTT_ERR_CONTRACT, "null out_peer pointer");
   return OTT_OK;
 }
 
 extern "C" {
+
+size_t ott_cache_struct_bytes(void) { return sizeof(ott_cache_t); }
 
 size_t ott_record_bytes(int32_t head_dim, int32_t group_size, int32_t bits) {
   if (bits < 1 || bits > 8) return 0;

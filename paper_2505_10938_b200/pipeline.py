@@ -28,13 +28,14 @@ class HostDecodePipeline:
     `step` returns without waiting (use `torch.cuda.current_stream().synchronize()`
     or the returned event)."""
 
-    def __init__(self, caches, n_q_heads: int, gather=None):
+    def __init__(self, caches, n_q_heads: int, gather=None, peer_gather=None):
         if not caches:
             raise ContractViolation("need at least one layer cache")
         c0 = caches[0]
         self.caches = list(caches)
         self.device = c0.device
         self.gather = gather  # optional callable(out_local, layer) -> tensor to read back (multi-GPU)
+        self.peer_gather = peer_gather  # optional parallel.PeerGather: all-gather fused into the attention
         B, H, d = c0.batch, c0.n_kv_heads, c0.config.head_dim
         if n_q_heads % H:
             raise ContractViolation("H_q must be a multiple of n_kv_heads")
@@ -85,9 +86,14 @@ class HostDecodePipeline:
             if l >= 2:
                 main.wait_event(read[l - 2])  # o_d[b] drained
             before = c.quantized_tokens
-            c.append_attend(self.k_d[b], self.v_d[b], self.q_d[b], out=self.o_d[b], n_splits=self.splits[l])
+            out_d = self.o_d[b] if self.peer_gather is None else self.peer_gather.out(l)
+            c.append_attend(self.k_d[b], self.v_d[b], self.q_d[b], out=out_d, n_splits=self.splits[l])
             self.launches += 2 + (1 if c.quantized_tokens != before else 0)
-            src = self.o_d[b] if self.gather is None else self.gather(self.o_d[b], l)
+            if self.peer_gather is not None:
+                self.peer_gather.wait(l)  # every rank's rows are in this rank's gather buffer
+                src = out_d
+            else:
+                src = out_d if self.gather is None else self.gather(out_d, l)
             computed[l].record(main)
             with torch.cuda.stream(self.d2h):
                 self.d2h.wait_event(computed[l])

@@ -36,6 +36,7 @@ def test_record_bytes_and_version_without_gpu():
     assert L.ott_record_bytes(128, 32, 2) == 32 * 128 // 2 + 8 * 128 + 8 * 32
     assert L.ott_record_bytes(64, 128, 2) == 128 * 64 // 2 + 8 * 64 + 8 * 128
     assert b"sm_100a" in L.ott_version()
+    assert L.ott_cache_struct_bytes() == ctypes.sizeof(_native.OttCacheT)
 
 
 def test_contract_errors_map_to_contract_violation():

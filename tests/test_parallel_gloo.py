@@ -74,3 +74,34 @@ def test_two_rank_gloo_matches_single_process(tmp_path):
     k, v, q = _workload(4, 2, 2, 100, 16)
     ref = _decode(k, v, q, 2)
     np.testing.assert_array_equal(full, ref)
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_peer_destinations_assemble_the_all_gather(world):
+    """PeerGather's address arithmetic: if every rank stores its rows at
+    peer_destinations(...) in each peer's buffer (what the combine kernel does over
+    NVLink) and at out(l) locally, every rank's buffer equals the all-gather."""
+    from paper_2505_10938_b200.parallel import gather_row_offset, peer_destinations
+
+    L, b_local, hq, d = 3, 2, 4, 8
+    row_bytes = hq * d * 2
+    size = L * b_local * world * row_bytes
+    bases = [(p + 1) << 32 for p in range(world)]  # distinct fake device addresses
+    mem = [np.zeros(size, np.uint8) for _ in range(world)]
+    rng = np.random.default_rng(world)
+    outs = rng.integers(0, 256, (world, L, b_local * row_bytes), dtype=np.uint8)
+    for r in range(world):
+        for l in range(L):
+            local = gather_row_offset(l, r, b_local, world, hq, d)
+            mem[r][local:local + b_local * row_bytes] = outs[r, l]
+            dests = peer_destinations(bases, r, l, b_local, hq, d)
+            assert len(dests) == world - 1
+            for a in dests:
+                p = (a >> 32) - 1
+                assert p != r
+                off = a - bases[p]
+                assert off == local
+                mem[p][off:off + b_local * row_bytes] = outs[r, l]
+    want = np.concatenate([outs[:, l].reshape(-1) for l in range(L)])
+    for p in range(world):
+        np.testing.assert_array_equal(mem[p], want)
