@@ -45,7 +45,7 @@ _lib = None
 
 def build(verbose: bool = False) -> str:
     """Compile libott_b200.so for sm_100a with nvcc (csrc/Makefile)."""
-    r = subprocess.run(["make", "-s", "-C", CSRC], capture_output=not verbose, text=True)
+    r = subprocess.run(["make", "-s", "-j4", "-C", CSRC], capture_output=not verbose, text=True)
     if r.returncode != 0:
         raise NativeError(f"nvcc build failed:\n{r.stdout}\n{r.stderr}")
     return LIB_PATH

@@ -809,3 +809,46 @@ def test_long_context_64k_vs_oracle():
         for r in range(n_rep):
             ok, err = within_tol(out[0, u * n_rep + r], ref.attend(qh[0, u * n_rep + r].astype(np.float32)))
             assert ok, (u, r, err)
+
+
+@pytest.mark.parametrize("bits", [2, 4, 8])
+def test_cache_larger_than_2gib_sampled(bits):
+    """One layer at B=128, H_kv=8 (config 4's unit count) with a 65,536-token context: the
+    block records alone exceed 2 GiB (2.9 / 11.3 / 19.9 GB at 2 / 4 / 8 bits), so any 32-bit
+    offset or TMA-coordinate overflow would corrupt the high units. The prompt is inserted in
+    8,192-token bulk updates, then decode appends with flushes; sampled units across the unit
+    range (incl. the last) are bit-exact against the oracle and GQA attention is in tolerance."""
+    from paper_2505_10938_b200 import OTTCache
+    from paper_2505_10938_b200.workloads import decode_rows, fill_prefill
+
+    B, H, n_rep, d, T0, chunk, steps = 128, 8, 8, 128, 65536, 8192, 40
+    units = ((0, 0), (64, 3), (127, 7))
+    gen = torch.Generator(device="cuda").manual_seed(bits)
+    cache = OTTCache(cfg_of(bits, 32, 128, 8, 16, d), B, H, max_tokens=T0 + steps)
+    assert cache.blocks.numel() > 2**31
+    k = torch.empty((B, H, chunk, d), dtype=torch.float16, device="cuda")
+    v = torch.empty_like(k)
+    keep_k, keep_v = [], []
+    for _ in range(T0 // chunk):
+        scale = fill_prefill(gen, k, v)
+        cache.update(k, v)
+        keep_k.append(torch.stack([k[b, h] for b, h in units]).cpu())
+        keep_v.append(torch.stack([v[b, h] for b, h in units]).cpu())
+    del k, v
+    for _ in range(steps):
+        kr, vr = decode_rows(gen, scale, B, H)
+        cache.append(kr, vr)
+        keep_k.append(torch.stack([kr[b, h] for b, h in units])[:, None].cpu())
+        keep_v.append(torch.stack([vr[b, h] for b, h in units])[:, None].cpu())
+    q = torch.randn((B, H * n_rep, d), generator=gen, device="cuda").half()
+    out = cache.attend(q).float().cpu().numpy()
+    kk = torch.cat(keep_k, dim=1).numpy()
+    vv = torch.cat(keep_v, dim=1).numpy()
+    qh = q.cpu().numpy()
+    for i, (b, h) in enumerate(units):
+        ref = oracle.OracleCache(bits, 32, 128, 8, 16, d)
+        ref.extend(kk[i].astype(np.float32), vv[i].astype(np.float32))
+        assert_unit_matches_oracle(cache.unit(b, h), ref, exact64=False)
+        for r in (0, n_rep - 1):
+            ok, err = within_tol(out[b, h * n_rep + r], ref.attend(qh[b, h * n_rep + r].astype(np.float32)))
+            assert ok, (b, h, r, err)
