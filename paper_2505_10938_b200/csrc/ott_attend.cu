@@ -24,6 +24,7 @@
 // per-(group, head) bias. V codes become exact fp16 subnormals c * 2^-16; the
 // per-token V step is folded into P' = 4 p step (fp16) and V x_min into a
 // per-head fp32 bias. See DESIGN.md §4.
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 
@@ -2844,6 +2845,49 @@ cudaError_t launch_attend(const ott_cache_t& c, const uint16_t* q, uint16_t* out
   OTT_CASE(1, 64) OTT_CASE(2, 64) OTT_CASE(4, 64) OTT_CASE(8, 64)
 #undef OTT_CASE
   return cudaErrorInvalidValue;
+}
+
+// Query-head counts the kernels are not instantiated for (3, 5, 6, 7): the heads of each
+// unit are staged into the next instantiated count (4 or 8) with zero rows, and only the real
+// heads' outputs are copied back (plus the fused peer stores, which the padded combine skips).
+__global__ void rep_pad_kernel(const uint16_t* __restrict__ q, uint16_t* __restrict__ qs, int64_t n, int n_rep,
+                               int nr, int d) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(i % d);
+    const int64_t row = i / d;  // unit * nr + r
+    const int r = (int)(row % nr);
+    const int64_t u = row / nr;
+    qs[i] = r < n_rep ? q[(u * n_rep + r) * d + j] : (uint16_t)0;
+  }
+}
+
+__global__ void rep_unpad_kernel(ott_cache_t c, const uint16_t* __restrict__ os, uint16_t* __restrict__ out,
+                                 int64_t n, int n_rep, int nr, int d) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(i % d);
+    const int64_t row = i / d;  // unit * n_rep + r
+    const int r = (int)(row % n_rep);
+    const int64_t u = row / n_rep;
+    const uint16_t x = os[(u * nr + r) * d + j];
+    out[i] = x;
+    for (int p = 0; p < c.n_out_peers; ++p) c.out_peer[p][i] = x;
+  }
+}
+
+cudaError_t launch_rep_pad(const uint16_t* q, uint16_t* qs, int n_units, int n_rep, int nr, int d, cudaStream_t st) {
+  const int64_t n = (int64_t)n_units * nr * d;
+  const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+  rep_pad_kernel<<<blocks, 256, 0, st>>>(q, qs, n, n_rep, nr, d);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rep_unpad(const ott_cache_t& c, const uint16_t* os, uint16_t* out, int n_rep, int nr,
+                             cudaStream_t st) {
+  const int d = c.head_dim;
+  const int64_t n = (int64_t)c.n_units * n_rep * d;
+  const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+  rep_unpad_kernel<<<blocks, 256, 0, st>>>(c, os, out, n, n_rep, nr, d);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_logits(const ott_cache_t& c, const uint16_t* q, float* logits, int n_rep, int64_t q_tokens,

@@ -18,7 +18,42 @@ cudaError_t launch_attend(const ott_cache_t& c, const uint16_t* q, uint16_t* out
 bool attend_fuses_ring_write(const ott_cache_t& c);
 cudaError_t launch_logits(const ott_cache_t& c, const uint16_t* q, float* logits, int n_rep, int64_t q_tokens,
                           int64_t total, cudaStream_t st);
+cudaError_t launch_rep_pad(const uint16_t* q, uint16_t* qs, int n_units, int n_rep, int nr, int d, cudaStream_t st);
+cudaError_t launch_rep_unpad(const ott_cache_t& c, const uint16_t* os, uint16_t* out, int n_rep, int nr,
+                             cudaStream_t st);
 }  // namespace ott
+
+// Query heads per KV head the attention kernels are instantiated for: 1, 2, 4, 8. Other counts
+// up to 8 run padded to the next one (zero query rows, outputs dropped).
+static int native_rep(int n_rep) {
+  if (n_rep < 1 || n_rep > 8) return 0;
+  return n_rep <= 2 ? n_rep : (n_rep <= 4 ? 4 : 8);
+}
+
+static size_t partial_floats(const ott_cache_t* c, int nr, int n_splits) {
+  // partials [units][nr][splits + 2][d + 2] (up to two full-precision-tier partials) + 2 floats
+  // (the launch's quantized-token count), rounded to 16 bytes
+  const size_t f = (size_t)c->n_units * nr * ((n_splits > 0 ? n_splits : 1) + 2) * (c->head_dim + 2) + 2;
+  return (f + 3) & ~(size_t)3;
+}
+
+static cudaError_t attend_any_rep(const ott_cache_t& c, const uint16_t* q, uint16_t* out, int n_rep, int64_t q_tokens,
+                                  int64_t total, float* ws, int n_splits, cudaStream_t st,
+                                  int64_t* dev_counts = nullptr, const uint16_t* new_k = nullptr,
+                                  const uint16_t* new_v = nullptr) {
+  const int nr = native_rep(n_rep);
+  if (nr == n_rep)
+    return ott::launch_attend(c, q, out, n_rep, q_tokens, total, ws, n_splits, st, dev_counts, new_k, new_v);
+  uint16_t* qs = reinterpret_cast<uint16_t*>(ws + partial_floats(&c, nr, n_splits));
+  uint16_t* os = qs + (size_t)c.n_units * nr * c.head_dim;
+  ott_cache_t cp = c;
+  cp.n_out_peers = 0;  // the real heads' rows go to the peers from the unpad kernel
+  cudaError_t e = ott::launch_rep_pad(q, qs, c.n_units, n_rep, nr, c.head_dim, st);
+  if (e == cudaSuccess)
+    e = ott::launch_attend(cp, qs, os, nr, q_tokens, total, ws, n_splits, st, dev_counts, new_k, new_v);
+  if (e == cudaSuccess) e = ott::launch_rep_unpad(c, os, out, n_rep, nr, st);
+  return e;
+}
 
 static thread_local char g_err[512];
 
@@ -130,10 +165,11 @@ int ott_pick_splits(const ott_cache_t* c, int32_t n_rep, int64_t total_tokens) {
 }
 
 size_t ott_attend_workspace_floats(const ott_cache_t* c, int32_t n_rep, int32_t n_splits) {
-  if (!c) return 0;
-  // partials [units][n_rep][splits + 2][d + 2] (up to two full-precision-tier partials) + 2 floats
-  // (the launch's quantized-token count)
-  return (size_t)c->n_units * n_rep * ((n_splits > 0 ? n_splits : 1) + 2) * (c->head_dim + 2) + 2;
+  const int nr = native_rep(n_rep);
+  if (!c || !nr) return 0;
+  size_t f = partial_floats(c, nr, n_splits);
+  if (nr != n_rep) f += (size_t)c->n_units * nr * c->head_dim;  // padded q and out staging (fp16)
+  return f;
 }
 
 int ott_attend(const ott_cache_t* c, const uint16_t* q, uint16_t* out, int32_t n_rep, int64_t quantized_tokens,
@@ -141,15 +177,14 @@ int ott_attend(const ott_cache_t* c, const uint16_t* q, uint16_t* out, int32_t n
   int s = check_cache(c);
   if (s) return s;
   if (total_tokens <= 0) return fail(OTT_ERR_CONTRACT, "cannot attend over an empty cache");
-  if (n_rep != 1 && n_rep != 2 && n_rep != 4 && n_rep != 8)
-    return fail(OTT_ERR_UNSUPPORTED, "n_rep (H_q / H_kv) must be 1, 2, 4 or 8");
+  if (!native_rep(n_rep)) return fail(OTT_ERR_UNSUPPORTED, "n_rep (H_q / H_kv) must be in [1, 8]");
   if (quantized_tokens < 0 || quantized_tokens > total_tokens || quantized_tokens % c->group_size)
     return fail(OTT_ERR_CONTRACT, "inconsistent token counts");
   if (total_tokens - quantized_tokens > c->group_size + c->residual)
     return fail(OTT_ERR_CONTRACT, "more pending rows than the ring holds");
   if (!q || !out || !workspace || n_splits < 1) return fail(OTT_ERR_CONTRACT, "null buffer or bad split count");
-  return cuda_status(ott::launch_attend(*c, q, out, n_rep, quantized_tokens, total_tokens, workspace, n_splits,
-                                        (cudaStream_t)stream));
+  return cuda_status(attend_any_rep(*c, q, out, n_rep, quantized_tokens, total_tokens, workspace, n_splits,
+                                    (cudaStream_t)stream));
 }
 
 int ott_append_attend(const ott_cache_t* c, const uint16_t* k, const uint16_t* v, const uint16_t* q, uint16_t* out,
@@ -159,8 +194,7 @@ int ott_append_attend(const ott_cache_t* c, const uint16_t* k, const uint16_t* v
   if (s) return s;
   if (!k || !v) return fail(OTT_ERR_CONTRACT, "null rows");
   if (total_tokens <= 0) return fail(OTT_ERR_CONTRACT, "cannot attend over an empty cache");
-  if (n_rep != 1 && n_rep != 2 && n_rep != 4 && n_rep != 8)
-    return fail(OTT_ERR_UNSUPPORTED, "n_rep (H_q / H_kv) must be 1, 2, 4 or 8");
+  if (!native_rep(n_rep)) return fail(OTT_ERR_UNSUPPORTED, "n_rep (H_q / H_kv) must be in [1, 8]");
   if (quantized_tokens < 0 || quantized_tokens > total_tokens - 1 || quantized_tokens % c->group_size)
     return fail(OTT_ERR_CONTRACT, "inconsistent token counts");
   if (total_tokens - quantized_tokens > c->group_size + c->residual)
@@ -171,8 +205,8 @@ int ott_append_attend(const ott_cache_t* c, const uint16_t* k, const uint16_t* v
   cudaError_t e = fuse ? cudaSuccess
                        : ott::launch_ring_write(*c, k, v, c->head_dim, total_tokens - 1, total_tokens - 1, 1, st);
   if (e == cudaSuccess)
-    e = ott::launch_attend(*c, q, out, n_rep, quantized_tokens, total_tokens, workspace, n_splits, st, nullptr,
-                           fuse ? k : nullptr, fuse ? v : nullptr);
+    e = attend_any_rep(*c, q, out, n_rep, quantized_tokens, total_tokens, workspace, n_splits, st, nullptr,
+                       fuse ? k : nullptr, fuse ? v : nullptr);
   return cuda_status(e);
 }
 
@@ -180,7 +214,7 @@ int ott_decode_step(const ott_cache_t* c, const uint16_t* k, const uint16_t* v, 
                     int32_t n_rep, int64_t* counters, float* workspace, int32_t n_splits, void* stream) {
   int s = check_cache(c);
   if (s) return s;
-  if (n_rep != 1 && n_rep != 2 && n_rep != 4 && n_rep != 8) return fail(OTT_ERR_UNSUPPORTED, "n_rep must be 1, 2, 4 or 8");
+  if (!native_rep(n_rep)) return fail(OTT_ERR_UNSUPPORTED, "n_rep (H_q / H_kv) must be in [1, 8]");
   if (!k || !v || !q || !out || !counters || !workspace || n_splits < 1)
     return fail(OTT_ERR_CONTRACT, "null buffer or bad split count");
   if (c->capacity > 0 && (!c->pool_pos || !c->pool_score || !c->pool_k || !c->pool_v))
@@ -190,8 +224,8 @@ int ott_decode_step(const ott_cache_t* c, const uint16_t* k, const uint16_t* v, 
   cudaError_t e = fuse ? cudaSuccess : ott::launch_ring_write(*c, k, v, c->head_dim, 0, 0, 1, st, counters);
   if (e == cudaSuccess) e = ott::launch_flush(*c, 0, 1, 0, nullptr, nullptr, 0, 0, st, counters);
   if (e == cudaSuccess)
-    e = ott::launch_attend(*c, q, out, n_rep, 0, 1, workspace, n_splits, st, counters, fuse ? k : nullptr,
-                           fuse ? v : nullptr);
+    e = attend_any_rep(*c, q, out, n_rep, 0, 1, workspace, n_splits, st, counters, fuse ? k : nullptr,
+                       fuse ? v : nullptr);
   return cuda_status(e);
 }
 

@@ -852,3 +852,59 @@ def test_cache_larger_than_2gib_sampled(bits):
         for r in (0, n_rep - 1):
             ok, err = within_tol(out[b, h * n_rep + r], ref.attend(qh[b, h * n_rep + r].astype(np.float32)))
             assert ok, (b, h, r, err)
+
+
+@pytest.mark.parametrize("bits,G,d,n_rep", [(2, 32, 128, 3), (2, 32, 128, 7), (4, 32, 128, 5), (8, 32, 128, 6),
+                                            (3, 32, 128, 3), (2, 16, 48, 5)])
+def test_any_query_heads_per_kv_head_vs_oracle(bits, G, d, n_rep):
+    """GQA ratios the kernels are not instantiated for (3, 5, 6, 7 query heads per KV head,
+    e.g. 28/4 or 40/8 head layouts) run padded to the next instantiated ratio: every query
+    head's output is within tolerance of the oracle for attend, fused append+attend and the
+    device-counter step, and the fused peer stores carry only the real heads' rows."""
+    from paper_2505_10938_b200 import OTTCache
+
+    B, Hkv, R = 2, 3, 16
+    T0, steps = 5 * G + R + 3, G + 2
+    rng = np.random.default_rng(n_rep * 10 + bits)
+    k = rng.standard_normal((B, Hkv, T0 + steps, d)).astype(np.float16)
+    k[..., :4] *= 10
+    v = rng.standard_normal((B, Hkv, T0 + steps, d)).astype(np.float16)
+    q = rng.standard_normal((steps + 1, B, Hkv * n_rep, d)).astype(np.float16)
+    cache = OTTCache(cfg_of(bits, G, R, 4, 8, d), B, Hkv, max_tokens=T0 + steps)
+    kt, vt, qt = torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda(), torch.from_numpy(q).cuda()
+    peer = torch.full((2 * B, Hkv * n_rep, d), float("nan"), dtype=torch.float16, device="cuda")
+    cache.set_output_peers([peer[B:].data_ptr()])
+    cache.update(kt[:, :, :T0].contiguous(), vt[:, :, :T0].contiguous())
+    refs = {}
+    for b in range(B):
+        for h in range(Hkv):
+            refs[b, h] = oracle.OracleCache(bits, G, R, 4, 8, d)
+            refs[b, h].extend(k[b, h, :T0].astype(np.float32), v[b, h, :T0].astype(np.float32))
+
+    def check(out, qi, tag):
+        out = out.float().cpu().numpy()
+        assert torch.equal(peer[B:].float().nan_to_num(7.0), torch.from_numpy(out).cuda().nan_to_num(7.0)), tag
+        assert torch.isnan(peer[:B]).all(), tag
+        for (b, h), ref in refs.items():
+            for r in range(n_rep):
+                hq = h * n_rep + r
+                ok, err = within_tol(out[b, hq], ref.attend(q[qi, b, hq].astype(np.float32)))
+                assert ok, (tag, b, h, r, err)
+
+    check(cache.attend(qt[0]), 0, "attend")
+    half = steps // 2
+    for t in range(half):
+        out = cache.append_attend(kt[:, :, T0 + t].contiguous(), vt[:, :, T0 + t].contiguous(), qt[t + 1])
+        for (b, h), ref in refs.items():
+            ref.append(k[b, h, T0 + t].astype(np.float32), v[b, h, T0 + t].astype(np.float32))
+        if t in (0, half - 1):
+            check(out, t + 1, f"append_attend {t}")
+    cache.sync_counters()
+    s = cache.splits(n_rep)
+    out = torch.empty((B, Hkv * n_rep, d), dtype=torch.float16, device="cuda")
+    for t in range(half, steps):
+        cache.decode_step(kt[:, :, T0 + t].contiguous(), vt[:, :, T0 + t].contiguous(), qt[t + 1].contiguous(), out, s)
+        for (b, h), ref in refs.items():
+            ref.append(k[b, h, T0 + t].astype(np.float32), v[b, h, T0 + t].astype(np.float32))
+    torch.cuda.synchronize()
+    check(out, steps, "decode_step")
