@@ -214,7 +214,17 @@ def run_ours(args, wl, rank, world, local_rank):
     # multi-GPU head-output all-gather: P2P stores fused into the attention's combine kernel
     # (parallel.PeerGather, default) or a separate NCCL all_gather per layer (OTT_GATHER=nccl)
     gather_mode = (os.environ.get("OTT_GATHER", "p2p") if world > 1 else "none")
-    pg = PeerGather(caches, Hq) if gather_mode == "p2p" else None
+    pg, gather_note = None, ""
+    if gather_mode == "p2p":
+        try:
+            pg = PeerGather(caches, Hq)
+        except Exception as exc:  # no P2P mapping between these GPUs: keep the NCCL collective
+            gather_mode, gather_note = "nccl", f" (P2P unavailable: {type(exc).__name__}: {str(exc)[:120]})"
+        ok = torch.tensor([1 if pg is not None else 0], device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)  # every rank must take the same path
+        if not int(ok.item()) and pg is not None:
+            pg.close()
+            pg, gather_mode, gather_note = None, "nccl", " (P2P unavailable on another rank)"
     gathered = (torch.empty((L, wl.batch, Hq, d), dtype=torch.float16, device=dev)
                 if gather_mode == "nccl" else None)
     splits = [c.splits(wl.n_rep) for c in caches]
@@ -354,7 +364,7 @@ def run_ours(args, wl, rank, world, local_rank):
                        "skip_layers": list(wl.skip_layers), "partition": f"batch/{world} x all kv heads per rank",
                        "gather": {"none": "none (1 GPU)", "nccl": "NCCL all_gather_into_tensor per layer",
                                   "p2p": "P2P stores fused into the combine kernel + signal-pad barrier per layer"}[
-                           gather_mode],
+                           gather_mode] + gather_note,
                        "l2": "working set > L2 (126 MB): %.1f GB of cache per GPU" % (
                            sum(c.hbm_bytes() for c in caches) / 1e9),
                        "prefill_s": round(prefill_s, 2)},
