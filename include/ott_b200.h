@@ -46,9 +46,14 @@ typedef enum {
 
 /* Device-side state of one layer's batched tiered cache. Sizes in elements.
  * Block record (one per (unit, group)), byte layout, all little-endian:
- *   [0, CB)                         K codes, reference pack_codes order; CB =
- *                                   ceil(G*d*bits/8) rounded up to 16 (= G*d*bits/8
- *                                   when d in {64, 128} and G % 32 == 0)
+ *   [0, CB)                         K codes, reference pack_codes order at the stored
+ *                                   width cb; CB = ceil(G*d*cb/8) rounded up to 16 (=
+ *                                   G*d*cb/8 when d in {64, 128} and G % 32 == 0).
+ *                                   cb = bits, except at d = 128: 1-bit codes in 2-bit
+ *                                   fields (G % 32 == 0; K codes stored doubled with the
+ *                                   K step halved, exact), 3-bit in 4-bit and 5..7-bit in
+ *                                   8-bit fields (G = 32), so every width decodes on a
+ *                                   tensor-core kernel
  *   [CB, 2 CB)                      V codes
  *   fp16 k_sh[d], k_sl[d]           per-channel K step = sh + sl, in pair order
  *                                   (index 16*(c/16) + 2*(c%8) + (c%16)/8 when
@@ -56,8 +61,8 @@ typedef enum {
  *   float32 k_e[d]                  per-channel K x_min - 4*u(c)*step, u(c) = 4^(4-P(c%8)),
  *                                   P = {3,4,2,3,4,2,3,4} (fp16 mantissa position of the
  *                                   code pair in the decode kernels)
- *   (4-bit, d % 8 == 0: sh/sl in 4-bit pair order (8w+k, 8w+k+4), e = x_min - 64 step;
- *   8-bit, d % 8 == 0: sh/sl in channel order, e = x_min - 1024 step; other widths: the
+ *   (stored width 4, d % 8 == 0: sh/sl in 4-bit pair order (8w+k, 8w+k+4), e = x_min - 64 step;
+ *   stored width 8, d % 8 == 0: sh/sl in channel order, e = x_min - 1024 step; other widths: the
  *   k_sh/k_sl bytes hold float32 step[d] and k_e float32 x_min[d], channel order: 1-bit steps
  *   can exceed the fp16 range)
  *   float32 v_step[G], v_xmin[G]    per-token V params
@@ -73,7 +78,7 @@ typedef struct {
   int32_t residual;     /* R >= 0 */
   int32_t capacity;     /* N: pool capacity for this layer (EngineConfig.outlier_capacity) */
   int32_t aux_capacity; /* A */
-  int32_t bits;         /* 1..8 (2: tensor-core attention; others: CUDA-core kernel) */
+  int32_t bits;         /* 1..8 (levels 2^bits - 1; the stored width picks the decode kernel) */
   int32_t max_groups;   /* block records allocated per unit */
   uint8_t* blocks;      /* [n_units][max_groups][record_bytes] */
   uint16_t* pend_k;     /* fp16 [n_units][G+R][d], slot = position % (G+R) */

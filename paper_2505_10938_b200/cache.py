@@ -57,9 +57,31 @@ def kpair_index(c, d=128):
     return c if d % 16 else 16 * (c // 16) + 2 * (c % 8) + (c % 16) // 8
 
 
+def code_bits(bits, d, G):
+    """Stored code width (ott_common.cuh code_bits): at the tensor-core shapes 1-bit codes live
+    in 2-bit fields, 3-bit in 4-bit and 5..7-bit in 8-bit fields (levels stay 2^bits - 1)."""
+    if d == 128 and G % 32 == 0 and bits == 1:
+        return 2
+    if d == 128 and G == 32 and bits == 3:
+        return 4
+    if d == 128 and G == 32 and 5 <= bits <= 7:
+        return 8
+    return bits
+
+
 def record_code_bytes(d, G, bits):
-    """Bytes of one code field of a block record: ceil(G d bits / 8) padded to 16."""
-    return ((G * d * bits + 7) // 8 + 15) & ~15
+    """Bytes of one code field of a block record: ceil(G d code_bits / 8) padded to 16."""
+    return ((G * d * code_bits(bits, d, G) + 7) // 8 + 15) & ~15
+
+
+def repack_codes(buf, n, from_bits, to_bits, shift=0):
+    """pack_codes stream (quant.py:241-256, LSB first) of n codes re-packed at another width
+    (codes stored shifted left by `shift` in their container are shifted back)."""
+    if from_bits == to_bits:
+        return bytes(buf[:(n * to_bits + 7) // 8])
+    bits = np.unpackbits(np.frombuffer(bytes(buf), np.uint8), bitorder="little")[: n * from_bits]
+    codes = bits.reshape(n, from_bits)[:, shift:shift + to_bits]  # the other container bits are zero
+    return np.packbits(codes.reshape(-1), bitorder="little").tobytes()
 
 
 def kpair4_index(c):
@@ -392,7 +414,8 @@ class UnitView:
         nb = cache.quantized_tokens // G
         rec = cache.blocks[u, :nb].cpu().numpy()
         code_b = record_code_bytes(d, G, cfg.bits)  # padded field (ott_b200.h)
-        code_n = (G * d * cfg.bits + 7) // 8  # the reference's packed size (quant.py:237-238)
+        pb = code_bits(cfg.bits, d, G)  # stored width; the views re-pack at cfg.bits
+        code_n = (G * d * pb + 7) // 8
         # K params are stored in the decode kernels' encoding (ott_b200.h): fp16 halves
         # sh + sl of the step in pair order and e = x_min - 4 u step; the float32 views
         # below are reconstructions, the exact values come from params64
@@ -401,15 +424,17 @@ class UnitView:
         self.k_e32 = rec[:, 2 * code_b + 4 * d: 2 * code_b + 8 * d].copy().view(np.float32)
         vst = rec[:, 2 * code_b + 8 * d: 2 * code_b + 8 * d + 4 * G].copy().view(np.float32)
         vmn = rec[:, 2 * code_b + 8 * d + 4 * G: 2 * code_b + 8 * d + 8 * G].copy().view(np.float32)
-        if cfg.bits == 2:  # tensor-core encoding: step = sh + sl (pair order), e = x_min - 4 u step
+        kshift = 1 if (cfg.bits == 1 and pb == 2) else 0  # 1-bit K: doubled codes, halved step
+        if pb == 2:  # tensor-core encoding: step = sh + sl (pair order), e = x_min - 4 u step
             pidx = kpair_index(np.arange(d), d)
             kst = self.k_sh16[:, pidx].astype(np.float32) + self.k_sl16[:, pidx].astype(np.float32)
             kmn = (self.k_e32 + np.float32(4) * kpair_u(np.arange(d)) * kst).astype(np.float32)
-        elif cfg.bits == 4 and d % 8 == 0:  # 4-bit tensor-core encoding: pair4 order, e = x_min - 64 step
+            kst = kst * np.float32(2 ** kshift)
+        elif pb == 4 and d % 8 == 0:  # 4-bit tensor-core encoding: pair4 order, e = x_min - 64 step
             pidx = kpair4_index(np.arange(d))
             kst = self.k_sh16[:, pidx].astype(np.float32) + self.k_sl16[:, pidx].astype(np.float32)
             kmn = (self.k_e32 + np.float32(64) * kst).astype(np.float32)
-        elif cfg.bits == 8 and d % 8 == 0:  # 8-bit tensor-core encoding: channel order, e = x_min - 1024 step
+        elif pb == 8 and d % 8 == 0:  # 8-bit tensor-core encoding: channel order, e = x_min - 1024 step
             kst = self.k_sh16.astype(np.float32) + self.k_sl16.astype(np.float32)
             kmn = (self.k_e32 + np.float32(1024) * kst).astype(np.float32)
         else:  # other widths: float32 step[d] in the sh/sl bytes, x_min in e
@@ -424,10 +449,11 @@ class UnitView:
         self.quantized_k, self.quantized_v = [], []
         for i in range(nb):
             b = cfg.bits
-            self.quantized_k.append(QuantizedBlock(rec[i, :code_n].tobytes(), GroupAxis.PER_CHANNEL,
+            self.quantized_k.append(QuantizedBlock(repack_codes(rec[i, :code_n], G * d, pb, b, kshift), GroupAxis.PER_CHANNEL,
                                                    [QuantParams(float(kmn64[i, c]), float(kst64[i, c]), b)
                                                     for c in range(d)], G, d, b))
-            self.quantized_v.append(QuantizedBlock(rec[i, code_b:code_b + code_n].tobytes(), GroupAxis.PER_TOKEN,
+            self.quantized_v.append(QuantizedBlock(repack_codes(rec[i, code_b:code_b + code_n], G * d, pb, b),
+                                                   GroupAxis.PER_TOKEN,
                                                    [QuantParams(float(vmn64[i, t]), float(vst64[i, t]), b)
                                                     for t in range(G)], G, d, b))
         cap = G + cfg.residual

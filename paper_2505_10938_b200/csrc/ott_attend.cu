@@ -143,8 +143,8 @@ __device__ void simt_body(const AttnArgs& a, const Counts& n, int u, int t_begin
   const ott_cache_t& c = a.c;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int G = c.group_size, N = c.capacity, cap = G + c.residual;
-  const int bits = c.bits;
-  const RecordLayout L(D, G, bits);
+  const RecordLayout L(D, G, c.bits);
+  const int bits = L.bits;  // stored code width
   WarpScratch<NR, D>& ws = sm.w[warp];
 
   for (int i = tid; i < NR * D; i += kAttnThreads)
@@ -351,8 +351,9 @@ __global__ void __launch_bounds__(kAttnThreads) attend_generic_kernel(AttnArgs a
   GenericSmem<NR>& sm = *reinterpret_cast<GenericSmem<NR>*>(smem_raw);
   const Counts n = counts_of(a);
   const ott_cache_t& c = a.c;
-  const int D = c.head_dim, G = c.group_size, N = c.capacity, cap = G + c.residual, bits = c.bits;
-  const RecordLayout L(D, G, bits);
+  const int D = c.head_dim, G = c.group_size, N = c.capacity, cap = G + c.residual;
+  const RecordLayout L(D, G, c.bits);
+  const int bits = L.bits;  // stored code width
   const int u = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nq = (int)((n.q_tokens + 31) / 32), np = (N + 31) / 32;
   const int nr = (int)((n.total_tokens - n.q_tokens + 31) / 32);
@@ -2544,7 +2545,7 @@ static cudaError_t launch_combine(const AttnArgs& a, int NR, cudaStream_t st, bo
   gd.NR = NR;
   gd.scale_log2 = a.scale_log2;
   gd.umax = umax;
-  gd.bits = a.c.bits;
+  gd.bits = code_bits(a.c.bits, a.c.head_dim, a.c.group_size);
   gd.n_qsplits = a.n_qsplits;
   return cudaLaunchKernelEx(&cfg, combine_kernel<D>, (const float*)a.ws, a.out, a.c.n_units * NR, a.n_splits,
                             const_cast<int64_t*>(a.dev_counts), a.c.group_size, a.c.residual, a.c.max_groups,
@@ -2577,7 +2578,7 @@ __global__ void logits_kernel(ott_cache_t c, const uint16_t* __restrict__ q, flo
       const uint8_t* rec = record_ptr(c, u, gi);
       for (int j = 0; j < D; ++j) {
         const float st = k_step_of(rec, L, j);
-        k[j] = fmaf((float)code_at(rec + L.k_codes(), (int64_t)row * D + j, c.bits), st, k_xmin_of(rec, L, j, st));
+        k[j] = fmaf((float)code_at(rec + L.k_codes(), (int64_t)row * D + j, L.bits), st, k_xmin_of(rec, L, j, st));
       }
     }
   } else {
@@ -2735,7 +2736,7 @@ static bool use_tc5() {
   return v == 1;
 }
 
-bool mma_eligible(const ott_cache_t& c) { return c.head_dim == 128 && c.bits == 2; }
+bool mma_eligible(const ott_cache_t& c) { return c.head_dim == 128 && code_bits(c.bits, c.head_dim, c.group_size) == 2; }
 #ifndef OTT_FP_SPLIT  // allow two full-precision-tier CTAs per unit (tensor-core kernels)
 #define OTT_FP_SPLIT 1
 #endif
@@ -2749,7 +2750,7 @@ bool mma_eligible(const ott_cache_t& c) { return c.head_dim == 128 && c.bits == 
 #define OTT_FUSE_RING 1
 #endif
 bool attend_fuses_ring_write(const ott_cache_t& c) {
-  return OTT_FUSE_RING && c.head_dim == 128 && c.bits == 2 && c.residual >= 1;
+  return OTT_FUSE_RING && mma_eligible(c) && c.residual >= 1;
 }
 
 cudaError_t launch_attend(const ott_cache_t& c, const uint16_t* q, uint16_t* out, int n_rep, int64_t q_tokens,
@@ -2783,7 +2784,8 @@ cudaError_t launch_attend(const ott_cache_t& c, const uint16_t* q, uint16_t* out
   }
   // tensor-core kernels: two CTAs share a unit's full-precision tiers when the quantized
   // splits are short (small MHA shapes such as config 1), so the fp tier is not the tail
-  const bool tc_path = (c.bits == 2 && mma_eligible(c)) || (OTT_MMA4 && (c.bits == 4 || c.bits == 8) && D == 128 && G == 32);
+  const int pb = code_bits(c.bits, D, G);  // stored code width: picks the decode kernel
+  const bool tc_path = mma_eligible(c) || (OTT_MMA4 && (pb == 4 || pb == 8) && D == 128 && G == 32);
   if (tc_path) {
     const int64_t ng = dev_counts ? (int64_t)c.max_groups : q_tokens / G;
     const int64_t per = (ng + n_qsplits - 1) / n_qsplits;
@@ -2796,27 +2798,27 @@ cudaError_t launch_attend(const ott_cache_t& c, const uint16_t* q, uint16_t* out
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
       if (sms <= 0) sms = 148;
     }
-    const int64_t slots = (int64_t)sms * (c.bits == 8 ? 2 : 4);
+    const int64_t slots = (int64_t)sms * (pb == 8 ? 2 : 4);
     const int64_t w1 = ((int64_t)c.n_units * (n_qsplits + 1) + slots - 1) / slots;
     const int64_t w2 = ((int64_t)c.n_units * (n_qsplits + 2) + slots - 1) / slots;
     a.n_fsplits = (OTT_FP_SPLIT && per < 96 && fp_tiles >= 6 && w2 == w1) ? 2 : 1;
     a.n_splits = n_qsplits + a.n_fsplits;
   }
-  if (OTT_MMA4 && c.bits == 4 && D == 128 && G == 32) {  // 4-bit tensor-core kernel
+  if (OTT_MMA4 && pb == 4 && D == 128 && G == 32) {  // 4-bit tensor-core kernel (also 3-bit codes)
     if (n_rep == 1) return launch_mma4_t<1>(a, st);
     if (n_rep == 2) return launch_mma4_t<2>(a, st);
     if (n_rep == 4) return launch_mma4_t<4>(a, st);
     if (n_rep == 8) return launch_mma4_t<8>(a, st);
     return cudaErrorInvalidValue;
   }
-  if (OTT_MMA4 && c.bits == 8 && D == 128 && G == 32) {  // 8-bit tensor-core kernel
+  if (OTT_MMA4 && pb == 8 && D == 128 && G == 32) {  // 8-bit tensor-core kernel (also 5..7-bit codes)
     if (n_rep == 1) return launch_mma8_t<1>(a, st);
     if (n_rep == 2) return launch_mma8_t<2>(a, st);
     if (n_rep == 4) return launch_mma8_t<4>(a, st);
     if (n_rep == 8) return launch_mma8_t<8>(a, st);
     return cudaErrorInvalidValue;
   }
-  if (c.bits != 2) {  // other widths: CUDA-core kernel with generic code extraction
+  if (pb != 2) {  // other widths: CUDA-core kernel with generic code extraction
 #define OTT_BCASE(NRv, Dv) \
   if (n_rep == NRv && D == Dv) return launch_simt_t<NRv, Dv>(a, st);
     OTT_BCASE(1, 64) OTT_BCASE(2, 64) OTT_BCASE(4, 64) OTT_BCASE(8, 64)

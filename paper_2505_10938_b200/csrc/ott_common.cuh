@@ -14,10 +14,22 @@ constexpr int kMaxG = 128;
 constexpr int kMaxN = 128;  // pool capacity supported by the flush kernel
 constexpr int kMaxA = 1024;
 
-// Block record layout (see ott_b200.h). All offsets in bytes.
+// Code width stored in the record. At the tensor-core shapes the widths without a kernel of
+// their own are stored in the next wider container (levels stay 2^bits - 1): 1-bit codes as
+// 2-bit fields (d = 128, G % 32 == 0), 3-bit as 4-bit and 5..7-bit as 8-bit (d = 128, G = 32), so
+// they decode on the 2-, 4- and 8-bit tensor-core attention kernels.
+__host__ __device__ constexpr int code_bits(int bits, int d, int G) {
+  return (d == 128 && G % 32 == 0 && bits == 1) ? 2
+         : (d == 128 && G == 32 && bits == 3) ? 4
+         : (d == 128 && G == 32 && bits >= 5 && bits <= 7) ? 8
+                                                          : bits;
+}
+
+// Block record layout (see ott_b200.h). All offsets in bytes. `bits` is the stored code
+// width (code_bits of the cache's bits).
 struct RecordLayout {
   int d, G, bits;
-  __host__ __device__ RecordLayout(int d_, int G_, int bits_ = 2) : d(d_), G(G_), bits(bits_) {}
+  __host__ __device__ RecordLayout(int d_, int G_, int bits_ = 2) : d(d_), G(G_), bits(code_bits(bits_, d_, G_)) {}
   // packed codes: ceil(G d bits / 8) bytes (quant.py:237-238), padded to 16 so every
   // field stays aligned (no padding at the tensor-core shapes d in {64, 128}, G % 32 == 0)
   __host__ __device__ int code_bytes() const { return ((G * d * bits + 7) / 8 + 15) & ~15; }

@@ -427,6 +427,7 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
     float* vxmin = reinterpret_cast<float*>(rec + L.v_xmin());
     if (warp < kwarps) {
       const int col = tid;
+      const int kshift = (c.bits == 1 && L.bits == 2) ? 1 : 0;
       float kst = 0.f;
       if (col < d) {
         float fmn = sk[col], fmx = fmn;
@@ -446,19 +447,21 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
           bool slow;
           int code = quant_code_f32(x, fmn, fmx, levels, fl, slow);
           if (slow) code = quant_code_slow(x, fmn, fmx, mn, step, inv, levels, eps);
-          kc[i * d + col] = (uint8_t)code;
+          kc[i * d + col] = (uint8_t)(code << kshift);
         }
         // decode-side encoding (ott_common.cuh): 2-bit: step = sh + sl, e = x_min - 4 u step;
-        // other widths: float32 step and x_min
-        kst = (float)step;
-        if (c.bits == 2 || k_tc4(c.bits, d) || k_tc8(c.bits, d)) {
-          const __half sh = __double2half(step);
-          const __half sl = __double2half(__dsub_rn(step, (double)__half2float(sh)));
-          const int j = c.bits == 2 ? kpair_index(col, d) : (c.bits == 4 ? kpair4_index(col) : col);
+        // other widths: float32 step and x_min. 1-bit K codes in 2-bit fields are stored
+        // doubled with the step halved (exact), so the fp16 step halves cannot overflow
+        const double kstep = kshift ? 0.5 * step : step;
+        kst = (float)kstep;
+        if (L.bits == 2 || k_tc4(L.bits, d) || k_tc8(L.bits, d)) {
+          const __half sh = __double2half(kstep);
+          const __half sl = __double2half(__dsub_rn(kstep, (double)__half2float(sh)));
+          const int j = L.bits == 2 ? kpair_index(col, d) : (L.bits == 4 ? kpair4_index(col) : col);
           ksh[j] = sh;
           ksl[j] = sl;
-          const double off = c.bits == 2 ? 4.0 * (double)kpair_u(col % 8) : (c.bits == 4 ? 64.0 : 1024.0);
-          ke[col] = __double2float_rn(__dsub_rn(mn, __dmul_rn(off, step)));
+          const double off = L.bits == 2 ? 4.0 * (double)kpair_u(col % 8) : (L.bits == 4 ? 64.0 : 1024.0);
+          ke[col] = __double2float_rn(__dsub_rn(mn, __dmul_rn(off, kstep)));
         } else {
           reinterpret_cast<float*>(ksh)[col] = __double2float_rn(step);
           ke[col] = __double2float_rn(mn);
@@ -468,7 +471,7 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
           p64[d + col] = step;
         }
       }
-      if (c.bits == 2 || c.bits == 4 || c.bits == 8) note_step_max(meta + 3, kst);
+      if (L.bits == 2 || L.bits == 4 || L.bits == 8) note_step_max(meta + 3, kst);
     } else {
       // warp vw owns tokens vw + j nvw (j < 32 since G <= 128 and nvw >= 4): the warp reduces
       // each token's min/max, lane j keeps token j's and derives its line parameters (one
@@ -512,7 +515,7 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
           p64[2 * d + G + i] = my_step;
         }
       }
-      if (c.bits == 2 || c.bits == 4 || c.bits == 8) note_step_max(meta + 3, lane < n_my ? (float)my_step : 0.f);
+      if (L.bits == 2 || L.bits == 4 || L.bits == 8) note_step_max(meta + 3, lane < n_my ? (float)my_step : 0.f);
       for (int j = 0; j < n_my; ++j) {
         const int i = vw + j * nvw;
         const float fmn = __shfl_sync(0xffffffffu, my_mn, j), fmx = __shfl_sync(0xffffffffu, my_mx, j);
@@ -537,7 +540,7 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
     {
       uint32_t* kw = reinterpret_cast<uint32_t*>(rec + L.k_codes());
       uint32_t* vw = reinterpret_cast<uint32_t*>(rec + L.v_codes());
-      const int bits = c.bits;
+      const int bits = L.bits;  // stored width (code_bits)
       const int n_codes = G * d;
       const int n_words = (n_codes * bits + 31) / 32;  // the tail of the last word stays 0
       for (int w = tid; w < 2 * n_words; w += kFlushThreads) {

@@ -68,6 +68,11 @@ def expected_k_encoding(step64, xmin64, bits=2):
     return sh_p, sl_p, e
 
 
+def code_bits(bits, d, G):
+    from paper_2505_10938_b200.cache import code_bits as cb
+    return cb(bits, d, G)
+
+
 def assert_unit_matches_oracle(u, ref, exact64=True):
     """Bit-exact quantization state of one GPU unit vs an oracle cache."""
     assert u.total_tokens == ref.total_tokens and u.quantized_tokens == ref.quantized_tokens
@@ -81,8 +86,10 @@ def assert_unit_matches_oracle(u, ref, exact64=True):
             assert [p.step for p in u.quantized_k[b].params] == blk["k_step"].tolist()
             assert [p.x_min for p in u.quantized_v[b].params] == blk["v_xmin"].tolist()
             assert [p.step for p in u.quantized_v[b].params] == blk["v_step"].tolist()
-        if u.config.bits == 2 or (u.config.bits in (4, 8) and u.config.head_dim % 8 == 0):
-            sh, sl, e = expected_k_encoding(blk["k_step"], blk["k_xmin"], u.config.bits)
+        pb = code_bits(u.config.bits, u.config.head_dim, u.config.group_size)  # stored code width
+        if pb == 2 or (pb in (4, 8) and u.config.head_dim % 8 == 0):
+            kst = blk["k_step"] * (0.5 if (pb == 2 and u.config.bits == 1) else 1.0)  # 1-bit: halved step
+            sh, sl, e = expected_k_encoding(kst, blk["k_xmin"], pb)
             np.testing.assert_array_equal(u.k_sh16[b].view(np.uint16), sh.view(np.uint16))
             np.testing.assert_array_equal(u.k_sl16[b].view(np.uint16), sl.view(np.uint16))
             np.testing.assert_array_equal(u.k_e32[b], e)
@@ -201,8 +208,9 @@ def test_config0_all_heads_bit_exact(N):
         assert ok, (h, err)
 
 
-@pytest.mark.parametrize("bits,d,n_rep", [(1, 128, 1), (3, 64, 4), (4, 128, 8), (4, 128, 1), (4, 128, 4), (8, 64, 2),
-                                          (8, 128, 8), (8, 128, 1), (5, 128, 4)])
+@pytest.mark.parametrize("bits,d,n_rep", [(1, 128, 1), (1, 128, 8), (3, 64, 4), (3, 128, 8), (4, 128, 8), (4, 128, 1),
+                                          (4, 128, 4), (8, 64, 2), (8, 128, 8), (8, 128, 1), (5, 128, 4), (6, 128, 2),
+                                          (7, 128, 8)])
 def test_other_bit_widths_vs_oracle(bits, d, n_rep):
     """Bit widths other than 2 (quant.py supports 1..8): flush codes,
     params, pool and packing bit-exact vs the oracle; attention through the CUDA-core
@@ -397,7 +405,7 @@ def test_unsupported_shapes_rejected():
         OTTCache(cfg_of(2, 32, 0, 200, 32, 128), 1, 1, 64)  # pool capacity > 128
 
 
-@pytest.mark.parametrize("bits,N", [(2, 4), (3, 4), (1, 4), (8, 4), (2, 0), (4, 4), (4, 0)])
+@pytest.mark.parametrize("bits,N", [(2, 4), (3, 4), (1, 4), (8, 4), (2, 0), (4, 4), (4, 0), (5, 4), (7, 0)])
 def test_flush_adversarial_lines_vs_oracle(bits, N):
     """Quantization lines built to stress K1's float32 fast path and float64 fallback and the
     frozen-pool kernel's fp16 code thresholds (N = 0: every group takes flush_frozen_kernel):
