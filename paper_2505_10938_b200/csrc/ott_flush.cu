@@ -1314,12 +1314,14 @@ __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen_kernel(ott_cac
 // staging as flush_frozen_kernel; substituted groups (sel != 0) are handled inline (float64
 // column sums of the original rows, float32 means, outlier.py:120-142). Codes take the float32
 // fast path with the float64 recipe as fallback (levels = 15 would need 15 thresholds).
+// kLevels = 7: 3-bit codes in the same 4-bit fields (code_bits).
+template <int kLevels>
 __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen4_kernel(ott_cache_t c, int64_t q0, int n_groups,
                                                                           int64_t ring_end,
                                                                           const uint16_t* __restrict__ in_k,
                                                                           const uint16_t* __restrict__ in_v,
                                                                           int64_t in_stride, int64_t in_first) {
-  constexpr int D = 128, G = 32, kLevels = 15;
+  constexpr int D = 128, G = 32;
   extern __shared__ __align__(16) unsigned char smem[];
   FrozenSmem& sm = *reinterpret_cast<FrozenSmem*>(smem);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1572,7 +1574,7 @@ cudaError_t launch_flush(const ott_cache_t& c, int64_t q0, int n_groups, int64_t
   // bulk flushes at the tensor-core shapes: the sequential kernel runs only the pool
   // competition (scoring, OutlierPool.update, masks, pool/aux rows) group by group, then
   // flush_frozen_kernel substitutes and quantizes all groups in parallel
-  const bool split = OTT_FLUSH_SPLIT && !dev_counts && n_groups > 1 && (c.bits == 2 || c.bits == 4) &&
+  const bool split = OTT_FLUSH_SPLIT && !dev_counts && n_groups > 1 && c.bits >= 2 && c.bits <= 4 &&
                      c.head_dim == 128 && c.group_size == 32;
   if (!split) {
     flush_kernel<<<c.n_units, kFlushThreads, smem, st>>>(c, q0, n_groups, ring_end, in_k, in_v, in_stride, in_first,
@@ -1596,11 +1598,12 @@ cudaError_t launch_flush(const ott_cache_t& c, int64_t q0, int n_groups, int64_t
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const int64_t items = (int64_t)c.n_units * n_groups;
-  if (c.bits == 4) {
-    e = cudaFuncSetAttribute(flush_frozen4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FrozenSmem));
+  if (c.bits == 3 || c.bits == 4) {  // 4-bit fields
+    auto kern = c.bits == 4 ? flush_frozen4_kernel<15> : flush_frozen4_kernel<7>;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FrozenSmem));
     if (e != cudaSuccess) return e;
-    flush_frozen4_kernel<<<(unsigned)((items + kFrozenWarps - 1) / kFrozenWarps), 32 * kFrozenWarps,
-                           sizeof(FrozenSmem), st>>>(c, q0, n_groups, ring_end, in_k, in_v, in_stride, in_first);
+    kern<<<(unsigned)((items + kFrozenWarps - 1) / kFrozenWarps), 32 * kFrozenWarps, sizeof(FrozenSmem), st>>>(
+        c, q0, n_groups, ring_end, in_k, in_v, in_stride, in_first);
     return cudaGetLastError();
   }
   const size_t fsm = OTT_FROZEN_PAIR ? sizeof(FrozenPairSmem) : sizeof(FrozenSmem);
