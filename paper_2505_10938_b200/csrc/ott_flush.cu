@@ -1314,8 +1314,10 @@ __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen_kernel(ott_cac
 // staging as flush_frozen_kernel; substituted groups (sel != 0) are handled inline (float64
 // column sums of the original rows, float32 means, outlier.py:120-142). Codes take the float32
 // fast path with the float64 recipe as fallback (levels = 15 would need 15 thresholds).
-// kLevels = 7: 3-bit codes in the same 4-bit fields (code_bits).
-template <int kLevels>
+// kLevels = 7: 3-bit codes in the same 4-bit fields (code_bits). kBits = 8: byte fields
+// (8-bit codes, and 5..7-bit codes in 8-bit fields): K params in channel order with
+// e = x_min - 1024 step, as K2-8 reads them.
+template <int kLevels, int kBits>
 __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen4_kernel(ott_cache_t c, int64_t q0, int n_groups,
                                                                           int64_t ring_end,
                                                                           const uint16_t* __restrict__ in_k,
@@ -1332,7 +1334,7 @@ __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen4_kernel(ott_ca
   const int base = (int)(q0 + (int64_t)g * G);
   const int64_t gi = base / G;
   uint8_t* rec = record_ptr(c, u, gi);
-  const RecordLayout L(D, G, 4);
+  const RecordLayout L(D, G, kBits);
   uint16_t* sk = sm.k[warp];
   uint16_t* sv = sm.v[warp];
   const uint32_t sel = c.subst_mask[(size_t)u * mask_words_per_unit(c) + (base >> 5)];
@@ -1418,16 +1420,19 @@ __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen4_kernel(ott_ca
       kst_max = fmaxf(kst_max, (float)step[j]);
       const __half sh = __double2half(step[j]);
       const __half sl = __double2half(__dsub_rn(step[j], (double)__half2float(sh)));
-      ksh[kpair4_index(col)] = sh;
-      ksl[kpair4_index(col)] = sl;
-      ke[j] = __double2float_rn(__dsub_rn(mn, __dmul_rn(64.0, step[j])));
+      const int kj = kBits == 4 ? kpair4_index(col) : col;
+      ksh[kj] = sh;
+      ksl[kj] = sl;
+      ke[j] = __double2float_rn(__dsub_rn(mn, __dmul_rn(kBits == 4 ? 64.0 : 1024.0, step[j])));
       if (p64) {
         p64[col] = mn;
         p64[D + col] = step[j];
       }
     }
     *reinterpret_cast<float4*>(rec + L.k_e() + 16 * lane) = make_float4(ke[0], ke[1], ke[2], ke[3]);
-    uint16_t* kcodes = reinterpret_cast<uint16_t*>(rec + L.k_codes()) + lane;  // channels 4 lane..+3 of token t
+    // channels 4 lane..+3 of token t: one uint16 of nibbles or one uint32 of bytes
+    uint16_t* kcodes4 = reinterpret_cast<uint16_t*>(rec + L.k_codes()) + lane;
+    uint32_t* kcodes8 = reinterpret_cast<uint32_t*>(rec + L.k_codes()) + lane;
 #pragma unroll 4
     for (int t = 0; t < G; ++t) {
       float x[4];
@@ -1438,9 +1443,10 @@ __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen4_kernel(ott_ca
         bool slow;
         int code = quant_code_f32(x[j], fmn[j], fmx[j], kLevels, fl[j], slow);
         if (slow) code = quant_code_slow(x[j], fmn[j], fmx[j], (double)fmn[j], step[j], inv[j], kLevels, eps);
-        h |= (uint32_t)code << (4 * j);
+        h |= (uint32_t)code << (kBits * j);
       }
-      kcodes[t * (D / 4)] = (uint16_t)h;
+      if (kBits == 4) kcodes4[t * (D / 4)] = (uint16_t)h;
+      else kcodes8[t * (D / 4)] = h;
     }
   }
   // ---- V column means (substituted groups only): lane l sums channels 4l..4l+3
@@ -1503,24 +1509,31 @@ __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen4_kernel(ott_ca
       p64[2 * D + t] = mn;
       p64[2 * D + G + t] = step;
     }
-    uint32_t w[D / 8];
+    constexpr int kWords = D * kBits / 32;  // words of one token's V codes
+    uint32_t w[kWords];
 #pragma unroll
-    for (int j = 0; j < D / 8; ++j) {  // chunk j = channels 8j..8j+7 = word j (nibbles)
+    for (int j = 0; j < D / 8; ++j) {  // chunk j = channels 8j..8j+7 = word j (nibbles) / 2j, 2j+1 (bytes)
       float x[8];
       vval(j, x);
-      uint32_t bits = 0;
+      uint32_t bits[2] = {0u, 0u};
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         bool slow;
         int code = quant_code_f32(x[e], fmn, fmx, kLevels, fl, slow);
         if (slow) code = quant_code_slow(x[e], fmn, fmx, mn, step, inv, kLevels, eps);
-        bits |= (uint32_t)code << (4 * e);
+        if (kBits == 4) bits[0] |= (uint32_t)code << (4 * e);
+        else bits[e >> 2] |= (uint32_t)code << (8 * (e & 3));
       }
-      w[j] = bits;
+      if (kBits == 4) {
+        w[j] = bits[0];
+      } else {
+        w[2 * j] = bits[0];
+        w[2 * j + 1] = bits[1];
+      }
     }
-    uint4* vcodes = reinterpret_cast<uint4*>(rec + L.v_codes() + t * (D / 2));
+    uint4* vcodes = reinterpret_cast<uint4*>(rec + L.v_codes() + t * (D * kBits / 8));
 #pragma unroll
-    for (int q = 0; q < 4; ++q) vcodes[q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+    for (int q = 0; q < kWords / 4; ++q) vcodes[q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
   }
   note_step_max(meta3, fmaxf(kst_max, vst));
 }
@@ -1574,8 +1587,8 @@ cudaError_t launch_flush(const ott_cache_t& c, int64_t q0, int n_groups, int64_t
   // bulk flushes at the tensor-core shapes: the sequential kernel runs only the pool
   // competition (scoring, OutlierPool.update, masks, pool/aux rows) group by group, then
   // flush_frozen_kernel substitutes and quantizes all groups in parallel
-  const bool split = OTT_FLUSH_SPLIT && !dev_counts && n_groups > 1 && c.bits >= 2 && c.bits <= 4 &&
-                     c.head_dim == 128 && c.group_size == 32;
+  const bool split = OTT_FLUSH_SPLIT && !dev_counts && n_groups > 1 && c.bits >= 2 && c.head_dim == 128 &&
+                     c.group_size == 32;
   if (!split) {
     flush_kernel<<<c.n_units, kFlushThreads, smem, st>>>(c, q0, n_groups, ring_end, in_k, in_v, in_stride, in_first,
                                                            dev_counts);
@@ -1598,8 +1611,13 @@ cudaError_t launch_flush(const ott_cache_t& c, int64_t q0, int n_groups, int64_t
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const int64_t items = (int64_t)c.n_units * n_groups;
-  if (c.bits == 3 || c.bits == 4) {  // 4-bit fields
-    auto kern = c.bits == 4 ? flush_frozen4_kernel<15> : flush_frozen4_kernel<7>;
+  if (c.bits >= 3) {  // 4-bit fields (3, 4 bits) and byte fields (5..8 bits)
+    auto kern = c.bits == 3   ? flush_frozen4_kernel<7, 4>
+                : c.bits == 4 ? flush_frozen4_kernel<15, 4>
+                : c.bits == 5 ? flush_frozen4_kernel<31, 8>
+                : c.bits == 6 ? flush_frozen4_kernel<63, 8>
+                : c.bits == 7 ? flush_frozen4_kernel<127, 8>
+                              : flush_frozen4_kernel<255, 8>;
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FrozenSmem));
     if (e != cudaSuccess) return e;
     kern<<<(unsigned)((items + kFrozenWarps - 1) / kFrozenWarps), 32 * kFrozenWarps, sizeof(FrozenSmem), st>>>(
