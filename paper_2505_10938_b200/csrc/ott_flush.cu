@@ -1314,7 +1314,8 @@ __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen_kernel(ott_cac
 // staging as flush_frozen_kernel; substituted groups (sel != 0) are handled inline (float64
 // column sums of the original rows, float32 means, outlier.py:120-142). Codes take the float32
 // fast path with the float64 recipe as fallback (levels = 15 would need 15 thresholds).
-// kLevels = 7: 3-bit codes in the same 4-bit fields (code_bits). kBits = 8: byte fields
+// kLevels = 7: 3-bit codes in the same 4-bit fields (code_bits). kBits = 2, kLevels = 1: 1-bit
+// codes in 2-bit fields (K codes doubled, K step halved, K params in K2's pair order). kBits = 8: byte fields
 // (8-bit codes, and 5..7-bit codes in 8-bit fields): K params in channel order with
 // e = x_min - 1024 step, as K2-8 reads them.
 template <int kLevels, int kBits>
@@ -1324,6 +1325,7 @@ __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen4_kernel(ott_ca
                                                                           const uint16_t* __restrict__ in_v,
                                                                           int64_t in_stride, int64_t in_first) {
   constexpr int D = 128, G = 32;
+  constexpr int kShift = (kBits == 2 && kLevels == 1) ? 1 : 0;
   extern __shared__ __align__(16) unsigned char smem[];
   FrozenSmem& sm = *reinterpret_cast<FrozenSmem*>(smem);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1417,20 +1419,24 @@ __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen4_kernel(ott_ca
       line_params(mn, (double)fmx[j], (double)kLevels, step[j]);
       inv[j] = step[j] > 0.0 ? __drcp_rn(step[j]) : 0.0;
       fl[j] = fast_line(fmn[j], fmx[j], step[j], inv[j], kLevels);
-      kst_max = fmaxf(kst_max, (float)step[j]);
-      const __half sh = __double2half(step[j]);
-      const __half sl = __double2half(__dsub_rn(step[j], (double)__half2float(sh)));
-      const int kj = kBits == 4 ? kpair4_index(col) : col;
+      // 1-bit codes in 2-bit fields: K codes doubled, step halved (exact; see flush_kernel)
+      const double kstep = kShift ? 0.5 * step[j] : step[j];
+      kst_max = fmaxf(kst_max, (float)kstep);
+      const __half sh = __double2half(kstep);
+      const __half sl = __double2half(__dsub_rn(kstep, (double)__half2float(sh)));
+      const int kj = kBits == 2 ? kpair_index(col, D) : (kBits == 4 ? kpair4_index(col) : col);
       ksh[kj] = sh;
       ksl[kj] = sl;
-      ke[j] = __double2float_rn(__dsub_rn(mn, __dmul_rn(kBits == 4 ? 64.0 : 1024.0, step[j])));
+      const double off = kBits == 2 ? 4.0 * (double)kpair_u(col % 8) : (kBits == 4 ? 64.0 : 1024.0);
+      ke[j] = __double2float_rn(__dsub_rn(mn, __dmul_rn(off, kstep)));
       if (p64) {
         p64[col] = mn;
         p64[D + col] = step[j];
       }
     }
     *reinterpret_cast<float4*>(rec + L.k_e() + 16 * lane) = make_float4(ke[0], ke[1], ke[2], ke[3]);
-    // channels 4 lane..+3 of token t: one uint16 of nibbles or one uint32 of bytes
+    // channels 4 lane..+3 of token t: one byte of 2-bit fields, one uint16 of nibbles or one uint32 of bytes
+    uint8_t* kcodes2 = rec + L.k_codes() + lane;
     uint16_t* kcodes4 = reinterpret_cast<uint16_t*>(rec + L.k_codes()) + lane;
     uint32_t* kcodes8 = reinterpret_cast<uint32_t*>(rec + L.k_codes()) + lane;
 #pragma unroll 4
@@ -1443,9 +1449,10 @@ __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen4_kernel(ott_ca
         bool slow;
         int code = quant_code_f32(x[j], fmn[j], fmx[j], kLevels, fl[j], slow);
         if (slow) code = quant_code_slow(x[j], fmn[j], fmx[j], (double)fmn[j], step[j], inv[j], kLevels, eps);
-        h |= (uint32_t)code << (kBits * j);
+        h |= (uint32_t)(code << kShift) << (kBits * j);
       }
-      if (kBits == 4) kcodes4[t * (D / 4)] = (uint16_t)h;
+      if (kBits == 2) kcodes2[t * (D / 4)] = (uint8_t)h;
+      else if (kBits == 4) kcodes4[t * (D / 4)] = (uint16_t)h;
       else kcodes8[t * (D / 4)] = h;
     }
   }
@@ -1511,6 +1518,10 @@ __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen4_kernel(ott_ca
     }
     constexpr int kWords = D * kBits / 32;  // words of one token's V codes
     uint32_t w[kWords];
+    if (kBits == 2) {
+#pragma unroll
+      for (int q = 0; q < kWords; ++q) w[q] = 0u;
+    }
 #pragma unroll
     for (int j = 0; j < D / 8; ++j) {  // chunk j = channels 8j..8j+7 = word j (nibbles) / 2j, 2j+1 (bytes)
       float x[8];
@@ -1521,10 +1532,13 @@ __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen4_kernel(ott_ca
         bool slow;
         int code = quant_code_f32(x[e], fmn, fmx, kLevels, fl, slow);
         if (slow) code = quant_code_slow(x[e], fmn, fmx, mn, step, inv, kLevels, eps);
-        if (kBits == 4) bits[0] |= (uint32_t)code << (4 * e);
+        if (kBits == 2) bits[0] |= (uint32_t)code << (2 * e);
+        else if (kBits == 4) bits[0] |= (uint32_t)code << (4 * e);
         else bits[e >> 2] |= (uint32_t)code << (8 * (e & 3));
       }
-      if (kBits == 4) {
+      if (kBits == 2) {
+        w[j >> 1] |= bits[0] << (16 * (j & 1));
+      } else if (kBits == 4) {
         w[j] = bits[0];
       } else {
         w[2 * j] = bits[0];
@@ -1587,8 +1601,7 @@ cudaError_t launch_flush(const ott_cache_t& c, int64_t q0, int n_groups, int64_t
   // bulk flushes at the tensor-core shapes: the sequential kernel runs only the pool
   // competition (scoring, OutlierPool.update, masks, pool/aux rows) group by group, then
   // flush_frozen_kernel substitutes and quantizes all groups in parallel
-  const bool split = OTT_FLUSH_SPLIT && !dev_counts && n_groups > 1 && c.bits >= 2 && c.head_dim == 128 &&
-                     c.group_size == 32;
+  const bool split = OTT_FLUSH_SPLIT && !dev_counts && n_groups > 1 && c.head_dim == 128 && c.group_size == 32;
   if (!split) {
     flush_kernel<<<c.n_units, kFlushThreads, smem, st>>>(c, q0, n_groups, ring_end, in_k, in_v, in_stride, in_first,
                                                            dev_counts);
@@ -1611,8 +1624,9 @@ cudaError_t launch_flush(const ott_cache_t& c, int64_t q0, int n_groups, int64_t
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const int64_t items = (int64_t)c.n_units * n_groups;
-  if (c.bits >= 3) {  // 4-bit fields (3, 4 bits) and byte fields (5..8 bits)
-    auto kern = c.bits == 3   ? flush_frozen4_kernel<7, 4>
+  if (c.bits != 2) {  // 2-bit fields (1 bit), 4-bit fields (3, 4 bits) and byte fields (5..8 bits)
+    auto kern = c.bits == 1   ? flush_frozen4_kernel<1, 2>
+                : c.bits == 3 ? flush_frozen4_kernel<7, 4>
                 : c.bits == 4 ? flush_frozen4_kernel<15, 4>
                 : c.bits == 5 ? flush_frozen4_kernel<31, 8>
                 : c.bits == 6 ? flush_frozen4_kernel<63, 8>
