@@ -1327,9 +1327,11 @@ __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen4_kernel(ott_ca
   constexpr int D = 128, G = 32;
   constexpr int kShift = (kBits == 2 && kLevels == 1) ? 1 : 0;
   extern __shared__ __align__(16) unsigned char smem[];
-  FrozenSmem& sm = *reinterpret_cast<FrozenSmem*>(smem);
+  FrozenPairSmem& sm = *reinterpret_cast<FrozenPairSmem*>(smem);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t item = (int64_t)blockIdx.x * kFrozenWarps + warp;
+  // warp pairs share a group: the even warp stages and quantizes the K rows, the odd one V
+  const int part = warp & 1;
+  const int64_t item = ((int64_t)blockIdx.x * kFrozenWarps + warp) >> 1;
   if (item >= (int64_t)c.n_units * n_groups) return;
   const int u = (int)(item / n_groups), g = (int)(item % n_groups);
   const int cap = G + c.residual;
@@ -1337,8 +1339,8 @@ __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen4_kernel(ott_ca
   const int64_t gi = base / G;
   uint8_t* rec = record_ptr(c, u, gi);
   const RecordLayout L(D, G, kBits);
-  uint16_t* sk = sm.k[warp];
-  uint16_t* sv = sm.v[warp];
+  uint16_t* sk = sm.rows[warp];
+  uint16_t* sv = sm.rows[warp];
   const uint32_t sel = c.subst_mask[(size_t)u * mask_words_per_unit(c) + (base >> 5)];
   {
     const int bslot = base % cap, ring_end32 = (int)ring_end, in_first32 = (int)in_first;
@@ -1359,8 +1361,8 @@ __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen4_kernel(ott_ca
         pk = in_k + off;
         pv = in_v + off;
       }
-      cp_async16(sk + row * D + ch * 8, pk);
-      cp_async16(sv + row * D + ((ch ^ (row & 15)) * 8), pv);
+      if (part == 0) cp_async16(sk + row * D + ch * 8, pk);
+      else cp_async16(sv + row * D + ((ch ^ (row & 15)) * 8), pv);
     }
     asm volatile("cp.async.wait_all;\n" ::: "memory");
     __syncwarp();
@@ -1371,7 +1373,7 @@ __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen4_kernel(ott_ca
   float kst_max = 0.f, vst = 0.f;
   const uint2* kr = reinterpret_cast<const uint2*>(sk) + lane;
   // ---- K: channels 4 lane .. +3
-  {
+  if (part == 0) {
     float mean[4] = {0.f, 0.f, 0.f, 0.f};
     if (sel) {
       double sum[4] = {0.0, 0.0, 0.0, 0.0};
@@ -1457,7 +1459,7 @@ __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen4_kernel(ott_ca
     }
   }
   // ---- V column means (substituted groups only): lane l sums channels 4l..4l+3
-  if (sel) {
+  if (part == 1 && sel) {
     double sum[4] = {0.0, 0.0, 0.0, 0.0};
     for (int t = 0; t < G; ++t) {
       const uint2 r = *reinterpret_cast<const uint2*>(sv + t * D + (((lane >> 1) ^ (t & 15)) * 8) + (lane & 1) * 4);
@@ -1473,7 +1475,7 @@ __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen4_kernel(ott_ca
     __syncwarp();
   }
   // ---- V: token `lane`
-  {
+  if (part == 1) {
     const int t = lane;
     const bool subst = (sel >> t) & 1u;
     const uint4* vr = reinterpret_cast<const uint4*>(sv + t * D);
@@ -1632,10 +1634,10 @@ cudaError_t launch_flush(const ott_cache_t& c, int64_t q0, int n_groups, int64_t
                 : c.bits == 6 ? flush_frozen4_kernel<63, 8>
                 : c.bits == 7 ? flush_frozen4_kernel<127, 8>
                               : flush_frozen4_kernel<255, 8>;
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FrozenSmem));
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FrozenPairSmem));
     if (e != cudaSuccess) return e;
-    kern<<<(unsigned)((items + kFrozenWarps - 1) / kFrozenWarps), 32 * kFrozenWarps, sizeof(FrozenSmem), st>>>(
-        c, q0, n_groups, ring_end, in_k, in_v, in_stride, in_first);
+    kern<<<(unsigned)((2 * items + kFrozenWarps - 1) / kFrozenWarps), 32 * kFrozenWarps, sizeof(FrozenPairSmem),
+           st>>>(c, q0, n_groups, ring_end, in_k, in_v, in_stride, in_first);
     return cudaGetLastError();
   }
   const size_t fsm = OTT_FROZEN_PAIR ? sizeof(FrozenPairSmem) : sizeof(FrozenSmem);
