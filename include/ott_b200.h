@@ -128,8 +128,9 @@ int ott_flush(const ott_cache_t* c, int64_t quantized_tokens, int32_t n_groups, 
               void* stream);
 
 /* Mixed-tier decode attention (attend_mixed) for n_rep query heads per unit.
- * q, out: fp16 [n_units][n_rep][d] (= [B][H_q][d] with H_q = H_kv*n_rep), n_rep in [1, 8]
- * (3, 5, 6, 7 run padded to 4 or 8 heads; the workspace then also holds the staged q/out).
+ * q, out: fp16 [n_units][n_rep][d] (= [B][H_q][d] with H_q = H_kv*n_rep), n_rep in [1, 128]
+ * (3, 5, 6, 7 run padded to 4 or 8 heads, more than 8 in chunks of 8 heads; the workspace then
+ * also holds the staged q/out).
  * The sequence axis is split n_splits ways (split-K flash decoding) and the
  * partials merged in-kernel; ott_pick_splits chooses a count that fills the
  * GPU, ott_attend_workspace_floats sizes the float32 workspace for it. */

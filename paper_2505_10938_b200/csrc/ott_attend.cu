@@ -69,6 +69,8 @@ struct AttnArgs {
                                      // taken from [quantized, total] before this step's append)
   const uint16_t *new_k, *new_v;     // non-null: this step's appended rows [n_units][d], written to
                                      // the pending ring (slot (total-1) % (G+R)) by the fp-tier CTA
+  bool advance;                      // device-counter mode: the combine advances the counts (false
+                                     // for all but the last head chunk of n_rep > 8)
 };
 
 // Token counts of one launch. Host mode: the launch arguments. Device-counter mode
@@ -2548,7 +2550,8 @@ static cudaError_t launch_combine(const AttnArgs& a, int NR, cudaStream_t st, bo
   gd.bits = code_bits(a.c.bits, a.c.head_dim, a.c.group_size);
   gd.n_qsplits = a.n_qsplits;
   return cudaLaunchKernelEx(&cfg, combine_kernel<D>, (const float*)a.ws, a.out, a.c.n_units * NR, a.n_splits,
-                            const_cast<int64_t*>(a.dev_counts), a.c.group_size, a.c.residual, a.c.max_groups,
+                            a.advance ? const_cast<int64_t*>(a.dev_counts) : nullptr, a.c.group_size, a.c.residual,
+                            a.c.max_groups,
                             a.c.head_dim, gd, tc_path ? 1 : 0);
 }
 
@@ -2755,9 +2758,10 @@ bool attend_fuses_ring_write(const ott_cache_t& c) {
 
 cudaError_t launch_attend(const ott_cache_t& c, const uint16_t* q, uint16_t* out, int n_rep, int64_t q_tokens,
                           int64_t total, float* ws, int n_qsplits, cudaStream_t st, int64_t* dev_counts,
-                          const uint16_t* new_k, const uint16_t* new_v) {
+                          const uint16_t* new_k, const uint16_t* new_v, bool advance) {
   AttnArgs a;
   a.dev_counts = dev_counts;
+  a.advance = advance;
   a.new_k = new_k;
   a.new_v = new_v;
   a.c = c;
@@ -2852,43 +2856,46 @@ cudaError_t launch_attend(const ott_cache_t& c, const uint16_t* q, uint16_t* out
 // Query-head counts the kernels are not instantiated for (3, 5, 6, 7): the heads of each
 // unit are staged into the next instantiated count (4 or 8) with zero rows, and only the real
 // heads' outputs are copied back (plus the fused peer stores, which the padded combine skips).
+// Heads [h0, h0 + nh) of every unit's n_rep query heads <-> the staged [units][nr][d] layout.
 __global__ void rep_pad_kernel(const uint16_t* __restrict__ q, uint16_t* __restrict__ qs, int64_t n, int n_rep,
-                               int nr, int d) {
+                               int h0, int nh, int nr, int d) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int j = (int)(i % d);
     const int64_t row = i / d;  // unit * nr + r
     const int r = (int)(row % nr);
     const int64_t u = row / nr;
-    qs[i] = r < n_rep ? q[(u * n_rep + r) * d + j] : (uint16_t)0;
+    qs[i] = r < nh ? q[(u * n_rep + h0 + r) * d + j] : (uint16_t)0;
   }
 }
 
 __global__ void rep_unpad_kernel(ott_cache_t c, const uint16_t* __restrict__ os, uint16_t* __restrict__ out,
-                                 int64_t n, int n_rep, int nr, int d) {
+                                 int64_t n, int n_rep, int h0, int nh, int nr, int d) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int j = (int)(i % d);
-    const int64_t row = i / d;  // unit * n_rep + r
-    const int r = (int)(row % n_rep);
-    const int64_t u = row / n_rep;
+    const int64_t row = i / d;  // unit * nh + r
+    const int r = (int)(row % nh);
+    const int64_t u = row / nh;
     const uint16_t x = os[(u * nr + r) * d + j];
-    out[i] = x;
-    for (int p = 0; p < c.n_out_peers; ++p) c.out_peer[p][i] = x;
+    const size_t o = (size_t)(u * n_rep + h0 + r) * d + j;
+    out[o] = x;
+    for (int p = 0; p < c.n_out_peers; ++p) c.out_peer[p][o] = x;
   }
 }
 
-cudaError_t launch_rep_pad(const uint16_t* q, uint16_t* qs, int n_units, int n_rep, int nr, int d, cudaStream_t st) {
+cudaError_t launch_rep_pad(const uint16_t* q, uint16_t* qs, int n_units, int n_rep, int h0, int nh, int nr, int d,
+                           cudaStream_t st) {
   const int64_t n = (int64_t)n_units * nr * d;
   const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
-  rep_pad_kernel<<<blocks, 256, 0, st>>>(q, qs, n, n_rep, nr, d);
+  rep_pad_kernel<<<blocks, 256, 0, st>>>(q, qs, n, n_rep, h0, nh, nr, d);
   return cudaGetLastError();
 }
 
-cudaError_t launch_rep_unpad(const ott_cache_t& c, const uint16_t* os, uint16_t* out, int n_rep, int nr,
-                             cudaStream_t st) {
+cudaError_t launch_rep_unpad(const ott_cache_t& c, const uint16_t* os, uint16_t* out, int n_rep, int h0, int nh,
+                             int nr, cudaStream_t st) {
   const int d = c.head_dim;
-  const int64_t n = (int64_t)c.n_units * n_rep * d;
+  const int64_t n = (int64_t)c.n_units * nh * d;
   const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
-  rep_unpad_kernel<<<blocks, 256, 0, st>>>(c, os, out, n, n_rep, nr, d);
+  rep_unpad_kernel<<<blocks, 256, 0, st>>>(c, os, out, n, n_rep, h0, nh, nr, d);
   return cudaGetLastError();
 }
 

@@ -14,19 +14,22 @@ cudaError_t launch_ring_write(const ott_cache_t& c, const uint16_t* k, const uin
                               const int64_t* dev_counts = nullptr);
 cudaError_t launch_attend(const ott_cache_t& c, const uint16_t* q, uint16_t* out, int n_rep, int64_t q_tokens,
                           int64_t total, float* ws, int n_splits, cudaStream_t st, int64_t* dev_counts = nullptr,
-                          const uint16_t* new_k = nullptr, const uint16_t* new_v = nullptr);
+                          const uint16_t* new_k = nullptr, const uint16_t* new_v = nullptr, bool advance = true);
 bool attend_fuses_ring_write(const ott_cache_t& c);
 cudaError_t launch_logits(const ott_cache_t& c, const uint16_t* q, float* logits, int n_rep, int64_t q_tokens,
                           int64_t total, cudaStream_t st);
-cudaError_t launch_rep_pad(const uint16_t* q, uint16_t* qs, int n_units, int n_rep, int nr, int d, cudaStream_t st);
-cudaError_t launch_rep_unpad(const ott_cache_t& c, const uint16_t* os, uint16_t* out, int n_rep, int nr,
-                             cudaStream_t st);
+cudaError_t launch_rep_pad(const uint16_t* q, uint16_t* qs, int n_units, int n_rep, int h0, int nh, int nr, int d,
+                           cudaStream_t st);
+cudaError_t launch_rep_unpad(const ott_cache_t& c, const uint16_t* os, uint16_t* out, int n_rep, int h0, int nh,
+                             int nr, cudaStream_t st);
 }  // namespace ott
 
 // Query heads per KV head the attention kernels are instantiated for: 1, 2, 4, 8. Other counts
-// up to 8 run padded to the next one (zero query rows, outputs dropped).
+// up to 8 run padded to the next one (zero query rows, outputs dropped); more than 8 (MQA-style
+// layouts) run in chunks of 8 heads, each chunk one padded launch over the unit's cache.
+constexpr int kMaxRep = 128;
 static int native_rep(int n_rep) {
-  if (n_rep < 1 || n_rep > 8) return 0;
+  if (n_rep < 1 || n_rep > kMaxRep) return 0;
   return n_rep <= 2 ? n_rep : (n_rep <= 4 ? 4 : 8);
 }
 
@@ -48,10 +51,15 @@ static cudaError_t attend_any_rep(const ott_cache_t& c, const uint16_t* q, uint1
   uint16_t* os = qs + (size_t)c.n_units * nr * c.head_dim;
   ott_cache_t cp = c;
   cp.n_out_peers = 0;  // the real heads' rows go to the peers from the unpad kernel
-  cudaError_t e = ott::launch_rep_pad(q, qs, c.n_units, n_rep, nr, c.head_dim, st);
-  if (e == cudaSuccess)
-    e = ott::launch_attend(cp, qs, os, nr, q_tokens, total, ws, n_splits, st, dev_counts, new_k, new_v);
-  if (e == cudaSuccess) e = ott::launch_rep_unpad(c, os, out, n_rep, nr, st);
+  cudaError_t e = cudaSuccess;
+  for (int h0 = 0; h0 < n_rep && e == cudaSuccess; h0 += 8) {
+    const int nh = n_rep - h0 < 8 ? n_rep - h0 : 8;
+    const bool last = h0 + 8 >= n_rep;
+    e = ott::launch_rep_pad(q, qs, c.n_units, n_rep, h0, nh, nr, c.head_dim, st);
+    if (e == cudaSuccess)
+      e = ott::launch_attend(cp, qs, os, nr, q_tokens, total, ws, n_splits, st, dev_counts, new_k, new_v, last);
+    if (e == cudaSuccess) e = ott::launch_rep_unpad(c, os, out, n_rep, h0, nh, nr, st);
+  }
   return e;
 }
 
@@ -177,7 +185,7 @@ int ott_attend(const ott_cache_t* c, const uint16_t* q, uint16_t* out, int32_t n
   int s = check_cache(c);
   if (s) return s;
   if (total_tokens <= 0) return fail(OTT_ERR_CONTRACT, "cannot attend over an empty cache");
-  if (!native_rep(n_rep)) return fail(OTT_ERR_UNSUPPORTED, "n_rep (H_q / H_kv) must be in [1, 8]");
+  if (!native_rep(n_rep)) return fail(OTT_ERR_UNSUPPORTED, "n_rep (H_q / H_kv) must be in [1, 128]");
   if (quantized_tokens < 0 || quantized_tokens > total_tokens || quantized_tokens % c->group_size)
     return fail(OTT_ERR_CONTRACT, "inconsistent token counts");
   if (total_tokens - quantized_tokens > c->group_size + c->residual)
@@ -194,7 +202,7 @@ int ott_append_attend(const ott_cache_t* c, const uint16_t* k, const uint16_t* v
   if (s) return s;
   if (!k || !v) return fail(OTT_ERR_CONTRACT, "null rows");
   if (total_tokens <= 0) return fail(OTT_ERR_CONTRACT, "cannot attend over an empty cache");
-  if (!native_rep(n_rep)) return fail(OTT_ERR_UNSUPPORTED, "n_rep (H_q / H_kv) must be in [1, 8]");
+  if (!native_rep(n_rep)) return fail(OTT_ERR_UNSUPPORTED, "n_rep (H_q / H_kv) must be in [1, 128]");
   if (quantized_tokens < 0 || quantized_tokens > total_tokens - 1 || quantized_tokens % c->group_size)
     return fail(OTT_ERR_CONTRACT, "inconsistent token counts");
   if (total_tokens - quantized_tokens > c->group_size + c->residual)
@@ -214,7 +222,7 @@ int ott_decode_step(const ott_cache_t* c, const uint16_t* k, const uint16_t* v, 
                     int32_t n_rep, int64_t* counters, float* workspace, int32_t n_splits, void* stream) {
   int s = check_cache(c);
   if (s) return s;
-  if (!native_rep(n_rep)) return fail(OTT_ERR_UNSUPPORTED, "n_rep (H_q / H_kv) must be in [1, 8]");
+  if (!native_rep(n_rep)) return fail(OTT_ERR_UNSUPPORTED, "n_rep (H_q / H_kv) must be in [1, 128]");
   if (!k || !v || !q || !out || !counters || !workspace || n_splits < 1)
     return fail(OTT_ERR_CONTRACT, "null buffer or bad split count");
   if (c->capacity > 0 && (!c->pool_pos || !c->pool_score || !c->pool_k || !c->pool_v))

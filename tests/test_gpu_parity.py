@@ -863,10 +863,12 @@ def test_cache_larger_than_2gib_sampled(bits):
 
 
 @pytest.mark.parametrize("bits,G,d,n_rep", [(2, 32, 128, 3), (2, 32, 128, 7), (4, 32, 128, 5), (8, 32, 128, 6),
-                                            (3, 32, 128, 3), (2, 16, 48, 5)])
+                                            (3, 32, 128, 3), (2, 16, 48, 5), (2, 32, 128, 16), (4, 32, 128, 12),
+                                            (2, 16, 48, 10)])
 def test_any_query_heads_per_kv_head_vs_oracle(bits, G, d, n_rep):
     """GQA ratios the kernels are not instantiated for (3, 5, 6, 7 query heads per KV head,
-    e.g. 28/4 or 40/8 head layouts) run padded to the next instantiated ratio: every query
+    e.g. 28/4 or 40/8 head layouts) run padded to the next instantiated ratio, and more than 8
+    (MQA-style) in chunks of 8 heads: every query
     head's output is within tolerance of the oracle for attend, fused append+attend and the
     device-counter step, and the fused peer stores carry only the real heads' rows."""
     from paper_2505_10938_b200 import OTTCache
