@@ -106,7 +106,7 @@ class OTTCache:
     Args:
         config: EngineConfig (same fields as the reference). bits in [1, 8]
             (2-bit uses the tensor-core kernels, other widths the CUDA-core kernel);
-            head_dim and group_size in [1, 128] (d = 128 with G % 32 == 0 runs the
+            head_dim in [1, 256] and group_size in [1, 128] (d = 128 with G % 32 == 0 runs the
             tensor-core kernels; other shapes, e.g. the reference tests' d = 2..16,
             G = 4..16, run a generic CUDA-core kernel).
         batch, n_kv_heads: unit grid.
@@ -123,7 +123,8 @@ class OTTCache:
         if not torch.cuda.is_available():
             raise _native.NativeError("OTTCache needs a CUDA device (B200); there is no CPU path")
         require(1 <= config.bits <= 8, "bits must be in [1, 8]")
-        require(1 <= config.head_dim <= 128, "head_dim must be in [1, 128] on the GPU path")
+        require(1 <= config.head_dim <= 256, "head_dim must be in [1, 256] on the GPU path")
+        require(config.head_dim * config.group_size <= 20480, "group_size * head_dim must be <= 20480 on the GPU path")
         require(1 <= config.group_size <= 128, "group_size must be in [1, 128] on the GPU path")
         require(batch >= 1 and n_kv_heads >= 1 and max_tokens >= 1, "batch, n_kv_heads, max_tokens must be >= 1")
         self.config = config

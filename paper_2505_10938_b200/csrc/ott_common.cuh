@@ -9,7 +9,7 @@
 
 namespace ott {
 
-constexpr int kMaxD = 128;
+constexpr int kMaxD = 256;  // generic kernels; the tensor-core kernels take d = 128
 constexpr int kMaxG = 128;
 constexpr int kMaxN = 128;  // pool capacity supported by the flush kernel
 constexpr int kMaxA = 1024;

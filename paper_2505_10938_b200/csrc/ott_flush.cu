@@ -472,11 +472,15 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
         }
       }
       if (L.bits == 2 || L.bits == 4 || L.bits == 8) note_step_max(meta + 3, kst);
-    } else {
+    }
+    // d <= 128: the K warps and the (>= 4) V warps run side by side; d > 128: the K lines take
+    // every warp, which then go on to the V lines
+    const bool kv_par = nwarps - kwarps >= 4;
+    if (!kv_par || warp >= kwarps) {
       // warp vw owns tokens vw + j nvw (j < 32 since G <= 128 and nvw >= 4): the warp reduces
       // each token's min/max, lane j keeps token j's and derives its line parameters (one
       // float64 division per lane instead of one per token), then the warp quantizes
-      const int vw = warp - kwarps, nvw = nwarps - kwarps;
+      const int vw = kv_par ? warp - kwarps : warp, nvw = kv_par ? nwarps - kwarps : nwarps;
       float my_mn = 0.f, my_mx = 0.f;
       int n_my = 0;
       for (int i = vw; i < G; i += nvw, ++n_my) {

@@ -398,7 +398,7 @@ def test_unsupported_shapes_rejected():
     from paper_2505_10938_b200 import ContractViolation, OTTCache
 
     with pytest.raises(ContractViolation):
-        OTTCache(cfg_of(2, 32, 0, 2, 32, 256), 1, 1, 64)  # head_dim > 128
+        OTTCache(cfg_of(2, 32, 0, 2, 32, 264), 1, 1, 64)  # head_dim > 256
     with pytest.raises(ContractViolation):
         OTTCache(cfg_of(2, 256, 0, 2, 32, 128), 1, 1, 64)  # group_size > 128
     with pytest.raises(ContractViolation):
@@ -510,6 +510,9 @@ def test_batch_shards_match_whole_batch():
     (4, 20, 7, 5, 4, 80, 2),
     (2, 32, 16, 3, 8, 40, 1),
     (8, 12, 3, 0, 0, 24, 1),    # N = 0: plain floor quantization (KIVI-like)
+    (2, 32, 16, 4, 8, 256, 8),  # head_dim 256 (Gemma-style heads)
+    (4, 64, 32, 3, 32, 256, 2),
+    (3, 16, 8, 2, 4, 192, 4),
 ])
 @pytest.mark.parametrize("mode", ["append", "update"])
 def test_generic_shapes_vs_oracle(bits, G, R, N, A, d, n_rep, mode):
