@@ -49,10 +49,10 @@ typedef enum {
  *   [0, CB)                         K codes, reference pack_codes order at the stored
  *                                   width cb; CB = ceil(G*d*cb/8) rounded up to 16 (=
  *                                   G*d*cb/8 when d in {64, 128} and G % 32 == 0).
- *                                   cb = bits, except at d = 128: 1-bit codes in 2-bit
- *                                   fields (G % 32 == 0; K codes stored doubled with the
- *                                   K step halved, exact), 3-bit in 4-bit and 5..7-bit in
- *                                   8-bit fields (G = 32), so every width decodes on a
+ *                                   cb = bits, except at d = 128, G in {32, 64, 128}:
+ *                                   1-bit codes in 2-bit fields (K codes stored doubled
+ *                                   with the K step halved, exact), 3-bit in 4-bit and
+ *                                   5..7-bit in 8-bit fields, so every width decodes on a
  *                                   tensor-core kernel
  *   [CB, 2 CB)                      V codes
  *   fp16 k_sh[d], k_sl[d]           per-channel K step = sh + sl, in pair order

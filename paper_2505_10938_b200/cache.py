@@ -60,11 +60,13 @@ def kpair_index(c, d=128):
 def code_bits(bits, d, G):
     """Stored code width (ott_common.cuh code_bits): at the tensor-core shapes 1-bit codes live
     in 2-bit fields, 3-bit in 4-bit and 5..7-bit in 8-bit fields (levels stay 2^bits - 1)."""
-    if d == 128 and G % 32 == 0 and bits == 1:
+    if d != 128 or G not in (32, 64, 128):
+        return bits
+    if bits == 1:
         return 2
-    if d == 128 and G == 32 and bits == 3:
+    if bits == 3:
         return 4
-    if d == 128 and G == 32 and 5 <= bits <= 7:
+    if 5 <= bits <= 7:
         return 8
     return bits
 

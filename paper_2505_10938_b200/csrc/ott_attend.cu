@@ -1259,6 +1259,31 @@ __device__ __forceinline__ void load_record4(uint32_t dst, const CUtensorMap* ma
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(q4::kRec) : "memory");
   tma_tensor_rows(dst, map, (int)(rec_index * q4::kRows), bar);
 }
+// Tensor maps of the 4/8-bit kernels. Records of G = 32 tokens load as one box (`rec`);
+// records of G = 64/128 tokens are consumed 32 tokens at a time, each staged in the G = 32
+// record layout from five boxes: the K and V code slices (`rec`, box = one slice), the
+// record's K params (`params`, 8 rows) and the two V param slices (`row`, 1 row).
+struct VgMaps {
+  CUtensorMap rec, params, row;
+};
+template <int GR, int kCodeRows, int kRecRows32>
+__device__ __forceinline__ void load_vgroup(uint32_t dst, const VgMaps* m, const ott_cache_t& c, int u, int vg,
+                                            uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+  if (GR == 32) {
+    tma_tensor_rows(dst, &m->rec, (int)(((int64_t)u * c.max_groups + vg) * kRecRows32), bar);
+    return;
+  }
+  constexpr int nsub = GR / 32, code_rows = kCodeRows * nsub, rec_rows = 2 * code_rows + 8 + 2 * nsub;
+  const int64_t base = ((int64_t)u * c.max_groups + vg / nsub) * rec_rows;
+  const int j = vg % nsub;
+  tma_tensor_rows(dst, &m->rec, (int)(base + j * kCodeRows), bar);
+  tma_tensor_rows(dst + kCodeRows * 128, &m->rec, (int)(base + code_rows + j * kCodeRows), bar);
+  tma_tensor_rows(dst + 2 * kCodeRows * 128, &m->params, (int)(base + 2 * code_rows), bar);
+  tma_tensor_rows(dst + (2 * kCodeRows + 8) * 128, &m->row, (int)(base + 2 * code_rows + 8 + j), bar);
+  tma_tensor_rows(dst + (2 * kCodeRows + 9) * 128, &m->row, (int)(base + 2 * code_rows + 8 + nsub + j), bar);
+}
+
 struct Nib {
   uint32_t l4, x, r4, r8;
 };
@@ -1278,8 +1303,8 @@ __device__ __forceinline__ uint32_t vq4(const Nib& n) {
   return nib_src<K>(n) & 0x00F000F0u;
 }
 
-template <int NR>
-__device__ void mma4_body(const AttnArgs& a, const Counts& n, const CUtensorMap* tmap, Mma4Smem& sm) {
+template <int NR, int GR>
+__device__ void mma4_body(const AttnArgs& a, const Counts& n, const VgMaps* tmap, Mma4Smem& sm) {
   constexpr int D = 128, G = 32, kMt = 2, kStages = q4::kStages;
   const RecordLayout L(D, G, 4);
   const ott_cache_t& c = a.c;
@@ -1318,7 +1343,9 @@ __device__ void mma4_body(const AttnArgs& a, const Counts& n, const CUtensorMap*
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
 #pragma unroll
     for (int s = 0; s < kStages; ++s)
-      if (s < my_n) load_record4(stage0 + s * q4::kSlot, tmap, unit_rec + g0 + warp + s * kAttnWarps, bar0 + 8 * s);
+      if (s < my_n)
+        load_vgroup<GR, 16, q4::kRows>(stage0 + s * q4::kSlot, tmap, c, u, g0 + warp + s * kAttnWarps, bar0 + 8 * s,
+                                       q4::kRec);
   }
   __syncthreads();
 
@@ -1497,7 +1524,8 @@ __device__ void mma4_body(const AttnArgs& a, const Counts& n, const CUtensorMap*
       const int ka = k + kStages;
       if (ka < my_n) {
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-        load_record4(stage0 + s * q4::kSlot, tmap, unit_rec + g0 + warp + ka * kAttnWarps, bar0 + 8 * s);
+        load_vgroup<GR, 16, q4::kRows>(stage0 + s * q4::kSlot, tmap, c, u, g0 + warp + ka * kAttnWarps, bar0 + 8 * s,
+                                       q4::kRec);
       }
     }
   }
@@ -1553,9 +1581,9 @@ __device__ void mma4_body(const AttnArgs& a, const Counts& n, const CUtensorMap*
   }
 }
 
-template <int NR>
+template <int NR, int GR>
 __global__ void __launch_bounds__(kAttnThreads, 4)
-    attend_mma4_kernel(const __grid_constant__ AttnArgs a, const __grid_constant__ CUtensorMap tmap) {
+    attend_mma4_kernel(const __grid_constant__ AttnArgs a, const __grid_constant__ VgMaps tmap) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   allow_dependents();
   if ((int)blockIdx.y >= a.n_qsplits) {  // full-precision tiers: pool + pending
@@ -1564,7 +1592,7 @@ __global__ void __launch_bounds__(kAttnThreads, 4)
       reinterpret_cast<int64_t*>(a.ws + (size_t)a.c.n_units * NR * a.n_splits * 130)[0] = n.q_tokens;
     fp_body<NR>(a, n, *reinterpret_cast<FpSmem*>(smem_raw));
   } else {
-    mma4_body<NR>(a, counts_of(a), &tmap, *reinterpret_cast<Mma4Smem*>(smem_raw));
+    mma4_body<NR, GR>(a, counts_of(a), &tmap, *reinterpret_cast<Mma4Smem*>(smem_raw));
   }
 }
 
@@ -1598,8 +1626,8 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
   return r;
 }
 
-template <int NR>
-__device__ void mma8_body(const AttnArgs& a, const Counts& n, const CUtensorMap* tmap, Mma8Smem& sm) {
+template <int NR, int GR>
+__device__ void mma8_body(const AttnArgs& a, const Counts& n, const VgMaps* tmap, Mma8Smem& sm) {
   constexpr int D = 128, G = 32, kMt = 2, kStages = q8::kStages;
   const RecordLayout L(D, G, 8);
   const ott_cache_t& c = a.c;
@@ -1636,7 +1664,9 @@ __device__ void mma8_body(const AttnArgs& a, const Counts& n, const CUtensorMap*
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
 #pragma unroll
     for (int s = 0; s < kStages; ++s)
-      if (s < my_n) load_record8(stage0 + s * q8::kSlot, tmap, unit_rec + g0 + warp + s * kAttnWarps, bar0 + 8 * s);
+      if (s < my_n)
+        load_vgroup<GR, 32, q8::kRows>(stage0 + s * q8::kSlot, tmap, c, u, g0 + warp + s * kAttnWarps, bar0 + 8 * s,
+                                       q8::kRec);
   }
   __syncthreads();
 
@@ -1803,7 +1833,8 @@ __device__ void mma8_body(const AttnArgs& a, const Counts& n, const CUtensorMap*
       const int ka = k + kStages;
       if (ka < my_n) {
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-        load_record8(stage0 + s * q8::kSlot, tmap, unit_rec + g0 + warp + ka * kAttnWarps, bar0 + 8 * s);
+        load_vgroup<GR, 32, q8::kRows>(stage0 + s * q8::kSlot, tmap, c, u, g0 + warp + ka * kAttnWarps, bar0 + 8 * s,
+                                       q8::kRec);
       }
     }
   }
@@ -1858,9 +1889,9 @@ __device__ void mma8_body(const AttnArgs& a, const Counts& n, const CUtensorMap*
   }
 }
 
-template <int NR>
+template <int NR, int GR>
 __global__ void __launch_bounds__(kAttnThreads, 2)
-    attend_mma8_kernel(const __grid_constant__ AttnArgs a, const __grid_constant__ CUtensorMap tmap) {
+    attend_mma8_kernel(const __grid_constant__ AttnArgs a, const __grid_constant__ VgMaps tmap) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   allow_dependents();
   if ((int)blockIdx.y >= a.n_qsplits) {  // full-precision tiers: pool + pending
@@ -1869,7 +1900,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
       reinterpret_cast<int64_t*>(a.ws + (size_t)a.c.n_units * NR * a.n_splits * 130)[0] = n.q_tokens;
     fp_body<NR>(a, n, *reinterpret_cast<FpSmem*>(smem_raw));
   } else {
-    mma8_body<NR>(a, counts_of(a), &tmap, *reinterpret_cast<Mma8Smem*>(smem_raw));
+    mma8_body<NR, GR>(a, counts_of(a), &tmap, *reinterpret_cast<Mma8Smem*>(smem_raw));
   }
 }
 
@@ -2641,14 +2672,12 @@ static cudaError_t record_tensor_map(const ott_cache_t& c, int box_rows, int rec
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
-// 4-bit records: 2-D uint8 view [rows of 128 B], SWIZZLE_128B, one 42-row box per record
-static cudaError_t record_tensor_map4(const ott_cache_t& c, CUtensorMap* map) {
-  CUtensorMap dummy;
-  cudaError_t e0 = record_tensor_map(c, 1, 1, &dummy);  // resolves the driver entry point
-  if (e0 != cudaSuccess) return e0;
-  const cuuint64_t dims[2] = {128, (cuuint64_t)c.n_units * (cuuint64_t)c.max_groups * (cuuint64_t)q4::kRows};
+// 4/8-bit records: 2-D uint8 view [rows of 128 B], SWIZZLE_128B. G = 32: one box per record;
+// G = 64/128: boxes of one 32-token code slice, of the 8 K-param rows and of one row (VgMaps).
+static cudaError_t record_rows_map(const ott_cache_t& c, int rec_rows, int box_rows, CUtensorMap* map) {
+  const cuuint64_t dims[2] = {128, (cuuint64_t)c.n_units * (cuuint64_t)c.max_groups * (cuuint64_t)rec_rows};
   const cuuint64_t strides[1] = {128};
-  const cuuint32_t box[2] = {128, (cuuint32_t)q4::kRows};
+  const cuuint32_t box[2] = {128, (cuuint32_t)box_rows};
   const cuuint32_t estr[2] = {1, 1};
   CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, c.blocks, dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -2656,43 +2685,49 @@ static cudaError_t record_tensor_map4(const ott_cache_t& c, CUtensorMap* map) {
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
-static cudaError_t record_tensor_map8(const ott_cache_t& c, CUtensorMap* map) {
+static cudaError_t record_vg_maps(const ott_cache_t& c, int code_rows32, int rec_rows32, VgMaps* m) {
   CUtensorMap dummy;
-  cudaError_t e0 = record_tensor_map(c, 1, 1, &dummy);  // resolves the driver entry point
-  if (e0 != cudaSuccess) return e0;
-  const cuuint64_t dims[2] = {128, (cuuint64_t)c.n_units * (cuuint64_t)c.max_groups * (cuuint64_t)q8::kRows};
-  const cuuint64_t strides[1] = {128};
-  const cuuint32_t box[2] = {128, (cuuint32_t)q8::kRows};
-  const cuuint32_t estr[2] = {1, 1};
-  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, c.blocks, dims, strides, box, estr,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+  cudaError_t e = record_tensor_map(c, 1, 1, &dummy);  // resolves the driver entry point
+  if (e != cudaSuccess) return e;
+  const int G = c.group_size;
+  if (G == 32) {
+    e = record_rows_map(c, rec_rows32, rec_rows32, &m->rec);
+    m->params = m->rec;
+    m->row = m->rec;
+    return e;
+  }
+  const int nsub = G / 32, rec_rows = 2 * code_rows32 * nsub + 8 + 2 * nsub;
+  e = record_rows_map(c, rec_rows, code_rows32, &m->rec);
+  if (e == cudaSuccess) e = record_rows_map(c, rec_rows, 8, &m->params);
+  if (e == cudaSuccess) e = record_rows_map(c, rec_rows, 1, &m->row);
+  return e;
 }
 
-template <int NR>
+template <int NR, int GR>
 static cudaError_t launch_mma8_t(const AttnArgs& a, cudaStream_t st) {
-  CUtensorMap tmap;
-  cudaError_t te = record_tensor_map8(a.c, &tmap);
+  VgMaps tmap;
+  cudaError_t te = record_vg_maps(a.c, 32, q8::kRows, &tmap);
   if (te != cudaSuccess) return te;
   const size_t smem = sizeof(Mma8Smem) > sizeof(FpSmem) ? sizeof(Mma8Smem) : sizeof(FpSmem);
-  cudaError_t e = cudaFuncSetAttribute(attend_mma8_kernel<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e =
+      cudaFuncSetAttribute(attend_mma8_kernel<NR, GR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  attend_mma8_kernel<NR><<<dim3(a.c.n_units, a.n_splits), kAttnThreads, smem, st>>>(a, tmap);
+  attend_mma8_kernel<NR, GR><<<dim3(a.c.n_units, a.n_splits), kAttnThreads, smem, st>>>(a, tmap);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   return launch_combine<128>(a, NR, st, true, 1.f);
 }
 
-template <int NR>
+template <int NR, int GR>
 static cudaError_t launch_mma4_t(const AttnArgs& a, cudaStream_t st) {
-  CUtensorMap tmap;
-  cudaError_t te = record_tensor_map4(a.c, &tmap);
+  VgMaps tmap;
+  cudaError_t te = record_vg_maps(a.c, 16, q4::kRows, &tmap);
   if (te != cudaSuccess) return te;
   const size_t smem = sizeof(Mma4Smem) > sizeof(FpSmem) ? sizeof(Mma4Smem) : sizeof(FpSmem);
-  cudaError_t e = cudaFuncSetAttribute(attend_mma4_kernel<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e =
+      cudaFuncSetAttribute(attend_mma4_kernel<NR, GR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  attend_mma4_kernel<NR><<<dim3(a.c.n_units, a.n_splits), kAttnThreads, smem, st>>>(a, tmap);
+  attend_mma4_kernel<NR, GR><<<dim3(a.c.n_units, a.n_splits), kAttnThreads, smem, st>>>(a, tmap);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   return launch_combine<128>(a, NR, st, true, 64.f);
@@ -2739,7 +2774,10 @@ static bool use_tc5() {
   return v == 1;
 }
 
-bool mma_eligible(const ott_cache_t& c) { return c.head_dim == 128 && code_bits(c.bits, c.head_dim, c.group_size) == 2; }
+bool mma_eligible(const ott_cache_t& c) {
+  return c.head_dim == 128 && code_bits(c.bits, c.head_dim, c.group_size) == 2 &&
+         (c.group_size == 32 || c.group_size == 64 || c.group_size == 128);
+}
 #ifndef OTT_FP_SPLIT  // allow two full-precision-tier CTAs per unit (tensor-core kernels)
 #define OTT_FP_SPLIT 1
 #endif
@@ -2789,7 +2827,8 @@ cudaError_t launch_attend(const ott_cache_t& c, const uint16_t* q, uint16_t* out
   // tensor-core kernels: two CTAs share a unit's full-precision tiers when the quantized
   // splits are short (small MHA shapes such as config 1), so the fp tier is not the tail
   const int pb = code_bits(c.bits, D, G);  // stored code width: picks the decode kernel
-  const bool tc_path = mma_eligible(c) || (OTT_MMA4 && (pb == 4 || pb == 8) && D == 128 && G == 32);
+  const bool tc_group = G == 32 || G == 64 || G == 128;  // record sizes the tensor-core kernels take
+  const bool tc_path = mma_eligible(c) || (OTT_MMA4 && (pb == 4 || pb == 8) && D == 128 && tc_group);
   if (tc_path) {
     const int64_t ng = dev_counts ? (int64_t)c.max_groups : q_tokens / G;
     const int64_t per = (ng + n_qsplits - 1) / n_qsplits;
@@ -2808,21 +2847,24 @@ cudaError_t launch_attend(const ott_cache_t& c, const uint16_t* q, uint16_t* out
     a.n_fsplits = (OTT_FP_SPLIT && per < 96 && fp_tiles >= 6 && w2 == w1) ? 2 : 1;
     a.n_splits = n_qsplits + a.n_fsplits;
   }
-  if (OTT_MMA4 && pb == 4 && D == 128 && G == 32) {  // 4-bit tensor-core kernel (also 3-bit codes)
-    if (n_rep == 1) return launch_mma4_t<1>(a, st);
-    if (n_rep == 2) return launch_mma4_t<2>(a, st);
-    if (n_rep == 4) return launch_mma4_t<4>(a, st);
-    if (n_rep == 8) return launch_mma4_t<8>(a, st);
+#define OTT_GCASE(FN, NRv, Gv) \
+  if (n_rep == NRv && G == Gv) return FN<NRv, Gv>(a, st);
+  if (OTT_MMA4 && pb == 4 && D == 128 && tc_group) {  // 4-bit tensor-core kernel (also 3-bit codes)
+    OTT_GCASE(launch_mma4_t, 1, 32) OTT_GCASE(launch_mma4_t, 2, 32) OTT_GCASE(launch_mma4_t, 4, 32)
+    OTT_GCASE(launch_mma4_t, 8, 32) OTT_GCASE(launch_mma4_t, 1, 64) OTT_GCASE(launch_mma4_t, 2, 64)
+    OTT_GCASE(launch_mma4_t, 4, 64) OTT_GCASE(launch_mma4_t, 8, 64) OTT_GCASE(launch_mma4_t, 1, 128)
+    OTT_GCASE(launch_mma4_t, 2, 128) OTT_GCASE(launch_mma4_t, 4, 128) OTT_GCASE(launch_mma4_t, 8, 128)
     return cudaErrorInvalidValue;
   }
-  if (OTT_MMA4 && pb == 8 && D == 128 && G == 32) {  // 8-bit tensor-core kernel (also 5..7-bit codes)
-    if (n_rep == 1) return launch_mma8_t<1>(a, st);
-    if (n_rep == 2) return launch_mma8_t<2>(a, st);
-    if (n_rep == 4) return launch_mma8_t<4>(a, st);
-    if (n_rep == 8) return launch_mma8_t<8>(a, st);
+  if (OTT_MMA4 && pb == 8 && D == 128 && tc_group) {  // 8-bit tensor-core kernel (also 5..7-bit codes)
+    OTT_GCASE(launch_mma8_t, 1, 32) OTT_GCASE(launch_mma8_t, 2, 32) OTT_GCASE(launch_mma8_t, 4, 32)
+    OTT_GCASE(launch_mma8_t, 8, 32) OTT_GCASE(launch_mma8_t, 1, 64) OTT_GCASE(launch_mma8_t, 2, 64)
+    OTT_GCASE(launch_mma8_t, 4, 64) OTT_GCASE(launch_mma8_t, 8, 64) OTT_GCASE(launch_mma8_t, 1, 128)
+    OTT_GCASE(launch_mma8_t, 2, 128) OTT_GCASE(launch_mma8_t, 4, 128) OTT_GCASE(launch_mma8_t, 8, 128)
     return cudaErrorInvalidValue;
   }
-  if (pb != 2) {  // other widths: CUDA-core kernel with generic code extraction
+#undef OTT_GCASE
+  if (pb != 2 || !mma_eligible(c)) {  // other widths / group sizes: CUDA-core kernel with generic code extraction
 #define OTT_BCASE(NRv, Dv) \
   if (n_rep == NRv && D == Dv) return launch_simt_t<NRv, Dv>(a, st);
     OTT_BCASE(1, 64) OTT_BCASE(2, 64) OTT_BCASE(4, 64) OTT_BCASE(8, 64)

@@ -16,13 +16,14 @@ constexpr int kMaxA = 1024;
 
 // Code width stored in the record. At the tensor-core shapes the widths without a kernel of
 // their own are stored in the next wider container (levels stay 2^bits - 1): 1-bit codes as
-// 2-bit fields (d = 128, G % 32 == 0), 3-bit as 4-bit and 5..7-bit as 8-bit (d = 128, G = 32), so
-// they decode on the 2-, 4- and 8-bit tensor-core attention kernels.
+// 2-bit fields, 3-bit as 4-bit and 5..7-bit as 8-bit (d = 128, G in {32, 64, 128}), so they
+// decode on the 2-, 4- and 8-bit tensor-core attention kernels.
 __host__ __device__ constexpr int code_bits(int bits, int d, int G) {
-  return (d == 128 && G % 32 == 0 && bits == 1) ? 2
-         : (d == 128 && G == 32 && bits == 3) ? 4
-         : (d == 128 && G == 32 && bits >= 5 && bits <= 7) ? 8
-                                                          : bits;
+  return (d != 128 || (G != 32 && G != 64 && G != 128)) ? bits
+         : bits == 1                                     ? 2
+         : bits == 3                                     ? 4
+         : (bits >= 5 && bits <= 7)                      ? 8
+                                                         : bits;
 }
 
 // Block record layout (see ott_b200.h). All offsets in bytes. `bits` is the stored code

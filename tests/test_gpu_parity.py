@@ -921,3 +921,31 @@ def test_any_query_heads_per_kv_head_vs_oracle(bits, G, d, n_rep):
             ref.append(k[b, h, T0 + t].astype(np.float32), v[b, h, T0 + t].astype(np.float32))
     torch.cuda.synchronize()
     check(out, steps, "decode_step")
+
+
+@pytest.mark.parametrize("bits,G,n_rep", [(4, 128, 8), (4, 64, 4), (8, 128, 2), (8, 64, 8), (3, 128, 4),
+                                          (5, 64, 1), (1, 128, 8), (2, 96, 4)])
+def test_large_groups_vs_oracle(bits, G, n_rep):
+    """4/8-bit (and container-width) caches with G = 64/128 -- the reference's default group size
+    is 128 -- decode on the tensor-core kernels, which stage each 32-token slice of a record
+    (code slices, the record's K params, V param slices) in the G = 32 layout; G = 96 runs on
+    the CUDA-core kernel. State bit-exact, attention within tolerance vs the oracle."""
+    from paper_2505_10938_b200 import OTTCache
+
+    B, Hkv, d, R = 1, 3, 128, 32
+    T = 5 * G + R + 17
+    k, v, q = config0_batch(7 + bits + G, B * Hkv, T, d)
+    cache = OTTCache(cfg_of(bits, G, R, 3, 32, d), B, Hkv, max_tokens=T, keep_f64_params=True)
+    kt, vt = torch.from_numpy(k.reshape(B, Hkv, T, d)).cuda(), torch.from_numpy(v.reshape(B, Hkv, T, d)).cuda()
+    cache.update(kt[:, :, : T - G - 5], vt[:, :, : T - G - 5])
+    for t in range(T - G - 5, T):
+        cache.append(kt[:, :, t], vt[:, :, t])
+    qh = q[:, :n_rep].reshape(B, Hkv * n_rep, d)
+    out = cache.attend(torch.from_numpy(qh).cuda()).float().cpu().numpy()
+    for u in range(B * Hkv):
+        ref = oracle.OracleCache(bits, G, R, 3, 32, d)
+        ref.extend(k[u].astype(np.float32), v[u].astype(np.float32))
+        assert_unit_matches_oracle(cache.unit(0, u), ref)
+        for r in range(n_rep):
+            ok, err = within_tol(out[0, u * n_rep + r], ref.attend(qh[0, u * n_rep + r].astype(np.float32)))
+            assert ok, (u, r, err)

@@ -22,13 +22,14 @@ ap.add_argument("--ctx", type=int, default=8192)
 ap.add_argument("--iters", type=int, default=20)
 ap.add_argument("--pool", type=int, default=32)
 ap.add_argument("--bits", type=int, default=2)
+ap.add_argument("--group", type=int, default=32)
 ap.add_argument("--splits", type=int, default=0)
 ap.add_argument("--append", action="store_true", help="time append_attend (fused ring write) steps")
 ap.add_argument("--graph", action="store_true", help="capture the iters attend launches in one CUDA graph (no host gaps)")
 args = ap.parse_args()
 
 torch.cuda.set_device(0)
-cfg = EngineConfig(bits=args.bits, group_size=32, residual=128, outlier_num=args.pool, aux_capacity=32, skip_layers=(),
+cfg = EngineConfig(bits=args.bits, group_size=args.group, residual=128, outlier_num=args.pool, aux_capacity=32, skip_layers=(),
                    head_dim=128)
 cache = OTTCache(cfg, args.batch, args.kv, args.ctx + 64 + args.iters)
 gen = torch.Generator(device="cuda").manual_seed(0)
