@@ -17,9 +17,10 @@ ap.add_argument("--ctx", type=int, default=4096)
 ap.add_argument("--pool", type=int, default=32)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--bits", type=int, default=2)
+ap.add_argument("--group", type=int, default=32)
 args = ap.parse_args()
 torch.cuda.set_device(0)
-cfg = EngineConfig(bits=args.bits, group_size=32, residual=128, outlier_num=args.pool, aux_capacity=32, skip_layers=(),
+cfg = EngineConfig(bits=args.bits, group_size=args.group, residual=128, outlier_num=args.pool, aux_capacity=32, skip_layers=(),
                    head_dim=128)
 gen = torch.Generator(device="cuda").manual_seed(0)
 k = torch.empty((args.batch, args.kv, args.ctx, 128), dtype=torch.float16, device="cuda")
