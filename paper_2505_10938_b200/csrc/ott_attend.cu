@@ -1336,7 +1336,6 @@ __device__ void mma4_body(const AttnArgs& a, const Counts& n, const VgMaps* tmap
   const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&sm.bar[warp][0]);
   const uint32_t stage0 = (uint32_t)__cvta_generic_to_shared(&sm.stage[warp][0][0]);
   if (stage0 & 1023u) __trap();  // SWIZZLE_128B needs 1 KB-aligned stage slots (see swz128)
-  const int64_t unit_rec = (int64_t)u * c.max_groups;
   if (lane == 0) {
 #pragma unroll
     for (int s = 0; s < kStages; ++s) mbar_init(bar0 + 8 * s, 1);
@@ -1657,7 +1656,6 @@ __device__ void mma8_body(const AttnArgs& a, const Counts& n, const VgMaps* tmap
   const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&sm.bar[warp][0]);
   const uint32_t stage0 = (uint32_t)__cvta_generic_to_shared(&sm.stage[warp][0][0]);
   if (stage0 & 1023u) __trap();  // SWIZZLE_128B needs 1 KB-aligned stage slots
-  const int64_t unit_rec = (int64_t)u * c.max_groups;
   if (lane == 0) {
 #pragma unroll
     for (int s = 0; s < kStages; ++s) mbar_init(bar0 + 8 * s, 1);
