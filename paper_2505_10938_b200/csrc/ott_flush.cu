@@ -119,12 +119,14 @@ struct FlushShared {
 };
 
 // Dynamic smem layout, sized on the host (flush_smem_bytes):
-//   float  sk[G*d], sv[G*d]           group rows (substituted in place)
+//   fp16   sk[G*d], sv[G*d]           group rows as staged (fp16, the inputs' own format)
+//   float  kmean[d], vmean[d]         column means that replace the substituted rows
 //   uint8  kc[G*d], vc[G*d]           codes (16-byte aligned when G*d % 16 == 0)
 //   double score[G]                   (8-byte aligned)
 //   double it_score[N+G]; int it_pos[N+G]; int it_rank[N+G]
 //   int    free_slot[N]; uint8 sel[G]
-__host__ __device__ inline size_t flush_score_offset(int d, int G) { return ((size_t)10 * G * d + 7) & ~(size_t)7; }
+__host__ __device__ inline size_t flush_codes_offset(int d, int G) { return ((size_t)4 * G * d + 8 * (size_t)d + 15) & ~(size_t)15; }
+__host__ __device__ inline size_t flush_score_offset(int d, int G) { return (flush_codes_offset(d, G) + (size_t)2 * G * d + 7) & ~(size_t)7; }
 __host__ __device__ inline size_t flush_smem_bytes(int d, int G, int N) {
   size_t b = flush_score_offset(d, G);
   b += (size_t)G * sizeof(double);
@@ -156,9 +158,11 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
   const double eps = 1e-9 * (double)(levels + 1);  // guard band of quant_code (qa <= levels + 1)
 
   extern __shared__ __align__(16) unsigned char smem[];
-  float* sk = reinterpret_cast<float*>(smem);
-  float* sv = sk + G * d;
-  uint8_t* kc = reinterpret_cast<uint8_t*>(sv + G * d);
+  uint16_t* sk = reinterpret_cast<uint16_t*>(smem);
+  uint16_t* sv = sk + G * d;
+  float* kmean = reinterpret_cast<float*>(sv + G * d);
+  float* vmean = kmean + d;
+  uint8_t* kc = smem + flush_codes_offset(d, G);
   uint8_t* vc = kc + G * d;
   double* score = reinterpret_cast<double*>(smem + flush_score_offset(d, G));
   double* it_score = score + G;
@@ -243,16 +247,16 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
       for (int e = tid; e < G * d; e += kFlushThreads) {
         const uint16_t *srck, *srcv;
         OTT_ROW_SRC(base32, bslot, e / d, e % d, srck, srcv)
-        sk[e] = h2f(*srck);
-        sv[e] = h2f(*srcv);
+        sk[e] = *srck;
+        sv[e] = *srcv;
       }
     }
 #pragma unroll
     for (int it = 0; it < kPre; ++it) {
       const int e = tid * 8 + it * kFlushThreads * 8;
       if (vec && e < G * d) {
-        store8(sk + e, pk8[it]);
-        store8(sv + e, pv8[it]);
+        *reinterpret_cast<uint4*>(sk + e) = pk8[it];
+        *reinterpret_cast<uint4*>(sv + e) = pv8[it];
       }
     }
     for (int e = tid * 8 + kPre * kFlushThreads * 8; vec && e < G * d; e += kFlushThreads * 8) {
@@ -263,8 +267,8 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
         k8 = *reinterpret_cast<const uint4*>(srck);
         v8 = *reinterpret_cast<const uint4*>(srcv);
       }
-      store8(sk + e, k8);
-      store8(sv + e, v8);
+      *reinterpret_cast<uint4*>(sk + e) = k8;
+      *reinterpret_cast<uint4*>(sv + e) = v8;
     }
     if (g + 1 < n_groups && vec) OTT_PREFETCH(base + G)
     if (tid < G) sel[tid] = 0;
@@ -276,7 +280,7 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
       // ---- 2a. score_tokens: L1 norm of each key row in float64 (outlier.py:45-49)
       for (int i = warp; i < G; i += nwarps) {
         double s = 0.0;
-        for (int col = lane; col < d; col += 32) s = __dadd_rn(s, fabs((double)sk[i * d + col]));
+        for (int col = lane; col < d; col += 32) s = __dadd_rn(s, fabs((double)h2f(sk[i * d + col])));
         s = warp_sum(s);
         if (lane == 0) score[i] = s;
       }
@@ -373,8 +377,8 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
         for (int j = 0; j < i; ++j) widx += it_rank[N + j] < N ? 1 : 0;
         const int s = free_slot[widx];
         for (int col = lane; col < d; col += 32) {
-          pk[(size_t)s * d + col] = f2h(sk[i * d + col]);  // original row (fp16-exact)
-          pv[(size_t)s * d + col] = f2h(sv[i * d + col]);
+          pk[(size_t)s * d + col] = sk[i * d + col];  // original row
+          pv[(size_t)s * d + col] = sv[i * d + col];
         }
         if (lane == 0) {
           ppos[s] = (int)(base + i);
@@ -400,22 +404,17 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
         for (int col = tid; col < d; col += kFlushThreads) {
           double mk = 0.0, mv = 0.0;
           for (int i = 0; i < G; ++i) {
-            mk = __dadd_rn(mk, (double)sk[i * d + col]);
-            mv = __dadd_rn(mv, (double)sv[i * d + col]);
+            mk = __dadd_rn(mk, (double)h2f(sk[i * d + col]));
+            mv = __dadd_rn(mv, (double)h2f(sv[i * d + col]));
           }
-          const float fk = __double2float_rn(__ddiv_rn(mk, (double)G));
-          const float fv = __double2float_rn(__ddiv_rn(mv, (double)G));
-          for (int i = 0; i < G; ++i) {
-            if (sel[i]) {
-              sk[i * d + col] = fk;
-              sv[i * d + col] = fv;
-            }
-          }
+          kmean[col] = __double2float_rn(__ddiv_rn(mk, (double)G));  // read in place of the sel rows
+          vmean[col] = __double2float_rn(__ddiv_rn(mv, (double)G));
         }
       }
       __syncthreads();
     }
 
+    const bool subst = active && sh.any_selected;  // block-uniform: kmean/vmean hold this group's means
     // ---- 3. quantize: K per channel (threads [0,d) of the first ceil(d/32) warps), V per
     // token (the remaining warps; d <= 128 leaves at least 4)
     const int kwarps = (d + 31) / 32;
@@ -430,9 +429,12 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
       const int kshift = (c.bits == 1 && L.bits == 2) ? 1 : 0;
       float kst = 0.f;
       if (col < d) {
-        float fmn = sk[col], fmx = fmn;
+        // rows selected by the pool competition read the column mean (outlier.py:120-142)
+        const float km = subst ? kmean[col] : 0.f;
+        auto kx = [&](int i) { return (subst && sel[i]) ? km : h2f(sk[i * d + col]); };
+        float fmn = kx(0), fmx = fmn;
         for (int i = 1; i < G; ++i) {
-          const float x = sk[i * d + col];
+          const float x = kx(i);
           fmn = fminf(fmn, x);
           fmx = fmaxf(fmx, x);
         }
@@ -443,7 +445,7 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
         const FastLine fl = fast_line(fmn, fmx, step, inv, levels);
 #pragma unroll 4
         for (int i = 0; i < G; ++i) {
-          const float x = sk[i * d + col];
+          const float x = kx(i);
           bool slow;
           int code = quant_code_f32(x, fmn, fmx, levels, fl, slow);
           if (slow) code = quant_code_slow(x, fmn, fmx, mn, step, inv, levels, eps);
@@ -486,8 +488,9 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
       for (int i = vw; i < G; i += nvw, ++n_my) {
         // min/max of fp16-valued floats are exact in float32: reduce in float (1 shuffle per level)
         float fmn = 3.4e38f, fmx = -3.4e38f;
+        const bool si = subst && sel[i];
         for (int col = lane; col < d; col += 32) {
-          const float x = sv[i * d + col];
+          const float x = si ? vmean[col] : h2f(sv[i * d + col]);
           fmn = fminf(fmn, x);
           fmx = fmaxf(fmx, x);
         }
@@ -528,9 +531,10 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
         fl.inv32 = __shfl_sync(0xffffffffu, my_fl.inv32, j);
         fl.ok = __shfl_sync(0xffffffffu, (int)my_fl.ok, j) != 0;
         fl.del = 4e-7f * (float)(levels + 1);
+        const bool si = subst && sel[i];
 #pragma unroll 4
         for (int col = lane; col < d; col += 32) {
-          const float x = sv[i * d + col];
+          const float x = si ? vmean[col] : h2f(sv[i * d + col]);
           bool slow;
           int code = quant_code_f32(x, fmn, fmx, levels, fl, slow);
           if (slow) code = quant_code_slow(x, fmn, fmx, (double)fmn, step, inv, levels, eps);
