@@ -73,7 +73,7 @@ typedef enum {
 
 typedef struct {
   int32_t n_units;      /* batch * n_kv_heads */
-  int32_t head_dim;     /* d in [1, 256], G*d <= 20480 (tensor-core kernels: 128; tile kernel: 64, 128) */
+  int32_t head_dim;     /* d in [1, 256] (tensor-core kernels: 128; tile kernel: 64, 128) */
   int32_t group_size;   /* G in [1, 128] (tensor-core / tile kernels: multiple of 32) */
   int32_t residual;     /* R >= 0 */
   int32_t capacity;     /* N: pool capacity for this layer (EngineConfig.outlier_capacity) */

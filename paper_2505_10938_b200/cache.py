@@ -126,7 +126,6 @@ class OTTCache:
             raise _native.NativeError("OTTCache needs a CUDA device (B200); there is no CPU path")
         require(1 <= config.bits <= 8, "bits must be in [1, 8]")
         require(1 <= config.head_dim <= 256, "head_dim must be in [1, 256] on the GPU path")
-        require(config.head_dim * config.group_size <= 20480, "group_size * head_dim must be <= 20480 on the GPU path")
         require(1 <= config.group_size <= 128, "group_size must be in [1, 128] on the GPU path")
         require(batch >= 1 and n_kv_heads >= 1 and max_tokens >= 1, "batch, n_kv_heads, max_tokens must be >= 1")
         self.config = config

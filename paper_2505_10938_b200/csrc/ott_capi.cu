@@ -82,8 +82,6 @@ static int check_cache(const ott_cache_t* c) {
   // any shape in range runs; d = 128 / 2-bit / G % 32 == 0 takes the tensor-core kernels,
   // d in {64, 128} with G % 32 == 0 the CUDA-core tile kernel, the rest the generic kernel
   if (c->head_dim < 1 || c->head_dim > ott::kMaxD) return fail(OTT_ERR_UNSUPPORTED, "head_dim must be in [1, 256]");
-  if ((size_t)10 * c->group_size * c->head_dim > 200 * 1024)  // flush kernel's staged group (10 B per element)
-    return fail(OTT_ERR_UNSUPPORTED, "group_size * head_dim must be <= 20480");
   if (c->group_size < 1 || c->group_size > ott::kMaxG)
     return fail(OTT_ERR_UNSUPPORTED, "group_size must be in [1, 128]");
   if (c->residual < 0 || c->capacity < 0 || c->aux_capacity < 0)

@@ -513,6 +513,7 @@ def test_batch_shards_match_whole_batch():
     (2, 32, 16, 4, 8, 256, 8),  # head_dim 256 (Gemma-style heads)
     (4, 64, 32, 3, 32, 256, 2),
     (3, 16, 8, 2, 4, 192, 4),
+    (2, 128, 16, 8, 8, 256, 1),  # the largest staged group (G = 128, d = 256)
 ])
 @pytest.mark.parametrize("mode", ["append", "update"])
 def test_generic_shapes_vs_oracle(bits, G, R, N, A, d, n_rep, mode):
