@@ -185,6 +185,16 @@ class OTTCache:
     def pending_rows(self) -> int:
         return self.total_tokens - self.quantized_tokens
 
+    def _check_out(self, out: torch.Tensor | None, q: torch.Tensor) -> torch.Tensor:
+        """Caller-supplied output buffer: the kernels write it through a raw pointer (and, with
+        output peers set, the same offsets into the peers' gather buffers), so it must be
+        exactly q's shape, fp16, contiguous and on the cache device."""
+        if out is None:
+            return torch.empty_like(q)
+        require(tuple(out.shape) == tuple(q.shape) and out.dtype == torch.float16 and out.device == self.device
+                and out.is_contiguous(), "out must be a contiguous float16 tensor of q's shape on the cache device")
+        return out
+
     def _check_rows(self, x: torch.Tensor, name: str, T: int | None = None) -> torch.Tensor:
         d = self.config.head_dim
         shape = (self.batch, self.n_kv_heads, d) if T is None else (self.batch, self.n_kv_heads, T, d)
@@ -280,8 +290,7 @@ class OTTCache:
             return self.attend(q, out=out, n_splits=n_splits)
         n_rep = q.shape[1] // self.n_kv_heads
         q = q.contiguous()
-        if out is None:
-            out = torch.empty_like(q)
+        out = self._check_out(out, q)
         G, R = self.config.group_size, self.config.residual
         due = self.total_tokens + 1 - self.quantized_tokens - R >= G  # cache.py:138
         require(not due or self.quantized_tokens // G + 1 <= self.max_groups, "cache capacity (max_tokens) exceeded")
@@ -324,7 +333,8 @@ class OTTCache:
         require(q.dim() == 3 and q.shape[0] == self.batch and q.shape[2] == self.config.head_dim
                 and q.shape[1] % self.n_kv_heads == 0 and q.dtype == torch.float16 and q.is_contiguous(),
                 "query must be contiguous float16 (batch, H_q, head_dim)")
-        require(out.shape == q.shape and out.dtype == torch.float16 and out.is_contiguous(), "bad output buffer")
+        require(q.device == self.device, "query must be on the cache device")
+        self._check_out(out, q)
         G, R = self.config.group_size, self.config.residual
         due = self.total_tokens + 1 - self.quantized_tokens - R >= G
         require(not due or self.quantized_tokens // G + 1 <= self.max_groups, "cache capacity (max_tokens) exceeded")
@@ -359,8 +369,7 @@ class OTTCache:
             raise ContractViolation("cannot attend over an empty cache")  # attention.py:89-90
         n_rep = q.shape[1] // self.n_kv_heads
         q = q.contiguous()
-        if out is None:
-            out = torch.empty_like(q)
+        out = self._check_out(out, q)
         s = n_splits or self.splits(n_rep)
         ws = self.workspace(n_rep, s)
         _native.check(_native.lib().ott_attend(self._cref, q.data_ptr(), out.data_ptr(), n_rep, self.quantized_tokens,
@@ -535,8 +544,9 @@ class TieredCache:
         require(k.ndim == 2 and k.shape == v.shape and k.shape[1] == self.config.head_dim, "bad prefill shape")
         require(np.isfinite(k).all() and np.isfinite(v).all(), "rows contain NaN or Inf")
         kh, vh = k.astype(np.float16), v.astype(np.float16)
-        require(np.array_equal(kh.astype(np.float32), k) and np.array_equal(vh.astype(np.float32), v),
-                "rows are not fp16-representable")
+        require(self.round_rows_to_fp16 or (np.array_equal(kh.astype(np.float32), k)
+                                            and np.array_equal(vh.astype(np.float32), v)),
+                "rows are not fp16-representable (TieredCache(round_rows_to_fp16=True) rounds them)")
         dev = self._c.device
         self._snap = None
         self._c.update(torch.from_numpy(kh).to(dev)[None, None], torch.from_numpy(vh).to(dev)[None, None])

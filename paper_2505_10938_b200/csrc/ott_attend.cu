@@ -28,75 +28,9 @@
 #include <cstdlib>
 #include <cstring>
 
-#include <cuda.h>
-#include <cudaTypedefs.h>
-
-#include "ott_common.cuh"
+#include "ott_attend.cuh"
 
 namespace ott {
-
-#ifndef OTT_MMA_MIN_BLOCKS
-#define OTT_MMA_MIN_BLOCKS 4
-#endif
-constexpr int kAttnThreads = 128;
-constexpr int kAttnWarps = kAttnThreads / 32;
-constexpr float kLog2e = 1.4426950408889634f;
-constexpr float kLazy = 6.f;
-#ifndef OTT_PDL  // launch the split combine as a programmatic dependent of the attention grid
-#define OTT_PDL 1
-#endif
-__device__ __forceinline__ void allow_dependents() {
-#if OTT_PDL
-  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
-#endif
-}
-// lazy-rescale threshold (log2 units, kLazy above): p <= 64, P' = 4 p step fits fp16
-
-struct AttnArgs {
-  ott_cache_t c;
-  const uint16_t* q;
-  uint16_t* out;
-  float* ws;  // [n_units][NR][n_splits][D+2]
-  int64_t q_tokens, total_tokens;
-  int n_splits;   // total partials per (unit, head) = n_qsplits + n_fsplits
-  int n_qsplits;  // splits over the quantized region
-  int n_fsplits;  // CTAs sharing the full-precision tiers (1, or 2 for small quantized regions)
-  int n_qtiles, n_ptiles, n_rtiles;  // 32-token tiles: quantized, pool, pending
-  float scale_log2;                  // log2(e) / float32(sqrt(d))
-  uint32_t k_magic;                  // 0x3C003C00 (fp16 1.0 pair), passed at run time so the
-                                     // compiler keeps it in a register: one LOP3 per code pair
-  const int64_t* dev_counts;         // non-null: device-counter decode step (token counts below are
-                                     // taken from [quantized, total] before this step's append)
-  const uint16_t *new_k, *new_v;     // non-null: this step's appended rows [n_units][d], written to
-                                     // the pending ring (slot (total-1) % (G+R)) by the fp-tier CTA
-  bool advance;                      // device-counter mode: the combine advances the counts (false
-                                     // for all but the last head chunk of n_rep > 8)
-};
-
-// Token counts of one launch. Host mode: the launch arguments. Device-counter mode
-// (CUDA-graph decode step: ring write, flush-if-due, attend, combine): the counters
-// hold the state before the step's append, which has already been written, and the
-// flush kernel has quantized one group iff it was due (cache.py:138).
-struct Counts {
-  int64_t q_tokens, total_tokens;
-  int n_qtiles, n_ptiles, n_rtiles;
-};
-__device__ __forceinline__ Counts counts_of(const AttnArgs& a) {
-  Counts k;
-  if (a.dev_counts) {
-    const int64_t qt = a.dev_counts[0], tot = a.dev_counts[1] + 1;
-    const bool due = tot - qt - a.c.residual >= a.c.group_size && qt / a.c.group_size + 1 <= a.c.max_groups;
-    k.q_tokens = qt + (due ? a.c.group_size : 0);
-    k.total_tokens = tot;
-  } else {
-    k.q_tokens = a.q_tokens;
-    k.total_tokens = a.total_tokens;
-  }
-  k.n_qtiles = (int)(k.q_tokens / 32);
-  k.n_ptiles = (a.c.capacity + 31) / 32;
-  k.n_rtiles = (int)((k.total_tokens - k.q_tokens + 31) / 32);
-  return k;
-}
 
 // ============================================================ SIMT (CUDA-core) tiles
 template <int NR, int D>
@@ -514,135 +448,12 @@ __global__ void __launch_bounds__(kAttnThreads) attend_generic_kernel(AttnArgs a
   }
 }
 
-// ============================================================ tensor-core path
-__device__ __forceinline__ void mma16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
-                                         uint32_t b0, uint32_t b1) {
-  // not volatile: a pure register op, so the scheduler may interleave independent chains
-  asm(
-      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-      "{%0,%1,%2,%3};\n"
-      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
-}
-__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], uint32_t saddr) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-               : "r"(saddr));
-}
-__device__ __forceinline__ void ldsm_x4_t(uint32_t (&r)[4], uint32_t saddr) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-               : "r"(saddr));
-}
-__device__ __forceinline__ float ex2(float x) {  // 2^x, MUFU.EX2 (ftz; -inf -> 0)
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;\n" : "=f"(y) : "f"(x));
-  return y;
-}
-__device__ __forceinline__ uint32_t movm_t(uint32_t x) {
-  uint32_t y;
-  asm("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;\n" : "=r"(y) : "r"(x));
-  return y;
-}
-__device__ __forceinline__ uint32_t pack_h2(float lo, float hi) {
-  uint32_t r;
-  asm("cvt.rn.f16x2.f32 %0, %1, %2;\n" : "=r"(r) : "f"(hi), "f"(lo));
-  return r;
-}
-__device__ __forceinline__ uint32_t h2_as_u32(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
-  uint32_t done = 0;
-  while (!done) {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(done)
-        : "r"(bar), "r"(phase)
-        : "memory");
-  }
-}
-__device__ __forceinline__ void tma_bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
-      "l"(src), "r"(bytes), "r"(bar)
-      : "memory");
-}
-
-// ---- 2-bit pair extraction. A word holds 16 codes (code m at bits 2m, code
-// m+8 at bits 16+2m). Pair m is used in place at fp16 mantissa position P(m)
-// (bits 2P..2P+1 of both halves) taken from one of three copies of the word:
-//   m:    0    1    2   3   4   5    6    7
-//   src:  <<6  <<6  x   x   x   >>6  >>6  >>6      (2 SHF + 8 LOP3 per word)
-//   P:    3    4    2   3   4   2    3    4
-// K codes become fp16 1 + c*2^(2P-10) (one LOP3 with the 1.0 magic); V codes
-// become exact fp16 subnormals c*2^(2P-24). The per-position scale is folded
-// into q' (K) or the final accumulator scale (V).
-struct Shifted {
-  uint32_t x, l6, r6;
-};
-__device__ __forceinline__ Shifted shifted(uint32_t w) { return {w, w << 6, w >> 6}; }
-__host__ __device__ constexpr int pair_pos(int m) { return m == 2 || m == 5 ? 2 : (m == 0 || m == 3 || m == 6 ? 3 : 4); }
-__host__ __device__ constexpr uint32_t pos_mask(int p) { return p == 2 ? 0x00300030u : (p == 3 ? 0x00C000C0u : 0x03000300u); }
-template <int M>
-__device__ __forceinline__ uint32_t pair_src(const Shifted& s) {
-  return M <= 1 ? s.l6 : (M <= 4 ? s.x : s.r6);
-}
-template <int M>
-__device__ __forceinline__ uint32_t kq(const Shifted& s, uint32_t magic) {
-  uint32_t r;
-  asm("lop3.b32 %0, %1, %2, %3, 0xEA;\n" : "=r"(r) : "r"(pair_src<M>(s)), "n"(pos_mask(pair_pos(M))), "r"(magic));
-  return r;
-}
-template <int M>
-__device__ __forceinline__ uint32_t vq(const Shifted& s) {
-  return pair_src<M>(s) & pos_mask(pair_pos(M));
-}
-
-__device__ __forceinline__ uint32_t swz(uint32_t o) { return o ^ ((o >> 3) & 16u); }  // Swizzle<1,4,3>
-__host__ __device__ constexpr int tile_slot(int v4, int tig) { return 4 * v4 + (tig ^ ((v4 >> 1) << 1)); }
-__device__ __forceinline__ void tma_tensor_rows(uint32_t dst, const CUtensorMap* map, int row, uint32_t bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
-          dst),
-      "l"(map), "r"(0), "r"(row), "r"(bar)
-      : "memory");
-}
-template <int G>
-struct RecTma {  // a record is kRows rows of 32 bytes; loaded as kBoxes boxes of kBoxRows rows
-  static constexpr int kRows = (G * 128 / 2 + 8 * 128 + 8 * G) / 32;
-  static constexpr int kBoxes = kRows > 256 ? 2 : 1;
-  static constexpr int kBoxRows = kRows / kBoxes;
-};
-template <int G>
-__device__ __forceinline__ void load_record(uint32_t dst, const CUtensorMap* map, int64_t rec_index, uint32_t bar) {
-  constexpr int kRec = RecTma<G>::kRows * 32;
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(kRec) : "memory");
-#pragma unroll
-  for (int b = 0; b < RecTma<G>::kBoxes; ++b)
-    tma_tensor_rows(dst + b * RecTma<G>::kBoxRows * 32, map,
-                    (int)(rec_index * RecTma<G>::kRows + b * RecTma<G>::kBoxRows), bar);
-}
 
 template <int G>
 struct MmaSmem {
   static constexpr int kRec = G * 128 / 2 + 8 * 128 + 8 * G;  // record bytes at d = 128
-#ifndef OTT_NO_TMA
-#define OTT_NO_TMA 0  // timing experiment only: compute on stale shared memory
-#endif
-#ifndef OTT_NG
-#define OTT_NG 1  // groups per loop iteration per warp (2 measured slower: register spills)
-#endif
-#ifndef OTT_QK_LO  // 1: Q.K^T also multiplies the lo halves of q' (2 HMMA per k-step)
-#define OTT_QK_LO 1
-#endif
-#ifndef OTT_STAGES
-#define OTT_STAGES 3  // 3 measured 2 % faster than 2 on config 4 (v7)
-#endif
-  static constexpr int kNG = G == 32 ? OTT_NG : 1;               // groups per loop iteration
-  static constexpr int kStages = G == 32 ? OTT_STAGES : 2;          // TMA pipeline depth per warp
+  static constexpr int kNG = 1;                        // groups per loop iteration (2 measured slower: spills)
+  static constexpr int kStages = G == 32 ? 3 : 2;      // TMA pipeline depth per warp (3 vs 2: -2 %, v7)
   float4 qt[8][32];  // q (fp32) per lane for the x_min bias, see mma_body
   // group records land here through a SWIZZLE_32B tensor map (16-byte chunk bit 4 ^= bit 7
   // of the offset): ldmatrix over 32-byte token rows is then bank-conflict free
@@ -694,7 +505,7 @@ __device__ void mma_body(const AttnArgs& a, const Counts& n, const CUtensorMap* 
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
 #pragma unroll
     for (int s = 0; s < kStages; ++s)
-      if (s < my_n && !OTT_NO_TMA)
+      if (s < my_n)
         load_record<G>(stage0 + s * kRec, tmap, unit_rec + g0 + warp + s * kAttnWarps, bar0 + 8 * s);
   }
   __syncthreads();
@@ -739,7 +550,7 @@ __device__ void mma_body(const AttnArgs& a, const Counts& n, const CUtensorMap* 
 #pragma unroll
       for (int w = 0; w < G / 32; ++w) mwords[j][w] = __ldg(&pmask[(size_t)gi * (G / 32) + w]);
       const int s = kk % kStages;
-      if (j < ng && !OTT_NO_TMA) mbar_wait(bar0 + 8 * s, (uint32_t)((kk / kStages) & 1));
+      if (j < ng) mbar_wait(bar0 + 8 * s, (uint32_t)((kk / kStages) & 1));
       rec[j] = &sm.stage[warp][s][0];
       rec_s[j] = stage0 + s * kRec;
     }
@@ -774,11 +585,6 @@ __device__ void mma_body(const AttnArgs& a, const Counts& n, const CUtensorMap* 
 #pragma unroll
       for (int mt = 0; mt < kMt; ++mt) ch[j][mt][0] = ch[j][mt][1] = ch[j][mt][2] = ch[j][mt][3] = 0.f;
     }
-#if !OTT_QK_LO
-    __half2 lo_acc[NG][2];
-#pragma unroll
-    for (int j = 0; j < NG; ++j) lo_acc[j][0] = lo_acc[j][1] = __float2half2_rn(0.f);
-#endif
 #pragma unroll
     for (int hw = 0; hw < 2; ++hw) {
 #pragma unroll
@@ -798,11 +604,7 @@ __device__ void mma_body(const AttnArgs& a, const Counts& n, const CUtensorMap* 
           const __half2 H = __hmul2(q16[hw][m], sh);
           const __half2 E = __hfma2(q16[hw][m], sh, __hneg2(H));
           bh[m] = h2_as_u32(H);
-#if OTT_QK_LO
           bl[m] = h2_as_u32(__hfma2(q16[hw][m], sl, E));
-#else
-          lo_acc[j][m & 1] = __hadd2(lo_acc[j][m & 1], __hfma2(q16[hw][m], sl, E));
-#endif
         }
         Shifted s0[kMt], s1[kMt];
 #pragma unroll
@@ -816,23 +618,13 @@ __device__ void mma_body(const AttnArgs& a, const Counts& n, const CUtensorMap* 
       const uint32_t a0 = kq<MM>(s0[mt], magic), a1 = kq<MM>(s1[mt], magic);         \
       const uint32_t a2 = kq<MM + 1>(s0[mt], magic), a3 = kq<MM + 1>(s1[mt], magic); \
       mma16816(ch[j][mt], a0, a1, a2, a3, bh[MM], bh[MM + 1]);                        \
-      if (OTT_QK_LO) mma16816(ch[j][mt], a0, a1, a2, a3, bl[MM], bl[MM + 1]);         \
+      mma16816(ch[j][mt], a0, a1, a2, a3, bl[MM], bl[MM + 1]);                        \
     }                                                                                 \
   }
         OTT_QK(0) OTT_QK(2) OTT_QK(4) OTT_QK(6)
 #undef OTT_QK
       }
     }
-#if !OTT_QK_LO
-    // Q.K^T used only the hi halves: ch = sum (q' - lo) (1 + c 2^(2P-10)). The bias takes
-    // back sum lo (the offset part, 4u/c times larger than the code part), leaving
-    // -sum lo c 2^(2P-10): the rounding error of q' step c in fp16, 2^-12 relative per term.
-#pragma unroll
-    for (int j = 0; j < NG; ++j) {
-      const float2 lf = __half22float2(__hadd2(lo_acc[j][0], lo_acc[j][1]));
-      bias_g[j] = fmaf(4.f, lf.x + lf.y, bias_g[j]);
-    }
-#endif
     float sc[NG][kMt][4];
 #pragma unroll
     for (int j = 0; j < NG; ++j) {
@@ -932,7 +724,7 @@ __device__ void mma_body(const AttnArgs& a, const Counts& n, const CUtensorMap* 
 #pragma unroll
       for (int j = 0; j < NG; ++j) {
         const int kk = k + j, ka = kk + kStages;
-        if (j < ng && ka < my_n && !OTT_NO_TMA) {
+        if (j < ng && ka < my_n) {
           asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
           load_record<G>(stage0 + (kk % kStages) * kRec, tmap, unit_rec + g0 + warp + ka * kAttnWarps,
                          bar0 + 8 * (kk % kStages));
@@ -993,239 +785,18 @@ __device__ void mma_body(const AttnArgs& a, const Counts& n, const CUtensorMap* 
   }
 }
 
-// ---- full-precision tiers (pool.entries + pending ring) on tensor cores.
-// 16-row tiles of fp16 K/V rows are staged with per-row TMA bulk copies into a
-// padded layout (272-byte row pitch: conflict-free ldmatrix); q (exact fp16) is
-// the B operand of Q K^T, P the B operand of V^T P. One stage per warp: these
-// tiers hold at most N + G + R - 1 rows per unit.
-struct FpSmem {
-  static constexpr int kRow = 272;
-  alignas(128) uint8_t kr[kAttnWarps][16][kRow];
-  alignas(128) uint8_t vr[kAttnWarps][16][kRow];
-  alignas(8) uint64_t bar[kAttnWarps];
-  float mm[kAttnWarps][8], ll[kAttnWarps][8];
-};
-
-// barrier over warps 0-3 only (the tcgen05 kernel's fifth warp does not take part)
-__device__ __forceinline__ void sync4() { asm volatile("bar.sync 1, 128;\n" ::: "memory"); }
-
-__device__ __forceinline__ void tma_row(uint32_t dst, const void* src, uint32_t bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 256, [%2];\n" ::"r"(dst),
-      "l"(src), "r"(bar)
-      : "memory");
-}
-
-template <int NR>
-__device__ void fp_body(const AttnArgs& a, const Counts& n, FpSmem& sm) {
-  constexpr int D = 128, kRow = FpSmem::kRow;
-  const ott_cache_t& c = a.c;
-  const int u = blockIdx.x, split = blockIdx.y;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = lane >> 2, tig = lane & 3;
-  const int N = c.capacity, cap = c.group_size + c.residual;
-  const int n_pool_t = (N + 15) / 16;
-  const int Tp = (int)(n.total_tokens - n.q_tokens);
-  const int n_tiles = n_pool_t + (Tp + 15) / 16;
-
-  // q (exact fp16) as the B fragments of Q K^T: head g, channels 16j + 2tig (+1), +8
-  uint32_t qb[8][2];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    if (g < NR) {
-      const uint32_t* qp = reinterpret_cast<const uint32_t*>(a.q + ((size_t)u * NR + g) * D + 16 * j + 2 * tig);
-      qb[j][0] = qp[0];
-      qb[j][1] = qp[4];
-    } else {
-      qb[j][0] = qb[j][1] = 0u;
-    }
-  }
-  // zero the staging rows once: rows a tile does not copy keep finite (stale or zero)
-  // data, so a zero softmax weight never meets a NaN
-  for (int i = lane; i < 16 * kRow / 16; i += 32) {
-    reinterpret_cast<uint4*>(&sm.kr[warp][0][0])[i] = make_uint4(0, 0, 0, 0);
-    reinterpret_cast<uint4*>(&sm.vr[warp][0][0])[i] = make_uint4(0, 0, 0, 0);
-  }
-  const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&sm.bar[warp]);
-  const uint32_t kr_s = (uint32_t)__cvta_generic_to_shared(&sm.kr[warp][0][0]);
-  const uint32_t vr_s = (uint32_t)__cvta_generic_to_shared(&sm.vr[warp][0][0]);
-  if (lane == 0) {
-    mbar_init(bar, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-  if (a.new_k) {  // fused ring write (cache.py:134-135): this CTA alone reads the pending tier
-    if (tid < 2 * D / 8) {
-      const size_t dst = ((size_t)u * cap + (size_t)((n.total_tokens - 1) % cap)) * D + (tid % (D / 8)) * 8;
-      const uint16_t* src = (tid < D / 8 ? a.new_k : a.new_v) + (size_t)u * D + (tid % (D / 8)) * 8;
-      *reinterpret_cast<uint4*>((tid < D / 8 ? c.pend_k : c.pend_v) + dst) = *reinterpret_cast<const uint4*>(src);
-      asm volatile("fence.proxy.async.global;\n" ::: "memory");  // visible to this CTA's TMA reads
-    }
-    sync4();
-  }
-  __syncwarp();
-
-  float o[8][4];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
-  float mrun[2] = {-INFINITY, -INFINITY}, lsum[2] = {0.f, 0.f};
-  // ldmatrix lane addressing (row, byte column) for K (non-trans) and V (trans)
-  const int k_row = (lane & 7) + ((lane >> 3) & 1) * 8, k_col = (lane >> 4) * 16;
-  const int v_row = (lane & 7) + ((lane >> 4) & 1) * 8, v_col = ((lane >> 3) & 1) * 16;
-  uint32_t phase = 0;
-
-  // the fp-tier CTAs of a unit (n_fsplits of them) interleave the 16-row tiles warp by warp
-  const int f = (int)blockIdx.y - a.n_qsplits;
-  for (int t = warp + kAttnWarps * f; t < n_tiles; t += kAttnWarps * a.n_fsplits) {
-    const bool is_pool = t < n_pool_t;
-    // row validity of this lane's two rows (g, g+8)
-    bool valid[2];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int r = g + 8 * h;
-      if (is_pool) {
-        const int slot = 16 * t + r;
-        valid[h] = slot < N && c.pool_pos[(size_t)u * N + slot] >= 0;
-      } else {
-        valid[h] = 16 * (t - n_pool_t) + r < Tp;
-      }
-    }
-    if (lane == 0) {
-      const int rows = is_pool ? min(16, N - 16 * t) : min(16, Tp - 16 * (t - n_pool_t));
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(rows * 512)
-                   : "memory");
-      // ring slot of the tile's first pending row, then consecutive slots (one modulo per tile)
-      int slot = is_pool ? 0 : (int)((n.q_tokens + 16 * (t - n_pool_t)) % cap);
-      for (int r = 0; r < rows; ++r) {
-        size_t off;
-        if (is_pool) {
-          off = ((size_t)u * N + 16 * t + r) * D;
-        } else {
-          off = ((size_t)u * cap + (size_t)slot) * D;
-          slot = slot + 1 == cap ? 0 : slot + 1;
-        }
-        tma_row(kr_s + r * kRow, (is_pool ? c.pool_k : c.pend_k) + off, bar);
-        tma_row(vr_s + r * kRow, (is_pool ? c.pool_v : c.pend_v) + off, bar);
-      }
-    }
-    mbar_wait(bar, phase);
-    phase ^= 1u;
-
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      uint32_t ak[4];
-      ldsm_x4(ak, kr_s + k_row * kRow + 32 * j + k_col);
-      mma16816(acc, ak[0], ak[1], ak[2], ak[3], qb[j][0], qb[j][1]);
-    }
-    float sc[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) sc[j] = valid[j >> 1] ? acc[j] * a.scale_log2 : -INFINITY;
-    float tmax[2];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      float tm = fmaxf(sc[h], sc[h + 2]);
-      tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 4));
-      tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 8));
-      tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 16));
-      tmax[h] = tm;
-    }
-    const bool need = tmax[0] > mrun[0] + kLazy || tmax[1] > mrun[1] + kLazy;
-    if (__any_sync(0xffffffffu, need)) {
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const float mnew = fmaxf(mrun[h], tmax[h]);
-        const float corr = mnew == -INFINITY ? 1.f : ex2(mrun[h] - mnew);
-        lsum[h] *= corr;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          o[j][h] *= corr;
-          o[j][h + 2] *= corr;
-        }
-        mrun[h] = mnew;
-      }
-    }
-    const float me0 = mrun[0] == -INFINITY ? 0.f : mrun[0];
-    const float me1 = mrun[1] == -INFINITY ? 0.f : mrun[1];
-    const float p00 = ex2(sc[0] - me0), p01 = ex2(sc[1] - me1);
-    const float p10 = ex2(sc[2] - me0), p11 = ex2(sc[3] - me1);
-    lsum[0] += p00 + p10;
-    lsum[1] += p01 + p11;
-    const uint32_t b0 = movm_t(pack_h2(p00, p01));
-    const uint32_t b1 = movm_t(pack_h2(p10, p11));
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      uint32_t av[4];
-      ldsm_x4_t(av, vr_s + v_row * kRow + 32 * j + v_col);
-      mma16816(o[j], av[0], av[1], av[2], av[3], b0, b1);
-    }
-    __syncwarp();
-    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-  }
-
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-#pragma unroll
-    for (int off = 4; off < 32; off <<= 1) lsum[h] += __shfl_xor_sync(0xffffffffu, lsum[h], off);
-  }
-  if (g == 0) {
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      sm.mm[warp][2 * tig + h] = mrun[h];
-      sm.ll[warp][2 * tig + h] = lsum[h];
-    }
-  }
-  sync4();
-  float* accw = reinterpret_cast<float*>(&sm.kr[warp][0][0]);  // [8 heads][128]
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      accw[(2 * tig + h) * D + 16 * j + g] = o[j][h];
-      accw[(2 * tig + h) * D + 16 * j + 8 + g] = o[j][h + 2];
-    }
-  }
-  sync4();
-  for (int i = tid; i < NR * D; i += kAttnThreads) {
-    const int r = i / D, col = i % D;
-    float M = -INFINITY;
-#pragma unroll
-    for (int w = 0; w < kAttnWarps; ++w) M = fmaxf(M, sm.mm[w][r]);
-    float Lsum = 0.f, A = 0.f;
-    if (M != -INFINITY) {
-#pragma unroll
-      for (int w = 0; w < kAttnWarps; ++w) {
-        if (sm.mm[w][r] == -INFINITY) continue;
-        const float f = exp2f(sm.mm[w][r] - M);
-        Lsum += sm.ll[w][r] * f;
-        A += reinterpret_cast<const float*>(&sm.kr[w][0][0])[r * D + col] * f;
-      }
-    }
-    float* base = a.ws + (((size_t)u * NR + r) * a.n_splits + split) * (D + 2);
-    base[2 + col] = A;
-    if (col == 0) {
-      base[0] = M;
-      base[1] = Lsum;
-    }
-  }
-}
 
 template <int NR, int G>
 __global__ void __launch_bounds__(kAttnThreads, OTT_MMA_MIN_BLOCKS)
     attend_mma_kernel(const __grid_constant__ AttnArgs a, const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(256) unsigned char smem_raw[];
   allow_dependents();
-#ifndef OTT_ABL_TIER  // timing ablation only (results wrong): 1 skip the fp-tier CTAs, 2 skip quantized CTAs
-#define OTT_ABL_TIER 0
-#endif
   if ((int)blockIdx.y >= a.n_qsplits) {  // full-precision tiers: pool + pending
-    if (OTT_ABL_TIER & 1) return;
     const Counts n = counts_of(a);
     if (blockIdx.x == 0 && blockIdx.y == a.n_qsplits && threadIdx.x == 0)  // token counts for the combine's guard
       reinterpret_cast<int64_t*>(a.ws + (size_t)a.c.n_units * NR * a.n_splits * 130)[0] = n.q_tokens;
     fp_body<NR>(a, n, *reinterpret_cast<FpSmem*>(smem_raw));
   } else {
-    if (OTT_ABL_TIER & 2) return;
     mma_body<NR, G>(a, counts_of(a), &tmap, *reinterpret_cast<MmaSmem<G>*>(smem_raw));
   }
 }
@@ -1902,462 +1473,6 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
   }
 }
 
-// ============================================================ tcgen05 path (d = 128, G = 32)
-// Q K^T on the 5th-generation tensor cores, P V on the warp-level path.
-//
-// CTA = 4 compute warps + 1 MMA-issuer warp. A 128-token chunk is 4 consecutive
-// groups, one per compute warp. Per chunk:
-//   * each compute warp (thread = token) unpacks its group's K codes into fp16
-//     (1 + c 2^(2P-10), one LOP3 per pair) and stores the 32 x 128 tile into its
-//     32 TMEM lanes (tcgen05.st, A operand of the MMA);
-//   * lane (head pair, code word) forms q' = q u step as an exact fp16 hi/lo split
-//     from the record's pair-ordered fp16 step halves: hi = q*sh, err = fma(q, sh,
-//     -hi) (exact), lo = fma(q, sl, err); rows 16w+h (hi) and 16w+8+h (lo) of the
-//     shared-memory B operand (K-major, canonical no-swizzle layout);
-//   * the issuer runs 8 tcgen05.mma kind::f16 (M=128 tokens, N=64, K=16) into a
-//     TMEM accumulator; only the diagonal 32x16 blocks are used;
-//   * while that runs the warps finish the previous chunk: tcgen05.ld of their
-//     logits (thread = token, 8 heads), lazily rescaled online softmax, P' = 4 p
-//     step to shared memory, and V^T P' with mma.sync m16n8k16 on the V codes
-//     (exact fp16 subnormals), accumulating in registers per warp.
-// logit = scale * (4 S + sum_c q_c e_c), e = x_min - 4 u step (record encoding).
-namespace tc5 {
-constexpr int kCW = 4;                       // compute warps
-constexpr int kThreads = 32 * (kCW + 1);     // + MMA issuer
-constexpr int kStages = 6;                   // record stages per compute warp (2 in use, 4 in flight)
-constexpr int kRec = 3328;                   // record bytes at d = 128, G = 32
-constexpr uint32_t kLBO = 128, kSBO = 16 * 128;  // B operand core-matrix strides (bytes)
-constexpr uint32_t kCols = 128;              // TMEM: A at 0 (f16 pairs), D at 64 (f32)
-constexpr uint32_t kIdesc = (1u << 4)        // D f32, A/B f16, both K-major
-                            | ((uint32_t)(64 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-}  // namespace tc5
-
-#ifndef OTT_TC5_MIN_BLOCKS
-#define OTT_TC5_MIN_BLOCKS 2
-#endif
-#ifndef OTT_TC5_ABL  // timing ablations only (results wrong): 1 no softmax/PV, 2 no q'/bias, 4 no K unpack
-#define OTT_TC5_ABL 0
-#endif
-
-struct Tc5Smem {
-  alignas(256) uint8_t stage[tc5::kCW][tc5::kStages][tc5::kRec];
-  alignas(128) uint8_t b1[64 * 128 * 2];       // q' hi/lo rows, K-major canonical
-  alignas(16) uint16_t pp[tc5::kCW][32][8];    // P' [token][head] per warp
-  alignas(16) float4 qt[8][32];                // q (fp32) per lane (head lane%8, channels 32(lane/8) + 4k..)
-  alignas(16) float bias[tc5::kCW][2][8];      // scale * sum_c q e per (warp, chunk parity, head)
-  float mm[tc5::kCW][8], ll[tc5::kCW][8];
-  alignas(8) uint64_t rbar[tc5::kCW][tc5::kStages];
-  alignas(8) uint64_t qk_ready, qk_done;
-  uint32_t tmem_base;
-};
-
-__device__ __forceinline__ uint64_t tc5_bdesc(uint32_t saddr) {
-  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)(tc5::kLBO >> 4) << 16) |
-         ((uint64_t)(tc5::kSBO >> 4) << 32) | (1ull << 46);
-}
-__device__ __forceinline__ void tmem_st64(uint32_t taddr, const uint32_t (&r)[64]) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x64.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
-      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,"
-      "%43,%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63,%64};\n" ::"r"(taddr),
-      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
-      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
-      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
-      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]), "r"(r[32]), "r"(r[33]), "r"(r[34]), "r"(r[35]), "r"(r[36]),
-      "r"(r[37]), "r"(r[38]), "r"(r[39]), "r"(r[40]), "r"(r[41]), "r"(r[42]), "r"(r[43]), "r"(r[44]), "r"(r[45]),
-      "r"(r[46]), "r"(r[47]), "r"(r[48]), "r"(r[49]), "r"(r[50]), "r"(r[51]), "r"(r[52]), "r"(r[53]), "r"(r[54]),
-      "r"(r[55]), "r"(r[56]), "r"(r[57]), "r"(r[58]), "r"(r[59]), "r"(r[60]), "r"(r[61]), "r"(r[62]), "r"(r[63])
-      : "memory");
-}
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr)
-      : "memory");
-  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
-}
-template <int I>
-__device__ __forceinline__ float pick4(const float (&v)[8], int tig) {  // v[2 tig + I]
-  return tig == 0 ? v[I] : (tig == 1 ? v[2 + I] : (tig == 2 ? v[4 + I] : v[6 + I]));
-}
-
-// K side of chunk j for compute warp w: A tile into TMEM, q' rows into B, bias.
-template <int NR>
-__device__ __forceinline__ void tc5_kstage(Tc5Smem& sm, int w, int lane, const uint8_t* rec, uint32_t a_lane,
-                                           uint8_t* b1, const __half2 (&q16)[2][8], uint32_t magic, float scale,
-                                           int slot) {
-  const RecordLayout L(128, 32);
-  if (!(OTT_TC5_ABL & 4)) {  // A row = token `lane`: 8 code words -> 64 fp16 pairs
-    const uint4 c0 = *reinterpret_cast<const uint4*>(rec + swz(L.k_codes() + lane * 32));
-    const uint4 c1 = *reinterpret_cast<const uint4*>(rec + swz(L.k_codes() + lane * 32 + 16));
-    const uint32_t wd[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
-    uint32_t r[64];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const Shifted sft = shifted(wd[j]);
-      r[8 * j + 0] = kq<0>(sft, magic);
-      r[8 * j + 1] = kq<1>(sft, magic);
-      r[8 * j + 2] = kq<2>(sft, magic);
-      r[8 * j + 3] = kq<3>(sft, magic);
-      r[8 * j + 4] = kq<4>(sft, magic);
-      r[8 * j + 5] = kq<5>(sft, magic);
-      r[8 * j + 6] = kq<6>(sft, magic);
-      r[8 * j + 7] = kq<7>(sft, magic);
-    }
-    tmem_st64(a_lane, r);
-  }
-  // q' rows: lane = (head h = lane % 8, word pair e4 = lane / 8: code words 2e4, 2e4+1 =
-  // channels 32e4 .. 32e4+31). Lanes 8k..8k+7 write rows 0..7 of one core matrix:
-  // 128 contiguous bytes per store phase, bank-conflict free.
-  const int h = lane & 7, e4 = lane >> 3;
-  float part = 0.f;
-  if (h < NR && !(OTT_TC5_ABL & 2)) {
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};  // sum_c q_c e_c, 4 independent chains
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const float4 ev = *reinterpret_cast<const float4*>(rec + swz(L.k_e() + 128 * e4 + 16 * k));
-      const float4 qv = sm.qt[k][lane];
-      acc[0] = fmaf(qv.x, ev.x, acc[0]);
-      acc[1] = fmaf(qv.y, ev.y, acc[1]);
-      acc[2] = fmaf(qv.z, ev.z, acc[2]);
-      acc[3] = fmaf(qv.w, ev.w, acc[3]);
-    }
-    part = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-#pragma unroll
-    for (int w2 = 0; w2 < 2; ++w2) {
-      const int wd = 2 * e4 + w2;  // code word: channels 16 wd .. 16 wd + 15
-      const uint4 h0 = *reinterpret_cast<const uint4*>(rec + swz(L.k_sh() + 32 * wd));
-      const uint4 h1 = *reinterpret_cast<const uint4*>(rec + swz(L.k_sh() + 32 * wd + 16));
-      const uint4 l0 = *reinterpret_cast<const uint4*>(rec + swz(L.k_sl() + 32 * wd));
-      const uint4 l1 = *reinterpret_cast<const uint4*>(rec + swz(L.k_sl() + 32 * wd + 16));
-      const uint32_t shw[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
-      const uint32_t slw[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
-      uint32_t hi[8], lo[8];
-#pragma unroll
-      for (int m = 0; m < 8; ++m) {
-        const __half2 sh = *reinterpret_cast<const __half2*>(&shw[m]);
-        const __half2 sl = *reinterpret_cast<const __half2*>(&slw[m]);
-        const __half2 H = __hmul2(q16[w2][m], sh);
-        const __half2 E = __hfma2(q16[w2][m], sh, __hneg2(H));  // exact rounding error of H
-        hi[m] = h2_as_u32(H);
-        lo[m] = h2_as_u32(__hfma2(q16[w2][m], sl, E));
-      }
-      uint8_t* bh = b1 + (2 * w) * tc5::kSBO + (2 * wd) * tc5::kLBO + h * 16;
-      uint8_t* bl = bh + tc5::kSBO;
-      *reinterpret_cast<uint4*>(bh) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-      *reinterpret_cast<uint4*>(bh + tc5::kLBO) = make_uint4(hi[4], hi[5], hi[6], hi[7]);
-      *reinterpret_cast<uint4*>(bl) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-      *reinterpret_cast<uint4*>(bl + tc5::kLBO) = make_uint4(lo[4], lo[5], lo[6], lo[7]);
-    }
-  }
-  // reduce over the 4 word pairs (all lanes take part; idle heads carry 0)
-  part += __shfl_xor_sync(0xffffffffu, part, 8);
-  part += __shfl_xor_sync(0xffffffffu, part, 16);
-  if (e4 == 0 && h < NR) sm.bias[w][slot][h] = part * scale;
-}
-
-template <int NR>
-__device__ void tc5_body(const AttnArgs& a, const Counts& n, const CUtensorMap* tmap, Tc5Smem& sm) {
-  constexpr int D = 128, G = 32, kS = tc5::kStages;
-  const RecordLayout L(D, G);
-  const ott_cache_t& c = a.c;
-  const int u = blockIdx.x, split = blockIdx.y;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = lane >> 2, tig = lane & 3;
-  const int n_groups = (int)(n.q_tokens / G);
-  const int per = (((n_groups + a.n_qsplits - 1) / a.n_qsplits) + 3) & ~3;  // whole chunks per split
-  const int g0 = min(n_groups, split * per);
-  const int g1 = min(n_groups, g0 + per);
-  const int n_chunks = (g1 - g0 + 3) / 4;
-  const int64_t unit_rec = (int64_t)u * c.max_groups;
-
-  const uint32_t qk_ready = (uint32_t)__cvta_generic_to_shared(&sm.qk_ready);
-  const uint32_t qk_done = (uint32_t)__cvta_generic_to_shared(&sm.qk_done);
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
-                     (uint32_t)__cvta_generic_to_shared(&sm.tmem_base)),
-                 "n"(tc5::kCols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
-  }
-  if (tid == 0) {
-    for (int w = 0; w < tc5::kCW; ++w)
-      for (int s = 0; s < kS; ++s) mbar_init((uint32_t)__cvta_generic_to_shared(&sm.rbar[w][s]), 1);
-    mbar_init(qk_ready, tc5::kCW);
-    mbar_init(qk_done, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  for (int i = tid; i < 8 * 32; i += tc5::kThreads) {  // q table: [k][lane] = q[lane % 8][32 (lane / 8) + 4k ..]
-    const int k = i >> 5, ln = i & 31, h = ln & 7;
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (h < NR) {
-      const uint2 raw = __ldg(reinterpret_cast<const uint2*>(a.q + ((size_t)u * NR + h) * D + 32 * (ln >> 3) + 4 * k));
-      const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&raw.x));
-      const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&raw.y));
-      v = make_float4(f0.x, f0.y, f1.x, f1.y);
-    }
-    sm.qt[k][ln] = v;
-  }
-  for (int i = tid; i < 64 * 128 * 2 / 16; i += tc5::kThreads)
-    reinterpret_cast<uint4*>(sm.b1)[i] = make_uint4(0u, 0u, 0u, 0u);
-  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-  const uint32_t tmem = sm.tmem_base;
-  const uint32_t a_tm = tmem, d_tm = tmem + 64;
-
-  float o[8][4];
-#pragma unroll
-  for (int cm = 0; cm < 8; ++cm) o[cm][0] = o[cm][1] = o[cm][2] = o[cm][3] = 0.f;
-  float m[8], l[8], vb[8];
-#pragma unroll
-  for (int h = 0; h < 8; ++h) {
-    m[h] = -INFINITY;
-    l[h] = 0.f;
-    vb[h] = 0.f;
-  }
-
-  if (warp == tc5::kCW) {
-    // ---------------- MMA issuer
-    const uint32_t b_s = (uint32_t)__cvta_generic_to_shared(sm.b1);
-    const uint32_t a_b = a_tm, d_b = d_tm;
-    for (int i = 0; i < n_chunks; ++i) {
-      mbar_wait(qk_ready, (uint32_t)(i & 1));
-      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-      if (lane == 0) {
-#pragma unroll
-        for (int s = 0; s < 8; ++s) {
-          const uint64_t bd = tc5_bdesc(b_s + s * 2 * tc5::kLBO);
-          asm volatile(
-              "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-              "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_b),
-              "r"(a_b + 8 * s), "l"(bd), "r"(tc5::kIdesc), "r"(s)
-              : "memory");
-        }
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(qk_done)
-                     : "memory");
-      }
-      __syncwarp();
-    }
-  } else {
-    // ---------------- compute warps
-    const int w = warp;
-    const uint32_t rbar0 = (uint32_t)__cvta_generic_to_shared(&sm.rbar[w][0]);
-    const uint32_t stage0 = (uint32_t)__cvta_generic_to_shared(&sm.stage[w][0][0]);
-    auto group_of = [&](int j) { return g0 + 4 * j + w; };
-    if (lane == 0) {
-#pragma unroll
-      for (int s = 0; s < kS; ++s)
-        if (s < n_chunks && group_of(s) < g1)
-          load_record<G>(stage0 + s * tc5::kRec, tmap, unit_rec + group_of(s), rbar0 + 8 * s);
-    }
-    const uint32_t magic = a.k_magic;
-    const float scale = a.scale_log2, scale4 = 4.f * a.scale_log2;
-    // q * u(m) as fp16 pairs (channels 16e+m, 16e+m+8) for heads 2hp, 2hp+1
-    // q * u(m) as fp16 pairs (channels 16wd+m, 16wd+m+8) of head lane % 8, words wd = 2e4 + w2
-    __half2 q16[2][8];
-#pragma unroll
-    for (int w2 = 0; w2 < 2; ++w2)
-#pragma unroll
-      for (int m = 0; m < 8; ++m) {
-        // channel 32e4 + 16w2 + m lives in table entry k = 4w2 + m/4, component m%4
-        const float4 qa = sm.qt[4 * w2 + m / 4][lane];
-        const float4 qb = sm.qt[4 * w2 + 2 + m / 4][lane];
-        const float lo = (m % 4 == 0 ? qa.x : m % 4 == 1 ? qa.y : m % 4 == 2 ? qa.z : qa.w) * kpair_u(m);
-        const float hi = (m % 4 == 0 ? qb.x : m % 4 == 1 ? qb.y : m % 4 == 2 ? qb.z : qb.w) * kpair_u(m);
-        q16[w2][m] = __floats2half2_rn(lo, hi);
-      }
-    const uint32_t a_lane = a_tm + ((uint32_t)(32 * w) << 16);
-    const uint32_t d_lane = d_tm + ((uint32_t)(32 * w) << 16) + 16 * w;
-    const uint32_t pp_s = (uint32_t)__cvta_generic_to_shared(&sm.pp[w][0][0]);
-    const uint32_t lm_off = (uint32_t)(((lane & 7) + ((lane >> 3) & 1) * 8) * 32 + (lane >> 4) * 16);
-    const uint32_t* pmask = c.pool_mask + (size_t)u * mask_words_per_unit(c);
-
-    auto kstage = [&](int j) {
-      const int gj = group_of(j);
-      if (gj < g1) {
-        mbar_wait(rbar0 + 8 * (j % kS), (uint32_t)((j / kS) & 1));
-        tc5_kstage<NR>(sm, w, lane, &sm.stage[w][j % kS][0], a_lane, sm.b1, q16, magic, scale, j & 1);
-      }
-      asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(qk_ready);
-    };
-    if (n_chunks > 0) kstage(0);
-
-    for (int i = 0; i < n_chunks; ++i) {
-      // ---- logits of chunk i (this warp's 32 tokens x 16 columns: hi heads, lo heads)
-      mbar_wait(qk_done, (uint32_t)(i & 1));
-      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-      uint32_t sv[16];
-      tmem_ld16(d_lane, sv);
-      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-      // ---- K side of chunk i + 1 (the MMA of chunk i is complete and its logits are
-      // read); the MMA of chunk i + 1 then runs under this chunk's softmax and P V
-      if (i + 1 < n_chunks) kstage(i + 1);
-
-      const int gi = group_of(i);
-      if (gi < g1 && !(OTT_TC5_ABL & 1)) {
-        const int st = i % kS;
-        const uint8_t* rec = &sm.stage[w][st][0];
-        const uint32_t rec_s = stage0 + st * tc5::kRec;
-        const float4 b0 = *reinterpret_cast<const float4*>(&sm.bias[w][i & 1][0]);
-        const float4 b1 = *reinterpret_cast<const float4*>(&sm.bias[w][i & 1][4]);
-        const float bias[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-        const bool pooled = (__ldg(&pmask[gi]) >> lane) & 1u;
-        float s[8];
-#pragma unroll
-        for (int h = 0; h < 8; ++h)
-          s[h] = (h < NR && !pooled)
-                     ? fmaf(__uint_as_float(sv[h]), scale4, fmaf(__uint_as_float(sv[8 + h]), scale4, bias[h]))
-                     : -INFINITY;
-        // lazily rescaled online softmax: the warp's running max moves only when a
-        // logit exceeds it by kLazy (p <= 2^kLazy keeps P' = 4 p step in fp16 range)
-        float dmax = -INFINITY;
-#pragma unroll
-        for (int h = 0; h < NR; ++h) dmax = fmaxf(dmax, s[h] - m[h]);
-        if (__any_sync(0xffffffffu, dmax > kLazy || m[0] == -INFINITY)) {
-          float corr[8];
-#pragma unroll
-          for (int h = 0; h < 8; ++h) {
-            corr[h] = 1.f;
-            if (h < NR) {
-              const float t = warp_max(s[h]);
-              const float mnew = fmaxf(m[h], t);
-              corr[h] = mnew == -INFINITY ? 1.f : ex2(m[h] - mnew);
-              m[h] = mnew;
-              l[h] *= corr[h];
-              vb[h] *= corr[h];
-            }
-          }
-          const float c0 = pick4<0>(corr, tig), c1 = pick4<1>(corr, tig);
-#pragma unroll
-          for (int cm = 0; cm < 8; ++cm) {
-            o[cm][0] *= c0;
-            o[cm][1] *= c1;
-            o[cm][2] *= c0;
-            o[cm][3] *= c1;
-          }
-        }
-        float me[8];
-#pragma unroll
-        for (int h = 0; h < 8; ++h) me[h] = m[h] == -INFINITY ? 0.f : m[h];
-        const float vs = *reinterpret_cast<const float*>(rec + swz(L.v_step() + 4 * lane));
-        const float vx = *reinterpret_cast<const float*>(rec + swz(L.v_xmin() + 4 * lane));
-        const float f = 4.f * vs;
-        float pq[8];
-#pragma unroll
-        for (int h = 0; h < 8; ++h) {
-          pq[h] = 0.f;
-          if (h < NR) {
-            const float p = ex2(s[h] - me[h]);
-            l[h] += p;
-            vb[h] = fmaf(p, vx, vb[h]);
-            pq[h] = p * f;
-          }
-        }
-        *reinterpret_cast<uint4*>(&sm.pp[w][lane][0]) =
-            make_uint4(pack_h2(pq[0], pq[1]), pack_h2(pq[2], pq[3]), pack_h2(pq[4], pq[5]), pack_h2(pq[6], pq[7]));
-        __syncwarp();
-        uint32_t bq[4];
-        ldsm_x4_t(bq, pp_s + lane * 16);
-#pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
-          const uint32_t bb0 = bq[2 * mt], bb1 = bq[2 * mt + 1];
-          uint32_t vr[4];
-          ldsm_x4_t(vr, rec_s + swz(L.v_codes() + mt * 16 * 32 + lm_off));
-          const Shifted v0 = shifted(vr[0]), v1 = shifted(vr[1]), v2 = shifted(vr[2]), v3 = shifted(vr[3]);
-#define OTT_PV5(CM) mma16816(o[CM], vq<CM>(v0), vq<CM>(v2), vq<CM>(v1), vq<CM>(v3), bb0, bb1);
-          OTT_PV5(0) OTT_PV5(1) OTT_PV5(2) OTT_PV5(3) OTT_PV5(4) OTT_PV5(5) OTT_PV5(6) OTT_PV5(7)
-#undef OTT_PV5
-        }
-      }
-      // ---- release this stage: prefetch the record of chunk i + kStages
-      __syncwarp();
-      if (lane == 0 && i + kS < n_chunks && group_of(i + kS) < g1) {
-        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-        load_record<G>(stage0 + (i % kS) * tc5::kRec, tmap, unit_rec + group_of(i + kS), rbar0 + 8 * (i % kS));
-      }
-    }
-
-    // ---- per-warp totals (thread = token: sum l, vb over the lanes)
-#pragma unroll
-    for (int h = 0; h < 8; ++h) {
-      l[h] = warp_sum(l[h]);
-      vb[h] = warp_sum(vb[h]);
-    }
-    if (lane == 0) {
-#pragma unroll
-      for (int h = 0; h < 8; ++h) {
-        sm.mm[w][h] = m[h];
-        sm.ll[w][h] = l[h];
-      }
-    }
-  }
-  __syncthreads();  // every warp is past its loop: stage memory is free
-  if (warp < tc5::kCW) {
-    float* accw = reinterpret_cast<float*>(&sm.stage[warp][0][0]);  // [8 heads][128] natural channel order
-    const float vb0 = pick4<0>(vb, tig), vb1 = pick4<1>(vb, tig);
-#pragma unroll
-    for (int cm = 0; cm < 8; ++cm) {
-      const float f = pair_pos(cm) == 2 ? 262144.f : (pair_pos(cm) == 3 ? 65536.f : 16384.f);  // 2^(22-2P)
-      accw[(2 * tig) * D + 8 * g + cm] = fmaf(o[cm][0], f, vb0);
-      accw[(2 * tig + 1) * D + 8 * g + cm] = fmaf(o[cm][1], f, vb1);
-      accw[(2 * tig) * D + 64 + 8 * g + cm] = fmaf(o[cm][2], f, vb0);
-      accw[(2 * tig + 1) * D + 64 + 8 * g + cm] = fmaf(o[cm][3], f, vb1);
-    }
-  }
-  __syncthreads();
-  for (int i = tid; i < NR * D; i += tc5::kThreads) {
-    const int r = i / D, col = i % D;
-    float M = -INFINITY;
-#pragma unroll
-    for (int w = 0; w < tc5::kCW; ++w) M = fmaxf(M, sm.mm[w][r]);
-    float Lsum = 0.f, A = 0.f;
-    if (M != -INFINITY) {
-#pragma unroll
-      for (int w = 0; w < tc5::kCW; ++w) {
-        if (sm.mm[w][r] == -INFINITY) continue;
-        const float f = exp2f(sm.mm[w][r] - M);
-        Lsum += sm.ll[w][r] * f;
-        A += reinterpret_cast<const float*>(&sm.stage[w][0][0])[r * D + col] * f;
-      }
-    }
-    float* base = a.ws + (((size_t)u * NR + r) * a.n_splits + split) * (D + 2);
-    base[2 + col] = A;
-    if (col == 0) {
-      base[0] = M;
-      base[1] = Lsum;
-    }
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-  __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(tc5::kCols));
-}
-
-template <int NR>
-__global__ void __launch_bounds__(tc5::kThreads, OTT_TC5_MIN_BLOCKS)
-    attend_tc5_kernel(const __grid_constant__ AttnArgs a, const __grid_constant__ CUtensorMap tmap) {
-  extern __shared__ __align__(256) unsigned char smem_raw[];
-  allow_dependents();
-  if ((int)blockIdx.y >= a.n_qsplits) {  // full-precision tiers on warps 0-3
-    if (threadIdx.x >= 128) return;
-    const Counts n = counts_of(a);
-    if (blockIdx.x == 0 && blockIdx.y == a.n_qsplits && threadIdx.x == 0)  // token counts for the combine's guard
-      reinterpret_cast<int64_t*>(a.ws + (size_t)a.c.n_units * NR * a.n_splits * 130)[0] = n.q_tokens;
-    fp_body<NR>(a, n, *reinterpret_cast<FpSmem*>(smem_raw));
-  } else {
-    tc5_body<NR>(a, counts_of(a), &tmap, *reinterpret_cast<Tc5Smem*>(smem_raw));
-  }
-}
-
 // ============================================================ combine + debug logits
 // Split combine: one warp per (unit, head) row, 8 rows per 256-thread block; lane
 // handles columns 2*lane, 2*lane+1 (+64, +65 at D = 128) with float2 loads.
@@ -2584,6 +1699,10 @@ static cudaError_t launch_combine(const AttnArgs& a, int NR, cudaStream_t st, bo
                             a.c.head_dim, gd, tc_path ? 1 : 0);
 }
 
+cudaError_t launch_combine_tc128(const AttnArgs& a, int NR, cudaStream_t st) {
+  return launch_combine<128>(a, NR, st, true);
+}
+
 template <int DT>  // 0: runtime head_dim (debug path; k lives in local memory then)
 __global__ void logits_kernel(ott_cache_t c, const uint16_t* __restrict__ q, float* __restrict__ logits, int NR,
                               int64_t q_tokens, int64_t total, float inv_sqrt_d) {
@@ -2652,7 +1771,7 @@ static cudaError_t launch_generic_t(const AttnArgs& a, cudaStream_t st) {
 // Tensor map over all block records of the cache: 2-D uint8 view [rows of 32 B],
 // SWIZZLE_32B, one (or two) boxes per record. Encoded per launch (host only).
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
-static cudaError_t record_tensor_map(const ott_cache_t& c, int box_rows, int rec_rows, CUtensorMap* map) {
+cudaError_t record_tensor_map(const ott_cache_t& c, int box_rows, int rec_rows, CUtensorMap* map) {
   if (!g_encode) {
     cudaDriverEntryPointQueryResult q;
     void* fn = nullptr;
@@ -2746,28 +1865,13 @@ static cudaError_t launch_mma_t(const AttnArgs& a, cudaStream_t st) {
   return launch_combine<128>(a, NR, st, true);
 }
 
-template <int NR>
-static cudaError_t launch_tc5_t(const AttnArgs& a, cudaStream_t st) {
-  CUtensorMap tmap;
-  cudaError_t te = record_tensor_map(a.c, RecTma<32>::kBoxRows, RecTma<32>::kRows, &tmap);
-  if (te != cudaSuccess) return te;
-  const size_t smem = sizeof(Tc5Smem) > sizeof(FpSmem) ? sizeof(Tc5Smem) : sizeof(FpSmem);
-  cudaError_t e = cudaFuncSetAttribute(attend_tc5_kernel<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  attend_tc5_kernel<NR><<<dim3(a.c.n_units, a.n_splits), tc5::kThreads, smem, st>>>(a, tmap);
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  return launch_combine<128>(a, NR, st, true);
-}
-
-// Attention kernel for (d = 128, G = 32): the mma.sync kernel (default, faster as
-// measured) or the tcgen05 Q K^T kernel (OTT_ATTN_KERNEL=tc5); read
-// once per process.
-static bool use_tc5() {
+// 2-bit, G = 32: the mma.sync K2 (default) or the tcgen05 Q K^T variant (ott_attend_tc.cu,
+// OTT_ATTN_KERNEL=tcq; slower as measured)
+static bool use_tcq() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("OTT_ATTN_KERNEL");
-    v = (e && strcmp(e, "tc5") == 0) ? 1 : 0;
+    v = (e && strcmp(e, "tcq") == 0) ? 1 : 0;
   }
   return v == 1;
 }
@@ -2870,13 +1974,7 @@ cudaError_t launch_attend(const ott_cache_t& c, const uint16_t* q, uint16_t* out
 #undef OTT_BCASE
     return cudaErrorInvalidValue;
   }
-  if (mma_eligible(c) && G == 32 && use_tc5()) {
-    if (n_rep == 1) return launch_tc5_t<1>(a, st);
-    if (n_rep == 2) return launch_tc5_t<2>(a, st);
-    if (n_rep == 4) return launch_tc5_t<4>(a, st);
-    if (n_rep == 8) return launch_tc5_t<8>(a, st);
-    return cudaErrorInvalidValue;
-  }
+  if (mma_eligible(c) && G == 32 && use_tcq()) return launch_tcq(a, n_rep, st);
   if (mma_eligible(c)) {
 #define OTT_MCASE(NRv, Gv) \
   if (n_rep == NRv && G == Gv) return launch_mma_t<NRv, Gv>(a, st);
