@@ -17,6 +17,9 @@
  *                       (reconstructed_kv attention.py:62-76,
  *                       attend_full_precision attention.py:35-59)
  *   ott_logits       <- AttentionResult.scores         attention.py:26-32 (debug)
+ *   ott_attend_exact <- attend_full_precision          attention.py:35-59
+ *   ott_pool_rank    <- OutlierPool.update (the competition)  outlier.py:84-117
+ *   ott_score_rows   <- score_tokens / OutlierEntry.from_rows  outlier.py:37-49
  *   ott_append_attend <- append + attend_mixed of one decode step (ring write fused)
  *   ott_decode_step  <- append + attend_mixed of one decode step, token counts in device
  *                       memory (CUDA-graph capturable)    cache.py:124-139, attention.py:79-92
@@ -58,14 +61,23 @@ typedef enum {
  *   fp16 k_sh[d], k_sl[d]           per-channel K step = sh + sl, in pair order
  *                                   (index 16*(c/16) + 2*(c%8) + (c%16)/8 when
  *                                   d % 16 == 0, else c)
- *   float32 k_e[d]                  per-channel K x_min - 4*u(c)*step, u(c) = 4^(4-P(c%8)),
- *                                   P = {3,4,2,3,4,2,3,4} (fp16 mantissa position of the
- *                                   code pair in the decode kernels)
- *   (stored width 4, d % 8 == 0: sh/sl in 4-bit pair order (8w+k, 8w+k+4), e = x_min - 64 step;
- *   stored width 8, d % 8 == 0: sh/sl in channel order, e = x_min - 1024 step; other widths: the
- *   k_sh/k_sl bytes hold float32 step[d] and k_e float32 x_min[d], channel order: 1-bit steps
- *   can exceed the fp16 range)
- *   float32 v_step[G], v_xmin[G]    per-token V params
+ *   stored width 2:
+ *     float32 v_step[G], v_xmin[G]  per-token V params
+ *     fp16 k_ehi[d], k_elo[d]       per-channel K term e = x_min - 4*u(c)*step, u(c) =
+ *                                   4^(4-P(c%8)), P = {3,4,2,3,4,2,3,4} (fp16 mantissa position
+ *                                   of the code pair in the decode kernels), stored as
+ *                                   t = e / (8 u(c)) split into hi = fp16(t), lo = fp16(t - hi)
+ *                                   (|t| < 65504 for any fp16 input),
+ *                                   pair order; last in the record, so the decode kernels stream
+ *                                   the record head and fetch the e fields of 8 groups at once
+ *   other widths:
+ *     float32 k_e[d]                stored width 4, d % 8 == 0: sh/sl in 4-bit pair order
+ *                                   (8w+k, 8w+k+4), e = x_min - 64 step; stored width 8,
+ *                                   d % 8 == 0: sh/sl in channel order, e = x_min - 1024 step;
+ *                                   otherwise the k_sh/k_sl bytes hold float32 step[d] and k_e
+ *                                   float32 x_min[d], channel order (1-bit steps can exceed the
+ *                                   fp16 range)
+ *     float32 v_step[G], v_xmin[G]  per-token V params
  *   (record size rounded up to 16 bytes)
  * The exact float64 QuantParams are kept in params64 when it is allocated. 
  * Per-token bitmasks hold one bit per absolute position (32 per word). */
@@ -163,6 +175,24 @@ int ott_decode_step(const ott_cache_t* c, const uint16_t* k, const uint16_t* v, 
 
 int ott_logits(const ott_cache_t* c, const uint16_t* q, float* logits, int32_t n_rep, int64_t quantized_tokens,
                int64_t total_tokens, void* stream);
+
+/* attend_full_precision (attention.py:35-59), the reference's exact single-query attention,
+ * for n_q independent problems in float32 device buffers: q [n_q][d], keys/values
+ * [n_q][n][d]; out [n_q][d], weights [n_q][n], scores [n_q][n] (scores = (K q) / f32(sqrt(d))
+ * in float32, softmax in float64 with max subtraction as tensor.py:45-57, out = weights V in
+ * float32). n >= 1 (attention.py:48-49). */
+int ott_attend_exact(const float* q, const float* keys, const float* values, int32_t n, int32_t d, int32_t n_q,
+                     float* out, float* weights, float* scores, void* stream);
+
+/* The competition of OutlierPool.update (outlier.py:84-117): rank of each of the n items
+ * (pool entries then candidates) in ascending (score, position) order, positions distinct
+ * (the caller rejects duplicates, outlier.py:96-100). Winners are the ranks < capacity, in
+ * rank order. scores f64 [n], positions i64 [n], rank i32 [n], device memory. */
+int ott_pool_rank(const double* scores, const int64_t* positions, int32_t n, int32_t* rank, void* stream);
+
+/* score_tokens / OutlierEntry.from_rows (outlier.py:37-49, row_l1_norm tensor.py:38-42):
+ * scores[r] = sum_j |rows[r][j]| in float64, rows float32 [n][d], device memory. */
+int ott_score_rows(const float* rows, int32_t n, int32_t d, double* scores, void* stream);
 
 /* Number of SMs of the current device (0 if unknown) and library version. */
 int ott_num_sms(void);

@@ -13,7 +13,8 @@ from .views import AttentionResult, GroupAxis, OutlierEntry, OutlierPoolView, Qu
 
 __all__ = [
     "AttentionResult", "ContractViolation", "EngineConfig", "GroupAxis", "MemoryBreakdown", "NativeError",
-    "OTTCache", "OutlierEntry", "OutlierPoolView", "QuantParams", "QuantizedBlock", "TieredCache", "attend_mixed",
+    "OTTCache", "OutlierEntry", "OutlierPool", "OutlierPoolView", "QuantParams", "QuantizedBlock", "TieredCache",
+    "attend_full_precision", "attend_mixed", "score_tokens",
 ]
 
 
@@ -22,4 +23,8 @@ def __getattr__(name):  # torch-dependent pieces load lazily
         from . import cache
 
         return getattr(cache, name)
+    if name in ("OutlierPool", "attend_full_precision", "score_tokens"):
+        from . import pool
+
+        return getattr(pool, name)
     raise AttributeError(name)

@@ -72,6 +72,9 @@ def lib() -> ctypes.CDLL:
         L.ott_model_rmsnorm.argtypes = [_vp, _vp, _vp, _i32, _i32, ctypes.c_float, _vp]
         L.ott_model_rope_qkv.argtypes = [_vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp]
         L.ott_model_silu_mul.argtypes = [_vp, _vp, _i32, _i32, _vp]
+        L.ott_attend_exact.argtypes = [_vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp]
+        L.ott_pool_rank.argtypes = [_vp, _vp, _i32, _vp, _vp]
+        L.ott_score_rows.argtypes = [_vp, _i32, _i32, _vp, _vp]
         L.ott_num_sms.argtypes = []
         L.ott_version.restype = ctypes.c_char_p
         L.ott_last_error.restype = ctypes.c_char_p
@@ -85,7 +88,8 @@ def lib() -> ctypes.CDLL:
 
 EXPORTED = ("ott_record_bytes", "ott_ring_write", "ott_flush", "ott_pick_splits", "ott_attend_workspace_floats",
             "ott_attend", "ott_logits", "ott_append_attend", "ott_decode_step", "ott_num_sms", "ott_version", "ott_last_error",
-            "ott_cache_struct_bytes", "ott_model_rmsnorm", "ott_model_rope_qkv", "ott_model_silu_mul")
+            "ott_cache_struct_bytes", "ott_model_rmsnorm", "ott_model_rope_qkv", "ott_model_silu_mul",
+            "ott_attend_exact", "ott_pool_rank", "ott_score_rows")
 
 
 def check(status: int) -> None:

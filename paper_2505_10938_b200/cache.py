@@ -432,14 +432,24 @@ class UnitView:
         # below are reconstructions, the exact values come from params64
         self.k_sh16 = rec[:, 2 * code_b: 2 * code_b + 2 * d].copy().view(np.float16)
         self.k_sl16 = rec[:, 2 * code_b + 2 * d: 2 * code_b + 4 * d].copy().view(np.float16)
-        self.k_e32 = rec[:, 2 * code_b + 4 * d: 2 * code_b + 8 * d].copy().view(np.float32)
-        vst = rec[:, 2 * code_b + 8 * d: 2 * code_b + 8 * d + 4 * G].copy().view(np.float32)
-        vmn = rec[:, 2 * code_b + 8 * d + 4 * G: 2 * code_b + 8 * d + 8 * G].copy().view(np.float32)
+        if pb == 2:  # ... sl | V step | V x_min | e hi | e lo (e last, ott_common.cuh RecordLayout)
+            vo = 2 * code_b + 4 * d
+            eo = vo + 8 * G
+            self.k_ehi16 = rec[:, eo: eo + 2 * d].copy().view(np.float16)
+            self.k_elo16 = rec[:, eo + 2 * d: eo + 4 * d].copy().view(np.float16)
+        else:
+            vo = 2 * code_b + 8 * d
+            self.k_e32 = rec[:, 2 * code_b + 4 * d: 2 * code_b + 8 * d].copy().view(np.float32)
+        vst = rec[:, vo: vo + 4 * G].copy().view(np.float32)
+        vmn = rec[:, vo + 4 * G: vo + 8 * G].copy().view(np.float32)
         kshift = 1 if (cfg.bits == 1 and pb == 2) else 0  # 1-bit K: doubled codes, halved step
-        if pb == 2:  # tensor-core encoding: step = sh + sl (pair order), e = x_min - 4 u step
+        if pb == 2:  # tensor-core encoding: step = sh + sl, e / (8 u) = hi + lo (pair order), e = x_min - 4 u step
             pidx = kpair_index(np.arange(d), d)
             kst = self.k_sh16[:, pidx].astype(np.float32) + self.k_sl16[:, pidx].astype(np.float32)
-            kmn = (self.k_e32 + np.float32(4) * kpair_u(np.arange(d)) * kst).astype(np.float32)
+            uf = kpair_u(np.arange(d)).astype(np.float32)
+            self.k_e32 = ((self.k_ehi16[:, pidx].astype(np.float32) + self.k_elo16[:, pidx].astype(np.float32))
+                          * (np.float32(8) * uf)).astype(np.float32)
+            kmn = (self.k_e32 + np.float32(4) * uf * kst).astype(np.float32)
             kst = kst * np.float32(2 ** kshift)
         elif pb == 4 and d % 8 == 0:  # 4-bit tensor-core encoding: pair4 order, e = x_min - 64 step
             pidx = kpair4_index(np.arange(d))

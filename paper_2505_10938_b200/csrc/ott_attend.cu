@@ -449,30 +449,80 @@ __global__ void __launch_bounds__(kAttnThreads) attend_generic_kernel(AttnArgs a
 }
 
 
+// ---- 2-bit records at d = 128 (RecordLayout, width 2): the decode kernel streams the record
+// head (codes, K step halves, V params) and fetches the K e fields of 8 groups at a time.
 template <int G>
 struct MmaSmem {
-  static constexpr int kRec = G * 128 / 2 + 8 * 128 + 8 * G;  // record bytes at d = 128
-  static constexpr int kNG = 1;                        // groups per loop iteration (2 measured slower: spills)
-  static constexpr int kStages = G == 32 ? 3 : 2;      // TMA pipeline depth per warp (3 vs 2: -2 %, v7)
-  float4 qt[8][32];  // q (fp32) per lane for the x_min bias, see mma_body
-  // group records land here through a SWIZZLE_32B tensor map (16-byte chunk bit 4 ^= bit 7
+  static constexpr int kHead = G * 128 / 2 + 2 * 2 * 128 + 8 * G;  // record head bytes
+  static constexpr int kStages = G == 32 ? 3 : 2;                  // TMA pipeline depth per warp (3 vs 2: -2 %, v7)
+  static constexpr int kEStride = 528;  // e slot per group (+16 B skew: conflict-free A-fragment loads)
+  // group record heads land here through a SWIZZLE_32B tensor map (16-byte chunk bit 4 ^= bit 7
   // of the offset): ldmatrix over 32-byte token rows is then bank-conflict free
-  alignas(256) uint8_t stage[kAttnWarps][kStages][kRec];
+  alignas(256) uint8_t stage[kAttnWarps][kStages][kHead];
+  alignas(16) uint8_t ebuf[kAttnWarps][8][kEStride];  // e / (8 u) (fp16 hi[128], lo[128]) of 8 groups
   alignas(8) uint64_t bar[kAttnWarps][kStages];
+  alignas(8) uint64_t ebar[kAttnWarps];
   float mm[kAttnWarps][8], ll[kAttnWarps][8];
 };
+template <int G>
+struct RecHead {  // record head as kBoxes TMA boxes of 32-byte rows; a record is kRecRows rows
+  static constexpr int kRecRows = (G * 128 / 2 + 8 * 128 + 8 * G) / 32;
+  static constexpr int kRows = MmaSmem<G>::kHead / 32;
+  static constexpr int kBoxes = kRows > 256 ? 2 : 1;
+  static constexpr int kBoxRows = kRows / kBoxes;
+};
+template <int G>
+__device__ __forceinline__ void load_record_head(uint32_t dst, const CUtensorMap* map, int64_t rec_index,
+                                                 uint32_t bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(MmaSmem<G>::kHead)
+               : "memory");
+#pragma unroll
+  for (int b = 0; b < RecHead<G>::kBoxes; ++b)
+    tma_tensor_rows(dst + b * RecHead<G>::kBoxRows * 32, map,
+                    (int)(rec_index * RecHead<G>::kRecRows + b * RecHead<G>::kBoxRows), bar);
+}
+__device__ __forceinline__ void bulk_copy(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+// V code pairs as exact fp16 subnormals c 2^(2P-24) in place: pair m (channels m, m+8 of a
+// code word) at mantissa position P = m for m <= 4 (AND only) and P = m - 5 for m >= 5 (from
+// w >> 10): one shift per word.
+struct VSrc {
+  uint32_t x, r10;
+};
+__device__ __forceinline__ VSrc vsrc(uint32_t w) { return {w, w >> 10}; }
+__host__ __device__ constexpr int vpos(int m) { return m <= 4 ? m : m - 5; }
+template <int M>
+__device__ __forceinline__ uint32_t vqt(const VSrc& s) {
+  return (M <= 4 ? s.x : s.r10) & (0x00030003u << (2 * vpos(M)));
+}
+constexpr float kMinit = -1e30f;  // finite initial running max (the first group always rescales)
 
 // Quantized-region partial for (unit blockIdx.x, split blockIdx.y < n_qsplits).
+// Per warp, per group of G tokens (records of the warp's groups g0 + warp + 4k):
+//   * Q K^T on tensor cores (mma.sync m16n8k16, f16 in, f32 accumulate): K codes become
+//     fp16 1 + c 2^(2P-10) in place (one LOP3 per pair); the B operand q' = q u step is an
+//     exact fp16 hi/lo split formed from the record's step halves.
+//   * x_min bias sum_c q e (e = x_min - 4 u step): for 8 groups at once, one m16n8k16 per
+//     k-step with A rows = the 8 groups' e / u (fp16 hi rows 0-7, lo rows 8-15, fetched by
+//     one bulk copy per group) and B = q u (the registers the q' split starts from).
+//   * online softmax with the running max folded into the bias, lazily rescaled.
+//   * O^T += V^T P' with V codes as exact fp16 subnormals and P' = 4 p step in fp16.
 template <int NR, int G>
 __device__ void mma_body(const AttnArgs& a, const Counts& n, const CUtensorMap* tmap, MmaSmem<G>& sm) {
   constexpr int D = 128;
-  constexpr int kRec = MmaSmem<G>::kRec;
+  constexpr int kHead = MmaSmem<G>::kHead;
   constexpr int kMt = G / 16;  // 16-token m-tiles per group
   constexpr int kStages = MmaSmem<G>::kStages;
+  constexpr int kES = MmaSmem<G>::kEStride;
   const RecordLayout L(D, G);
   const ott_cache_t& c = a.c;
   const int u = blockIdx.x, split = blockIdx.y;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);  // warp-uniform for the compiler
   const int g = lane >> 2, tig = lane & 3;
 
   const uint32_t magic = a.k_magic;
@@ -482,202 +532,212 @@ __device__ void mma_body(const AttnArgs& a, const Counts& n, const CUtensorMap* 
   const int g1 = min(n_groups, g0 + per);
   const int my_n = g1 > g0 + warp ? (g1 - g0 - warp + kAttnWarps - 1) / kAttnWarps : 0;
 
-  // q (fp32) table for the x_min bias: [k][lane] = q[head lane/4][channels of words tig, 4+tig]:
-  // k < 4: 16 tig + 4k .. +3; k >= 4: 64 + 16 tig + 4(k-4) .. +3  (conflict-free LDS.128)
-  for (int i = tid; i < 8 * 32; i += kAttnThreads) {
-    const int k = i >> 5, ln = i & 31, h = ln >> 2, t4 = ln & 3;
-    const int ch = (k < 4 ? 16 * t4 : 64 + 16 * t4) + 4 * (k & 3);
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (h < NR) {
-      const uint2 raw = __ldg(reinterpret_cast<const uint2*>(a.q + ((size_t)u * NR + h) * D + ch));
-      const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&raw.x));
-      const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&raw.y));
-      v = make_float4(f0.x, f0.y, f1.x, f1.y);
-    }
-    sm.qt[k][ln] = v;
-  }
   const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&sm.bar[warp][0]);
+  const uint32_t ebar = (uint32_t)__cvta_generic_to_shared(&sm.ebar[warp]);
   const uint32_t stage0 = (uint32_t)__cvta_generic_to_shared(&sm.stage[warp][0][0]);
+  const uint32_t ebuf0 = (uint32_t)__cvta_generic_to_shared(&sm.ebuf[warp][0][0]);
   const int64_t unit_rec = (int64_t)u * c.max_groups;  // record index of group 0
+  const size_t rec_bytes = (size_t)L.bytes();
+  // e fields of the warp's groups k0 .. k0 + 7 into the batch buffer (one bulk copy each)
+  auto load_ebatch = [&](int k0) {
+    const int nb = min(8, my_n - k0);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(ebar), "r"(nb * 4 * D) : "memory");
+    for (int j = 0; j < nb; ++j)
+      bulk_copy(ebuf0 + j * kES,
+                c.blocks + (size_t)(unit_rec + g0 + warp + (k0 + j) * kAttnWarps) * rec_bytes + L.k_e(), 4 * D,
+                ebar);
+  };
   if (lane == 0) {
 #pragma unroll
     for (int s = 0; s < kStages; ++s) mbar_init(bar0 + 8 * s, 1);
+    mbar_init(ebar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
 #pragma unroll
     for (int s = 0; s < kStages; ++s)
-      if (s < my_n)
-        load_record<G>(stage0 + s * kRec, tmap, unit_rec + g0 + warp + s * kAttnWarps, bar0 + 8 * s);
+      if (s < my_n) load_record_head<G>(stage0 + s * kHead, tmap, unit_rec + g0 + warp + s * kAttnWarps, bar0 + 8 * s);
+    if (my_n > 0) load_ebatch(0);
+  }
+  // q * u(m) as exact fp16 pairs (channels 16w+m, 16w+m+8) of head g, words w = tig + 4 hw:
+  // the B operand of the bias MMA, and the q' = q u step split starts from it
+  __half2 q16[2][8];
+#pragma unroll
+  for (int hw = 0; hw < 2; ++hw) {
+    const int wd = tig + 4 * hw;
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      float lo = 0.f, hi = 0.f;
+      if (g < NR) {
+        const uint16_t* qr = a.q + ((size_t)u * NR + g) * D + 16 * wd + m;
+        lo = h2f(__ldg(qr)) * kpair_u(m);
+        hi = h2f(__ldg(qr + 8)) * kpair_u(m);
+      }
+      q16[hw][m] = __floats2half2_rn(lo, hi);
+    }
   }
   __syncthreads();
 
   float o[8][4];
 #pragma unroll
   for (int cm = 0; cm < 8; ++cm) o[cm][0] = o[cm][1] = o[cm][2] = o[cm][3] = 0.f;
-  float mrun[2] = {-INFINITY, -INFINITY}, lsum[2] = {0.f, 0.f}, vb[2] = {0.f, 0.f};
+  float mrun[2] = {kMinit, kMinit}, lsum[2] = {0.f, 0.f}, vb[2] = {0.f, 0.f};
   const uint32_t* pmask = c.pool_mask + (size_t)u * mask_words_per_unit(c);
 
   // ldmatrix row addresses (bytes, relative to a 16-token tile): matrix i = lane/8,
   // row r = lane%8: i0 tokens 0-7 bytes 0-15, i1 tokens 8-15 bytes 0-15,
   // i2 tokens 0-7 bytes 16-31, i3 tokens 8-15 bytes 16-31.
   const uint32_t lm_off = (uint32_t)(((lane & 7) + ((lane >> 3) & 1) * 8) * 32 + (lane >> 4) * 16);
-  __syncthreads();
-  // q * u(m) as exact fp16 pairs (channels 16w+m, 16w+m+8) of head g, words w = tig + 4 hw:
-  // the B operand q' = q u step is formed per group from the record's fp16 step halves
-  __half2 q16[2][8];
+  const float scale = a.scale_log2, scale4 = 4.f * a.scale_log2;
+  float eb0 = 0.f, eb1 = 0.f;  // scaled bias of group (batch base + g), heads 2 tig, 2 tig + 1
+  uint32_t eph = 0, ph = 0;
+  uint32_t mreg = 0;  // G = 32: pool-mask word of group (k & ~31) + lane (one load per 32 groups)
+  // stage index and phase are compile-time within a round of kStages groups
+  for (int k0 = 0; k0 < my_n; k0 += kStages, ph ^= 1u)
 #pragma unroll
-  for (int hw = 0; hw < 2; ++hw)
-#pragma unroll
-    for (int m = 0; m < 8; ++m) {
-      const float4 qa = sm.qt[4 * hw + m / 4][lane];
-      const float4 qb = sm.qt[4 * hw + 2 + m / 4][lane];
-      const float lo = (m % 4 == 0 ? qa.x : m % 4 == 1 ? qa.y : m % 4 == 2 ? qa.z : qa.w) * kpair_u(m);
-      const float hi = (m % 4 == 0 ? qb.x : m % 4 == 1 ? qb.y : m % 4 == 2 ? qb.z : qb.w) * kpair_u(m);
-      q16[hw][m] = __floats2half2_rn(lo, hi);
-    }
-  const float scale4 = 4.f * a.scale_log2;
-  // Groups are processed NG at a time (two independent instruction streams per
-  // warp for the scheduler); a lone tail group is paired with a masked dummy.
-  constexpr int NG = MmaSmem<G>::kNG;
-  for (int k = 0; k < my_n; k += NG) {
-    const int ng = min(NG, my_n - k);
-    const uint8_t* rec[NG];
-    uint32_t rec_s[NG];
-    uint32_t mwords[NG][G / 32];
-#pragma unroll
-    for (int j = 0; j < NG; ++j) {
-      const int kk = k + (j < ng ? j : 0);
-      const int gi = g0 + warp + kk * kAttnWarps;
-#pragma unroll
-      for (int w = 0; w < G / 32; ++w) mwords[j][w] = __ldg(&pmask[(size_t)gi * (G / 32) + w]);
-      const int s = kk % kStages;
-      if (j < ng) mbar_wait(bar0 + 8 * s, (uint32_t)((kk / kStages) & 1));
-      rec[j] = &sm.stage[warp][s][0];
-      rec_s[j] = stage0 + s * kRec;
-    }
-    uint32_t kw[NG][kMt][4];
-#pragma unroll
-    for (int j = 0; j < NG; ++j) {
-      // K code words (ldmatrix: token g / g+8, words tig and 4+tig)
-#pragma unroll
-      for (int mt = 0; mt < kMt; ++mt) ldsm_x4(kw[j][mt], rec_s[j] + swz(L.k_codes() + mt * 16 * 32 + lm_off));
-    }
-    __syncwarp();
-
-    // ---- S = Q K^T on tensor cores. B operand q' = q u step as an exact fp16 hi/lo split
-    // from the record's fp16 step halves (sh + sl): hi = q sh, err = fma(q, sh, -hi) (exact),
-    // lo = fma(q, sl, err); hi and lo accumulate into one chain.
-    // x_min bias (scale * sum_c q e, e = x_min - 4 u step from the record) per head g.
-    float ch[NG][kMt][4];
-    float bias_g[NG];
-#pragma unroll
-    for (int j = 0; j < NG; ++j) {
-      float2 acc2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
-                        make_float2(0.f, 0.f)};  // 4 independent chains
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int wd = k < 4 ? tig : 4 + tig;
-        const float4 ev = *reinterpret_cast<const float4*>(rec[j] + swz(L.k_e() + 64 * wd + 16 * (k & 3)));
-        const float4 qv = sm.qt[k][lane];
-        acc2[(2 * k) & 3] = __ffma2_rn(make_float2(qv.x, qv.y), make_float2(ev.x, ev.y), acc2[(2 * k) & 3]);
-        acc2[(2 * k + 1) & 3] = __ffma2_rn(make_float2(qv.z, qv.w), make_float2(ev.z, ev.w), acc2[(2 * k + 1) & 3]);
+  for (int st = 0; st < kStages; ++st) {
+    const int k = k0 + st;
+    if (k >= my_n) break;
+    const int gi = g0 + warp + k * kAttnWarps;
+    uint32_t mwords[G / 32];
+    if (G == 32) {
+      if ((k & 31) == 0) {
+        const int kl = k + lane;
+        mreg = kl < my_n ? __ldg(&pmask[(size_t)(g0 + warp + kl * kAttnWarps)]) : 0u;
       }
-      bias_g[j] = ((acc2[0].x + acc2[0].y) + (acc2[1].x + acc2[1].y)) + ((acc2[2].x + acc2[2].y) + (acc2[3].x + acc2[3].y));
+      mwords[0] = __shfl_sync(0xffffffffu, mreg, k & 31);
+    } else {
 #pragma unroll
-      for (int mt = 0; mt < kMt; ++mt) ch[j][mt][0] = ch[j][mt][1] = ch[j][mt][2] = ch[j][mt][3] = 0.f;
+      for (int w = 0; w < G / 32; ++w) mwords[w] = __ldg(&pmask[(size_t)gi * (G / 32) + w]);
     }
+    if ((k & 7) == 0) {  // ---- x_min bias of the next 8 groups on tensor cores
+      mbar_wait(ebar, eph);
+      eph ^= 1u;
+      const uint8_t* eg = &sm.ebuf[warp][g][0];  // lane (g, tig): group k + g
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int hw = 0; hw < 2; ++hw) {
+        const int wd = tig + 4 * hw;
+        const uint4 h0 = *reinterpret_cast<const uint4*>(eg + 32 * wd);
+        const uint4 h1 = *reinterpret_cast<const uint4*>(eg + 32 * wd + 16);
+        const uint4 l0 = *reinterpret_cast<const uint4*>(eg + 2 * D + 32 * wd);
+        const uint4 l1 = *reinterpret_cast<const uint4*>(eg + 2 * D + 32 * wd + 16);
+        const uint32_t hiw[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+        const uint32_t low[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
+#pragma unroll
+        for (int mm = 0; mm < 8; mm += 2)
+          mma16816(acc, hiw[mm], low[mm], hiw[mm + 1], low[mm + 1], h2_as_u32(q16[hw][mm]), h2_as_u32(q16[hw][mm + 1]));
+      }
+      eb0 = (acc[0] + acc[2]) * (kEScale * scale);
+      eb1 = (acc[1] + acc[3]) * (kEScale * scale);
+      __syncwarp();
+      if (lane == 0 && k + 8 < my_n) {
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        load_ebatch(k + 8);
+      }
+    }
+    const float bias0 = __shfl_sync(0xffffffffu, eb0, 4 * (k & 7) + tig);  // head 2 tig
+    const float bias1 = __shfl_sync(0xffffffffu, eb1, 4 * (k & 7) + tig);  // head 2 tig + 1
+    mbar_wait(bar0 + 8 * st, ph);
+    const uint8_t* rec = &sm.stage[warp][st][0];
+    const uint32_t rec_s = stage0 + st * kHead;
+    uint32_t kw[kMt][4];
+#pragma unroll
+    for (int mt = 0; mt < kMt; ++mt) ldsm_x4(kw[mt], rec_s + swz(L.k_codes() + mt * 16 * 32 + lm_off));
+
+    // ---- S = Q K^T. B operand q' = q u step as an exact fp16 hi/lo split from the record's
+    // fp16 step halves (sh + sl): hi = q sh, err = fma(q, sh, -hi) (exact), lo = fma(q, sl, err)
+    float ch[kMt][4];
+#pragma unroll
+    for (int mt = 0; mt < kMt; ++mt) ch[mt][0] = ch[mt][1] = ch[mt][2] = ch[mt][3] = 0.f;
 #pragma unroll
     for (int hw = 0; hw < 2; ++hw) {
+      const int wd = tig + 4 * hw;
+      const uint4 h0 = *reinterpret_cast<const uint4*>(rec + swz(L.k_sh() + 32 * wd));
+      const uint4 h1 = *reinterpret_cast<const uint4*>(rec + swz(L.k_sh() + 32 * wd + 16));
+      const uint4 l0 = *reinterpret_cast<const uint4*>(rec + swz(L.k_sl() + 32 * wd));
+      const uint4 l1 = *reinterpret_cast<const uint4*>(rec + swz(L.k_sl() + 32 * wd + 16));
+      const uint32_t shw[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+      const uint32_t slw[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
+      uint32_t bh[8], bl[8];
 #pragma unroll
-      for (int j = 0; j < NG; ++j) {
-        const int wd = tig + 4 * hw;
-        const uint4 h0 = *reinterpret_cast<const uint4*>(rec[j] + swz(L.k_sh() + 32 * wd));
-        const uint4 h1 = *reinterpret_cast<const uint4*>(rec[j] + swz(L.k_sh() + 32 * wd + 16));
-        const uint4 l0 = *reinterpret_cast<const uint4*>(rec[j] + swz(L.k_sl() + 32 * wd));
-        const uint4 l1 = *reinterpret_cast<const uint4*>(rec[j] + swz(L.k_sl() + 32 * wd + 16));
-        const uint32_t shw[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
-        const uint32_t slw[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
-        uint32_t bh[8], bl[8];
+      for (int m = 0; m < 8; ++m) {
+        const __half2 sh = *reinterpret_cast<const __half2*>(&shw[m]);
+        const __half2 sl = *reinterpret_cast<const __half2*>(&slw[m]);
+        const __half2 H = __hmul2(q16[hw][m], sh);
+        const __half2 E = __hfma2(q16[hw][m], sh, __hneg2(H));
+        bh[m] = h2_as_u32(H);
+        bl[m] = h2_as_u32(__hfma2(q16[hw][m], sl, E));
+      }
+      Shifted s0[kMt], s1[kMt];
 #pragma unroll
-        for (int m = 0; m < 8; ++m) {
-          const __half2 sh = *reinterpret_cast<const __half2*>(&shw[m]);
-          const __half2 sl = *reinterpret_cast<const __half2*>(&slw[m]);
-          const __half2 H = __hmul2(q16[hw][m], sh);
-          const __half2 E = __hfma2(q16[hw][m], sh, __hneg2(H));
-          bh[m] = h2_as_u32(H);
-          bl[m] = h2_as_u32(__hfma2(q16[hw][m], sl, E));
-        }
-        Shifted s0[kMt], s1[kMt];
-#pragma unroll
-        for (int mt = 0; mt < kMt; ++mt) {
-          s0[mt] = shifted(kw[j][mt][2 * hw]);
-          s1[mt] = shifted(kw[j][mt][2 * hw + 1]);
-        }
+      for (int mt = 0; mt < kMt; ++mt) {
+        s0[mt] = shifted(kw[mt][2 * hw]);
+        s1[mt] = shifted(kw[mt][2 * hw + 1]);
+      }
 #define OTT_QK(MM)                                                                    \
   {                                                                                   \
     _Pragma("unroll") for (int mt = 0; mt < kMt; ++mt) {                              \
       const uint32_t a0 = kq<MM>(s0[mt], magic), a1 = kq<MM>(s1[mt], magic);         \
       const uint32_t a2 = kq<MM + 1>(s0[mt], magic), a3 = kq<MM + 1>(s1[mt], magic); \
-      mma16816(ch[j][mt], a0, a1, a2, a3, bh[MM], bh[MM + 1]);                        \
-      mma16816(ch[j][mt], a0, a1, a2, a3, bl[MM], bl[MM + 1]);                        \
+      mma16816(ch[mt], a0, a1, a2, a3, bh[MM], bh[MM + 1]);                           \
+      mma16816(ch[mt], a0, a1, a2, a3, bl[MM], bl[MM + 1]);                           \
     }                                                                                 \
   }
-        OTT_QK(0) OTT_QK(2) OTT_QK(4) OTT_QK(6)
+      OTT_QK(0) OTT_QK(2) OTT_QK(4) OTT_QK(6)
 #undef OTT_QK
-      }
     }
-    float sc[NG][kMt][4];
+
+    // ---- x = logit - m (log2 units), heads 2 tig (cols 0, 2) and 2 tig + 1 (cols 1, 3)
+    const float bm0 = bias0 - mrun[0], bm1 = bias1 - mrun[1];
+    float x[kMt][4];
 #pragma unroll
-    for (int j = 0; j < NG; ++j) {
-      float bias = bias_g[j];
-      bias += __shfl_xor_sync(0xffffffffu, bias, 1);
-      bias += __shfl_xor_sync(0xffffffffu, bias, 2);
-      bias *= a.scale_log2;
-      const float bias0 = __shfl_sync(0xffffffffu, bias, 8 * tig);      // head 2*tig
-      const float bias1 = __shfl_sync(0xffffffffu, bias, 8 * tig + 4);  // head 2*tig+1
-      const bool dummy = j >= ng;
+    for (int mt = 0; mt < kMt; ++mt) {
+      x[mt][0] = fmaf(ch[mt][0], scale4, bm0);
+      x[mt][1] = fmaf(ch[mt][1], scale4, bm1);
+      x[mt][2] = fmaf(ch[mt][2], scale4, bm0);
+      x[mt][3] = fmaf(ch[mt][3], scale4, bm1);
+    }
+    // pooled positions: their logits come from the pool tile (overwrite semantics)
+    bool any_pooled = false;
 #pragma unroll
-      for (int mt = 0; mt < kMt; ++mt) {
-        sc[j][mt][0] = dummy ? -INFINITY : fmaf(ch[j][mt][0], scale4, bias0);
-        sc[j][mt][1] = dummy ? -INFINITY : fmaf(ch[j][mt][1], scale4, bias1);
-        sc[j][mt][2] = dummy ? -INFINITY : fmaf(ch[j][mt][2], scale4, bias0);
-        sc[j][mt][3] = dummy ? -INFINITY : fmaf(ch[j][mt][3], scale4, bias1);
-      }
-      // pooled positions: their logits come from the pool tile (overwrite semantics)
+    for (int w = 0; w < G / 32; ++w) any_pooled |= mwords[w] != 0u;
+    if (any_pooled) {
 #pragma unroll
       for (int w = 0; w < G / 32; ++w) {
-        const uint32_t mw = mwords[j][w];
-        if (mw) {
+        const uint32_t mw = mwords[w];
 #pragma unroll
-          for (int mt = 2 * w; mt < 2 * w + 2; ++mt) {
-            if ((mw >> ((mt & 1) * 16 + g)) & 1u) sc[j][mt][0] = sc[j][mt][1] = -INFINITY;
-            if ((mw >> ((mt & 1) * 16 + g + 8)) & 1u) sc[j][mt][2] = sc[j][mt][3] = -INFINITY;
-          }
+        for (int mt = 2 * w; mt < 2 * w + 2; ++mt) {
+          if ((mw >> ((mt & 1) * 16 + g)) & 1u) x[mt][0] = x[mt][1] = -INFINITY;
+          if ((mw >> ((mt & 1) * 16 + g + 8)) & 1u) x[mt][2] = x[mt][3] = -INFINITY;
         }
       }
     }
 
-    // ---- online softmax (heads 2*tig, 2*tig+1), lazily rescaled: the running max
-    // only moves when a logit exceeds it by kLazy (log2 units), so p <= 2^kLazy
-    float tmax[2];
+    // ---- online softmax, lazily rescaled: the running max only moves when a logit exceeds it
+    // by kLazy (log2 units), so p <= 2^kLazy
+    float xmax = x[0][0];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      float t = -INFINITY;
+    for (int mt = 0; mt < kMt; ++mt)
 #pragma unroll
-      for (int j = 0; j < NG; ++j)
+      for (int e = 0; e < 4; ++e) xmax = fmaxf(xmax, x[mt][e]);
+    if (__any_sync(0xffffffffu, xmax > kLazy)) {  // rare: recompute the logits against the new max
+      float t[2] = {-INFINITY, -INFINITY};
 #pragma unroll
-        for (int mt = 0; mt < kMt; ++mt) t = fmaxf(t, fmaxf(sc[j][mt][h], sc[j][mt][h + 2]));
-      tmax[h] = t;
-    }
-    const bool need = tmax[0] > mrun[0] + kLazy || tmax[1] > mrun[1] + kLazy;
-    if (__any_sync(0xffffffffu, need)) {  // rare: warp max over the token rows, rescale
+      for (int mt = 0; mt < kMt; ++mt) {
+        x[mt][0] = x[mt][0] == -INFINITY ? -INFINITY : fmaf(ch[mt][0], scale4, bias0);
+        x[mt][1] = x[mt][1] == -INFINITY ? -INFINITY : fmaf(ch[mt][1], scale4, bias1);
+        x[mt][2] = x[mt][2] == -INFINITY ? -INFINITY : fmaf(ch[mt][2], scale4, bias0);
+        x[mt][3] = x[mt][3] == -INFINITY ? -INFINITY : fmaf(ch[mt][3], scale4, bias1);
+        t[0] = fmaxf(t[0], fmaxf(x[mt][0], x[mt][2]));
+        t[1] = fmaxf(t[1], fmaxf(x[mt][1], x[mt][3]));
+      }
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        float t = tmax[h];
-        t = fmaxf(t, __shfl_xor_sync(0xffffffffu, t, 4));
-        t = fmaxf(t, __shfl_xor_sync(0xffffffffu, t, 8));
-        t = fmaxf(t, __shfl_xor_sync(0xffffffffu, t, 16));
-        const float mnew = fmaxf(mrun[h], t);
-        const float corr = mnew == -INFINITY ? 1.f : ex2(mrun[h] - mnew);
+        float tm = t[h];
+        tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 4));
+        tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 8));
+        tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 16));
+        const float mnew = fmaxf(mrun[h], tm);
+        const float corr = ex2(mrun[h] - mnew);
         lsum[h] *= corr;
         vb[h] *= corr;
 #pragma unroll
@@ -686,50 +746,44 @@ __device__ void mma_body(const AttnArgs& a, const Counts& n, const CUtensorMap* 
           o[cm][h + 2] *= corr;
         }
         mrun[h] = mnew;
+#pragma unroll
+        for (int mt = 0; mt < kMt; ++mt) {
+          x[mt][h] -= mnew;
+          x[mt][h + 2] -= mnew;
+        }
       }
     }
-    const float me0 = mrun[0] == -INFINITY ? 0.f : mrun[0];
-    const float me1 = mrun[1] == -INFINITY ? 0.f : mrun[1];
 
     // ---- O^T += V^T P'  (P' = 4 p step fp16, V x_min into vb; with V codes as
     // subnormals the accumulator holds sum(p step c) * 2^(2P-22))
 #pragma unroll
-    for (int j = 0; j < NG; ++j) {
-#pragma unroll
-      for (int mt = 0; mt < kMt; ++mt) {
-        const float vs0 = *reinterpret_cast<const float*>(rec[j] + swz(L.v_step() + 4 * (mt * 16 + g)));
-        const float vs1 = *reinterpret_cast<const float*>(rec[j] + swz(L.v_step() + 4 * (mt * 16 + g + 8)));
-        const float ve0 = *reinterpret_cast<const float*>(rec[j] + swz(L.v_xmin() + 4 * (mt * 16 + g)));
-        const float ve1 = *reinterpret_cast<const float*>(rec[j] + swz(L.v_xmin() + 4 * (mt * 16 + g + 8)));
-        const float p00 = ex2(sc[j][mt][0] - me0), p01 = ex2(sc[j][mt][1] - me1);
-        const float p10 = ex2(sc[j][mt][2] - me0), p11 = ex2(sc[j][mt][3] - me1);
-        lsum[0] += p00 + p10;
-        lsum[1] += p01 + p11;
-        vb[0] = fmaf(p00, ve0, fmaf(p10, ve1, vb[0]));
-        vb[1] = fmaf(p01, ve0, fmaf(p11, ve1, vb[1]));
-        const float f0 = 4.f * vs0, f1 = 4.f * vs1;
-        const uint32_t b0 = movm_t(pack_h2(p00 * f0, p01 * f0));
-        const uint32_t b1 = movm_t(pack_h2(p10 * f1, p11 * f1));
-        uint32_t vr[4];
-        ldsm_x4_t(vr, rec_s[j] + swz(L.v_codes() + mt * 16 * 32 + lm_off));
-        const Shifted v0 = shifted(vr[0]), v1 = shifted(vr[1]), v2 = shifted(vr[2]), v3 = shifted(vr[3]);
-#define OTT_PV(CM) mma16816(o[CM], vq<CM>(v0), vq<CM>(v2), vq<CM>(v1), vq<CM>(v3), b0, b1);
-        OTT_PV(0) OTT_PV(1) OTT_PV(2) OTT_PV(3) OTT_PV(4) OTT_PV(5) OTT_PV(6) OTT_PV(7)
+    for (int mt = 0; mt < kMt; ++mt) {
+      const float vs0 = *reinterpret_cast<const float*>(rec + swz(L.v_step() + 4 * (mt * 16 + g)));
+      const float vs1 = *reinterpret_cast<const float*>(rec + swz(L.v_step() + 4 * (mt * 16 + g + 8)));
+      const float ve0 = *reinterpret_cast<const float*>(rec + swz(L.v_xmin() + 4 * (mt * 16 + g)));
+      const float ve1 = *reinterpret_cast<const float*>(rec + swz(L.v_xmin() + 4 * (mt * 16 + g + 8)));
+      const float p00 = ex2(x[mt][0]), p01 = ex2(x[mt][1]);
+      const float p10 = ex2(x[mt][2]), p11 = ex2(x[mt][3]);
+      lsum[0] += p00 + p10;
+      lsum[1] += p01 + p11;
+      vb[0] = fmaf(p00, ve0, fmaf(p10, ve1, vb[0]));
+      vb[1] = fmaf(p01, ve0, fmaf(p11, ve1, vb[1]));
+      const float f0 = 4.f * vs0, f1 = 4.f * vs1;
+      const uint32_t b0 = movm_t(pack_h2(p00 * f0, p01 * f0));
+      const uint32_t b1 = movm_t(pack_h2(p10 * f1, p11 * f1));
+      uint32_t vr[4];
+      ldsm_x4_t(vr, rec_s + swz(L.v_codes() + mt * 16 * 32 + lm_off));
+      const VSrc v0 = vsrc(vr[0]), v1 = vsrc(vr[1]), v2 = vsrc(vr[2]), v3 = vsrc(vr[3]);
+#define OTT_PV(CM) mma16816(o[CM], vqt<CM>(v0), vqt<CM>(v2), vqt<CM>(v1), vqt<CM>(v3), b0, b1);
+      OTT_PV(0) OTT_PV(1) OTT_PV(2) OTT_PV(3) OTT_PV(4) OTT_PV(5) OTT_PV(6) OTT_PV(7)
 #undef OTT_PV
-      }
     }
 
+    // ---- release the stage: prefetch the record head of group k + kStages
     __syncwarp();
-    if (lane == 0) {
-#pragma unroll
-      for (int j = 0; j < NG; ++j) {
-        const int kk = k + j, ka = kk + kStages;
-        if (j < ng && ka < my_n) {
-          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-          load_record<G>(stage0 + (kk % kStages) * kRec, tmap, unit_rec + g0 + warp + ka * kAttnWarps,
-                         bar0 + 8 * (kk % kStages));
-        }
-      }
+    if (lane == 0 && k + kStages < my_n) {
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      load_record_head<G>(rec_s, tmap, unit_rec + gi + kStages * kAttnWarps, bar0 + 8 * st);
     }
   }
 
@@ -745,7 +799,7 @@ __device__ void mma_body(const AttnArgs& a, const Counts& n, const CUtensorMap* 
   if (g == 0) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      sm.mm[warp][2 * tig + h] = mrun[h];
+      sm.mm[warp][2 * tig + h] = lsum[h] > 0.f ? mrun[h] : -INFINITY;  // no token: empty partial
       sm.ll[warp][2 * tig + h] = lsum[h];
     }
   }
@@ -753,7 +807,7 @@ __device__ void mma_body(const AttnArgs& a, const Counts& n, const CUtensorMap* 
   float* accw = reinterpret_cast<float*>(&sm.stage[warp][0][0]);  // [8 heads][128] natural channel order
 #pragma unroll
   for (int cm = 0; cm < 8; ++cm) {
-    const float f = pair_pos(cm) == 2 ? 262144.f : (pair_pos(cm) == 3 ? 65536.f : 16384.f);  // 2^(22-2P)
+    const float f = (float)(1 << (22 - 2 * vpos(cm)));  // 2^(22-2P)
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       accw[(2 * tig + h) * D + 8 * g + cm] = fmaf(o[cm][h], f, vb[h]);
@@ -1853,7 +1907,7 @@ static cudaError_t launch_mma4_t(const AttnArgs& a, cudaStream_t st) {
 template <int NR, int G>
 static cudaError_t launch_mma_t(const AttnArgs& a, cudaStream_t st) {
   CUtensorMap tmap;
-  cudaError_t te = record_tensor_map(a.c, RecTma<G>::kBoxRows, RecTma<G>::kRows, &tmap);
+  cudaError_t te = record_tensor_map(a.c, RecHead<G>::kBoxRows, RecHead<G>::kRecRows, &tmap);
   if (te != cudaSuccess) return te;
   const size_t smem = sizeof(MmaSmem<G>) > sizeof(FpSmem) ? sizeof(MmaSmem<G>) : sizeof(FpSmem);
   cudaError_t e =
@@ -1863,17 +1917,6 @@ static cudaError_t launch_mma_t(const AttnArgs& a, cudaStream_t st) {
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   return launch_combine<128>(a, NR, st, true);
-}
-
-// 2-bit, G = 32: the mma.sync K2 (default) or the tcgen05 Q K^T variant (ott_attend_tc.cu,
-// OTT_ATTN_KERNEL=tcq; slower as measured)
-static bool use_tcq() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("OTT_ATTN_KERNEL");
-    v = (e && strcmp(e, "tcq") == 0) ? 1 : 0;
-  }
-  return v == 1;
 }
 
 bool mma_eligible(const ott_cache_t& c) {
@@ -1974,7 +2017,6 @@ cudaError_t launch_attend(const ott_cache_t& c, const uint16_t* q, uint16_t* out
 #undef OTT_BCASE
     return cudaErrorInvalidValue;
   }
-  if (mma_eligible(c) && G == 32 && use_tcq()) return launch_tcq(a, n_rep, st);
   if (mma_eligible(c)) {
 #define OTT_MCASE(NRv, Gv) \
   if (n_rep == NRv && G == Gv) return launch_mma_t<NRv, Gv>(a, st);

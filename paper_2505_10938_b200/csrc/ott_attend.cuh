@@ -411,6 +411,5 @@ __device__ void fp_body(const AttnArgs& a, const Counts& n, FpSmem& sm) {
 // launchers shared between the attention translation units (ott_attend.cu)
 cudaError_t record_tensor_map(const ott_cache_t& c, int box_rows, int rec_rows, CUtensorMap* map);
 cudaError_t launch_combine_tc128(const AttnArgs& a, int NR, cudaStream_t st);
-cudaError_t launch_tcq(const AttnArgs& a, int n_rep, cudaStream_t st);  // ott_attend_tc.cu
 
 }  // namespace ott

@@ -22,6 +22,10 @@ cudaError_t launch_rep_pad(const uint16_t* q, uint16_t* qs, int n_units, int n_r
                            cudaStream_t st);
 cudaError_t launch_rep_unpad(const ott_cache_t& c, const uint16_t* os, uint16_t* out, int n_rep, int h0, int nh,
                              int nr, cudaStream_t st);
+cudaError_t launch_attend_exact(const float* q, const float* keys, const float* values, int n, int d, int n_q,
+                                float* out, float* weights, float* scores, cudaStream_t st);
+cudaError_t launch_pool_rank(const double* s, const int64_t* p, int n, int32_t* rank, cudaStream_t st);
+cudaError_t launch_score_rows(const float* rows, int n, int d, double* out, cudaStream_t st);
 }  // namespace ott
 
 // Query heads per KV head the attention kernels are instantiated for: 1, 2, 4, 8. Other counts
@@ -247,7 +251,28 @@ int ott_logits(const ott_cache_t* c, const uint16_t* q, float* logits, int32_t n
       ott::launch_logits(*c, q, logits, n_rep, quantized_tokens, total_tokens, (cudaStream_t)stream));
 }
 
-const char* ott_version(void) { return "ott_b200 0.1 (sm_100a)"; }
+int ott_attend_exact(const float* q, const float* keys, const float* values, int32_t n, int32_t d, int32_t n_q,
+                     float* out, float* weights, float* scores, void* stream) {
+  if (n < 1) return fail(OTT_ERR_CONTRACT, "attention needs at least one cached token");  // attention.py:48-49
+  if (d < 1 || n_q < 1) return fail(OTT_ERR_CONTRACT, "bad shape");
+  if (!q || !keys || !values || !out || !weights || !scores) return fail(OTT_ERR_CONTRACT, "null buffer");
+  return cuda_status(ott::launch_attend_exact(q, keys, values, n, d, n_q, out, weights, scores, (cudaStream_t)stream));
+}
+
+int ott_pool_rank(const double* scores, const int64_t* positions, int32_t n, int32_t* rank, void* stream) {
+  if (n < 0) return fail(OTT_ERR_CONTRACT, "bad item count");
+  if (n == 0) return OTT_OK;
+  if (!scores || !positions || !rank) return fail(OTT_ERR_CONTRACT, "null buffer");
+  return cuda_status(ott::launch_pool_rank(scores, positions, n, rank, (cudaStream_t)stream));
+}
+
+int ott_score_rows(const float* rows, int32_t n, int32_t d, double* scores, void* stream) {
+  if (n < 1 || d < 1) return fail(OTT_ERR_CONTRACT, "score_tokens expects a non-empty 2-D key matrix");
+  if (!rows || !scores) return fail(OTT_ERR_CONTRACT, "null buffer");
+  return cuda_status(ott::launch_score_rows(rows, n, d, scores, (cudaStream_t)stream));
+}
+
+const char* ott_version(void) { return "ott_b200 0.2 (sm_100a)"; }
 const char* ott_last_error(void) { return g_err; }
 
 }  // extern "C"

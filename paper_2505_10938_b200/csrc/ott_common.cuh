@@ -28,6 +28,10 @@ __host__ __device__ constexpr int code_bits(int bits, int d, int G) {
 
 // Block record layout (see ott_b200.h). All offsets in bytes. `bits` is the stored code
 // width (code_bits of the cache's bits).
+//   width 2:      K codes | V codes | K sh[d] | K sl[d] | V step[G] | V x_min[G] | K e hi[d] | K e lo[d]
+//   other widths: K codes | V codes | K sh[d] | K sl[d] | K e[d] (f32) | V step[G] | V x_min[G]
+// At width 2 the K x_min term comes last so the decode kernels can stream a record's head
+// (head_bytes) and fetch the e fields of 8 groups at once (batched bias, ott_attend.cu).
 struct RecordLayout {
   int d, G, bits;
   __host__ __device__ RecordLayout(int d_, int G_, int bits_ = 2) : d(d_), G(G_), bits(code_bits(bits_, d_, G_)) {}
@@ -38,11 +42,15 @@ struct RecordLayout {
   __host__ __device__ int v_codes() const { return code_bytes(); }
   __host__ __device__ int k_sh() const { return 2 * code_bytes(); }  // fp16 [d], pair order
   __host__ __device__ int k_sl() const { return k_sh() + 2 * d; }     // fp16 [d], pair order
-  __host__ __device__ int k_e() const { return k_sl() + 2 * d; }      // f32 [d], channel order
-  __host__ __device__ int v_step() const { return k_e() + 4 * d; }
+  __host__ __device__ int v_step() const { return bits == 2 ? k_sl() + 2 * d : k_sl() + 6 * d; }
   __host__ __device__ int v_xmin() const { return v_step() + 4 * G; }
-  __host__ __device__ int bytes() const { return (v_xmin() + 4 * G + 15) & ~15; }
+  // width 2: fp16 hi [d] then lo [d] (pair order) of e / u; other widths: f32 [d], channel order
+  __host__ __device__ int k_e() const { return bits == 2 ? v_xmin() + 4 * G : k_sl() + 2 * d; }
+  __host__ __device__ int head_bytes() const { return bits == 2 ? k_e() : bytes(); }  // before the e fields
+  __host__ __device__ int bytes() const { return (v_step() + 8 * G + (bits == 2 ? 4 * d : 0) + 15) & ~15; }
 };
+
+constexpr float kEScale = 8.f;  // width-2 K e fields hold e / (kEScale u), see store_k_e2
 
 // ---- K parameter encoding (tensor-core friendly; exact values live in params64).
 // A 32-bit code word holds 16 channels of one token; the decode kernels extract
@@ -96,13 +104,32 @@ __device__ __forceinline__ float k_step_of(const uint8_t* rec, const RecordLayou
   return h2f(reinterpret_cast<const uint16_t*>(rec + L.k_sh())[j]) + h2f(reinterpret_cast<const uint16_t*>(rec + L.k_sl())[j]);
 }
 __device__ __forceinline__ float k_xmin_of(const uint8_t* rec, const RecordLayout& L, int c, float step) {
+  if (L.bits == 2) {  // e / (8 u) as fp16 hi + lo in pair order
+    const int j = kpair_index(c, L.d);
+    const uint16_t* eh = reinterpret_cast<const uint16_t*>(rec + L.k_e());
+    const float u = kpair_u(c % 8);
+    return fmaf(4.f * u, step, (h2f(eh[j]) + h2f(eh[L.d + j])) * (kEScale * u));
+  }
   const float e = reinterpret_cast<const float*>(rec + L.k_e())[c];
-  if (L.bits == 2) return fmaf(4.f * kpair_u(c % 8), step, e);
   if (k_tc4(L.bits, L.d)) return fmaf(64.f, step, e);
   if (k_tc8(L.bits, L.d)) return fmaf(1024.f, step, e);
   return e;
 }
 __device__ __forceinline__ uint16_t f2h(float f) { return __half_as_ushort(__float2half_rn(f)); }
+// Width-2 K x_min term of channel c: e = f32(x_min - 4 u step) (computed by the caller in
+// float64), stored as t = e / (8 u) (exact) split into fp16 hi = fp16(t), lo = fp16(t - hi) in
+// pair order: the decode kernels multiply it by q u (their Q K^T B operand) on tensor cores.
+// |t| <= (65504 + 4 * 65504) / 8 for any fp16 input (1-bit steps included), so t never
+// overflows fp16.
+__device__ __forceinline__ void store_k_e2(uint8_t* rec, const RecordLayout& L, int c, float e) {
+  const float t = e / (kEScale * kpair_u(c % 8));
+  const __half hi = __float2half_rn(t);
+  const __half lo = __float2half_rn(t - __half2float(hi));
+  uint16_t* eh = reinterpret_cast<uint16_t*>(rec + L.k_e());
+  const int j = kpair_index(c, L.d);
+  eh[j] = __half_as_ushort(hi);
+  eh[L.d + j] = __half_as_ushort(lo);
+}
 
 // Largest K or V step of a unit's 2-bit groups (pool_meta[u][3], float bits, atomic max):
 // the tensor-core attention scales its fp16 operands (q u step, 4 p v_step) by powers of two

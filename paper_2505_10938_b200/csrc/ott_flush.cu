@@ -463,7 +463,9 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
           ksh[j] = sh;
           ksl[j] = sl;
           const double off = L.bits == 2 ? 4.0 * (double)kpair_u(col % 8) : (L.bits == 4 ? 64.0 : 1024.0);
-          ke[col] = __double2float_rn(__dsub_rn(mn, __dmul_rn(off, kstep)));
+          const float e = __double2float_rn(__dsub_rn(mn, __dmul_rn(off, kstep)));
+          if (L.bits == 2) store_k_e2(rec, L, col, e);
+          else ke[col] = e;
         } else {
           reinterpret_cast<float*>(ksh)[col] = __double2float_rn(step);
           ke[col] = __double2float_rn(mn);
@@ -1018,7 +1020,8 @@ __device__ __forceinline__ void frozen_group_subst(uint8_t* rec, double* p64, co
         p64[D + col] = step[j];
       }
     }
-    *reinterpret_cast<float4*>(rec + L.k_e() + 16 * lane) = make_float4(ke[0], ke[1], ke[2], ke[3]);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) store_k_e2(rec, L, 4 * lane + j, ke[j]);
     uint8_t* kcodes = rec + L.k_codes() + lane;
     for (int t = 0; t < G; ++t) {
       float x[4];
@@ -1229,7 +1232,8 @@ __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen_kernel(ott_cac
         p64[D + col] = step[j];
       }
     }
-    *reinterpret_cast<float4*>(rec + L.k_e() + 16 * lane) = make_float4(ke[0], ke[1], ke[2], ke[3]);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) store_k_e2(rec, L, 4 * lane + j, ke[j]);
     uint8_t* kcodes = rec + L.k_codes() + lane;  // byte (t d + 4 lane) / 4 holds channels 4 lane..+3 of token t
     if (exact) {
       __half2 t01[kLevels], t23[kLevels];
@@ -1444,7 +1448,12 @@ __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen4_kernel(ott_ca
         p64[D + col] = step[j];
       }
     }
-    *reinterpret_cast<float4*>(rec + L.k_e() + 16 * lane) = make_float4(ke[0], ke[1], ke[2], ke[3]);
+    if (kBits == 2) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) store_k_e2(rec, L, 4 * lane + j, ke[j]);
+    } else {
+      *reinterpret_cast<float4*>(rec + L.k_e() + 16 * lane) = make_float4(ke[0], ke[1], ke[2], ke[3]);
+    }
     // channels 4 lane..+3 of token t: one byte of 2-bit fields, one uint16 of nibbles or one uint32 of bytes
     uint8_t* kcodes2 = rec + L.k_codes() + lane;
     uint16_t* kcodes4 = reinterpret_cast<uint16_t*>(rec + L.k_codes()) + lane;

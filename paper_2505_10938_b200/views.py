@@ -86,6 +86,13 @@ class OutlierEntry:
     value: np.ndarray
     score: float
 
+    @classmethod
+    def from_rows(cls, position: int, key, value) -> "OutlierEntry":
+        """outlier.py:37-42 (the float64 L1 score is computed by the library, pool.py)."""
+        from .pool import entry_from_rows
+
+        return entry_from_rows(position, key, value)
+
 
 @dataclass
 class OutlierPoolView:

@@ -45,16 +45,24 @@ def cfg_of(bits, G, R, N, A, d):
 def expected_k_encoding(step64, xmin64, bits=2):
     """The record's K parameter encoding (ott_b200.h) computed from the exact
     float64 params: sh = fp16(step), sl = fp16(step - sh) in pair order, and
-    e = f32(x_min - 4 u(c) step) (2-bit) or f32(x_min - 64 step) (4-bit)."""
+    e = f32(x_min - 4 u(c) step) stored as fp16 (hi, lo) of e / (8 u) in pair order (2-bit),
+    f32(x_min - 64 step) (4-bit) or f32(x_min - 1024 step) (8-bit)."""
     from paper_2505_10938_b200.cache import kpair4_index, kpair_index, kpair_u
     step64 = np.asarray(step64, np.float64)
     xmin64 = np.asarray(xmin64, np.float64)
     d = len(step64)
     sh = step64.astype(np.float16)
     sl = (step64 - sh.astype(np.float64)).astype(np.float16)
-    if bits == 2:
-        e = (xmin64 - 4.0 * kpair_u(np.arange(d)).astype(np.float64) * step64).astype(np.float32)
+    if bits == 2:  # e / (8 u) as fp16 hi + lo in pair order (ott_common.cuh store_k_e2)
+        u = kpair_u(np.arange(d)).astype(np.float64)
+        e32 = (xmin64 - 4.0 * u * step64).astype(np.float32)
+        t = (e32 / (np.float32(8) * u.astype(np.float32))).astype(np.float32)
+        hi = t.astype(np.float16)
+        lo = (t - hi.astype(np.float32)).astype(np.float16)
         idx = kpair_index(np.arange(d), d)
+        e = (np.empty(d, np.float16), np.empty(d, np.float16))
+        e[0][idx] = hi
+        e[1][idx] = lo
     elif bits == 4:
         e = (xmin64 - 64.0 * step64).astype(np.float32)
         idx = kpair4_index(np.arange(d))
@@ -92,7 +100,11 @@ def assert_unit_matches_oracle(u, ref, exact64=True):
             sh, sl, e = expected_k_encoding(kst, blk["k_xmin"], pb)
             np.testing.assert_array_equal(u.k_sh16[b].view(np.uint16), sh.view(np.uint16))
             np.testing.assert_array_equal(u.k_sl16[b].view(np.uint16), sl.view(np.uint16))
-            np.testing.assert_array_equal(u.k_e32[b], e)
+            if pb == 2:
+                np.testing.assert_array_equal(u.k_ehi16[b].view(np.uint16), e[0].view(np.uint16))
+                np.testing.assert_array_equal(u.k_elo16[b].view(np.uint16), e[1].view(np.uint16))
+            else:
+                np.testing.assert_array_equal(u.k_e32[b], e)
         else:  # float32 step / x_min (ott_b200.h)
             np.testing.assert_array_equal(u.k_step32[b], blk["k_step"].astype(np.float32))
             np.testing.assert_array_equal(u.k_xmin32[b], blk["k_xmin"].astype(np.float32))
