@@ -5,9 +5,9 @@ Default workload (N=1): BASELINE configs[4], the Llama-3-70B-shaped KV cache —
 R=128, outlier pool 32 (aux 32, paper skip_layers (0, 1)). A decode step =
 for every layer: append one token per (batch, kv head) unit (flush the
 residual window when due) + mixed-tier attention for all 64 query heads.
-Under torchrun (N>1) the batch is partitioned across ranks (whole sequences,
-all kv heads of a sequence on one rank) and head outputs are all-gathered over
-NCCL every layer.
+Under torchrun (N>1) the B x H_kv units are partitioned across ranks (contiguous
+unit ranges, GQA groups whole) and head outputs are all-gathered every layer (P2P
+stores fused into the attention epilogue, or NCCL with OTT_GATHER=nccl).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4|c3|c3s|c2|c0|c1]
   python bench.py --impl reference ...   # CPU oracle port of the reference path
@@ -137,6 +137,21 @@ def cpu_sample(wl, n_units, steps, threads, seed=0):
     return statistics.median(times) / n_units
 
 
+def workload_config(wl, world):
+    """The `config` dict both arms print (workload only; measurements go elsewhere)."""
+    U = wl.batch * wl.n_kv_heads
+    cache_gb = wl.n_layers * U * (
+        (max(0, (wl.context - wl.residual)) // wl.group_size) * (wl.group_size * wl.head_dim * wl.bits // 4
+                                                                 + 8 * wl.head_dim + 8 * wl.group_size)
+        + (wl.group_size + wl.residual + 2 * wl.outlier_num) * wl.head_dim * 4) / 1e9
+    return {"workload": wl.name, "bits": wl.bits, "layers": wl.n_layers, "batch": wl.batch,
+            "n_q_heads": wl.n_q_heads, "n_kv_heads": wl.n_kv_heads, "head_dim": wl.head_dim, "context": wl.context,
+            "group_size": wl.group_size, "residual": wl.residual, "outlier_pool": wl.outlier_num,
+            "aux_capacity": wl.aux_capacity, "skip_layers": list(wl.skip_layers),
+            "partition": f"{U} (batch x kv-head) units / {world} rank(s), contiguous, GQA groups whole",
+            "l2": "working set > L2 (126 MB): ~%.0f GB of cache" % cache_gb}
+
+
 def run_reference(args, wl, rank, world):
     if rank != 0:
         return
@@ -153,7 +168,8 @@ def run_reference(args, wl, rank, world):
         "impl": "reference", "metric": METRIC, "value": tok_s, "unit": "tokens/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64 params / f32 attention", "data": "synthetic",
-        "config": {"workload": wl.name, "layers": wl.n_layers, "batch": wl.batch, "context": wl.context},
+        "config": workload_config(wl, world),
+        "extrapolated": True, "sample_units": n_units, "units_per_step": units_per_step,
         "cpu_baseline": {"value": tok_s, "unit": "tokens/s", "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": tok_s, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
@@ -162,32 +178,83 @@ def run_reference(args, wl, rank, world):
 # ----------------------------------------------------------------------------- GPU arm
 
 
+def expected_k_halves(step64, d):
+    """The record's fp16 K step halves (sh, sl) in pair order from exact float64 steps."""
+    import numpy as np
+
+    from paper_2505_10938_b200.cache import kpair_index
+
+    step64 = np.asarray(step64, np.float64)
+    sh = step64.astype(np.float16)
+    sl = (step64 - sh.astype(np.float64)).astype(np.float16)
+    idx = kpair_index(np.arange(d), d)
+    sh_p, sl_p = np.empty(d, np.float16), np.empty(d, np.float16)
+    sh_p[idx], sl_p[idx] = sh, sl
+    return sh_p, sl_p
+
+
+def check_unit(view, ref):
+    """Bit-exact quantization state of one bench unit vs the oracle: codes, the record's K
+    step halves, V params (float32 of the exact values), pool entries (positions, scores),
+    aux positions, frozen flag."""
+    import numpy as np
+
+    d = view.config.head_dim
+    if len(view.quantized_k) != ref.n_blocks:
+        return False
+    for b in range(ref.n_blocks):
+        blk = ref.block(b)
+        if view.quantized_k[b].codes != blk["k_codes"] or view.quantized_v[b].codes != blk["v_codes"]:
+            return False
+        sh, sl = expected_k_halves(blk["k_step"], d)
+        if not (np.array_equal(view.k_sh16[b].view(np.uint16), sh.view(np.uint16))
+                and np.array_equal(view.k_sl16[b].view(np.uint16), sl.view(np.uint16))
+                and np.array_equal(view.v_step32[b], blk["v_step"].astype(np.float32))
+                and np.array_equal(view.v_xmin32[b], blk["v_xmin"].astype(np.float32))):
+            return False
+    pe, ae = ref.pool_entries(), ref.aux_entries()
+    return ([e.position for e in view.pool.entries] == pe["position"].tolist()
+            and [e.score for e in view.pool.entries] == pe["score"].tolist()
+            and [e.position for e in view.pool.aux] == ae["position"].tolist()
+            and view.pool.frozen == ref.frozen)
+
+
 def run_ours(args, wl, rank, world, local_rank):
+    import numpy as np
     import torch
     import torch.distributed as dist
 
     from paper_2505_10938_b200 import EngineConfig, OTTCache
-    from paper_2505_10938_b200.parallel import PeerGather, all_gather_heads, shard_bounds
+    from paper_2505_10938_b200.parallel import PeerGather, all_gather_heads, unit_bounds
     from paper_2505_10938_b200.workloads import decode_rows, fill_prefill
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
-    b_lo, b_hi = shard_bounds(wl.batch, world, rank)
-    B = b_hi - b_lo  # whole sequences per rank (batch x kv-head partitioning)
-    H, Hq, d, L = wl.n_kv_heads, wl.n_q_heads, wl.head_dim, wl.n_layers
+    H, Hq, d, L, nrep = wl.n_kv_heads, wl.n_q_heads, wl.head_dim, wl.n_layers, wl.n_rep
+    U = wl.batch * H
+    u_lo, u_hi = unit_bounds(U, world, rank)
+    Ul = u_hi - u_lo  # this rank's (batch x kv-head) units: one OTTCache "batch row" each
     cfg = EngineConfig(bits=wl.bits, group_size=wl.group_size, residual=wl.residual, outlier_num=wl.outlier_num,
                        aux_capacity=wl.aux_capacity, skip_layers=wl.skip_layers, n_layers=L, n_heads=H, head_dim=d)
-    total_steps = 2 * (args.warmup + args.steps) + 8
+    total_steps = 2 * (args.warmup + args.steps) + wl.group_size + 8
     max_tokens = wl.context + total_steps
-    caches = [OTTCache(cfg, B, H, max_tokens, layer=l, device=dev) for l in range(L)]
+    caches = [OTTCache(cfg, Ul, 1, max_tokens, layer=l, device=dev) for l in range(L)]
     gen = torch.Generator(device=dev).manual_seed(1000 + rank)
+    # parity sample (rank 0): units of the first layer (a paper skip layer: N = 0), the third
+    # and the last layer; their fp16 input streams are kept on the host for the oracle
+    check = rank == 0 and not args.no_parity
+    samp_layers = sorted({0, min(2, L - 1), L - 1})
+    samp = {l: sorted({(3 * l) % Ul, (Ul - 1 - 5 * l) % Ul}) for l in samp_layers} if check else {}
+    host_pre = {}
     t0 = time.time()
-    kbuf = torch.empty((B, H, wl.context, d), dtype=torch.float16, device=dev)
+    kbuf = torch.empty((Ul, 1, wl.context, d), dtype=torch.float16, device=dev)
     vbuf = torch.empty_like(kbuf)
     scales = []
     pev = []  # device time of each layer's bulk prefill (OTTCache.update = K1 over all groups)
     for l in range(L):
         scales.append(fill_prefill(gen, kbuf, vbuf))
+        for u in samp.get(l, []):
+            host_pre[(l, u)] = (kbuf[u, 0].cpu().numpy(), vbuf[u, 0].cpu().numpy())
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         caches[l].update(kbuf, vbuf)
@@ -197,27 +264,27 @@ def run_ours(args, wl, rank, world, local_rank):
     prefill_ms = sum(a.elapsed_time(b) for a, b in pev)
     # algorithmic bytes of one layer's prefill: K/V rows in, block records + pending rows out
     n_grp = (wl.context - wl.residual) // wl.group_size
-    prefill_bytes = B * H * (wl.context * d * 2 * 2 + n_grp * caches[0].record_bytes
-                             + (wl.context - n_grp * wl.group_size) * d * 2 * 2)
+    prefill_bytes = Ul * (wl.context * d * 2 * 2 + n_grp * caches[0].record_bytes
+                          + (wl.context - n_grp * wl.group_size) * d * 2 * 2)
     del kbuf, vbuf
     torch.cuda.empty_cache()
     prefill_s = time.time() - t0
 
     n_sets = 2
-    kin = torch.empty((n_sets, L, B, H, d), dtype=torch.float16, device=dev)
+    kin = torch.empty((n_sets, L, Ul, 1, d), dtype=torch.float16, device=dev)
     vin = torch.empty_like(kin)
     for s in range(n_sets):
         for l in range(L):
-            kin[s, l], vin[s, l] = decode_rows(gen, scales[l], B, H)
-    qin = torch.randn((n_sets, L, B, Hq, d), generator=gen, device=dev).half()
-    outs = torch.empty((L, B, Hq, d), dtype=torch.float16, device=dev)
+            kin[s, l], vin[s, l] = decode_rows(gen, scales[l], Ul, 1)
+    qin = torch.randn((n_sets, L, Ul, nrep, d), generator=gen, device=dev).half()
+    outs = torch.empty((L, Ul, nrep, d), dtype=torch.float16, device=dev)
     # multi-GPU head-output all-gather: P2P stores fused into the attention's combine kernel
     # (parallel.PeerGather, default) or a separate NCCL all_gather per layer (OTT_GATHER=nccl)
     gather_mode = (os.environ.get("OTT_GATHER", "p2p") if world > 1 else "none")
     pg, gather_note = None, ""
     if gather_mode == "p2p":
         try:
-            pg = PeerGather(caches, Hq)
+            pg = PeerGather(caches, nrep)
         except Exception as exc:  # no P2P mapping between these GPUs: keep the NCCL collective
             gather_mode, gather_note = "nccl", f" (P2P unavailable: {type(exc).__name__}: {str(exc)[:120]})"
         ok = torch.tensor([1 if pg is not None else 0], device=dev)
@@ -225,20 +292,29 @@ def run_ours(args, wl, rank, world, local_rank):
         if not int(ok.item()) and pg is not None:
             pg.close()
             pg, gather_mode, gather_note = None, "nccl", " (P2P unavailable on another rank)"
-    gathered = (torch.empty((L, wl.batch, Hq, d), dtype=torch.float16, device=dev)
-                if gather_mode == "nccl" else None)
-    splits = [c.splits(wl.n_rep) for c in caches]
+    gathered = (torch.empty((L, U, nrep, d), dtype=torch.float16, device=dev) if gather_mode == "nccl" else None)
+    splits = [c.splits(nrep) for c in caches]
 
     launches = {"n": 0}
+    appended = []  # decode-row set of every step, in order (oracle replay)
 
-    def step(i, ev=None):
+    def step(i, ev=None, fev=None):
         s = i % n_sets
+        appended.append(s)
+        if pg is not None:
+            pg.next_step()
         for l in range(L):
             c = caches[l]
             # the flush this token makes due (cache.py:138) never needs the token itself
-            # (R >= 1): run it first so the timed region holds the attention launches only
+            # (R >= 1): launched first, timed on its own
             if c.total_tokens + 1 - c.quantized_tokens - c.config.residual >= c.config.group_size:
+                if fev is not None:
+                    fe = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                    fe[0].record()
                 c.quantize_oldest_group()
+                if fev is not None:
+                    fe[1].record()
+                    fev.append(fe)
                 launches["n"] += 1
             if ev is not None:
                 ev[l][0].record()
@@ -255,6 +331,13 @@ def run_ours(args, wl, rank, world, local_rank):
 
     for i in range(args.warmup):
         step(i)
+    # start the timed window at a step that flushes every layer: any K timed steps then hold
+    # ceil(K / G) decode flushes per layer (cache.py:138), at least the proportional share
+    pre = 0
+    c0 = caches[0]
+    while c0.total_tokens + 1 - c0.quantized_tokens - c0.config.residual < c0.config.group_size:
+        step(args.warmup + pre)
+        pre += 1
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -263,12 +346,13 @@ def run_ours(args, wl, rank, world, local_rank):
     time.sleep(0.3)
     launches["n"] = 0
     evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(L)] for _ in range(args.steps)]
+    fevs = []
     tok_before = [(c.quantized_tokens, c.total_tokens) for c in caches]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     start.record()
     for i in range(args.steps):
-        step(args.warmup + i, evs[i])
+        step(args.warmup + pre + i, evs[i], fevs)
     end.record()
     torch.cuda.synchronize()
     if world > 1:
@@ -281,8 +365,10 @@ def run_ours(args, wl, rank, world, local_rank):
     ms = float(ms_t.item())
     ms_per_step = ms / args.steps
     value = wl.batch * args.steps / (ms / 1e3)  # whole-job decode tokens/s (all ranks)
+    last_set = appended[-1]
 
-    # roofline of the dominant kernel (attention), algorithmic bytes per launch
+    # roofline of the dominant kernel (attention): SURVEY 8(d) algorithmic bytes per launch
+    # (16-bit param accounting, cache.py:188-203); this build's layout bytes beside it
     att_ms, att_bytes, att_bytes_ref = 0.0, 0, 0
     for i in range(args.steps):
         for l in range(L):
@@ -295,10 +381,12 @@ def run_ours(args, wl, rank, world, local_rank):
             Tq = ((T - wl.residual) // wl.group_size) * wl.group_size if T >= wl.residual + wl.group_size else 0
             Tq = max(Tq, q0)
             pool_rows = min(c.N, Tq)
-            att_bytes += B * H * unit_bytes(wl, Tq, T - Tq, pool_rows)
-            att_bytes_ref += B * H * unit_bytes(wl, Tq, T - Tq, pool_rows, ref_accounting=True)
+            att_bytes += Ul * unit_bytes(wl, Tq, T - Tq, pool_rows)
+            att_bytes_ref += Ul * unit_bytes(wl, Tq, T - Tq, pool_rows, ref_accounting=True)
     avg_att_s = att_ms / n_att / 1e3
-    achieved = att_bytes / n_att / avg_att_s / 1e9
+    achieved_ref = att_bytes_ref / n_att / avg_att_s / 1e9
+    achieved_layout = att_bytes / n_att / avg_att_s / 1e9
+    flush_ms = sum(a.elapsed_time(b) for a, b in fevs)
     peak, peak_kind = peaks()
     traffic = None
     try:
@@ -310,76 +398,114 @@ def run_ours(args, wl, rank, world, local_rank):
         pass
     gpu_launches = launches["n"]
 
-    # e2e: through the public API with HOST buffers (pinned), copies inside the timed region
+    # parity of the bench's own caches (rank 0, after timing): sampled units vs the oracle fed
+    # the same fp16 rows (prefill + every appended decode row), state bit-exact and the last
+    # timed step's attention within tolerance
+    parity = None
+    if check:
+        import oracle
+
+        kin_h, vin_h, q_h = kin.cpu().numpy(), vin.cpu().numpy(), qin[last_set].cpu().numpy()
+        out_h = (outs if pg is None else torch.stack([pg.out(l).view(Ul, nrep, d) for l in range(L)])).cpu().numpy()
+        keys = [(l, u) for l in samp_layers for u in samp[l]]
+        refs = [oracle.OracleCache(wl.bits, wl.group_size, wl.residual, cfg.outlier_capacity(l), wl.aux_capacity, d)
+                for (l, u) in keys]
+        threads = len(os.sched_getaffinity(0))
+        oracle.prefill(refs, np.stack([host_pre[key][0] for key in keys]).astype(np.float32),
+                       np.stack([host_pre[key][1] for key in keys]).astype(np.float32), threads)
+        exact, worst = True, 0.0
+        for ref, (l, u) in zip(refs, keys):
+            for s in appended:
+                ref.append(kin_h[s, l, u, 0].astype(np.float32), vin_h[s, l, u, 0].astype(np.float32))
+            exact &= check_unit(caches[l].unit(u, 0), ref)
+            for r in range(nrep):
+                o_ref = ref.attend(q_h[l, u, r].astype(np.float32))
+                err = np.abs(out_h[l, u, r].astype(np.float32) - o_ref)
+                worst = max(worst, float((err / (2e-3 + 1e-2 * np.abs(o_ref))).max()))
+        parity = {"units": [f"layer{l}/unit{u_lo + u}" for (l, u) in keys], "bit_exact": bool(exact),
+                  "max_err_over_tol": worst, "tol": "2e-3 + 1e-2 |ref| (fp16 output vs oracle f32)",
+                  "checked": "K/V codes, K step halves, V params, pool entries/scores, aux, frozen; "
+                             "attention of the last timed step (all n_rep heads)"}
+
+    # e2e: through the public API with HOST buffers (pinned), copies inside the timed region;
+    # with N > 1 every rank reads back the gathered [B, H_q, d] of every layer
     e2e = None
     if not args.no_e2e:
         from paper_2505_10938_b200.pipeline import HostDecodePipeline
 
         k_h = kin[0].cpu().pin_memory()
         v_h = vin[0].cpu().pin_memory()
-        q_h = qin[0].cpu().pin_memory()
-        o_h = torch.empty((L, B, Hq, d), dtype=torch.float16).pin_memory()
+        qh = qin[0].cpu().pin_memory()
+        o_h = torch.empty((L, U if world > 1 else Ul, nrep, d), dtype=torch.float16).pin_memory()
         gather = None
         if gathered is not None:
             def gather(o_local, l):
                 all_gather_heads(o_local, out=gathered[l])
-                return gathered[l][b_lo:b_hi]
-        pipe = HostDecodePipeline(caches, Hq, gather=gather, peer_gather=pg)
-        pipe.step(k_h, v_h, q_h, o_h)  # warm-up (streams, events)
+                return gathered[l]
+        pipe = HostDecodePipeline(caches, nrep, gather=gather, peer_gather=pg, world=world)
+        pipe.step(k_h, v_h, qh, o_h)  # warm-up (streams, events)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for i in range(args.steps):
-            pipe.step(k_h, v_h, q_h, o_h)
+            pipe.step(k_h, v_h, qh, o_h)
         e1.record()
         torch.cuda.synchronize()
         e_ms = torch.tensor([e0.elapsed_time(e1)], device=dev)
         if world > 1:
             dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
-        h2d = L * (k_h[0].numel() + v_h[0].numel() + q_h[0].numel()) * 2
+        h2d = L * (k_h[0].numel() + v_h[0].numel() + qh[0].numel()) * 2
         d2h = L * o_h[0].numel() * 2
         e2e = {"value": wl.batch * args.steps / (float(e_ms.item()) / 1e3), "unit": "tokens/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+        if world > 1:  # the host copy of the last layer = an NCCL all-gather of the local rows
+            last = L - 1
+            local = pg.out(last).view(Ul, nrep, d) if pg is not None else pipe.o_d[last % 2].view(Ul, nrep, d)
+            ref = all_gather_heads(local.contiguous())
+            e2e["gathered_output_verified"] = bool(torch.equal(ref.cpu(), o_h[last]))
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = len(os.sched_getaffinity(0))
         n_units = threads
         per_unit = cpu_sample(wl, n_units, 2, threads)
-        cpu_step = per_unit * L * wl.batch * H
+        cpu_step = per_unit * L * U
         cpu = {"value": wl.batch / cpu_step, "unit": "tokens/s", "cores": threads, "kind": "port",
-               "sample": f"{n_units} units prefilled to T={wl.context}, 2 decode steps (append + {wl.n_rep} "
-                         f"attend_mixed each), extrapolated to {L * wl.batch * H} units per step"}
+               "sample": f"{n_units} units prefilled to T={wl.context}, 2 decode steps (append + {nrep} "
+                         f"attend_mixed each), extrapolated to {L * U} units per step"}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": f"u{wl.bits} codes / f32 params / f16 rows, f32 accumulate", "data": "synthetic",
-            "config": {"workload": wl.name, "bits": wl.bits, "layers": L, "batch": wl.batch, "n_q_heads": Hq, "n_kv_heads": H,
-                       "head_dim": d, "context": wl.context, "group_size": wl.group_size, "residual": wl.residual,
-                       "outlier_pool": wl.outlier_num, "aux_capacity": wl.aux_capacity,
-                       "skip_layers": list(wl.skip_layers), "partition": f"batch/{world} x all kv heads per rank",
-                       "gather": {"none": "none (1 GPU)", "nccl": "NCCL all_gather_into_tensor per layer",
-                                  "p2p": "P2P stores fused into the combine kernel + signal-pad barrier per layer"}[
-                           gather_mode] + gather_note,
-                       "l2": "working set > L2 (126 MB): %.1f GB of cache per GPU" % (
-                           sum(c.hbm_bytes() for c in caches) / 1e9),
-                       "prefill_s": round(prefill_s, 2)},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                         "kernel": "ott attend (split-K decode with fused ring write + combine)", "avg_launch_us": avg_att_s * 1e6,
-                         "bytes_per_launch": att_bytes / n_att,
-                         "achieved_ref_accounting_GBs": att_bytes_ref / n_att / avg_att_s / 1e9},
+            "vs_baseline": None, "dtype": f"u{wl.bits} codes / fp16 K-param halves + f32 V params / f16 rows, "
+                                          f"f32 accumulate", "data": "synthetic",
+            "config": workload_config(wl, world),
+            "gather": {"none": "none (1 GPU)", "nccl": "NCCL all_gather_into_tensor per layer",
+                       "p2p": "P2P stores fused into the combine kernel + signal-pad barrier per layer"}[
+                gather_mode] + gather_note,
+            "roofline": {"bound": "hbm", "achieved": achieved_ref, "peak": peak, "unit": "GB/s",
+                         "frac": achieved_ref / peak, "traffic": traffic, "peak_kind": peak_kind,
+                         "bytes": "SURVEY 8(d) algorithmic bytes (16-bit params, cache.py:188-203)",
+                         "kernel": "ott attend (split-K decode with fused ring write + combine)",
+                         "avg_launch_us": avg_att_s * 1e6, "bytes_per_launch": att_bytes_ref / n_att,
+                         "layout_bytes_per_launch": att_bytes / n_att, "achieved_layout_GBs": achieved_layout,
+                         "frac_layout": achieved_layout / peak},
+            "decode_flush": {"flushes_in_window": len(fevs),
+                             "us_per_layer_flush": flush_ms * 1e3 / len(fevs) if fevs else None,
+                             "ms_per_step_amortized": flush_ms / args.steps,
+                             "untimed_steps_before_window": args.warmup + pre},
+            "parity": parity,
             "cpu_baseline": cpu,
             "e2e": e2e,
             # bulk prefill (OTTCache.update, K1 over all groups), device-timed per layer
-            "prefill": {"ms_per_layer": prefill_ms / L, "tokens_per_s": B * H * wl.context * L / (prefill_ms / 1e3),
+            "prefill": {"ms_per_layer": prefill_ms / L, "tokens_per_s": Ul * wl.context * L / (prefill_ms / 1e3),
                         "achieved_GBs": prefill_bytes * L / (prefill_ms / 1e3) / 1e9,
                         "frac": prefill_bytes * L / (prefill_ms / 1e3) / 1e9 / peak,
-                        "bytes_per_layer": prefill_bytes, "tokens": "per (b, kv-head) unit"},
+                        "bytes_per_layer": prefill_bytes, "tokens": "per (b, kv-head) unit",
+                        "wall_s": round(prefill_s, 2)},
             "gpu_launches": gpu_launches,
             "clocks": clk,
         }
@@ -460,6 +586,7 @@ def main():
     ap.add_argument("--config", default="c4")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-parity", action="store_true", help="skip the oracle check of sampled bench units")
     ap.add_argument("--bits", type=int, default=2, help="code width of the cache (BASELINE: 2)")
     ap.add_argument("--layers", type=int, default=0, help="override the workload's layer count (variants)")
     args = ap.parse_args()

@@ -23,19 +23,24 @@ from .errors import ContractViolation
 
 class HostDecodePipeline:
     """Runs `step(k_h, v_h, q_h, out_h)` for caches[0..L): per layer l, append
-    (k_h[l], v_h[l]) [B, H_kv, d] and attend q_h[l] [B, H_q, d] -> out_h[l].
+    (k_h[l], v_h[l]) [B, H_kv, d] and attend q_h[l] [B, H_q, d] -> out_h[l] ([world * B,
+    H_q, d] with a gather: every rank's head outputs).
     Host tensors must be pinned fp16. Work is enqueued on the current stream;
     `step` returns without waiting (use `torch.cuda.current_stream().synchronize()`
     or the returned event)."""
 
-    def __init__(self, caches, n_q_heads: int, gather=None, peer_gather=None):
+    def __init__(self, caches, n_q_heads: int, gather=None, peer_gather=None, world: int = 1):
         if not caches:
             raise ContractViolation("need at least one layer cache")
         c0 = caches[0]
         self.caches = list(caches)
         self.device = c0.device
-        self.gather = gather  # optional callable(out_local, layer) -> tensor to read back (multi-GPU)
-        self.peer_gather = peer_gather  # optional parallel.PeerGather: all-gather fused into the attention
+        # multi-GPU: the step reads back every rank's rows ([world * batch, H_q, d] per layer),
+        # all-gathered by `gather` (callable(out_local, layer) -> gathered rows, NCCL) or by
+        # `peer_gather` (parallel.PeerGather: P2P stores fused into the attention)
+        self.gather = gather
+        self.peer_gather = peer_gather
+        self.world = world if (gather is not None or peer_gather is not None) else 1
         B, H, d = c0.batch, c0.n_kv_heads, c0.config.head_dim
         if n_q_heads % H:
             raise ContractViolation("H_q must be a multiple of n_kv_heads")
@@ -44,6 +49,7 @@ class HostDecodePipeline:
         self.v_d = [torch.empty((B, H, d), **kw) for _ in range(2)]
         self.q_d = [torch.empty((B, n_q_heads, d), **kw) for _ in range(2)]
         self.o_d = [torch.empty((B, n_q_heads, d), **kw) for _ in range(2)]
+        self.out_shape = (B * self.world, n_q_heads, d)
         self.h2d = torch.cuda.Stream(self.device)
         self.d2h = torch.cuda.Stream(self.device)
         self.splits = [c.splits(n_q_heads // H) for c in self.caches]
@@ -60,8 +66,10 @@ class HostDecodePipeline:
         self._check(k_h, (L, *self.k_d[0].shape), "k_h")
         self._check(v_h, (L, *self.v_d[0].shape), "v_h")
         self._check(q_h, (L, *self.q_d[0].shape), "q_h")
-        self._check(out_h, (L, *self.o_d[0].shape), "out_h")
+        self._check(out_h, (L, *self.out_shape), "out_h")
         main = torch.cuda.current_stream(self.device)
+        if self.peer_gather is not None:
+            self.peer_gather.next_step()  # the other slot of the symmetric gather buffer
         start = torch.cuda.Event()
         start.record(main)
         loaded = [torch.cuda.Event() for _ in range(L)]
@@ -91,7 +99,7 @@ class HostDecodePipeline:
             self.launches += 2 + (1 if c.quantized_tokens != before else 0)
             if self.peer_gather is not None:
                 self.peer_gather.wait(l)  # every rank's rows are in this rank's gather buffer
-                src = out_d
+                src = self.peer_gather.gathered(l)
             else:
                 src = out_d if self.gather is None else self.gather(out_d, l)
             computed[l].record(main)

@@ -100,7 +100,7 @@ def test_peer_gather_symmetric_memory_world1():
         q = torch.from_numpy(rng.standard_normal((B, Hkv * n_rep, d)).astype(np.float16)).cuda()
         for c in caches:
             c.update(k, v)
-        pg = PeerGather(caches, Hkv * n_rep)
+        pg = PeerGather(caches, n_rep)
         for l, c in enumerate(caches):
             c.attend(q, out=pg.out(l))
             pg.wait(l)

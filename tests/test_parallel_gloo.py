@@ -85,23 +85,24 @@ def test_peer_destinations_assemble_the_all_gather(world):
 
     L, b_local, hq, d = 3, 2, 4, 8
     row_bytes = hq * d * 2
-    size = L * b_local * world * row_bytes
+    size = 2 * L * b_local * world * row_bytes  # two step slots
     bases = [(p + 1) << 32 for p in range(world)]  # distinct fake device addresses
     mem = [np.zeros(size, np.uint8) for _ in range(world)]
     rng = np.random.default_rng(world)
-    outs = rng.integers(0, 256, (world, L, b_local * row_bytes), dtype=np.uint8)
-    for r in range(world):
-        for l in range(L):
-            local = gather_row_offset(l, r, b_local, world, hq, d)
-            mem[r][local:local + b_local * row_bytes] = outs[r, l]
-            dests = peer_destinations(bases, r, l, b_local, hq, d)
-            assert len(dests) == world - 1
-            for a in dests:
-                p = (a >> 32) - 1
-                assert p != r
-                off = a - bases[p]
-                assert off == local
-                mem[p][off:off + b_local * row_bytes] = outs[r, l]
-    want = np.concatenate([outs[:, l].reshape(-1) for l in range(L)])
+    outs = rng.integers(0, 256, (2, world, L, b_local * row_bytes), dtype=np.uint8)
+    for slot in range(2):
+        for r in range(world):
+            for l in range(L):
+                local = gather_row_offset(l, r, b_local, world, hq, d, slot, L)
+                mem[r][local:local + b_local * row_bytes] = outs[slot, r, l]
+                dests = peer_destinations(bases, r, l, b_local, hq, d, slot, L)
+                assert len(dests) == world - 1
+                for a in dests:
+                    p = (a >> 32) - 1
+                    assert p != r
+                    off = a - bases[p]
+                    assert off == local
+                    mem[p][off:off + b_local * row_bytes] = outs[slot, r, l]
+    want = np.concatenate([outs[s, :, l].reshape(-1) for s in range(2) for l in range(L)])
     for p in range(world):
         np.testing.assert_array_equal(mem[p], want)
