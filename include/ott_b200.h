@@ -163,8 +163,10 @@ int ott_append_attend(const ott_cache_t* c, const uint16_t* k, const uint16_t* v
                       int32_t n_splits, void* stream);
 
 /* One decode step with the token counts in device memory, so a whole model step can be
- * captured in a CUDA graph and replayed: counters = int64[2] {quantized_tokens,
- * total_tokens} on the device, read by the kernels and advanced by the last one.
+ * captured in a CUDA graph and replayed: counters = int64[3] {quantized_tokens,
+ * total_tokens, error} on the device, read by the kernels and advanced by the last one;
+ * a step that makes a flush due with no group record left sets error = 1 and leaves the
+ * counts unchanged (the host raises ContractViolation when it reads the flag).
  * Launches: ring write of (k, v) [n_units][head_dim] at position total, flush of one
  * group per unit iff it became due (cache.py:138; the kernel returns early otherwise),
  * split-K attention of q [n_units*n_rep][head_dim] -> out, and the combine. n_splits

@@ -7,7 +7,7 @@ produced and consumed by the sm_100a kernels in ``csrc/`` via the C ABI in
 ``libott_b200.so`` every method raises.
 
 HBM layout per unit (u = b * H_kv + h), see DESIGN.md §3:
-  blocks     uint8 [U, max_groups, record]  K codes | V codes | K step,x_min f32[d] | V step,x_min f32[G]
+  blocks     uint8 [U, max_groups, record]  K codes | V codes | K step halves | V step,x_min f32[G] | K e hi/lo
   pend_k/v   fp16  [U, G+R, d]              pending ring, slot = position % (G+R)
   pool_*     slot-stable pool.entries (pos, score f64, K/V rows fp16), aux ledger, meta
   pool_mask  uint32 [U, max_tokens/32]      1 bit per position currently in pool.entries
@@ -176,7 +176,7 @@ class OTTCache:
         self.total_tokens = 0
         self.quantized_tokens = 0
         # device copy of (quantized_tokens, total_tokens) for graph-capturable decode steps
-        self.counters = torch.zeros(2, dtype=torch.int64, device=dev)
+        self.counters = torch.zeros(3, dtype=torch.int64, device=dev)  # quantized, total, error
         self._ws = None
         self._ws_key = None
 
@@ -319,7 +319,13 @@ class OTTCache:
     @_on_device
     def sync_counters(self) -> None:
         """Copy the host token counts into `counters` (before capturing `decode_step`)."""
-        self.counters.copy_(torch.tensor([self.quantized_tokens, self.total_tokens], dtype=torch.int64))
+        self.counters.copy_(torch.tensor([self.quantized_tokens, self.total_tokens, 0], dtype=torch.int64))
+
+    def device_error(self) -> None:
+        """Raise if a device-counter step ran out of group records (the combine kernel sets
+        counters[2] and stops advancing; the host mirror normally refuses such a step first)."""
+        if int(self.counters[2].item()):
+            raise ContractViolation("cache capacity (max_tokens) exceeded in a device-counter decode step")
 
     @_on_device
     def decode_step(self, k: torch.Tensor, v: torch.Tensor, q: torch.Tensor, out: torch.Tensor,

@@ -1624,6 +1624,22 @@ __device__ __forceinline__ void store_out2(const ott_cache_t& c, uint16_t* out, 
   for (int i = 0; i < c.n_out_peers; ++i) *reinterpret_cast<__half2*>(c.out_peer[i] + off) = v;
 }
 
+// Device-counter step (counters = {quantized, total, error}): the append made a flush due
+// (cache.py:138) and the flush kernel ran it, unless the cache is out of group records: then
+// the flush was skipped, the step's new row overwrote a pending row, and the counts stop
+// advancing with the error flag set (OTTCache.decode_step / device_error raise it on the host).
+__device__ __forceinline__ void advance_counts(int64_t* cnt, int G, int R, int max_groups) {
+  const int64_t qt = cnt[0], tot = cnt[1] + 1;
+  if (tot - qt - R >= G) {
+    if (qt / G + 1 > max_groups) {
+      cnt[2] = 1;
+      return;
+    }
+    cnt[0] = qt + G;
+  }
+  cnt[1] = tot;
+}
+
 template <int D>
 __global__ void __launch_bounds__(32 * kCombineRows) combine_kernel(const float* __restrict__ ws,
                                                                    uint16_t* __restrict__ out, int n_rows,
@@ -1665,22 +1681,15 @@ __global__ void __launch_bounds__(32 * kCombineRows) combine_kernel(const float*
         }
         const float inv = 1.f / Lt;
         for (int k = 0; k < 4; ++k) store_out(gd.c, out, (size_t)urow * D + lane + 32 * k, f2h(At[k] * inv));
-        if (dev_counts && blockIdx.x == 0 && threadIdx.x == 0) {
-          const int64_t qt = dev_counts[0], tot = dev_counts[1] + 1;
-          if (tot - qt - R >= G && qt / G + 1 <= max_groups) dev_counts[0] = qt + G;
-          dev_counts[1] = tot;
-        }
+        if (dev_counts && blockIdx.x == 0 && threadIdx.x == 0) advance_counts(dev_counts, G, R, max_groups);
         return;
       }
     }
   }
   const int lane = threadIdx.x & 31;
   const int ur = blockIdx.x * kCombineRows + (threadIdx.x >> 5);  // unit*NR + r
-  if (dev_counts && blockIdx.x == 0 && threadIdx.x == 0) {  // last kernel of a device-counter step: advance
-    const int64_t qt = dev_counts[0], tot = dev_counts[1] + 1;
-    if (tot - qt - R >= G && qt / G + 1 <= max_groups) dev_counts[0] = qt + G;
-    dev_counts[1] = tot;
-  }
+  // last kernel of a device-counter step: advance the counts
+  if (dev_counts && blockIdx.x == 0 && threadIdx.x == 0) advance_counts(dev_counts, G, R, max_groups);
   if (ur >= n_rows) return;
   if constexpr (D == 0) {  // generic head_dim: lane-strided columns
     const float* base = ws + (size_t)ur * n_splits * (d + 2);

@@ -773,8 +773,31 @@ def test_device_counter_decode_step_and_graph():
         ref = host.attend(q, n_splits=3)
         dev.decode_step(k, v, q, out, n_splits=3)
         assert torch.equal(out, ref), i
-        assert dev.counters.tolist() == [host.quantized_tokens, host.total_tokens]
+        assert dev.counters.tolist() == [host.quantized_tokens, host.total_tokens, 0]
     assert torch.equal(dev.blocks, host.blocks) and torch.equal(dev.pool_pos, host.pool_pos)
+    dev.device_error()  # no error flag
+
+    # out of group records on the device (the host check bypassed): the combine flags it and
+    # the counts stop advancing
+    from paper_2505_10938_b200 import ContractViolation, _native
+
+    small = OTTCache(cfg_of(2, 32, 32, 4, 32, d), B, H, max_tokens=T)
+    small.update(torch.from_numpy(pre_k).cuda(), torch.from_numpy(pre_v).cuda())
+    small.sync_counters()
+    ws = small.workspace(n_rep, 3)
+    before = None
+    for i in range(120):
+        k, v = (torch.from_numpy(rng.standard_normal((B, H, d)).astype(np.float16)).cuda() for _ in range(2))
+        _native.check(_native.lib().ott_decode_step(small._cref, k.data_ptr(), v.data_ptr(), q.data_ptr(),
+                                                    out.data_ptr(), n_rep, small.counters.data_ptr(), ws.data_ptr(),
+                                                    3, torch.cuda.current_stream().cuda_stream))
+        cnt = small.counters.tolist()
+        if cnt[2]:
+            before = before or cnt
+            assert cnt[:2] == before[:2]
+    assert before is not None
+    with pytest.raises(ContractViolation):
+        small.device_error()
 
     cfg = DecoderConfig(n_layers=3, hidden=512, n_heads=4, n_kv_heads=4, head_dim=128, mlp=1024, vocab=1000)
     prompt = torch.randint(0, cfg.vocab, (2, 300), generator=torch.Generator().manual_seed(4)).cuda()
