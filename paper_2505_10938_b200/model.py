@@ -71,7 +71,15 @@ class Decoder:
     """Random-init decoder; `generate(prompt, steps)` = prefill + greedy decode."""
 
     def __init__(self, cfg: DecoderConfig, batch: int, max_tokens: int, kv: str = "ott",
-                 ott: EngineConfig | None = None, device=None, seed: int = 0):
+                 ott: EngineConfig | None = None, device=None, seed: int = 0, k_outliers: int = 0,
+                 track_exact: bool = False):
+        """k_outliers > 0: per kv head, that many seeded outlier channels in the cached keys (an
+        offset of 6x the channel's spread with a tight spread around it), missing on a seeded 1%
+        of token ids (outlier tokens); plain random-init keys are isotropic, so 2-bit schemes
+        would all look alike. track_exact: keep an fp16 shadow of every K/V row and,
+        in eager decode steps, record the reference's fidelity metric (cli.py:208-218): per step
+        the mean over (layer, batch, head) of the L1 distance between the cache's attention
+        output and exact float32 attention over the same rows (`attn_l1`)."""
         if kv not in ("ott", "fp16"):
             raise ContractViolation("kv must be 'ott' or 'fp16'")
         self.cfg, self.batch, self.max_tokens, self.kv = cfg, batch, max_tokens, kv
@@ -84,14 +92,27 @@ class Decoder:
 
         self.embed = w(cfg.vocab, D)
         self.layers = []
+        self.k_struct = []
         for _ in range(cfg.n_layers):
+            wqkv = w(D, (H + 2 * Hkv) * d)
+            if k_outliers:
+                # outlier-channel structure of the cache input (made one-sided
+                # as massive-activation channels are): per kv head, k_outliers channels carry a
+                # large offset (6x the channel's natural spread) with a tight spread around it;
+                # "outlier tokens" (a seeded 1% of the vocabulary, e.g. sink-like tokens) lack it
+                # (x0.05), so they stretch their group's quantization range (PAPER.md motivation)
+                ch = torch.rand((Hkv, d), generator=g, device=dev).argsort(dim=1)[:, :k_outliers]
+                cols = (H * d + torch.arange(Hkv, device=dev)[:, None] * d + ch).reshape(-1)
+                spread = wqkv[:, cols].float().norm(dim=0)  # std of norm(x) @ w_c
+                self.k_struct.append((ch, (6.0 * spread).view(Hkv, k_outliers)))
             self.layers.append({
-                "wqkv": w(D, (H + 2 * Hkv) * d), "wo": w(H * d, D), "wgu": w(D, 2 * cfg.mlp), "wd": w(cfg.mlp, D),
+                "wqkv": wqkv, "wo": w(H * d, D), "wgu": w(D, 2 * cfg.mlp), "wd": w(cfg.mlp, D),
                 "n1": torch.ones(D, dtype=torch.float16, device=dev), "n2": torch.ones(D, dtype=torch.float16, device=dev),
             })
         self.norm = torch.ones(D, dtype=torch.float16, device=dev)
         self.lm_head = w(D, cfg.vocab)
         self.cos, self.sin = rope_tables(d, max_tokens, cfg.rope_theta, dev)
+        self.special = (torch.rand(cfg.vocab, generator=g, device=dev) < 0.01) if k_outliers else None
         if kv == "ott":
             ott = ott or EngineConfig(bits=2, group_size=32, residual=128, outlier_num=32, aux_capacity=32,
                                       n_layers=cfg.n_layers, n_heads=Hkv, head_dim=d)
@@ -101,6 +122,11 @@ class Decoder:
             self.v_cache = torch.zeros_like(self.k_cache)
         self.pos = 0
         self.graph = None
+        self.track_exact = track_exact and kv == "ott"
+        self.attn_l1 = []
+        if self.track_exact:
+            self.sk = torch.zeros((cfg.n_layers, batch, Hkv, max_tokens, d), dtype=torch.float16, device=dev)
+            self.sv = torch.zeros_like(self.sk)
 
     # ------------------------------------------------------------------ blocks
     def _qkv(self, x, lw, pos0, cos=None, sin=None):
@@ -115,6 +141,26 @@ class Decoder:
         if cos is None:
             cos, sin = self.cos[pos0:pos0 + T], self.sin[pos0:pos0 + T]
         return apply_rope(q, cos, sin), apply_rope(k, cos, sin), v.contiguous()
+
+    def _apply_kstruct(self, l, k, tok):
+        """k [B, Hkv, (T,) d] post-RoPE in place: outlier channels -> offset + 0.1 k, or 0.05 k for
+        the outlier tokens `tok` ([B] or [B, T] ids)."""
+        if not self.k_struct:
+            return
+        ch, off = self.k_struct[l]
+        sp = self.special[tok].to(k.dtype)  # [B] or [B, T]
+        B, Hkv = k.shape[0], k.shape[1]
+        idx = ch.view(1, Hkv, -1)
+        if k.dim() == 4:
+            kc = k.gather(3, idx[:, :, None, :].expand(B, Hkv, k.shape[2], -1)).float()
+            spb = sp[:, None, :, None].float()
+            new = spb * 0.05 * kc + (1 - spb) * (off[None, :, None, :] + 0.1 * kc)
+            k.scatter_(3, idx[:, :, None, :].expand(B, Hkv, k.shape[2], -1), new.to(k.dtype))
+        else:
+            kc = k.gather(2, idx.expand(B, Hkv, -1)).float()
+            spb = sp[:, None, None].float()
+            new = spb * 0.05 * kc + (1 - spb) * (off[None] + 0.1 * kc)
+            k.scatter_(2, idx.expand(B, Hkv, -1), new.to(k.dtype))
 
     def _mlp(self, x, lw):
         h = rms_norm(x, lw["n2"], self.cfg.eps) @ lw["wgu"]
@@ -136,11 +182,16 @@ class Decoder:
         rep = cfg.n_heads // cfg.n_kv_heads
         for l, lw in enumerate(self.layers):
             q, k, v = self._qkv(x, lw, 0)
+            k = k.contiguous()
+            self._apply_kstruct(l, k, tokens)
             kk = k.repeat_interleave(rep, dim=1) if rep > 1 else k
             vv = v.repeat_interleave(rep, dim=1) if rep > 1 else v
             o = F.scaled_dot_product_attention(q, kk, vv, is_causal=True)
             if self.kv == "ott":
                 self.caches[l].update(k.contiguous(), v)
+                if self.track_exact:
+                    self.sk[l, :, :, :T] = k
+                    self.sv[l, :, :, :T] = v
             else:
                 self.k_cache[l, :, :, :T] = k
                 self.v_cache[l, :, :, :T] = v
@@ -165,7 +216,7 @@ class Decoder:
             }
         return self._dbuf
 
-    def _layers_step(self, x, pos_host: int, pos_dev=None, graph: bool = False):
+    def _layers_step(self, x, pos_host: int, pos_dev=None, graph: bool = False, tok=None):
         """One decode step over all layers on the residual stream x [B, D] (updated in
         place): fused RMSNorm / RoPE+split / SiLU-gate kernels (ott_model.h), cuBLAS
         GEMMs with the residual adds in their epilogues (addmm_), and the OTT cache
@@ -175,11 +226,14 @@ class Decoder:
         bf = self._decode_buffers()
         h, qkv, q, k, v, o, gu, act = (bf[n] for n in ("h", "qkv", "q", "k", "v", "o", "gu", "act"))
         pos_ptr = pos_dev.data_ptr() if pos_dev is not None else None
+        l1_sum = 0.0
         for l, lw in enumerate(self.layers):
             _native.check(lib.ott_model_rmsnorm(x.data_ptr(), lw["n1"].data_ptr(), h.data_ptr(), B, D, cfg.eps, st))
             torch.mm(h, lw["wqkv"], out=qkv)
             _native.check(lib.ott_model_rope_qkv(qkv.data_ptr(), self.cos.data_ptr(), self.sin.data_ptr(), pos_ptr,
                                                  pos_host, q.data_ptr(), k.data_ptr(), v.data_ptr(), B, H, Hkv, d, st))
+            if self.k_struct:
+                self._apply_kstruct(l, k, tok)
             if self.kv == "ott":
                 c = self.caches[l]
                 if graph:
@@ -187,6 +241,8 @@ class Decoder:
                 else:
                     c.append(k, v)
                     c.attend(q, out=o)
+                    if self.track_exact:
+                        l1_sum += self._exact_l1(l, k, v, q, o, pos_host)
             else:
                 p = pos_host
                 self.k_cache[l, :, :, p] = k
@@ -203,7 +259,24 @@ class Decoder:
             x.addmm_(act, lw["wd"])
         _native.check(lib.ott_model_rmsnorm(x.data_ptr(), self.norm.data_ptr(), h.data_ptr(), B, D, cfg.eps, st))
         torch.mm(h, self.lm_head, out=bf["logits"])
+        if self.track_exact and not graph:
+            self.attn_l1.append(float(l1_sum) / cfg.n_layers)
         return bf["logits"]
+
+    def _exact_l1(self, l, k, v, q, o, p):
+        """Mean over (batch, head) of sum_d |o - exact| for layer l at position p: exact float32
+        attention (attend_full_precision, attention.py:35-59) over the fp16 shadow rows."""
+        cfg = self.cfg
+        self.sk[l, :, :, p] = k
+        self.sv[l, :, :, p] = v
+        rep = cfg.n_heads // cfg.n_kv_heads
+        kk = self.sk[l, :, :, : p + 1].float()
+        vv = self.sv[l, :, :, : p + 1].float()
+        if rep > 1:
+            kk, vv = kk.repeat_interleave(rep, dim=1), vv.repeat_interleave(rep, dim=1)
+        s = torch.einsum("bhd,bhtd->bht", q.float(), kk) / float(cfg.head_dim) ** 0.5
+        ex = torch.einsum("bht,bhtd->bhd", torch.softmax(s.double(), dim=-1).float(), vv)
+        return (o.float() - ex).abs().sum(-1).mean()
 
     @torch.no_grad()
     def decode(self, tokens: torch.Tensor) -> torch.Tensor:
@@ -211,7 +284,7 @@ class Decoder:
         if self.pos + 1 > self.max_tokens:
             raise ContractViolation("decoder is full")
         x = self.embed.index_select(0, tokens)
-        logits = self._layers_step(x, self.pos)
+        logits = self._layers_step(x, self.pos, tok=tokens)
         self.pos += 1
         self.last_logits = logits.clone()
         return logits.argmax(-1)
@@ -221,7 +294,7 @@ class Decoder:
         """One decode step on static buffers: token ids g_tok, position g_pos (device),
         OTT decode steps with device token counters; writes g_next, advances g_pos."""
         self.g_x.copy_(self.embed.index_select(0, self.g_tok))
-        logits = self._layers_step(self.g_x, 0, pos_dev=self.g_pos, graph=True)
+        logits = self._layers_step(self.g_x, 0, pos_dev=self.g_pos, graph=True, tok=self.g_tok)
         self.g_logits.copy_(logits)
         self.g_next.copy_(logits.argmax(-1))
         self.g_pos.add_(1)
