@@ -563,8 +563,9 @@ def run_c1(args, rank, world, local_rank):
     random prompt, 256 greedy decode steps with the OTT cache (2-bit, G=32, R=128,
     pool 32, paper skip_layers (0, 1)); the fp16-KV-cache decoder with the same
     weights is timed beside it. Replicas only under torchrun (each rank its own batch).
-    The K projections carry 4 seeded x15 outlier channels per kv head (config 0's
-    structure; isotropic random-init keys would make every 2-bit scheme look alike)."""
+    The throughput runs use the plain random-init model; the fidelity runs (c1_fidelity) add
+    the outlier-channel / outlier-token key structure (isotropic random-init keys would make
+    every 2-bit scheme look alike)."""
     import torch
 
     from paper_2505_10938_b200.model import LLAMA2_7B, Decoder
@@ -582,8 +583,7 @@ def run_c1(args, rank, world, local_rank):
         # the run, so every K/V row stays in the fp16 tier (a plain fp16 KV cache)
         lossless = EngineConfig(bits=2, group_size=32, residual=T + steps + 64, outlier_num=0,
                                 n_layers=LLAMA2_7B.n_layers, n_heads=LLAMA2_7B.n_kv_heads, head_dim=LLAMA2_7B.head_dim)
-        m = Decoder(LLAMA2_7B, B, T + steps + 8, kv="ott", ott=None if kv == "ott" else lossless, device=dev, seed=0,
-                    k_outliers=k_out)
+        m = Decoder(LLAMA2_7B, B, T + steps + 8, kv="ott", ott=None if kv == "ott" else lossless, device=dev, seed=0)
         torch.cuda.synchronize()
         t0 = time.time()
         tok = m.prefill(prompt)
@@ -612,7 +612,8 @@ def run_c1(args, rank, world, local_rank):
             "unit": "tokens/s", "n_gpus": world, "steps": steps, "warmup": args.warmup,
             "ms_per_step": res["ott"]["ms_per_step"], "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f16 weights/activations, u2 KV codes",
-            "data": "synthetic (random ids, random-init N(0, 0.02) weights, 4 x15 K outlier channels per kv head)",
+            "data": "synthetic (random ids, random-init N(0, 0.02) weights; fidelity runs: + outlier-channel / "
+                    "outlier-token key structure, model.Decoder(k_outliers=4))",
             "config": {"workload": "config1-llama2-7b-B8-prompt2048-decode%d" % steps, "batch": B, "prompt": T,
                        "layers": LLAMA2_7B.n_layers, "parallelism": f"replicas x{world}", "decode": "CUDA graph per step"},
             "fp16_kv_baseline": {"value": res["fp16"]["tok_s"] * world, "ms_per_step": res["fp16"]["ms_per_step"],
