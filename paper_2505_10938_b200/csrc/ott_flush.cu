@@ -889,6 +889,14 @@ __device__ __forceinline__ double h_val(uint16_t b) { return (double)__half2floa
 // decides between v and the next fp16 value (false is returned, and quant_code is used per
 // element, if fp16 values there are closer than 4 margin). t[levels-1] = x_max: T_levels lies
 // within float64 rounding below x_max (line_params) and x_max has code levels (quant.py:101).
+// The rare case of code_thresholds: the fp16 ceiling v of T lies within the margin of T, so the
+// float64 quotient at v decides. Out of line, so the division is not if-converted into every call.
+__device__ __noinline__ uint16_t threshold_tie(uint16_t vb, double dv, double mn, double step, int k, double margin,
+                                               bool& ok) {
+  const uint16_t nb = h_next(vb);
+  if (h_val(nb) - dv <= 4.0 * margin) ok = false;
+  return floor(__ddiv_rn(__dsub_rn(dv, mn), step)) >= (double)k ? vb : nb;
+}
 __device__ __forceinline__ bool code_thresholds(uint16_t* t, float mnf, float mxf, double mn, double step, double inv,
                                                 int levels, double eps) {
   (void)inv;
@@ -905,11 +913,7 @@ __device__ __forceinline__ bool code_thresholds(uint16_t* t, float mnf, float mx
     uint16_t vb = __half_as_ushort(__float2half_ru(__double2float_ru(T)));  // smallest fp16 >= T (or +inf)
     if ((vb & 0x7C00u) != 0x7C00u) {
       const double dv = h_val(vb);
-      if (dv - T <= margin) {
-        const uint16_t nb = h_next(vb);
-        if (h_val(nb) - dv <= 4.0 * margin) ok = false;
-        if (!(floor(__ddiv_rn(__dsub_rn(dv, mn), step)) >= (double)k)) vb = nb;
-      }
+      if (dv - T <= margin) vb = threshold_tie(vb, dv, mn, step, k, margin, ok);
     }
     if ((vb & 0x7C00u) == 0x7C00u || h_val(vb) > (double)mxf) vb = mxb;
     t[k - 1] = vb;
@@ -932,6 +936,27 @@ __device__ __forceinline__ uint32_t codes_h2(__half2 x, const __half2* th) {
   return *reinterpret_cast<const uint32_t*>(&c) & 0x00030003u;
 }
 
+// V codes of token row vr (16-byte chunks swizzled by sw) with the per-element float64 recipe:
+// the rare path of lines without exact fp16 thresholds, out of line (instruction cache)
+__device__ __noinline__ void frozen_v_codes_slow(const uint4* vr, int sw, float fmn, float fmx, double mn, double step,
+                                                 double inv, int levels, double eps, uint4* vcodes) {
+  uint32_t w[8];
+  for (int j = 0; j < 16; ++j) {
+    const uint4 r = vr[j ^ sw];
+    const __half2* h = reinterpret_cast<const __half2*>(&r);
+    uint32_t bits = 0;
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = __half22float2(h[e]);
+      bits |= ((uint32_t)quant_code(f.x, fmn, fmx, mn, step, inv, levels, eps) << (4 * e)) |
+              ((uint32_t)quant_code(f.y, fmn, fmx, mn, step, inv, levels, eps) << (4 * e + 2));
+    }
+    if (j & 1) w[j / 2] |= bits << 16;
+    else w[j / 2] = bits;
+  }
+  vcodes[0] = make_uint4(w[0], w[1], w[2], w[3]);
+  vcodes[1] = make_uint4(w[4], w[5], w[6], w[7]);
+}
+
 constexpr int kFrozenWarps = 4;
 #ifndef OTT_FROZEN_PAIR  // 1: two warps per group in the 2-bit kernel (K rows / V rows), 8 KB of rows each
 #define OTT_FROZEN_PAIR 1
@@ -951,7 +976,9 @@ struct FrozenPairSmem {  // per warp: the K or the V rows of its group
 // are exact for fp16 inputs, / G, rounded to float32) before quantization. The substituted
 // values are float32, so these lines use the float32 fast path / float64 fallback per element
 // instead of fp16 thresholds. `sel` bit t = token t substituted.
-__device__ __forceinline__ void frozen_group_subst(uint8_t* rec, double* p64, const uint16_t* sk, const uint16_t* sv,
+// out of line: substituted groups are rare, and inlined into both warp roles this path more
+// than doubled the kernel (instruction-cache misses were its top stall)
+__device__ __noinline__ void frozen_group_subst(uint8_t* rec, double* p64, const uint16_t* sk, const uint16_t* sv,
                                                 float* vmean, uint32_t sel, int lane, int32_t* meta3, int part) {
   constexpr int D = 128, G = 32, kLevels = 3;
   const RecordLayout L(D, G, 2);
@@ -1120,7 +1147,7 @@ __device__ __forceinline__ void frozen_group_subst(uint8_t* rec, double* p64, co
 }
 
 
-__global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen_kernel(ott_cache_t c, int64_t q0, int n_groups,
+__global__ void __launch_bounds__(32 * kFrozenWarps, 6) flush_frozen_kernel(ott_cache_t c, int64_t q0, int n_groups,
                                                                          int64_t ring_end,
                                                                          const uint16_t* __restrict__ in_k,
                                                                          const uint16_t* __restrict__ in_v,
@@ -1156,6 +1183,17 @@ __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen_kernel(ott_cac
   {
     const int bslot = base % cap, ring_end32 = (int)ring_end, in_first32 = (int)in_first;
     const int ch = lane & 15;
+    if (base >= ring_end32) {  // bulk prefill: every row of the group comes from the input
+      const size_t off = (size_t)u * in_stride + (size_t)(base - in_first32 + (lane >> 4)) * D + ch * 8;
+      const uint16_t* pk = in_k + off;
+      const uint16_t* pv = in_v + off;
+#pragma unroll 4
+      for (int it = 0; it < G / 2; ++it) {
+        const int row = 2 * it + (lane >> 4);
+        if (part != 1) cp_async16(sk + row * D + ch * 8, pk + (size_t)it * 2 * D);
+        if (part != 0) cp_async16(sv + row * D + ((ch ^ (row & 15)) * 8), pv + (size_t)it * 2 * D);
+      }
+    } else
 #pragma unroll 4
     for (int it = 0; it < G / 2; ++it) {
       const int row = 2 * it + (lane >> 4);
@@ -1295,29 +1333,23 @@ __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen_kernel(ott_cac
     __half2 th[kLevels];
 #pragma unroll
     for (int k = 0; k < kLevels; ++k) th[k] = __half2half2(__ushort_as_half(thr[k]));
-    uint32_t w[D / 16];
-#pragma unroll
-    for (int j = 0; j < D / 8; ++j) {  // chunk j = channels 8j..8j+7 -> half of word j / 2
-      const uint4 r = vr[j ^ sw];
-      const __half2* h = reinterpret_cast<const __half2*>(&r);
-      uint32_t bits = 0;
-      if (exact) {
-        bits = codes4(codes_h2_raw(h[0], th), codes_h2_raw(h[1], th)) |
-               (codes4(codes_h2_raw(h[2], th), codes_h2_raw(h[3], th)) << 8);
-      } else {
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float2 f = __half22float2(h[e]);
-          bits |= ((uint32_t)quant_code_slow(f.x, fmn, fmx, mn, step, inv, kLevels, eps) << (4 * e)) |
-                  ((uint32_t)quant_code_slow(f.y, fmn, fmx, mn, step, inv, kLevels, eps) << (4 * e + 2));
-        }
-      }
-      if (j & 1) w[j / 2] |= bits << 16;
-      else w[j / 2] = bits;
-    }
     uint4* vcodes = reinterpret_cast<uint4*>(rec + L.v_codes() + t * (D / 4));
-    vcodes[0] = make_uint4(w[0], w[1], w[2], w[3]);
-    vcodes[1] = make_uint4(w[4], w[5], w[6], w[7]);
+    if (exact) {
+      uint32_t w[D / 16];
+#pragma unroll
+      for (int j = 0; j < D / 8; ++j) {  // chunk j = channels 8j..8j+7 -> half of word j / 2
+        const uint4 r = vr[j ^ sw];
+        const __half2* h = reinterpret_cast<const __half2*>(&r);
+        const uint32_t bits = codes4(codes_h2_raw(h[0], th), codes_h2_raw(h[1], th)) |
+                              (codes4(codes_h2_raw(h[2], th), codes_h2_raw(h[3], th)) << 8);
+        if (j & 1) w[j / 2] |= bits << 16;
+        else w[j / 2] = bits;
+      }
+      vcodes[0] = make_uint4(w[0], w[1], w[2], w[3]);
+      vcodes[1] = make_uint4(w[4], w[5], w[6], w[7]);
+    } else {  // a line without exact thresholds: the float64 recipe per element, out of line
+      frozen_v_codes_slow(vr, sw, fmn, fmx, mn, step, inv, kLevels, eps, vcodes);
+    }
   }
   note_step_max(meta3, fmaxf(kst_max, vst));
 }
