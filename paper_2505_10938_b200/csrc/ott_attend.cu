@@ -481,6 +481,38 @@ __device__ __forceinline__ void load_record_head(uint32_t dst, const CUtensorMap
     tma_tensor_rows(dst + b * RecHead<G>::kBoxRows * 32, map,
                     (int)(rec_index * RecHead<G>::kRecRows + b * RecHead<G>::kBoxRows), bar);
 }
+// Warp-collective issue of the async copies (all lanes call, elect.sync picks one): the
+// operands are warp-uniform values, so they stay in uniform registers (no per-lane issue loop).
+__device__ __forceinline__ void elect_arrive_expect(uint32_t bar, uint32_t bytes) {
+  asm volatile(
+      "{\n .reg .pred p;\n elect.sync _|p, 0xffffffff;\n"
+      "@p mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n}\n" ::"r"(bar), "r"(bytes)
+      : "memory");
+}
+__device__ __forceinline__ void elect_tma_rows(uint32_t dst, const CUtensorMap* map, int row, uint32_t bar) {
+  asm volatile(
+      "{\n .reg .pred p;\n elect.sync _|p, 0xffffffff;\n"
+      "@p cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n}\n" ::"r"(
+          dst),
+      "l"(map), "r"(0), "r"(row), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void elect_bulk_copy(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile(
+      "{\n .reg .pred p;\n elect.sync _|p, 0xffffffff;\n"
+      "@p cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n}\n" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+template <int G>
+__device__ __forceinline__ void warp_load_record_head(uint32_t dst, const CUtensorMap* map, int64_t rec_index,
+                                                      uint32_t bar) {
+  elect_arrive_expect(bar, MmaSmem<G>::kHead);
+#pragma unroll
+  for (int b = 0; b < RecHead<G>::kBoxes; ++b)
+    elect_tma_rows(dst + b * RecHead<G>::kBoxRows * 32, map,
+                   (int)(rec_index * RecHead<G>::kRecRows + b * RecHead<G>::kBoxRows), bar);
+}
 __device__ __forceinline__ void bulk_copy(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
@@ -539,24 +571,25 @@ __device__ void mma_body(const AttnArgs& a, const Counts& n, const CUtensorMap* 
   const int64_t unit_rec = (int64_t)u * c.max_groups;  // record index of group 0
   const size_t rec_bytes = (size_t)L.bytes();
   // e fields of the warp's groups k0 .. k0 + 7 into the batch buffer (one bulk copy each)
-  auto load_ebatch = [&](int k0) {
+  auto load_ebatch = [&](int k0) {  // whole warp
     const int nb = min(8, my_n - k0);
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(ebar), "r"(nb * 4 * D) : "memory");
+    elect_arrive_expect(ebar, nb * 4 * D);
     for (int j = 0; j < nb; ++j)
-      bulk_copy(ebuf0 + j * kES,
-                c.blocks + (size_t)(unit_rec + g0 + warp + (k0 + j) * kAttnWarps) * rec_bytes + L.k_e(), 4 * D,
-                ebar);
+      elect_bulk_copy(ebuf0 + j * kES,
+                      c.blocks + (size_t)(unit_rec + g0 + warp + (k0 + j) * kAttnWarps) * rec_bytes + L.k_e(), 4 * D,
+                      ebar);
   };
   if (lane == 0) {
 #pragma unroll
     for (int s = 0; s < kStages; ++s) mbar_init(bar0 + 8 * s, 1);
     mbar_init(ebar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-#pragma unroll
-    for (int s = 0; s < kStages; ++s)
-      if (s < my_n) load_record_head<G>(stage0 + s * kHead, tmap, unit_rec + g0 + warp + s * kAttnWarps, bar0 + 8 * s);
-    if (my_n > 0) load_ebatch(0);
   }
+  __syncwarp();
+#pragma unroll
+  for (int s = 0; s < kStages; ++s)
+    if (s < my_n) warp_load_record_head<G>(stage0 + s * kHead, tmap, unit_rec + g0 + warp + s * kAttnWarps, bar0 + 8 * s);
+  if (my_n > 0) load_ebatch(0);
   // q * u(m) as exact fp16 pairs (channels 16w+m, 16w+m+8) of head g, words w = tig + 4 hw:
   // the B operand of the bias MMA, and the q' = q u step split starts from it
   __half2 q16[2][8];
@@ -629,7 +662,7 @@ __device__ void mma_body(const AttnArgs& a, const Counts& n, const CUtensorMap* 
       eb0 = (acc[0] + acc[2]) * (kEScale * scale);
       eb1 = (acc[1] + acc[3]) * (kEScale * scale);
       __syncwarp();
-      if (lane == 0 && k + 8 < my_n) {
+      if (k + 8 < my_n) {
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         load_ebatch(k + 8);
       }
@@ -781,9 +814,9 @@ __device__ void mma_body(const AttnArgs& a, const Counts& n, const CUtensorMap* 
 
     // ---- release the stage: prefetch the record head of group k + kStages
     __syncwarp();
-    if (lane == 0 && k + kStages < my_n) {
+    if (k + kStages < my_n) {
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      load_record_head<G>(rec_s, tmap, unit_rec + gi + kStages * kAttnWarps, bar0 + 8 * st);
+      warp_load_record_head<G>(rec_s, tmap, unit_rec + gi + kStages * kAttnWarps, bar0 + 8 * st);
     }
   }
 
