@@ -207,6 +207,9 @@ struct FpSmem {
 // barrier over warps 0-3 only (the tcgen05 kernel's fifth warp does not take part)
 __device__ __forceinline__ void sync4() { asm volatile("bar.sync 1, 128;\n" ::: "memory"); }
 
+__device__ __forceinline__ void cp_async16_s(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
+}
 __device__ __forceinline__ void tma_row(uint32_t dst, const void* src, uint32_t bar) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 256, [%2];\n" ::"r"(dst),
@@ -244,20 +247,13 @@ __device__ void fp_body(const AttnArgs& a, const Counts& n, FpSmem& sm) {
     reinterpret_cast<uint4*>(&sm.kr[warp][0][0])[i] = make_uint4(0, 0, 0, 0);
     reinterpret_cast<uint4*>(&sm.vr[warp][0][0])[i] = make_uint4(0, 0, 0, 0);
   }
-  const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&sm.bar[warp]);
   const uint32_t kr_s = (uint32_t)__cvta_generic_to_shared(&sm.kr[warp][0][0]);
   const uint32_t vr_s = (uint32_t)__cvta_generic_to_shared(&sm.vr[warp][0][0]);
-  if (lane == 0) {
-    mbar_init(bar, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
   if (a.new_k) {  // fused ring write (cache.py:134-135): this CTA alone reads the pending tier
     if (tid < 2 * D / 8) {
       const size_t dst = ((size_t)u * cap + (size_t)((n.total_tokens - 1) % cap)) * D + (tid % (D / 8)) * 8;
       const uint16_t* src = (tid < D / 8 ? a.new_k : a.new_v) + (size_t)u * D + (tid % (D / 8)) * 8;
       *reinterpret_cast<uint4*>((tid < D / 8 ? c.pend_k : c.pend_v) + dst) = *reinterpret_cast<const uint4*>(src);
-      asm volatile("fence.proxy.async.global;\n" ::: "memory");  // visible to this CTA's TMA reads
     }
     sync4();
   }
@@ -270,7 +266,6 @@ __device__ void fp_body(const AttnArgs& a, const Counts& n, FpSmem& sm) {
   // ldmatrix lane addressing (row, byte column) for K (non-trans) and V (trans)
   const int k_row = (lane & 7) + ((lane >> 3) & 1) * 8, k_col = (lane >> 4) * 16;
   const int v_row = (lane & 7) + ((lane >> 4) & 1) * 8, v_col = ((lane >> 3) & 1) * 16;
-  uint32_t phase = 0;
 
   // the fp-tier CTAs of a unit (n_fsplits of them) interleave the 16-row tiles warp by warp
   const int f = (int)blockIdx.y - a.n_qsplits;
@@ -288,26 +283,29 @@ __device__ void fp_body(const AttnArgs& a, const Counts& n, FpSmem& sm) {
         valid[h] = 16 * (t - n_pool_t) + r < Tp;
       }
     }
-    if (lane == 0) {
+    {  // stage the tile's rows: 16-byte cp.async per lane (lane = chunk lane % 16 of rows 2 it + lane / 16)
       const int rows = is_pool ? min(16, N - 16 * t) : min(16, Tp - 16 * (t - n_pool_t));
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(rows * 512)
-                   : "memory");
-      // ring slot of the tile's first pending row, then consecutive slots (one modulo per tile)
-      int slot = is_pool ? 0 : (int)((n.q_tokens + 16 * (t - n_pool_t)) % cap);
-      for (int r = 0; r < rows; ++r) {
-        size_t off;
-        if (is_pool) {
-          off = ((size_t)u * N + 16 * t + r) * D;
-        } else {
-          off = ((size_t)u * cap + (size_t)slot) * D;
-          slot = slot + 1 == cap ? 0 : slot + 1;
+      // ring slot of the tile's first pending row (one modulo per tile); cap >= 32 > 16 rows
+      const int slot0 = is_pool ? 0 : (int)((n.q_tokens + 16 * (t - n_pool_t)) % cap);
+      const int ch = lane & 15;
+#pragma unroll
+      for (int it = 0; it < 8; ++it) {
+        const int r = 2 * it + (lane >> 4);
+        if (r < rows) {
+          size_t off;
+          if (is_pool) {
+            off = ((size_t)u * N + 16 * t + r) * D;
+          } else {
+            const int sl = slot0 + r >= cap ? slot0 + r - cap : slot0 + r;
+            off = ((size_t)u * cap + (size_t)sl) * D;
+          }
+          cp_async16_s(kr_s + r * kRow + 16 * ch, (is_pool ? c.pool_k : c.pend_k) + off + 8 * ch);
+          cp_async16_s(vr_s + r * kRow + 16 * ch, (is_pool ? c.pool_v : c.pend_v) + off + 8 * ch);
         }
-        tma_row(kr_s + r * kRow, (is_pool ? c.pool_k : c.pend_k) + off, bar);
-        tma_row(vr_s + r * kRow, (is_pool ? c.pool_v : c.pend_v) + off, bar);
       }
+      asm volatile("cp.async.wait_all;\n" ::: "memory");
+      __syncwarp();
     }
-    mbar_wait(bar, phase);
-    phase ^= 1u;
 
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -357,8 +355,7 @@ __device__ void fp_body(const AttnArgs& a, const Counts& n, FpSmem& sm) {
       ldsm_x4_t(av, vr_s + v_row * kRow + 32 * j + v_col);
       mma16816(o[j], av[0], av[1], av[2], av[3], b0, b1);
     }
-    __syncwarp();
-    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    __syncwarp();  // the next tile's cp.async overwrites the staging rows
   }
 
 #pragma unroll
