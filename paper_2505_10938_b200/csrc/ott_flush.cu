@@ -922,6 +922,23 @@ __device__ __forceinline__ bool code_thresholds(uint16_t* t, float mnf, float mx
   return ok;
 }
 
+// 2-bit codes of two fp16 inputs as bit masks (16-bit all-ones / zero halves): with t1 <= t2 <= t3,
+// code(x) = [x >= t1] + [x >= t2] + [x >= t3], so its high bit is b1 = [x >= t2] and its low bit
+// b0 = [x >= (b1 ? t3 : t1)]: two mask compares and one select per two inputs
+struct CodeMasks {
+  uint32_t b0, b1;
+};
+__device__ __forceinline__ CodeMasks code_masks(__half2 x, const uint32_t* th) {
+  const uint32_t b1 = __hge2_mask(x, *reinterpret_cast<const __half2*>(&th[1]));
+  const uint32_t ts = (b1 & th[2]) | (~b1 & th[0]);
+  return {__hge2_mask(x, *reinterpret_cast<const __half2*>(&ts)), b1};
+}
+// OR the two codes of m into acc: low-half input at bits LO, LO + 1, high-half input at HI, HI + 1
+template <int LO, int HI>
+__device__ __forceinline__ uint32_t put_codes(uint32_t acc, const CodeMasks& m) {
+  constexpr uint32_t c0 = (1u << LO) | (1u << (16 + HI)), c1 = c0 << 1;
+  return acc | (m.b0 & c0) | (m.b1 & c1);
+}
 // codes of two fp16 inputs against per-lane thresholds th[0..2]: code at bits 0-1 (low half)
 // and 16-17 (high half). Each compare gives 1.0 or 0.0; 1024 + code is exact in fp16.
 // the same as fp16 bits 1024 + code (bytes: code, 0x64, code', 0x64), unmasked
@@ -1274,17 +1291,19 @@ __global__ void __launch_bounds__(32 * kFrozenWarps, 6) flush_frozen_kernel(ott_
     for (int j = 0; j < 4; ++j) store_k_e2(rec, L, 4 * lane + j, ke[j]);
     uint8_t* kcodes = rec + L.k_codes() + lane;  // byte (t d + 4 lane) / 4 holds channels 4 lane..+3 of token t
     if (exact) {
-      __half2 t01[kLevels], t23[kLevels];
+      uint32_t t01[kLevels], t23[kLevels];  // thresholds of channels (0, 1) and (2, 3) as half2 words
 #pragma unroll
       for (int k = 0; k < kLevels; ++k) {
-        t01[k] = __halves2half2(__ushort_as_half(thr[0][k]), __ushort_as_half(thr[1][k]));
-        t23[k] = __halves2half2(__ushort_as_half(thr[2][k]), __ushort_as_half(thr[3][k]));
+        t01[k] = (uint32_t)thr[0][k] | ((uint32_t)thr[1][k] << 16);
+        t23[k] = (uint32_t)thr[2][k] | ((uint32_t)thr[3][k] << 16);
       }
 #pragma unroll 4
       for (int t = 0; t < G; ++t) {
         const uint2 r = kr[t * (D / 4)];
-        kcodes[t * (D / 4)] = (uint8_t)codes4(codes_h2_raw(*reinterpret_cast<const __half2*>(&r.x), t01),
-                                              codes_h2_raw(*reinterpret_cast<const __half2*>(&r.y), t23));
+        // channel j of the lane at bits 2j, 2j + 1 of the byte (pack order)
+        uint32_t acc = put_codes<0, 2>(0u, code_masks(*reinterpret_cast<const __half2*>(&r.x), t01));
+        acc = put_codes<4, 6>(acc, code_masks(*reinterpret_cast<const __half2*>(&r.y), t23));
+        kcodes[t * (D / 4)] = (uint8_t)(acc | (acc >> 16));
       }
     } else {  // a line without exact thresholds (extreme range): the float64 recipe per element
       for (int t = 0; t < G; ++t) {
@@ -1330,9 +1349,9 @@ __global__ void __launch_bounds__(32 * kFrozenWarps, 6) flush_frozen_kernel(ott_
       p64[2 * D + t] = mn;
       p64[2 * D + G + t] = step;
     }
-    __half2 th[kLevels];
+    uint32_t th[kLevels];
 #pragma unroll
-    for (int k = 0; k < kLevels; ++k) th[k] = __half2half2(__ushort_as_half(thr[k]));
+    for (int k = 0; k < kLevels; ++k) th[k] = (uint32_t)thr[k] * 0x00010001u;
     uint4* vcodes = reinterpret_cast<uint4*>(rec + L.v_codes() + t * (D / 4));
     if (exact) {
       uint32_t w[D / 16];
@@ -1340,10 +1359,13 @@ __global__ void __launch_bounds__(32 * kFrozenWarps, 6) flush_frozen_kernel(ott_
       for (int j = 0; j < D / 8; ++j) {  // chunk j = channels 8j..8j+7 -> half of word j / 2
         const uint4 r = vr[j ^ sw];
         const __half2* h = reinterpret_cast<const __half2*>(&r);
-        const uint32_t bits = codes4(codes_h2_raw(h[0], th), codes_h2_raw(h[1], th)) |
-                              (codes4(codes_h2_raw(h[2], th), codes_h2_raw(h[3], th)) << 8);
-        if (j & 1) w[j / 2] |= bits << 16;
-        else w[j / 2] = bits;
+        // channels 8j + 2e (low half) and 8j + 2e + 1 (high half) at field bits 4e and 4e + 2
+        uint32_t acc = put_codes<0, 2>(0u, code_masks(h[0], th));
+        acc = put_codes<4, 6>(acc, code_masks(h[1], th));
+        acc = put_codes<8, 10>(acc, code_masks(h[2], th));
+        acc = put_codes<12, 14>(acc, code_masks(h[3], th));
+        if (j & 1) w[j / 2] |= (acc + (acc << 16)) & 0xFFFF0000u;
+        else w[j / 2] = (acc + (acc >> 16)) & 0xFFFFu;
       }
       vcodes[0] = make_uint4(w[0], w[1], w[2], w[3]);
       vcodes[1] = make_uint4(w[4], w[5], w[6], w[7]);

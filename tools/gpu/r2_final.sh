@@ -8,6 +8,6 @@ timeout 120 python tools/prof_attend.py --batch 128 --rep 8 --ctx 16384 --iters 
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:attend_mma -s 1 -c 1 -o gpurun_out/r2f/ncu_attend \
   python tools/prof_attend.py --batch 128 --rep 8 --ctx 16384 --iters 2 > gpurun_out/r2f/ncu_attend.log 2>&1
 timeout 900 python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --no-parity > gpurun_out/r2f/bench_small.json 2>&1 && \
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"attend|flush|ring_write|combine" -c 1200 --csv \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"^flush_kernel|attend_mma|combine|ring_write" -c 2000 --csv \
   --log-file gpurun_out/r2f/launches.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --no-parity > gpurun_out/r2f/ncu_launch.log 2>&1
 timeout 120 python tools/prof_peer_wait.py > gpurun_out/r2f/peer_wait.log 2>&1
