@@ -27,7 +27,15 @@ constexpr int kFlushThreads = 256;
 // quant.py:59-102 for one line held in registers/smem by ONE thread.
 // levels = 2^bits - 1. Returns step.
 __device__ __forceinline__ void line_params(double mn, double mx, double levels, double& step_out) {
-  double step = __ddiv_rn(__dsub_rn(mx, mn), levels);  // quant.py:64
+  const double range = __dsub_rn(mx, mn);
+  double step;
+  if (levels == 3.0) {  // RN(range / 3) by Markstein's FMA correction of RN(range * RN(1/3)): exact
+    const double c = 1.0 / 3.0;
+    const double q0 = __dmul_rn(range, c);
+    step = __fma_rn(__fma_rn(-q0, 3.0, range), c, q0);
+  } else {
+    step = __ddiv_rn(range, levels);  // quant.py:64
+  }
   // quant.py:68-69: while step > 0 and x_min + levels*step > x_max: nextafter(step, 0)
   while (step > 0.0 && __dadd_rn(mn, __dmul_rn(levels, step)) > mx)
     step = __longlong_as_double(__double_as_longlong(step) - 1);
@@ -891,11 +899,25 @@ __device__ __forceinline__ double h_val(uint16_t b) { return (double)__half2floa
 // within float64 rounding below x_max (line_params) and x_max has code levels (quant.py:101).
 // The rare case of code_thresholds: the fp16 ceiling v of T lies within the margin of T, so the
 // float64 quotient at v decides. Out of line, so the division is not if-converted into every call.
-__device__ __noinline__ uint16_t threshold_tie(uint16_t vb, double dv, double mn, double step, int k, double margin,
-                                               bool& ok) {
+__device__ __noinline__ bool quotient_ge(double dv, double mn, double step, int k) {
+  return floor(__ddiv_rn(__dsub_rn(dv, mn), step)) >= (double)k;
+}
+// For k = 1, 2 without the division: fl(d / step) >= k iff d / step >= k (1 - 2^-54), the
+// rounding boundary below k (a tie rounds to the even k). d = dv - mn is exact, and here it lies
+// within (1 +- 1e-8) k step (dv - T <= margin, |mn| <= 6144 step for fp16 lines), so d - k step
+// is exact (Sterbenz) and k step is exact: the comparison is exact.
+__device__ __forceinline__ uint16_t threshold_tie(uint16_t vb, double dv, double mn, double step, int k, double margin,
+                                                  bool& ok) {
   const uint16_t nb = h_next(vb);
   if (h_val(nb) - dv <= 4.0 * margin) ok = false;
-  return floor(__ddiv_rn(__dsub_rn(dv, mn), step)) >= (double)k ? vb : nb;
+  bool ge;
+  if (k <= 2) {
+    const double ks = __dmul_rn((double)k, step);
+    ge = __dsub_rn(__dsub_rn(dv, mn), ks) >= -ks * 0x1p-54;
+  } else {
+    ge = quotient_ge(dv, mn, step, k);
+  }
+  return ge ? vb : nb;
 }
 __device__ __forceinline__ bool code_thresholds(uint16_t* t, float mnf, float mxf, double mn, double step, double inv,
                                                 int levels, double eps) {
