@@ -122,7 +122,7 @@ __device__ __forceinline__ uint16_t f2h(float f) { return __half_as_ushort(__flo
 // |t| <= (65504 + 4 * 65504) / 8 for any fp16 input (1-bit steps included), so t never
 // overflows fp16.
 __device__ __forceinline__ void store_k_e2(uint8_t* rec, const RecordLayout& L, int c, float e) {
-  const float t = e / (kEScale * kpair_u(c % 8));
+  const float t = e * (1.f / (kEScale * kpair_u(c % 8)));  // 8 u is a power of two: the same value as e / (8 u)
   const __half hi = __float2half_rn(t);
   const __half lo = __float2half_rn(t - __half2float(hi));
   uint16_t* eh = reinterpret_cast<uint16_t*>(rec + L.k_e());

@@ -601,6 +601,19 @@ __global__ void __launch_bounds__(kFlushThreads, OTT_FLUSH_MIN_BLOCKS) flush_ker
 //   * codes come from the same float32 fast path / float64 fallback as flush_kernel, so the
 //     results are bit-identical.
 // 16-byte global -> shared copy without a register round trip
+// (unit, group) of a flat work item: 32-bit division when the item count allows (the 64-bit
+// division routine is ~3x the instructions)
+__device__ __forceinline__ void split_item(int64_t item, int64_t total, int n_groups, int& u, int& g) {
+  if (total <= 0xffffffffLL) {
+    const uint32_t it = (uint32_t)item, q = it / (uint32_t)n_groups;
+    u = (int)q;
+    g = (int)(it - q * (uint32_t)n_groups);
+  } else {
+    u = (int)(item / n_groups);
+    g = (int)(item % n_groups);
+  }
+}
+
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
   const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gsrc) : "memory");
@@ -617,7 +630,8 @@ __global__ void __launch_bounds__(128) flush_score_kernel(ott_cache_t c, int64_t
   const int lane = threadIdx.x & 31;
   const int64_t item = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
   if (item >= (int64_t)c.n_units * n_groups) return;
-  const int u = (int)(item / n_groups), g = (int)(item % n_groups);
+  int u, g;
+  split_item(item, (int64_t)c.n_units * n_groups, n_groups, u, g);
   if (c.pool_meta[(size_t)u * 4 + 2]) return;  // frozen: nothing will read the scores
   const int cap = G + c.residual;
   const int base = (int)(q0 + (int64_t)g * G), p = base + lane;
@@ -1199,7 +1213,8 @@ __global__ void __launch_bounds__(32 * kFrozenWarps, 6) flush_frozen_kernel(ott_
   const int64_t item = OTT_FROZEN_PAIR ? ((int64_t)blockIdx.x * kFrozenWarps + warp) >> 1
                                        : (int64_t)blockIdx.x * kFrozenWarps + warp;
   if (item >= (int64_t)c.n_units * n_groups) return;
-  const int u = (int)(item / n_groups), g = (int)(item % n_groups);
+  int u, g;
+  split_item(item, (int64_t)c.n_units * n_groups, n_groups, u, g);
   const int cap = G + c.residual;
   const int base = (int)(q0 + (int64_t)g * G);
   const int64_t gi = base / G;
@@ -1421,7 +1436,8 @@ __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen4_kernel(ott_ca
   const int part = warp & 1;
   const int64_t item = ((int64_t)blockIdx.x * kFrozenWarps + warp) >> 1;
   if (item >= (int64_t)c.n_units * n_groups) return;
-  const int u = (int)(item / n_groups), g = (int)(item % n_groups);
+  int u, g;
+  split_item(item, (int64_t)c.n_units * n_groups, n_groups, u, g);
   const int cap = G + c.residual;
   const int base = (int)(q0 + (int64_t)g * G);
   const int64_t gi = base / G;
