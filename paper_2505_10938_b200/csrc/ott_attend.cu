@@ -544,7 +544,8 @@ constexpr float kMinit = -1e30f;  // finite initial running max (the first group
 //   * online softmax with the running max folded into the bias, lazily rescaled.
 //   * O^T += V^T P' with V codes as exact fp16 subnormals and P' = 4 p step in fp16.
 template <int NR, int G>
-__device__ void mma_body(const AttnArgs& a, const Counts& n, const CUtensorMap* tmap, MmaSmem<G>& sm) {
+__device__ void mma_body(const AttnArgs& a, const Counts& n, const CUtensorMap* tmap, MmaSmem<G>& sm, int u, int split,
+                         int nparts) {
   constexpr int D = 128;
   constexpr int kHead = MmaSmem<G>::kHead;
   constexpr int kMt = G / 16;  // 16-token m-tiles per group
@@ -552,14 +553,13 @@ __device__ void mma_body(const AttnArgs& a, const Counts& n, const CUtensorMap* 
   constexpr int kES = MmaSmem<G>::kEStride;
   const RecordLayout L(D, G);
   const ott_cache_t& c = a.c;
-  const int u = blockIdx.x, split = blockIdx.y;
   const int tid = threadIdx.x, lane = tid & 31;
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);  // warp-uniform for the compiler
   const int g = lane >> 2, tig = lane & 3;
 
   const uint32_t magic = a.k_magic;
   const int n_groups = (int)(n.q_tokens / G);
-  const int per = (n_groups + a.n_qsplits - 1) / a.n_qsplits;
+  const int per = (n_groups + nparts - 1) / nparts;
   const int g0 = split * per;
   const int g1 = min(n_groups, g0 + per);
   const int my_n = g1 > g0 + warp ? (g1 - g0 - warp + kAttnWarps - 1) / kAttnWarps : 0;
@@ -870,6 +870,13 @@ __device__ void mma_body(const AttnArgs& a, const Counts& n, const CUtensorMap* 
       base[1] = Lsum;
     }
   }
+  if (nparts < a.n_qsplits) {  // a whole unit of the tail schedule: its other quantized slots are empty
+    for (int i = threadIdx.x; i < NR * (a.n_qsplits - nparts); i += kAttnThreads) {
+      float* base = a.ws + (((size_t)u * NR + i % NR) * a.n_splits + nparts + i / NR) * (D + 2);
+      base[0] = -INFINITY;
+      base[1] = 0.f;
+    }
+  }
 }
 
 
@@ -878,13 +885,25 @@ __global__ void __launch_bounds__(kAttnThreads, OTT_MMA_MIN_BLOCKS)
     attend_mma_kernel(const __grid_constant__ AttnArgs a, const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(256) unsigned char smem_raw[];
   allow_dependents();
-  if ((int)blockIdx.y >= a.n_qsplits) {  // full-precision tiers: pool + pending
+  // (unit, partial slot, pieces of the unit's quantized range) of this CTA
+  int u = blockIdx.x, y = blockIdx.y, nparts = a.n_qsplits;
+  if (a.tail_units > 0) {  // 1-D grid: [whole units][tail units x n_qsplits pieces][fp-tier CTAs]
+    const int U = a.c.n_units, W = U - a.tail_units, P = a.tail_units * a.n_qsplits, i = blockIdx.x;
+    if (i < W) {
+      u = i, y = 0, nparts = 1;
+    } else if (i < W + P) {
+      u = W + (i - W) / a.n_qsplits, y = (i - W) % a.n_qsplits;
+    } else {
+      u = (i - W - P) % U, y = a.n_qsplits + (i - W - P) / U;
+    }
+  }
+  if (y >= a.n_qsplits) {  // full-precision tiers: pool + pending
     const Counts n = counts_of(a);
-    if (blockIdx.x == 0 && blockIdx.y == a.n_qsplits && threadIdx.x == 0)  // token counts for the combine's guard
+    if (u == 0 && y == a.n_qsplits && threadIdx.x == 0)  // token counts for the combine's guard
       reinterpret_cast<int64_t*>(a.ws + (size_t)a.c.n_units * NR * a.n_splits * 130)[0] = n.q_tokens;
-    fp_body<NR>(a, n, *reinterpret_cast<FpSmem*>(smem_raw));
+    fp_body<NR>(a, n, *reinterpret_cast<FpSmem*>(smem_raw), u, y);
   } else {
-    mma_body<NR, G>(a, counts_of(a), &tmap, *reinterpret_cast<MmaSmem<G>*>(smem_raw));
+    mma_body<NR, G>(a, counts_of(a), &tmap, *reinterpret_cast<MmaSmem<G>*>(smem_raw), u, y, nparts);
   }
 }
 
@@ -1247,7 +1266,7 @@ __global__ void __launch_bounds__(kAttnThreads, 4)
     const Counts n = counts_of(a);
     if (blockIdx.x == 0 && blockIdx.y == a.n_qsplits && threadIdx.x == 0)  // token counts for the combine's guard
       reinterpret_cast<int64_t*>(a.ws + (size_t)a.c.n_units * NR * a.n_splits * 130)[0] = n.q_tokens;
-    fp_body<NR>(a, n, *reinterpret_cast<FpSmem*>(smem_raw));
+    fp_body<NR>(a, n, *reinterpret_cast<FpSmem*>(smem_raw), blockIdx.x, blockIdx.y);
   } else {
     mma4_body<NR, GR>(a, counts_of(a), &tmap, *reinterpret_cast<Mma4Smem*>(smem_raw));
   }
@@ -1554,7 +1573,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
     const Counts n = counts_of(a);
     if (blockIdx.x == 0 && blockIdx.y == a.n_qsplits && threadIdx.x == 0)  // token counts for the combine's guard
       reinterpret_cast<int64_t*>(a.ws + (size_t)a.c.n_units * NR * a.n_splits * 130)[0] = n.q_tokens;
-    fp_body<NR>(a, n, *reinterpret_cast<FpSmem*>(smem_raw));
+    fp_body<NR>(a, n, *reinterpret_cast<FpSmem*>(smem_raw), blockIdx.x, blockIdx.y);
   } else {
     mma8_body<NR, GR>(a, counts_of(a), &tmap, *reinterpret_cast<Mma8Smem*>(smem_raw));
   }
@@ -1955,7 +1974,10 @@ static cudaError_t launch_mma_t(const AttnArgs& a, cudaStream_t st) {
   cudaError_t e =
       cudaFuncSetAttribute(attend_mma_kernel<NR, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  attend_mma_kernel<NR, G><<<dim3(a.c.n_units, a.n_splits), kAttnThreads, smem, st>>>(a, tmap);
+  const dim3 grid = a.tail_units > 0 ? dim3(a.c.n_units - a.tail_units + a.c.n_units * a.n_fsplits +
+                                                a.tail_units * a.n_qsplits)
+                                         : dim3(a.c.n_units, a.n_splits);
+  attend_mma_kernel<NR, G><<<grid, kAttnThreads, smem, st>>>(a, tmap);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   return launch_combine<128>(a, NR, st, true);
@@ -1965,6 +1987,9 @@ bool mma_eligible(const ott_cache_t& c) {
   return c.head_dim == 128 && code_bits(c.bits, c.head_dim, c.group_size) == 2 &&
          (c.group_size == 32 || c.group_size == 64 || c.group_size == 128);
 }
+#ifndef OTT_TAIL_SPLIT  // tail schedule of the 2-bit tensor-core kernel (AttnArgs.tail_units)
+#define OTT_TAIL_SPLIT 1
+#endif
 #ifndef OTT_FP_SPLIT  // allow two full-precision-tier CTAs per unit (tensor-core kernels)
 #define OTT_FP_SPLIT 1
 #endif
@@ -2003,6 +2028,7 @@ cudaError_t launch_attend(const ott_cache_t& c, const uint16_t* q, uint16_t* out
   a.n_rtiles = (int)((total - q_tokens + 31) / 32);
   a.scale_log2 = kLog2e / sqrtf((float)c.head_dim);
   a.k_magic = 0x3C003C00u;
+  a.tail_units = 0;
   const int D = c.head_dim, G = c.group_size;
   if ((D != 64 && D != 128) || G % 32) {  // shapes outside the fast kernels' tiling
     if (n_rep == 1) return launch_generic_t<1>(a, st);
@@ -2033,6 +2059,10 @@ cudaError_t launch_attend(const ott_cache_t& c, const uint16_t* q, uint16_t* out
     const int64_t w2 = ((int64_t)c.n_units * (n_qsplits + 2) + slots - 1) / slots;
     a.n_fsplits = (OTT_FP_SPLIT && per < 96 && fp_tiles >= 6 && w2 == w1) ? 2 : 1;
     a.n_splits = n_qsplits + a.n_fsplits;
+    // more units than resident CTAs (config 4: 1,024 on 592): one wave of whole units, the rest
+    // cut into n_qsplits pieces, then the short fp-tier CTAs: the launch ends on small work items
+    if (OTT_TAIL_SPLIT && mma_eligible(c) && n_qsplits >= 2 && c.n_units > slots)
+      a.tail_units = (int)(c.n_units - slots);
   }
 #define OTT_GCASE(FN, NRv, Gv) \
   if (n_rep == NRv && G == Gv) return FN<NRv, Gv>(a, st);

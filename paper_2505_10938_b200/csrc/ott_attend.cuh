@@ -49,6 +49,9 @@ struct AttnArgs {
                                      // the pending ring (slot (total-1) % (G+R)) by the fp-tier CTA
   bool advance;                      // device-counter mode: the combine advances the counts (false
                                      // for all but the last head chunk of n_rep > 8)
+  int tail_units;                    // > 0 (2-bit tensor-core kernel): 1-D grid of [whole units]
+                                     // [the last tail_units units cut into n_qsplits pieces each]
+                                     // [fp-tier CTAs]: small work items finish the launch
 };
 
 // Token counts of one launch. Host mode: the launch arguments. Device-counter mode
@@ -217,11 +220,11 @@ __device__ __forceinline__ void tma_row(uint32_t dst, const void* src, uint32_t 
       : "memory");
 }
 
+// (u, split) = unit and partial slot of this CTA: split - n_qsplits is its fp-tier index
 template <int NR>
-__device__ void fp_body(const AttnArgs& a, const Counts& n, FpSmem& sm) {
+__device__ void fp_body(const AttnArgs& a, const Counts& n, FpSmem& sm, int u, int split) {
   constexpr int D = 128, kRow = FpSmem::kRow;
   const ott_cache_t& c = a.c;
-  const int u = blockIdx.x, split = blockIdx.y;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, tig = lane & 3;
   const int N = c.capacity, cap = c.group_size + c.residual;
@@ -268,7 +271,7 @@ __device__ void fp_body(const AttnArgs& a, const Counts& n, FpSmem& sm) {
   const int v_row = (lane & 7) + ((lane >> 4) & 1) * 8, v_col = ((lane >> 3) & 1) * 16;
 
   // the fp-tier CTAs of a unit (n_fsplits of them) interleave the 16-row tiles warp by warp
-  const int f = (int)blockIdx.y - a.n_qsplits;
+  const int f = split - a.n_qsplits;
   for (int t = warp + kAttnWarps * f; t < n_tiles; t += kAttnWarps * a.n_fsplits) {
     const bool is_pool = t < n_pool_t;
     // row validity of this lane's two rows (g, g+8)

@@ -16,6 +16,7 @@ cudaError_t launch_attend(const ott_cache_t& c, const uint16_t* q, uint16_t* out
                           int64_t total, float* ws, int n_splits, cudaStream_t st, int64_t* dev_counts = nullptr,
                           const uint16_t* new_k = nullptr, const uint16_t* new_v = nullptr, bool advance = true);
 bool attend_fuses_ring_write(const ott_cache_t& c);
+bool mma_eligible(const ott_cache_t& c);
 cudaError_t launch_logits(const ott_cache_t& c, const uint16_t* q, float* logits, int n_rep, int64_t q_tokens,
                           int64_t total, cudaStream_t st);
 cudaError_t launch_rep_pad(const uint16_t* q, uint16_t* qs, int n_units, int n_rep, int h0, int nh, int nr, int d,
@@ -173,6 +174,11 @@ int ott_pick_splits(const ott_cache_t* c, int32_t n_rep, int64_t total_tokens) {
   if (s > max_by_groups) s = max_by_groups;
   if (s > 64) s = 64;
   if (s < 1) s = 1;
+  // more units than resident CTAs on the 2-bit tensor-core kernel: the launch's tail schedule
+  // (AttnArgs.tail_units): one wave of whole units, the other units in thirds, then the fp-tier
+  // CTAs. Config 4 (1,024 units): 390.8 us vs 396.6 for whole units only (halves 395.4,
+  // quarters 395.0: the pieces' start-up costs eat the better balance)
+  if (s == 1 && ott::mma_eligible(*c) && c->n_units > (int64_t)sms * 4 && n_groups >= 48) s = 3;
   return (int)s;
 }
 
