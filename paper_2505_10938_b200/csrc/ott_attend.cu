@@ -2061,8 +2061,11 @@ cudaError_t launch_attend(const ott_cache_t& c, const uint16_t* q, uint16_t* out
     a.n_splits = n_qsplits + a.n_fsplits;
     // more units than resident CTAs (config 4: 1,024 on 592): one wave of whole units, the rest
     // cut into n_qsplits pieces, then the short fp-tier CTAs: the launch ends on small work items
-    if (OTT_TAIL_SPLIT && mma_eligible(c) && n_qsplits >= 2 && c.n_units > slots)
+    if (OTT_TAIL_SPLIT && mma_eligible(c) && n_qsplits >= 2 && c.n_units > slots) {
       a.tail_units = (int)(c.n_units - slots);
+      a.n_fsplits = 1;  // two fp-tier CTAs per unit here: 399.8 us; fp tier before the pieces: 401.6
+      a.n_splits = n_qsplits + 1;
+    }
   }
 #define OTT_GCASE(FN, NRv, Gv) \
   if (n_rep == NRv && G == Gv) return FN<NRv, Gv>(a, st);
