@@ -592,6 +592,10 @@ __device__ void mma_body(const AttnArgs& a, const Counts& n, const CUtensorMap* 
   if (my_n > 0) load_ebatch(0);
   // q * u(m) as exact fp16 pairs (channels 16w+m, 16w+m+8) of head g, words w = tig + 4 hw:
   // the B operand of the bias MMA, and the q' = q u step split starts from it
+  // NR <= 4: B column g holds head g & 3 -- the q' hi half in columns 0-3 and the lo half in
+  // columns 4-7 -- so one HMMA per k-step covers both halves (kHiLoN below)
+  constexpr bool kHiLoN = NR <= 4;
+  const int qhead = kHiLoN ? (g & 3) : g;
   __half2 q16[2][8];
 #pragma unroll
   for (int hw = 0; hw < 2; ++hw) {
@@ -599,8 +603,8 @@ __device__ void mma_body(const AttnArgs& a, const Counts& n, const CUtensorMap* 
 #pragma unroll
     for (int m = 0; m < 8; ++m) {
       float lo = 0.f, hi = 0.f;
-      if (g < NR) {
-        const uint16_t* qr = a.q + ((size_t)u * NR + g) * D + 16 * wd + m;
+      if (qhead < NR) {
+        const uint16_t* qr = a.q + ((size_t)u * NR + qhead) * D + 16 * wd + m;
         lo = h2f(__ldg(qr)) * kpair_u(m);
         hi = h2f(__ldg(qr + 8)) * kpair_u(m);
       }
@@ -699,6 +703,7 @@ __device__ void mma_body(const AttnArgs& a, const Counts& n, const CUtensorMap* 
         const __half2 E = __hfma2(q16[hw][m], sh, __hneg2(H));
         bh[m] = h2_as_u32(H);
         bl[m] = h2_as_u32(__hfma2(q16[hw][m], sl, E));
+        if (kHiLoN) bh[m] = g >= 4 ? bl[m] : bh[m];  // column g: hi (g < 4) or lo (g >= 4) half
       }
       Shifted s0[kMt], s1[kMt];
 #pragma unroll
@@ -712,13 +717,19 @@ __device__ void mma_body(const AttnArgs& a, const Counts& n, const CUtensorMap* 
       const uint32_t a0 = kq<MM>(s0[mt], magic), a1 = kq<MM>(s1[mt], magic);         \
       const uint32_t a2 = kq<MM + 1>(s0[mt], magic), a3 = kq<MM + 1>(s1[mt], magic); \
       mma16816(ch[mt], a0, a1, a2, a3, bh[MM], bh[MM + 1]);                           \
-      mma16816(ch[mt], a0, a1, a2, a3, bl[MM], bl[MM + 1]);                           \
+      if (!kHiLoN) mma16816(ch[mt], a0, a1, a2, a3, bl[MM], bl[MM + 1]);             \
     }                                                                                 \
   }
       OTT_QK(0) OTT_QK(2) OTT_QK(4) OTT_QK(6)
 #undef OTT_QK
     }
 
+    if (kHiLoN) {  // logit = hi column + lo column (lanes tig, tig ^ 2); tig >= 2 lanes hold copies
+#pragma unroll
+      for (int mt = 0; mt < kMt; ++mt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) ch[mt][e] += __shfl_xor_sync(0xffffffffu, ch[mt][e], 2);
+    }
     // ---- x = logit - m (log2 units), heads 2 tig (cols 0, 2) and 2 tig + 1 (cols 1, 3)
     const float bm0 = bias0 - mrun[0], bm1 = bias1 - mrun[1];
     float x[kMt][4];
