@@ -149,7 +149,8 @@ def workload_config(wl, world):
             "group_size": wl.group_size, "residual": wl.residual, "outlier_pool": wl.outlier_num,
             "aux_capacity": wl.aux_capacity, "skip_layers": list(wl.skip_layers),
             "partition": f"{U} (batch x kv-head) units / {world} rank(s), contiguous, GQA groups whole",
-            "l2": "working set > L2 (126 MB): ~%.0f GB of cache" % cache_gb}
+            "l2": ("working set > L2 (126 MB): ~%.0f GB of cache" % cache_gb if cache_gb > 0.126 else
+                   "working set %.0f MB fits the 126 MB L2 (no flush between steps)" % (cache_gb * 1e3))}
 
 
 def run_reference(args, wl, rank, world):
@@ -230,6 +231,8 @@ def run_ours(args, wl, rank, world, local_rank):
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
+    # scalars of the rank collectives live where the backend reduces them (gloo: host)
+    coll_dev = dev if world == 1 or dist.get_backend() == "nccl" else torch.device("cpu")
     H, Hq, d, L, nrep = wl.n_kv_heads, wl.n_q_heads, wl.head_dim, wl.n_layers, wl.n_rep
     U = wl.batch * H
     u_lo, u_hi = unit_bounds(U, world, rank)
@@ -287,7 +290,7 @@ def run_ours(args, wl, rank, world, local_rank):
             pg = PeerGather(caches, nrep)
         except Exception as exc:  # no P2P mapping between these GPUs: keep the NCCL collective
             gather_mode, gather_note = "nccl", f" (P2P unavailable: {type(exc).__name__}: {str(exc)[:120]})"
-        ok = torch.tensor([1 if pg is not None else 0], device=dev)
+        ok = torch.tensor([1 if pg is not None else 0], device=coll_dev)
         dist.all_reduce(ok, op=dist.ReduceOp.MIN)  # every rank must take the same path
         if not int(ok.item()) and pg is not None:
             pg.close()
@@ -359,7 +362,7 @@ def run_ours(args, wl, rank, world, local_rank):
         dist.barrier()
     clk = clocks.stop()
     ms = start.elapsed_time(end)
-    ms_t = torch.tensor([ms], device=dev)
+    ms_t = torch.tensor([ms], device=coll_dev)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms = float(ms_t.item())
@@ -453,7 +456,7 @@ def run_ours(args, wl, rank, world, local_rank):
             pipe.step(k_h, v_h, qh, o_h)
         e1.record()
         torch.cuda.synchronize()
-        e_ms = torch.tensor([e0.elapsed_time(e1)], device=dev)
+        e_ms = torch.tensor([e0.elapsed_time(e1)], device=coll_dev)
         if world > 1:
             dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
         h2d = L * (k_h[0].numel() + v_h[0].numel() + qh[0].numel()) * 2
@@ -642,6 +645,13 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hook (tests/test_gpu_bench_multirank.py): every rank on GPU 0 with a gloo process group
+    # and the NCCL-style gather path, so the N > 1 branch runs on a one-GPU box; no rank's kernels
+    # wait on another's (the gather is a host-side collective)
+    one_gpu_test = os.environ.get("OTT_BENCH_ONE_GPU_TEST") == "1"
+    if one_gpu_test:
+        local_rank = 0
+        os.environ["OTT_GATHER"] = "nccl"
     if args.config == "c1":
         if args.impl == "reference":
             if rank == 0:
@@ -667,7 +677,10 @@ def main():
         import torch.distributed as dist
 
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if one_gpu_test:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     run_ours(args, wl, rank, world, local_rank)
     if world > 1:
         import torch.distributed as dist

@@ -49,8 +49,12 @@ def all_gather_heads(local: torch.Tensor, out: torch.Tensor | None = None, group
     if world == 1:
         out.copy_(local)
         return out
-    if local.is_cuda:
+    if local.is_cuda and dist.get_backend(group) != "gloo":
         dist.all_gather_into_tensor(out, local.contiguous(), group=group)
+    elif local.is_cuda:  # gloo process group over CUDA tensors (multi-rank tests on one GPU): via host
+        parts = list(torch.empty((world, *local.shape), dtype=local.dtype).unbind(0))
+        dist.all_gather(parts, local.cpu(), group=group)
+        out.copy_(torch.cat(parts, dim=0))
     else:  # gloo (CPU tests): list form
         parts = list(out.chunk(world, dim=0))
         dist.all_gather(parts, local.contiguous(), group=group)
