@@ -629,6 +629,52 @@ def test_config3_scale_sampled_units():
             assert ok, (b, h, r, err)
 
 
+def test_tail_schedule_units_and_decode_paths():
+    """More units than resident CTAs (80 x 8 = 640 > 4 x 148): with n_splits = 3 the 2-bit
+    kernel runs the tail schedule (one wave of whole units, the rest in thirds, then the fp tier).
+    Units on both sides of the split point are checked against the oracle, and append + attend,
+    append_attend and the device-counter decode_step agree step by step."""
+    from paper_2505_10938_b200 import OTTCache
+
+    B, Hkv, n_rep, T0, steps, d = 80, 8, 8, 1536, 40, 128
+    gen = torch.Generator(device="cuda").manual_seed(11)
+    k = torch.randn((B, Hkv, T0 + steps, d), device="cuda", generator=gen)
+    k[..., :4] *= 15
+    k = k.half()
+    v = torch.randn((B, Hkv, T0 + steps, d), device="cuda", generator=gen).half()
+    q = torch.randn((steps, B, Hkv * n_rep, d), device="cuda", generator=gen).half()
+    caches = [OTTCache(cfg_of(2, 32, 128, 32, 32, d), B, Hkv, max_tokens=T0 + steps + 8) for _ in range(3)]
+    for c in caches:
+        c.update(k[:, :, :T0], v[:, :, :T0])
+    caches[2].sync_counters()
+    outs = [[], [], []]
+    for s in range(steps):
+        t = T0 + s
+        caches[0].append(k[:, :, t], v[:, :, t])
+        outs[0].append(caches[0].attend(q[s], n_splits=3).clone())
+        outs[1].append(caches[1].append_attend(k[:, :, t].contiguous(), v[:, :, t].contiguous(), q[s],
+                                               n_splits=3).clone())
+        o = torch.empty_like(q[s])
+        outs[2].append(caches[2].decode_step(k[:, :, t].contiguous(), v[:, :, t].contiguous(), q[s], o, 3).clone())
+    for i in (1, 2):
+        for a, b in zip(outs[0], outs[i]):
+            torch.testing.assert_close(a, b, atol=0, rtol=0)  # same schedule, same partials
+    whole = caches[0].attend(q[-1], n_splits=1).float().cpu().numpy()  # no tail schedule
+    out = outs[0][-1].float().cpu().numpy()
+    kh, vh, qh = k.cpu().numpy(), v.cpu().numpy(), q[-1].cpu().numpy()
+    for b, h in ((0, 0), (73, 7), (74, 0), (79, 7)):  # units 0, 591 (whole) and 592, 639 (thirds)
+        ref = oracle.OracleCache(2, 32, 128, 32, 32, d)
+        ref.extend(kh[b, h, :T0].astype(np.float32), vh[b, h, :T0].astype(np.float32))
+        for t in range(T0, T0 + steps):
+            ref.append(kh[b, h, t].astype(np.float32), vh[b, h, t].astype(np.float32))
+        assert_unit_matches_oracle(caches[0].unit(b, h), ref, exact64=False)
+        for r in range(n_rep):
+            o_ref = ref.attend(qh[b, h * n_rep + r].astype(np.float32))
+            for got in (out, whole):
+                ok, err = within_tol(got[b, h * n_rep + r], o_ref)
+                assert ok, (b, h, r, err)
+
+
 def test_graft_smoke():
     import __graft_entry__
 
