@@ -1,0 +1,9 @@
+mkdir -p gpurun_out/r2
+O=gpurun_out/r2/fusefp.log; : > $O
+timeout 900 python -m pytest tests -m gpu -x -q >> $O 2>&1; echo "pytest_exit=$?" >> $O
+for a in "--batch 16 --splits 3" "--batch 16 --splits 4" "--batch 32 --splits 2" "--batch 32 --splits 4" "--batch 128 --splits 0"; do
+  echo "$(timeout 120 python tools/prof_attend.py --rep 8 --ctx 16384 --iters 20 --graph $a 2>&1 | tail -1)" >> $O
+done
+for a in "--batch 16 --rep 4 --ctx 4096 --splits 4" "--batch 16 --rep 4 --ctx 4096 --splits 3"; do
+  echo "$(timeout 120 python tools/prof_attend.py --iters 20 --graph $a 2>&1 | tail -1)" >> $O
+done
