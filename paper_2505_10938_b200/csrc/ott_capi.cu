@@ -3,6 +3,8 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <algorithm>
+
 #include "ott_common.cuh"
 
 namespace ott {
@@ -171,6 +173,15 @@ int ott_pick_splits(const ott_cache_t* c, int32_t n_rep, int64_t total_tokens) {
   const int64_t target = (int64_t)sms * 3;
   int64_t s = (target + c->n_units / 2) / c->n_units;
   const int64_t max_by_groups = n_groups / 16 > 0 ? n_groups / 16 : 1;
+  // long contexts (>= 256 groups per unit) on 256-592 units: aim at ~1,024 quantized CTAs with
+  // pieces of >= 96 groups. The config-4 shards of 2 and 4 GPUs (512 / 256 units at 16K
+  // tokens): 224.7 -> 208.3 us (2 pieces) and 122.5 -> 116.1 us (4 pieces); 128 units keep 3
+  // (4-8 pieces: 70.5-76.5 vs 69.8 us) and shorter contexts the rule above
+  // (profiles/r2_shard_splits.log)
+  if (n_groups >= 256 && c->n_units >= 256 && c->n_units <= (int64_t)sms * 4) {
+    const int64_t s_long = std::min<int64_t>((1024 + c->n_units / 2) / c->n_units, n_groups / 96);
+    if (s_long > s) s = s_long;
+  }
   if (s > max_by_groups) s = max_by_groups;
   if (s > 64) s = 64;
   if (s < 1) s = 1;
