@@ -70,3 +70,27 @@ def test_product_does_not_import_oracle():
                 src = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"^\s*(import|from)\s+oracle", src, re.M), f
                 assert "ott_oracle" not in src, f
+
+
+def test_split_policy_without_gpu():
+    """ott_pick_splits is host arithmetic (148 SMs assumed without a device): the split counts the
+    measured sweeps chose (profiles/r2_shard_splits.log, r2_pick_splits.log) for the BASELINE
+    shapes. 1,024 units run the tail schedule with thirds; 256-592 units at long contexts aim at
+    ~1,024 quantized CTAs; short contexts keep ~3 CTAs per SM."""
+    from paper_2505_10938_b200 import _native
+
+    L = _native.lib()
+
+    def pick(units, tokens, bits=2, d=128, G=32):
+        c = _native.OttCacheT(n_units=units, head_dim=d, group_size=G, residual=128, capacity=32, aux_capacity=32,
+                              bits=bits)
+        return L.ott_pick_splits(ctypes.byref(c), 8, tokens)
+
+    assert pick(1024, 16384) == 3  # config 4 at N = 1: tail schedule
+    assert pick(512, 16384) == 2   # config-4 shard at N = 2
+    assert pick(256, 16384) == 4   # N = 4
+    assert pick(128, 16384) == 3   # N = 8
+    assert pick(128, 4096) == 3 and pick(512, 8192) == 1  # config 3
+    assert pick(256, 2304) == 2    # config 1 layer (B = 8, H = 32)
+    assert pick(32, 1024) == 1     # config 0
+    assert pick(1024, 16384, bits=4) == 1  # the tail schedule is the 2-bit kernel's
