@@ -536,6 +536,10 @@ template <int M>
 __device__ __forceinline__ uint32_t vqt(const VSrc& s) {
   return (M <= 4 ? s.x : s.r10) & (0x00030003u << (2 * vpos(M)));
 }
+#ifdef OTT_EXP_TIMELINE
+constexpr uint32_t kTimelineMax = 16384;
+__device__ uint64_t g_timeline[kTimelineMax][4];  // per CTA: start, end (globaltimer ns), SM, blockIdx.y
+#endif
 constexpr float kMinit = -1e30f;
 #ifdef OTT_EXP_NOTMA
 constexpr bool kNoTma = true;
@@ -947,6 +951,10 @@ template <int NR, int G>
 __global__ void __launch_bounds__(kAttnThreads, OTT_MMA_MIN_BLOCKS)
     attend_mma_kernel(const __grid_constant__ AttnArgs a, const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(256) unsigned char smem_raw[];
+#ifdef OTT_EXP_TIMELINE
+  uint64_t t_start;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+#endif
   allow_dependents();
   if ((int)blockIdx.y >= a.n_qsplits) {  // full-precision tiers: pool + pending
     const Counts n = counts_of(a);
@@ -956,6 +964,21 @@ __global__ void __launch_bounds__(kAttnThreads, OTT_MMA_MIN_BLOCKS)
   } else {
     mma_body<NR, G>(a, counts_of(a), &tmap, *reinterpret_cast<MmaSmem<G>*>(smem_raw));
   }
+#ifdef OTT_EXP_TIMELINE
+  if (threadIdx.x == 0) {
+    uint64_t t_end;
+    uint32_t smid;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    const uint32_t i = blockIdx.y * gridDim.x + blockIdx.x;
+    if (i < kTimelineMax) {
+      g_timeline[i][0] = t_start;
+      g_timeline[i][1] = t_end;
+      g_timeline[i][2] = smid;
+      g_timeline[i][3] = blockIdx.y;
+    }
+  }
+#endif
 }
 
 // ============================================================ 4-bit tensor-core path (d = 128, G = 32)
@@ -2202,3 +2225,14 @@ cudaError_t launch_logits(const ott_cache_t& c, const uint16_t* q, float* logits
 }
 
 }  // namespace ott
+
+#ifdef OTT_EXP_TIMELINE
+extern "C" int ott_exp_timeline(uint64_t* host, int n) {
+  if (n > (int)ott::kTimelineMax) n = ott::kTimelineMax;
+  return (int)cudaMemcpyFromSymbol(host, ott::g_timeline, (size_t)n * 4 * sizeof(uint64_t));
+}
+extern "C" int ott_exp_timeline_clear(void) {
+  static uint64_t zero[ott::kTimelineMax][4];
+  return (int)cudaMemcpyToSymbol(ott::g_timeline, zero, sizeof(zero));
+}
+#endif
