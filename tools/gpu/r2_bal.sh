@@ -1,10 +1,9 @@
 mkdir -p gpurun_out/r2
-O=gpurun_out/r2/bal.log; : > $O
+O=gpurun_out/r2/bal2.log; : > $O
 timeout 900 python -m pytest tests -m gpu -x -q >> $O 2>&1; echo "pytest_exit=$?" >> $O
-for a in "--batch 4 --kv 32 --rep 1 --ctx 32768" "--batch 16 --rep 4 --ctx 4096" "--batch 16 --rep 4 --ctx 8192" "--batch 64 --rep 4 --ctx 4096" "--batch 64 --rep 4 --ctx 8192" "--batch 8 --kv 32 --rep 1 --ctx 2304" "--batch 1 --kv 32 --rep 1 --ctx 1024" "--batch 16 --rep 8 --ctx 16384" "--batch 32 --rep 8 --ctx 16384" "--batch 64 --rep 8 --ctx 16384" "--batch 128 --rep 8 --ctx 16384"; do
-  for v in product bal0 bal2; do
+for a in "--batch 16 --rep 8 --ctx 16384" "--batch 32 --rep 8 --ctx 16384" "--batch 64 --rep 8 --ctx 16384" "--batch 4 --kv 32 --rep 1 --ctx 32768" "--batch 16 --rep 4 --ctx 4096" "--batch 16 --rep 4 --ctx 8192" "--batch 64 --rep 4 --ctx 4096" "--batch 64 --rep 4 --ctx 8192" "--batch 8 --kv 32 --rep 1 --ctx 2304" "--batch 128 --rep 8 --ctx 16384"; do
+  for v in product bps0 bps2 bps4 bps6; do
     if [ $v = product ]; then L=""; else L="tools/variants/$v.so"; fi
     echo "$v: $(OTT_LIB_PATH=$L timeout 120 python tools/prof_attend.py $a --iters 20 --graph 2>&1 | tail -1)" >> $O
   done
 done
-OTT_LIB_PATH=tools/variants/bal2.so timeout 600 python -m pytest tests/test_gpu_parity.py -x -q 2>&1 | tail -1 >> $O
