@@ -84,3 +84,12 @@ if w1.sum() > 0:
     du = d
     print("  duration by unit quartile:", [round(float(du[(units >= U * k // 4) & (units < U * (k + 1) // 4)].mean()), 1)
                                           for k in range(4) if ((units >= U * k // 4) & (units < U * (k + 1) // 4)).any()])
+
+# duration by dispatch rank (linear CTA index // SM count) of the quantized CTAs
+lin = np.arange(len(buf))  # buffer rows are in linear blockIdx order (x fastest, then y)
+rank = lin // 148
+for rk in range(int(rank.max()) + 1):
+    m = (~kind) & (rank == rk)
+    if m.any():
+        d = e[m] - s[m]
+        print(f"  rank {rk}: {m.sum()} quantized CTAs, duration mean {d.mean():.1f} min {d.min():.1f} max {d.max():.1f} us, start {s[m].mean():.1f}")
