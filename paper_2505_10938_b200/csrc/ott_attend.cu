@@ -1008,8 +1008,11 @@ __device__ void mma4_body(const AttnArgs& a, const Counts& n, const VgMaps* tmap
 
   // q (fp32) for the bias: slot 2 s + j of lane (head h, t) = channels 8 w + 4 j .. +3 of word
   // w = 32 (s >> 1) + 8 (s & 1)... i.e. words W(s) = {t, 4+t, 8+t, 12+t}[s]
+  // NR <= 4: B column g holds head g & 3 -- the q' hi half in columns 0-3, the lo half in 4-7
+  // -- so one HMMA per k-step covers both halves (as in mma_body)
+  constexpr bool kHiLoN = NR <= 4;
   for (int i = tid; i < 8 * 32; i += kAttnThreads) {
-    const int k = i >> 5, ln = i & 31, h = ln >> 2, t4 = ln & 3;
+    const int k = i >> 5, ln = i & 31, h = kHiLoN ? ((ln >> 2) & 3) : (ln >> 2), t4 = ln & 3;
     const int w = 4 * (k >> 1) + t4;  // words t, 4+t, 8+t, 12+t
     const int ch = 8 * w + 4 * (k & 1);
     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1107,6 +1110,7 @@ __device__ void mma4_body(const AttnArgs& a, const Counts& n, const VgMaps* tmap
           const __half2 E = __hfma2(qq, sh, __hneg2(H));
           bh[b][kk] = h2_as_u32(H);
           bl[b][kk] = h2_as_u32(__hfma2(qq, sl, E));
+          if (kHiLoN) bh[b][kk] = g >= 4 ? bl[b][kk] : bh[b][kk];
         }
       }
       Nib n0[kMt], n1[kMt], n2[kMt], n3[kMt];
@@ -1123,11 +1127,17 @@ __device__ void mma4_body(const AttnArgs& a, const Counts& n, const VgMaps* tmap
       const uint32_t a0 = kq4<K>(n0[mt], magic), a1 = kq4<K>(n1[mt], magic);                 \
       const uint32_t a2 = kq4<K>(n2[mt], magic), a3 = kq4<K>(n3[mt], magic);                 \
       mma16816(ch[mt], a0, a1, a2, a3, bh[0][K], bh[1][K]);                                   \
-      mma16816(ch[mt], a0, a1, a2, a3, bl[0][K], bl[1][K]);                                   \
+      if (!kHiLoN) mma16816(ch[mt], a0, a1, a2, a3, bl[0][K], bl[1][K]);                     \
     }                                                                                         \
   }
       OTT_QK4(0) OTT_QK4(1) OTT_QK4(2) OTT_QK4(3)
 #undef OTT_QK4
+    }
+    if (kHiLoN) {  // logit = hi column + lo column (lanes tig, tig ^ 2); tig >= 2 lanes hold copies
+#pragma unroll
+      for (int mt = 0; mt < kMt; ++mt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) ch[mt][e] += __shfl_xor_sync(0xffffffffu, ch[mt][e], 2);
     }
     float sc[kMt][4];
     {
