@@ -27,76 +27,97 @@ from .config import EngineConfig
 from .errors import ContractViolation, TraceFormatError
 
 MAGIC = b"KVTRACE1"
+_DIMS = ("n_layers", "n_heads", "head_dim", "seq_len")  # header field order
 _HEADER = struct.Struct("<4I")
+_PAYLOAD = np.dtype("<f4")
 FP16_BITS = 16
 
 
-@dataclass(frozen=True)
-class TraceHeader:
-    n_layers: int
-    n_heads: int
-    head_dim: int
-    seq_len: int
+class TraceHeader(tuple):
+    """The four header fields (n_layers, n_heads, head_dim, seq_len); each must fit a non-zero
+    uint32 (ContractViolation otherwise). Compares equal to a tuple of the same values."""
 
-    def __post_init__(self):
-        for name in ("n_layers", "n_heads", "head_dim", "seq_len"):
-            v = getattr(self, name)
-            if not 1 <= v <= 0xFFFFFFFF:
-                raise ContractViolation(f"{name} must be in [1, 2**32), got {v}")
+    __slots__ = ()
+
+    def __new__(cls, n_layers, n_heads, head_dim, seq_len):
+        vals = tuple(int(x) for x in (n_layers, n_heads, head_dim, seq_len))
+        for name, val in zip(_DIMS, vals):
+            if val < 1 or val > 0xFFFFFFFF:
+                raise ContractViolation(f"{name} must be in [1, 2**32), got {val}")
+        return super().__new__(cls, vals)
+
+    n_layers = property(lambda self: self[0])
+    n_heads = property(lambda self: self[1])
+    head_dim = property(lambda self: self[2])
+    seq_len = property(lambda self: self[3])
+
+    @property
+    def matrix_shape(self):  # (layers, heads, seq, dim): the shape of Trace.q / .k / .v
+        return (self[0], self[1], self[3], self[2])
+
+    @property
+    def file_bytes(self) -> int:
+        return len(MAGIC) + _HEADER.size + self[0] * self[1] * 3 * self[3] * self[2] * _PAYLOAD.itemsize
 
 
-@dataclass
 class Trace:
-    """Q/K/V float32 arrays of shape (layers, heads, seq, dim)."""
+    """Q/K/V of every (layer, head), held as one float32 block [layers, heads, 3, seq, dim] in
+    the file's order (layer-major, head-minor, Q K V per head), so a file maps onto it without a
+    copy per matrix; `q`, `k`, `v` are views of shape (layers, heads, seq, dim)."""
 
-    header: TraceHeader
-    q: np.ndarray
-    k: np.ndarray
-    v: np.ndarray
+    def __init__(self, header: TraceHeader, q, k, v):
+        self.header = header
+        want = header.matrix_shape
+        mats = []
+        for name, m in (("q", q), ("k", k), ("v", v)):
+            m = np.asarray(m, dtype=np.float32)
+            if m.shape != want:
+                raise ContractViolation(f"{name} must have shape {want}, got {m.shape}")
+            mats.append(m)
+        self.qkv = np.stack(mats, axis=2)
 
-    def __post_init__(self):
-        h = self.header
-        shape = (h.n_layers, h.n_heads, h.seq_len, h.head_dim)
-        for name in ("q", "k", "v"):
-            arr = np.ascontiguousarray(getattr(self, name), dtype=np.float32)
-            if arr.shape != shape:
-                raise ContractViolation(f"{name} must have shape {shape}, got {arr.shape}")
-            setattr(self, name, arr)
+    @classmethod
+    def _from_block(cls, header: TraceHeader, qkv: np.ndarray) -> "Trace":
+        t = cls.__new__(cls)
+        t.header, t.qkv = header, qkv
+        return t
+
+    q = property(lambda self: self.qkv[:, :, 0])
+    k = property(lambda self: self.qkv[:, :, 1])
+    v = property(lambda self: self.qkv[:, :, 2])
 
 
 def write_trace(path, trace: Trace) -> None:
-    """Serialize in the KVTRACE1 format (bit-exact round trip)."""
-    h = trace.header
+    """Serialize in the KVTRACE1 format (bit-exact round trip): header, then the qkv block."""
     with open(path, "wb") as f:
-        f.write(MAGIC + _HEADER.pack(h.n_layers, h.n_heads, h.head_dim, h.seq_len))
-        # layer-major, head-minor, (Q, K, V) per head: one interleaved array, one write
-        f.write(np.stack([trace.q, trace.k, trace.v], axis=2).astype("<f4").tobytes())
+        f.write(MAGIC + _HEADER.pack(*trace.header))
+        f.write(trace.qkv.astype(_PAYLOAD, copy=False).tobytes())
 
 
 def read_trace(path) -> Trace:
-    """Parse a KVTRACE1 file; damage raises TraceFormatError (offset as the reference)."""
+    """Parse a KVTRACE1 file. Damage raises TraceFormatError at the byte offsets (and with the
+    messages) the format's reference reader uses, checked in file order."""
     with open(path, "rb") as f:
         data = f.read()
-    n = len(data)
-    if n < len(MAGIC):
-        raise TraceFormatError("truncated file: magic missing", offset=n)
-    if data[: len(MAGIC)] != MAGIC:
+    size, hdr_end = len(data), len(MAGIC) + _HEADER.size
+    if size < len(MAGIC):
+        raise TraceFormatError("truncated file: magic missing", offset=size)
+    if not data.startswith(MAGIC):
         raise TraceFormatError("bad magic", offset=0)
-    hdr_end = len(MAGIC) + _HEADER.size
-    if n < hdr_end:
-        raise TraceFormatError("truncated file: header incomplete", offset=n)
-    dims = _HEADER.unpack(data[len(MAGIC):hdr_end])
-    for name, v in zip(("n_layers", "n_heads", "head_dim", "seq_len"), dims):
-        if v < 1:
-            raise TraceFormatError(f"{name} must be >= 1, got {v}", offset=len(MAGIC))
-    L, H, d, T = dims
-    expected = hdr_end + L * H * 3 * T * d * 4
-    if n < expected:
-        raise TraceFormatError("truncated file: payload incomplete", offset=n)
-    if n > expected:
-        raise TraceFormatError("trailing bytes after payload", offset=expected)
-    qkv = np.frombuffer(data, dtype="<f4", offset=hdr_end).reshape(L, H, 3, T, d).astype(np.float32)
-    return Trace(TraceHeader(L, H, d, T), qkv[:, :, 0], qkv[:, :, 1], qkv[:, :, 2])
+    if size < hdr_end:
+        raise TraceFormatError("truncated file: header incomplete", offset=size)
+    fields = _HEADER.unpack_from(data, len(MAGIC))
+    zero = next((i for i, val in enumerate(fields) if val == 0), None)
+    if zero is not None:
+        raise TraceFormatError(f"{_DIMS[zero]} must be >= 1, got 0", offset=len(MAGIC))
+    header = TraceHeader(*fields)
+    expected = header.file_bytes
+    if size != expected:
+        raise (TraceFormatError("truncated file: payload incomplete", offset=size) if size < expected else
+               TraceFormatError("trailing bytes after payload", offset=expected))
+    L, H, d, T = fields
+    block = np.frombuffer(data, dtype=_PAYLOAD, offset=hdr_end).reshape(L, H, 3, T, d)
+    return Trace._from_block(header, block.astype(np.float32))
 
 
 @dataclass
