@@ -67,14 +67,11 @@ class QuantizedBlock:
                                                                                            self.n_channels)
 
     def to_matrix(self) -> np.ndarray:
-        codes = self.code_matrix().astype(np.float64)
-        steps = np.array([p.step for p in self.params])
-        mins = np.array([p.x_min for p in self.params])
-        if self.group_axis is GroupAxis.PER_CHANNEL:
-            out = codes * steps[None, :] + mins[None, :]
-        else:
-            out = codes * steps[:, None] + mins[:, None]
-        return out.astype(np.float32)
+        """codes * step + x_min in float64 per line (a column per channel, a row per token),
+        rounded once to float32 (quant.py:105-111, 154-163)."""
+        line = np.array([(p.step, p.x_min) for p in self.params], dtype=np.float64)
+        bcast = (1, -1) if self.group_axis is GroupAxis.PER_CHANNEL else (-1, 1)
+        return (self.code_matrix() * line[:, 0].reshape(bcast) + line[:, 1].reshape(bcast)).astype(np.float32)
 
 
 @dataclass
