@@ -11,8 +11,6 @@ The arithmetic runs in the library's kernels (ott_api.cu, C ABI ``ott_pool_rank`
 
 from __future__ import annotations
 
-from dataclasses import dataclass, field
-
 import numpy as np
 import torch
 
@@ -66,54 +64,56 @@ def _ranks(items) -> np.ndarray:
     return r.cpu().numpy()
 
 
-@dataclass
 class OutlierPool:
-    """outlier.py:57-117: the ``capacity`` lowest-(score, position) tokens seen so far; members
-    that lose their slot move to ``aux`` (up to ``aux_capacity``), and a full ``aux`` freezes
-    the pool for good."""
+    """The reference's outlier pool (outlier.py:57-117) with the competition ranked on the GPU.
 
-    capacity: int
-    aux_capacity: int = 32
-    entries: list = field(default_factory=list)
-    aux: list = field(default_factory=list)
-    frozen: bool = False
+    The pool holds the ``capacity`` lowest (score, position) tokens presented so far. A member
+    that loses its slot is retired to ``aux`` while there is room, and a full ``aux`` freezes the
+    pool: later updates change nothing."""
 
-    def __post_init__(self):
-        if self.capacity < 0 or self.aux_capacity < 0:
+    def __init__(self, capacity: int, aux_capacity: int = 32, entries=None, aux=None, frozen: bool = False):
+        if min(capacity, aux_capacity) < 0:
             raise ContractViolation("pool capacities must be nonnegative")  # outlier.py:75-76
-        if len(self.aux) >= self.aux_capacity:
-            self.frozen = True
+        self.capacity, self.aux_capacity = capacity, aux_capacity
+        self.entries = list(entries or ())
+        self.aux = list(aux or ())
+        self.frozen = bool(frozen) or len(self.aux) >= aux_capacity
+
+    def __repr__(self) -> str:
+        return (f"OutlierPool(capacity={self.capacity}, aux_capacity={self.aux_capacity}, "
+                f"positions={sorted(self.positions)}, aux={len(self.aux)}, frozen={self.frozen})")
 
     @property
     def positions(self) -> set:
         return {e.position for e in self.entries}
 
     def update(self, candidates) -> tuple:
-        """Returns (selected positions, evicted entries), as outlier.py:84-117."""
+        """One competition round of the members and ``candidates``: returns (positions of the
+        candidates that won a slot, former members that lost theirs, in member order)."""
         if self.frozen or self.capacity == 0:
             return set(), []
         candidates = list(candidates)
-        seen = {e.position for e in self.entries}
-        for c in candidates:
-            if c.position in seen:
-                raise ContractViolation(f"duplicate position {c.position} in pool update")  # outlier.py:96-100
-            seen.add(c.position)
-        items = self.entries + candidates
-        if not items:
+        taken = self.positions
+        for c in candidates:  # outlier.py:96-100
+            if c.position in taken:
+                raise ContractViolation(f"duplicate position {c.position} in pool update")
+            taken.add(c.position)
+        field = self.entries + candidates
+        if not field:
             return set(), []
-        rank = _ranks(items)
-        order = np.argsort(rank, kind="stable")
-        winners = [items[i] for i in order[: self.capacity]]
-        winner_positions = {e.position for e in winners}
-        old_positions = self.positions
-        selected = {e.position for e in winners if e.position not in old_positions}
-        evicted = [e for e in self.entries if e.position not in winner_positions]  # old-entry order
-        self.entries = winners
-        room = self.aux_capacity - len(self.aux)
-        self.aux.extend(evicted[:room])
+        kept = np.argsort(_ranks(field), kind="stable")[: self.capacity]
+        n_members = len(self.entries)
+        kept_set = set(kept.tolist())
+        won = {field[i].position for i in kept if i >= n_members}
+        lost = [e for i, e in enumerate(self.entries) if i not in kept_set]
+        self.entries = [field[i] for i in kept]
+        self._retire(lost)
+        return won, lost
+
+    def _retire(self, lost) -> None:
+        self.aux += lost[: max(0, self.aux_capacity - len(self.aux))]
         if len(self.aux) >= self.aux_capacity:
             self.frozen = True
-        return selected, evicted
 
 
 def attend_full_precision(q, keys, values, with_weights: bool = True) -> AttentionResult:
