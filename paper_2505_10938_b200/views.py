@@ -35,12 +35,15 @@ class QuantParams:
 
 
 def unpack_codes(data: bytes, bits: int, count: int) -> np.ndarray:
-    """Inverse of pack_codes (quant.py:259-273): LSB-first bit stream."""
+    """The `count` codes of a little-endian (LSB-first) stream of `bits`-bit fields, as int64
+    (the layout of the reference's pack_codes, quant.py:241-273). Code i starts at bit i * bits;
+    a field of <= 8 bits lies inside the 16-bit window starting at its first byte."""
     if count == 0:
         return np.zeros(0, dtype=np.int64)
-    stream = np.unpackbits(np.frombuffer(data, dtype=np.uint8), bitorder="little")
-    cols = stream[: count * bits].reshape(count, bits).astype(np.int64)
-    return cols @ (1 << np.arange(bits, dtype=np.int64))
+    window = np.frombuffer(bytes(data) + b"\0", dtype=np.uint8).astype(np.int64)
+    first = np.arange(count, dtype=np.int64) * bits
+    lo = first >> 3
+    return ((window[lo] | (window[lo + 1] << 8)) >> (first & 7)) & ((1 << bits) - 1)
 
 
 @dataclass
