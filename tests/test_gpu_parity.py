@@ -467,6 +467,36 @@ def test_flush_adversarial_lines_vs_oracle(bits, N):
     assert ok, err
 
 
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_flush_threshold_ties_random(seed):
+    """Lines whose fp16 thresholds x_min + k step land exactly on fp16 values (range divisible
+    by 3 in fp16 units, at many magnitudes): the division-free tie rule of code_thresholds
+    (k = 1, 2) and the Markstein line step, bit-exact vs the oracle over 64 units and both
+    pool settings (N = 0: every group through the threshold path)."""
+    from paper_2505_10938_b200 import OTTCache
+
+    d, G, U, T = 128, 32, 16, 32 * 10 + 7
+    rng = np.random.default_rng(100 + seed)
+    # K line (unit, channel, group): values (b + L) ulp with L in [0, 3 m], both ends present in
+    # every group, so x_min + k step = (b + k m) ulp is an fp16 value (|b + L| < 2048: exact)
+    ulp = 2.0 ** rng.integers(-20, 2, size=(U, 1, 1, d))
+    b = rng.integers(-1000, 1000, size=(U, 1, 1, d))
+    span = 3 * rng.integers(1, 20, size=(U, 1, 1, d))
+    lattice = rng.integers(0, span + 1, size=(U, 1, T, d))
+    lattice[:, :, 0::G] = 0
+    lattice[:, :, 1::G] = np.broadcast_to(span, lattice[:, :, 1::G].shape)
+    k = ((b + lattice) * ulp).astype(np.float16)
+    assert np.array_equal(k.astype(np.float64), (b + lattice) * ulp)
+    v = (rng.integers(-30, 30, size=(U, 1, T, d)) * 2.0 ** rng.integers(-12, 2, size=(U, 1, T, 1))).astype(np.float16)
+    for N in (0, 32):
+        cache = OTTCache(cfg_of(2, G, 64, N, 8, d), U, 1, max_tokens=T, keep_f64_params=True)
+        cache.update(torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda())
+        for u in (0, 5, U - 1):
+            ref = oracle.OracleCache(2, G, 64, N, 8, d)
+            ref.extend(k[u, 0].astype(np.float32), v[u, 0].astype(np.float32))
+            assert_unit_matches_oracle(cache.unit(u, 0), ref)
+
+
 def test_batch_shards_match_whole_batch():
     """a rank owns a contiguous batch slice with all its kv heads and needs no
     exchange but the output all-gather. Two half-batch caches (what two ranks hold) give the
