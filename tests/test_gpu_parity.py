@@ -469,10 +469,10 @@ def test_flush_adversarial_lines_vs_oracle(bits, N):
 
 @pytest.mark.parametrize("seed", [1, 2, 3])
 def test_flush_threshold_ties_random(seed):
-    """Lines whose fp16 thresholds x_min + k step land exactly on fp16 values (range divisible
-    by 3 in fp16 units, at many magnitudes): the division-free tie rule of code_thresholds
-    (k = 1, 2) and the Markstein line step, bit-exact vs the oracle over 64 units and both
-    pool settings (N = 0: every group through the threshold path)."""
+    """K and V lines whose fp16 thresholds x_min + k step land exactly on fp16 values (range
+    divisible by 3 in fp16 units, at many magnitudes): the division-free tie rule of
+    code_thresholds (k = 1, 2) and the Markstein line step, bit-exact vs the oracle over 16
+    units and both pool settings (N = 0: every group through the threshold path)."""
     from paper_2505_10938_b200 import OTTCache
 
     d, G, U, T = 128, 32, 16, 32 * 10 + 7
@@ -487,7 +487,14 @@ def test_flush_threshold_ties_random(seed):
     lattice[:, :, 1::G] = np.broadcast_to(span, lattice[:, :, 1::G].shape)
     k = ((b + lattice) * ulp).astype(np.float16)
     assert np.array_equal(k.astype(np.float64), (b + lattice) * ulp)
-    v = (rng.integers(-30, 30, size=(U, 1, T, d)) * 2.0 ** rng.integers(-12, 2, size=(U, 1, T, 1))).astype(np.float16)
+    # V line (unit, token): the same construction along the channels
+    vulp = 2.0 ** rng.integers(-20, 2, size=(U, 1, T, 1))
+    vb = rng.integers(-1000, 1000, size=(U, 1, T, 1))
+    vspan = 3 * rng.integers(1, 20, size=(U, 1, T, 1))
+    vlat = rng.integers(0, vspan + 1, size=(U, 1, T, d))
+    vlat[..., 0] = 0
+    vlat[..., 1] = vspan[..., 0]
+    v = ((vb + vlat) * vulp).astype(np.float16)
     for N in (0, 32):
         cache = OTTCache(cfg_of(2, G, 64, N, 8, d), U, 1, max_tokens=T, keep_f64_params=True)
         cache.update(torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda())
