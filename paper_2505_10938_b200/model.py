@@ -15,7 +15,10 @@ random N(0, 0.02) fp16 weights (no checkpoints are available offline):
   and attends through the OTT cache kernels (K4 ring write, K1 flush when due,
   K2/K3 attention);
 * `kv="fp16"` swaps the OTT cache for a plain fp16 KV cache attended with
-  torch SDPA: the accuracy/throughput baseline the paper compares against.
+  torch SDPA: the accuracy/throughput baseline the paper compares against;
+* `kv="flash"` is an independent fp16 throughput baseline: a plain fp16 KV cache attended with
+  FlashAttention-2's decode kernel (`flash_attn_with_kvcache`, library code, device-side
+  sequence lengths), captured in the same CUDA graph step.
 """
 
 from __future__ import annotations
@@ -80,8 +83,8 @@ class Decoder:
         in eager decode steps, record the reference's fidelity metric (cli.py:208-218): per step
         the mean over (layer, batch, head) of the L1 distance between the cache's attention
         output and exact float32 attention over the same rows (`attn_l1`)."""
-        if kv not in ("ott", "fp16"):
-            raise ContractViolation("kv must be 'ott' or 'fp16'")
+        if kv not in ("ott", "fp16", "flash"):
+            raise ContractViolation("kv must be 'ott', 'fp16' or 'flash'")
         self.cfg, self.batch, self.max_tokens, self.kv = cfg, batch, max_tokens, kv
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         dev, H, Hkv, d, D = self.device, cfg.n_heads, cfg.n_kv_heads, cfg.head_dim, cfg.hidden
@@ -117,6 +120,10 @@ class Decoder:
             ott = ott or EngineConfig(bits=2, group_size=32, residual=128, outlier_num=32, aux_capacity=32,
                                       n_layers=cfg.n_layers, n_heads=Hkv, head_dim=d)
             self.caches = [OTTCache(ott, batch, Hkv, max_tokens, layer=l, device=dev) for l in range(cfg.n_layers)]
+        elif kv == "flash":  # [layer, batch, token, kv head, d] (flash_attn_with_kvcache's layout)
+            self.k_cache = torch.zeros((cfg.n_layers, batch, max_tokens, Hkv, d), dtype=torch.float16, device=dev)
+            self.v_cache = torch.zeros_like(self.k_cache)
+            self.seqlens = torch.zeros(batch, dtype=torch.int32, device=dev)
         else:
             self.k_cache = torch.zeros((cfg.n_layers, batch, Hkv, max_tokens, d), dtype=torch.float16, device=dev)
             self.v_cache = torch.zeros_like(self.k_cache)
@@ -192,12 +199,17 @@ class Decoder:
                 if self.track_exact:
                     self.sk[l, :, :, :T] = k
                     self.sv[l, :, :, :T] = v
+            elif self.kv == "flash":
+                self.k_cache[l, :, :T] = k.transpose(1, 2)
+                self.v_cache[l, :, :T] = v.transpose(1, 2)
             else:
                 self.k_cache[l, :, :, :T] = k
                 self.v_cache[l, :, :, :T] = v
             x = x + o.transpose(1, 2).reshape(B, T, -1) @ lw["wo"]
             x = x + self._mlp(x, lw)
         self.pos = T
+        if self.kv == "flash":
+            self.seqlens.fill_(T)
         self.last_logits = self._logits(x[:, -1])
         return self.last_logits.argmax(-1)
 
@@ -243,6 +255,13 @@ class Decoder:
                     c.attend(q, out=o)
                     if self.track_exact:
                         l1_sum += self._exact_l1(l, k, v, q, o, pos_host)
+            elif self.kv == "flash":
+                from flash_attn import flash_attn_with_kvcache
+
+                # appends k, v at seqlens[b] and attends over seqlens[b] + 1 rows (device lengths)
+                o.copy_(flash_attn_with_kvcache(q.view(B, 1, H, d), self.k_cache[l], self.v_cache[l],
+                                                k=k.view(B, 1, Hkv, d), v=v.view(B, 1, Hkv, d),
+                                                cache_seqlens=self.seqlens).view(B, H, d))
             else:
                 p = pos_host
                 self.k_cache[l, :, :, p] = k
@@ -285,6 +304,8 @@ class Decoder:
             raise ContractViolation("decoder is full")
         x = self.embed.index_select(0, tokens)
         logits = self._layers_step(x, self.pos, tok=tokens)
+        if self.kv == "flash":
+            self.seqlens.add_(1)
         self.pos += 1
         self.last_logits = logits.clone()
         return logits.argmax(-1)
@@ -298,13 +319,15 @@ class Decoder:
         self.g_logits.copy_(logits)
         self.g_next.copy_(logits.argmax(-1))
         self.g_pos.add_(1)
+        if self.kv == "flash":
+            self.seqlens.add_(1)
 
     @torch.no_grad()
     def capture_decode_graph(self) -> None:
         """Capture one OTT decode step (all layers: GEMMs, RoPE, ring write, flush-if-due,
         attention, combine) in a CUDA graph; `decode_graph` then replays it per step."""
-        if self.kv != "ott":
-            raise ContractViolation("graph decode needs the OTT cache (device token counters)")
+        if self.kv == "fp16":
+            raise ContractViolation("graph decode needs device-side lengths (kv='ott' or 'flash')")
         cfg, B, dev = self.cfg, self.batch, self.device
         self.g_tok = torch.zeros(B, dtype=torch.int64, device=dev)
         self.g_next = torch.zeros(B, dtype=torch.int64, device=dev)
@@ -313,19 +336,24 @@ class Decoder:
         self._decode_buffers()
         self.g_logits = torch.zeros((B, cfg.vocab), dtype=torch.float16, device=dev)
         n_rep = cfg.n_heads // cfg.n_kv_heads
+        caches = self.caches if self.kv == "ott" else []
         # splits sized for the longest context of the run; workspaces allocated before capture
-        self.g_splits = [c.splits(n_rep) for c in self.caches]
+        self.g_splits = [c.splits(n_rep) for c in caches]
         saved = []
-        for c, s in zip(self.caches, self.g_splits):
+        for c, s in zip(caches, self.g_splits):
             c.workspace(n_rep, s)
             c.sync_counters()
             saved.append((c.total_tokens, c.quantized_tokens))
+        if self.kv == "flash":
+            saved_len = self.seqlens.clone()
         torch.cuda.synchronize(dev)
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph):
             self._graph_body()
-        for c, (t, q) in zip(self.caches, saved):  # capture ran the host side once, not the kernels
+        for c, (t, q) in zip(caches, saved):  # capture ran the host side once, not the kernels
             c.total_tokens, c.quantized_tokens = t, q
+        if self.kv == "flash":
+            self.seqlens.copy_(saved_len)
 
     @torch.no_grad()
     def decode_graph(self, tokens: torch.Tensor) -> torch.Tensor:
@@ -334,7 +362,7 @@ class Decoder:
             self.capture_decode_graph()
         if self.pos + 1 > self.max_tokens:
             raise ContractViolation("decoder is full")
-        for c in self.caches:
+        for c in (self.caches if self.kv == "ott" else []):
             c.advance_host_counts()  # checks capacity before the replay writes
         self.g_tok.copy_(tokens)
         self.graph.replay()

@@ -34,3 +34,23 @@ def test_lossless_cache_matches_exact_attention():
 def test_outlier_tracking_beats_n0_in_the_decoder():
     ott, n0 = _run(_cfg(32, 32)), _run(_cfg(32, 0))
     assert ott < 0.95 * n0, (ott, n0)  # measured 36.6 vs 43.0
+
+
+def test_flash_fp16_baseline_matches_sdpa_decoder():
+    """The independent fp16 baseline (plain KV cache + flash_attn_with_kvcache, graph-captured)
+    decodes like the SDPA fp16 decoder: same greedy tokens, logits within fp16 noise."""
+    import torch
+
+    from paper_2505_10938_b200.model import Decoder, DecoderConfig
+
+    pytest.importorskip("flash_attn")
+    cfg = DecoderConfig(n_layers=2, hidden=512, n_heads=4, n_kv_heads=2, head_dim=128, mlp=1024, vocab=1000)
+    prompt = torch.randint(0, cfg.vocab, (2, 200), generator=torch.Generator().manual_seed(5)).cuda()
+    a = Decoder(cfg, 2, 240, kv="fp16", seed=3)
+    b = Decoder(cfg, 2, 240, kv="flash", seed=3)
+    ta, tb = a.prefill(prompt), b.prefill(prompt)
+    assert torch.equal(ta, tb)
+    for _ in range(8):
+        ta, tb = a.decode(ta), b.decode_graph(tb)
+        torch.testing.assert_close(a.last_logits.float(), b.last_logits.float(), atol=2e-2, rtol=0)
+        assert torch.equal(ta, tb)
