@@ -24,29 +24,30 @@ ap.add_argument("--pool", type=int, default=32)
 ap.add_argument("--bits", type=int, default=2)
 ap.add_argument("--group", type=int, default=32)
 ap.add_argument("--splits", type=int, default=0)
+ap.add_argument("--dim", type=int, default=128)
 ap.add_argument("--append", action="store_true", help="time append_attend (fused ring write) steps")
 ap.add_argument("--graph", action="store_true", help="capture the iters attend launches in one CUDA graph (no host gaps)")
 args = ap.parse_args()
 
 torch.cuda.set_device(0)
 cfg = EngineConfig(bits=args.bits, group_size=args.group, residual=128, outlier_num=args.pool, aux_capacity=32, skip_layers=(),
-                   head_dim=128)
+                   head_dim=args.dim)
 cache = OTTCache(cfg, args.batch, args.kv, args.ctx + 64 + args.iters)
 gen = torch.Generator(device="cuda").manual_seed(0)
-k = torch.empty((args.batch, args.kv, args.ctx, 128), dtype=torch.float16, device="cuda")
+k = torch.empty((args.batch, args.kv, args.ctx, args.dim), dtype=torch.float16, device="cuda")
 v = torch.empty_like(k)
 fill_prefill(gen, k, v)
 cache.update(k, v)
 del k, v
-q = torch.randn((args.batch, args.kv * args.rep, 128), generator=gen, device="cuda").half()
+q = torch.randn((args.batch, args.kv * args.rep, args.dim), generator=gen, device="cuda").half()
 out = torch.empty_like(q)
 splits = args.splits or cache.splits(args.rep)
 for _ in range(3):
     cache.attend(q, out=out, n_splits=splits)
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-kn = torch.randn((args.batch, args.kv, 128), generator=gen, device="cuda").half()
-vn = torch.randn((args.batch, args.kv, 128), generator=gen, device="cuda").half()
+kn = torch.randn((args.batch, args.kv, args.dim), generator=gen, device="cuda").half()
+vn = torch.randn((args.batch, args.kv, args.dim), generator=gen, device="cuda").half()
 if args.graph:  # same launches, replayed from one graph so small shapes are not host bound
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g):
