@@ -909,29 +909,22 @@ __device__ __forceinline__ double h_val(uint16_t b) { return (double)__half2floa
 //     margin = 1e-12 (|x_min| + levels step) (all float64 roundings involved are < 2^-50 of it).
 // So t = the fp16 ceiling v of T, except when v - T <= margin: then the float64 quotient at v
 // decides between v and the next fp16 value (false is returned, and quant_code is used per
-// element, if fp16 values there are closer than 4 margin). t[levels-1] = x_max: T_levels lies
+// element, when 4 margin reaches the smallest fp16 spacing 2^-24). t[levels-1] = x_max: T_levels lies
 // within float64 rounding below x_max (line_params) and x_max has code levels (quant.py:101).
-// The rare case of code_thresholds: the fp16 ceiling v of T lies within the margin of T, so the
-// float64 quotient at v decides. Out of line, so the division is not if-converted into every call.
-__device__ __noinline__ bool quotient_ge(double dv, double mn, double step, int k) {
-  return floor(__ddiv_rn(__dsub_rn(dv, mn), step)) >= (double)k;
-}
-// For k = 1, 2 without the division: fl(d / step) >= k iff d / step >= k (1 - 2^-54), the
-// rounding boundary below k (a tie rounds to the even k). d = dv - mn is exact, and here it lies
-// within (1 +- 1e-8) k step (dv - T <= margin, |mn| <= 6144 step for fp16 lines), so d - k step
-// is exact (Sterbenz) and k step is exact: the comparison is exact.
-__device__ __forceinline__ uint16_t threshold_tie(uint16_t vb, double dv, double mn, double step, int k, double margin,
-                                                  bool& ok) {
-  const uint16_t nb = h_next(vb);
-  if (h_val(nb) - dv <= 4.0 * margin) ok = false;
-  bool ge;
-  if (k <= 2) {
-    const double ks = __dmul_rn((double)k, step);
-    ge = __dsub_rn(__dsub_rn(dv, mn), ks) >= -ks * 0x1p-54;
-  } else {
-    ge = quotient_ge(dv, mn, step, k);
-  }
-  return ge ? vb : nb;
+// The tie case of code_thresholds: the fp16 ceiling v of T lies within the margin of T, so the
+// float64 quotient at v decides: fl(d / step) >= k, d = v - x_min (exact: both are fp16 values).
+// fl(q) >= k iff q >= k - delta_k, the midpoint below k (ties round to k, whose significand is
+// even): delta_k = 2^(e - 53) for 2^e < k < 2^(e+1), 2^(e - 54) for k = 2^e. That is decided
+// without the division as fma(-k, step, d) >= -delta_k step: d and k step are multiples of
+// ulp(step) / 2 and d lies within (1 +- 1e-7) k step here, so d - k step is representable and the
+// fma exact; delta_k step is a power-of-two scaling, exact. Common for fp16 lines (x_min + k step
+// is an fp16 value whenever the range is a multiple of levels / gcd(k, levels) fp16 units).
+__host__ __device__ constexpr double tie_delta(int k) {
+  int e = 0;
+  while ((2 << e) <= k) ++e;
+  double d = 1.0;
+  for (int i = 0; i < 53 + ((k & (k - 1)) == 0 ? 1 : 0) - e; ++i) d *= 0.5;
+  return d;
 }
 __device__ __forceinline__ bool code_thresholds(uint16_t* t, float mnf, float mxf, double mn, double step, double inv,
                                                 int levels, double eps) {
@@ -939,19 +932,25 @@ __device__ __forceinline__ bool code_thresholds(uint16_t* t, float mnf, float mx
   (void)eps;
   const uint16_t mxb = __half_as_ushort(__float2half_rn(mxf));  // x_max is an fp16 value
   if (step == 0.0) {  // quant.py:91-92: every code 0 (no max rule)
+#pragma unroll
     for (int k = 0; k < levels; ++k) t[k] = 0x7C00u;  // +inf
     return true;
   }
   const double margin = 1e-12 * (fabs(mn) + (double)levels * step);
-  bool ok = true;
+  // fp16 values lie >= 2^-24 apart, so below this bound the value after a tie candidate is never
+  // within 4 margin of it (lines with |x_min| + range beyond ~1.5e4 take the per-element path)
+  const bool ok = 4.0 * margin < 0x1p-24;
+#pragma unroll
   for (int k = 1; k < levels; ++k) {
     const double T = __dadd_rn(mn, __dmul_rn((double)k, step));
     uint16_t vb = __half_as_ushort(__float2half_ru(__double2float_ru(T)));  // smallest fp16 >= T (or +inf)
-    if ((vb & 0x7C00u) != 0x7C00u) {
-      const double dv = h_val(vb);
-      if (dv - T <= margin) vb = threshold_tie(vb, dv, mn, step, k, margin, ok);
-    }
-    if ((vb & 0x7C00u) == 0x7C00u || h_val(vb) > (double)mxf) vb = mxb;
+    const double dv = h_val(vb);
+    // a tie candidate (dv - T <= margin; never for +inf): the float64 quotient at v decides,
+    // branch-free (ties are common in fp16 lines, so a branch would diverge in most warps)
+    const bool tie = __dsub_rn(dv, T) <= margin;
+    const bool ge = __fma_rn(-(double)k, step, __dsub_rn(dv, mn)) >= -step * tie_delta(k);
+    if (tie && !ge) vb = h_next(vb);
+    if ((vb & 0x7C00u) == 0x7C00u || __half2float(__ushort_as_half(vb)) > mxf) vb = mxb;
     t[k - 1] = vb;
   }
   t[levels - 1] = mxb;
@@ -975,6 +974,39 @@ __device__ __forceinline__ uint32_t put_codes(uint32_t acc, const CodeMasks& m) 
   constexpr uint32_t c0 = (1u << LO) | (1u << (16 + HI)), c1 = c0 << 1;
   return acc | (m.b0 & c0) | (m.b1 & c1);
 }
+// 4-bit (levels 15) / 3-bit (levels 7) codes of two fp16 inputs by binary search over the
+// line's thresholds th[k - 1] = t_k (half2 words, monotone): each level is one mask compare
+// against a threshold selected by the higher code bits (bitwise selects on the 0xFFFF masks).
+// Returns the code bits as masks: b[0] = lowest.
+__device__ __forceinline__ uint32_t sel_mask(uint32_t m, uint32_t a, uint32_t b) { return (m & a) | (~m & b); }
+__device__ __forceinline__ uint32_t ge_mask(__half2 x, uint32_t t) {
+  return __hge2_mask(x, *reinterpret_cast<const __half2*>(&t));
+}
+template <int kLevels>
+__device__ __forceinline__ void nib_masks(__half2 x, const uint32_t* th, uint32_t (&b)[4]) {
+  if constexpr (kLevels == 15) {
+    b[3] = ge_mask(x, th[7]);
+    b[2] = ge_mask(x, sel_mask(b[3], th[11], th[3]));
+    b[1] = ge_mask(x, sel_mask(b[3], sel_mask(b[2], th[13], th[9]), sel_mask(b[2], th[5], th[1])));
+    const uint32_t d0 = sel_mask(b[2], sel_mask(b[1], th[14], th[12]), sel_mask(b[1], th[10], th[8]));
+    const uint32_t d1 = sel_mask(b[2], sel_mask(b[1], th[6], th[4]), sel_mask(b[1], th[2], th[0]));
+    b[0] = ge_mask(x, sel_mask(b[3], d0, d1));
+  } else {  // kLevels == 7
+    b[3] = 0u;
+    b[2] = ge_mask(x, th[3]);
+    b[1] = ge_mask(x, sel_mask(b[2], th[5], th[1]));
+    b[0] = ge_mask(x, sel_mask(b[2], sel_mask(b[1], th[6], th[4]), sel_mask(b[1], th[2], th[0])));
+  }
+}
+// OR the 4-bit codes of m into acc: low-half input at bits LO..LO+3, high-half input at
+// bits 16 + HI..16 + HI + 3 (fold with acc >> 16 afterwards)
+template <int LO, int HI>
+__device__ __forceinline__ uint32_t put_nibs(uint32_t acc, const uint32_t (&b)[4]) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) acc |= b[k] & ((1u << (LO + k)) | (1u << (16 + HI + k)));
+  return acc;
+}
+
 // codes of two fp16 inputs against per-lane thresholds th[0..2]: code at bits 0-1 (low half)
 // and 16-17 (high half). Each compare gives 1.0 or 0.0; 1024 + code is exact in fp16.
 // the same as fp16 bits 1024 + code (bytes: code, 0x64, code', 0x64), unmasked
@@ -1550,6 +1582,36 @@ __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen4_kernel(ott_ca
     uint8_t* kcodes2 = rec + L.k_codes() + lane;
     uint16_t* kcodes4 = reinterpret_cast<uint16_t*>(rec + L.k_codes()) + lane;
     uint32_t* kcodes8 = reinterpret_cast<uint32_t*>(rec + L.k_codes()) + lane;
+    bool done = false;
+    if constexpr (kBits == 4 && (kLevels == 15 || kLevels == 7)) {
+      if (!sel) {  // fp16 inputs: exact fp16 thresholds per line (code_thresholds), binary search
+        uint16_t thr[4][kLevels];
+        bool exact = true;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          exact &= code_thresholds(thr[j], fmn[j], fmx[j], (double)fmn[j], step[j], inv[j], kLevels, eps);
+        if (exact) {
+          uint32_t t01[kLevels], t23[kLevels];
+#pragma unroll
+          for (int k = 0; k < kLevels; ++k) {
+            t01[k] = (uint32_t)thr[0][k] | ((uint32_t)thr[1][k] << 16);
+            t23[k] = (uint32_t)thr[2][k] | ((uint32_t)thr[3][k] << 16);
+          }
+#pragma unroll 2
+          for (int t = 0; t < G; ++t) {
+            const uint2 r = kr[t * (D / 4)];
+            uint32_t b[4];
+            nib_masks<kLevels>(*reinterpret_cast<const __half2*>(&r.x), t01, b);
+            uint32_t acc = put_nibs<0, 4>(0u, b);  // channels 4 lane, 4 lane + 1: nibbles 0, 1
+            nib_masks<kLevels>(*reinterpret_cast<const __half2*>(&r.y), t23, b);
+            acc = put_nibs<8, 12>(acc, b);         // channels 4 lane + 2, + 3: nibbles 2, 3
+            kcodes4[t * (D / 4)] = (uint16_t)(acc | (acc >> 16));
+          }
+          done = true;
+        }
+      }
+    }
+    if (!done)
 #pragma unroll 4
     for (int t = 0; t < G; ++t) {
       float x[4];
@@ -1633,6 +1695,34 @@ __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen4_kernel(ott_ca
 #pragma unroll
       for (int q = 0; q < kWords; ++q) w[q] = 0u;
     }
+    bool vdone = false;
+    if constexpr (kBits == 4 && (kLevels == 15 || kLevels == 7)) {
+      if (!subst) {  // fp16 inputs: exact thresholds, binary search (see the K part)
+        uint16_t thr[kLevels];
+        if (code_thresholds(thr, fmn, fmx, mn, step, inv, kLevels, eps)) {
+          uint32_t th[kLevels];
+#pragma unroll
+          for (int k = 0; k < kLevels; ++k) th[k] = (uint32_t)thr[k] * 0x00010001u;
+#pragma unroll 2
+          for (int j = 0; j < D / 8; ++j) {  // chunk j = channels 8j..8j+7 = nibbles of word j
+            const uint4 r = vr[j ^ sw];
+            const __half2* h = reinterpret_cast<const __half2*>(&r);
+            uint32_t b[4];
+            nib_masks<kLevels>(h[0], th, b);
+            uint32_t lo = put_nibs<0, 4>(0u, b);
+            nib_masks<kLevels>(h[1], th, b);
+            lo = put_nibs<8, 12>(lo, b);
+            nib_masks<kLevels>(h[2], th, b);
+            uint32_t hi = put_nibs<0, 4>(0u, b);
+            nib_masks<kLevels>(h[3], th, b);
+            hi = put_nibs<8, 12>(hi, b);
+            w[j] = ((lo | (lo >> 16)) & 0xFFFFu) | ((hi | (hi >> 16)) << 16);
+          }
+          vdone = true;
+        }
+      }
+    }
+    if (!vdone)
 #pragma unroll
     for (int j = 0; j < D / 8; ++j) {  // chunk j = channels 8j..8j+7 = word j (nibbles) / 2j, 2j+1 (bytes)
       float x[8];

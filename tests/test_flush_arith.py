@@ -3,8 +3,9 @@ rational arithmetic on the CPU:
 
 * line_params, 2-bit: RN(range / 3) as Markstein's FMA correction of RN(range * RN(1/3))
   (quant.py:64 divides in float64);
-* threshold_tie, k = 1, 2: floor(fl((v - x_min) / step)) >= k decided without the division as
-  (v - x_min) - k step >= -k step 2^-54, exact when v - x_min lies within a factor 2 of k step.
+* threshold_tie: floor(fl((v - x_min) / step)) >= k decided without the division as
+  fma(-k, step, v - x_min) >= -delta_k step, delta_k the distance from k to the rounding
+  midpoint below it (2^(e-53), or 2^(e-54) for k = 2^e), exact when v - x_min is close to k step.
 
 The GPU parity suite checks the kernels bit-exactly against the oracle. These tests pin the
 arithmetic claims themselves, including significands near 1, 4/3 and 2."""
@@ -42,20 +43,24 @@ def test_markstein_division_by_three_is_correctly_rounded():
         assert div3(x) == x / 3.0, x.hex()
 
 
+def tie_delta(k):  # ott_flush.cu tie_delta
+    e = k.bit_length() - 1
+    return 2.0 ** (e - 53 - (1 if k & (k - 1) == 0 else 0))
+
+
 def test_threshold_tie_without_division():
     rng = np.random.default_rng(6)
-    seen = set()
-    for _ in range(20000):
+    seen = {}
+    for it in range(40000):
         step = float(rng.random() * 2.0 ** int(rng.integers(-24, 12)))
         if step == 0.0:
             continue
-        k = int(rng.integers(1, 3))
-        ks = k * step  # exact for k = 1, 2
-        d = ks
+        k = int(rng.integers(1, 3)) if it % 2 else int(rng.integers(1, 255))  # levels up to 255 (8-bit)
+        d = k * step  # RN(k step)
         j = int(rng.integers(-5, 6))
         for _ in range(abs(j)):
             d = float(np.nextafter(d, math.inf if j > 0 else -math.inf))
         ref = math.floor(d / step) >= k
-        assert ((d - ks) >= -ks * 2.0 ** -54) == ref, (step, k, j)
-        seen.add(ref)
-    assert seen == {True, False}
+        assert (fma(-k, step, d) >= -step * tie_delta(k)) == ref, (step, k, j)
+        seen[ref] = seen.get(ref, 0) + 1
+    assert min(seen.get(True, 0), seen.get(False, 0)) > 1000

@@ -467,21 +467,23 @@ def test_flush_adversarial_lines_vs_oracle(bits, N):
     assert ok, err
 
 
-@pytest.mark.parametrize("seed", [1, 2, 3])
-def test_flush_threshold_ties_random(seed):
+@pytest.mark.parametrize("seed,bits", [(1, 2), (2, 2), (3, 2), (4, 3), (5, 4), (6, 4)])
+def test_flush_threshold_ties_random(seed, bits):
     """K and V lines whose fp16 thresholds x_min + k step land exactly on fp16 values (range
-    divisible by 3 in fp16 units, at many magnitudes): the division-free tie rule of
-    code_thresholds (k = 1, 2) and the Markstein line step, bit-exact vs the oracle over 16
-    units and both pool settings (N = 0: every group through the threshold path)."""
+    divisible by the level count in fp16 units, at many magnitudes): the division-free tie rule
+    of code_thresholds (k = 1, 2), its quotient rule (k >= 3), the Markstein line step (2-bit)
+    and the 3/4-bit binary-search code path, bit-exact vs the oracle over 16 units and both
+    pool settings (N = 0: every group through the threshold path)."""
     from paper_2505_10938_b200 import OTTCache
 
     d, G, U, T = 128, 32, 16, 32 * 10 + 7
+    levels = (1 << bits) - 1
     rng = np.random.default_rng(100 + seed)
     # K line (unit, channel, group): values (b + L) ulp with L in [0, 3 m], both ends present in
     # every group, so x_min + k step = (b + k m) ulp is an fp16 value (|b + L| < 2048: exact)
     ulp = 2.0 ** rng.integers(-20, 2, size=(U, 1, 1, d))
     b = rng.integers(-1000, 1000, size=(U, 1, 1, d))
-    span = 3 * rng.integers(1, 20, size=(U, 1, 1, d))
+    span = levels * rng.integers(1, 20, size=(U, 1, 1, d))
     lattice = rng.integers(0, span + 1, size=(U, 1, T, d))
     lattice[:, :, 0::G] = 0
     lattice[:, :, 1::G] = np.broadcast_to(span, lattice[:, :, 1::G].shape)
@@ -490,16 +492,16 @@ def test_flush_threshold_ties_random(seed):
     # V line (unit, token): the same construction along the channels
     vulp = 2.0 ** rng.integers(-20, 2, size=(U, 1, T, 1))
     vb = rng.integers(-1000, 1000, size=(U, 1, T, 1))
-    vspan = 3 * rng.integers(1, 20, size=(U, 1, T, 1))
+    vspan = levels * rng.integers(1, 20, size=(U, 1, T, 1))
     vlat = rng.integers(0, vspan + 1, size=(U, 1, T, d))
     vlat[..., 0] = 0
     vlat[..., 1] = vspan[..., 0]
     v = ((vb + vlat) * vulp).astype(np.float16)
     for N in (0, 32):
-        cache = OTTCache(cfg_of(2, G, 64, N, 8, d), U, 1, max_tokens=T, keep_f64_params=True)
+        cache = OTTCache(cfg_of(bits, G, 64, N, 8, d), U, 1, max_tokens=T, keep_f64_params=True)
         cache.update(torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda())
         for u in (0, 5, U - 1):
-            ref = oracle.OracleCache(2, G, 64, N, 8, d)
+            ref = oracle.OracleCache(bits, G, 64, N, 8, d)
             ref.extend(k[u, 0].astype(np.float32), v[u, 0].astype(np.float32))
             assert_unit_matches_oracle(cache.unit(u, 0), ref)
 
