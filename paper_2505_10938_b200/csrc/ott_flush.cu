@@ -1481,6 +1481,15 @@ __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen4_kernel(ott_ca
   {
     const int bslot = base % cap, ring_end32 = (int)ring_end, in_first32 = (int)in_first;
     const int ch = lane & 15;
+    if (base >= ring_end32) {  // bulk prefill: every row of the group comes from the input
+      const size_t off = (size_t)u * in_stride + (size_t)(base - in_first32 + (lane >> 4)) * D + ch * 8;
+      const uint16_t* src = (part == 0 ? in_k : in_v) + off;
+#pragma unroll
+      for (int it = 0; it < G / 2; ++it) {
+        const int row = 2 * it + (lane >> 4);
+        cp_async16(sk + row * D + (part == 0 ? ch : ch ^ (row & 15)) * 8, src + (size_t)it * 2 * D);
+      }
+    } else
 #pragma unroll 4
     for (int it = 0; it < G / 2; ++it) {
       const int row = 2 * it + (lane >> 4);
@@ -1536,13 +1545,30 @@ __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen4_kernel(ott_ca
       }
     };
     float fmn[4] = {3.4e38f, 3.4e38f, 3.4e38f, 3.4e38f}, fmx[4] = {-3.4e38f, -3.4e38f, -3.4e38f, -3.4e38f};
-    for (int t = 0; t < G; ++t) {
-      float x[4];
-      kval(t, x);
+    if (!sel) {  // fp16 rows only: packed min/max (as flush_frozen_kernel)
+      __half2 mn01 = __float2half2_rn(65504.f), mn23 = mn01, mx01 = __float2half2_rn(-65504.f), mx23 = mx01;
+#pragma unroll 8
+      for (int t = 0; t < G; ++t) {
+        const uint2 r = kr[t * (D / 4)];
+        const __half2 a = *reinterpret_cast<const __half2*>(&r.x), b = *reinterpret_cast<const __half2*>(&r.y);
+        mn01 = __hmin2(mn01, a);
+        mx01 = __hmax2(mx01, a);
+        mn23 = __hmin2(mn23, b);
+        mx23 = __hmax2(mx23, b);
+      }
+      const float2 a = __half22float2(mn01), b = __half22float2(mn23), x = __half22float2(mx01),
+                   y = __half22float2(mx23);
+      fmn[0] = a.x; fmn[1] = a.y; fmn[2] = b.x; fmn[3] = b.y;
+      fmx[0] = x.x; fmx[1] = x.y; fmx[2] = y.x; fmx[3] = y.y;
+    } else {
+      for (int t = 0; t < G; ++t) {
+        float x[4];
+        kval(t, x);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        fmn[j] = fminf(fmn[j], x[j]);
-        fmx[j] = fmaxf(fmx[j], x[j]);
+        for (int j = 0; j < 4; ++j) {
+          fmn[j] = fminf(fmn[j], x[j]);
+          fmx[j] = fmaxf(fmx[j], x[j]);
+        }
       }
     }
     double step[4], inv[4];
@@ -1668,13 +1694,26 @@ __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen4_kernel(ott_ca
       }
     };
     float fmn = 3.4e38f, fmx = -3.4e38f;
-    for (int j = 0; j < D / 8; ++j) {
-      float x[8];
-      vval(j, x);
+    if (!subst) {  // fp16 row: packed min/max
+      __half2 mn2 = __float2half2_rn(65504.f), mx2 = __float2half2_rn(-65504.f);
+#pragma unroll 4
+      for (int j = 0; j < D / 8; ++j) {
+        const uint4 r = vr[j ^ sw];
+        const __half2* h = reinterpret_cast<const __half2*>(&r);
+        mn2 = __hmin2(__hmin2(mn2, h[0]), __hmin2(h[1], __hmin2(h[2], h[3])));
+        mx2 = __hmax2(__hmax2(mx2, h[0]), __hmax2(h[1], __hmax2(h[2], h[3])));
+      }
+      fmn = fminf(__low2float(mn2), __high2float(mn2));
+      fmx = fmaxf(__low2float(mx2), __high2float(mx2));
+    } else {
+      for (int j = 0; j < D / 8; ++j) {
+        float x[8];
+        vval(j, x);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        fmn = fminf(fmn, x[e]);
-        fmx = fmaxf(fmx, x[e]);
+        for (int e = 0; e < 8; ++e) {
+          fmn = fminf(fmn, x[e]);
+          fmx = fmaxf(fmx, x[e]);
+        }
       }
     }
     const double mn = (double)fmn;
