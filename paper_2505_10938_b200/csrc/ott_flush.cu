@@ -673,6 +673,8 @@ struct ScanSmem {
   double it_score[kScanWarps][kMaxN + 32];
   int it_rank[kScanWarps][kMaxN + 32];
   int free_slot[kScanWarps][kMaxN];
+  int ev_slot[kScanWarps][kMaxN];  // aux index - n_aux -> evicted slot
+  int win_cand[kScanWarps][32];    // winner number -> candidate index
 };
 
 __global__ void __launch_bounds__(32 * kScanWarps) flush_scan_kernel(ott_cache_t c, int64_t q0, int n_groups,
@@ -707,6 +709,8 @@ __global__ void __launch_bounds__(32 * kScanWarps) flush_scan_kernel(ott_cache_t
   double* it_score = sm.it_score[warp];
   int* it_rank = sm.it_rank[warp];
   int* free_slot = sm.free_slot[warp];
+  int* ev_slot = sm.ev_slot[warp];
+  int* win_cand = sm.win_cand[warp];
   for (int s = lane; s < N; s += 32) {
     spos[s] = ppos[s];
     sscore[s] = pscore[s];
@@ -831,43 +835,59 @@ __global__ void __launch_bounds__(32 * kScanWarps) flush_scan_kernel(ott_cache_t
         if (eidx < room) {
           apos[n_aux + eidx] = it_pos[s];
           ascore[n_aux + eidx] = it_score[s];
+          ev_slot[eidx] = s;
         }
         const int p = it_pos[s];
         atomicAnd(&pmask[p >> 5], ~(1u << (p & 31)));  // back to its shadow row
       }
     }
     __syncwarp();
-    // copy evicted rows into aux before their slots are reused (lanes 0-15 K, 16-31 V)
-    for (int s = 0; s < N; ++s) {
-      const int r = it_rank[s];
-      if (r < N) continue;
-      int eidx = 0;
-      for (int q = 0; q < N; ++q) eidx += (it_rank[q] >= N && it_rank[q] < r) ? 1 : 0;
-      if (eidx >= room) continue;
-      const int a = n_aux + eidx, j = lane & 15;
-      if (lane < 16) reinterpret_cast<uint4*>(ak + (size_t)a * D)[j] = reinterpret_cast<const uint4*>(pk + (size_t)s * D)[j];
-      else reinterpret_cast<uint4*>(av + (size_t)a * D)[j] = reinterpret_cast<const uint4*>(pv + (size_t)s * D)[j];
+    // Row copies: lane = (K or V, 16-byte chunk) of one row; the loads of up to 8 rows are issued
+    // before their stores, so a group's copies cost a few memory round trips, not one per row.
+    // Evicted rows go into aux first, before their slots are reused.
+    const int j16 = lane & 15;
+    const int n_copy = n_ev < room ? n_ev : room;
+    for (int r0 = 0; r0 < n_copy; r0 += 8) {
+      uint4 buf[8];
+#pragma unroll
+      for (int m = 0; m < 8; ++m)
+        if (r0 + m < n_copy) buf[m] = reinterpret_cast<const uint4*>((lane < 16 ? pk : pv) + (size_t)ev_slot[r0 + m] * D)[j16];
+#pragma unroll
+      for (int m = 0; m < 8; ++m)
+        if (r0 + m < n_copy)
+          reinterpret_cast<uint4*>((lane < 16 ? ak : av) + (size_t)(n_aux + r0 + m) * D)[j16] = buf[m];
     }
     __syncwarp();
     // winning candidates take the free slots in candidate order
     const bool win = it_rank[N + lane] < N;
     const uint32_t wins = __ballot_sync(0xffffffffu, win);
-    for (uint32_t wm = wins; wm; wm &= wm - 1) {
-      const int i = __ffs(wm) - 1;
-      const int widx = __popc(wins & ((1u << i) - 1u));
+    const int n_win = __popc(wins);
+    if (win) {
+      const int widx = __popc(wins & ((1u << lane) - 1u));
       const int s = free_slot[widx];
-      const int p = base + i, j = lane & 15;
-      if (lane < 16)
-        reinterpret_cast<uint4*>(pk + (size_t)s * D)[j] =
-            prescored ? reinterpret_cast<const uint4*>(row_of(p, c.pend_k, in_k))[j]
-                      : reinterpret_cast<const uint4*>(srow + i * D)[j ^ (i & 15)];
-      else reinterpret_cast<uint4*>(pv + (size_t)s * D)[j] = reinterpret_cast<const uint4*>(row_of(p, c.pend_v, in_v))[j];
-      if (lane == 0) {
-        spos[s] = p;
-        sscore[s] = it_score[N + i];
-        atomicOr(&pmask[p >> 5], 1u << (p & 31));
-        atomicOr(&smask[p >> 5], 1u << (p & 31));  // cache.py:173
-      }
+      win_cand[widx] = lane;
+      spos[s] = base + lane;
+      sscore[s] = it_score[N + lane];
+    }
+    if (lane == 0 && wins) {  // positions base..base+31 share one mask word (base is 32-aligned)
+      atomicOr(&pmask[base >> 5], wins);
+      atomicOr(&smask[base >> 5], wins);  // cache.py:173
+    }
+    __syncwarp();
+    for (int w0 = 0; w0 < n_win; w0 += 8) {
+      uint4 buf[8];
+#pragma unroll
+      for (int m = 0; m < 8; ++m)
+        if (w0 + m < n_win) {
+          const int i = win_cand[w0 + m], p = base + i;
+          buf[m] = lane >= 16   ? reinterpret_cast<const uint4*>(row_of(p, c.pend_v, in_v))[j16]
+                   : prescored ? reinterpret_cast<const uint4*>(row_of(p, c.pend_k, in_k))[j16]
+                               : reinterpret_cast<const uint4*>(srow + i * D)[j16 ^ (i & 15)];
+        }
+#pragma unroll
+      for (int m = 0; m < 8; ++m)
+        if (w0 + m < n_win)
+          reinterpret_cast<uint4*>((lane < 16 ? pk : pv) + (size_t)free_slot[w0 + m] * D)[j16] = buf[m];
     }
     __syncwarp();
     n_aux += n_ev < room ? n_ev : room;

@@ -1,0 +1,9 @@
+# prefill scan A/B (old = tools/variants/old_flush.so, the previous commit) + the GPU suite
+mkdir -p gpurun_out/r2
+timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -3
+for lib in tools/variants/old_flush.so paper_2505_10938_b200/_lib/libott_b200.so; do
+ for n in 32 3; do echo "$lib N=$n"; OTT_LIB_PATH=$lib timeout 300 python tools/prof_flush.py --batch 128 --kv 8 --ctx 16384 --pool $n --reps 3; done
+ echo "$lib config2"; OTT_LIB_PATH=$lib timeout 300 python tools/prof_flush.py --batch 16 --kv 8 --ctx 32768 --pool 3 --reps 3
+done
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:flush_ --csv --log-file gpurun_out/r2/scan_launches.csv \
+  python tools/prof_flush.py --batch 128 --kv 8 --ctx 16384 --pool 32 --reps 1 > /dev/null 2>&1
