@@ -815,23 +815,28 @@ __global__ void __launch_bounds__(32 * kScanWarps) flush_scan_kernel(ott_cache_t
       it_rank[t] = r;
     }
     __syncwarp();
-    // evicted old entries -> aux in old-entry order (ascending rank); free slots ascending
+    // evicted old entries -> aux in old-entry order (ascending rank); free slots ascending.
+    // Ranks are distinct and an evicted entry's rank lies in [N, N + 32): one bit each, so an
+    // entry's aux index is the number of evicted ranks below its own.
     const int room = A - n_aux;  // outlier.py:113-114
-    int n_ev = 0;
+    uint32_t ev_bits = 0u;
+    for (int s0 = 0; s0 < N; s0 += 32) {
+      const int s = s0 + lane;
+      const int r = s < N ? it_rank[s] : 0;
+      ev_bits |= __reduce_or_sync(0xffffffffu, (s < N && r >= N) ? 1u << (r - N) : 0u);
+    }
+    const int n_ev = __popc(ev_bits);
+    int n_free = 0;
     for (int s0 = 0; s0 < N; s0 += 32) {
       const int s = s0 + lane;
       const int r = s < N ? it_rank[s] : 0;
       const bool evicted = s < N && r >= N;
       const bool is_free = s < N && (r < 0 || r >= N);
-      n_ev += __popc(__ballot_sync(0xffffffffu, evicted));
-      if (is_free) {
-        int fidx = 0;
-        for (int q = 0; q < s; ++q) fidx += (it_rank[q] < 0 || it_rank[q] >= N) ? 1 : 0;
-        free_slot[fidx] = s;
-      }
+      const uint32_t fb = __ballot_sync(0xffffffffu, is_free);
+      if (is_free) free_slot[n_free + __popc(fb & ((1u << lane) - 1u))] = s;
+      n_free += __popc(fb);
       if (evicted) {
-        int eidx = 0;
-        for (int q = 0; q < N; ++q) eidx += (it_rank[q] >= N && it_rank[q] < r) ? 1 : 0;
+        const int eidx = __popc(ev_bits & ((1u << (r - N)) - 1u));
         if (eidx < room) {
           apos[n_aux + eidx] = it_pos[s];
           ascore[n_aux + eidx] = it_score[s];
