@@ -618,6 +618,24 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
   const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gsrc) : "memory");
 }
+// The 32 rows of one tensor of a bulk-prefill group (g = its first row, d = 128) into smem rows
+// (row r at r * 128 halves): lane = 16-byte chunk (lane & 15) of rows 2 it + (lane >> 4), V rows
+// XOR-swizzled (chunk ^ (row & 15), and (2 it + hi) & 15 = (2 it & 15) ^ hi). The shared address
+// is converted once and the global one advances by immediate offsets: two integer ops per copy
+// instead of a generic-to-shared conversion and 64-bit address math each.
+template <bool kSwizzle>
+__device__ __forceinline__ void stage_rows_bulk(uint16_t* srows, const uint16_t* g, int lane) {
+  constexpr int D = 128, G = 32;
+  const int hi = lane >> 4, ch = lane & 15;
+  const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(srows) + hi * D * 2;
+  const uint32_t c16 = (kSwizzle ? (ch ^ hi) : ch) * 16;
+  const char* gp = reinterpret_cast<const char*>(g + (size_t)hi * D + ch * 8);
+#pragma unroll
+  for (int it = 0; it < G / 2; ++it) {
+    const uint32_t sa = s0 + it * 2 * D * 2 + (kSwizzle ? (c16 ^ ((2 * it & 15) * 16)) : c16);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gp + it * 2 * D * 2) : "memory");
+  }
+}
 
 // K1a': score_tokens (outlier.py:45-49) for every token of a bulk flush in parallel, ahead of
 // flush_scan_kernel (used when the pool is expected to stay active for many groups, N < A):
@@ -1295,15 +1313,9 @@ __global__ void __launch_bounds__(32 * kFrozenWarps, 6) flush_frozen_kernel(ott_
     const int bslot = base % cap, ring_end32 = (int)ring_end, in_first32 = (int)in_first;
     const int ch = lane & 15;
     if (base >= ring_end32) {  // bulk prefill: every row of the group comes from the input
-      const size_t off = (size_t)u * in_stride + (size_t)(base - in_first32 + (lane >> 4)) * D + ch * 8;
-      const uint16_t* pk = in_k + off;
-      const uint16_t* pv = in_v + off;
-#pragma unroll 4
-      for (int it = 0; it < G / 2; ++it) {
-        const int row = 2 * it + (lane >> 4);
-        if (part != 1) cp_async16(sk + row * D + ch * 8, pk + (size_t)it * 2 * D);
-        if (part != 0) cp_async16(sv + row * D + ((ch ^ (row & 15)) * 8), pv + (size_t)it * 2 * D);
-      }
+      const size_t off0 = (size_t)u * in_stride + (size_t)(base - in_first32) * D;
+      if (part != 1) stage_rows_bulk<false>(sk, in_k + off0, lane);
+      if (part != 0) stage_rows_bulk<true>(sv, in_v + off0, lane);
     } else
 #pragma unroll 4
     for (int it = 0; it < G / 2; ++it) {
@@ -1507,13 +1519,9 @@ __global__ void __launch_bounds__(32 * kFrozenWarps) flush_frozen4_kernel(ott_ca
     const int bslot = base % cap, ring_end32 = (int)ring_end, in_first32 = (int)in_first;
     const int ch = lane & 15;
     if (base >= ring_end32) {  // bulk prefill: every row of the group comes from the input
-      const size_t off = (size_t)u * in_stride + (size_t)(base - in_first32 + (lane >> 4)) * D + ch * 8;
-      const uint16_t* src = (part == 0 ? in_k : in_v) + off;
-#pragma unroll
-      for (int it = 0; it < G / 2; ++it) {
-        const int row = 2 * it + (lane >> 4);
-        cp_async16(sk + row * D + (part == 0 ? ch : ch ^ (row & 15)) * 8, src + (size_t)it * 2 * D);
-      }
+      const size_t off0 = (size_t)u * in_stride + (size_t)(base - in_first32) * D;
+      if (part == 0) stage_rows_bulk<false>(sk, in_k + off0, lane);
+      else stage_rows_bulk<true>(sv, in_v + off0, lane);
     } else
 #pragma unroll 4
     for (int it = 0; it < G / 2; ++it) {
