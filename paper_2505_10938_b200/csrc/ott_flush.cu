@@ -661,7 +661,7 @@ __global__ void __launch_bounds__(128) flush_score_kernel(ott_cache_t c, int64_t
   }
   const uint4* kr = reinterpret_cast<const uint4*>(row);
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-#pragma unroll 4
+#pragma unroll  // all 16 loads of the row in flight
   for (int j = 0; j < D / 8; ++j) {
     const uint4 r = kr[j];
     const __half2* h = reinterpret_cast<const __half2*>(&r);
@@ -672,7 +672,14 @@ __global__ void __launch_bounds__(128) flush_score_kernel(ott_cache_t c, int64_t
     a2 = __dadd_rn(a2, __dadd_rn(fabs((double)f2.x), fabs((double)f2.y)));
     a3 = __dadd_rn(a3, __dadd_rn(fabs((double)f3.x), fabs((double)f3.y)));
   }
-  reinterpret_cast<double*>(record_ptr(c, u, base / G))[lane] = __dadd_rn(__dadd_rn(a0, a1), __dadd_rn(a2, a3));
+  const double sc = __dadd_rn(__dadd_rn(a0, a1), __dadd_rn(a2, a3));
+  double* rec = reinterpret_cast<double*>(record_ptr(c, u, base / G));
+  rec[lane] = sc;
+  // the group's smallest score after them: the scan skips 32 groups at a time by these
+  double m = sc;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmin(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane == 0) rec[32] = m;
 }
 
 // K1a: the sequential part of a bulk flush (cache.py:158-173 for every group in order):
@@ -759,9 +766,7 @@ __global__ void __launch_bounds__(32 * kScanWarps) flush_scan_kernel(ott_cache_t
     if (g < n_groups) {
       uint16_t* dst = sm.rows[warp][g % kScanStages];
       const int base = q0i + g * G, ch = lane & 15;
-      if (prescored) {
-        if (lane < 16) cp_async16(dst + 8 * lane, record_ptr(c, u, base / G) + 16 * lane);
-      } else {
+      if (!prescored) {  // pre-scored groups are read directly (the scan skips ahead over them)
 #pragma unroll 4
         for (int it = 0; it < G / 2; ++it) {
           const int row = 2 * it + (lane >> 4);
@@ -776,15 +781,34 @@ __global__ void __launch_bounds__(32 * kScanWarps) flush_scan_kernel(ott_cache_t
   __syncwarp();
   double wmax = max_entry_score();
   for (int g = 0; g < n_groups && !frozen; ++g) {
+    if (prescored && n_entries == N) {
+      // A full pool changes only for a group with a candidate below its largest entry
+      // (outlier.py:102-117): find the next such group from the group minima, 32 at a time.
+      for (;;) {
+        const int gg = g + lane;
+        const double gmin =
+            gg < n_groups ? reinterpret_cast<const double*>(record_ptr(c, u, (q0i + gg * G) / G))[32] : INFINITY;
+        const uint32_t need = __ballot_sync(0xffffffffu, gmin < wmax);
+        if (need) {
+          g += __ffs(need) - 1;
+          break;
+        }
+        g += 32;
+        if (g >= n_groups) break;
+      }
+      if (g >= n_groups) break;
+    }
     const int base = q0i + g * G;
-    load_group(g + kScanStages - 1);
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(kScanStages - 1) : "memory");
-    __syncwarp();
     const uint16_t* srow = sm.rows[warp][g % kScanStages];
+    if (!prescored) {
+      load_group(g + kScanStages - 1);
+      asm volatile("cp.async.wait_group %0;\n" ::"n"(kScanStages - 1) : "memory");
+      __syncwarp();
+    }
     // ---- score_tokens (outlier.py:45-49): L1 norm of key row `lane` in float64 (exact)
     double sc;
     if (prescored) {
-      sc = reinterpret_cast<const double*>(srow)[lane];
+      sc = reinterpret_cast<const double*>(record_ptr(c, u, base / G))[lane];
     } else {
       const uint4* kr = reinterpret_cast<const uint4*>(srow + lane * D);
       const int sw = lane & 15;
