@@ -652,29 +652,40 @@ __global__ void __launch_bounds__(128) flush_score_kernel(ott_cache_t c, int64_t
   split_item(item, (int64_t)c.n_units * n_groups, n_groups, u, g);
   if (c.pool_meta[(size_t)u * 4 + 2]) return;  // frozen: nothing will read the scores
   const int cap = G + c.residual;
-  const int base = (int)(q0 + (int64_t)g * G), p = base + lane;
-  const uint16_t* row;
-  if (p < (int)ring_end) {
-    row = c.pend_k + ((size_t)u * cap + (size_t)(p % cap)) * D;
-  } else {
-    row = in_k + (size_t)u * in_stride + (size_t)(p - (int)in_first) * D;
-  }
-  const uint4* kr = reinterpret_cast<const uint4*>(row);
-  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-#pragma unroll  // all 16 loads of the row in flight
-  for (int j = 0; j < D / 8; ++j) {
-    const uint4 r = kr[j];
+  const int base = (int)(q0 + (int64_t)g * G);
+  // Coalesced: load i brings rows 2i, 2i+1 (lane = 16-byte chunk ch of row 2i + hi), each lane
+  // keeps one float64 partial per row pair, and a butterfly over the 16 lanes of each half
+  // leaves lane (hi, ch) with the whole sum of row 2 ch + hi (exact in any order: fp16 magnitudes).
+  const int hi = lane >> 4, ch = lane & 15;
+  double part[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int p = base + 2 * i + hi;
+    const uint16_t* row = p < (int)ring_end ? c.pend_k + ((size_t)u * cap + (size_t)(p % cap)) * D
+                                            : in_k + (size_t)u * in_stride + (size_t)(p - (int)in_first) * D;
+    const uint4 r = reinterpret_cast<const uint4*>(row)[ch];
     const __half2* h = reinterpret_cast<const __half2*>(&r);
     const float2 f0 = __half22float2(h[0]), f1 = __half22float2(h[1]), f2 = __half22float2(h[2]),
                  f3 = __half22float2(h[3]);
-    a0 = __dadd_rn(a0, __dadd_rn(fabs((double)f0.x), fabs((double)f0.y)));
-    a1 = __dadd_rn(a1, __dadd_rn(fabs((double)f1.x), fabs((double)f1.y)));
-    a2 = __dadd_rn(a2, __dadd_rn(fabs((double)f2.x), fabs((double)f2.y)));
-    a3 = __dadd_rn(a3, __dadd_rn(fabs((double)f3.x), fabs((double)f3.y)));
+    part[i] = __dadd_rn(__dadd_rn(__dadd_rn(fabs((double)f0.x), fabs((double)f0.y)),
+                                  __dadd_rn(fabs((double)f1.x), fabs((double)f1.y))),
+                        __dadd_rn(__dadd_rn(fabs((double)f2.x), fabs((double)f2.y)),
+                                  __dadd_rn(fabs((double)f3.x), fabs((double)f3.y))));
   }
-  const double sc = __dadd_rn(__dadd_rn(a0, a1), __dadd_rn(a2, a3));
+#pragma unroll
+  for (int o = 8; o >= 1; o >>= 1) {  // after step o, part[k] (k < o) holds row pair k + (ch & ~(o - 1))
+    const bool upper = ch & o;
+#pragma unroll
+    for (int k = 0; k < o; ++k) {
+      const double send = upper ? part[k] : part[k + o];
+      const double keep = upper ? part[k + o] : part[k];
+      part[k] = __dadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, o));
+    }
+  }
+  const int t = 2 * ch + hi;  // this lane's token
+  const double sc = part[0];
   double* rec = reinterpret_cast<double*>(record_ptr(c, u, base / G));
-  rec[lane] = sc;
+  rec[t] = sc;
   // the group's smallest score after them: the scan skips 32 groups at a time by these
   double m = sc;
 #pragma unroll
