@@ -791,20 +791,25 @@ __global__ void __launch_bounds__(32 * kScanWarps) flush_scan_kernel(ott_cache_t
   for (int st = 0; st < kScanStages - 1; ++st) load_group(st);
   __syncwarp();
   double wmax = max_entry_score();
+  int wbase = -32;  // pre-scored skip window (see below)
+  double wmin = INFINITY;
   for (int g = 0; g < n_groups && !frozen; ++g) {
     if (prescored && n_entries == N) {
       // A full pool changes only for a group with a candidate below its largest entry
-      // (outlier.py:102-117): find the next such group from the group minima, 32 at a time.
+      // (outlier.py:102-117): find the next such group from the group minima, a window of 32
+      // at a time (lane j holds group wbase + j; the window is reloaded only when passed).
       for (;;) {
-        const int gg = g + lane;
-        const double gmin =
-            gg < n_groups ? reinterpret_cast<const double*>(record_ptr(c, u, (q0i + gg * G) / G))[32] : INFINITY;
-        const uint32_t need = __ballot_sync(0xffffffffu, gmin < wmax);
+        if (g >= wbase + 32) {
+          wbase = g;
+          const int gg = g + lane;
+          wmin = gg < n_groups ? reinterpret_cast<const double*>(record_ptr(c, u, (q0i + gg * G) / G))[32] : INFINITY;
+        }
+        const uint32_t need = __ballot_sync(0xffffffffu, wmin < wmax) & ~((1u << (g - wbase)) - 1u);
         if (need) {
-          g += __ffs(need) - 1;
+          g = wbase + __ffs(need) - 1;
           break;
         }
-        g += 32;
+        g = wbase + 32;
         if (g >= n_groups) break;
       }
       if (g >= n_groups) break;
