@@ -1070,3 +1070,56 @@ def test_large_groups_vs_oracle(bits, G, n_rep):
         for r in range(n_rep):
             ok, err = within_tol(out[0, u * n_rep + r], ref.attend(qh[0, u * n_rep + r].astype(np.float32)))
             assert ok, (u, r, err)
+
+
+@pytest.mark.parametrize("B,splits", [(96, None), (96, 3), (20, 4)])
+def test_sync_stress_many_ctas(B, splits):
+    """The kernels' cross-CTA synchronisation under load (compute-sanitizer is unavailable on
+    the GPU pool): the ring write fused into the attention kernel (fp-tier CTA + async-proxy
+    fence), the PDL-launched split combine, the tail schedule (B = 96: 768 units > one wave) and
+    the device-counter CUDA-graph step, over 80 decode steps and 2 flushes, against append +
+    attend with the same split count. A race between a producer and its reader would show up
+    as a bit difference in some step."""
+    from paper_2505_10938_b200 import OTTCache
+
+    H, n_rep, d, T, steps = 8, 8, 128, 1000, 80
+    rng = np.random.default_rng(B + (splits or 0))
+    pre_k, pre_v = (torch.from_numpy(rng.standard_normal((B, H, T, d)).astype(np.float16)).cuda() for _ in range(2))
+    cs = []
+    for _ in range(3):
+        c = OTTCache(cfg_of(2, 32, 128, 8, 16, d), B, H, max_tokens=T + steps + 8)
+        c.update(pre_k, pre_v)
+        cs.append(c)
+    ref, fused, dev = cs
+    graph = None
+    if splits is not None:  # device-counter step captured once, replayed per step
+        gk, gv = (torch.zeros((B, H, d), dtype=torch.float16, device="cuda") for _ in range(2))
+        gq = torch.zeros((B, H * n_rep, d), dtype=torch.float16, device="cuda")
+        out = torch.empty_like(gq)
+        dev.workspace(n_rep, splits)
+        dev.sync_counters()
+        saved = (dev.total_tokens, dev.quantized_tokens)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            dev.decode_step(gk, gv, gq, out, n_splits=splits)
+        dev.total_tokens, dev.quantized_tokens = saved  # the capture ran the host side only
+    for i in range(steps):
+        k, v = (torch.from_numpy(rng.standard_normal((B, H, d)).astype(np.float16)).cuda() for _ in range(2))
+        q = torch.from_numpy(rng.standard_normal((B, H * n_rep, d)).astype(np.float16)).cuda()
+        ref.append(k, v)
+        want = ref.attend(q, n_splits=splits)
+        got = fused.append_attend(k, v, q, n_splits=splits)
+        assert torch.equal(got, want), ("fused", i)
+        if graph is not None:
+            gk.copy_(k)
+            gv.copy_(v)
+            gq.copy_(q)
+            dev.advance_host_counts()
+            graph.replay()
+            assert torch.equal(out, want), ("graph", i)
+    assert ref.quantized_tokens > T - 128 + 32  # flushes happened in the window
+    assert torch.equal(fused.blocks, ref.blocks) and torch.equal(fused.pool_pos, ref.pool_pos)
+    if graph is not None:
+        assert dev.counters.tolist() == [ref.quantized_tokens, ref.total_tokens, 0]
+        assert torch.equal(dev.blocks, ref.blocks) and torch.equal(dev.pool_pos, ref.pool_pos)
