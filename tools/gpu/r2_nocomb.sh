@@ -1,4 +1,6 @@
 # how much does the split combine cost in the step? (variant: combine launch skipped, timing only)
+# variant: ott_attend.cu with `if (getenv("OTT_NOCOMBINE")) return cudaSuccess;` at the top of launch_combine<D>,
+# built by tools/build_variant.sh nocomb "" <that copy> into tools/variants/nocomb.so
 mkdir -p gpurun_out/r2
 for i in 1 2; do
  for nc in 0 1; do
