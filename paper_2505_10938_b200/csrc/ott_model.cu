@@ -11,19 +11,35 @@ namespace {
 __device__ __forceinline__ float h2f(uint16_t h) { return __half2float(__ushort_as_half(h)); }
 __device__ __forceinline__ uint16_t f2h(float f) { return __half_as_ushort(__float2half_rn(f)); }
 
-// y[r] = fp16(x[r] * rsqrt(mean(x[r]^2) + eps)) * w   (one CTA per row)
+// y[r] = fp16(x[r] * rsqrt(mean(x[r]^2) + eps)) * w   (one CTA per row). The row stays in
+// registers between the reduction and the scaling (up to kChunks 16-byte chunks per thread,
+// dim <= 8 * kChunks * blockDim), and the weights are loaded before the reduction, so the
+// kernel is one global round trip plus the block reduction (the decode step runs it with
+// only B rows, so its latency is what counts).
+constexpr int kNormChunks = 4;
 __global__ void rmsnorm_kernel(const uint16_t* __restrict__ x, const uint16_t* __restrict__ w,
                                uint16_t* __restrict__ y, int dim, float eps) {
   const uint16_t* xr = x + (size_t)blockIdx.x * dim;
   uint16_t* yr = y + (size_t)blockIdx.x * dim;
+  uint4 xv[kNormChunks], wv[kNormChunks];
   float ss = 0.f;
-  for (int i = threadIdx.x * 8; i < dim; i += blockDim.x * 8) {
-    const uint4 v = *reinterpret_cast<const uint4*>(xr + i);
-    const uint32_t u[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&u[k]));
-      ss = fmaf(f.x, f.x, fmaf(f.y, f.y, ss));
+  for (int c = 0; c < kNormChunks; ++c) {
+    const int i = (c * blockDim.x + threadIdx.x) * 8;
+    if (i < dim) {
+      xv[c] = *reinterpret_cast<const uint4*>(xr + i);
+      wv[c] = *reinterpret_cast<const uint4*>(w + i);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < kNormChunks; ++c) {
+    if ((c * blockDim.x + threadIdx.x) * 8 < dim) {
+      const uint32_t u[4] = {xv[c].x, xv[c].y, xv[c].z, xv[c].w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&u[k]));
+        ss = fmaf(f.x, f.x, fmaf(f.y, f.y, ss));
+      }
     }
   }
   __shared__ float red[32];
@@ -31,27 +47,25 @@ __global__ void rmsnorm_kernel(const uint16_t* __restrict__ x, const uint16_t* _
   for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
   __syncthreads();
-  if (threadIdx.x < 32) {
-    float t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+  float t = (threadIdx.x & 31) < (blockDim.x >> 5) ? red[threadIdx.x & 31] : 0.f;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-    if (threadIdx.x == 0) red[0] = t;
-  }
-  __syncthreads();
-  const float r = rsqrtf(red[0] / (float)dim + eps);
-  for (int i = threadIdx.x * 8; i < dim; i += blockDim.x * 8) {
-    const uint4 v = *reinterpret_cast<const uint4*>(xr + i);
-    const uint4 g = *reinterpret_cast<const uint4*>(w + i);
-    const uint32_t u[4] = {v.x, v.y, v.z, v.w}, gw[4] = {g.x, g.y, g.z, g.w};
-    uint32_t o[4];
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);  // every warp reduces the partials
+  const float r = rsqrtf(t / (float)dim + eps);
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&u[k]));
-      const __half2 n = __floats2half2_rn(f.x * r, f.y * r);
-      const __half2 m = __hmul2(n, *reinterpret_cast<const __half2*>(&gw[k]));
-      o[k] = *reinterpret_cast<const uint32_t*>(&m);
+  for (int c = 0; c < kNormChunks; ++c) {
+    const int i = (c * blockDim.x + threadIdx.x) * 8;
+    if (i < dim) {
+      const uint32_t u[4] = {xv[c].x, xv[c].y, xv[c].z, xv[c].w}, gw[4] = {wv[c].x, wv[c].y, wv[c].z, wv[c].w};
+      uint32_t o[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&u[k]));
+        const __half2 n = __floats2half2_rn(f.x * r, f.y * r);
+        const __half2 m = __hmul2(n, *reinterpret_cast<const __half2*>(&gw[k]));
+        o[k] = *reinterpret_cast<const uint32_t*>(&m);
+      }
+      *reinterpret_cast<uint4*>(yr + i) = make_uint4(o[0], o[1], o[2], o[3]);
     }
-    *reinterpret_cast<uint4*>(yr + i) = make_uint4(o[0], o[1], o[2], o[3]);
   }
 }
 
@@ -73,10 +87,10 @@ __global__ void rope_qkv_kernel(const uint16_t* __restrict__ qkv, const float* _
   uint16_t* dst = head < H ? q + ((size_t)b * H + head) * d : k + ((size_t)b * Hkv + (head - H)) * d;
   const float* c = cosT + (size_t)p * d;
   const float* s = sinT + (size_t)p * d;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) {
-    const float x = h2f(src[i]);
-    const float rot = i < half ? -h2f(src[i + half]) : h2f(src[i - half]);
-    dst[i] = f2h(x * c[i] + rot * s[i]);
+  for (int i = threadIdx.x; i < half; i += blockDim.x) {  // the pair (i, i + half) per thread
+    const float x0 = h2f(src[i]), x1 = h2f(src[i + half]);
+    dst[i] = f2h(x0 * c[i] - x1 * s[i]);
+    dst[i + half] = f2h(x1 * c[i + half] + x0 * s[i + half]);
   }
 }
 
@@ -100,8 +114,11 @@ extern "C" {
 
 int ott_model_rmsnorm(const uint16_t* x, const uint16_t* w, uint16_t* y, int32_t rows, int32_t dim, float eps,
                       void* stream) {
-  if (!x || !w || !y || rows < 1 || dim < 8 || dim % 8) return 1;
-  rmsnorm_kernel<<<rows, 256, 0, (cudaStream_t)stream>>>(x, w, y, dim, eps);
+  if (!x || !w || !y || rows < 1 || dim < 8 || dim % 8 || dim > 8 * kNormChunks * 1024) return 1;
+  // one 16-byte chunk per thread where possible (dim / 8 threads, whole warps, <= 1024)
+  int threads = (dim / 8 + 31) / 32 * 32;
+  while (threads > 1024) threads = (threads / 2 + 31) / 32 * 32;
+  rmsnorm_kernel<<<rows, threads, 0, (cudaStream_t)stream>>>(x, w, y, dim, eps);
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 
