@@ -695,10 +695,11 @@ __global__ void __launch_bounds__(128) flush_score_kernel(ott_cache_t c, int64_t
 
 // K1a: the sequential part of a bulk flush (cache.py:158-173 for every group in order):
 // score_tokens, OutlierPool.update, the pool/aux rows and the pool/substitution bitmasks.
-// One warp per unit; lane t scores token t of each group; the competition is the same
-// rank-by-count as flush_kernel (outlier.py:84-117). Substitution and quantization are left
-// to flush_frozen_kernel (all groups in parallel). Stops when the pool freezes. d = 128,
-// G = 32, N <= 128.
+// One warp per unit; lane t scores token t of each group (or reads the score that
+// flush_score_kernel left in the group's record, skipping 32 groups at a time by their
+// minima while the pool is full); the competition is the same rank-by-count as flush_kernel
+// (outlier.py:84-117). Substitution and quantization are left to flush_frozen_kernel (all
+// groups in parallel). Stops when the pool freezes. d = 128, G = 32, N <= 128.
 constexpr int kScanWarps = 1;  // one warp per block: a unit's scan is latency bound
 constexpr int kScanStages = 4;  // K-row groups in flight per warp (cp.async ring)
 struct ScanSmem {
@@ -771,13 +772,13 @@ __global__ void __launch_bounds__(32 * kScanWarps) flush_scan_kernel(ott_cache_t
     }
     return in + (size_t)u * in_stride + (size_t)(p - in_first32) * D;
   };
-  // K rows of group g -> stage g % kScanStages (one cp.async group per load); pre-scored:
-  // the group's 32 float64 scores (flush_score_kernel left them in its record)
+  // K rows of group g -> stage g % kScanStages (one cp.async group per load; nothing for
+  // pre-scored groups, whose scores are read from their records directly)
   auto load_group = [&](int g) {
     if (g < n_groups) {
       uint16_t* dst = sm.rows[warp][g % kScanStages];
       const int base = q0i + g * G, ch = lane & 15;
-      if (!prescored) {  // pre-scored groups are read directly (the scan skips ahead over them)
+      if (!prescored) {
 #pragma unroll 4
         for (int it = 0; it < G / 2; ++it) {
           const int row = 2 * it + (lane >> 4);
