@@ -1912,10 +1912,11 @@ cudaError_t launch_flush(const ott_cache_t& c, int64_t q0, int n_groups, int64_t
   const size_t smem = flush_smem_bytes(c.head_dim, c.group_size, c.capacity);
   cudaError_t e = cudaFuncSetAttribute(flush_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  // bulk flushes at the tensor-core shapes: the sequential kernel runs only the pool
-  // competition (scoring, OutlierPool.update, masks, pool/aux rows) group by group, then
-  // flush_frozen_kernel substitutes and quantizes all groups in parallel
-  const bool split = OTT_FLUSH_SPLIT && !dev_counts && n_groups > 1 && c.head_dim == 128 && c.group_size == 32;
+  // host-triggered flushes at the tensor-core shapes (bulk prefill and decode flushes): the
+  // sequential kernel runs only the pool competition (scoring, OutlierPool.update, masks,
+  // pool/aux rows) group by group -- nothing once a unit's pool has frozen -- then
+  // flush_frozen_kernel substitutes and quantizes all groups in parallel, a warp pair per group
+  const bool split = OTT_FLUSH_SPLIT && !dev_counts && c.head_dim == 128 && c.group_size == 32;
   if (!split) {
     flush_kernel<<<c.n_units, kFlushThreads, smem, st>>>(c, q0, n_groups, ring_end, in_k, in_v, in_stride, in_first,
                                                            dev_counts);
